@@ -1,0 +1,213 @@
+/*
+ * harvest_b200.h — C ABI of the B200-native Harvest peer-fetch data plane.
+ *
+ * The reference (arXiv 2602.00328, /root/reference/pkg/src/harvestsim) is a
+ * pure-Python discrete-event simulator: every "transfer" on the fetch path is
+ * `fixed_cost + size/bandwidth` arithmetic (interconnect.py:51-54) scheduled by
+ * TransferEngine.schedule_transfer (interconnect.py:133-165) on behalf of
+ * HarvestRuntime.app_transfer (runtime.py:320-364), and object content is a
+ * 64-bit hash (runtime.py:38-44, :305-315).  This library replaces those
+ * modeled pieces with real ones, one entry point per modeled function:
+ *
+ *   reference (file:line)                          replaced by
+ *   ---------------------------------------------  ---------------------------------
+ *   memalloc.alloc_best_fit / free_segment          hv_seg_* (native best-fit, same
+ *     (memalloc.py:90-138), allocated_bytes (:86)     decisions, O(log n) per call)
+ *   DeviceState / init_device (memalloc.py:67-79)   hv_seg_create
+ *   "switches to that device context, and          hv_pool_* (per-donor VMM pool:
+ *     allocates memory", the          cuMemCreate/cuMemMap/
+ *     peer tier of Topology (interconnect.py:57)     cuMemSetAccess, or cudaIpc)
+ *   HOST_DRAM tier (memalloc.py:14-17)              hv_host_alloc (pinned, mapped)
+ *   app_transfer -> schedule_transfer ->            hv_kv_gather (K1), hv_batch_copy
+ *     transfer_time (runtime.py:320-364,             (K2), hv_swap_blocks_batch
+ *     interconnect.py:133-165, :51-54)               (host-array form)
+ *   rebalance copy-in host->peer (moe.py:191-195)   hv_batch_copy / hv_ce_batch_copy
+ *   cudaMemcpyPeerAsync data path    hv_ce_batch_copy (baseline)
+ *   expert_content / stable_hash64 content model    hv_fill_content, hv_digest,
+ *     (moe.py:114-115, runtime.py:38-44)             hv_verify_content
+ *   drain of in-flight transfers before free        hv_event_* (stream-ordered
+ *     (runtime.py:345-356, :396-411)                 completion events)
+ *
+ * Conventions: C linkage, plain pointers and sizes, no C++ exceptions across
+ * the ABI, no internal threads.  Every function returns an int status: 0 on
+ * success, a negative HV_E* code otherwise (hv_error_string() describes it).
+ * Stream arguments are cudaStream_t passed as void* (NULL = legacy default
+ * stream of the current device).  "d_" pointers are device-visible addresses
+ * (device memory, peer-mapped VA or the device alias of mapped pinned host
+ * memory); "h_" pointers are host memory.  All copies are stream-ordered.
+ */
+#ifndef HARVEST_B200_H_
+#define HARVEST_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HV_ABI_VERSION 1
+
+/* ---- status codes ------------------------------------------------------ */
+#define HV_OK 0
+#define HV_E_INVALID (-1)      /* bad argument (ValueError in Python)            */
+#define HV_E_NOCAPACITY (-2)   /* nothing fits (the reference returns None)      */
+#define HV_E_DOUBLEFREE (-3)   /* memalloc.DoubleFreeError (memalloc.py:20-21)   */
+#define HV_E_UNSUPPORTED (-4)  /* feature missing on this device/driver          */
+#define HV_E_NOMEM (-5)        /* host allocation failed                         */
+#define HV_E_CUDA_BASE (-1000) /* -1000 - cudaError_t                            */
+#define HV_E_CU_BASE (-3000)   /* -3000 - CUresult (driver API)                  */
+
+int hv_abi_version(void);
+const char* hv_error_string(int status);
+
+/* ---- devices ----------------------------------------------------------- */
+int hv_device_count(int* n);
+int hv_sm_count(int device, int* n);
+/* can `reader` load from memory resident on `donor` (NVLink P2P)? */
+int hv_can_access_peer(int reader, int donor, int* ok);
+/* cudaDeviceEnablePeerAccess(donor) on `reader`; idempotent */
+int hv_enable_peer_access(int reader, int donor);
+int hv_device_synchronize(int device);
+
+/* ---- native best-fit segment allocator (memalloc.py:67-159) ------------- */
+typedef struct hv_seg hv_seg;
+/* usable = capacity - reserved - headroom (memalloc.py:43-45); one free
+ * segment [0, usable) when usable > 0 (memalloc.py:74-79). */
+int hv_seg_create(uint64_t usable, hv_seg** out);
+int hv_seg_destroy(hv_seg* s);
+/* alloc_best_fit (memalloc.py:90-114): min (leftover, base); HV_E_NOCAPACITY
+ * if nothing fits. */
+int hv_seg_alloc(hv_seg* s, uint64_t size, uint64_t* base_out);
+/* best-fit probe without allocating: key (leftover, base) of the segment
+ * alloc would take (runtime.py:155-167 scans the same key). */
+int hv_seg_probe(const hv_seg* s, uint64_t size, uint64_t* leftover, uint64_t* base);
+/* free_segment (memalloc.py:117-138): coalescing; HV_E_DOUBLEFREE if
+ * (base,size) is not a live allocation. */
+int hv_seg_free(hv_seg* s, uint64_t base, uint64_t size);
+int hv_seg_allocated_bytes(const hv_seg* s, uint64_t* out);   /* memalloc.py:86-87 */
+int hv_seg_free_bytes(const hv_seg* s, uint64_t* out);        /* memalloc.py:82-83 */
+int hv_seg_num_free(const hv_seg* s, uint64_t* out);
+/* copy out the base-sorted free list as (base,size) pairs; *n in = capacity
+ * in pairs, out = pairs written (or needed when capacity is too small). */
+int hv_seg_free_list(const hv_seg* s, uint64_t* pairs, uint64_t* n);
+/* check_invariants (memalloc.py:141-159); HV_E_INVALID on violation */
+int hv_seg_check(const hv_seg* s);
+
+/* ---- per-donor peer-memory pool ----------------------------------------- */
+typedef struct hv_pool hv_pool;
+#define HV_POOL_VMM 0u   /* cuMemAddressReserve + on-demand cuMemCreate/cuMemMap */
+#define HV_POOL_IPC 1u   /* one cudaMalloc slab, exportable with cudaIpc          */
+#define HV_POOL_EAGER 2u /* VMM: commit the whole range at creation               */
+/* Reserve `bytes` of donor-resident memory, readable and writable by the
+ * donor and every device in reader_devs.  VMM pools commit physical chunks of
+ * `chunk_bytes` (rounded to the allocation granularity) on demand. */
+int hv_pool_create(int donor_dev, uint64_t bytes, uint64_t chunk_bytes,
+                   const int* reader_devs, int n_readers, unsigned flags,
+                   hv_pool** out);
+int hv_pool_destroy(hv_pool* p);
+int hv_pool_info(const hv_pool* p, uint64_t* va, uint64_t* bytes,
+                 uint64_t* chunk_bytes, int* donor_dev);
+/* back [offset, offset+bytes) with physical donor memory (refcounted per
+ * chunk); the harvest_alloc side of "allocates memory" */
+int hv_pool_commit(hv_pool* p, uint64_t offset, uint64_t bytes);
+/* drop the refcount; chunks reaching zero are unmapped and released back to
+ * the donor.  Callers must have drained every reader first (runtime.py:396). */
+int hv_pool_decommit(hv_pool* p, uint64_t offset, uint64_t bytes);
+int hv_pool_committed_bytes(const hv_pool* p, uint64_t* out);
+/* cross-process sharing (HV_POOL_IPC): 64-byte cudaIpcMemHandle_t */
+int hv_pool_export_ipc(const hv_pool* p, void* handle64);
+int hv_pool_import_ipc(const void* handle64, int donor_dev, uint64_t bytes,
+                       int reader_dev, hv_pool** out);
+
+/* ---- host tier: pinned, portable, mapped ------------------------------- */
+int hv_host_alloc(uint64_t bytes, void** h_ptr, uint64_t* d_alias);
+int hv_host_free(void* h_ptr);
+/* pin an existing host range (cudaHostRegister, mapped+portable) */
+int hv_host_register(void* h_ptr, uint64_t bytes, uint64_t* d_alias);
+int hv_host_unregister(void* h_ptr);
+
+/* ---- device scratch ------------------------------------------------------ */
+int hv_dev_alloc(int device, uint64_t bytes, uint64_t* d_ptr);
+int hv_dev_free(int device, uint64_t d_ptr);
+int hv_memcpy_h2d(uint64_t d_dst, const void* h_src, uint64_t bytes, void* stream);
+int hv_memcpy_d2h(void* h_dst, uint64_t d_src, uint64_t bytes, void* stream);
+int hv_memset_d8(uint64_t d_dst, int value, uint64_t bytes, void* stream);
+
+/* ---- streams and events (drain ordering, runtime.py:345-356) ----------- */
+int hv_stream_create(int device, int priority, void** stream);
+int hv_stream_destroy(void* stream);
+int hv_stream_synchronize(void* stream);
+int hv_event_create(int device, unsigned timing, void** event);
+int hv_event_destroy(void* event);
+int hv_event_record(void* event, void* stream);
+/* *done = 1 if every op captured by the event has completed */
+int hv_event_query(void* event, int* done);
+int hv_event_synchronize(void* event);
+int hv_event_elapsed_ms(void* start, void* stop, float* ms);
+int hv_stream_wait_event(void* stream, void* event);
+
+/* ---- fetch engines (the hot path) ------------------------------------- */
+/* engine selector for hv_batch_copy / hv_kv_gather */
+#define HV_ENGINE_AUTO 0
+#define HV_ENGINE_LDG 1  /* SM-issued 128-bit ld.global.nc / st.global, warp per 4 KiB chunk */
+#define HV_ENGINE_TMA 2  /* cp.async.bulk global->smem->global ring, one issuing lane per CTA */
+
+/* K1: block-table-indexed KV-page gather.  Page i is copied from
+ * d_src_page_ptrs[i] to d_dst_page_ptrs[i] (or, when d_dst_page_ptrs is NULL,
+ * to d_dst_base + i*page_bytes).  Sources may be on any donor, local or the
+ * host tier; one launch moves every page.  max_ctas caps the grid (0 = fill
+ * the device) so the gather can share SMs with decode compute.  Replaces one
+ * app_transfer per KV block (runtime.py:320-364). */
+int hv_kv_gather(const uint64_t* d_src_page_ptrs, const uint64_t* d_dst_page_ptrs,
+                 uint64_t d_dst_base, uint32_t n_pages, uint64_t page_bytes,
+                 int engine, int max_ctas, void* stream);
+
+/* K1 with the block table resolved on the device: page i comes from
+ *   d_slot_base[loc >> 32] + (loc & 0xffffffff) * page_bytes,
+ * loc = d_locs[i] (base index, slot).  Avoids shipping one pointer per page. */
+int hv_kv_gather_table(const uint64_t* d_slot_bases, const uint64_t* d_locs,
+                       uint64_t d_dst_base, const uint64_t* d_dst_page_ptrs,
+                       uint32_t n_pages, uint64_t page_bytes, int engine,
+                       int max_ctas, void* stream);
+
+/* K2: variable-size batched fetch (expert weights, placement copy-in):
+ * d_src[i] -> d_dst[i], d_bytes[i] bytes, for i < n.  One launch for a whole
+ * pipeline stage (moe.py:282-313). */
+int hv_batch_copy(const uint64_t* d_src, const uint64_t* d_dst, const uint64_t* d_bytes,
+                  uint32_t n, int engine, int max_ctas, void* stream);
+
+/* vLLM-compatible host-array form of K2 (swap_blocks_batch(src_ptrs,
+ * dst_ptrs, sizes), vllm/_custom_ops.py:2681-2703): the arrays are staged
+ * through a pinned ring and uploaded on `stream` before the launch. */
+int hv_swap_blocks_batch(const uint64_t* h_src, const uint64_t* h_dst,
+                         const uint64_t* h_bytes, uint32_t n, int engine,
+                         int max_ctas, void* stream);
+
+/* Copy-engine baselines: per-object cudaMemcpyAsync (peer copies route over
+ * NVLink via UVA, i.e. cudaMemcpyPeerAsync) when batched == 0,
+ * one cudaMemcpyBatchAsync submission when batched == 1. Host arrays. */
+int hv_ce_batch_copy(const uint64_t* h_src, const uint64_t* h_dst,
+                     const uint64_t* h_bytes, uint32_t n, int batched, void* stream);
+
+/* ---- synthetic content (test / bench inputs) --------------------------- */
+/* byte j of object = byte (j%8) (little-endian) of splitmix64 word j/8:
+ *   w_i = fmix(seed + (i+1)*0x9E3779B97F4A7C15)
+ * seeded by stable_hash64(tag) (runtime.py:38-44). */
+int hv_fill_content(const uint64_t* d_dst, const uint64_t* d_bytes,
+                    const uint64_t* d_seeds, uint32_t n, void* stream);
+/* position-keyed 64-bit digest per object (see oracle/hv_oracle.c) */
+int hv_digest(const uint64_t* d_src, const uint64_t* d_bytes, uint32_t n,
+              uint64_t* d_out, void* stream);
+/* count of 8-byte words differing from the generator, per object */
+int hv_verify_content(const uint64_t* d_src, const uint64_t* d_bytes,
+                      const uint64_t* d_seeds, uint32_t n, uint64_t* d_mismatch,
+                      void* stream);
+
+/* number of kernel launches issued by this library in this process */
+int hv_launch_count(uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HARVEST_B200_H_ */

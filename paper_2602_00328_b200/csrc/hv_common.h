@@ -1,0 +1,34 @@
+// Internal helpers shared by the translation units of libharvest_b200.so.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/harvest_b200.h"
+
+#define HV_EXPORT extern "C" __attribute__((visibility("default")))
+
+static inline int hv_cuda_status(cudaError_t e) {
+  return e == cudaSuccess ? HV_OK : (HV_E_CUDA_BASE - (int)e);
+}
+
+#define HV_CUDA(expr)                                  \
+  do {                                                 \
+    cudaError_t hv_e_ = (expr);                        \
+    if (hv_e_ != cudaSuccess) {                        \
+      (void)cudaGetLastError();                        \
+      return hv_cuda_status(hv_e_);                    \
+    }                                                  \
+  } while (0)
+
+#define HV_CHECK_ARG(cond)         \
+  do {                             \
+    if (!(cond)) return HV_E_INVALID; \
+  } while (0)
+
+namespace hv {
+// Make the device that owns `stream` current (static cudart keeps its own
+// notion of the current device, so never rely on the caller's).
+int bind_stream_device(void* stream, int* device_out);
+void note_launch(uint64_t n = 1);
+int sm_count(int device);
+}  // namespace hv

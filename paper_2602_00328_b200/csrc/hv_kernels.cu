@@ -1,0 +1,822 @@
+// Fetch kernels of the B200 Harvest data plane (sm_100a).
+//
+// The reference never moves bytes: a fetch is `fixed_cost + size/bandwidth`
+// (interconnect.py:51-54), serialized FIFO per device pair
+// (interconnect.py:147-150) and issued one object at a time by
+// HarvestRuntime.app_transfer (runtime.py:320-364) from the MoE stage loop
+// (moe.py:282-313) or the KV reload path.  Here one launch
+// moves a whole batch (every page of a decode step/layer, every expert of a
+// pipeline stage), with all objects in flight at once.
+//
+// Work decomposition (shared by every engine and op): each object is cut into
+// fixed-size chunks; chunk c of the flattened batch is handled by one warp
+// (LDG engine, 4 KiB chunks) or one CTA pipeline slot (TMA engine, 16 KiB
+// chunks).  Objects are either uniform pages (chunk -> page by division) or
+// variable-size descriptors (chunk -> object through a per-CTA shared-memory
+// prefix of chunk counts).
+//
+// LDG engine: every lane front-batches 8 x 128-bit `ld.global.nc.L1::no_allocate`
+// (4 KiB per warp in flight) then streams them out with `st.global.L1::no_allocate`.
+// Peer loads through NVLink bypass the local L2 and take ~2 us, so the bytes
+// in flight per SM, not instruction issue, set the rate (Little's law).
+// TMA engine: one lane per CTA drives a ring of shared-memory stages with
+// `cp.async.bulk` global->smem (mbarrier complete_tx) and smem->global
+// (bulk_group), so a handful of CTAs keep megabytes in flight while leaving the
+// SMs' issue slots to decode compute.
+#include <atomic>
+#include <string.h>
+#include <type_traits>
+#include <mutex>
+#include <vector>
+
+#include "hv_common.h"
+
+namespace hv {
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch(uint64_t n) { g_launches += n; }
+
+int bind_stream_device(void* stream, int* device_out) {
+  int dev = 0;
+  if (stream) {
+    cudaError_t e = cudaStreamGetDevice((cudaStream_t)stream, &dev);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      return hv_cuda_status(e);
+    }
+  } else {
+    HV_CUDA(cudaGetDevice(&dev));
+  }
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != dev) HV_CUDA(cudaSetDevice(dev));
+  if (device_out) *device_out = dev;
+  return HV_OK;
+}
+
+int sm_count(int device) {
+  static int cache[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (!cache[device]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+      (void)cudaGetLastError();
+      n = 148;
+    }
+    cache[device] = n;
+  }
+  return cache[device];
+}
+
+}  // namespace hv
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// constants
+constexpr int kLdgThreads = 512;                 // 16 warps per CTA
+constexpr int kLdgUnroll = 8;                    // 128-bit loads in flight per lane
+constexpr uint32_t kLdgChunk = kLdgUnroll * 32 * 16;  // 4 KiB per warp iteration
+constexpr int kTmaThreads = 32;                  // one warp; lane 0 issues
+constexpr uint32_t kTmaChunk = 16384;            // bytes per bulk copy
+constexpr int kTmaStages = 8;                    // 128 KiB of smem ring per CTA
+constexpr uint32_t kMaxSmemDescs = 2048;         // variable-size descriptors per launch
+constexpr uint32_t kPageBatchMax = 1u << 30;
+
+// splitmix64 (Steele, Lea, Flood 2014) — the synthetic content generator; the
+// seed is stable_hash64(tag) (runtime.py:38-44, moe.py:114-115).
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kDigestKey = 0xD1B54A32D192ED03ull;
+
+__host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t content_word(uint64_t seed, uint64_t i) {
+  return fmix64(seed + (i + 1) * kGolden);
+}
+__host__ __device__ __forceinline__ uint64_t digest_term(uint64_t i, uint64_t w) {
+  return fmix64(w ^ ((i + 1) * kDigestKey));
+}
+
+// ---------------------------------------------------------------------------
+// memory primitives
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(void* p, const uint4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// chunk resolvers: chunk index -> (src, dst, len, object index, offset)
+struct ChunkRef {
+  const char* src;
+  char* dst;
+  uint32_t len;
+  uint32_t obj;
+  uint64_t off;
+};
+
+// Uniform pages (K1).  kTable: src = slot_bases[loc>>32] + (loc&0xffffffff)*page.
+template <bool kTable>
+struct PageResolver {
+  const uint64_t* src;      // per-page pointers, or slot bases (kTable)
+  const uint64_t* locs;     // kTable only
+  const uint64_t* dst_ptrs; // nullable
+  uint64_t dst_base;
+  uint64_t page_bytes;
+  uint32_t chunks_per_page;
+  uint32_t n_pages;
+  uint32_t chunk;
+
+  __device__ __forceinline__ uint32_t setup(void*) const { return n_pages * chunks_per_page; }
+  __device__ __forceinline__ ChunkRef at(uint32_t c, uint32_t& hint) const {
+    (void)hint;
+    const uint32_t page = c / chunks_per_page;
+    const uint32_t ci = c - page * chunks_per_page;
+    uint64_t s;
+    if (kTable) {
+      const uint64_t loc = __ldg(locs + page);
+      s = __ldg(src + (loc >> 32)) + (loc & 0xffffffffull) * page_bytes;
+    } else {
+      s = __ldg(src + page);
+    }
+    const uint64_t d = dst_ptrs ? __ldg(dst_ptrs + page) : dst_base + (uint64_t)page * page_bytes;
+    ChunkRef r;
+    r.off = (uint64_t)ci * chunk;
+    const uint64_t rem = page_bytes - r.off;
+    r.len = rem < chunk ? (uint32_t)rem : chunk;
+    r.src = reinterpret_cast<const char*>(s) + r.off;
+    r.dst = reinterpret_cast<char*>(d) + r.off;
+    r.obj = page;
+    return r;
+  }
+};
+
+// Variable-size descriptors (K2).  The per-CTA prefix of chunk counts lives
+// in shared memory; a warp's successive chunks are monotone in c, so the
+// object index is found by a short forward probe before falling back to
+// binary search.
+struct DescResolver {
+  const uint64_t* src;
+  const uint64_t* dst;
+  const uint64_t* bytes;
+  uint32_t n;
+  uint32_t chunk;
+
+  // s_start must hold n+1 entries; all threads of the CTA call setup().
+  __device__ uint32_t setup(void* smem) const {
+    uint32_t* s_start = reinterpret_cast<uint32_t*>(smem);
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_total;
+    const uint32_t nt = blockDim.x, tid = threadIdx.x;
+    const uint32_t lane = tid & 31, warp = tid >> 5, nwarps = (nt + 31) >> 5;
+    const uint32_t per = (n + nt - 1) / nt;
+    const uint32_t i0 = tid * per;
+    uint32_t local = 0;
+    for (uint32_t k = 0; k < per; ++k) {
+      const uint32_t i = i0 + k;
+      if (i < n) {
+        const uint32_t cnt = (uint32_t)((__ldg(bytes + i) + chunk - 1) / chunk);
+        s_start[i] = cnt;
+        local += cnt;
+      }
+    }
+    uint32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += t;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t w = lane < nwarps ? s_warp[lane] : 0;
+      uint32_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= (uint32_t)o) wi += t;
+      }
+      if (lane < nwarps) s_warp[lane] = wi - w;
+      if (lane == 31) s_total = wi;
+    }
+    __syncthreads();
+    uint32_t run = s_warp[warp] + incl - local;
+    for (uint32_t k = 0; k < per; ++k) {
+      const uint32_t i = i0 + k;
+      if (i < n) {
+        const uint32_t cnt = s_start[i];
+        s_start[i] = run;
+        run += cnt;
+      }
+    }
+    if (tid == 0) s_start[n] = s_total;
+    __syncthreads();
+    return s_total;
+  }
+
+  __device__ __forceinline__ ChunkRef at(uint32_t c, uint32_t& hint, const uint32_t* s_start) const {
+    uint32_t lo = hint;
+    if (!(s_start[lo] <= c && c < s_start[lo + 1])) {
+      if (lo + 2 <= n && s_start[lo + 1] <= c && c < s_start[lo + 2]) {
+        lo = lo + 1;
+      } else {
+        uint32_t l = 0, h = n;  // s_start[l] <= c < s_start[h]
+        while (h - l > 1) {
+          const uint32_t m = (l + h) >> 1;
+          if (s_start[m] <= c) l = m; else h = m;
+        }
+        lo = l;
+      }
+    }
+    hint = lo;
+    ChunkRef r;
+    r.obj = lo;
+    r.off = (uint64_t)(c - s_start[lo]) * chunk;
+    const uint64_t rem = __ldg(bytes + lo) - r.off;
+    r.len = rem < chunk ? (uint32_t)rem : chunk;
+    r.src = reinterpret_cast<const char*>(__ldg(src + lo)) + r.off;
+    r.dst = reinterpret_cast<char*>(__ldg(dst + lo)) + r.off;
+    return r;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// per-chunk operations (warp-cooperative)
+
+__device__ __forceinline__ void copy_chunk_ldg(const ChunkRef& r, uint32_t lane) {
+  const bool aligned = ((reinterpret_cast<uintptr_t>(r.src) | reinterpret_cast<uintptr_t>(r.dst)) & 15) == 0;
+  if (aligned && r.len == kLdgChunk) {
+    uint4 v[kLdgUnroll];
+#pragma unroll
+    for (int j = 0; j < kLdgUnroll; ++j) v[j] = ld_stream(r.src + (j * 32 + lane) * 16);
+#pragma unroll
+    for (int j = 0; j < kLdgUnroll; ++j) st_stream(r.dst + (j * 32 + lane) * 16, v[j]);
+    return;
+  }
+  uint32_t done = 0;
+  if (aligned) {
+    const uint32_t nvec = r.len >> 4;
+    for (uint32_t v = lane; v < nvec; v += 32) st_stream(r.dst + v * 16, ld_stream(r.src + v * 16));
+    done = nvec << 4;
+  }
+  for (uint32_t b = done + lane; b < r.len; b += 32) r.dst[b] = r.src[b];
+}
+
+// generic warp-per-chunk driver
+template <typename Res, typename Op>
+__device__ __forceinline__ void warp_loop(const Res& res, uint32_t total, Op op, const uint32_t* smem) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t wpb = blockDim.x >> 5;
+  const uint32_t nwarps = gridDim.x * wpb;
+  uint32_t hint = 0;
+  for (uint32_t c = blockIdx.x * wpb + (threadIdx.x >> 5); c < total; c += nwarps) {
+    ChunkRef r;
+    if constexpr (std::is_same<Res, DescResolver>::value) r = res.at(c, hint, smem);
+    else r = res.at(c, hint);
+    op(r, lane);
+  }
+}
+
+struct CopyOp {
+  __device__ __forceinline__ void operator()(const ChunkRef& r, uint32_t lane) const { copy_chunk_ldg(r, lane); }
+};
+
+// content ops work on 8-byte words; objects must start 8-byte aligned
+struct FillOp {
+  const uint64_t* seeds;
+  __device__ __forceinline__ void operator()(const ChunkRef& r, uint32_t lane) const {
+    const uint64_t seed = __ldg(seeds + r.obj);
+    const uint64_t w0 = r.off >> 3;
+    const uint32_t nfull = r.len >> 3;
+    uint64_t* d = reinterpret_cast<uint64_t*>(r.dst);
+    for (uint32_t k = lane; k < nfull; k += 32) d[k] = content_word(seed, w0 + k);
+    const uint32_t tail = r.len & 7;
+    if (tail && lane == 0) {
+      const uint64_t w = content_word(seed, w0 + nfull);
+      for (uint32_t b = 0; b < tail; ++b) r.dst[nfull * 8 + b] = (char)((w >> (8 * b)) & 0xff);
+    }
+  }
+};
+
+__device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ uint64_t load_word_tail(const char* p, uint32_t n) {
+  uint64_t w = 0;
+  for (uint32_t b = 0; b < n; ++b) w |= (uint64_t)(uint8_t)p[b] << (8 * b);
+  return w;
+}
+
+struct DigestOp {
+  const uint64_t* bytes;  // for the size term
+  unsigned long long* out;
+  __device__ __forceinline__ void operator()(const ChunkRef& r, uint32_t lane) const {
+    const uint64_t w0 = r.off >> 3;
+    const uint32_t nfull = r.len >> 3;
+    const uint64_t* s = reinterpret_cast<const uint64_t*>(r.src);
+    uint64_t acc = 0;
+    for (uint32_t k = lane; k < nfull; k += 32) acc += digest_term(w0 + k, s[k]);
+    const uint32_t tail = r.len & 7;
+    if (tail && lane == 0) acc += digest_term(w0 + nfull, load_word_tail(r.src + nfull * 8, tail));
+    if (r.off == 0 && lane == 0) acc += __ldg(bytes + r.obj);
+    acc = warp_sum(acc);
+    if (lane == 0) atomicAdd(out + r.obj, (unsigned long long)acc);
+  }
+};
+
+struct VerifyOp {
+  const uint64_t* seeds;
+  unsigned long long* out;
+  __device__ __forceinline__ void operator()(const ChunkRef& r, uint32_t lane) const {
+    const uint64_t seed = __ldg(seeds + r.obj);
+    const uint64_t w0 = r.off >> 3;
+    const uint32_t nfull = r.len >> 3;
+    const uint64_t* s = reinterpret_cast<const uint64_t*>(r.src);
+    uint64_t bad = 0;
+    for (uint32_t k = lane; k < nfull; k += 32) bad += (s[k] != content_word(seed, w0 + k));
+    const uint32_t tail = r.len & 7;
+    if (tail && lane == 0) {
+      const uint64_t mask = (1ull << (8 * tail)) - 1;
+      bad += ((load_word_tail(r.src + nfull * 8, tail) ^ content_word(seed, w0 + nfull)) & mask) != 0;
+    }
+    bad = warp_sum(bad);
+    if (lane == 0 && bad) atomicAdd(out + r.obj, (unsigned long long)bad);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// LDG-engine kernels
+
+template <bool kTable>
+__global__ void __launch_bounds__(kLdgThreads) page_copy_ldg(PageResolver<kTable> res) {
+  const uint32_t total = res.setup(nullptr);
+  warp_loop(res, total, CopyOp{}, nullptr);
+}
+
+template <typename Op>
+__global__ void __launch_bounds__(kLdgThreads) desc_op_kernel(DescResolver res, Op op) {
+  __shared__ uint32_t s_start[kMaxSmemDescs + 1];
+  const uint32_t total = res.setup(s_start);
+  warp_loop(res, total, op, s_start);
+}
+
+// ---------------------------------------------------------------------------
+// TMA (bulk-copy) engine
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "HV_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra HV_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ bool tma_ok(const ChunkRef& r) {
+  return ((reinterpret_cast<uintptr_t>(r.src) | reinterpret_cast<uintptr_t>(r.dst) | r.len) & 15) == 0 && r.len > 0;
+}
+
+// One warp per CTA.  Chunks b, b+G, b+2G... of the batch flow through a ring
+// of kTmaStages shared-memory stages: load k+S-1 is in flight while chunk k is
+// stored.  Irregular chunks (unaligned or len % 16) are copied by the warp.
+template <typename Res>
+__device__ __forceinline__ void tma_loop(const Res& res, uint32_t total, const uint32_t* s_desc,
+                                         char* ring, uint64_t* bars) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (lane == 0) {
+    for (int s = 0; s < kTmaStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const uint32_t G = gridDim.x;
+  const uint32_t mine = blockIdx.x < total ? (total - blockIdx.x + G - 1) / G : 0;
+  uint32_t hint_issue = 0, hint_store = 0;
+  auto chunk_of = [&](uint32_t t, uint32_t& hint) -> ChunkRef {
+    const uint32_t c = blockIdx.x + t * G;
+    if constexpr (std::is_same<Res, DescResolver>::value) return res.at(c, hint, s_desc);
+    else return res.at(c, hint);
+  };
+  // prologue: fill the ring
+  const uint32_t pro = mine < (uint32_t)kTmaStages ? mine : (uint32_t)kTmaStages;
+  for (uint32_t t = 0; t < pro; ++t) {
+    const ChunkRef r = chunk_of(t, hint_issue);
+    if (tma_ok(r) && lane == 0) {
+      mbar_expect_tx(&bars[t], r.len);
+      bulk_g2s(ring + (size_t)t * kTmaChunk, r.src, r.len, &bars[t]);
+    }
+  }
+  uint32_t next_issue = pro;
+  for (uint32_t t = 0; t < mine; ++t) {
+    const uint32_t stage = t % kTmaStages;
+    const uint32_t parity = (t / kTmaStages) & 1;
+    const ChunkRef r = chunk_of(t, hint_store);
+    if (tma_ok(r)) {
+      mbar_wait(&bars[stage], parity);
+      if (lane == 0) bulk_s2g(r.dst, ring + (size_t)stage * kTmaChunk, r.len);
+    } else {
+      copy_chunk_ldg(r, lane);  // generic path; stage stays unused this round
+      if (lane == 0) {          // keep the barrier phase sequence regular
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bars[stage])) : "memory");
+      }
+      mbar_wait(&bars[stage], parity);
+    }
+    // one bulk group per iteration (possibly empty) so that wait_group.read<1>
+    // below always means "the store of chunk t-1 has finished reading smem"
+    if (lane == 0) bulk_commit();
+    // refill the stage consumed one iteration ago once its store has read smem
+    if (next_issue < mine && t >= 1) {
+      const uint32_t rs = (t - 1) % kTmaStages;
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
+      const ChunkRef n = chunk_of(next_issue, hint_issue);
+      if (tma_ok(n) && lane == 0) {
+        mbar_expect_tx(&bars[rs], n.len);
+        bulk_g2s(ring + (size_t)rs * kTmaChunk, n.src, n.len, &bars[rs]);
+      }
+      ++next_issue;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) bulk_wait_all();
+  __syncwarp();
+}
+
+// NOTE on the refill order: chunk t+S-1 goes into stage (t-1)%S, which is the
+// stage chunk t-1 used; chunk index t' always maps to stage t'%S because
+// next_issue == t-1+S at that point (prologue issued S chunks, one refill per
+// iteration from t=1 on), so (t-1)%S == next_issue%S.
+
+template <bool kTable>
+__global__ void __launch_bounds__(kTmaThreads) page_copy_tma(PageResolver<kTable> res) {
+  extern __shared__ __align__(128) char dyn_smem[];
+  __shared__ __align__(8) uint64_t bars[kTmaStages];
+  const uint32_t total = res.setup(nullptr);
+  tma_loop(res, total, nullptr, dyn_smem, bars);
+}
+
+__global__ void __launch_bounds__(kTmaThreads) desc_copy_tma(DescResolver res) {
+  extern __shared__ __align__(128) char dyn_smem[];
+  __shared__ __align__(8) uint64_t bars[kTmaStages];
+  __shared__ uint32_t s_start[kMaxSmemDescs + 1];
+  const uint32_t total = res.setup(s_start);
+  tma_loop(res, total, s_start, dyn_smem, bars);
+}
+
+constexpr size_t kTmaSmem = (size_t)kTmaStages * kTmaChunk;
+
+// ---------------------------------------------------------------------------
+// launch helpers
+
+int pick_engine(int engine) { return engine == HV_ENGINE_AUTO ? HV_ENGINE_LDG : engine; }
+
+int ldg_grid(int dev, uint64_t chunks, int max_ctas) {
+  const int sms = hv::sm_count(dev);
+  int per_sm = 2048 / kLdgThreads;  // 4 CTAs of 512 threads = full occupancy
+  int64_t g = (int64_t)sms * per_sm;
+  const int64_t need = (int64_t)((chunks + (kLdgThreads / 32) - 1) / (kLdgThreads / 32));
+  if (need < g) g = need;
+  if (max_ctas > 0 && g > max_ctas) g = max_ctas;
+  return (int)(g < 1 ? 1 : g);
+}
+
+int tma_grid(int dev, uint64_t chunks, int max_ctas) {
+  const int sms = hv::sm_count(dev);
+  int64_t g = sms;  // 128 KiB ring: one CTA per SM
+  if ((int64_t)chunks < g) g = (int64_t)chunks;
+  if (max_ctas > 0 && g > max_ctas) g = max_ctas;
+  return (int)(g < 1 ? 1 : g);
+}
+
+int set_tma_attrs() {
+  static std::once_flag once;
+  static int st = HV_OK;
+  std::call_once(once, [] {
+    cudaError_t e = cudaFuncSetAttribute(page_copy_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(page_copy_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(desc_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+    st = hv_cuda_status(e);
+    (void)cudaGetLastError();
+  });
+  return st;
+}
+
+template <bool kTable>
+int launch_pages(PageResolver<kTable> res, int engine, int max_ctas, void* stream) {
+  int dev = 0;
+  int st = hv::bind_stream_device(stream, &dev);
+  if (st) return st;
+  if (res.n_pages == 0 || res.page_bytes == 0) return HV_OK;
+  engine = pick_engine(engine);
+  if (engine == HV_ENGINE_TMA) {
+    if ((st = set_tma_attrs())) return st;
+    res.chunk = kTmaChunk;
+    res.chunks_per_page = (uint32_t)((res.page_bytes + kTmaChunk - 1) / kTmaChunk);
+    const uint64_t total = (uint64_t)res.n_pages * res.chunks_per_page;
+    if (total >= 0xffffffffull) return HV_E_INVALID;
+    page_copy_tma<kTable><<<tma_grid(dev, total, max_ctas), kTmaThreads, kTmaSmem, (cudaStream_t)stream>>>(res);
+  } else if (engine == HV_ENGINE_LDG) {
+    res.chunk = kLdgChunk;
+    res.chunks_per_page = (uint32_t)((res.page_bytes + kLdgChunk - 1) / kLdgChunk);
+    const uint64_t total = (uint64_t)res.n_pages * res.chunks_per_page;
+    if (total >= 0xffffffffull) return HV_E_INVALID;
+    page_copy_ldg<kTable><<<ldg_grid(dev, total, max_ctas), kLdgThreads, 0, (cudaStream_t)stream>>>(res);
+  } else {
+    return HV_E_INVALID;
+  }
+  HV_CUDA(cudaGetLastError());
+  hv::note_launch();
+  return HV_OK;
+}
+
+// Variable-size launch: up to kMaxSmemDescs descriptors per launch.  The
+// chunk count is not known on the host (sizes are device-resident), so the
+// grid is sized to fill the device (capped by max_ctas).
+template <typename Op>
+int launch_descs(const uint64_t* d_src, const uint64_t* d_dst, const uint64_t* d_bytes, uint32_t n,
+                 int engine, int max_ctas, void* stream, Op op, bool is_copy) {
+  int dev = 0;
+  int st = hv::bind_stream_device(stream, &dev);
+  if (st) return st;
+  engine = pick_engine(engine);
+  if (engine == HV_ENGINE_TMA && is_copy && (st = set_tma_attrs())) return st;
+  for (uint32_t base = 0; base < n; base += kMaxSmemDescs) {
+    const uint32_t m = (n - base) < kMaxSmemDescs ? (n - base) : kMaxSmemDescs;
+    DescResolver res;
+    res.src = d_src ? d_src + base : nullptr;
+    res.dst = d_dst ? d_dst + base : nullptr;
+    res.bytes = d_bytes + base;
+    res.n = m;
+    Op o = op;
+    o.rebase(base);
+    if (is_copy && engine == HV_ENGINE_TMA) {
+      res.chunk = kTmaChunk;
+      desc_copy_tma<<<tma_grid(dev, ~0ull, max_ctas), kTmaThreads, kTmaSmem, (cudaStream_t)stream>>>(res);
+    } else if (engine == HV_ENGINE_LDG || !is_copy) {
+      res.chunk = kLdgChunk;
+      desc_op_kernel<<<ldg_grid(dev, ~0ull, max_ctas), kLdgThreads, 0, (cudaStream_t)stream>>>(res, o);
+    } else {
+      return HV_E_INVALID;
+    }
+    HV_CUDA(cudaGetLastError());
+    hv::note_launch();
+  }
+  return HV_OK;
+}
+
+struct CopyOpR : CopyOp {
+  __host__ __device__ void rebase(uint32_t) {}
+};
+struct FillOpR : FillOp {
+  __host__ __device__ void rebase(uint32_t b) { seeds += b; }
+};
+struct DigestOpR : DigestOp {
+  __host__ __device__ void rebase(uint32_t b) {
+    bytes += b;
+    out += b;
+  }
+};
+struct VerifyOpR : VerifyOp {
+  __host__ __device__ void rebase(uint32_t b) {
+    seeds += b;
+    out += b;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// pinned staging ring for host-array entry points (hv_swap_blocks_batch)
+
+constexpr uint32_t kRingSlots = 32;
+constexpr uint32_t kSlotDescs = kMaxSmemDescs;  // descriptors per slot
+
+struct StagingRing {
+  bool init = false;
+  uint64_t* h = nullptr;  // pinned: kRingSlots * 3 * kSlotDescs words
+  uint64_t* d = nullptr;
+  cudaEvent_t ev[kRingSlots] = {};
+  bool used[kRingSlots] = {};
+  uint32_t next = 0;
+};
+
+std::mutex g_ring_mu;
+StagingRing g_rings[64];
+
+int ring_acquire(int dev, uint32_t* slot, StagingRing** ring) {
+  if (dev < 0 || dev >= 64) return HV_E_INVALID;
+  StagingRing& r = g_rings[dev];
+  if (!r.init) {
+    const size_t words = (size_t)kRingSlots * 3 * kSlotDescs;
+    HV_CUDA(cudaHostAlloc((void**)&r.h, words * 8, cudaHostAllocPortable));
+    HV_CUDA(cudaMalloc((void**)&r.d, words * 8));
+    for (uint32_t i = 0; i < kRingSlots; ++i) HV_CUDA(cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming));
+    r.init = true;
+  }
+  const uint32_t s = r.next;
+  r.next = (r.next + 1) % kRingSlots;
+  if (r.used[s]) HV_CUDA(cudaEventSynchronize(r.ev[s]));  // previous user of the slot is done
+  *slot = s;
+  *ring = &r;
+  return HV_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+HV_EXPORT int hv_abi_version(void) { return HV_ABI_VERSION; }
+
+HV_EXPORT const char* hv_error_string(int status) {
+  switch (status) {
+    case HV_OK: return "ok";
+    case HV_E_INVALID: return "invalid argument";
+    case HV_E_NOCAPACITY: return "no capacity";
+    case HV_E_DOUBLEFREE: return "double free or unknown segment";
+    case HV_E_UNSUPPORTED: return "unsupported on this device/driver";
+    case HV_E_NOMEM: return "host allocation failed";
+    default: break;
+  }
+  if (status <= HV_E_CU_BASE) return "CUDA driver API error (code = -3000 - CUresult)";
+  if (status <= HV_E_CUDA_BASE) return cudaGetErrorString((cudaError_t)(HV_E_CUDA_BASE - status));
+  return "unknown status";
+}
+
+HV_EXPORT int hv_launch_count(uint64_t* out) {
+  HV_CHECK_ARG(out);
+  *out = hv::g_launches.load();
+  return HV_OK;
+}
+
+HV_EXPORT int hv_kv_gather(const uint64_t* d_src_page_ptrs, const uint64_t* d_dst_page_ptrs, uint64_t d_dst_base,
+                           uint32_t n_pages, uint64_t page_bytes, int engine, int max_ctas, void* stream) {
+  HV_CHECK_ARG(n_pages == 0 || d_src_page_ptrs != nullptr);
+  HV_CHECK_ARG(n_pages == 0 || d_dst_page_ptrs != nullptr || d_dst_base != 0);
+  HV_CHECK_ARG(n_pages <= kPageBatchMax);
+  PageResolver<false> r{};
+  r.src = d_src_page_ptrs;
+  r.locs = nullptr;
+  r.dst_ptrs = d_dst_page_ptrs;
+  r.dst_base = d_dst_base;
+  r.page_bytes = page_bytes;
+  r.n_pages = n_pages;
+  return launch_pages(r, engine, max_ctas, stream);
+}
+
+HV_EXPORT int hv_kv_gather_table(const uint64_t* d_slot_bases, const uint64_t* d_locs, uint64_t d_dst_base,
+                                 const uint64_t* d_dst_page_ptrs, uint32_t n_pages, uint64_t page_bytes, int engine,
+                                 int max_ctas, void* stream) {
+  HV_CHECK_ARG(n_pages == 0 || (d_slot_bases != nullptr && d_locs != nullptr));
+  HV_CHECK_ARG(n_pages == 0 || d_dst_page_ptrs != nullptr || d_dst_base != 0);
+  HV_CHECK_ARG(n_pages <= kPageBatchMax);
+  PageResolver<true> r{};
+  r.src = d_slot_bases;
+  r.locs = d_locs;
+  r.dst_ptrs = d_dst_page_ptrs;
+  r.dst_base = d_dst_base;
+  r.page_bytes = page_bytes;
+  r.n_pages = n_pages;
+  return launch_pages(r, engine, max_ctas, stream);
+}
+
+HV_EXPORT int hv_batch_copy(const uint64_t* d_src, const uint64_t* d_dst, const uint64_t* d_bytes, uint32_t n,
+                            int engine, int max_ctas, void* stream) {
+  if (n == 0) return HV_OK;
+  HV_CHECK_ARG(d_src && d_dst && d_bytes);
+  return launch_descs(d_src, d_dst, d_bytes, n, engine, max_ctas, stream, CopyOpR{}, true);
+}
+
+HV_EXPORT int hv_swap_blocks_batch(const uint64_t* h_src, const uint64_t* h_dst, const uint64_t* h_bytes, uint32_t n,
+                                   int engine, int max_ctas, void* stream) {
+  if (n == 0) return HV_OK;
+  HV_CHECK_ARG(h_src && h_dst && h_bytes);
+  int dev = 0;
+  int st = hv::bind_stream_device(stream, &dev);
+  if (st) return st;
+  std::lock_guard<std::mutex> lk(g_ring_mu);
+  for (uint32_t base = 0; base < n; base += kSlotDescs) {
+    const uint32_t m = (n - base) < kSlotDescs ? (n - base) : kSlotDescs;
+    uint32_t slot = 0;
+    StagingRing* ring = nullptr;
+    if ((st = ring_acquire(dev, &slot, &ring))) return st;
+    uint64_t* hs = ring->h + (size_t)slot * 3 * kSlotDescs;
+    uint64_t* ds = ring->d + (size_t)slot * 3 * kSlotDescs;
+    memcpy(hs, h_src + base, m * 8);
+    memcpy(hs + kSlotDescs, h_dst + base, m * 8);
+    memcpy(hs + 2 * kSlotDescs, h_bytes + base, m * 8);
+    HV_CUDA(cudaMemcpyAsync(ds, hs, (size_t)3 * kSlotDescs * 8, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    st = launch_descs(ds, ds + kSlotDescs, ds + 2 * kSlotDescs, m, engine, max_ctas, stream, CopyOpR{}, true);
+    if (st) return st;
+    HV_CUDA(cudaEventRecord(ring->ev[slot], (cudaStream_t)stream));
+    ring->used[slot] = true;
+  }
+  return HV_OK;
+}
+
+HV_EXPORT int hv_ce_batch_copy(const uint64_t* h_src, const uint64_t* h_dst, const uint64_t* h_bytes, uint32_t n,
+                               int batched, void* stream) {
+  if (n == 0) return HV_OK;
+  HV_CHECK_ARG(h_src && h_dst && h_bytes);
+  int dev = 0;
+  int st = hv::bind_stream_device(stream, &dev);
+  if (st) return st;
+  if (!batched) {
+    for (uint32_t i = 0; i < n; ++i)
+      HV_CUDA(cudaMemcpyAsync((void*)h_dst[i], (const void*)h_src[i], h_bytes[i], cudaMemcpyDefault,
+                              (cudaStream_t)stream));
+    return HV_OK;
+  }
+  std::vector<void*> dsts(n), srcs(n);
+  std::vector<size_t> sizes(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    dsts[i] = (void*)h_dst[i];
+    srcs[i] = (void*)h_src[i];
+    sizes[i] = (size_t)h_bytes[i];
+  }
+  cudaMemcpyAttributes attr;
+  memset(&attr, 0, sizeof(attr));
+  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+  size_t attr_idx = 0, fail_idx = 0;
+  HV_CUDA(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr, &attr_idx, 1, &fail_idx,
+                               (cudaStream_t)stream));
+  return HV_OK;
+}
+
+HV_EXPORT int hv_fill_content(const uint64_t* d_dst, const uint64_t* d_bytes, const uint64_t* d_seeds, uint32_t n,
+                              void* stream) {
+  if (n == 0) return HV_OK;
+  HV_CHECK_ARG(d_dst && d_bytes && d_seeds);
+  FillOpR op;
+  op.seeds = d_seeds;
+  // FillOp writes through r.dst; the resolver's src is unused but must be valid
+  return launch_descs(d_dst, d_dst, d_bytes, n, HV_ENGINE_LDG, 0, stream, op, false);
+}
+
+HV_EXPORT int hv_digest(const uint64_t* d_src, const uint64_t* d_bytes, uint32_t n, uint64_t* d_out, void* stream) {
+  if (n == 0) return HV_OK;
+  HV_CHECK_ARG(d_src && d_bytes && d_out);
+  int dev = 0;
+  int st = hv::bind_stream_device(stream, &dev);
+  if (st) return st;
+  HV_CUDA(cudaMemsetAsync(d_out, 0, (size_t)n * 8, (cudaStream_t)stream));
+  DigestOpR op;
+  op.bytes = d_bytes;
+  op.out = reinterpret_cast<unsigned long long*>(d_out);
+  return launch_descs(d_src, d_src, d_bytes, n, HV_ENGINE_LDG, 0, stream, op, false);
+}
+
+HV_EXPORT int hv_verify_content(const uint64_t* d_src, const uint64_t* d_bytes, const uint64_t* d_seeds, uint32_t n,
+                                uint64_t* d_mismatch, void* stream) {
+  if (n == 0) return HV_OK;
+  HV_CHECK_ARG(d_src && d_bytes && d_seeds && d_mismatch);
+  int dev = 0;
+  int st = hv::bind_stream_device(stream, &dev);
+  if (st) return st;
+  HV_CUDA(cudaMemsetAsync(d_mismatch, 0, (size_t)n * 8, (cudaStream_t)stream));
+  VerifyOpR op;
+  op.seeds = d_seeds;
+  op.out = reinterpret_cast<unsigned long long*>(d_mismatch);
+  return launch_descs(d_src, d_src, d_bytes, n, HV_ENGINE_LDG, 0, stream, op, false);
+}

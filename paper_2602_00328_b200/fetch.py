@@ -1,0 +1,134 @@
+"""Device-side fetch primitives (K1 KV-page gather, K2 batched fetch, K3 copy-in).
+
+Thin typed wrappers over the C ABI; device buffers are torch tensors (torch
+is plumbing for device memory and streams here, the copies are the library's
+own sm_100a kernels).  Reference call sites these replace:
+
+* ``kv_gather``       one app_transfer per KV block reload (SPEC.md:408-416,
+                      runtime.py:320-364) -> one launch per step x layer
+* ``batch_copy``      one app_transfer per activated expert of a stage
+                      (moe.py:298-313) -> one launch per stage; also the
+                      host->peer placement copy-in of rebalance (moe.py:191-195)
+* ``swap_blocks_batch``  vLLM's offload data plane signature
+                      (vllm/_custom_ops.py:2681-2703), host int64 arrays
+* ``ce_batch_copy``   copy-engine baselines (cudaMemcpyPeerAsync-per-object,
+                      cudaMemcpyBatchAsync), the paper's own data path
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+
+def _engine(engine) -> int:
+    if isinstance(engine, int):
+        return engine
+    return N.ENGINES[engine]
+
+
+def _dev_u64(t: torch.Tensor, name: str) -> int:
+    if t is None:
+        return 0
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype not in (torch.int64, torch.uint64):
+        raise ValueError(f"{name} must be int64")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t.data_ptr()
+
+
+def kv_gather(src_page_ptrs: torch.Tensor, page_bytes: int, dst: torch.Tensor | None = None,
+              dst_page_ptrs: torch.Tensor | None = None, engine="auto", max_ctas: int = 0,
+              stream=None) -> None:
+    """Copy page i from src_page_ptrs[i] to dst (contiguous, page i at offset
+    i*page_bytes) or to dst_page_ptrs[i]."""
+    n = src_page_ptrs.numel()
+    if dst is None and dst_page_ptrs is None:
+        raise ValueError("need dst or dst_page_ptrs")
+    if dst is not None and dst.numel() * dst.element_size() < n * page_bytes:
+        raise ValueError("dst too small")
+    N.call("hv_kv_gather", _dev_u64(src_page_ptrs, "src_page_ptrs"),
+           _dev_u64(dst_page_ptrs, "dst_page_ptrs") if dst_page_ptrs is not None else 0,
+           dst.data_ptr() if dst is not None else 0, n, page_bytes, _engine(engine), max_ctas,
+           N.stream_handle(stream))
+
+
+def kv_gather_table(slot_bases: torch.Tensor, locs: torch.Tensor, page_bytes: int,
+                    dst: torch.Tensor | None = None, dst_page_ptrs: torch.Tensor | None = None,
+                    engine="auto", max_ctas: int = 0, stream=None) -> None:
+    """K1 with device-side table resolution: page i comes from
+    slot_bases[locs[i] >> 32] + (locs[i] & 0xffffffff) * page_bytes."""
+    n = locs.numel()
+    N.call("hv_kv_gather_table", _dev_u64(slot_bases, "slot_bases"), _dev_u64(locs, "locs"),
+           dst.data_ptr() if dst is not None else 0,
+           _dev_u64(dst_page_ptrs, "dst_page_ptrs") if dst_page_ptrs is not None else 0,
+           n, page_bytes, _engine(engine), max_ctas, N.stream_handle(stream))
+
+
+def batch_copy(src_ptrs: torch.Tensor, dst_ptrs: torch.Tensor, sizes: torch.Tensor,
+               engine="auto", max_ctas: int = 0, stream=None) -> None:
+    n = src_ptrs.numel()
+    if dst_ptrs.numel() != n or sizes.numel() != n:
+        raise ValueError("src_ptrs, dst_ptrs and sizes must have equal length")
+    N.call("hv_batch_copy", _dev_u64(src_ptrs, "src_ptrs"), _dev_u64(dst_ptrs, "dst_ptrs"),
+           _dev_u64(sizes, "sizes"), n, _engine(engine), max_ctas, N.stream_handle(stream))
+
+
+def _host_u64(a) -> np.ndarray:
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda:
+            raise ValueError("host arrays expected")
+        a = a.numpy()
+    return np.ascontiguousarray(a, dtype=np.uint64)
+
+
+def swap_blocks_batch(src_ptrs, dst_ptrs, sizes, engine="auto", max_ctas: int = 0, stream=None) -> None:
+    """vLLM swap_blocks_batch contract: CPU int64 arrays of raw pointers/sizes."""
+    s, d, z = _host_u64(src_ptrs), _host_u64(dst_ptrs), _host_u64(sizes)
+    if not (len(s) == len(d) == len(z)):
+        raise ValueError("length mismatch")
+    N.call("hv_swap_blocks_batch", s.ctypes.data, d.ctypes.data, z.ctypes.data, len(s),
+           _engine(engine), max_ctas, N.stream_handle(stream))
+
+
+def ce_batch_copy(src_ptrs, dst_ptrs, sizes, batched: bool = True, stream=None) -> None:
+    s, d, z = _host_u64(src_ptrs), _host_u64(dst_ptrs), _host_u64(sizes)
+    if not (len(s) == len(d) == len(z)):
+        raise ValueError("length mismatch")
+    N.call("hv_ce_batch_copy", s.ctypes.data, d.ctypes.data, z.ctypes.data, len(s), int(batched),
+           N.stream_handle(stream))
+
+
+def _seeds_tensor(seeds, device) -> torch.Tensor:
+    arr = np.asarray([int(x) & ((1 << 64) - 1) for x in seeds], dtype=np.uint64).view(np.int64)
+    return torch.from_numpy(arr.copy()).to(device)
+
+
+def fill_content(dst_ptrs: torch.Tensor, sizes: torch.Tensor, seeds, stream=None) -> None:
+    """Write the synthetic content of each object (splitmix64 keyed by its seed)."""
+    sd = seeds if isinstance(seeds, torch.Tensor) else _seeds_tensor(seeds, dst_ptrs.device)
+    N.call("hv_fill_content", _dev_u64(dst_ptrs, "dst_ptrs"), _dev_u64(sizes, "sizes"),
+           _dev_u64(sd, "seeds"), dst_ptrs.numel(), N.stream_handle(stream))
+
+
+def digest(src_ptrs: torch.Tensor, sizes: torch.Tensor, stream=None) -> torch.Tensor:
+    out = torch.empty(src_ptrs.numel(), dtype=torch.int64, device=src_ptrs.device)
+    N.call("hv_digest", _dev_u64(src_ptrs, "src_ptrs"), _dev_u64(sizes, "sizes"), src_ptrs.numel(),
+           out.data_ptr(), N.stream_handle(stream))
+    return out
+
+
+def verify_content(src_ptrs: torch.Tensor, sizes: torch.Tensor, seeds, stream=None) -> torch.Tensor:
+    sd = seeds if isinstance(seeds, torch.Tensor) else _seeds_tensor(seeds, src_ptrs.device)
+    out = torch.empty(src_ptrs.numel(), dtype=torch.int64, device=src_ptrs.device)
+    N.call("hv_verify_content", _dev_u64(src_ptrs, "src_ptrs"), _dev_u64(sizes, "sizes"),
+           _dev_u64(sd, "seeds"), src_ptrs.numel(), out.data_ptr(), N.stream_handle(stream))
+    return out
+
+
+def ptrs_tensor(ptrs, device) -> torch.Tensor:
+    arr = np.asarray(ptrs, dtype=np.uint64).view(np.int64)
+    return torch.from_numpy(arr.copy()).to(device)
