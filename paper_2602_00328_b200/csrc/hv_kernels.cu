@@ -510,21 +510,23 @@ constexpr size_t kTmaSmem = (size_t)kTmaStages * kTmaChunk;
 
 int pick_engine(int engine) { return engine == HV_ENGINE_AUTO ? HV_ENGINE_LDG : engine; }
 
+constexpr uint64_t kUnknownChunks = ~0ull;  // device-resident sizes: fill the device
+
 int ldg_grid(int dev, uint64_t chunks, int max_ctas) {
-  const int sms = hv::sm_count(dev);
-  int per_sm = 2048 / kLdgThreads;  // 4 CTAs of 512 threads = full occupancy
-  int64_t g = (int64_t)sms * per_sm;
-  const int64_t need = (int64_t)((chunks + (kLdgThreads / 32) - 1) / (kLdgThreads / 32));
-  if (need < g) g = need;
-  if (max_ctas > 0 && g > max_ctas) g = max_ctas;
+  const uint64_t wpb = kLdgThreads / 32;
+  uint64_t g = (uint64_t)hv::sm_count(dev) * (2048 / kLdgThreads);  // full occupancy
+  if (chunks != kUnknownChunks) {
+    const uint64_t need = chunks / wpb + (chunks % wpb != 0);
+    if (need < g) g = need;
+  }
+  if (max_ctas > 0 && g > (uint64_t)max_ctas) g = (uint64_t)max_ctas;
   return (int)(g < 1 ? 1 : g);
 }
 
 int tma_grid(int dev, uint64_t chunks, int max_ctas) {
-  const int sms = hv::sm_count(dev);
-  int64_t g = sms;  // 128 KiB ring: one CTA per SM
-  if ((int64_t)chunks < g) g = (int64_t)chunks;
-  if (max_ctas > 0 && g > max_ctas) g = max_ctas;
+  uint64_t g = (uint64_t)hv::sm_count(dev);  // 128 KiB ring: one CTA per SM
+  if (chunks != kUnknownChunks && chunks < g) g = chunks;
+  if (max_ctas > 0 && g > (uint64_t)max_ctas) g = (uint64_t)max_ctas;
   return (int)(g < 1 ? 1 : g);
 }
 
@@ -593,10 +595,10 @@ int launch_descs(const uint64_t* d_src, const uint64_t* d_dst, const uint64_t* d
     o.rebase(base);
     if (is_copy && engine == HV_ENGINE_TMA) {
       res.chunk = kTmaChunk;
-      desc_copy_tma<<<tma_grid(dev, ~0ull, max_ctas), kTmaThreads, kTmaSmem, (cudaStream_t)stream>>>(res);
+      desc_copy_tma<<<tma_grid(dev, kUnknownChunks, max_ctas), kTmaThreads, kTmaSmem, (cudaStream_t)stream>>>(res);
     } else if (engine == HV_ENGINE_LDG || !is_copy) {
       res.chunk = kLdgChunk;
-      desc_op_kernel<<<ldg_grid(dev, ~0ull, max_ctas), kLdgThreads, 0, (cudaStream_t)stream>>>(res, o);
+      desc_op_kernel<<<ldg_grid(dev, kUnknownChunks, max_ctas), kLdgThreads, 0, (cudaStream_t)stream>>>(res, o);
     } else {
       return HV_E_INVALID;
     }
@@ -779,8 +781,29 @@ HV_EXPORT int hv_ce_batch_copy(const uint64_t* h_src, const uint64_t* h_dst, con
   attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
   attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
   size_t attr_idx = 0, fail_idx = 0;
+  if (stream != nullptr) {
+    HV_CUDA(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr, &attr_idx, 1, &fail_idx,
+                                 (cudaStream_t)stream));
+    return HV_OK;
+  }
+  // batched copies are rejected on the legacy NULL stream: run them on a
+  // side stream fenced by events on both sides, which keeps NULL-stream order
+  static std::mutex mu;
+  static cudaStream_t side[64] = {};
+  static cudaEvent_t before[64] = {}, after[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= 64) return HV_E_INVALID;
+  if (!side[dev]) {
+    HV_CUDA(cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking));
+    HV_CUDA(cudaEventCreateWithFlags(&before[dev], cudaEventDisableTiming));
+    HV_CUDA(cudaEventCreateWithFlags(&after[dev], cudaEventDisableTiming));
+  }
+  HV_CUDA(cudaEventRecord(before[dev], nullptr));
+  HV_CUDA(cudaStreamWaitEvent(side[dev], before[dev], 0));
   HV_CUDA(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr, &attr_idx, 1, &fail_idx,
-                               (cudaStream_t)stream));
+                               side[dev]));
+  HV_CUDA(cudaEventRecord(after[dev], side[dev]));
+  HV_CUDA(cudaStreamWaitEvent(nullptr, after[dev], 0));
   return HV_OK;
 }
 

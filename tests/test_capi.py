@@ -1,0 +1,96 @@
+"""The C-ABI library loads without a GPU, exports every symbol declared in
+include/harvest_b200.h, and its native allocator makes the reference's exact
+decisions (tests/golden/allocator.json, memalloc.py:90-138)."""
+import ctypes as C
+import json
+import os
+import random
+import re
+
+import pytest
+
+from paper_2602_00328_b200 import _native as N
+from paper_2602_00328_b200 import memalloc as M
+from oracle import harvest_oracle as O
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    text = open(os.path.join(REPO, "include", "harvest_b200.h")).read()
+    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(hv_\w+)\(", text, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = N.load()
+    syms = header_symbols()
+    assert len(syms) >= 50
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(N.exported_symbols())
+    assert lib.hv_abi_version() == 1
+
+
+def test_error_strings_and_no_device_behaviour():
+    lib = N.load()
+    assert lib.hv_error_string(0) == b"ok"
+    assert lib.hv_error_string(-2) == b"no capacity"
+    n = C.c_int(-1)
+    assert lib.hv_device_count(C.byref(n)) == 0
+    assert n.value >= 0
+
+
+def test_native_allocator_matches_reference_runs():
+    g = json.load(open(os.path.join(REPO, "tests", "golden", "allocator.json")))
+    for case in g["cases"]:
+        st = M.init_device(M.DeviceSpec(1, M.Tier.PEER_HBM, case["usable"]))
+        for kind, a, b, want in case["ops"]:
+            if kind == "alloc":
+                seg = M.alloc_best_fit(st, a)
+                assert (None if seg is None else seg.base) == want
+            else:
+                M.free_segment(st, M.Segment(a, b))
+            M.check_invariants(st)
+        assert [[s.base, s.size] for s in st.free_list] == case["free_list"]
+        assert M.allocated_bytes(st) == case["allocated_bytes"]
+
+
+def test_native_allocator_vs_oracle_random():
+    rng = random.Random(3)
+    for trial in range(20):
+        usable = rng.choice([1000, 1 << 30])
+        st = M.init_device(M.DeviceSpec(1, M.Tier.PEER_HBM, usable))
+        fl, live = [(0, usable)], []
+        for _ in range(300):
+            if live and rng.random() < 0.4:
+                base, size = live.pop(rng.randrange(len(live)))
+                M.free_segment(st, M.Segment(base, size))
+                fl = O.free_coalesce(fl, base, size)
+            else:
+                size = rng.randint(1, usable // rng.choice([5, 40, 300]))
+                seg = M.alloc_best_fit(st, size)
+                want, fl = O.best_fit(fl, size)
+                assert (None if seg is None else seg.base) == want
+                if seg is not None:
+                    live.append((seg.base, size))
+            assert [(s.base, s.size) for s in st.free_list] == fl
+
+
+def test_allocator_errors_spec():
+    # SPEC.md:47-49, 64-67
+    st = M.init_device(M.DeviceSpec(1, M.Tier.PEER_HBM, 100, reserved=20))
+    assert [(s.base, s.size) for s in st.free_list] == [(0, 80)]
+    with pytest.raises(ValueError):
+        M.init_device(M.DeviceSpec(1, M.Tier.PEER_HBM, 10, reserved=8, headroom=4))
+    with pytest.raises(M.DoubleFreeError):
+        M.free_segment(st, M.Segment(5, 3))
+    a = M.alloc_best_fit(st, 10)
+    b = M.alloc_best_fit(st, 10)
+    M.free_segment(st, a)
+    M.free_segment(st, b)
+    assert [(s.base, s.size) for s in st.free_list] == [(0, 80)]
+    with pytest.raises(M.DoubleFreeError):
+        M.free_segment(st, a)
+    with pytest.raises(ValueError):
+        M.alloc_best_fit(st, 0)
+    assert M.alloc_best_fit(st, 81) is None
