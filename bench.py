@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""Harvest-on-B200 contract benchmark: expert fetch GB/s (BASELINE.json configs[1]).
+
+Workload (config 2): Qwen1.5-MoE-A2.7B-shaped experts (24 layers x 60 experts,
+17,301,504 B each, bf16 gate+up+down), decode batch 32, top-4 routing over
+N(0,1) router logits, 100% of experts offloaded.  One step = one decode step:
+for each of the 24 layers, the distinct activated experts (~53) are fetched
+into local HBM with ONE launch of the K2 batched-fetch kernel (~22 GB/step).
+
+* N=1 (one GPU): experts live in the pinned host tier (the authoritative copy);
+  the fetch reads them over PCIe ("1 GPU (host tier only)").
+* N>1 (torchrun, one process per GPU): every rank is a compute GPU whose
+  experts were placed by its own HarvestRuntime (harvest_alloc, best-fit) in the
+  donated HBM of the N-1 other GPUs (cudaIpc pools); the fetch pulls them over
+  NVLink 5 / NVSwitch.  No collective on the data path ("scaling": "weak").
+
+``value``: device-resident descriptors, the timed region holds only the fetch
+launches.  ``e2e``: the same steps through the public fetch hook
+(ExpertFetcher.issue_fetches: host routing -> descriptors staged H2D -> launch)
+plus a per-step verification kernel whose mismatch counts are read back D2H.
+
+``--impl reference``: the reference CPU path (oracle port of the fetch, a
+memcpy gather from the host-authoritative copy) on the box's host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+GiB = 1 << 30
+METRIC = "peer-fetch GB/s"
+TOKENS, SEED = 32, 2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "ldg", "tma"])
+    ap.add_argument("--max-ctas", type=int, default=0)
+    ap.add_argument("--cpu-baseline-s", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    a.warmup = max(3, a.warmup)
+    return a
+
+
+def model():
+    from paper_2602_00328_b200.moe import QWEN15_MOE_A27B
+    return QWEN15_MOE_A27B
+
+
+def routing(m, steps, seed=SEED):
+    from paper_2602_00328_b200.moe import topk_routing
+    return topk_routing(m, TOKENS, steps, seed)
+
+
+def workload_config(m, n, source):
+    return {"workload": f"{m.name} expert fetch (BASELINE configs[1]): {m.num_layers} layers x "
+                        f"{m.num_experts} experts x {m.expert_size} B, decode batch {TOKENS}, top-{m.top_k}, "
+                        f"100% offloaded; one step = every layer's activated experts",
+            "source_tier": source, "donors_per_rank": max(0, n - 1),
+            "l2": "inputs larger than L2 (~22 GB fetched per step, 126 MB L2)",
+            "routing": f"top-{m.top_k} of N(0,1) logits, seed {SEED}"}
+
+
+# --------------------------------------------------------------------- CPU paths
+def cpu_gather_sample(m, host_buf, route_steps, seconds, threads):
+    """Oracle port of the fetch (memcpy gather of the activated experts from
+    the host-authoritative copy) on host cores, for ~``seconds``."""
+    from oracle import harvest_oracle as O
+    dst = np.empty(m.num_experts * m.expert_size, dtype=np.uint8)
+    base = host_buf.ctypes.data if isinstance(host_buf, np.ndarray) else host_buf
+    moved, t0, layers = 0, time.perf_counter(), 0
+    while True:
+        for step in route_steps:
+            for layer, ex in enumerate(step):
+                src = [base + ((layer * m.num_experts + int(e)) % (host_nexp(m, host_buf))) * m.expert_size for e in ex]
+                dp = [dst.ctypes.data + i * m.expert_size for i in range(len(ex))]
+                O.gather(src, dp, [m.expert_size] * len(ex), threads=threads)
+                moved += len(ex) * m.expert_size
+                layers += 1
+                if time.perf_counter() - t0 >= seconds:
+                    dt = time.perf_counter() - t0
+                    return moved / dt / 1e9, dt, layers, moved
+
+
+def host_nexp(m, host_buf):
+    return (host_buf.size // m.expert_size) if isinstance(host_buf, np.ndarray) else m.num_layers * m.num_experts
+
+
+def cpu_host_copy(m, n_experts):
+    """A host-resident expert table for the CPU legs (content from the oracle)."""
+    from oracle import harvest_oracle as O
+    from paper_2602_00328_b200.runtime import stable_hash64
+    buf = np.empty(n_experts * m.expert_size, dtype=np.uint8)
+    O.fill_batch([buf.ctypes.data + i * m.expert_size for i in range(n_experts)], [m.expert_size] * n_experts,
+                 [stable_hash64("expert", m.name, i // m.num_experts, i % m.num_experts) for i in range(n_experts)],
+                 threads=os.cpu_count() or 1)
+    return buf
+
+
+def run_reference(a):
+    """--impl reference: the oracle port timed on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    m = model()
+    threads = os.cpu_count() or 1
+    sample_experts = 4 * m.num_experts          # 4 layers' worth of distinct experts (4.15 GB)
+    host = cpu_host_copy(m, sample_experts)
+    routes = routing(m, a.steps + a.warmup)
+    per_step = []
+
+    def one_step(step):
+        # bounded sample of the step: its first 4 layers (the same activated sets)
+        from oracle import harvest_oracle as O
+        dst = one_step.dst
+        moved = 0
+        t0 = time.perf_counter()
+        for layer in range(4):
+            ex = step[layer]
+            src = [host.ctypes.data + (layer * m.num_experts + int(e)) * m.expert_size for e in ex]
+            dp = [dst.ctypes.data + i * m.expert_size for i in range(len(ex))]
+            O.gather(src, dp, [m.expert_size] * len(ex), threads=threads)
+            moved += len(ex) * m.expert_size
+        return moved, time.perf_counter() - t0
+
+    one_step.dst = np.empty(m.num_experts * m.expert_size, dtype=np.uint8)
+    for s in range(a.warmup):
+        one_step(routes[s])
+    moved = dt = 0.0
+    for s in range(a.warmup, a.warmup + a.steps):
+        mv, t = one_step(routes[s])
+        moved += mv
+        dt += t
+        per_step.append(t)
+    gbps = moved / dt / 1e9
+    line = {"metric": METRIC, "value": gbps, "unit": "GB/s", "impl": "reference", "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * dt / a.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic", "config": workload_config(m, 1, "host"),
+            "cpu_baseline": {"value": gbps, "unit": "GB/s", "cores": threads, "kind": "port",
+                             "sample": f"first 4 of {m.num_layers} layers of each decode step "
+                                       f"(memcpy gather, oracle/hv_oracle.c, {threads} threads)"},
+            "e2e": {"value": gbps, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    emit(line, a)
+    return 0
+
+
+# --------------------------------------------------------------------- GPU path
+def measure_pcie_h2d(dev):
+    import torch
+    from paper_2602_00328_b200.pool import HostTier
+    h = HostTier(1 << 30)
+    d = torch.empty(1 << 30, dtype=torch.uint8, device=f"cuda:{dev}")
+    s = torch.cuda.Stream(dev)
+    best = 0.0
+    with torch.cuda.stream(s):
+        src = torch.from_numpy(h.view())
+        for i in range(6):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            d.copy_(src, non_blocking=True)
+            e1.record(s)
+            e1.synchronize()
+            if i:
+                best = max(best, (1 << 30) / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    del src
+    h.close()
+    return best
+
+
+def emit(line, a):
+    s = json.dumps(line)
+    print(s, flush=True)
+    if a.out:
+        with open(a.out, "a") as f:
+            f.write(s + "\n")
+
+
+def load_traffic():
+    p = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return {}
+    return {}
+
+
+def run_b200(a):
+    import torch
+    import torch.distributed as dist
+    from paper_2602_00328_b200 import _native as N
+    from paper_2602_00328_b200 import fetch as F
+    from paper_2602_00328_b200.memalloc import Tier
+    from paper_2602_00328_b200.moe import ExpertFetcher, ExpertResidency, ExpertStore, expert_content
+    from paper_2602_00328_b200.pool import HostTier, PeerPool
+    from paper_2602_00328_b200.runtime import AllocationHints, Durability
+    from paper_2602_00328_b200.system import HarvestSystem
+    from tools.clocks import ClockSampler
+
+    world = a.gpus
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = local
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+    m = model()
+    L, E, S = m.num_layers, m.num_experts, m.expert_size
+    routes = routing(m, a.warmup + a.steps, seed=SEED + 1000 * rank)
+    imported, host_tier = [], None
+
+    if world == 1:
+        source = "host"
+        host_tier = HostTier(L * E * S)
+        sysm = HarvestSystem(dev, host_tier=host_tier, local_bytes=1, engine=a.engine, max_ctas=a.max_ctas,
+                             log_transfers=False)
+        store = ExpertStore(m, sysm.host_id, host_tier)
+        store.fill_host(dev)
+        residency = ExpertResidency(m)       # every expert HOST_DRAM
+    else:
+        source = "peer"
+        others = [r for r in range(world) if r != rank]
+        per_reader = math.ceil(L * E / (world - 1)) * S
+        my_pool = PeerPool(dev, per_reader * (world - 1), readers=[dev], mode="ipc")
+        handles = [None] * world
+        dist.all_gather_object(handles, my_pool.export_ipc())
+        views = {}
+        for i, d in enumerate(others, start=1):
+            p = PeerPool.import_ipc(handles[d], d, per_reader * (world - 1), dev)
+            imported.append(p)
+            # my section of donor d: my position among d's readers
+            pos = [r for r in range(world) if r != d].index(rank)
+            views[i] = p.view(pos * per_reader, per_reader)
+        sysm = HarvestSystem(dev, pools=views, local_bytes=1, engine=a.engine, max_ctas=a.max_ctas,
+                             log_transfers=False)
+        store = ExpertStore(m, sysm.host_id, None)
+        residency = ExpertResidency(m)
+        rt = sysm.runtime
+        # placement: the runtime's own harvest_alloc decisions (runtime.py:198-235);
+        # the copy-in is the synthetic-content fill written over NVLink
+        ptrs, seeds = [], []
+        for layer in range(L):
+            for e in range(E):
+                h = rt.harvest_alloc(S, AllocationHints(durability=Durability.BACKED, client_id="moe"))
+                assert h is not None, "donor capacity exhausted"
+                rt.set_tag(h, ("expert", layer, e))
+                rt.write_peer(h, ("expert", layer, e), expert_content(m, layer, e))
+                residency.set_tier(layer, e, Tier.PEER_HBM, h)
+                ptrs.append(rt.address(h))
+                seeds.append(expert_content(m, layer, e))
+        for i in range(0, len(ptrs), 120):
+            F.fill_content(F.ptrs_tensor(ptrs[i:i + 120], f"cuda:{dev}"),
+                           F.ptrs_tensor([S] * len(ptrs[i:i + 120]), f"cuda:{dev}"), seeds[i:i + 120])
+        torch.cuda.synchronize()
+        dist.barrier()
+
+    fetcher = ExpertFetcher(sysm.runtime, m, residency, store)
+    stream_h = sysm.engine.stream
+    stream = torch.cuda.ExternalStream(stream_h, device=f"cuda:{dev}")
+    staging = [torch.empty(E * S, dtype=torch.uint8, device=f"cuda:{dev}") for _ in range(2)]
+    stage_ptrs = [np.array([b.data_ptr() + i * S for i in range(E)], dtype=np.uint64) for b in staging]
+
+    # ---- device-resident descriptors for the kernel-only (value) loop
+    desc = []
+    for s in range(a.warmup + a.steps):
+        row = []
+        for layer in range(L):
+            ex = routes[s][layer]
+            src = fetcher.src_addr[layer, ex]
+            dst = stage_ptrs[layer % 2][:len(ex)]
+            row.append((F.ptrs_tensor(src, f"cuda:{dev}"), F.ptrs_tensor(dst, f"cuda:{dev}"),
+                        F.ptrs_tensor([S] * len(ex), f"cuda:{dev}"), len(ex) * S))
+        desc.append(row)
+    torch.cuda.synchronize()
+
+    def value_step(s, evs=None):
+        for layer, (sp, dp, sz, nb) in enumerate(desc[s]):
+            if evs is not None:
+                evs[layer][0].record(stream)
+            F.batch_copy(sp, dp, sz, engine=a.engine, max_ctas=a.max_ctas, stream=stream_h)
+            if evs is not None:
+                evs[layer][1].record(stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for s in range(a.warmup):
+        value_step(s)
+    torch.cuda.synchronize()
+    launches0 = N.launch_count()
+    step_events = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    for _ in range(L)] for _ in range(a.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        t0.record(stream)
+        for k in range(a.steps):
+            value_step(a.warmup + k, step_events[k])
+        t1.record(stream)
+        t1.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    launches = N.launch_count() - launches0
+    dt = max_over_ranks(t0.elapsed_time(t1) * 1e-3)
+    my_bytes = sum(nb for s in range(a.warmup, a.warmup + a.steps) for (_, _, _, nb) in desc[s])
+    total_bytes = my_bytes * world
+    value = total_bytes / dt / 1e9
+    launch_ms = [step_events[k][l][0].elapsed_time(step_events[k][l][1])
+                 for k in range(a.steps) for l in range(L)]
+    bytes_per_launch = my_bytes / (a.steps * L)
+    achieved = bytes_per_launch / (statistics.mean(launch_ms) * 1e-3) / 1e9
+
+    # ---- e2e through the public fetch hook
+    seeds_dev = {}
+
+    def e2e_step(s, check):
+        fb = None
+        for layer in range(L):
+            ex = routes[s][layer]
+            fb = fetcher.issue_fetches(layer, ex, stage_ptrs[layer % 2][:len(ex)])
+        if check:  # verify the last layer against the generator, read counts back
+            layer = L - 1
+            ex = routes[s][layer]
+            key = (s, layer)
+            if key not in seeds_dev:
+                seeds_dev[key] = F._seeds_tensor([expert_content(m, layer, int(e)) for e in ex], f"cuda:{dev}")
+            with torch.cuda.stream(stream):
+                bad = F.verify_content(F.ptrs_tensor(stage_ptrs[layer % 2][:len(ex)], f"cuda:{dev}"),
+                                       F.ptrs_tensor([S] * len(ex), f"cuda:{dev}"), seeds_dev[key],
+                                       stream=stream_h)
+                host_bad = bad.to("cpu", non_blocking=False)
+            return int(host_bad.sum()), len(ex)
+        return 0, 0
+
+    for s in range(a.warmup):
+        e2e_step(s, True)
+    sysm.loop.run()
+    barrier()
+    torch.cuda.synchronize()
+    mism = 0
+    d2h = h2d = 0
+    w0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(a.steps):
+        s = a.warmup + k
+        bad, n_last = e2e_step(s, True)
+        mism += bad
+        d2h += 8 * n_last
+        h2d += sum(24 * len(routes[s][layer]) for layer in range(L))
+        sysm.loop.poll()
+    e1.record(stream)
+    e1.synchronize()
+    sysm.loop.run()
+    wall = time.perf_counter() - w0
+    barrier()
+    e2e_dt = max_over_ranks(max(wall, e0.elapsed_time(e1) * 1e-3))
+    e2e_value = total_bytes / e2e_dt / 1e9
+    mism_all = max_over_ranks(float(mism))
+
+    if rank == 0:
+        if source == "host":
+            peak = measure_pcie_h2d(dev)
+            roof = {"bound": "pcie", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak if peak else None,
+                    "peak_source": "measured in this run: pinned host->device cudaMemcpyAsync, 1 GiB, best of 5"}
+        else:
+            peak = 770.0
+            roof = {"bound": "nvlink", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak,
+                    "peak_source": "B200_PROFILING.md fallback: measured peer copy 770 GB/s per direction "
+                                   "(900 nominal)"}
+        tr = load_traffic().get("batch_copy_" + source)
+        roof["traffic"] = tr
+        roof["bytes_per_launch"] = bytes_per_launch
+        roof["mean_launch_ms"] = statistics.mean(launch_ms)
+        cpu = None
+        if not a.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            hc = cpu_host_copy(m, 4 * E)
+            gbps, secs, layers, moved = cpu_gather_sample(m, hc, routes[a.warmup:], a.cpu_baseline_s, threads)
+            cpu = {"value": gbps, "unit": "GB/s", "cores": threads, "kind": "port",
+                   "sample": f"{layers} layer-fetches ({moved / 1e9:.1f} GB) of the same routing, memcpy gather "
+                             f"from a host expert table (oracle/hv_oracle.c), {secs:.1f} s, {threads} threads"}
+        line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+                "config": {**workload_config(m, world, source), "engine": a.engine,
+                           "parallelism": f"{world} compute GPU(s)" + (f", each reading N-1={world - 1} donors"
+                                                                       if world > 1 else "")},
+                "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": h2d // a.steps,
+                        "d2h_bytes_per_step": d2h // a.steps, "verify_mismatched_words": int(mism_all)},
+                "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
+                "clocks": clk.summary(),
+                "latency_ms_per_layer_fetch": statistics.median(launch_ms)}
+        emit(line, a)
+    barrier()
+    sysm.close()
+    for p in imported:
+        p.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    return run_b200(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

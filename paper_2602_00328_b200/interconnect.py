@@ -254,8 +254,10 @@ class CudaTransferEngine:
         return self.launch_raw(src, dst, size, reqs, on_completes, initiator, handle_keys)
 
     def launch_raw(self, src: np.ndarray, dst: np.ndarray, size: np.ndarray, reqs=None,
-                   on_completes=None, initiator: str = "app", handle_keys=None):
-        """Launch one batched fetch over raw device addresses (host arrays)."""
+                   on_completes=None, initiator: str = "app", handle_keys=None, callbacks=()):
+        """Launch one batched fetch over raw device addresses (host arrays).
+        ``callbacks`` (no-argument... called with None) run at completion too;
+        the batch's event is left in ``self.last_event`` until it is polled."""
         n = len(src)
         N.call("hv_swap_blocks_batch", src.ctypes.data, dst.ctypes.data, size.ctypes.data, n,
                self.engine, self.max_ctas, self.stream)
@@ -272,8 +274,11 @@ class CudaTransferEngine:
                 seq = self.sim.record("transfer_start", start=now, **fields).seq if self.log_transfers else -1
                 xfer = Transfer(r, self.topology.link_between(r.src[0], r.dst[0]), now, None, seq)
                 items.append((xfer, on_completes[i] if on_completes else None, fields))
+        xfers = [x for x, _, _ in items]
+        items.extend((None, cb, None) for cb in callbacks)
         self._pending.append((ev, items))
-        return [x for x, _, _ in items]
+        self.last_event = ev
+        return xfers
 
     def launch_pages(self, src_page_ptrs_dev: int, n_pages: int, page_bytes: int, dst_base: int = 0,
                      dst_page_ptrs_dev: int = 0, callbacks=()):

@@ -65,6 +65,13 @@ class PeerPool:
         N.call("hv_pool_import_ipc", buf, donor, nbytes, reader, C.byref(p))
         return cls(donor, nbytes, mode="ipc", _handle=p)
 
+    def view(self, offset: int, nbytes: int) -> "PoolView":
+        """A window of a pre-backed (IPC) pool, e.g. one reader's section of a
+        donor slab shared by several compute processes."""
+        if offset + nbytes > self.nbytes:
+            raise ValueError("view outside the pool")
+        return PoolView(self, offset, nbytes)
+
     def close(self) -> None:
         if self._p:
             N.call("hv_pool_destroy", self._p)
@@ -75,6 +82,32 @@ class PeerPool:
             self.close()
         except Exception:
             pass
+
+
+class PoolView:
+    """Section [offset, offset+nbytes) of an IPC pool; commit/decommit are
+    no-ops because IPC slabs are backed for their whole lifetime."""
+
+    def __init__(self, pool: PeerPool, offset: int, nbytes: int):
+        self.pool, self.offset = pool, offset
+        self.donor, self.mode = pool.donor, "ipc-view"
+        self.va, self.nbytes, self.chunk_bytes = pool.va + offset, nbytes, nbytes
+
+    def commit(self, offset: int, nbytes: int) -> None:
+        pass
+
+    def decommit(self, offset: int, nbytes: int) -> None:
+        pass
+
+    @property
+    def committed_bytes(self) -> int:
+        return self.nbytes
+
+    def address(self, offset: int) -> int:
+        return self.va + offset
+
+    def close(self) -> None:
+        pass
 
 
 class HostTier:
