@@ -48,11 +48,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--engine", default="auto", choices=["auto", "ldg", "tma"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "ldg", "ldg256", "tma"])
     ap.add_argument("--max-ctas", type=int, default=0)
     ap.add_argument("--cpu-baseline-s", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     a = ap.parse_args()
     a.warmup = max(3, a.warmup)
     return a
@@ -217,10 +218,17 @@ def run_b200(a):
     world = a.gpus
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    dev = local
+    # HV_DEVICE_MAP="0,0" runs several ranks on one GPU (tests of the
+    # multi-process IPC path on a single-GPU box; use --dist-backend gloo)
+    dmap = os.environ.get("HV_DEVICE_MAP")
+    dev = int(dmap.split(",")[local]) if dmap else local
     torch.cuda.set_device(dev)
+    backend = a.dist_backend
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+        else:
+            dist.init_process_group(backend)
     m = model()
     L, E, S = m.num_layers, m.num_experts, m.expert_size
     routes = routing(m, a.warmup + a.steps, seed=SEED + 1000 * rank)
@@ -305,7 +313,7 @@ def run_b200(a):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 

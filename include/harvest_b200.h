@@ -152,6 +152,7 @@ int hv_stream_wait_event(void* stream, void* event);
 #define HV_ENGINE_AUTO 0
 #define HV_ENGINE_LDG 1  /* SM-issued 128-bit ld.global.nc / st.global, warp per 4 KiB chunk */
 #define HV_ENGINE_TMA 2  /* cp.async.bulk global->smem->global ring, one issuing lane per CTA */
+#define HV_ENGINE_LDG256 3 /* LDG with the L2::256B sector-promotion hint (larger remote reads) */
 
 /* K1: block-table-indexed KV-page gather.  Page i is copied from
  * d_src_page_ptrs[i] to d_dst_page_ptrs[i] (or, when d_dst_page_ptrs is NULL,

@@ -21,7 +21,8 @@ HV_E_NOMEM = -5
 ENGINE_AUTO = 0
 ENGINE_LDG = 1
 ENGINE_TMA = 2
-ENGINES = {"auto": ENGINE_AUTO, "ldg": ENGINE_LDG, "tma": ENGINE_TMA}
+ENGINE_LDG256 = 3
+ENGINES = {"auto": ENGINE_AUTO, "ldg": ENGINE_LDG, "tma": ENGINE_TMA, "ldg256": ENGINE_LDG256}
 
 POOL_VMM = 0
 POOL_IPC = 1

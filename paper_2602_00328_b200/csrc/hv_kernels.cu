@@ -108,6 +108,20 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
                : "l"(p));
   return r;
 }
+// same load with an L2 256-byte sector-promotion hint: the L2 fetches whole
+// 256 B blocks, i.e. larger read requests over PCIe / NVLink
+__device__ __forceinline__ uint4 ld_stream256(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+template <bool kL2Hint>
+__device__ __forceinline__ uint4 ld_src(const void* p) {
+  if constexpr (kL2Hint) return ld_stream256(p);
+  else return ld_stream(p);
+}
 __device__ __forceinline__ void st_stream(void* p, const uint4& v) {
   asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w)
@@ -252,12 +266,13 @@ struct DescResolver {
 // ---------------------------------------------------------------------------
 // per-chunk operations (warp-cooperative)
 
+template <bool kL2Hint = false>
 __device__ __forceinline__ void copy_chunk_ldg(const ChunkRef& r, uint32_t lane) {
   const bool aligned = ((reinterpret_cast<uintptr_t>(r.src) | reinterpret_cast<uintptr_t>(r.dst)) & 15) == 0;
   if (aligned && r.len == kLdgChunk) {
     uint4 v[kLdgUnroll];
 #pragma unroll
-    for (int j = 0; j < kLdgUnroll; ++j) v[j] = ld_stream(r.src + (j * 32 + lane) * 16);
+    for (int j = 0; j < kLdgUnroll; ++j) v[j] = ld_src<kL2Hint>(r.src + (j * 32 + lane) * 16);
 #pragma unroll
     for (int j = 0; j < kLdgUnroll; ++j) st_stream(r.dst + (j * 32 + lane) * 16, v[j]);
     return;
@@ -265,7 +280,7 @@ __device__ __forceinline__ void copy_chunk_ldg(const ChunkRef& r, uint32_t lane)
   uint32_t done = 0;
   if (aligned) {
     const uint32_t nvec = r.len >> 4;
-    for (uint32_t v = lane; v < nvec; v += 32) st_stream(r.dst + v * 16, ld_stream(r.src + v * 16));
+    for (uint32_t v = lane; v < nvec; v += 32) st_stream(r.dst + v * 16, ld_src<kL2Hint>(r.src + v * 16));
     done = nvec << 4;
   }
   for (uint32_t b = done + lane; b < r.len; b += 32) r.dst[b] = r.src[b];
@@ -286,9 +301,13 @@ __device__ __forceinline__ void warp_loop(const Res& res, uint32_t total, Op op,
   }
 }
 
-struct CopyOp {
-  __device__ __forceinline__ void operator()(const ChunkRef& r, uint32_t lane) const { copy_chunk_ldg(r, lane); }
+template <bool kL2Hint>
+struct CopyOpT {
+  __device__ __forceinline__ void operator()(const ChunkRef& r, uint32_t lane) const {
+    copy_chunk_ldg<kL2Hint>(r, lane);
+  }
 };
+using CopyOp = CopyOpT<false>;
 
 // content ops work on 8-byte words; objects must start 8-byte aligned
 struct FillOp {
@@ -359,10 +378,10 @@ struct VerifyOp {
 // ---------------------------------------------------------------------------
 // LDG-engine kernels
 
-template <bool kTable>
+template <bool kTable, bool kL2Hint>
 __global__ void __launch_bounds__(kLdgThreads) page_copy_ldg(PageResolver<kTable> res) {
   const uint32_t total = res.setup(nullptr);
-  warp_loop(res, total, CopyOp{}, nullptr);
+  warp_loop(res, total, CopyOpT<kL2Hint>{}, nullptr);
 }
 
 template <typename Op>
@@ -559,12 +578,16 @@ int launch_pages(PageResolver<kTable> res, int engine, int max_ctas, void* strea
     const uint64_t total = (uint64_t)res.n_pages * res.chunks_per_page;
     if (total >= 0xffffffffull) return HV_E_INVALID;
     page_copy_tma<kTable><<<tma_grid(dev, total, max_ctas), kTmaThreads, kTmaSmem, (cudaStream_t)stream>>>(res);
-  } else if (engine == HV_ENGINE_LDG) {
+  } else if (engine == HV_ENGINE_LDG || engine == HV_ENGINE_LDG256) {
     res.chunk = kLdgChunk;
     res.chunks_per_page = (uint32_t)((res.page_bytes + kLdgChunk - 1) / kLdgChunk);
     const uint64_t total = (uint64_t)res.n_pages * res.chunks_per_page;
     if (total >= 0xffffffffull) return HV_E_INVALID;
-    page_copy_ldg<kTable><<<ldg_grid(dev, total, max_ctas), kLdgThreads, 0, (cudaStream_t)stream>>>(res);
+    const int g = ldg_grid(dev, total, max_ctas);
+    if (engine == HV_ENGINE_LDG256)
+      page_copy_ldg<kTable, true><<<g, kLdgThreads, 0, (cudaStream_t)stream>>>(res);
+    else
+      page_copy_ldg<kTable, false><<<g, kLdgThreads, 0, (cudaStream_t)stream>>>(res);
   } else {
     return HV_E_INVALID;
   }
@@ -596,6 +619,10 @@ int launch_descs(const uint64_t* d_src, const uint64_t* d_dst, const uint64_t* d
     if (is_copy && engine == HV_ENGINE_TMA) {
       res.chunk = kTmaChunk;
       desc_copy_tma<<<tma_grid(dev, kUnknownChunks, max_ctas), kTmaThreads, kTmaSmem, (cudaStream_t)stream>>>(res);
+    } else if (is_copy && engine == HV_ENGINE_LDG256) {
+      res.chunk = kLdgChunk;
+      desc_op_kernel<<<ldg_grid(dev, kUnknownChunks, max_ctas), kLdgThreads, 0, (cudaStream_t)stream>>>(
+          res, CopyOpT<true>{});
     } else if (engine == HV_ENGINE_LDG || !is_copy) {
       res.chunk = kLdgChunk;
       desc_op_kernel<<<ldg_grid(dev, kUnknownChunks, max_ctas), kLdgThreads, 0, (cudaStream_t)stream>>>(res, o);

@@ -1,0 +1,45 @@
+"""Short, ncu-friendly driver: a few launches of each fetch kernel at the
+bench shapes.  Usage: python tools/profile_target.py [host|hbm|kv] [engine]"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2602_00328_b200 import fetch as F  # noqa: E402
+from paper_2602_00328_b200.pool import HostTier  # noqa: E402
+
+
+def main():
+    what = sys.argv[1] if len(sys.argv) > 1 else "host"
+    eng = sys.argv[2] if len(sys.argv) > 2 else "ldg"
+    reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    dev = "cuda:0"
+    if what in ("host", "hbm"):
+        S, n = 17_301_504, 53
+        if what == "host":
+            tier = HostTier(n * S)
+            base = tier.device_address()
+        else:
+            buf = torch.empty(n * S, dtype=torch.uint8, device=dev)
+            base = buf.data_ptr()
+        dst = torch.empty(n * S, dtype=torch.uint8, device=dev)
+        sp = F.ptrs_tensor([base + i * S for i in range(n)], dev)
+        dp = F.ptrs_tensor([dst.data_ptr() + i * S for i in range(n)], dev)
+        sz = F.ptrs_tensor([S] * n, dev)
+        for _ in range(reps):
+            F.batch_copy(sp, dp, sz, engine=eng)
+    else:  # KV config 1: 1024 pages x 64 KiB from 4096 HBM slots
+        page, npg, nslots = 65536, 1024, 4096
+        slots = torch.empty(nslots * page, dtype=torch.uint8, device=dev)
+        perm = np.random.default_rng(1).permutation(nslots)[:npg]
+        sp = F.ptrs_tensor([slots.data_ptr() + int(p) * page for p in perm], dev)
+        dst = torch.empty(npg * page, dtype=torch.uint8, device=dev)
+        for _ in range(reps):
+            F.kv_gather(sp, page, dst=dst, engine=eng)
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main()
