@@ -68,6 +68,8 @@ class EventLog:
 
 
 class _LoopBase:
+    wall_clock = False
+
     def __init__(self):
         self._queue: list[tuple[float, int, tuple]] = []
         self._counter = itertools.count()
@@ -80,11 +82,17 @@ class _LoopBase:
     def schedule(self, delay: float, fn, *args) -> int:
         if delay < 0:
             raise ValueError(f"negative delay {delay}")
-        return self.schedule_at(self.now + delay, fn, *args)
+        return self._push(self.now + delay, fn, args)
 
     def schedule_at(self, t: float, fn, *args) -> int:
-        if t < self.now - 1e-12:
-            raise ValueError(f"cannot schedule at {t} before now {self.now}")
+        now = self.now
+        if t < now:
+            if not self.wall_clock:
+                raise ValueError(f"cannot schedule at {t} before now {now}")
+            t = now  # wall time moved on between computing t and this call
+        return self._push(t, fn, args)
+
+    def _push(self, t: float, fn, args) -> int:
         seq = self.next_seq()
         heapq.heappush(self._queue, (t, seq, (fn, args)))
         return seq
@@ -122,6 +130,8 @@ class VirtualLoop(_LoopBase):
 
 class DeviceLoop(_LoopBase):
     """Wall-clock loop.  ``now`` is seconds since construction."""
+
+    wall_clock = True
 
     def __init__(self):
         super().__init__()

@@ -1,0 +1,454 @@
+"""KV-cache offload over Harvest: block table, append/evict/reload, revocation
+fallback, and the block-table-indexed page gather (K1).
+
+The reference ships no KV code; its contract is SPEC.md:367-460 (module
+``kv_sim``): BlockTable (:380-383), OffloadPolicy (:384-387), append_kv
+(:390-398), evict (:399-407), reload (:408-416), resolve_fallback (:417-425),
+reload_latency_experiment (:426-434); defaults: 16-token blocks (:444), Lossy
+durability (:447).  PAPER.md §5.2 (lines 308-314) describes the vLLM
+integration it models (KVOffloadManager + OffloadingHandler).
+
+B200 layout.  A page is one layer of one 16-token block, K and V:
+``block_tokens * kv_heads * head_dim * 2 * dtype_bytes`` (Llama-3-8B: 65,536 B).
+Every tier stores pages layer-major, ``[layer][slot]``, like vLLM's per-layer
+KV tensors, so page (l, b) of block b lives at ``base[b] + l * stride[b]``:
+
+  local HBM   base = cache + slot*page        stride = local_blocks*page
+  peer slab   base = slab_va + slot*page      stride = slab_blocks*page
+  host tier   base = host_alias + slot*page   stride = host_blocks*page
+
+Peer memory is taken in slabs of ``slab_blocks`` blocks through
+``harvest_alloc`` (one revocable handle per slab, not per 64 KiB page); a slab
+revocation invalidates its blocks: Backed blocks fall back to their host copy,
+Lossy blocks become NotMaterialized (recompute).  Every data movement of a call
+(all pages of all blocks, all layers) is ONE K1 launch with per-page
+source/destination pointers resolved from the table on the host (vectorised)
+and uploaded once.
+"""
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .interconnect import LinkSpec, transfer_time
+from .pool import HostTier
+from .runtime import AllocationHints, Durability, HarvestHandle, RevokeReason, stable_hash64
+
+
+class KVTier(enum.Enum):
+    LOCAL_HBM = "LocalHBM"
+    PEER_HBM = "PeerHBM"
+    HOST_DRAM = "HostDRAM"
+    NOT_MATERIALIZED = "NotMaterialized"
+
+
+_T = {KVTier.LOCAL_HBM: 0, KVTier.PEER_HBM: 1, KVTier.HOST_DRAM: 2, KVTier.NOT_MATERIALIZED: 3}
+
+
+class TierExhausted(Exception):
+    """Neither the peer tier nor the host tier can hold a block."""
+
+
+@dataclass(frozen=True)
+class KVModelSpec:
+    """SPEC.md:372-375 plus the dense shape that defines a page."""
+    name: str
+    num_layers: int
+    kv_heads: int
+    head_dim: int
+    dtype_bytes: int = 2
+    block_tokens: int = 16
+    recompute_time_per_entry: float = 1.0
+
+    @property
+    def page_bytes(self) -> int:
+        return self.block_tokens * self.kv_heads * self.head_dim * 2 * self.dtype_bytes
+
+    @property
+    def bytes_per_entry(self) -> int:
+        return self.num_layers * self.kv_heads * self.head_dim * 2 * self.dtype_bytes
+
+    @property
+    def block_bytes(self) -> int:
+        return self.num_layers * self.page_bytes
+
+
+LLAMA3_8B = KVModelSpec("llama-3-8b", num_layers=32, kv_heads=8, head_dim=128)
+assert LLAMA3_8B.page_bytes == 65536 and LLAMA3_8B.bytes_per_entry == 131072
+
+
+class EvictionOrder(enum.Enum):
+    LRU = "LRU"
+    FIFO = "FIFO"
+    SEQUENCE_TAIL = "SequenceTail"
+
+
+@dataclass
+class OffloadPolicy:
+    """SPEC.md:384-387."""
+    order: EvictionOrder = EvictionOrder.LRU
+    local_watermark: float = 1.0
+
+    def validate(self) -> None:
+        if not 0.0 < self.local_watermark <= 1.0:
+            raise ValueError("watermark must be in (0, 1]")
+
+
+@dataclass
+class KVBlock:
+    """SPEC.md:376-383 (one BlockTable entry)."""
+    block_id: int
+    sequence_id: int
+    index: int
+    entries: int
+    durability: Durability
+    tier: KVTier = KVTier.LOCAL_HBM
+    slot: int = -1                 # local slot, peer slab slot, or host slot
+    slab: int = -1                 # peer slab index when PEER_HBM
+    host_slot: int | None = None   # authoritative host copy (Backed, or host-resident)
+    last_access: float = 0.0
+    created: int = 0
+
+
+def kv_seed(layer: int, seq: int, block_index: int) -> int:
+    """Content identity of page (layer, seq, block) — stable_hash64 of its tag."""
+    return stable_hash64("kv", layer, seq, block_index)
+
+
+@dataclass
+class _Slab:
+    handle: HarvestHandle
+    va: int
+    free: list = field(default_factory=list)
+    blocks: dict = field(default_factory=dict)  # slot -> block_id
+    live: bool = True
+
+
+class KVCacheManager:
+    """Block table + offloading handler for one compute GPU (a HarvestSystem)."""
+
+    def __init__(self, system, model: KVModelSpec, local_blocks: int, host_blocks: int,
+                 policy: OffloadPolicy | None = None, slab_blocks: int = 32,
+                 durability: Durability = Durability.LOSSY, engine: str = "auto", max_ctas: int = 0):
+        self.sys = system
+        self.rt = system.runtime
+        self.m = model
+        self.policy = policy or OffloadPolicy()
+        self.policy.validate()
+        self.default_durability = durability
+        self.engine = N.ENGINES[engine]
+        self.max_ctas = max_ctas
+        self.dev = f"cuda:{system.compute}"
+        self.page = model.page_bytes
+        self.L = model.num_layers
+        self.local_blocks, self.host_blocks, self.slab_blocks = local_blocks, host_blocks, slab_blocks
+        self.cache = torch.empty((self.L, local_blocks, self.page), dtype=torch.uint8, device=self.dev)
+        self.host = HostTier(max(1, host_blocks) * self.L * self.page)
+        self.local_free = list(range(local_blocks - 1, -1, -1))
+        self.host_free = list(range(host_blocks - 1, -1, -1))
+        self.table: dict[int, KVBlock] = {}
+        self.slabs: list[_Slab] = []
+        self.seq_blocks: dict[int, list[int]] = {}
+        self._next_id = 0
+        self._created = 0
+        self.stream = system.engine.stream
+        self.recomputed = 0
+        self.stats = {"evict_peer": 0, "evict_host": 0, "reload_peer": 0, "reload_host": 0, "recompute": 0}
+
+    # ------------------------------------------------------------ addressing
+    def _page_base(self, b: KVBlock) -> tuple[int, int]:
+        if b.tier == KVTier.LOCAL_HBM:
+            return self.cache.data_ptr() + b.slot * self.page, self.local_blocks * self.page
+        if b.tier == KVTier.PEER_HBM:
+            return self.slabs[b.slab].va + b.slot * self.page, self.slab_blocks * self.page
+        if b.tier == KVTier.HOST_DRAM:
+            return self.host.device_address(b.host_slot * self.page), self.host_blocks * self.page
+        raise ValueError(f"block {b.block_id} is not materialized")
+
+    def _host_base(self, host_slot: int) -> tuple[int, int]:
+        return self.host.device_address(host_slot * self.page), self.host_blocks * self.page
+
+    def _pages(self, bases: np.ndarray, strides: np.ndarray, layers=None) -> np.ndarray:
+        """Page addresses [len(layers) x n_blocks] flattened layer-major."""
+        layers = np.arange(self.L, dtype=np.uint64) if layers is None else np.asarray(layers, dtype=np.uint64)
+        return (bases[None, :] + layers[:, None] * strides[None, :]).reshape(-1)
+
+    def _launch_pages(self, src: np.ndarray, dst: np.ndarray, handles=(), on_done=None) -> None:
+        """One K1 launch over per-page pointers; drain tracked on `handles`."""
+        if len(src) == 0:
+            if on_done:
+                on_done()
+            return
+        both = torch.from_numpy(np.concatenate([src, dst]).view(np.int64)).pin_memory()
+        # stream-ordered upload of the pointer arrays on the fetch stream
+        dbuf = torch.empty(both.numel(), dtype=torch.int64, device=self.dev)
+        N.call("hv_memcpy_h2d", dbuf.data_ptr(), both.data_ptr(), both.numel() * 8, self.stream)
+        batch = self.rt.begin_reads(list(handles)) if handles else None
+        n = len(src)
+
+        def _done(_x, batch=batch, keep=(both, dbuf)):
+            if batch is not None:
+                self.rt.end_reads(batch)
+            if on_done:
+                on_done()
+
+        self.sys.engine.launch_pages(dbuf.data_ptr(), n, self.page, dst_page_ptrs_dev=dbuf.data_ptr() + 8 * n,
+                                     callbacks=[_done])
+
+    # ------------------------------------------------------------ append
+    def append_kv(self, sequence_id: int, tokens: int, durability: Durability | None = None) -> list[int]:
+        """Fill the sequence's open tail block, then new LocalHBM blocks; new
+        pages get their content (the KV the decode step produced)."""
+        if tokens <= 0:
+            raise ValueError("tokens must be > 0")
+        dur = durability or self.default_durability
+        blocks = self.seq_blocks.setdefault(sequence_id, [])
+        touched = []
+        now = self.sys.loop.now
+        while tokens > 0:
+            tail = self.table[blocks[-1]] if blocks else None
+            if tail is not None and tail.entries < self.m.block_tokens:
+                if tail.tier != KVTier.LOCAL_HBM:
+                    self.reload([tail.block_id])
+                take = min(tokens, self.m.block_tokens - tail.entries)
+                tail.entries += take
+                tail.last_access = now
+                tokens -= take
+                touched.append(tail.block_id)
+                continue
+            slot = self._take_local_slot()
+            bid = self._next_id
+            self._next_id += 1
+            self._created += 1
+            take = min(tokens, self.m.block_tokens)
+            b = KVBlock(bid, sequence_id, len(blocks), take, dur, KVTier.LOCAL_HBM, slot=slot, last_access=now,
+                        created=self._created)
+            self.table[bid] = b
+            blocks.append(bid)
+            tokens -= take
+            touched.append(bid)
+            self._materialize([b])
+        return touched
+
+    def _materialize(self, blocks: list[KVBlock]) -> None:
+        """Write the blocks' synthetic KV content into their local slots."""
+        if not blocks:
+            return
+        ptrs, seeds = [], []
+        for b in blocks:
+            base, stride = self._page_base(b)
+            for layer in range(self.L):
+                ptrs.append(base + layer * stride)
+                seeds.append(kv_seed(layer, b.sequence_id, b.index))
+        from . import fetch as F
+        torch.cuda.synchronize(self.sys.compute)  # slots may be targets of pending copies
+        F.fill_content(F.ptrs_tensor(ptrs, self.dev), F.ptrs_tensor([self.page] * len(ptrs), self.dev), seeds)
+        torch.cuda.synchronize(self.sys.compute)
+
+    def _local_used(self) -> int:
+        return self.local_blocks - len(self.local_free)
+
+    def _take_local_slot(self) -> int:
+        limit = int(self.policy.local_watermark * self.local_blocks)
+        if self._local_used() + 1 > limit or not self.local_free:
+            self.evict(self.m.block_bytes * max(1, self._local_used() + 1 - limit))
+        if not self.local_free:
+            raise TierExhausted("local HBM has no free KV slot after eviction")
+        return self.local_free.pop()
+
+    # ------------------------------------------------------------ evict
+    def _eviction_order(self) -> list[KVBlock]:
+        local = [b for b in self.table.values() if b.tier == KVTier.LOCAL_HBM]
+        if self.policy.order == EvictionOrder.LRU:
+            local.sort(key=lambda b: (b.last_access, b.created))
+        elif self.policy.order == EvictionOrder.FIFO:
+            local.sort(key=lambda b: b.created)
+        else:  # sequence tail: the newest blocks of each sequence first
+            local.sort(key=lambda b: (-b.index, b.sequence_id))
+        return local
+
+    def _peer_slot(self, durability: Durability) -> tuple[int, int] | None:
+        for i, s in enumerate(self.slabs):
+            if s.live and s.free:
+                return i, s.free.pop()
+        h = self.rt.harvest_alloc(self.slab_blocks * self.L * self.page,
+                                  AllocationHints(durability=durability, client_id="kv"))
+        if h is None:
+            return None
+        idx = len(self.slabs)
+        slab = _Slab(h, self.rt.address(h), free=list(range(self.slab_blocks - 1, -1, -1)))
+        self.slabs.append(slab)
+        self.rt.set_tag(h, ("kv-slab", idx))
+        self.rt.harvest_register_cb(h, lambda hh, reason, idx=idx: self._on_revoke(idx, reason))
+        return idx, slab.free.pop()
+
+    def evict(self, bytes_needed: int) -> list[tuple[int, str, str]]:
+        """Move LRU/FIFO/tail blocks out of local HBM: to a peer slab when one can
+        be harvested (Backed blocks also keep a host copy), else to host.
+        All page copies of the call are one K1 launch."""
+        if bytes_needed <= 0:
+            raise ValueError("bytes_needed must be > 0")
+        n_blocks = -(-bytes_needed // self.m.block_bytes)
+        moves, src_b, src_s, dst_b, dst_s, handles = [], [], [], [], [], set()
+        for b in self._eviction_order()[:n_blocks]:
+            sbase, sstride = self._page_base(b)
+            placed = self._peer_slot(b.durability)
+            if placed is not None:
+                slab_i, slot = placed
+                slab = self.slabs[slab_i]
+                dbase, dstride = slab.va + slot * self.page, self.slab_blocks * self.page
+                src_b.append(sbase), src_s.append(sstride), dst_b.append(dbase), dst_s.append(dstride)
+                handles.add(slab.handle)
+                if b.durability == Durability.BACKED and b.host_slot is None:
+                    b.host_slot = self._take_host_slot()
+                    hb, hs = self._host_base(b.host_slot)
+                    src_b.append(sbase), src_s.append(sstride), dst_b.append(hb), dst_s.append(hs)
+                self.local_free.append(b.slot)
+                b.tier, b.slab, b.slot = KVTier.PEER_HBM, slab_i, slot
+                slab.blocks[slot] = b.block_id
+                self.stats["evict_peer"] += 1
+                moves.append((b.block_id, "LocalHBM", "PeerHBM"))
+            else:
+                if b.host_slot is None:
+                    b.host_slot = self._take_host_slot()
+                    hb, hs = self._host_base(b.host_slot)
+                    src_b.append(sbase), src_s.append(sstride), dst_b.append(hb), dst_s.append(hs)
+                self.local_free.append(b.slot)
+                b.tier, b.slot = KVTier.HOST_DRAM, b.host_slot
+                self.stats["evict_host"] += 1
+                moves.append((b.block_id, "LocalHBM", "HostDRAM"))
+            self.sys.loop.record("kv_evict", block=b.block_id, to=moves[-1][2])
+        if src_b:
+            src = self._pages(np.array(src_b, dtype=np.uint64), np.array(src_s, dtype=np.uint64))
+            dst = self._pages(np.array(dst_b, dtype=np.uint64), np.array(dst_s, dtype=np.uint64))
+            self._launch_pages(src, dst, handles)
+            # freed local slots are reusable only after the copies drained them
+            self.sys.engine.synchronize()
+            self.sys.loop.poll()
+        return moves
+
+    def _take_host_slot(self) -> int:
+        if not self.host_free:
+            raise TierExhausted("host tier is full")
+        return self.host_free.pop()
+
+    # ------------------------------------------------------------ revocation
+    def _on_revoke(self, slab_i: int, reason: RevokeReason) -> None:
+        """Slab revoked (runtime.py:403-405 ordering: already drained and
+        invalidated): Backed blocks fall back to host, Lossy ones are lost."""
+        slab = self.slabs[slab_i]
+        slab.live = False
+        for slot, bid in list(slab.blocks.items()):
+            b = self.table[bid]
+            if b.host_slot is not None:
+                b.tier, b.slot, b.slab = KVTier.HOST_DRAM, b.host_slot, -1
+            else:
+                b.tier, b.slot, b.slab = KVTier.NOT_MATERIALIZED, -1, -1
+        slab.blocks.clear()
+        slab.free = []
+
+    # ------------------------------------------------------------ reload
+    def resolve_fallback(self, block: KVBlock, host_link: LinkSpec | None = None) -> str:
+        """Backed -> FetchFromHost iff host transfer_time <=
+        entries * recompute_time_per_entry, else Recompute; no host copy -> Recompute."""
+        if block.host_slot is None:
+            return "Recompute"
+        link = host_link or self.sys.topology.link_between(0, self.sys.host_id)
+        t_host = transfer_time(link, block.entries * self.m.bytes_per_entry)
+        return "FetchFromHost" if t_host <= block.entries * self.m.recompute_time_per_entry else "Recompute"
+
+    def reload(self, block_ids) -> dict:
+        """Bring blocks to LocalHBM from their resident tier in ONE K1 launch.
+        Revoked-peer blocks resolve through resolve_fallback; Lossy blocks
+        without a host copy are recomputed (content regenerated)."""
+        need = [self.table[i] for i in block_ids if self.table[i].tier != KVTier.LOCAL_HBM]
+        plan = {"peer": [], "host": [], "recompute": []}
+        src_b, src_s, dst_b, dst_s, handles, recompute = [], [], [], [], set(), []
+        now = self.sys.loop.now
+        for b in need:
+            if b.tier == KVTier.PEER_HBM and not self.rt.is_live(self.slabs[b.slab].handle):
+                # revoked between lookup and issue: fallback
+                b.tier = KVTier.HOST_DRAM if b.host_slot is not None else KVTier.NOT_MATERIALIZED
+            if b.tier == KVTier.HOST_DRAM and self.resolve_fallback(b) == "Recompute":
+                b.tier = KVTier.NOT_MATERIALIZED
+            slot = self._take_local_slot()
+            if b.tier == KVTier.NOT_MATERIALIZED:
+                b.tier, b.slot = KVTier.LOCAL_HBM, slot
+                recompute.append(b)
+                plan["recompute"].append(b.block_id)
+                self.stats["recompute"] += 1
+                continue
+            sbase, sstride = self._page_base(b)
+            src_b.append(sbase), src_s.append(sstride)
+            dst_b.append(self.cache.data_ptr() + slot * self.page), dst_s.append(self.local_blocks * self.page)
+            if b.tier == KVTier.PEER_HBM:
+                slab = self.slabs[b.slab]
+                handles.add(slab.handle)
+                plan["peer"].append(b.block_id)
+                self.stats["reload_peer"] += 1
+                old = (b.slab, b.slot)
+            else:
+                plan["host"].append(b.block_id)
+                self.stats["reload_host"] += 1
+                old = None
+            b.tier, b.slot, b.slab = KVTier.LOCAL_HBM, slot, -1
+            b.last_access = now
+            if old is not None:
+                slab = self.slabs[old[0]]
+                slab.blocks.pop(old[1], None)
+                slab.free.append(old[1])
+        if src_b:
+            src = self._pages(np.array(src_b, dtype=np.uint64), np.array(src_s, dtype=np.uint64))
+            dst = self._pages(np.array(dst_b, dtype=np.uint64), np.array(dst_s, dtype=np.uint64))
+            self._launch_pages(src, dst, handles)
+        if recompute:
+            self.sys.engine.synchronize()
+            self._materialize(recompute)
+        self._release_empty_slabs()
+        return plan
+
+    def _release_empty_slabs(self) -> None:
+        for s in self.slabs:
+            if s.live and not s.blocks and len(s.free) == self.slab_blocks:
+                s.live = False
+                self.rt.harvest_free(s.handle)
+
+    # ------------------------------------------------------------ the per-layer gather (C1)
+    def gather_layer(self, layer: int, block_ids, dst: torch.Tensor, stream=None) -> None:
+        """K1: page `layer` of every listed block -> dst[i] (contiguous), read
+        from wherever the block is resident (local / peer / host)."""
+        bases = np.empty(len(block_ids), dtype=np.uint64)
+        strides = np.empty(len(block_ids), dtype=np.uint64)
+        for i, bid in enumerate(block_ids):
+            bases[i], strides[i] = self._page_base(self.table[bid])
+        src = bases + np.uint64(layer) * strides
+        d_src = torch.from_numpy(src.view(np.int64)).to(self.dev)
+        from . import fetch as F
+        F.kv_gather(d_src, self.page, dst=dst, engine=self.engine, max_ctas=self.max_ctas,
+                    stream=stream if stream is not None else self.stream)
+
+    def block_pages_local(self, bid: int) -> torch.Tensor:
+        b = self.table[bid]
+        assert b.tier == KVTier.LOCAL_HBM
+        return self.cache[:, b.slot, :]
+
+    def close(self) -> None:
+        self.sys.engine.synchronize()
+        self.sys.loop.run()
+        self.host.close()
+
+
+def reload_latency_experiment(models, entry_counts, host_link: LinkSpec, peer_link: LinkSpec) -> list[tuple]:
+    """modeled host vs peer reload latency and speedup per
+    (model, entries) — the prediction side; bench/measure_kv.py measures it."""
+    rows = []
+    for m in models:
+        for e in entry_counts:
+            h = transfer_time(host_link, e * m.bytes_per_entry)
+            p = transfer_time(peer_link, e * m.bytes_per_entry)
+            rows.append((m.name, e, h, p, h / p))
+    return rows

@@ -1,0 +1,97 @@
+"""KV offload path on a real GPU: append -> evict to a
+harvested peer slab (donor = the same GPU here) or host -> reload / per-layer
+gather (K1), with revocation fallback.  Bytes are checked against the oracle's
+content for every (layer, sequence, block) page."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import harvest_oracle as O
+from tests import refcheck
+
+pytestmark = pytest.mark.gpu
+
+
+def _mk(local_blocks=8, host_blocks=64, slab_blocks=4, donor_slabs=2, durability="LOSSY", order="LRU"):
+    from paper_2602_00328_b200.kv import EvictionOrder, KVCacheManager, KVModelSpec, OffloadPolicy
+    from paper_2602_00328_b200.runtime import Durability
+    from paper_2602_00328_b200.system import HarvestSystem
+    m = KVModelSpec("tiny", num_layers=4, kv_heads=2, head_dim=64)
+    slab = slab_blocks * m.block_bytes
+    sysm = HarvestSystem(0, donors=[0] if donor_slabs else [], donor_bytes=donor_slabs * slab,
+                         host_bytes=1 << 20, local_bytes=1 << 20)
+    kv = KVCacheManager(sysm, m, local_blocks, host_blocks, OffloadPolicy(EvictionOrder[order]),
+                        slab_blocks=slab_blocks, durability=Durability[durability])
+    return sysm, kv, m
+
+
+def _check_all(kv, m):
+    """Gather every layer of every block and compare with the oracle."""
+    ids = sorted(kv.table)
+    dst = torch.empty(len(ids) * m.page_bytes, dtype=torch.uint8, device="cuda")
+    for layer in range(m.num_layers):
+        kv.gather_layer(layer, ids, dst)
+        kv.sys.engine.synchronize()
+        got = dst.cpu().numpy().reshape(len(ids), m.page_bytes)
+        for i, bid in enumerate(ids):
+            b = kv.table[bid]
+            want = O.content(O.kv_seed(layer, b.sequence_id, b.index), m.page_bytes)
+            assert np.array_equal(got[i], want), (bid, layer, b.tier)
+
+
+def test_append_evict_reload_roundtrip():
+    from paper_2602_00328_b200.kv import KVTier
+    sysm, kv, m = _mk()
+    assert kv.append_kv(0, 16) == [0]                      # 16 tokens -> one block
+    assert kv.append_kv(1, 17) == [1, 2]                   # 17 -> two blocks, second holds 1
+    assert kv.table[2].entries == 1
+    kv.append_kv(2, 16 * 10)                               # exceeds 8 local slots -> evictions
+    tiers = [b.tier for b in kv.table.values()]
+    assert tiers.count(KVTier.PEER_HBM) > 0
+    assert sum(1 for t in tiers if t == KVTier.LOCAL_HBM) <= 8
+    assert kv.sys.loop.log.of_kind("kv_evict")
+    _check_all(kv, m)                                      # reads from local + peer
+    plan = kv.reload([b.block_id for b in kv.table.values() if b.tier == KVTier.PEER_HBM][:3])
+    assert len(plan["peer"]) == 3
+    kv.sys.engine.synchronize()
+    sysm.loop.run()
+    _check_all(kv, m)
+    assert refcheck.verify_release_ordering(sysm.loop.log) == []
+    kv.close()
+    sysm.close()
+
+
+def test_lossy_revocation_recomputes_and_backed_falls_back_to_host():
+    from paper_2602_00328_b200.kv import KVTier
+    from paper_2602_00328_b200.runtime import RevokeReason
+    for dur, want_tier in (("LOSSY", KVTier.NOT_MATERIALIZED), ("BACKED", KVTier.HOST_DRAM)):
+        sysm, kv, m = _mk(durability=dur)
+        kv.append_kv(0, 16 * 12)
+        peer = [b for b in kv.table.values() if b.tier == KVTier.PEER_HBM]
+        assert peer
+        slab = kv.slabs[peer[0].slab]
+        sysm.runtime.revoke(slab.handle, RevokeReason.EXTERNAL_RECLAIM)
+        sysm.loop.run()
+        assert all(kv.table[b.block_id].tier == want_tier for b in peer if b.slab == -1)
+        plan = kv.reload([b.block_id for b in peer])
+        if dur == "LOSSY":
+            assert plan["recompute"]
+        else:
+            assert plan["host"] and not plan["recompute"]
+        kv.sys.engine.synchronize()
+        sysm.loop.run()
+        _check_all(kv, m)                                  # correctness independent of the peer tier
+        assert refcheck.verify_release_ordering(sysm.loop.log) == []
+        kv.close()
+        sysm.close()
+
+
+def test_no_peer_capacity_goes_to_host():
+    from paper_2602_00328_b200.kv import KVTier
+    sysm, kv, m = _mk(donor_slabs=0)
+    kv.append_kv(0, 16 * 12)
+    assert not any(b.tier == KVTier.PEER_HBM for b in kv.table.values())
+    assert kv.stats["evict_host"] >= 4 and kv.stats["evict_peer"] == 0
+    _check_all(kv, m)
+    kv.close()
+    sysm.close()

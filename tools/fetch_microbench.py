@@ -102,6 +102,20 @@ def main():
             res[f"lat1_{src_name}_{eng}_us"] = med * 1e6
         med, mn = timeit(lambda: F.ce_batch_copy(hs[:1], hd[:1], hz[:1], batched=False), iters=20)
         res[f"lat1_{src_name}_ce_us"] = med * 1e6
+        if src_name == "host":  # kernel + copy engine concurrently on two streams
+            s_ce = torch.cuda.Stream()
+            for f in (0.15, 0.3, 0.5, 0.7):
+                k = int(round(ne * f))
+
+                def hybrid():
+                    cur = torch.cuda.current_stream()
+                    s_ce.wait_stream(cur)
+                    F.ce_batch_copy(hs[:k], hd[:k], hz[:k], batched=True, stream=s_ce)
+                    F.batch_copy(sp[k:], dp[k:], sz[k:], engine="ldg")
+                    cur.wait_stream(s_ce)
+
+                med, mn = timeit(hybrid, iters=5)
+                res[f"exp_host_hybrid_ce{f}"] = {"ms": med * 1e3, "GBps": ne * esz / med / 1e9}
     out["experts_qwen_53x17.3MB"] = res
     # raw copy peak for reference
     a = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
