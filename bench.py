@@ -185,6 +185,60 @@ def measure_pcie_h2d(dev):
     return best
 
 
+def same_run_comparisons(dev, m, a, source, n=53):
+    """Same-box comparisons for one layer's worth of experts (n x 17.3 MB):
+    the copy-engine paths on the same source (cudaMemcpyBatchAsync: the
+    paper's/vLLM's data path) and the same kernel on a local-HBM source
+    against the HBM roofline (kernel quality independent of the link)."""
+    import torch
+    from paper_2602_00328_b200 import fetch as F
+    from paper_2602_00328_b200.pool import HostTier
+    S = m.expert_size
+    dst = torch.empty(n * S, dtype=torch.uint8, device=f"cuda:{dev}")
+    loc = torch.empty(n * S, dtype=torch.uint8, device=f"cuda:{dev}")
+    s = torch.cuda.Stream(dev)
+
+    def t(fn, iters=5):
+        best = []
+        for i in range(iters + 2):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            fn()
+            e1.record(s)
+            e1.synchronize()
+            if i >= 2:
+                best.append(e0.elapsed_time(e1) * 1e-3)
+        return statistics.median(best)
+
+    out = {}
+    dp = F.ptrs_tensor([dst.data_ptr() + i * S for i in range(n)], f"cuda:{dev}")
+    sz = F.ptrs_tensor([S] * n, f"cuda:{dev}")
+    lp = F.ptrs_tensor([loc.data_ptr() + i * S for i in range(n)], f"cuda:{dev}")
+    dt = t(lambda: F.batch_copy(lp, dp, sz, engine=a.engine, stream=s.cuda_stream))
+    hbm_peak = 6553.0
+    try:
+        hbm_peak = float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        pass
+    out["roofline_local_source"] = {"bound": "hbm", "achieved": 2 * n * S / dt / 1e9, "peak": hbm_peak,
+                                    "unit": "GB/s", "frac": 2 * n * S / dt / 1e9 / hbm_peak,
+                                    "note": "same K2 kernel, local-HBM source: read+write bytes / time vs "
+                                            "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"}
+    if source == "host":
+        h = HostTier(n * S)
+        hs = np.array([h.host_address(i * S) for i in range(n)], dtype=np.uint64)
+        hd = np.array([dst.data_ptr() + i * S for i in range(n)], dtype=np.uint64)
+        hz = np.full(n, S, dtype=np.uint64)
+        dce = t(lambda: F.ce_batch_copy(hs, hd, hz, batched=True, stream=s.cuda_stream))
+        out["copy_engine_same_source_GBps"] = n * S / dce / 1e9
+        dce1 = t(lambda: F.ce_batch_copy(hs[:1], hd[:1], hz[:1], batched=False, stream=s.cuda_stream))
+        dk1 = t(lambda: F.batch_copy(F.ptrs_tensor([h.device_address(0)], f"cuda:{dev}"), dp[:1], sz[:1],
+                                     engine=a.engine, stream=s.cuda_stream))
+        out["single_expert_latency_us"] = {"kernel_host": dk1 * 1e6, "copy_engine_host": dce1 * 1e6}
+        h.close()
+    return out
+
+
 def emit(line, a):
     s = json.dumps(line)
     print(s, flush=True)
@@ -405,9 +459,13 @@ def run_b200(a):
                     "peak_source": "B200_PROFILING.md fallback: measured peer copy 770 GB/s per direction "
                                    "(900 nominal)"}
         tr = load_traffic().get("batch_copy_" + source)
-        roof["traffic"] = tr
+        roof["traffic"] = tr["traffic_bytes_per_launch"] if tr else None
+        if tr:
+            roof["traffic_source"] = (f"profiles/traffic.json[{'batch_copy_' + source}]: one ncu --set full capture "
+                                      f"({tr['report']}), algorithmic {tr['algorithmic_bytes_per_launch']:.0f} B/launch")
         roof["bytes_per_launch"] = bytes_per_launch
         roof["mean_launch_ms"] = statistics.mean(launch_ms)
+        extra = same_run_comparisons(dev, m, a, source)
         cpu = None
         if not a.no_cpu_baseline:
             threads = os.cpu_count() or 1
@@ -426,7 +484,7 @@ def run_b200(a):
                         "d2h_bytes_per_step": d2h // a.steps, "verify_mismatched_words": int(mism_all)},
                 "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
                 "clocks": clk.summary(),
-                "latency_ms_per_layer_fetch": statistics.median(launch_ms)}
+                "latency_ms_per_layer_fetch": statistics.median(launch_ms), **extra}
         emit(line, a)
     barrier()
     sysm.close()

@@ -367,15 +367,17 @@ class KVCacheManager:
         without a host copy are recomputed (content regenerated)."""
         need = [self.table[i] for i in block_ids if self.table[i].tier != KVTier.LOCAL_HBM]
         plan = {"peer": [], "host": [], "recompute": []}
-        src_b, src_s, dst_b, dst_s, handles, recompute = [], [], [], [], set(), []
+        src_b, src_s, dst_b, dst_s, handles, recompute, vacated = [], [], [], [], set(), [], []
         now = self.sys.loop.now
-        for b in need:
+        # reserve every destination slot first: evictions triggered here only
+        # see blocks that are already local, never the ones being reloaded
+        slots = [self._take_local_slot() for _ in need]
+        for b, slot in zip(need, slots):
             if b.tier == KVTier.PEER_HBM and not self.rt.is_live(self.slabs[b.slab].handle):
                 # revoked between lookup and issue: fallback
                 b.tier = KVTier.HOST_DRAM if b.host_slot is not None else KVTier.NOT_MATERIALIZED
             if b.tier == KVTier.HOST_DRAM and self.resolve_fallback(b) == "Recompute":
                 b.tier = KVTier.NOT_MATERIALIZED
-            slot = self._take_local_slot()
             if b.tier == KVTier.NOT_MATERIALIZED:
                 b.tier, b.slot = KVTier.LOCAL_HBM, slot
                 recompute.append(b)
@@ -398,13 +400,18 @@ class KVCacheManager:
             b.tier, b.slot, b.slab = KVTier.LOCAL_HBM, slot, -1
             b.last_access = now
             if old is not None:
-                slab = self.slabs[old[0]]
-                slab.blocks.pop(old[1], None)
-                slab.free.append(old[1])
+                vacated.append(old)
         if src_b:
             src = self._pages(np.array(src_b, dtype=np.uint64), np.array(src_s, dtype=np.uint64))
             dst = self._pages(np.array(dst_b, dtype=np.uint64), np.array(dst_s, dtype=np.uint64))
             self._launch_pages(src, dst, handles)
+        # old peer slots become reusable only now: any later write into them is
+        # stream-ordered after this launch's reads (same fetch stream)
+        for slab_i, slot in vacated:
+            slab = self.slabs[slab_i]
+            slab.blocks.pop(slot, None)
+            if slab.live:
+                slab.free.append(slot)
         if recompute:
             self.sys.engine.synchronize()
             self._materialize(recompute)
