@@ -318,9 +318,14 @@ def run_b200(a):
         # placement: the runtime's own harvest_alloc decisions (runtime.py:198-235);
         # the copy-in is the synthetic-content fill written over NVLink
         ptrs, seeds = [], []
+        # round-robin preference (the reference's preferred_devices hint,
+        # runtime.py:205-214) so every layer's experts span all N-1 donors and
+        # no donor's NVLink egress serves a whole layer alone
         for layer in range(L):
             for e in range(E):
-                h = rt.harvest_alloc(S, AllocationHints(durability=Durability.BACKED, client_id="moe"))
+                pref = [1 + (layer * E + e) % (world - 1)]
+                h = rt.harvest_alloc(S, AllocationHints(preferred_devices=pref, durability=Durability.BACKED,
+                                                        client_id="moe"))
                 assert h is not None, "donor capacity exhausted"
                 rt.set_tag(h, ("expert", layer, e))
                 rt.write_peer(h, ("expert", layer, e), expert_content(m, layer, e))
