@@ -197,6 +197,10 @@ int hv_ce_batch_copy(const uint64_t* h_src, const uint64_t* h_dst,
  * seeded by stable_hash64(tag) (runtime.py:38-44). */
 int hv_fill_content(const uint64_t* d_dst, const uint64_t* d_bytes,
                     const uint64_t* d_seeds, uint32_t n, void* stream);
+/* the same stream as bf16 expert weights: each 16-bit lane becomes
+ * (lane & 0x807F) | 0x3C00, a finite value with |w| in [2^-7, 2^-6) */
+int hv_fill_weights_bf16(const uint64_t* d_dst, const uint64_t* d_bytes,
+                         const uint64_t* d_seeds, uint32_t n, void* stream);
 /* position-keyed 64-bit digest per object (see oracle/hv_oracle.c) */
 int hv_digest(const uint64_t* d_src, const uint64_t* d_bytes, uint32_t n,
               uint64_t* d_out, void* stream);

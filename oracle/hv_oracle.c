@@ -53,6 +53,21 @@ void hvo_fill(uint8_t* dst, uint64_t bytes, uint64_t seed) {
   }
 }
 
+/* bf16-weights variant of the stream (hv_fill_weights_bf16): every 16-bit
+ * lane keeps sign + 7 mantissa bits, exponent fixed at 2^-7 */
+void hvo_fill_weights(uint8_t* dst, uint64_t bytes, uint64_t seed) {
+  const uint64_t nfull = bytes / 8;
+  for (uint64_t i = 0; i < nfull; ++i) {
+    const uint64_t w = (hvo_content_word(seed, i) & 0x807F807F807F807Full) | 0x3C003C003C003C00ull;
+    memcpy(dst + 8 * i, &w, 8);
+  }
+  const uint64_t tail = bytes & 7;
+  if (tail) {
+    const uint64_t w = (hvo_content_word(seed, nfull) & 0x807F807F807F807Full) | 0x3C003C003C003C00ull;
+    for (uint64_t b = 0; b < tail; ++b) dst[8 * nfull + b] = (uint8_t)(w >> (8 * b));
+  }
+}
+
 uint64_t hvo_digest(const uint8_t* src, uint64_t bytes) {
   uint64_t acc = bytes;
   const uint64_t nfull = bytes / 8;

@@ -102,6 +102,7 @@ _SIGS = {
     "hv_swap_blocks_batch": [vp, vp, vp, u32, i32, i32, vp],
     "hv_ce_batch_copy": [vp, vp, vp, u32, i32, vp],
     "hv_fill_content": [u64, u64, u64, u32, vp],
+    "hv_fill_weights_bf16": [u64, u64, u64, u32, vp],
     "hv_digest": [u64, u64, u32, u64, vp],
     "hv_verify_content": [u64, u64, u64, u32, u64, vp],
     "hv_launch_count": [P64],

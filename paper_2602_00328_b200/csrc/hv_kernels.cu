@@ -310,17 +310,29 @@ struct CopyOpT {
 using CopyOp = CopyOpT<false>;
 
 // content ops work on 8-byte words; objects must start 8-byte aligned
+// kind 0: raw splitmix64 bytes.  kind 1: bf16 weights — every 16-bit lane of
+// the word keeps its sign and 7 mantissa bits with the exponent fixed at 2^-7,
+// i.e. |w| in [2^-7, 2^-6): finite, small, still a keyed pseudo-random stream.
+__host__ __device__ __forceinline__ uint64_t weights_word(uint64_t w) {
+  return (w & 0x807F807F807F807Full) | 0x3C003C003C003C00ull;
+}
+
 struct FillOp {
   const uint64_t* seeds;
+  uint32_t kind;
+  __device__ __forceinline__ uint64_t word(uint64_t seed, uint64_t i) const {
+    const uint64_t w = content_word(seed, i);
+    return kind ? weights_word(w) : w;
+  }
   __device__ __forceinline__ void operator()(const ChunkRef& r, uint32_t lane) const {
     const uint64_t seed = __ldg(seeds + r.obj);
     const uint64_t w0 = r.off >> 3;
     const uint32_t nfull = r.len >> 3;
     uint64_t* d = reinterpret_cast<uint64_t*>(r.dst);
-    for (uint32_t k = lane; k < nfull; k += 32) d[k] = content_word(seed, w0 + k);
+    for (uint32_t k = lane; k < nfull; k += 32) d[k] = word(seed, w0 + k);
     const uint32_t tail = r.len & 7;
     if (tail && lane == 0) {
-      const uint64_t w = content_word(seed, w0 + nfull);
+      const uint64_t w = word(seed, w0 + nfull);
       for (uint32_t b = 0; b < tail; ++b) r.dst[nfull * 8 + b] = (char)((w >> (8 * b)) & 0xff);
     }
   }
@@ -840,7 +852,18 @@ HV_EXPORT int hv_fill_content(const uint64_t* d_dst, const uint64_t* d_bytes, co
   HV_CHECK_ARG(d_dst && d_bytes && d_seeds);
   FillOpR op;
   op.seeds = d_seeds;
+  op.kind = 0;
   // FillOp writes through r.dst; the resolver's src is unused but must be valid
+  return launch_descs(d_dst, d_dst, d_bytes, n, HV_ENGINE_LDG, 0, stream, op, false);
+}
+
+HV_EXPORT int hv_fill_weights_bf16(const uint64_t* d_dst, const uint64_t* d_bytes, const uint64_t* d_seeds,
+                                   uint32_t n, void* stream) {
+  if (n == 0) return HV_OK;
+  HV_CHECK_ARG(d_dst && d_bytes && d_seeds);
+  FillOpR op;
+  op.seeds = d_seeds;
+  op.kind = 1;
   return launch_descs(d_dst, d_dst, d_bytes, n, HV_ENGINE_LDG, 0, stream, op, false);
 }
 

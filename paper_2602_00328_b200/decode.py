@@ -1,0 +1,175 @@
+"""Pipelined MoE decode with expert weights served by Harvest tiers.
+
+Reference semantics: moe._DecodeRun (moe.py:211-340).
+- Stages (layer, micro-batch) run in layer-major order.
+- The weights of stage s+1 are fetched while stage s computes ("issue fetches
+  for stage s+1 at the start of stage s", moe.py:327-340).
+- A stage starts when compute(s-1) is done AND every fetch of s has arrived.
+Here the compute is real, not a constant per stage: a router GEMM, top-k, and
+a SwiGLU expert FFN (bf16, cuBLAS batched GEMMs on the compute stream). The
+fetch is the K2 kernel on the fetch stream, and "arrived" is a CUDA event.
+
+B200-native choices:
+- The fetch plan is built ON THE DEVICE. Router -> top-k -> active-expert
+  mask -> per-expert size (0 when inactive), against a device copy of the
+  residency address table, then one hv_batch_copy over all E descriptors.
+  Zero-size descriptors are skipped by the kernel. No host synchronisation
+  happens anywhere in a decode step, so the whole step can be captured in a
+  CUDA graph.
+- Two staging buffers alternate between stages. The compute of stage s reads
+  buffer s%2 while the fetch of s+1 fills buffer (s+1)%2; a fetch waits for
+  the compute that last read its buffer.
+- Every expert slot of the staging buffer is zero-initialised, so inactive
+  slots hold finite bytes. Their combine weight is exactly 0, which lets the
+  FFN run densely over all E experts with fixed shapes.
+- Drain: a stage may read any peer handle of its layer, so all of them join
+  the stage's in-flight set (a superset of the reference's per-expert sets,
+  which keeps drain-before-free).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.nn.functional as TF
+
+from . import _native as N
+from .moe import ExpertFetcher
+
+
+class MoEDecoder:
+    def __init__(self, fetcher: ExpertFetcher, tokens: int, microbatches: int = 1, seed: int = 0,
+                 engine: str = "auto", max_ctas: int = 0, router_scale: float = 0.5,
+                 residual_scale: float = 1.0):
+        m = fetcher.model
+        if not (m.hidden and m.intermediate):
+            raise ValueError("model profile needs hidden/intermediate sizes")
+        if tokens % microbatches:
+            raise ValueError("tokens must split evenly into micro-batches")
+        self.f, self.m, self.rt = fetcher, m, fetcher.rt
+        self.engine_id = N.ENGINES[engine]
+        self.max_ctas = max_ctas
+        eng = fetcher.engine
+        self.dev = torch.device(f"cuda:{eng.cuda_device}")
+        self.L, self.E, self.H, self.I, self.S = m.num_layers, m.num_experts, m.hidden, m.intermediate, m.expert_size
+        self.T, self.nmb = tokens, microbatches
+        # h <- h + residual_scale * moe(h); a power of two keeps it exact in bf16
+        self.residual_scale = residual_scale
+        self.tmb = tokens // microbatches
+        g = torch.Generator().manual_seed(seed)
+        self.router = [(torch.randn(self.E, self.H, generator=g) * router_scale / self.H ** 0.5)
+                       .to(torch.bfloat16).to(self.dev) for _ in range(self.L)]
+        self.x0 = (torch.randn(tokens, self.H, generator=g) * 0.5).to(torch.bfloat16).to(self.dev)
+        self.staging = [torch.zeros(self.E, self.S, dtype=torch.uint8, device=self.dev) for _ in range(2)]
+        self.dst_ptrs = [torch.tensor([b.data_ptr() + e * self.S for e in range(self.E)], dtype=torch.int64,
+                                      device=self.dev) for b in self.staging]
+        self.compute = torch.cuda.Stream(self.dev)
+        self.fetch_stream_h = eng.stream
+        self.fetch = torch.cuda.ExternalStream(eng.stream, device=self.dev)
+        self.sync_tables()
+        n = self.L * self.nmb
+        self.sizes = [torch.zeros(self.E, dtype=torch.int64, device=self.dev) for _ in range(2)]
+        self.comb = [torch.zeros(self.tmb, self.E, dtype=torch.float32, device=self.dev) for _ in range(2)]
+        self.stages = [(layer, mb) for layer in range(self.L) for mb in range(self.nmb)]
+        self.bytes_fetched_per_step = None
+        self._n_stages = n
+
+    # ---------------------------------------------------------------- tables
+    def sync_tables(self) -> None:
+        """Upload the residency address table and fetch mask (call after
+        placement or revocation changed ExpertFetcher's tables)."""
+        # LOCAL experts are staged from their resident copy in HBM (a device-
+        # local copy); PEER/HOST experts are the fetches the reference counts
+        src = np.where(self.f.tier == 0, self.f.local_addr, self.f.src_addr).astype(np.uint64)
+        if np.any(src == 0):
+            raise ValueError("an expert has no source address (LOCAL tier needs ExpertFetcher(local_addr=...))")
+        self.addr = torch.from_numpy(src.view(np.int64).copy()).to(self.dev)
+        self.fetchable = torch.from_numpy((self.f.tier != 0).copy()).to(self.dev)
+        self.layer_handles = [[h for (l, _e), h in self.f.handles.items() if l == layer] for layer in range(self.L)]
+
+    # ---------------------------------------------------------------- pieces
+    def _route(self, h: torch.Tensor, layer: int, slot: int) -> None:
+        logits = (h @ self.router[layer].t()).float()
+        topv, topi = logits.topk(self.m.top_k, dim=1)
+        probs = torch.softmax(topv, dim=1)
+        comb = self.comb[slot]
+        comb.zero_()
+        comb.scatter_(1, topi, probs)
+        active = (comb > 0).any(dim=0)
+        torch.where(active, torch.full_like(self.sizes[slot], self.S), torch.zeros_like(self.sizes[slot]),
+                    out=self.sizes[slot])
+
+    def _ffn(self, h: torch.Tensor, slot: int, buf: int) -> torch.Tensor:
+        E, I, H = self.E, self.I, self.H
+        w = self.staging[buf].view(torch.bfloat16).view(E, 3 * I * H)
+        gate = w[:, :I * H].view(E, I, H)
+        up = w[:, I * H:2 * I * H].view(E, I, H)
+        down = w[:, 2 * I * H:].view(E, H, I)
+        x = h.unsqueeze(0).expand(E, h.shape[0], H)
+        a = TF.silu(torch.bmm(x, gate.transpose(1, 2))) * torch.bmm(x, up.transpose(1, 2))
+        y = torch.bmm(a, down.transpose(1, 2))                       # [E, T, H]
+        wts = self.comb[slot].t().unsqueeze(-1).to(y.dtype)          # [E, T, 1]
+        return (y * wts).sum(0)
+
+    def _issue_fetch(self, s: int, ready: torch.cuda.Event, buf_free: torch.cuda.Event | None) -> torch.cuda.Event:
+        layer, _ = self.stages[s]
+        slot = s % 2
+        self.fetch.wait_event(ready)
+        if buf_free is not None:
+            self.fetch.wait_event(buf_free)
+        N.call("hv_batch_copy", self.addr[layer].data_ptr(), self.dst_ptrs[slot].data_ptr(),
+               self.sizes[slot].data_ptr(), self.E, self.engine_id, self.max_ctas, self.fetch_stream_h)
+        handles = self.layer_handles[layer]
+        if handles:
+            batch = self.rt.begin_reads(handles)
+            self.f.engine.track([lambda _x, b=batch: self.rt.end_reads(b)])
+        ev = torch.cuda.Event()
+        ev.record(self.fetch)
+        return ev
+
+    # ---------------------------------------------------------------- step
+    def step(self, x: torch.Tensor) -> torch.Tensor:
+        """One decode step over all layers; returns the new hidden states."""
+        hs = list(x.view(self.nmb, self.tmb, self.H).clone().unbind(0))
+        cur = torch.cuda.current_stream(self.dev)
+        self.compute.wait_stream(cur)
+        n = self._n_stages
+        fetched = [None] * n
+        buf_free = [None, None]
+        with torch.cuda.stream(self.compute):
+            layer0, mb0 = self.stages[0]
+            self._route(hs[mb0], layer0, 0)
+            ev = torch.cuda.Event()
+            ev.record(self.compute)
+        fetched[0] = self._issue_fetch(0, ev, None)
+        for s in range(n):
+            layer, mb = self.stages[s]
+            slot = buf = s % 2
+            with torch.cuda.stream(self.compute):
+                nxt_ready = None
+                if s + 1 < n and self.nmb > 1:   # stage s+1's input already exists
+                    l2, mb2 = self.stages[s + 1]
+                    self._route(hs[mb2], l2, (s + 1) % 2)
+                    nxt_ready = torch.cuda.Event()
+                    nxt_ready.record(self.compute)
+                self.compute.wait_event(fetched[s])
+                y = self._ffn(hs[mb], slot, buf)
+                hs[mb] = hs[mb] + (y * self.residual_scale if self.residual_scale != 1.0 else y)
+                done = torch.cuda.Event()
+                done.record(self.compute)
+                buf_free[buf] = done
+                if s + 1 < n and self.nmb == 1:  # next stage depends on this one
+                    l2, mb2 = self.stages[s + 1]
+                    self._route(hs[mb2], l2, (s + 1) % 2)
+                    nxt_ready = torch.cuda.Event()
+                    nxt_ready.record(self.compute)
+            if s + 1 < n:
+                fetched[s + 1] = self._issue_fetch(s + 1, nxt_ready, buf_free[(s + 1) % 2] if s >= 1 else None)
+        cur.wait_stream(self.compute)
+        return torch.stack(hs).view(self.T, self.H)
+
+    def decode(self, steps: int, x: torch.Tensor | None = None) -> torch.Tensor:
+        h = self.x0 if x is None else x
+        for _ in range(steps):
+            h = self.step(h)
+            self.rt.sim.poll() if hasattr(self.rt.sim, "poll") else None
+        return h

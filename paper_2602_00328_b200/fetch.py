@@ -114,6 +114,13 @@ def fill_content(dst_ptrs: torch.Tensor, sizes: torch.Tensor, seeds, stream=None
            _dev_u64(sd, "seeds"), dst_ptrs.numel(), N.stream_handle(stream))
 
 
+def fill_weights_bf16(dst_ptrs: torch.Tensor, sizes: torch.Tensor, seeds, stream=None) -> None:
+    """Same keyed stream, each 16-bit lane mapped to a small finite bf16 weight."""
+    sd = seeds if isinstance(seeds, torch.Tensor) else _seeds_tensor(seeds, dst_ptrs.device)
+    N.call("hv_fill_weights_bf16", _dev_u64(dst_ptrs, "dst_ptrs"), _dev_u64(sizes, "sizes"),
+           _dev_u64(sd, "seeds"), dst_ptrs.numel(), N.stream_handle(stream))
+
+
 def digest(src_ptrs: torch.Tensor, sizes: torch.Tensor, stream=None) -> torch.Tensor:
     out = torch.empty(src_ptrs.numel(), dtype=torch.int64, device=src_ptrs.device)
     N.call("hv_digest", _dev_u64(src_ptrs, "src_ptrs"), _dev_u64(sizes, "sizes"), src_ptrs.numel(),

@@ -291,6 +291,15 @@ class CudaTransferEngine:
         self._pending.append((ev, [(None, cb, None) for cb in callbacks]))
         return ev
 
+    def track(self, callbacks=()):
+        """Record an event after whatever was just enqueued on the fetch stream
+        (e.g. a device-descriptor launch) and run ``callbacks`` when it completes."""
+        ev = self._event()
+        N.call("hv_event_record", ev, self.stream)
+        self._pending.append((ev, [(None, cb, None) for cb in callbacks]))
+        self.last_event = ev
+        return ev
+
     # -- poller protocol (DeviceLoop)
     def pending(self) -> int:
         return len(self._pending)

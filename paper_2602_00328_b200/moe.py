@@ -147,16 +147,17 @@ class ExpertStore:
     def host_segment(self, layer: int, expert: int) -> Segment:
         return Segment(self.host_offset(layer, expert), self.model.expert_size)
 
-    def fill_host(self, device: int = 0, layers=None) -> None:
+    def fill_host(self, device: int = 0, layers=None, weights: bool = False) -> None:
         """Write every expert's synthetic content into the pinned host tier
-        (the fill kernel writes through the mapped alias over PCIe)."""
+        (the fill kernel writes through the mapped alias over PCIe).
+        ``weights=True`` writes the bf16-weights variant (finite values)."""
         m = self.model
         layers = range(m.num_layers) if layers is None else layers
+        fill = F.fill_weights_bf16 if weights else F.fill_content
         for layer in layers:
             ptrs = [self.host.device_address(self.host_offset(layer, e)) for e in range(m.num_experts)]
-            F.fill_content(F.ptrs_tensor(ptrs, f"cuda:{device}"),
-                           F.ptrs_tensor([m.expert_size] * m.num_experts, f"cuda:{device}"),
-                           [expert_content(m, layer, e) for e in range(m.num_experts)])
+            fill(F.ptrs_tensor(ptrs, f"cuda:{device}"), F.ptrs_tensor([m.expert_size] * m.num_experts, f"cuda:{device}"),
+                 [expert_content(m, layer, e) for e in range(m.num_experts)])
         torch.cuda.synchronize(device)
 
 
@@ -248,6 +249,10 @@ class ExpertFetcher:
         self.host_addr = np.array([[host_base + store.host_offset(l, e) for e in range(E)] for l in range(L)],
                                   dtype=np.uint64)
         self.src_addr = self.host_addr.copy()
+        # device addresses of locally resident expert weights (LOCAL tier); the
+        # fetch plan skips them exactly like moe.py:295-296
+        self.local_addr = (np.zeros((L, E), dtype=np.uint64) if local_addr is None
+                           else np.asarray(local_addr, dtype=np.uint64).reshape(L, E))
         self.tier = np.full((L, E), 2, dtype=np.int8)   # 0 local, 1 peer, 2 host
         self.handles: dict[tuple[int, int], HarvestHandle] = {}
         for (l, e), ent in residency.entries.items():
