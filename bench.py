@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--out", default=None)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--no-host-compare", action="store_true",
+                    help="N>1: skip rank 0's host-offload decode comparison")
     a = ap.parse_args()
     a.warmup = max(3, a.warmup)
     return a
@@ -185,6 +187,50 @@ def measure_pcie_h2d(dev):
     return best
 
 
+def run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, microbatches=2, steps=3, warm=2):
+    """MoE decode tokens/s: batch 32 split into `microbatches`, layer-major
+    stages, each stage's experts fetched one stage ahead (K2, device-side
+    plan) while the previous stage's SwiGLU experts run on the compute stream."""
+    import torch
+    from paper_2602_00328_b200.decode import MoEDecoder
+    dec = MoEDecoder(fetcher, tokens=TOKENS, microbatches=microbatches, seed=7, engine=a.engine,
+                     max_ctas=a.max_ctas)
+    h = dec.decode(warm)
+    torch.cuda.synchronize()
+    barrier()
+    cur = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(cur)
+    h = dec.decode(steps, h)
+    e1.record(cur)
+    e1.synchronize()
+    dt = max_over_ranks(e0.elapsed_time(e1) * 1e-3)
+    out = {"tokens_per_s": TOKENS * steps * world / dt, "per_rank_tokens_per_s": TOKENS * steps / dt,
+           "batch": TOKENS, "microbatches": microbatches, "steps": steps, "warmup": warm,
+           "ms_per_decode_step": dt / steps * 1e3, "expert_source": source,
+           "outputs_finite": bool(torch.isfinite(h.float()).all()),
+           "model": "24 MoE layers (router + top-4 + SwiGLU experts, bf16); attention not modeled"}
+    del dec
+    return out
+
+
+def host_offload_decode(m, dev, a, microbatches=2, steps=3, warm=2):
+    """The same decode with every expert served from pinned host DRAM (the
+    CPU-offload baseline of PAPER.md §4.5), on this GPU."""
+    import torch
+    from paper_2602_00328_b200.moe import ExpertFetcher, ExpertResidency, ExpertStore
+    from paper_2602_00328_b200.pool import HostTier
+    from paper_2602_00328_b200.system import HarvestSystem
+    host = HostTier(m.num_layers * m.num_experts * m.expert_size)
+    sysm = HarvestSystem(dev, host_tier=host, local_bytes=1, engine=a.engine, log_transfers=False)
+    store = ExpertStore(m, sysm.host_id, host)
+    store.fill_host(dev, weights=True)
+    fetcher = ExpertFetcher(sysm.runtime, m, ExpertResidency(m), store)
+    r = run_decode(fetcher, m, dev, 1, lambda x: x, lambda: None, a, "host", microbatches, steps, warm)
+    sysm.close()
+    return r
+
+
 def same_run_comparisons(dev, m, a, source, n=53):
     """Same-box comparisons for one layer's worth of experts (n x 17.3 MB):
     the copy-engine paths on the same source (cudaMemcpyBatchAsync: the
@@ -294,7 +340,7 @@ def run_b200(a):
         sysm = HarvestSystem(dev, host_tier=host_tier, local_bytes=1, engine=a.engine, max_ctas=a.max_ctas,
                              log_transfers=False)
         store = ExpertStore(m, sysm.host_id, host_tier)
-        store.fill_host(dev)
+        store.fill_host(dev, weights=True)
         residency = ExpertResidency(m)       # every expert HOST_DRAM
     else:
         source = "peer"
@@ -333,7 +379,7 @@ def run_b200(a):
                 ptrs.append(rt.address(h))
                 seeds.append(expert_content(m, layer, e))
         for i in range(0, len(ptrs), 120):
-            F.fill_content(F.ptrs_tensor(ptrs[i:i + 120], f"cuda:{dev}"),
+            F.fill_weights_bf16(F.ptrs_tensor(ptrs[i:i + 120], f"cuda:{dev}"),
                            F.ptrs_tensor([S] * len(ptrs[i:i + 120]), f"cuda:{dev}"), seeds[i:i + 120])
         torch.cuda.synchronize()
         dist.barrier()
@@ -420,7 +466,7 @@ def run_b200(a):
             with torch.cuda.stream(stream):
                 bad = F.verify_content(F.ptrs_tensor(stage_ptrs[layer % 2][:len(ex)], f"cuda:{dev}"),
                                        F.ptrs_tensor([S] * len(ex), f"cuda:{dev}"), seeds_dev[key],
-                                       stream=stream_h)
+                                       stream=stream_h, weights=True)
                 host_bad = bad.to("cpu", non_blocking=False)
             return int(host_bad.sum()), len(ex)
         return 0, 0
@@ -450,6 +496,16 @@ def run_b200(a):
     e2e_dt = max_over_ranks(max(wall, e0.elapsed_time(e1) * 1e-3))
     e2e_value = total_bytes / e2e_dt / 1e9
     mism_all = max_over_ranks(float(mism))
+
+    # ---- MoE decode tokens/s through the pipelined decoder (moe.py:211-340)
+    del desc
+    decode = run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source)
+    sysm.loop.run()
+    if world > 1 and rank == 0 and not a.no_host_compare:
+        decode["host_offload"] = host_offload_decode(m, dev, a)
+        decode["speedup_vs_host_offload_per_gpu"] = (decode["per_rank_tokens_per_s"]
+                                                     / decode["host_offload"]["tokens_per_s"])
+    barrier()
 
     if rank == 0:
         if source == "host":
@@ -489,7 +545,7 @@ def run_b200(a):
                         "d2h_bytes_per_step": d2h // a.steps, "verify_mismatched_words": int(mism_all)},
                 "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
                 "clocks": clk.summary(),
-                "latency_ms_per_layer_fetch": statistics.median(launch_ms), **extra}
+                "latency_ms_per_layer_fetch": statistics.median(launch_ms), "decode": decode, **extra}
         emit(line, a)
     barrier()
     sysm.close()

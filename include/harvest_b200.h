@@ -209,6 +209,10 @@ int hv_verify_content(const uint64_t* d_src, const uint64_t* d_bytes,
                       const uint64_t* d_seeds, uint32_t n, uint64_t* d_mismatch,
                       void* stream);
 
+/* hv_verify_content against the bf16-weights variant (hv_fill_weights_bf16) */
+int hv_verify_weights_bf16(const uint64_t* d_src, const uint64_t* d_bytes,
+                           const uint64_t* d_seeds, uint32_t n, uint64_t* d_mismatch,
+                           void* stream);
 /* number of kernel launches issued by this library in this process */
 int hv_launch_count(uint64_t* out);
 

@@ -105,6 +105,7 @@ _SIGS = {
     "hv_fill_weights_bf16": [u64, u64, u64, u32, vp],
     "hv_digest": [u64, u64, u32, u64, vp],
     "hv_verify_content": [u64, u64, u64, u32, u64, vp],
+    "hv_verify_weights_bf16": [u64, u64, u64, u32, u64, vp],
     "hv_launch_count": [P64],
 }
 _RESTYPES = {"hv_error_string": C.c_char_p}

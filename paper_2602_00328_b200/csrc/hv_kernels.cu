@@ -370,17 +370,22 @@ struct DigestOp {
 struct VerifyOp {
   const uint64_t* seeds;
   unsigned long long* out;
+  uint32_t kind;  // as FillOp::kind
+  __device__ __forceinline__ uint64_t word(uint64_t seed, uint64_t i) const {
+    const uint64_t w = content_word(seed, i);
+    return kind ? weights_word(w) : w;
+  }
   __device__ __forceinline__ void operator()(const ChunkRef& r, uint32_t lane) const {
     const uint64_t seed = __ldg(seeds + r.obj);
     const uint64_t w0 = r.off >> 3;
     const uint32_t nfull = r.len >> 3;
     const uint64_t* s = reinterpret_cast<const uint64_t*>(r.src);
     uint64_t bad = 0;
-    for (uint32_t k = lane; k < nfull; k += 32) bad += (s[k] != content_word(seed, w0 + k));
+    for (uint32_t k = lane; k < nfull; k += 32) bad += (s[k] != word(seed, w0 + k));
     const uint32_t tail = r.len & 7;
     if (tail && lane == 0) {
       const uint64_t mask = (1ull << (8 * tail)) - 1;
-      bad += ((load_word_tail(r.src + nfull * 8, tail) ^ content_word(seed, w0 + nfull)) & mask) != 0;
+      bad += ((load_word_tail(r.src + nfull * 8, tail) ^ word(seed, w0 + nfull)) & mask) != 0;
     }
     bad = warp_sum(bad);
     if (lane == 0 && bad) atomicAdd(out + r.obj, (unsigned long long)bad);
@@ -891,5 +896,21 @@ HV_EXPORT int hv_verify_content(const uint64_t* d_src, const uint64_t* d_bytes, 
   VerifyOpR op;
   op.seeds = d_seeds;
   op.out = reinterpret_cast<unsigned long long*>(d_mismatch);
+  op.kind = 0;
+  return launch_descs(d_src, d_src, d_bytes, n, HV_ENGINE_LDG, 0, stream, op, false);
+}
+
+HV_EXPORT int hv_verify_weights_bf16(const uint64_t* d_src, const uint64_t* d_bytes, const uint64_t* d_seeds,
+                                     uint32_t n, uint64_t* d_mismatch, void* stream) {
+  if (n == 0) return HV_OK;
+  HV_CHECK_ARG(d_src && d_bytes && d_seeds && d_mismatch);
+  int dev = 0;
+  int st = hv::bind_stream_device(stream, &dev);
+  if (st) return st;
+  HV_CUDA(cudaMemsetAsync(d_mismatch, 0, (size_t)n * 8, (cudaStream_t)stream));
+  VerifyOpR op;
+  op.seeds = d_seeds;
+  op.out = reinterpret_cast<unsigned long long*>(d_mismatch);
+  op.kind = 1;
   return launch_descs(d_src, d_src, d_bytes, n, HV_ENGINE_LDG, 0, stream, op, false);
 }

@@ -128,10 +128,13 @@ def digest(src_ptrs: torch.Tensor, sizes: torch.Tensor, stream=None) -> torch.Te
     return out
 
 
-def verify_content(src_ptrs: torch.Tensor, sizes: torch.Tensor, seeds, stream=None) -> torch.Tensor:
+def verify_content(src_ptrs: torch.Tensor, sizes: torch.Tensor, seeds, stream=None,
+                   weights: bool = False) -> torch.Tensor:
+    """Per-object count of 8-byte words that differ from the generator
+    (``weights=True``: the bf16-weights variant)."""
     sd = seeds if isinstance(seeds, torch.Tensor) else _seeds_tensor(seeds, src_ptrs.device)
     out = torch.empty(src_ptrs.numel(), dtype=torch.int64, device=src_ptrs.device)
-    N.call("hv_verify_content", _dev_u64(src_ptrs, "src_ptrs"), _dev_u64(sizes, "sizes"),
+    N.call("hv_verify_weights_bf16" if weights else "hv_verify_content", _dev_u64(src_ptrs, "src_ptrs"), _dev_u64(sizes, "sizes"),
            _dev_u64(sd, "seeds"), src_ptrs.numel(), out.data_ptr(), N.stream_handle(stream))
     return out
 
