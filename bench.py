@@ -214,7 +214,7 @@ def run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, micro
     return out
 
 
-def host_offload_decode(m, dev, a, microbatches=2, steps=3, warm=2):
+def host_offload_decode(m, dev, a, microbatches=1, steps=3, warm=2):
     """The same decode with every expert served from pinned host DRAM (the
     CPU-offload baseline of PAPER.md §4.5), on this GPU."""
     import torch
@@ -231,7 +231,7 @@ def host_offload_decode(m, dev, a, microbatches=2, steps=3, warm=2):
     return r
 
 
-def same_run_comparisons(dev, m, a, source, n=53):
+def same_run_comparisons(dev, m, a, source, fetcher=None, n=53):
     """Same-box comparisons for one layer's worth of experts (n x 17.3 MB):
     the copy-engine paths on the same source (cudaMemcpyBatchAsync: the
     paper's/vLLM's data path) and the same kernel on a local-HBM source
@@ -270,18 +270,53 @@ def same_run_comparisons(dev, m, a, source, n=53):
                                     "unit": "GB/s", "frac": 2 * n * S / dt / 1e9 / hbm_peak,
                                     "note": "same K2 kernel, local-HBM source: read+write bytes / time vs "
                                             "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"}
+    hd = np.array([dst.data_ptr() + i * S for i in range(n)], dtype=np.uint64)
+    hz = np.full(n, S, dtype=np.uint64)
+    h = HostTier(n * S)
+    hs = np.array([h.host_address(i * S) for i in range(n)], dtype=np.uint64)
+    lat = {}
+    lat["kernel_host"] = t(lambda: F.batch_copy(F.ptrs_tensor([h.device_address(0)], f"cuda:{dev}"), dp[:1],
+                                                sz[:1], engine=a.engine, stream=s.cuda_stream)) * 1e6
+    lat["copy_engine_host"] = t(lambda: F.ce_batch_copy(hs[:1], hd[:1], hz[:1], batched=False,
+                                                        stream=s.cuda_stream)) * 1e6
     if source == "host":
-        h = HostTier(n * S)
-        hs = np.array([h.host_address(i * S) for i in range(n)], dtype=np.uint64)
-        hd = np.array([dst.data_ptr() + i * S for i in range(n)], dtype=np.uint64)
-        hz = np.full(n, S, dtype=np.uint64)
         dce = t(lambda: F.ce_batch_copy(hs, hd, hz, batched=True, stream=s.cuda_stream))
         out["copy_engine_same_source_GBps"] = n * S / dce / 1e9
-        dce1 = t(lambda: F.ce_batch_copy(hs[:1], hd[:1], hz[:1], batched=False, stream=s.cuda_stream))
-        dk1 = t(lambda: F.batch_copy(F.ptrs_tensor([h.device_address(0)], f"cuda:{dev}"), dp[:1], sz[:1],
-                                     engine=a.engine, stream=s.cuda_stream))
-        out["single_expert_latency_us"] = {"kernel_host": dk1 * 1e6, "copy_engine_host": dce1 * 1e6}
-        h.close()
+    else:
+        # peer experts of layer 0 (spread over every donor)
+        ps = np.ascontiguousarray(fetcher.src_addr[0, :n])
+        pdev = F.ptrs_tensor(ps, f"cuda:{dev}")
+        dce = t(lambda: F.ce_batch_copy(ps, hd, hz, batched=True, stream=s.cuda_stream))
+        out["copy_engine_same_source_GBps"] = n * S / dce / 1e9
+        dce_loop = t(lambda: F.ce_batch_copy(ps, hd, hz, batched=False, stream=s.cuda_stream))
+        out["copy_engine_peer_per_object_GBps"] = n * S / dce_loop / 1e9
+        lat["kernel_peer"] = t(lambda: F.batch_copy(pdev[:1], dp[:1], sz[:1], engine=a.engine,
+                                                    stream=s.cuda_stream)) * 1e6
+        lat["copy_engine_peer"] = t(lambda: F.ce_batch_copy(ps[:1], hd[:1], hz[:1], batched=False,
+                                                            stream=s.cuda_stream)) * 1e6
+        lat["peer_vs_host_speedup"] = lat["copy_engine_host"] / lat["kernel_peer"]
+    out["single_expert_latency_us"] = lat
+    # KV config 1 (BASELINE configs[0] shape): 1,024 x 64 KiB pages = one layer
+    # of 4 sequences x 4k tokens, gathered by K1 from the tier under test
+    page, npg = 65536, 1024
+    rng = np.random.default_rng(5)
+    kv = {}
+    kdst = torch.empty(npg * page, dtype=torch.uint8, device=f"cuda:{dev}")
+    hp = HostTier(4 * npg * page)
+    host_pages = F.ptrs_tensor([hp.device_address(int(p) * page) for p in rng.permutation(4 * npg)[:npg]],
+                               f"cuda:{dev}")
+    dt_h = t(lambda: F.kv_gather(host_pages, page, dst=kdst, engine=a.engine, stream=s.cuda_stream))
+    kv["host_us"], kv["host_GBps"] = dt_h * 1e6, npg * page / dt_h / 1e9
+    if source == "peer":
+        base = fetcher.src_addr[0, :n]   # peer memory of n experts viewed as page slots
+        slots = [int(base[i]) + j * page for i in range(n) for j in range(S // page)]
+        peer_pages = F.ptrs_tensor([slots[int(p)] for p in rng.permutation(len(slots))[:npg]], f"cuda:{dev}")
+        dt_p = t(lambda: F.kv_gather(peer_pages, page, dst=kdst, engine=a.engine, stream=s.cuda_stream))
+        kv["peer_us"], kv["peer_GBps"] = dt_p * 1e6, npg * page / dt_p / 1e9
+        kv["peer_vs_host_speedup"] = dt_h / dt_p
+    out["kv_config1_layer_gather"] = kv
+    hp.close()
+    h.close()
     return out
 
 
@@ -499,7 +534,12 @@ def run_b200(a):
 
     # ---- MoE decode tokens/s through the pipelined decoder (moe.py:211-340)
     del desc
-    decode = run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source)
+    # one micro-batch: each stage fetches its layer once (fetch-bound path);
+    # two micro-batches: the reference's CGOPipe overlap (moe.py:327-340)
+    decode = run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, microbatches=1)
+    d2 = run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, microbatches=2)
+    decode["pipelined_2_microbatches"] = {k: d2[k] for k in ("tokens_per_s", "per_rank_tokens_per_s",
+                                                             "ms_per_decode_step", "outputs_finite")}
     sysm.loop.run()
     if world > 1 and rank == 0 and not a.no_host_compare:
         decode["host_offload"] = host_offload_decode(m, dev, a)
@@ -526,7 +566,7 @@ def run_b200(a):
                                       f"({tr['report']}), algorithmic {tr['algorithmic_bytes_per_launch']:.0f} B/launch")
         roof["bytes_per_launch"] = bytes_per_launch
         roof["mean_launch_ms"] = statistics.mean(launch_ms)
-        extra = same_run_comparisons(dev, m, a, source)
+        extra = same_run_comparisons(dev, m, a, source, fetcher)
         cpu = None
         if not a.no_cpu_baseline:
             threads = os.cpu_count() or 1
