@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--out", default=None)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--overlap-max-ctas", type=int, default=64,
+                    help="fetch grid cap in the 2-micro-batch (overlapped) decode")
     ap.add_argument("--no-host-compare", action="store_true",
                     help="N>1: skip rank 0's host-offload decode comparison")
     a = ap.parse_args()
@@ -187,14 +189,15 @@ def measure_pcie_h2d(dev):
     return best
 
 
-def run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, microbatches=2, steps=3, warm=2):
+def run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, microbatches=2, steps=3, warm=2,
+               max_ctas=None):
     """MoE decode tokens/s: batch 32 split into `microbatches`, layer-major
     stages, each stage's experts fetched one stage ahead (K2, device-side
     plan) while the previous stage's SwiGLU experts run on the compute stream."""
     import torch
     from paper_2602_00328_b200.decode import MoEDecoder
     dec = MoEDecoder(fetcher, tokens=TOKENS, microbatches=microbatches, seed=7, engine=a.engine,
-                     max_ctas=a.max_ctas)
+                     max_ctas=a.max_ctas if max_ctas is None else max_ctas)
     h = dec.decode(warm)
     torch.cuda.synchronize()
     barrier()
@@ -315,8 +318,54 @@ def same_run_comparisons(dev, m, a, source, fetcher=None, n=53):
         kv["peer_us"], kv["peer_GBps"] = dt_p * 1e6, npg * page / dt_p / 1e9
         kv["peer_vs_host_speedup"] = dt_h / dt_p
     out["kv_config1_layer_gather"] = kv
+    out.update(latency_curves(dev, a, s, t, h, fetcher if source == "peer" else None))
     hp.close()
     h.close()
+    return out
+
+
+def latency_curves(dev, a, s, t, host, fetcher):
+    """Measured single-object fetch latency vs size on each available tier,
+    refit with the reference's own calibrate() (interconnect.py:168-200), and
+    the paper's KV reload-latency experiment (Fig 7:
+    FP16 KV, 100..8000 entries, host vs peer) measured instead of modeled."""
+    import torch
+    from paper_2602_00328_b200 import fetch as F
+    from paper_2602_00328_b200.interconnect import calibrate, calibration_rms
+    sizes = [65536, 262144, 1 << 20, 4 << 20, 17_301_504]
+    dst = torch.empty(max(sizes) + (8000 * 70_272), dtype=torch.uint8, device=f"cuda:{dev}")
+    tiers = {"host": host.device_address(0)}
+    if fetcher is not None:
+        tiers["peer"] = int(fetcher.src_addr[0, 0])
+    one = F.ptrs_tensor([S for S in [0]], f"cuda:{dev}")
+    curves, fits = {}, {}
+    for name, base in tiers.items():
+        pts = []
+        for nb in sizes:
+            sp = F.ptrs_tensor([base], f"cuda:{dev}")
+            dp = F.ptrs_tensor([dst.data_ptr()], f"cuda:{dev}")
+            sz = F.ptrs_tensor([nb], f"cuda:{dev}")
+            pts.append((nb, t(lambda: F.batch_copy(sp, dp, sz, engine=a.engine, stream=s.cuda_stream))))
+        curves[name] = [[nb, lat * 1e6] for nb, lat in pts]
+        fc, bw = calibrate(pts)
+        fits[name] = {"fixed_cost_us": fc * 1e6, "bandwidth_GBps": bw / 1e9, "rms_rel": calibration_rms(pts, fc, bw)}
+    out = {"latency_vs_size_us": curves, "calibrated_links": fits}
+    if fetcher is not None:
+        rows = []
+        for model, bpe in (("kimi-k2", 70_272), ("mistral-large-3", 12_800)):   # profiles.py:116-122
+            for e in (100, 500, 1000, 2000, 4000, 8000):
+                nb = e * bpe
+                lat = {}
+                for name, base in tiers.items():
+                    sp = F.ptrs_tensor([base], f"cuda:{dev}")
+                    dp = F.ptrs_tensor([dst.data_ptr()], f"cuda:{dev}")
+                    sz = F.ptrs_tensor([nb], f"cuda:{dev}")
+                    lat[name] = t(lambda: F.batch_copy(sp, dp, sz, engine=a.engine, stream=s.cuda_stream))
+                rows.append([model, e, lat["host"] * 1e6, lat["peer"] * 1e6, lat["host"] / lat["peer"]])
+        out["kv_reload_latency_experiment"] = {"columns": ["model", "entries", "host_us", "peer_us", "speedup"],
+                                               "rows": rows,
+                                               "paper_h100": "kimi-k2 5.42x@100 -> 5.68x@8000 (PAPER.md:319)"}
+    del one
     return out
 
 
@@ -537,9 +586,12 @@ def run_b200(a):
     # one micro-batch: each stage fetches its layer once (fetch-bound path);
     # two micro-batches: the reference's CGOPipe overlap (moe.py:327-340)
     decode = run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, microbatches=1)
-    d2 = run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, microbatches=2)
+    # overlap mode: the fetch kernel's grid is capped so decode compute keeps SMs
+    d2 = run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, microbatches=2,
+                    max_ctas=a.overlap_max_ctas)
     decode["pipelined_2_microbatches"] = {k: d2[k] for k in ("tokens_per_s", "per_rank_tokens_per_s",
                                                              "ms_per_decode_step", "outputs_finite")}
+    decode["pipelined_2_microbatches"]["fetch_max_ctas"] = a.overlap_max_ctas
     sysm.loop.run()
     if world > 1 and rank == 0 and not a.no_host_compare:
         decode["host_offload"] = host_offload_decode(m, dev, a)

@@ -1,0 +1,4 @@
+set -x
+mkdir -p gpurun_out
+HV_DEVICE_MAP=0,0 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29515 bench.py --gpus 2 --steps 3 --warmup 3 --dist-backend gloo --no-cpu-baseline --no-host-compare > gpurun_out/r10_bench2.json 2> gpurun_out/r10_bench2.err; tail -3 gpurun_out/r10_bench2.err; cat gpurun_out/r10_bench2.json
+timeout 900 python bench.py > gpurun_out/r10_bench.json 2> gpurun_out/r10_bench.err; tail -3 gpurun_out/r10_bench.err; cat gpurun_out/r10_bench.json
