@@ -82,9 +82,19 @@ class MoEDecoder:
         src = np.where(self.f.tier == 0, self.f.local_addr, self.f.src_addr).astype(np.uint64)
         if np.any(src == 0):
             raise ValueError("an expert has no source address (LOCAL tier needs ExpertFetcher(local_addr=...))")
-        self.addr = torch.from_numpy(src.view(np.int64).copy()).to(self.dev)
-        self.fetchable = torch.from_numpy((self.f.tier != 0).copy()).to(self.dev)
+        new_addr = torch.from_numpy(src.view(np.int64).copy())
+        new_fetchable = torch.from_numpy((self.f.tier != 0).copy())
+        if getattr(self, "addr", None) is None:
+            self.addr = new_addr.to(self.dev)
+            self.fetchable = new_fetchable.to(self.dev)
+        else:
+            # in-flight fetch kernels read the table through raw pointers:
+            # let them finish before it changes (revocations are rare)
+            torch.cuda.synchronize(self.dev)
+            self.addr.copy_(new_addr)
+            self.fetchable.copy_(new_fetchable)
         self.layer_handles = [[h for (l, _e), h in self.f.handles.items() if l == layer] for layer in range(self.L)]
+        self._table_version = getattr(self.f, "version", 0)
 
     # ---------------------------------------------------------------- pieces
     def _route(self, h: torch.Tensor, layer: int, slot: int) -> None:
@@ -128,7 +138,12 @@ class MoEDecoder:
 
     # ---------------------------------------------------------------- step
     def step(self, x: torch.Tensor) -> torch.Tensor:
-        """One decode step over all layers; returns the new hidden states."""
+        """One decode step over all layers; returns the new hidden states.
+        Residency changes (revocation callbacks, re-placement arrivals) seen
+        since the last step are uploaded first; within a step the table is a
+        snapshot, and reads of a handle revoked meanwhile extend its drain."""
+        if getattr(self.f, "version", 0) != self._table_version:
+            self.sync_tables()
         hs = list(x.view(self.nmb, self.tmb, self.H).clone().unbind(0))
         cur = torch.cuda.current_stream(self.dev)
         self.compute.wait_stream(cur)

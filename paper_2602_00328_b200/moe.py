@@ -261,6 +261,7 @@ class ExpertFetcher:
         self.sizes_cache: dict[int, np.ndarray] = {}
 
     def _update(self, layer, expert, tier, handle) -> None:
+        self.version = getattr(self, "version", 0) + 1
         if tier == Tier.LOCAL_HBM:
             self.tier[layer, expert] = 0
             self.handles.pop((layer, expert), None)

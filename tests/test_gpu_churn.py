@@ -1,0 +1,64 @@
+"""Config 5 on one GPU: a donor availability timeline revokes peer experts in
+the middle of a decode and gives capacity back later; rebalance re-places the
+experts.  Decode outputs must stay bit-identical to an all-local run and the
+release ordering must hold on the real event log (verify.py:25-69)."""
+import time
+
+import numpy as np
+import pytest
+import torch
+
+from tests import refcheck
+from tests.test_gpu_decode import RS, _all_local, _tiny
+
+pytestmark = pytest.mark.gpu
+
+
+def test_decode_under_churn_matches_all_local():
+    from paper_2602_00328_b200.churn import AvailabilityProcess, ChurnDriver, expert_tier_counts
+    from paper_2602_00328_b200.decode import MoEDecoder
+    from paper_2602_00328_b200.moe import ExpertFetcher, ExpertResidency, ExpertStore, rebalance
+    from paper_2602_00328_b200.system import HarvestSystem
+    model = _tiny()
+    L, E, S = model.num_layers, model.num_experts, model.expert_size
+    cap = 12 * S
+    sysm = HarvestSystem(0, donors=[0], donor_bytes=cap, host_bytes=L * E * S, local_bytes=1 << 20)
+    store = ExpertStore(model, sysm.host_id, sysm.host)
+    store.fill_host(0, weights=True)
+    res = ExpertResidency(model)
+    counts = np.arange(L * E, dtype=np.int64).reshape(L, E)[::-1].copy()
+    replace = lambda: rebalance(sysm.loop, sysm.runtime, model, res, counts, sysm.host_id, store=store)
+    replace()
+    sysm.loop.run()
+    assert expert_tier_counts(res)["PeerHBM"] == 12
+    fetcher = ExpertFetcher(sysm.runtime, model, res, store)
+    dec = MoEDecoder(fetcher, tokens=16, microbatches=2, seed=0, residual_scale=RS)
+    # availability: full -> 1/3 at 0.15 s -> 0 at 0.3 s -> full at 0.45 s
+    proc = AvailabilityProcess(steps=[(0.0, cap), (0.15, cap // 3), (0.3, 0), (0.45, cap)])
+    drv = ChurnDriver(sysm, {1: proc})
+    drv.start()
+    h = dec.x0
+    peer_counts = []
+    t0 = time.perf_counter()
+    steps = 0
+    while time.perf_counter() - t0 < 0.75 or steps < 4:
+        h = dec.step(h)
+        steps += 1
+        drv.tick(replace)
+        peer_counts.append(expert_tier_counts(res)["PeerHBM"])
+        time.sleep(0.02)
+    torch.cuda.synchronize()
+    sysm.loop.run()
+    revokes = sysm.loop.log.of_kind("revoke_begin")
+    assert revokes and all(r.data["reason"] == "ExternalReclaim" for r in revokes)
+    assert min(peer_counts) == 0                  # everything fell back to host at the 0 step
+    assert expert_tier_counts(res)["PeerHBM"] > 0  # re-placed after capacity returned
+    assert refcheck.verify_release_ordering(sysm.loop.log) == []
+    sys2, dec2, _keep = _all_local(model, 16, 2, 0, store)
+    h2 = dec2.x0
+    for _ in range(steps):
+        h2 = dec2.step(h2)
+    torch.cuda.synchronize()
+    assert torch.equal(h.view(torch.int16), h2.view(torch.int16))
+    sysm.close()
+    sys2.close()
