@@ -189,6 +189,28 @@ def measure_pcie_h2d(dev):
     return best
 
 
+def autotune(layer_desc, stream, stream_h, F, reps=3):
+    """Time one layer's real fetch under each engine x grid cap; pick the fastest."""
+    import torch
+    sp, dp, sz, nb = layer_desc
+    rows = []
+    for engine in ("ldg", "ldg256", "tma"):
+        for max_ctas in (0, 296, 148):
+            for _ in range(1):  # warm
+                F.batch_copy(sp, dp, sz, engine=engine, max_ctas=max_ctas, stream=stream_h)
+            ts = []
+            for _ in range(reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                F.batch_copy(sp, dp, sz, engine=engine, max_ctas=max_ctas, stream=stream_h)
+                e1.record(stream)
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1) * 1e-3)
+            rows.append({"engine": engine, "max_ctas": max_ctas, "GBps": nb / statistics.median(ts) / 1e9})
+    best = max(rows, key=lambda r: r["GBps"])
+    return {"best": best, "candidates": rows}
+
+
 def run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, microbatches=2, steps=3, warm=2,
                max_ctas=None):
     """MoE decode tokens/s: batch 32 split into `microbatches`, layer-major
@@ -487,6 +509,19 @@ def run_b200(a):
         desc.append(row)
     torch.cuda.synchronize()
 
+    # ---- engine / grid autotune on the link actually under test (a few launches
+    # of one layer's real descriptors); "--engine X" pins the choice instead
+    tune = None
+    if a.engine == "auto":
+        tune = autotune(desc[0][0], stream, stream_h, F)
+        a.engine, a.max_ctas = tune["best"]["engine"], tune["best"]["max_ctas"]
+        if world > 1:  # every rank must run the same configuration: rank 0 decides
+            choice = [a.engine, a.max_ctas]
+            dist.broadcast_object_list(choice, src=0)
+            a.engine, a.max_ctas = choice
+        fetcher.engine.engine = N.ENGINES[a.engine]
+        fetcher.engine.max_ctas = a.max_ctas
+
     def value_step(s, evs=None):
         for layer, (sp, dp, sz, nb) in enumerate(desc[s]):
             if evs is not None:
@@ -630,7 +665,8 @@ def run_b200(a):
         line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-                "config": {**workload_config(m, world, source), "engine": a.engine,
+                "config": {**workload_config(m, world, source), "engine": a.engine, "max_ctas": a.max_ctas,
+                           "engine_autotune": tune,
                            "parallelism": f"{world} compute GPU(s)" + (f", each reading N-1={world - 1} donors"
                                                                        if world > 1 else "")},
                 "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": h2d // a.steps,
