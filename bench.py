@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--out", default=None)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--no-kv", action="store_true", help="skip the config-4 long-context KV measurement")
     ap.add_argument("--overlap-max-ctas", type=int, default=64,
                     help="fetch grid cap in the 2-micro-batch (overlapped) decode")
     ap.add_argument("--no-host-compare", action="store_true",
@@ -187,6 +188,62 @@ def measure_pcie_h2d(dev):
     del src
     h.close()
     return best
+
+
+KV_TOKENS, KV_SLAB_BLOCKS = 131072, 64   # BASELINE configs[3]: one 128k-token Llama-3-8B sequence
+
+
+def kv_slab_bytes():
+    from paper_2602_00328_b200.kv import LLAMA3_8B
+    return KV_SLAB_BLOCKS * LLAMA3_8B.block_bytes
+
+
+def kv_long_context(sysm, source, a):
+    """Config 4: a 128k-token Llama-3-8B sequence (8,192 blocks x 32 layers x
+    64 KiB = 16 GiB) is appended (KV produced locally), evicted out of local
+    HBM to harvested peer slabs (N>1, Lossy) or the host tier (N=1, Backed),
+    then reloaded with ONE K1 launch of 262,144 pages.  Reports the kernel
+    time, the end-to-end reload() time, and a content check of sampled pages."""
+    import torch
+    from paper_2602_00328_b200 import fetch as F
+    from paper_2602_00328_b200.kv import LLAMA3_8B, KVCacheManager, kv_seed
+    from paper_2602_00328_b200.runtime import Durability
+    m = LLAMA3_8B
+    nblk = KV_TOKENS // m.block_tokens
+    host = source == "host"
+    kv = KVCacheManager(sysm, m, local_blocks=nblk, host_blocks=nblk if host else 1, slab_blocks=KV_SLAB_BLOCKS,
+                        durability=Durability.BACKED if host else Durability.LOSSY, engine=a.engine,
+                        max_ctas=a.max_ctas)
+    kv.append_kv(0, KV_TOKENS)
+    t0 = time.perf_counter()
+    kv.timing = []
+    moves = kv.evict(nblk * m.block_bytes)
+    evict_wall = time.perf_counter() - t0
+    e_ev0, e_ev1, e_nb = kv.timing[-1]
+    where = {}
+    for _bid, _frm, to in moves:
+        where[to] = where.get(to, 0) + 1
+    ids = sorted(kv.table)
+    kv.timing = []
+    t0 = time.perf_counter()
+    plan = kv.reload(ids)
+    sysm.engine.synchronize()
+    wall = time.perf_counter() - t0
+    ev0, ev1, nb = kv.timing[-1]
+    ms = ev0.elapsed_time(ev1)
+    rng = np.random.default_rng(0)
+    sample = [(int(l), int(b)) for l, b in zip(rng.integers(0, m.num_layers, 64), rng.integers(0, nblk, 64))]
+    ptrs = [kv.cache[l, kv.table[b].slot].data_ptr() for l, b in sample]
+    bad = F.verify_content(F.ptrs_tensor(ptrs, kv.dev), F.ptrs_tensor([m.page_bytes] * len(ptrs), kv.dev),
+                           [kv_seed(l, 0, kv.table[b].index) for l, b in sample])
+    out = {"sequence_tokens": KV_TOKENS, "blocks": nblk, "pages": nblk * m.num_layers, "bytes": nb,
+           "evicted_to": where, "reload_from": {k: len(v) for k, v in plan.items()},
+           "reload_kernel_ms": ms, "reload_kernel_GBps": nb / (ms * 1e-3) / 1e9,
+           "reload_e2e_ms": wall * 1e3, "evict_kernel_ms": e_ev0.elapsed_time(e_ev1),
+           "evict_e2e_ms": evict_wall * 1e3, "sampled_pages_mismatched_words": int(bad.sum()),
+           "model": "llama-3-8b: 32 layers x 8 KV heads x 128 x fp16, 16-token blocks"}
+    kv.close()
+    return out
 
 
 def autotune(layer_desc, stream, stream_h, F, reps=3):
@@ -452,6 +509,8 @@ def run_b200(a):
         source = "peer"
         others = [r for r in range(world) if r != rank]
         per_reader = math.ceil(L * E / (world - 1)) * S
+        if not a.no_kv:  # room for config 4's 128k-token KV sequence (128 slabs of 128 MiB)
+            per_reader += math.ceil((KV_TOKENS // 16) / KV_SLAB_BLOCKS / (world - 1)) * kv_slab_bytes()
         my_pool = PeerPool(dev, per_reader * (world - 1), readers=[dev], mode="ipc")
         handles = [None] * world
         dist.all_gather_object(handles, my_pool.export_ipc())
@@ -628,6 +687,11 @@ def run_b200(a):
                                                              "ms_per_decode_step", "outputs_finite")}
     decode["pipelined_2_microbatches"]["fetch_max_ctas"] = a.overlap_max_ctas
     sysm.loop.run()
+    kvlc = None
+    if not a.no_kv:
+        kvlc = kv_long_context(sysm, source, a)
+        kvlc["reload_kernel_GBps_all_ranks_min"] = -max_over_ranks(-kvlc["reload_kernel_GBps"])
+    barrier()
     if world > 1 and rank == 0 and not a.no_host_compare:
         decode["host_offload"] = host_offload_decode(m, dev, a)
         decode["speedup_vs_host_offload_per_gpu"] = (decode["per_rank_tokens_per_s"]
@@ -673,7 +737,8 @@ def run_b200(a):
                         "d2h_bytes_per_step": d2h // a.steps, "verify_mismatched_words": int(mism_all)},
                 "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
                 "clocks": clk.summary(),
-                "latency_ms_per_layer_fetch": statistics.median(launch_ms), "decode": decode, **extra}
+                "latency_ms_per_layer_fetch": statistics.median(launch_ms), "decode": decode,
+                "kv_long_context_128k": kvlc, **extra}
         emit(line, a)
     barrier()
     sysm.close()

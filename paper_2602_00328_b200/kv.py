@@ -133,8 +133,10 @@ class KVCacheManager:
 
     def __init__(self, system, model: KVModelSpec, local_blocks: int, host_blocks: int,
                  policy: OffloadPolicy | None = None, slab_blocks: int = 32,
-                 durability: Durability = Durability.LOSSY, engine: str = "auto", max_ctas: int = 0):
+                 durability: Durability = Durability.LOSSY, engine: str = "auto", max_ctas: int = 0,
+                 spread: bool = True):
         self.sys = system
+        self.spread = spread
         self.rt = system.runtime
         self.m = model
         self.policy = policy or OffloadPolicy()
@@ -196,8 +198,15 @@ class KVCacheManager:
             if on_done:
                 on_done()
 
+        timing = getattr(self, "timing", None)
+        if timing is not None:  # kernel-only time of this launch, on the fetch stream
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(torch.cuda.ExternalStream(self.stream, device=self.dev))
         self.sys.engine.launch_pages(dbuf.data_ptr(), n, self.page, dst_page_ptrs_dev=dbuf.data_ptr() + 8 * n,
                                      callbacks=[_done])
+        if timing is not None:
+            ev1.record(torch.cuda.ExternalStream(self.stream, device=self.dev))
+            timing.append((ev0, ev1, n * self.page))
 
     # ------------------------------------------------------------ append
     def append_kv(self, sequence_id: int, tokens: int, durability: Durability | None = None) -> list[int]:
@@ -209,6 +218,7 @@ class KVCacheManager:
         blocks = self.seq_blocks.setdefault(sequence_id, [])
         touched = []
         now = self.sys.loop.now
+        self._pending_fill = []
         while tokens > 0:
             tail = self.table[blocks[-1]] if blocks else None
             if tail is not None and tail.entries < self.m.block_tokens:
@@ -231,8 +241,17 @@ class KVCacheManager:
             blocks.append(bid)
             tokens -= take
             touched.append(bid)
-            self._materialize([b])
+            self._pending_fill.append(b)
+        self._flush_fill()
         return touched
+
+    def _flush_fill(self) -> None:
+        """Materialize the content of blocks created since the last flush (one
+        fill launch); must run before any of them can be evicted."""
+        pend = getattr(self, "_pending_fill", None)
+        if pend:
+            self._pending_fill = []
+            self._materialize(pend)
 
     def _materialize(self, blocks: list[KVBlock]) -> None:
         """Write the blocks' synthetic KV content into their local slots."""
@@ -255,6 +274,7 @@ class KVCacheManager:
     def _take_local_slot(self) -> int:
         limit = int(self.policy.local_watermark * self.local_blocks)
         if self._local_used() + 1 > limit or not self.local_free:
+            self._flush_fill()
             self.evict(self.m.block_bytes * max(1, self._local_used() + 1 - limit))
         if not self.local_free:
             raise TierExhausted("local HBM has no free KV slot after eviction")
@@ -272,16 +292,25 @@ class KVCacheManager:
         return local
 
     def _peer_slot(self, durability: Durability) -> tuple[int, int] | None:
+        cur = getattr(self, "_open_slab", 0)
+        if cur < len(self.slabs) and self.slabs[cur].live and self.slabs[cur].free:
+            return cur, self.slabs[cur].free.pop()
         for i, s in enumerate(self.slabs):
             if s.live and s.free:
+                self._open_slab = i
                 return i, s.free.pop()
+        peers = [st.spec.device_id for st in self.rt.peer_states()]
+        # round-robin preference over donors (runtime.py:205-214 hint): a big
+        # reload then reads every donor's NVLink egress at once
+        pref = [peers[len(self.slabs) % len(peers)]] if (self.spread and peers) else None
         h = self.rt.harvest_alloc(self.slab_blocks * self.L * self.page,
-                                  AllocationHints(durability=durability, client_id="kv"))
+                                  AllocationHints(preferred_devices=pref, durability=durability, client_id="kv"))
         if h is None:
             return None
         idx = len(self.slabs)
         slab = _Slab(h, self.rt.address(h), free=list(range(self.slab_blocks - 1, -1, -1)))
         self.slabs.append(slab)
+        self._open_slab = idx
         self.rt.set_tag(h, ("kv-slab", idx))
         self.rt.harvest_register_cb(h, lambda hh, reason, idx=idx: self._on_revoke(idx, reason))
         return idx, slab.free.pop()
