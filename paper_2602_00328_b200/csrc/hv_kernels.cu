@@ -618,7 +618,8 @@ int launch_pages(PageResolver<kTable> res, int engine, int max_ctas, void* strea
 // grid is sized to fill the device (capped by max_ctas).
 template <typename Op>
 int launch_descs(const uint64_t* d_src, const uint64_t* d_dst, const uint64_t* d_bytes, uint32_t n,
-                 int engine, int max_ctas, void* stream, Op op, bool is_copy) {
+                 int engine, int max_ctas, void* stream, Op op, bool is_copy,
+                 uint64_t chunks_hint = kUnknownChunks) {
   int dev = 0;
   int st = hv::bind_stream_device(stream, &dev);
   if (st) return st;
@@ -635,14 +636,14 @@ int launch_descs(const uint64_t* d_src, const uint64_t* d_dst, const uint64_t* d
     o.rebase(base);
     if (is_copy && engine == HV_ENGINE_TMA) {
       res.chunk = kTmaChunk;
-      desc_copy_tma<<<tma_grid(dev, kUnknownChunks, max_ctas), kTmaThreads, kTmaSmem, (cudaStream_t)stream>>>(res);
+      desc_copy_tma<<<tma_grid(dev, chunks_hint, max_ctas), kTmaThreads, kTmaSmem, (cudaStream_t)stream>>>(res);
     } else if (is_copy && engine == HV_ENGINE_LDG256) {
       res.chunk = kLdgChunk;
-      desc_op_kernel<<<ldg_grid(dev, kUnknownChunks, max_ctas), kLdgThreads, 0, (cudaStream_t)stream>>>(
+      desc_op_kernel<<<ldg_grid(dev, chunks_hint, max_ctas), kLdgThreads, 0, (cudaStream_t)stream>>>(
           res, CopyOpT<true>{});
     } else if (engine == HV_ENGINE_LDG || !is_copy) {
       res.chunk = kLdgChunk;
-      desc_op_kernel<<<ldg_grid(dev, kUnknownChunks, max_ctas), kLdgThreads, 0, (cudaStream_t)stream>>>(res, o);
+      desc_op_kernel<<<ldg_grid(dev, chunks_hint, max_ctas), kLdgThreads, 0, (cudaStream_t)stream>>>(res, o);
     } else {
       return HV_E_INVALID;
     }
@@ -788,11 +789,36 @@ HV_EXPORT int hv_swap_blocks_batch(const uint64_t* h_src, const uint64_t* h_dst,
     if ((st = ring_acquire(dev, &slot, &ring))) return st;
     uint64_t* hs = ring->h + (size_t)slot * 3 * kSlotDescs;
     uint64_t* ds = ring->d + (size_t)slot * 3 * kSlotDescs;
+    // sizes are host-visible here: detect the uniform case (expert / page
+    // batches) and the exact chunk count, so the launch needs no device-side
+    // prefix scan and its grid matches the work
+    bool uniform = true;
+    uint64_t total_bytes = 0;
+    for (uint32_t i = 0; i < m; ++i) {
+      uniform &= (h_bytes[base + i] == h_bytes[base]);
+      total_bytes += h_bytes[base + i];
+    }
+    // packed [src m][dst m][bytes m]: one H2D of exactly what is used
     memcpy(hs, h_src + base, m * 8);
-    memcpy(hs + kSlotDescs, h_dst + base, m * 8);
-    memcpy(hs + 2 * kSlotDescs, h_bytes + base, m * 8);
-    HV_CUDA(cudaMemcpyAsync(ds, hs, (size_t)3 * kSlotDescs * 8, cudaMemcpyHostToDevice, (cudaStream_t)stream));
-    st = launch_descs(ds, ds + kSlotDescs, ds + 2 * kSlotDescs, m, engine, max_ctas, stream, CopyOpR{}, true);
+    memcpy(hs + m, h_dst + base, m * 8);
+    memcpy(hs + 2 * m, h_bytes + base, m * 8);
+    HV_CUDA(cudaMemcpyAsync(ds, hs, (size_t)(uniform ? 2 : 3) * m * 8, cudaMemcpyHostToDevice,
+                            (cudaStream_t)stream));
+    if (uniform && h_bytes[base] > 0) {
+      PageResolver<false> r{};
+      r.src = ds;
+      r.locs = nullptr;
+      r.dst_ptrs = ds + m;
+      r.dst_base = 0;
+      r.page_bytes = h_bytes[base];
+      r.n_pages = m;
+      st = launch_pages(r, engine, max_ctas, stream);
+    } else if (!uniform) {
+      const int eng = pick_engine(engine);
+      const uint64_t chunk = eng == HV_ENGINE_TMA ? kTmaChunk : kLdgChunk;
+      const uint64_t chunks = total_bytes / chunk + m;  // upper bound on the chunk count
+      st = launch_descs(ds, ds + m, ds + 2 * m, m, engine, max_ctas, stream, CopyOpR{}, true, chunks);
+    }
     if (st) return st;
     HV_CUDA(cudaEventRecord(ring->ev[slot], (cudaStream_t)stream));
     ring->used[slot] = true;
