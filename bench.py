@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--out", default=None)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--no-kv", action="store_true", help="skip the config-4 long-context KV measurement")
+    ap.add_argument("--no-phi", action="store_true", help="N>1: skip the config-3 Phi-3.5-MoE decode phase")
+    ap.add_argument("--phi-layers", type=int, default=32,
+                    help="layers of the Phi-3.5-MoE phase (32 = the real model; fewer only for single-GPU tests)")
     ap.add_argument("--overlap-max-ctas", type=int, default=64,
                     help="fetch grid cap in the 2-micro-batch (overlapped) decode")
     ap.add_argument("--no-host-compare", action="store_true",
@@ -739,14 +742,129 @@ def run_b200(a):
                 "clocks": clk.summary(),
                 "latency_ms_per_layer_fetch": statistics.median(launch_ms), "decode": decode,
                 "kv_long_context_128k": kvlc, **extra}
-        emit(line, a)
     barrier()
     sysm.close()
     for p in imported:
         p.close()
+    barrier()
+    if world > 1:
+        del my_pool  # every reader closed its import above
+        import gc
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        phi = None
+        if not a.no_phi:
+            try:
+                phi = phi_phase(world, rank, dev, a, dist, barrier, max_over_ranks)
+            except Exception as e:  # report, never lose the main line
+                phi = {"error": repr(e)[:300]}
+        if rank == 0:
+            line["phi35_config3"] = phi
+    elif rank == 0:
+        line["phi35_config3"] = {"skipped": "config 3 spreads the expert cache over 7 donor B200s; "
+                                            "N=1 has no donors (host-tier decode is reported under 'decode')"}
+    if rank == 0:
+        emit(line, a)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def phi_phase(world, rank, dev, a, dist, barrier, max_over_ranks, batches=(1, 16, 64)):
+    """BASELINE configs[2]: Phi-3.5-MoE-shaped experts (32 layers x 16 experts,
+    top-2, 157,286,400 B each) placed by each rank's runtime across its N-1
+    donors (up to 7), decode tokens/s at batch 1/16/64.  Rank 0 also times the
+    same layers served from pinned host DRAM on a 4-layer slice."""
+    import torch
+    from paper_2602_00328_b200 import fetch as F
+    from paper_2602_00328_b200.decode import MoEDecoder
+    from paper_2602_00328_b200.memalloc import Tier
+    from paper_2602_00328_b200.moe import (PHI35_MOE, ExpertFetcher, ExpertResidency, ExpertStore, MoEProfile,
+                                           expert_content)
+    from paper_2602_00328_b200.pool import HostTier, PeerPool
+    from paper_2602_00328_b200.runtime import AllocationHints, Durability
+    from paper_2602_00328_b200.system import HarvestSystem
+    m = PHI35_MOE
+    if a.phi_layers != m.num_layers:
+        m = MoEProfile(m.name, a.phi_layers, m.num_experts, m.top_k, m.expert_size, hidden=m.hidden,
+                       intermediate=m.intermediate)
+    L, E, S = m.num_layers, m.num_experts, m.expert_size
+    others = [r for r in range(world) if r != rank]
+    per_reader = math.ceil(L * E / (world - 1)) * S
+    pool = PeerPool(dev, per_reader * (world - 1), readers=[dev], mode="ipc")
+    handles = [None] * world
+    dist.all_gather_object(handles, pool.export_ipc())
+    imported, views = [], {}
+    for i, d in enumerate(others, start=1):
+        p = PeerPool.import_ipc(handles[d], d, per_reader * (world - 1), dev)
+        imported.append(p)
+        views[i] = p.view([r for r in range(world) if r != d].index(rank) * per_reader, per_reader)
+    sysm = HarvestSystem(dev, pools=views, local_bytes=1, engine=a.engine, max_ctas=a.max_ctas, log_transfers=False)
+    rt = sysm.runtime
+    res = ExpertResidency(m)
+    ptrs, seeds = [], []
+    for layer in range(L):
+        for e in range(E):
+            h = rt.harvest_alloc(S, AllocationHints(preferred_devices=[1 + (layer * E + e) % (world - 1)],
+                                                    durability=Durability.BACKED, client_id="moe"))
+            assert h is not None, "donor capacity exhausted"
+            res.set_tier(layer, e, Tier.PEER_HBM, h)
+            ptrs.append(rt.address(h))
+            seeds.append(expert_content(m, layer, e))
+    for i in range(0, len(ptrs), 32):
+        F.fill_weights_bf16(F.ptrs_tensor(ptrs[i:i + 32], f"cuda:{dev}"), F.ptrs_tensor([S] * len(ptrs[i:i + 32]), f"cuda:{dev}"),
+                            seeds[i:i + 32])
+    torch.cuda.synchronize()
+    barrier()
+    fetcher = ExpertFetcher(rt, m, res, ExpertStore(m, sysm.host_id, None))
+    out = {"model": f"{m.name}: {L} layers x {E} experts x {S} B, top-{m.top_k}", "donors_per_rank": world - 1}
+    for b in batches:
+        dec = MoEDecoder(fetcher, tokens=b, microbatches=1, seed=11)
+        h = dec.decode(1)
+        torch.cuda.synchronize()
+        barrier()
+        cur = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cur)
+        h = dec.decode(3, h)
+        e1.record(cur)
+        e1.synchronize()
+        dt = max_over_ranks(e0.elapsed_time(e1) * 1e-3)
+        out[f"batch{b}"] = {"tokens_per_s": b * 3 * world / dt, "per_rank_tokens_per_s": b * 3 / dt,
+                            "ms_per_layer": dt / 3 / L * 1e3, "outputs_finite": bool(torch.isfinite(h.float()).all())}
+        del dec
+        torch.cuda.empty_cache()
+    sysm.loop.run()
+    if rank == 0 and not a.no_host_compare:
+        try:  # host-offload baseline on a 4-layer slice (75 GiB would not fit pinned next to the rest)
+            ms = MoEProfile(m.name, 4, E, m.top_k, S, hidden=m.hidden, intermediate=m.intermediate)
+            host = HostTier(4 * E * S)
+            hsys = HarvestSystem(dev, host_tier=host, local_bytes=1, engine=a.engine, log_transfers=False)
+            st = ExpertStore(ms, hsys.host_id, host)
+            st.fill_host(dev, weights=True)
+            hf = ExpertFetcher(hsys.runtime, ms, ExpertResidency(ms), st)
+            for b in batches:
+                dec = MoEDecoder(hf, tokens=b, microbatches=1, seed=11)
+                dec.decode(1)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                dec.decode(2)
+                torch.cuda.synchronize()
+                host_ms_layer = (time.perf_counter() - t0) / 2 / 4 * 1e3
+                out[f"batch{b}"]["host_offload_ms_per_layer"] = host_ms_layer
+                out[f"batch{b}"]["speedup_vs_host_offload"] = host_ms_layer / out[f"batch{b}"]["ms_per_layer"]
+                del dec
+            hsys.close()
+        except Exception as e:
+            out["host_compare_error"] = repr(e)[:300]
+    barrier()
+    sysm.close()
+    for p in imported:
+        p.close()
+    barrier()
+    pool.close()
+    return out
 
 
 def main():

@@ -122,6 +122,10 @@ int hv_pool_import_ipc(const void* handle64, int donor_dev, uint64_t bytes,
 
 /* ---- host tier: pinned, portable, mapped ------------------------------- */
 int hv_host_alloc(uint64_t bytes, void** h_ptr, uint64_t* d_alias);
+/* flags: HV_HOST_WRITE_COMBINED = cudaHostAllocWriteCombined (non-snooped
+ * PCIe reads; CPU reads of the region become very slow) */
+#define HV_HOST_WRITE_COMBINED 1u
+int hv_host_alloc_flags(uint64_t bytes, unsigned flags, void** h_ptr, uint64_t* d_alias);
 int hv_host_free(void* h_ptr);
 /* pin an existing host range (cudaHostRegister, mapped+portable) */
 int hv_host_register(void* h_ptr, uint64_t bytes, uint64_t* d_alias);

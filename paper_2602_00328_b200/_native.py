@@ -78,6 +78,7 @@ _SIGS = {
     "hv_pool_export_ipc": [vp, vp],
     "hv_pool_import_ipc": [vp, i32, u64, i32, C.POINTER(vp)],
     "hv_host_alloc": [u64, C.POINTER(vp), P64],
+    "hv_host_alloc_flags": [u64, C.c_uint, C.POINTER(vp), P64],
     "hv_host_free": [vp],
     "hv_host_register": [vp, u64, P64],
     "hv_host_unregister": [vp],

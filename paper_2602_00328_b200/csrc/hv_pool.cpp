@@ -364,6 +364,24 @@ HV_EXPORT int hv_host_alloc(uint64_t bytes, void** h_ptr, uint64_t* d_alias) {
   return HV_OK;
 }
 
+HV_EXPORT int hv_host_alloc_flags(uint64_t bytes, unsigned flags, void** h_ptr, uint64_t* d_alias) {
+  HV_CHECK_ARG(h_ptr && bytes > 0);
+  unsigned f = cudaHostAllocPortable | cudaHostAllocMapped;
+  if (flags & HV_HOST_WRITE_COMBINED) f |= cudaHostAllocWriteCombined;
+  void* p = nullptr;
+  HV_CUDA(cudaHostAlloc(&p, bytes, f));
+  void* d = nullptr;
+  cudaError_t e = cudaHostGetDevicePointer(&d, p, 0);
+  if (e != cudaSuccess) {
+    cudaFreeHost(p);
+    (void)cudaGetLastError();
+    return hv_cuda_status(e);
+  }
+  *h_ptr = p;
+  if (d_alias) *d_alias = (uint64_t)d;
+  return HV_OK;
+}
+
 HV_EXPORT int hv_host_free(void* h_ptr) {
   if (!h_ptr) return HV_OK;
   HV_CUDA(cudaFreeHost(h_ptr));

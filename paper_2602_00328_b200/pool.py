@@ -113,11 +113,12 @@ class PoolView:
 class HostTier:
     """Pinned + mapped host memory; ``d_alias`` is its device-visible address."""
 
-    def __init__(self, nbytes: int):
+    def __init__(self, nbytes: int, write_combined: bool = False):
         self.nbytes = nbytes
+        self.write_combined = write_combined
         self.h_ptr = C.c_void_p()
         alias = C.c_uint64()
-        N.call("hv_host_alloc", nbytes, C.byref(self.h_ptr), C.byref(alias))
+        N.call("hv_host_alloc_flags", nbytes, 1 if write_combined else 0, C.byref(self.h_ptr), C.byref(alias))
         self.d_alias = alias.value
 
     def view(self) -> np.ndarray:

@@ -46,9 +46,11 @@ def main():
             "torch_copy_us": gpu_time(lambda: dst[:nb].copy_(src[:nb]), torch.cuda.current_stream()),
         }
     # ExpertFetcher.issue_fetches host cost per call (53 experts, host tier)
+    # 4 KiB "experts": GPU time is negligible, so the host time is the overhead
     m = QWEN15_MOE_A27B
+    m = type(m)(m.name, 2, m.num_experts, m.top_k, 4096, hidden=m.hidden, intermediate=m.intermediate)
     sysm = HarvestSystem(dev, host_bytes=2 * m.num_experts * m.expert_size, local_bytes=1, log_transfers=False)
-    small = type(m)(m.name, 2, m.num_experts, m.top_k, m.expert_size, hidden=m.hidden, intermediate=m.intermediate)
+    small = m
     store = ExpertStore(small, sysm.host_id, sysm.host)
     fetcher = ExpertFetcher(sysm.runtime, small, ExpertResidency(small), store)
     stage = torch.empty(m.num_experts * m.expert_size, dtype=torch.uint8, device="cuda")
@@ -64,6 +66,18 @@ def main():
     host_us = (time.perf_counter() - t0) / n * 1e6
     sysm.loop.run()
     out["issue_fetches_host_us_per_call_53_experts"] = host_us
+    import cProfile
+    import io
+    import pstats
+    pr = cProfile.Profile()
+    pr.enable()
+    for i in range(n):
+        fetcher.issue_fetches(i % 2, ex, ptrs[:53])
+    pr.disable()
+    sio = io.StringIO()
+    pstats.Stats(pr, stream=sio).sort_stats("tottime").print_stats(12)
+    out["profile"] = sio.getvalue().splitlines()[:40]
+    sysm.loop.run()
     sysm.close()
     print(json.dumps(out, indent=1))
 
