@@ -59,9 +59,15 @@ class MoEDecoder:
         self.router = [(torch.randn(self.E, self.H, generator=g) * router_scale / self.H ** 0.5)
                        .to(torch.bfloat16).to(self.dev) for _ in range(self.L)]
         self.x0 = (torch.randn(tokens, self.H, generator=g) * 0.5).to(torch.bfloat16).to(self.dev)
-        self.staging = [torch.zeros(self.E, self.S, dtype=torch.uint8, device=self.dev) for _ in range(2)]
-        self.dst_ptrs = [torch.tensor([b.data_ptr() + e * self.S for e in range(self.E)], dtype=torch.int64,
-                                      device=self.dev) for b in self.staging]
+        # at most K experts can be active in one stage: K compact staging slots
+        # per buffer; expert e goes to slot rank(e) among the active ones
+        self.K = min(self.E, (tokens // microbatches) * m.top_k)
+        self.staging = [torch.zeros(self.K, self.S, dtype=torch.uint8, device=self.dev) for _ in range(2)]
+        self.slot_base = [b.data_ptr() for b in self.staging]
+        self.dst_ptrs = [torch.zeros(self.E, dtype=torch.int64, device=self.dev) for _ in range(2)]
+        self.idx = [torch.zeros(self.K, dtype=torch.int64, device=self.dev) for _ in range(2)]
+        self.valid = [torch.zeros(self.K, dtype=torch.bool, device=self.dev) for _ in range(2)]
+        self._kslots = torch.arange(self.K, device=self.dev)
         self.compute = torch.cuda.Stream(self.dev)
         self.fetch_stream_h = eng.stream
         self.fetch = torch.cuda.ExternalStream(eng.stream, device=self.dev)
@@ -107,17 +113,27 @@ class MoEDecoder:
         active = (comb > 0).any(dim=0)
         torch.where(active, torch.full_like(self.sizes[slot], self.S), torch.zeros_like(self.sizes[slot]),
                     out=self.sizes[slot])
+        # compact placement: rank among active experts -> staging slot; the
+        # K slot owners in order (active first, stable) for the FFN
+        rank = torch.cumsum(active.to(torch.int64), 0) - 1
+        torch.add(rank.clamp_(min=0) * self.S, self.slot_base[slot], out=self.dst_ptrs[slot])
+        order = torch.argsort((~active).to(torch.int8), stable=True)[:self.K]
+        self.idx[slot].copy_(order)
+        torch.lt(self._kslots, active.sum(), out=self.valid[slot])
 
     def _ffn(self, h: torch.Tensor, slot: int, buf: int) -> torch.Tensor:
-        E, I, H = self.E, self.I, self.H
-        w = self.staging[buf].view(torch.bfloat16).view(E, 3 * I * H)
-        gate = w[:, :I * H].view(E, I, H)
-        up = w[:, I * H:2 * I * H].view(E, I, H)
-        down = w[:, 2 * I * H:].view(E, H, I)
-        x = h.unsqueeze(0).expand(E, h.shape[0], H)
+        K, I, H = self.K, self.I, self.H
+        w = self.staging[buf].view(torch.bfloat16).view(K, 3 * I * H)
+        gate = w[:, :I * H].view(K, I, H)
+        up = w[:, I * H:2 * I * H].view(K, I, H)
+        down = w[:, 2 * I * H:].view(K, H, I)
+        x = h.unsqueeze(0).expand(K, h.shape[0], H)
         a = TF.silu(torch.bmm(x, gate.transpose(1, 2))) * torch.bmm(x, up.transpose(1, 2))
-        y = torch.bmm(a, down.transpose(1, 2))                       # [E, T, H]
-        wts = self.comb[slot].t().unsqueeze(-1).to(y.dtype)          # [E, T, 1]
+        y = torch.bmm(a, down.transpose(1, 2))                       # [K, T, H]
+        # combine weights of the slot owners; unused slots (stale but finite
+        # bytes) get weight exactly 0
+        wk = self.comb[slot].index_select(1, self.idx[slot]) * self.valid[slot].to(torch.float32)
+        wts = wk.t().unsqueeze(-1).to(y.dtype)                       # [K, T, 1]
         return (y * wts).sum(0)
 
     def _issue_fetch(self, s: int, ready: torch.cuda.Event, buf_free: torch.cuda.Event | None) -> torch.cuda.Event:
