@@ -65,7 +65,9 @@ class MoEDecoder:
         self.staging = [torch.zeros(self.K, self.S, dtype=torch.uint8, device=self.dev) for _ in range(2)]
         self.slot_base = [b.data_ptr() for b in self.staging]
         self.dst_ptrs = [torch.zeros(self.E, dtype=torch.int64, device=self.dev) for _ in range(2)]
-        self.idx = [torch.zeros(self.K, dtype=torch.int64, device=self.dev) for _ in range(2)]
+        self.idx_ext = [torch.zeros(self.K + 1, dtype=torch.int64, device=self.dev) for _ in range(2)]
+        self.idx = [x[:self.K] for x in self.idx_ext]
+        self._earange = torch.arange(self.E, device=self.dev)
         self.valid = [torch.zeros(self.K, dtype=torch.bool, device=self.dev) for _ in range(2)]
         self._kslots = torch.arange(self.K, device=self.dev)
         self.compute = torch.cuda.Stream(self.dev)
@@ -116,9 +118,11 @@ class MoEDecoder:
         # compact placement: rank among active experts -> staging slot; the
         # K slot owners in order (active first, stable) for the FFN
         rank = torch.cumsum(active.to(torch.int64), 0) - 1
+        # slot owners: scatter e into position rank(e) (inactive -> dummy slot K)
+        ext = self.idx_ext[slot]
+        ext.zero_()
+        ext.scatter_(0, torch.where(active, rank, self.K), self._earange)
         torch.add(rank.clamp_(min=0) * self.S, self.slot_base[slot], out=self.dst_ptrs[slot])
-        order = torch.argsort((~active).to(torch.int8), stable=True)[:self.K]
-        self.idx[slot].copy_(order)
         torch.lt(self._kslots, active.sum(), out=self.valid[slot])
 
     def _ffn(self, h: torch.Tensor, slot: int, buf: int) -> torch.Tensor:
