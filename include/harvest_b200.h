@@ -69,6 +69,8 @@ int hv_can_access_peer(int reader, int donor, int* ok);
 /* cudaDeviceEnablePeerAccess(donor) on `reader`; idempotent */
 int hv_enable_peer_access(int reader, int donor);
 int hv_device_synchronize(int device);
+/* cudaMemGetInfo on `device`: the donor's real free HBM (co-tenant pressure) */
+int hv_mem_get_info(int device, uint64_t* free_bytes, uint64_t* total_bytes);
 
 /* ---- native best-fit segment allocator (memalloc.py:67-159) ------------- */
 typedef struct hv_seg hv_seg;

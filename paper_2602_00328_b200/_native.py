@@ -59,6 +59,7 @@ _SIGS = {
     "hv_can_access_peer": [i32, i32, C.POINTER(i32)],
     "hv_enable_peer_access": [i32, i32],
     "hv_device_synchronize": [i32],
+    "hv_mem_get_info": [i32, P64, P64],
     "hv_seg_create": [u64, C.POINTER(vp)],
     "hv_seg_destroy": [vp],
     "hv_seg_alloc": [vp, u64, P64],

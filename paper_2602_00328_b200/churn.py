@@ -98,6 +98,50 @@ class ChurnDriver:
         return {"revoked": len(self.sys.loop.log.of_kind("revoke_begin")), "migrated": len(migrated)}
 
 
+def mem_get_info(device: int) -> tuple[int, int]:
+    """(free, total) HBM bytes of a CUDA device (hv_mem_get_info)."""
+    import ctypes as C
+
+    from . import _native as N
+    free, total = C.c_uint64(), C.c_uint64()
+    N.call("hv_mem_get_info", device, C.byref(free), C.byref(total))
+    return free.value, total.value
+
+
+class DonorMonitor:
+    """Real co-tenant pressure: poll each donor GPU's free HBM (cudaMemGetInfo)
+    and set the runtime's availability ceiling for that peer to what the
+    harvest currently holds plus what is still free, minus a safety headroom.
+    A drop triggers the reference's own reclaim (runtime.py:476-487): LRU
+    revocation, drained, invalidated, called back, and the VMM chunks
+    unmapped so the co-tenant gets the memory."""
+
+    def __init__(self, system, headroom: int = 1 << 30, meminfo=None):
+        self.sys = system
+        self.rt = system.runtime
+        self.headroom = headroom
+        self.meminfo = meminfo or mem_get_info
+        self.last: dict[int, int] = {}
+
+    def level(self, peer_id: int) -> int:
+        pool = self.sys.pools[peer_id]
+        free, _total = self.meminfo(pool.donor)
+        held = pool.committed_bytes   # HBM this harvest already holds on the donor
+        return max(0, int(free) + int(held) - self.headroom)
+
+    def poll(self) -> dict:
+        """Apply the current levels now; returns {peer_id: level}."""
+        out = {}
+        for peer_id in self.sys.pools:
+            lv = min(self.level(peer_id), self.rt.devices[peer_id].spec.usable)
+            if self.last.get(peer_id) != lv:
+                self.rt._availability_step(peer_id, lv)
+                self.last[peer_id] = lv
+            out[peer_id] = lv
+        self.sys.loop.poll()
+        return out
+
+
 def expert_tier_counts(residency) -> dict:
     c = {t.value: 0 for t in Tier}
     for e in residency.entries.values():

@@ -416,6 +416,20 @@ HV_EXPORT int hv_device_count(int* n) {
   return HV_OK;
 }
 
+HV_EXPORT int hv_mem_get_info(int device, uint64_t* free_bytes, uint64_t* total_bytes) {
+  HV_CHECK_ARG(free_bytes && total_bytes);
+  int cur = -1;
+  HV_CUDA(cudaGetDevice(&cur));
+  if (cur != device) HV_CUDA(cudaSetDevice(device));
+  size_t f = 0, t = 0;
+  cudaError_t e = cudaMemGetInfo(&f, &t);
+  if (cur != device) cudaSetDevice(cur);
+  HV_CUDA(e);
+  *free_bytes = f;
+  *total_bytes = t;
+  return HV_OK;
+}
+
 HV_EXPORT int hv_sm_count(int device, int* n) {
   HV_CHECK_ARG(n);
   HV_CUDA(cudaDeviceGetAttribute(n, cudaDevAttrMultiProcessorCount, device));

@@ -14,6 +14,38 @@ from tests.test_gpu_decode import RS, _all_local, _tiny
 pytestmark = pytest.mark.gpu
 
 
+def test_donor_monitor_reclaims_under_cotenant_pressure():
+    """Co-tenant pressure on the donor (simulated free-memory readings on top
+    of a real cudaMemGetInfo probe) revokes LRU handles in order and returns
+    their VMM chunks to the donor."""
+    from paper_2602_00328_b200.churn import DonorMonitor, mem_get_info
+    from paper_2602_00328_b200.runtime import AllocationHints
+    from paper_2602_00328_b200.system import HarvestSystem
+    free0, total0 = mem_get_info(0)
+    assert 0 < free0 <= total0
+    seg = 64 << 20
+    sysm = HarvestSystem(0, donors=[0], donor_bytes=16 * seg, host_bytes=1, local_bytes=1)
+    rt = sysm.runtime
+    hs = [rt.harvest_alloc(seg, AllocationHints(client_id="t")) for _ in range(10)]
+    assert all(h is not None for h in hs) and sysm.pools[1].committed_bytes == 10 * seg
+    fired = []
+    for h in hs:
+        rt.harvest_register_cb(h, lambda hh, r: fired.append(hh.generation))
+    for h in hs[5:]:
+        rt.touch(h)          # make hs[0..4] the least recently used
+    state = {"free": 8 << 30}
+    mon = DonorMonitor(sysm, headroom=512 << 20, meminfo=lambda dev: (state["free"], total0))
+    mon.poll()
+    assert not fired       # plenty of room: nothing happens
+    state["free"] = 128 << 20   # a co-tenant took the rest: level = 128M + 640M - 512M = 256M
+    mon.poll()
+    sysm.loop.run()
+    assert sorted(fired) == sorted(h.generation for h in hs[:6])   # LRU first, >= 384 MiB reclaimed
+    assert sysm.pools[1].committed_bytes == 4 * seg                 # chunks unmapped back to the donor
+    assert refcheck.verify_release_ordering(sysm.loop.log) == []
+    sysm.close()
+
+
 def test_decode_under_churn_matches_all_local():
     from paper_2602_00328_b200.churn import AvailabilityProcess, ChurnDriver, expert_tier_counts
     from paper_2602_00328_b200.decode import MoEDecoder
