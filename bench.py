@@ -612,15 +612,27 @@ def run_b200(a):
     barrier()
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clk:
-        t0.record(stream)
-        for k in range(a.steps):
-            value_step(a.warmup + k, step_events[k])
-        t1.record(stream)
-        t1.synchronize()
-    torch.cuda.synchronize()
+    remeasured = None
+    for attempt in range(2):
+        with ClockSampler(dev) as clk:
+            t0.record(stream)
+            for k in range(a.steps):
+                value_step(a.warmup + k, step_events[k])
+            t1.record(stream)
+            t1.synchronize()
+        torch.cuda.synchronize()
+        bad = clk.summary().get("rejected", False)
+        if world > 1:  # every rank re-measures if any rank saw a bad reason
+            flag = [bool(bad)]
+            flags = [None] * world
+            dist.all_gather_object(flags, flag)
+            bad = any(f[0] for f in flags)
+        if not bad:
+            break
+        remeasured = clk.summary()  # hw/thermal slowdown seen: keep the record, measure once more
+        barrier()
     barrier()
-    launches = N.launch_count() - launches0
+    launches = (N.launch_count() - launches0) // (attempt + 1)   # per timed attempt
     dt = max_over_ranks(t0.elapsed_time(t1) * 1e-3)
     my_bytes = sum(nb for s in range(a.warmup, a.warmup + a.steps) for (_, _, _, nb) in desc[s])
     total_bytes = my_bytes * world
@@ -739,7 +751,7 @@ def run_b200(a):
                 "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": h2d // a.steps,
                         "d2h_bytes_per_step": d2h // a.steps, "verify_mismatched_words": int(mism_all)},
                 "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
-                "clocks": clk.summary(),
+                "clocks": {**clk.summary(), "first_attempt_rejected": remeasured},
                 "latency_ms_per_layer_fetch": statistics.median(launch_ms), "decode": decode,
                 "kv_long_context_128k": kvlc, **extra}
     barrier()
