@@ -68,7 +68,12 @@ def parse():
 
 
 def model():
-    from paper_2602_00328_b200.moe import QWEN15_MOE_A27B
+    from paper_2602_00328_b200.moe import QWEN15_MOE_A27B, MoEProfile
+    layers = int(os.environ.get("HV_BENCH_QWEN_LAYERS", "0"))
+    if layers:  # test-only: many ranks on one GPU (the reported config is the 24-layer model)
+        m = QWEN15_MOE_A27B
+        return MoEProfile(m.name, layers, m.num_experts, m.top_k, m.expert_size, hidden=m.hidden,
+                          intermediate=m.intermediate)
     return QWEN15_MOE_A27B
 
 
