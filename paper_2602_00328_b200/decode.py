@@ -93,14 +93,21 @@ class MoEDecoder:
         new_addr = torch.from_numpy(src.view(np.int64).copy())
         new_fetchable = torch.from_numpy((self.f.tier != 0).copy())
         if getattr(self, "addr", None) is None:
-            self.addr = new_addr.to(self.dev)
+            # two device copies of the table: in-flight fetch kernels read the
+            # current one through raw pointers while the next one is written
+            self._addr_bufs = [new_addr.to(self.dev), new_addr.to(self.dev)]
+            self._addr_done = [None, None]
+            self._addr_cur = 0
+            self.addr = self._addr_bufs[0]
             self.fetchable = new_fetchable.to(self.dev)
         else:
-            # in-flight fetch kernels read the table through raw pointers:
-            # let them finish before it changes (revocations are rare)
-            torch.cuda.synchronize(self.dev)
-            self.addr.copy_(new_addr)
+            nxt = 1 - self._addr_cur
+            if self._addr_done[nxt] is not None:
+                self._addr_done[nxt].synchronize()   # last step that read buffer nxt is done
+            self._addr_bufs[nxt].copy_(new_addr)
             self.fetchable.copy_(new_fetchable)
+            self._addr_cur = nxt
+            self.addr = self._addr_bufs[nxt]
         self.layer_handles = [[h for (l, _e), h in self.f.handles.items() if l == layer] for layer in range(self.L)]
         self._table_version = getattr(self.f, "version", 0)
 
@@ -200,6 +207,9 @@ class MoEDecoder:
             if s + 1 < n:
                 fetched[s + 1] = self._issue_fetch(s + 1, nxt_ready, buf_free[(s + 1) % 2] if s >= 1 else None)
         cur.wait_stream(self.compute)
+        done = torch.cuda.Event()
+        done.record(cur)              # every fetch of this step read self.addr before this point
+        self._addr_done[self._addr_cur] = done
         return torch.stack(hs).view(self.T, self.H)
 
     def decode(self, steps: int, x: torch.Tensor | None = None) -> torch.Tensor:

@@ -197,7 +197,7 @@ def rebalance(sim, runtime: HarvestRuntime, model: MoEProfile, residency: Expert
                           payload=expert_content(model, layer, expert), on_complete=_arrived))
         migrations.append((layer, expert, handle))
     if items:
-        runtime.app_transfer_batch(items)
+        runtime.app_transfer_batch(items, engine=getattr(runtime, "placement_engine", None))
     return migrations
 
 

@@ -88,10 +88,16 @@ class HarvestSystem:
                                          engine=engine, max_ctas=max_ctas, log_transfers=log_transfers)
         self.runtime = HarvestRuntime(self.loop, self.topology, policy, compute_device_id=0,
                                       engine=self.engine, pools=self.pools)
+        # placement copy-ins (K3, rebalance) run on their own stream so they
+        # share the links with, but never queue behind, the fetch stream
+        self.placement_engine = CudaTransferEngine(self.loop, self.topology, self.memory, compute,
+                                                   engine=engine, max_ctas=max_ctas, log_transfers=log_transfers)
+        self.runtime.placement_engine = self.placement_engine
 
     def close(self) -> None:
         self.loop.run()
         self.engine.close()
+        self.placement_engine.close()
         for p in self.pools.values():
             p.close()
         if self.host is not None:
