@@ -256,12 +256,48 @@ def kv_long_context(sysm, source, a):
     return out
 
 
-def autotune(layer_desc, stream, stream_h, F, reps=3):
+PROBE_CHILD = r"""
+import json, sys
+sys.path.insert(0, {repo!r})
+import torch
+from paper_2602_00328_b200 import fetch as F
+from paper_2602_00328_b200.pool import PeerPool
+p = PeerPool.import_ipc(bytes.fromhex({handle!r}), {donor}, {nbytes}, {dev})
+n = 4 << 20
+a = torch.empty(n, dtype=torch.uint8, device="cuda:{dev}")
+b = torch.empty(n, dtype=torch.uint8, device="cuda:{dev}")
+src = F.ptrs_tensor([p.va], "cuda:{dev}")
+sz = F.ptrs_tensor([n], "cuda:{dev}")
+F.batch_copy(src, F.ptrs_tensor([a.data_ptr()], "cuda:{dev}"), sz, engine="ldg")
+F.batch_copy(src, F.ptrs_tensor([b.data_ptr()], "cuda:{dev}"), sz, engine={engine!r})
+torch.cuda.synchronize()
+print(json.dumps({{"ok": bool(torch.equal(a, b))}}))
+p.close()
+"""
+
+
+def probe_engines_on_peer(handle: bytes, donor: int, nbytes: int, dev: int) -> dict:
+    """Run each non-LDG engine on a real peer pointer in a throw-away child
+    process: a fault there cannot poison this process's CUDA context."""
+    import subprocess
+    ok = {"ldg": True}
+    for engine in ("ldg256", "tma"):
+        code = PROBE_CHILD.format(repo=REPO, handle=handle.hex(), donor=donor, nbytes=nbytes, dev=dev,
+                                  engine=engine)
+        try:
+            r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=180)
+            ok[engine] = r.returncode == 0 and '"ok": true' in r.stdout
+        except Exception:
+            ok[engine] = False
+    return ok
+
+
+def autotune(layer_desc, stream, stream_h, F, reps=3, engines=("ldg", "ldg256", "tma")):
     """Time one layer's real fetch under each engine x grid cap; pick the fastest."""
     import torch
     sp, dp, sz, nb = layer_desc
     rows = []
-    for engine in ("ldg", "ldg256", "tma"):
+    for engine in engines:
         for max_ctas in (0, 296, 148):
             for _ in range(1):  # warm
                 F.batch_copy(sp, dp, sz, engine=engine, max_ctas=max_ctas, stream=stream_h)
@@ -583,7 +619,18 @@ def run_b200(a):
     # of one layer's real descriptors); "--engine X" pins the choice instead
     tune = None
     if a.engine == "auto":
-        tune = autotune(desc[0][0], stream, stream_h, F)
+        engines = ("ldg", "ldg256", "tma")
+        safe = None
+        if world > 1:  # engines other than LDG are proven on a peer pointer first, out of process
+            if rank == 0:
+                d = others[0]
+                safe = probe_engines_on_peer(handles[d], d, per_reader * (world - 1), dev)
+            box = [safe]
+            dist.broadcast_object_list(box, src=0)
+            safe = box[0]
+            engines = tuple(e for e in engines if safe.get(e))
+        tune = autotune(desc[0][0], stream, stream_h, F, engines=engines)
+        tune["peer_engine_probe"] = safe
         a.engine, a.max_ctas = tune["best"]["engine"], tune["best"]["max_ctas"]
         if world > 1:  # every rank must run the same configuration: rank 0 decides
             choice = [a.engine, a.max_ctas]
