@@ -394,45 +394,64 @@ class KVCacheManager:
         """Bring blocks to LocalHBM from their resident tier in ONE K1 launch.
         Revoked-peer blocks resolve through resolve_fallback; Lossy blocks
         without a host copy are recomputed (content regenerated)."""
-        need = [self.table[i] for i in block_ids if self.table[i].tier != KVTier.LOCAL_HBM]
+        table, LOCAL, PEER, HOST, NM = self.table, KVTier.LOCAL_HBM, KVTier.PEER_HBM, KVTier.HOST_DRAM, \
+            KVTier.NOT_MATERIALIZED
+        need = [table[i] for i in block_ids if table[i].tier is not LOCAL]
         plan = {"peer": [], "host": [], "recompute": []}
-        src_b, src_s, dst_b, dst_s, handles, recompute, vacated = [], [], [], [], set(), [], []
+        handles, recompute, vacated = set(), [], []
         now = self.sys.loop.now
+        n = len(need)
         # reserve every destination slot first: evictions triggered here only
         # see blocks that are already local, never the ones being reloaded
-        slots = [self._take_local_slot() for _ in need]
+        limit = int(self.policy.local_watermark * self.local_blocks)
+        if n and len(self.local_free) >= n and self._local_used() + n <= limit:
+            slots = self.local_free[-n:][::-1]          # bulk: no eviction needed
+            del self.local_free[-n:]
+        else:
+            slots = [self._take_local_slot() for _ in need]
+        src_b = np.empty(n, dtype=np.uint64)
+        src_s = np.empty(n, dtype=np.uint64)
+        dst_b = np.empty(n, dtype=np.uint64)
+        k = 0
+        page, cache0 = self.page, self.cache.data_ptr()
+        slab_stride, host_stride = self.slab_blocks * page, self.host_blocks * page
+        host0 = self.host.device_address(0)
+        live_cache: dict[int, bool] = {}
+        plan_peer, plan_host = plan["peer"], plan["host"]
         for b, slot in zip(need, slots):
-            if b.tier == KVTier.PEER_HBM and not self.rt.is_live(self.slabs[b.slab].handle):
-                # revoked between lookup and issue: fallback
-                b.tier = KVTier.HOST_DRAM if b.host_slot is not None else KVTier.NOT_MATERIALIZED
-            if b.tier == KVTier.HOST_DRAM and self.resolve_fallback(b) == "Recompute":
-                b.tier = KVTier.NOT_MATERIALIZED
-            if b.tier == KVTier.NOT_MATERIALIZED:
-                b.tier, b.slot = KVTier.LOCAL_HBM, slot
+            t = b.tier
+            if t is PEER:
+                live = live_cache.get(b.slab)
+                if live is None:
+                    live = live_cache[b.slab] = self.rt.is_live(self.slabs[b.slab].handle)
+                if not live:  # revoked between lookup and issue: fallback
+                    t = b.tier = HOST if b.host_slot is not None else NM
+            if t is HOST and self.resolve_fallback(b) == "Recompute":
+                t = b.tier = NM
+            if t is NM:
+                b.tier, b.slot = LOCAL, slot
                 recompute.append(b)
                 plan["recompute"].append(b.block_id)
-                self.stats["recompute"] += 1
                 continue
-            sbase, sstride = self._page_base(b)
-            src_b.append(sbase), src_s.append(sstride)
-            dst_b.append(self.cache.data_ptr() + slot * self.page), dst_s.append(self.local_blocks * self.page)
-            if b.tier == KVTier.PEER_HBM:
+            if t is PEER:
                 slab = self.slabs[b.slab]
+                src_b[k], src_s[k] = slab.va + b.slot * page, slab_stride
                 handles.add(slab.handle)
-                plan["peer"].append(b.block_id)
-                self.stats["reload_peer"] += 1
-                old = (b.slab, b.slot)
+                plan_peer.append(b.block_id)
+                vacated.append((b.slab, b.slot))
             else:
-                plan["host"].append(b.block_id)
-                self.stats["reload_host"] += 1
-                old = None
-            b.tier, b.slot, b.slab = KVTier.LOCAL_HBM, slot, -1
+                src_b[k], src_s[k] = host0 + b.host_slot * page, host_stride
+                plan_host.append(b.block_id)
+            dst_b[k] = cache0 + slot * page
+            k += 1
+            b.tier, b.slot, b.slab = LOCAL, slot, -1
             b.last_access = now
-            if old is not None:
-                vacated.append(old)
-        if src_b:
-            src = self._pages(np.array(src_b, dtype=np.uint64), np.array(src_s, dtype=np.uint64))
-            dst = self._pages(np.array(dst_b, dtype=np.uint64), np.array(dst_s, dtype=np.uint64))
+        self.stats["recompute"] += len(plan["recompute"])
+        self.stats["reload_peer"] += len(plan_peer)
+        self.stats["reload_host"] += len(plan_host)
+        if k:
+            src = self._pages(src_b[:k], src_s[:k])
+            dst = self._pages(dst_b[:k], np.full(k, self.local_blocks * page, dtype=np.uint64))
             self._launch_pages(src, dst, handles)
         # old peer slots become reusable only now: any later write into them is
         # stream-ordered after this launch's reads (same fetch stream)
