@@ -1,0 +1,67 @@
+"""Shared definitions of the contract benchmark (bench.py): the workload, its routing, output."""
+from __future__ import annotations
+
+import json
+import math
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if REPO not in sys.path:
+    sys.path.insert(0, REPO)
+
+
+
+GiB = 1 << 30
+
+METRIC = "peer-fetch GB/s"
+
+TOKENS, SEED = 32, 2
+
+KV_TOKENS, KV_SLAB_BLOCKS = 131072, 64   # BASELINE configs[3]: one 128k-token Llama-3-8B sequence
+
+def model():
+    from paper_2602_00328_b200.moe import QWEN15_MOE_A27B, MoEProfile
+    layers = int(os.environ.get("HV_BENCH_QWEN_LAYERS", "0"))
+    if layers:  # test-only: many ranks on one GPU (the reported config is the 24-layer model)
+        m = QWEN15_MOE_A27B
+        return MoEProfile(m.name, layers, m.num_experts, m.top_k, m.expert_size, hidden=m.hidden,
+                          intermediate=m.intermediate)
+    return QWEN15_MOE_A27B
+
+def routing(m, steps, seed=SEED):
+    from paper_2602_00328_b200.moe import topk_routing
+    return topk_routing(m, TOKENS, steps, seed)
+
+def workload_config(m, n, source):
+    return {"workload": f"{m.name} expert fetch (BASELINE configs[1]): {m.num_layers} layers x "
+                        f"{m.num_experts} experts x {m.expert_size} B, decode batch {TOKENS}, top-{m.top_k}, "
+                        f"100% offloaded; one step = every layer's activated experts",
+            "source_tier": source, "donors_per_rank": max(0, n - 1),
+            "l2": f"inputs larger than L2 (~{m.num_layers * 53 * m.expert_size / 1e9:.0f} GB fetched per step, "
+                  "126 MB L2)",
+            "routing": f"top-{m.top_k} of N(0,1) logits, seed {SEED}"}
+
+def emit(line, a):
+    s = json.dumps(line)
+    print(s, flush=True)
+    if a.out:
+        with open(a.out, "a") as f:
+            f.write(s + "\n")
+
+def load_traffic():
+    p = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return {}
+    return {}
+
+def kv_slab_bytes():
+    from paper_2602_00328_b200.kv import LLAMA3_8B
+    return KV_SLAB_BLOCKS * LLAMA3_8B.block_bytes

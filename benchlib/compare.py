@@ -1,0 +1,223 @@
+"""Same-run comparisons (copy engine, latency curves, KV config-1 gather), engine probe and autotune."""
+from __future__ import annotations
+
+import json
+import math
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+
+from benchlib.common import REPO, model
+
+
+def measure_pcie_h2d(dev):
+    import torch
+    from paper_2602_00328_b200.pool import HostTier
+    h = HostTier(1 << 30)
+    d = torch.empty(1 << 30, dtype=torch.uint8, device=f"cuda:{dev}")
+    s = torch.cuda.Stream(dev)
+    best = 0.0
+    with torch.cuda.stream(s):
+        src = torch.from_numpy(h.view())
+        for i in range(6):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            d.copy_(src, non_blocking=True)
+            e1.record(s)
+            e1.synchronize()
+            if i:
+                best = max(best, (1 << 30) / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    del src
+    h.close()
+    return best
+
+PROBE_CHILD = r"""
+import json, sys
+sys.path.insert(0, {repo!r})
+import torch
+from paper_2602_00328_b200 import fetch as F
+from paper_2602_00328_b200.pool import PeerPool
+p = PeerPool.import_ipc(bytes.fromhex({handle!r}), {donor}, {nbytes}, {dev})
+n = 4 << 20
+a = torch.empty(n, dtype=torch.uint8, device="cuda:{dev}")
+b = torch.empty(n, dtype=torch.uint8, device="cuda:{dev}")
+src = F.ptrs_tensor([p.va], "cuda:{dev}")
+sz = F.ptrs_tensor([n], "cuda:{dev}")
+F.batch_copy(src, F.ptrs_tensor([a.data_ptr()], "cuda:{dev}"), sz, engine="ldg")
+F.batch_copy(src, F.ptrs_tensor([b.data_ptr()], "cuda:{dev}"), sz, engine={engine!r})
+torch.cuda.synchronize()
+print(json.dumps({{"ok": bool(torch.equal(a, b))}}))
+p.close()
+"""
+
+def probe_engines_on_peer(handle: bytes, donor: int, nbytes: int, dev: int) -> dict:
+    """Run each non-LDG engine on a real peer pointer in a throw-away child
+    process: a fault there cannot poison this process's CUDA context."""
+    import subprocess
+    ok = {"ldg": True}
+    for engine in ("ldg256", "tma"):
+        code = PROBE_CHILD.format(repo=REPO, handle=handle.hex(), donor=donor, nbytes=nbytes, dev=dev,
+                                  engine=engine)
+        try:
+            r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=180)
+            ok[engine] = r.returncode == 0 and '"ok": true' in r.stdout
+        except Exception:
+            ok[engine] = False
+    return ok
+
+def autotune(layer_desc, stream, stream_h, F, reps=3, engines=("ldg", "ldg256", "tma")):
+    """Time one layer's real fetch under each engine x grid cap; pick the fastest."""
+    import torch
+    sp, dp, sz, nb = layer_desc
+    rows = []
+    for engine in engines:
+        for max_ctas in (0, 296, 148):
+            for _ in range(1):  # warm
+                F.batch_copy(sp, dp, sz, engine=engine, max_ctas=max_ctas, stream=stream_h)
+            ts = []
+            for _ in range(reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                F.batch_copy(sp, dp, sz, engine=engine, max_ctas=max_ctas, stream=stream_h)
+                e1.record(stream)
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1) * 1e-3)
+            rows.append({"engine": engine, "max_ctas": max_ctas, "GBps": nb / statistics.median(ts) / 1e9})
+    best = max(rows, key=lambda r: r["GBps"])
+    return {"best": best, "candidates": rows}
+
+def same_run_comparisons(dev, m, a, source, fetcher=None, n=53):
+    """Same-box comparisons for one layer's worth of experts (n x 17.3 MB):
+    the copy-engine paths on the same source (cudaMemcpyBatchAsync: the
+    paper's/vLLM's data path) and the same kernel on a local-HBM source
+    against the HBM roofline (kernel quality independent of the link)."""
+    import torch
+    from paper_2602_00328_b200 import fetch as F
+    from paper_2602_00328_b200.pool import HostTier
+    S = m.expert_size
+    dst = torch.empty(n * S, dtype=torch.uint8, device=f"cuda:{dev}")
+    loc = torch.empty(n * S, dtype=torch.uint8, device=f"cuda:{dev}")
+    s = torch.cuda.Stream(dev)
+
+    def t(fn, iters=5):
+        best = []
+        for i in range(iters + 2):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            fn()
+            e1.record(s)
+            e1.synchronize()
+            if i >= 2:
+                best.append(e0.elapsed_time(e1) * 1e-3)
+        return statistics.median(best)
+
+    out = {}
+    dp = F.ptrs_tensor([dst.data_ptr() + i * S for i in range(n)], f"cuda:{dev}")
+    sz = F.ptrs_tensor([S] * n, f"cuda:{dev}")
+    lp = F.ptrs_tensor([loc.data_ptr() + i * S for i in range(n)], f"cuda:{dev}")
+    dt = t(lambda: F.batch_copy(lp, dp, sz, engine=a.engine, stream=s.cuda_stream))
+    hbm_peak = 6553.0
+    try:
+        hbm_peak = float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        pass
+    out["roofline_local_source"] = {"bound": "hbm", "achieved": 2 * n * S / dt / 1e9, "peak": hbm_peak,
+                                    "unit": "GB/s", "frac": 2 * n * S / dt / 1e9 / hbm_peak,
+                                    "note": "same K2 kernel, local-HBM source: read+write bytes / time vs "
+                                            "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"}
+    hd = np.array([dst.data_ptr() + i * S for i in range(n)], dtype=np.uint64)
+    hz = np.full(n, S, dtype=np.uint64)
+    h = HostTier(n * S)
+    hs = np.array([h.host_address(i * S) for i in range(n)], dtype=np.uint64)
+    lat = {}
+    lat["kernel_host"] = t(lambda: F.batch_copy(F.ptrs_tensor([h.device_address(0)], f"cuda:{dev}"), dp[:1],
+                                                sz[:1], engine=a.engine, stream=s.cuda_stream)) * 1e6
+    lat["copy_engine_host"] = t(lambda: F.ce_batch_copy(hs[:1], hd[:1], hz[:1], batched=False,
+                                                        stream=s.cuda_stream)) * 1e6
+    if source == "host":
+        dce = t(lambda: F.ce_batch_copy(hs, hd, hz, batched=True, stream=s.cuda_stream))
+        out["copy_engine_same_source_GBps"] = n * S / dce / 1e9
+    else:
+        # peer experts of layer 0 (spread over every donor)
+        ps = np.ascontiguousarray(fetcher.src_addr[0, :n])
+        pdev = F.ptrs_tensor(ps, f"cuda:{dev}")
+        dce = t(lambda: F.ce_batch_copy(ps, hd, hz, batched=True, stream=s.cuda_stream))
+        out["copy_engine_same_source_GBps"] = n * S / dce / 1e9
+        dce_loop = t(lambda: F.ce_batch_copy(ps, hd, hz, batched=False, stream=s.cuda_stream))
+        out["copy_engine_peer_per_object_GBps"] = n * S / dce_loop / 1e9
+        lat["kernel_peer"] = t(lambda: F.batch_copy(pdev[:1], dp[:1], sz[:1], engine=a.engine,
+                                                    stream=s.cuda_stream)) * 1e6
+        lat["copy_engine_peer"] = t(lambda: F.ce_batch_copy(ps[:1], hd[:1], hz[:1], batched=False,
+                                                            stream=s.cuda_stream)) * 1e6
+        lat["peer_vs_host_speedup"] = lat["copy_engine_host"] / lat["kernel_peer"]
+    out["single_expert_latency_us"] = lat
+    # KV config 1 (BASELINE configs[0] shape): 1,024 x 64 KiB pages = one layer
+    # of 4 sequences x 4k tokens, gathered by K1 from the tier under test
+    page, npg = 65536, 1024
+    rng = np.random.default_rng(5)
+    kv = {}
+    kdst = torch.empty(npg * page, dtype=torch.uint8, device=f"cuda:{dev}")
+    hp = HostTier(4 * npg * page)
+    host_pages = F.ptrs_tensor([hp.device_address(int(p) * page) for p in rng.permutation(4 * npg)[:npg]],
+                               f"cuda:{dev}")
+    dt_h = t(lambda: F.kv_gather(host_pages, page, dst=kdst, engine=a.engine, stream=s.cuda_stream))
+    kv["host_us"], kv["host_GBps"] = dt_h * 1e6, npg * page / dt_h / 1e9
+    if source == "peer":
+        base = fetcher.src_addr[0, :n]   # peer memory of n experts viewed as page slots
+        slots = [int(base[i]) + j * page for i in range(n) for j in range(S // page)]
+        peer_pages = F.ptrs_tensor([slots[int(p)] for p in rng.permutation(len(slots))[:npg]], f"cuda:{dev}")
+        dt_p = t(lambda: F.kv_gather(peer_pages, page, dst=kdst, engine=a.engine, stream=s.cuda_stream))
+        kv["peer_us"], kv["peer_GBps"] = dt_p * 1e6, npg * page / dt_p / 1e9
+        kv["peer_vs_host_speedup"] = dt_h / dt_p
+    out["kv_config1_layer_gather"] = kv
+    out.update(latency_curves(dev, a, s, t, h, fetcher if source == "peer" else None))
+    hp.close()
+    h.close()
+    return out
+
+def latency_curves(dev, a, s, t, host, fetcher):
+    """Measured single-object fetch latency vs size on each available tier,
+    refit with the reference's own calibrate() (interconnect.py:168-200), and
+    the paper's KV reload-latency experiment (Fig 7:
+    FP16 KV, 100..8000 entries, host vs peer) measured instead of modeled."""
+    import torch
+    from paper_2602_00328_b200 import fetch as F
+    from paper_2602_00328_b200.interconnect import calibrate, calibration_rms
+    sizes = [65536, 262144, 1 << 20, 4 << 20, 17_301_504]
+    dst = torch.empty(max(sizes) + (8000 * 70_272), dtype=torch.uint8, device=f"cuda:{dev}")
+    tiers = {"host": host.device_address(0)}
+    if fetcher is not None:
+        tiers["peer"] = int(fetcher.src_addr[0, 0])
+    one = F.ptrs_tensor([S for S in [0]], f"cuda:{dev}")
+    curves, fits = {}, {}
+    for name, base in tiers.items():
+        pts = []
+        for nb in sizes:
+            sp = F.ptrs_tensor([base], f"cuda:{dev}")
+            dp = F.ptrs_tensor([dst.data_ptr()], f"cuda:{dev}")
+            sz = F.ptrs_tensor([nb], f"cuda:{dev}")
+            pts.append((nb, t(lambda: F.batch_copy(sp, dp, sz, engine=a.engine, stream=s.cuda_stream))))
+        curves[name] = [[nb, lat * 1e6] for nb, lat in pts]
+        fc, bw = calibrate(pts)
+        fits[name] = {"fixed_cost_us": fc * 1e6, "bandwidth_GBps": bw / 1e9, "rms_rel": calibration_rms(pts, fc, bw)}
+    out = {"latency_vs_size_us": curves, "calibrated_links": fits}
+    if fetcher is not None:
+        rows = []
+        for model, bpe in (("kimi-k2", 70_272), ("mistral-large-3", 12_800)):   # profiles.py:116-122
+            for e in (100, 500, 1000, 2000, 4000, 8000):
+                nb = e * bpe
+                lat = {}
+                for name, base in tiers.items():
+                    sp = F.ptrs_tensor([base], f"cuda:{dev}")
+                    dp = F.ptrs_tensor([dst.data_ptr()], f"cuda:{dev}")
+                    sz = F.ptrs_tensor([nb], f"cuda:{dev}")
+                    lat[name] = t(lambda: F.batch_copy(sp, dp, sz, engine=a.engine, stream=s.cuda_stream))
+                rows.append([model, e, lat["host"] * 1e6, lat["peer"] * 1e6, lat["host"] / lat["peer"]])
+        out["kv_reload_latency_experiment"] = {"columns": ["model", "entries", "host_us", "peer_us", "speedup"],
+                                               "rows": rows,
+                                               "paper_h100": "kimi-k2 5.42x@100 -> 5.68x@8000 (PAPER.md:319)"}
+    del one
+    return out
