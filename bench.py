@@ -308,8 +308,9 @@ def run_b200(a):
     # overlap mode: the fetch kernel's grid is capped so decode compute keeps SMs
     d2 = run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, microbatches=2,
                     max_ctas=a.overlap_max_ctas)
-    decode["pipelined_2_microbatches"] = {k: d2[k] for k in ("tokens_per_s", "per_rank_tokens_per_s",
-                                                             "ms_per_decode_step", "outputs_finite")}
+    decode["pipelined_2_microbatches"] = {k: d2.get(k) for k in ("tokens_per_s", "per_rank_tokens_per_s",
+                                                                 "ms_per_decode_step", "outputs_finite",
+                                                                 "overlap")}
     decode["pipelined_2_microbatches"]["fetch_max_ctas"] = a.overlap_max_ctas
     sysm.loop.run()
     kvlc = None

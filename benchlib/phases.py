@@ -39,6 +39,10 @@ def run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, micro
            "outputs_finite": bool(torch.isfinite(h.float()).all()),
            "model": f"{m.num_layers} MoE layers (router + top-{m.top_k} + SwiGLU experts, bf16); "
                     "attention not modeled"}
+    if microbatches > 1:  # one extra, traced step: device-clock proof of fetch/compute overlap
+        dec.trace = True
+        dec.step(h)
+        out["overlap"] = dec.overlap_report()
     del dec
     return out
 

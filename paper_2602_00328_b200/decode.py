@@ -39,7 +39,7 @@ from .moe import ExpertFetcher
 class MoEDecoder:
     def __init__(self, fetcher: ExpertFetcher, tokens: int, microbatches: int = 1, seed: int = 0,
                  engine: str = "auto", max_ctas: int = 0, router_scale: float = 0.5,
-                 residual_scale: float = 1.0):
+                 residual_scale: float = 1.0, trace: bool = False):
         m = fetcher.model
         if not (m.hidden and m.intermediate):
             raise ValueError("model profile needs hidden/intermediate sizes")
@@ -52,6 +52,10 @@ class MoEDecoder:
         self.dev = torch.device(f"cuda:{eng.cuda_device}")
         self.L, self.E, self.H, self.I, self.S = m.num_layers, m.num_experts, m.hidden, m.intermediate, m.expert_size
         self.T, self.nmb = tokens, microbatches
+        # trace=True: timing events around every fetch (fetch stream) and every
+        # expert FFN (compute stream) -> overlap_report()
+        self.trace = trace
+        self._tr: dict = {}
         # h <- h + residual_scale * moe(h); a power of two keeps it exact in bf16
         self.residual_scale = residual_scale
         self.tmb = tokens // microbatches
@@ -153,8 +157,15 @@ class MoEDecoder:
         self.fetch.wait_event(ready)
         if buf_free is not None:
             self.fetch.wait_event(buf_free)
+        if self.trace:
+            fs = torch.cuda.Event(enable_timing=True)
+            fs.record(self.fetch)
         N.call("hv_batch_copy", self.addr[layer].data_ptr(), self.dst_ptrs[slot].data_ptr(),
                self.sizes[slot].data_ptr(), self.E, self.engine_id, self.max_ctas, self.fetch_stream_h)
+        if self.trace:
+            fe = torch.cuda.Event(enable_timing=True)
+            fe.record(self.fetch)
+            self._tr.setdefault(s, {})["fetch"] = (fs, fe)
         handles = self.layer_handles[layer]
         if handles:
             batch = self.rt.begin_reads(handles)
@@ -194,7 +205,14 @@ class MoEDecoder:
                     nxt_ready = torch.cuda.Event()
                     nxt_ready.record(self.compute)
                 self.compute.wait_event(fetched[s])
+                if self.trace:
+                    cs = torch.cuda.Event(enable_timing=True)
+                    cs.record(self.compute)
                 y = self._ffn(hs[mb], slot, buf)
+                if self.trace:
+                    ce = torch.cuda.Event(enable_timing=True)
+                    ce.record(self.compute)
+                    self._tr.setdefault(s, {})["compute"] = (cs, ce)
                 hs[mb] = hs[mb] + (y * self.residual_scale if self.residual_scale != 1.0 else y)
                 done = torch.cuda.Event()
                 done.record(self.compute)
@@ -211,6 +229,29 @@ class MoEDecoder:
         done.record(cur)              # every fetch of this step read self.addr before this point
         self._addr_done[self._addr_cur] = done
         return torch.stack(hs).view(self.T, self.H)
+
+    def overlap_report(self) -> dict:
+        """From the last traced step: per-stage fetch and FFN intervals on the
+        device clock, and how much of each stage-(s+1) fetch ran while stage s
+        computed (the CGOPipe overlap, moe.py:327-340)."""
+        torch.cuda.synchronize(self.dev)
+        stages = sorted(k for k, v in self._tr.items() if "fetch" in v and "compute" in v)
+        if not stages:
+            return {}
+        base = self._tr[stages[0]]["fetch"][0]
+        iv = {s: {k: (base.elapsed_time(a), base.elapsed_time(b)) for k, (a, b) in self._tr[s].items()}
+              for s in stages}
+        fetch_ms = sum(v["fetch"][1] - v["fetch"][0] for v in iv.values())
+        comp_ms = sum(v["compute"][1] - v["compute"][0] for v in iv.values())
+        ov = 0.0
+        for s in stages:
+            if s + 1 in iv:
+                (f0, f1), (c0, c1) = iv[s + 1]["fetch"], iv[s]["compute"]
+                ov += max(0.0, min(f1, c1) - max(f0, c0))
+        span = max(v["compute"][1] for v in iv.values()) - min(v["fetch"][0] for v in iv.values())
+        return {"stages": len(stages), "fetch_ms": fetch_ms, "compute_ms": comp_ms, "overlap_ms": ov,
+                "compute_hidden_fraction": ov / comp_ms if comp_ms else None, "span_ms": span,
+                "serial_ms": fetch_ms + comp_ms}
 
     def decode(self, steps: int, x: torch.Tensor | None = None) -> torch.Tensor:
         h = self.x0 if x is None else x
