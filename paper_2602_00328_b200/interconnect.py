@@ -256,7 +256,7 @@ class CudaTransferEngine:
     def launch_raw(self, src: np.ndarray, dst: np.ndarray, size: np.ndarray, reqs=None,
                    on_completes=None, initiator: str = "app", handle_keys=None, callbacks=()):
         """Launch one batched fetch over raw device addresses (host arrays).
-        ``callbacks`` (no-argument... called with None) run at completion too;
+        Each of ``callbacks`` is called with None when the batch completes;
         the batch's event is left in ``self.last_event`` until it is polled."""
         n = len(src)
         N.call("hv_swap_blocks_batch", src.ctypes.data, dst.ctypes.data, size.ctypes.data, n,
