@@ -265,7 +265,7 @@ def run_b200(a):
             ex = routes[s][layer]
             key = (s, layer)
             if key not in seeds_dev:
-                seeds_dev[key] = F._seeds_tensor([expert_content(m, layer, int(e)) for e in ex], f"cuda:{dev}")
+                seeds_dev[key] = F.seeds_tensor([expert_content(m, layer, int(e)) for e in ex], f"cuda:{dev}")
             with torch.cuda.stream(stream):
                 bad = F.verify_content(F.ptrs_tensor(stage_ptrs[layer % 2][:len(ex)], f"cuda:{dev}"),
                                        F.ptrs_tensor([S] * len(ex), f"cuda:{dev}"), seeds_dev[key],

@@ -135,7 +135,7 @@ class DonorMonitor:
         for peer_id in self.sys.pools:
             lv = min(self.level(peer_id), self.rt.devices[peer_id].spec.usable)
             if self.last.get(peer_id) != lv:
-                self.rt._availability_step(peer_id, lv)
+                self.rt.set_availability(peer_id, lv)
                 self.last[peer_id] = lv
             out[peer_id] = lv
         self.sys.loop.poll()

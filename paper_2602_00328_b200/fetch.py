@@ -102,21 +102,21 @@ def ce_batch_copy(src_ptrs, dst_ptrs, sizes, batched: bool = True, stream=None) 
            N.stream_handle(stream))
 
 
-def _seeds_tensor(seeds, device) -> torch.Tensor:
+def seeds_tensor(seeds, device) -> torch.Tensor:
     arr = np.asarray([int(x) & ((1 << 64) - 1) for x in seeds], dtype=np.uint64).view(np.int64)
     return torch.from_numpy(arr.copy()).to(device)
 
 
 def fill_content(dst_ptrs: torch.Tensor, sizes: torch.Tensor, seeds, stream=None) -> None:
     """Write the synthetic content of each object (splitmix64 keyed by its seed)."""
-    sd = seeds if isinstance(seeds, torch.Tensor) else _seeds_tensor(seeds, dst_ptrs.device)
+    sd = seeds if isinstance(seeds, torch.Tensor) else seeds_tensor(seeds, dst_ptrs.device)
     N.call("hv_fill_content", _dev_u64(dst_ptrs, "dst_ptrs"), _dev_u64(sizes, "sizes"),
            _dev_u64(sd, "seeds"), dst_ptrs.numel(), N.stream_handle(stream))
 
 
 def fill_weights_bf16(dst_ptrs: torch.Tensor, sizes: torch.Tensor, seeds, stream=None) -> None:
     """Same keyed stream, each 16-bit lane mapped to a small finite bf16 weight."""
-    sd = seeds if isinstance(seeds, torch.Tensor) else _seeds_tensor(seeds, dst_ptrs.device)
+    sd = seeds if isinstance(seeds, torch.Tensor) else seeds_tensor(seeds, dst_ptrs.device)
     N.call("hv_fill_weights_bf16", _dev_u64(dst_ptrs, "dst_ptrs"), _dev_u64(sizes, "sizes"),
            _dev_u64(sd, "seeds"), dst_ptrs.numel(), N.stream_handle(stream))
 
@@ -132,7 +132,7 @@ def verify_content(src_ptrs: torch.Tensor, sizes: torch.Tensor, seeds, stream=No
                    weights: bool = False) -> torch.Tensor:
     """Per-object count of 8-byte words that differ from the generator
     (``weights=True``: the bf16-weights variant)."""
-    sd = seeds if isinstance(seeds, torch.Tensor) else _seeds_tensor(seeds, src_ptrs.device)
+    sd = seeds if isinstance(seeds, torch.Tensor) else seeds_tensor(seeds, src_ptrs.device)
     out = torch.empty(src_ptrs.numel(), dtype=torch.int64, device=src_ptrs.device)
     N.call("hv_verify_weights_bf16" if weights else "hv_verify_content", _dev_u64(src_ptrs, "src_ptrs"), _dev_u64(sizes, "sizes"),
            _dev_u64(sd, "seeds"), src_ptrs.numel(), out.data_ptr(), N.stream_handle(stream))

@@ -72,7 +72,7 @@ def test_decode_under_churn_matches_all_local():
     steps = 7
     for k in range(steps):
         if k in levels:
-            sysm.runtime._availability_step(1, levels[k])   # runtime.py:476-487
+            sysm.runtime.set_availability(1, levels[k])   # runtime.py:476-487
         h = dec.step(h)          # reads of handles revoked meanwhile extend their drain
         sysm.loop.run()          # drain -> invalidate -> callback -> free
         replace()                # re-place on whatever capacity is left

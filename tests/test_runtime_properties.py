@@ -57,7 +57,7 @@ def test_random_schedules_keep_invariants(ops, kind):
         elif k == "reclaim":
             rt.external_reclaim(o[1], o[2])
         elif k == "avail":
-            rt._availability_step(o[1], o[2])
+            rt.set_availability(o[1], o[2])
         elif k == "time":
             loop.run(until=loop.now + o[1])
         # exact accounting after every op
