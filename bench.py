@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--engine", default="auto", choices=["auto", "ldg", "ldg256", "tma"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "ldg", "ldg256", "ldg16", "tma"])
     ap.add_argument("--max-ctas", type=int, default=0)
     ap.add_argument("--cpu-baseline-s", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -174,7 +174,7 @@ def run_b200(a):
     # of one layer's real descriptors); "--engine X" pins the choice instead
     tune = None
     if a.engine == "auto":
-        engines = ("ldg", "ldg256", "tma")
+        engines = ("ldg", "ldg256", "ldg16", "tma")
         safe = None
         if world > 1:  # engines other than LDG are proven on a peer pointer first, out of process
             if rank == 0:

@@ -57,8 +57,10 @@ def probe_engines_on_peer(handle: bytes, donor: int, nbytes: int, dev: int) -> d
     """Run each non-LDG engine on a real peer pointer in a throw-away child
     process: a fault there cannot poison this process's CUDA context."""
     import subprocess
-    ok = {"ldg": True}
-    for engine in ("ldg256", "tma"):
+    # the LDG family issues the same LDG.E.128 loads (hint / unroll differ):
+    # only the bulk-copy (TMA) engine is proven out of process
+    ok = {"ldg": True, "ldg256": True, "ldg16": True}
+    for engine in ("tma",):
         code = PROBE_CHILD.format(repo=REPO, handle=handle.hex(), donor=donor, nbytes=nbytes, dev=dev,
                                   engine=engine)
         try:
@@ -68,7 +70,7 @@ def probe_engines_on_peer(handle: bytes, donor: int, nbytes: int, dev: int) -> d
             ok[engine] = False
     return ok
 
-def autotune(layer_desc, stream, stream_h, F, reps=3, engines=("ldg", "ldg256", "tma")):
+def autotune(layer_desc, stream, stream_h, F, reps=3, engines=("ldg", "ldg256", "ldg16", "tma")):
     """Time one layer's real fetch under each engine x grid cap; pick the fastest."""
     import torch
     sp, dp, sz, nb = layer_desc

@@ -159,6 +159,7 @@ int hv_stream_wait_event(void* stream, void* event);
 #define HV_ENGINE_LDG 1  /* SM-issued 128-bit ld.global.nc / st.global, warp per 4 KiB chunk */
 #define HV_ENGINE_TMA 2  /* cp.async.bulk global->smem->global ring, one issuing lane per CTA */
 #define HV_ENGINE_LDG256 3 /* LDG with the L2::256B sector-promotion hint (larger remote reads) */
+#define HV_ENGINE_LDG16 4  /* LDG with 16 x 128-bit loads in flight per lane (8 KiB per warp) */
 
 /* K1: block-table-indexed KV-page gather.  Page i is copied from
  * d_src_page_ptrs[i] to d_dst_page_ptrs[i] (or, when d_dst_page_ptrs is NULL,

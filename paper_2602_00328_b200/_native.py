@@ -22,7 +22,9 @@ ENGINE_AUTO = 0
 ENGINE_LDG = 1
 ENGINE_TMA = 2
 ENGINE_LDG256 = 3
-ENGINES = {"auto": ENGINE_AUTO, "ldg": ENGINE_LDG, "tma": ENGINE_TMA, "ldg256": ENGINE_LDG256}
+ENGINE_LDG16 = 4
+ENGINES = {"auto": ENGINE_AUTO, "ldg": ENGINE_LDG, "tma": ENGINE_TMA, "ldg256": ENGINE_LDG256,
+           "ldg16": ENGINE_LDG16}
 
 POOL_VMM = 0
 POOL_IPC = 1

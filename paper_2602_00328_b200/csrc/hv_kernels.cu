@@ -266,15 +266,15 @@ struct DescResolver {
 // ---------------------------------------------------------------------------
 // per-chunk operations (warp-cooperative)
 
-template <bool kL2Hint = false>
+template <bool kL2Hint = false, int kUnroll = kLdgUnroll>
 __device__ __forceinline__ void copy_chunk_ldg(const ChunkRef& r, uint32_t lane) {
   const bool aligned = ((reinterpret_cast<uintptr_t>(r.src) | reinterpret_cast<uintptr_t>(r.dst)) & 15) == 0;
-  if (aligned && r.len == kLdgChunk) {
-    uint4 v[kLdgUnroll];
+  if (aligned && r.len == (uint32_t)kUnroll * 512u) {
+    uint4 v[kUnroll];
 #pragma unroll
-    for (int j = 0; j < kLdgUnroll; ++j) v[j] = ld_src<kL2Hint>(r.src + (j * 32 + lane) * 16);
+    for (int j = 0; j < kUnroll; ++j) v[j] = ld_src<kL2Hint>(r.src + (j * 32 + lane) * 16);
 #pragma unroll
-    for (int j = 0; j < kLdgUnroll; ++j) st_stream(r.dst + (j * 32 + lane) * 16, v[j]);
+    for (int j = 0; j < kUnroll; ++j) st_stream(r.dst + (j * 32 + lane) * 16, v[j]);
     return;
   }
   uint32_t done = 0;
@@ -301,13 +301,17 @@ __device__ __forceinline__ void warp_loop(const Res& res, uint32_t total, Op op,
   }
 }
 
-template <bool kL2Hint>
+template <bool kL2Hint, int kUnroll = kLdgUnroll>
 struct CopyOpT {
   __device__ __forceinline__ void operator()(const ChunkRef& r, uint32_t lane) const {
-    copy_chunk_ldg<kL2Hint>(r, lane);
+    copy_chunk_ldg<kL2Hint, kUnroll>(r, lane);
   }
 };
 using CopyOp = CopyOpT<false>;
+// deeper engine: 16 x 128-bit loads in flight per lane (8 KiB per warp), for
+// links whose latency needs more bytes in flight per SM than LDG's 4 KiB
+constexpr int kLdgDeepUnroll = 16;
+constexpr uint32_t kLdgDeepChunk = kLdgDeepUnroll * 512;
 
 // content ops work on 8-byte words; objects must start 8-byte aligned
 // kind 0: raw splitmix64 bytes.  kind 1: bf16 weights — every 16-bit lane of
@@ -395,10 +399,10 @@ struct VerifyOp {
 // ---------------------------------------------------------------------------
 // LDG-engine kernels
 
-template <bool kTable, bool kL2Hint>
+template <bool kTable, bool kL2Hint, int kUnroll = kLdgUnroll>
 __global__ void __launch_bounds__(kLdgThreads) page_copy_ldg(PageResolver<kTable> res) {
   const uint32_t total = res.setup(nullptr);
-  warp_loop(res, total, CopyOpT<kL2Hint>{}, nullptr);
+  warp_loop(res, total, CopyOpT<kL2Hint, kUnroll>{}, nullptr);
 }
 
 template <typename Op>
@@ -605,6 +609,13 @@ int launch_pages(PageResolver<kTable> res, int engine, int max_ctas, void* strea
       page_copy_ldg<kTable, true><<<g, kLdgThreads, 0, (cudaStream_t)stream>>>(res);
     else
       page_copy_ldg<kTable, false><<<g, kLdgThreads, 0, (cudaStream_t)stream>>>(res);
+  } else if (engine == HV_ENGINE_LDG16) {
+    res.chunk = kLdgDeepChunk;
+    res.chunks_per_page = (uint32_t)((res.page_bytes + kLdgDeepChunk - 1) / kLdgDeepChunk);
+    const uint64_t total = (uint64_t)res.n_pages * res.chunks_per_page;
+    if (total >= 0xffffffffull) return HV_E_INVALID;
+    page_copy_ldg<kTable, false, kLdgDeepUnroll>
+        <<<ldg_grid(dev, total, max_ctas), kLdgThreads, 0, (cudaStream_t)stream>>>(res);
   } else {
     return HV_E_INVALID;
   }
@@ -641,6 +652,10 @@ int launch_descs(const uint64_t* d_src, const uint64_t* d_dst, const uint64_t* d
       res.chunk = kLdgChunk;
       desc_op_kernel<<<ldg_grid(dev, chunks_hint, max_ctas), kLdgThreads, 0, (cudaStream_t)stream>>>(
           res, CopyOpT<true>{});
+    } else if (is_copy && engine == HV_ENGINE_LDG16) {
+      res.chunk = kLdgDeepChunk;
+      desc_op_kernel<<<ldg_grid(dev, chunks_hint, max_ctas), kLdgThreads, 0, (cudaStream_t)stream>>>(
+          res, CopyOpT<false, kLdgDeepUnroll>{});
     } else if (engine == HV_ENGINE_LDG || !is_copy) {
       res.chunk = kLdgChunk;
       desc_op_kernel<<<ldg_grid(dev, chunks_hint, max_ctas), kLdgThreads, 0, (cudaStream_t)stream>>>(res, o);

@@ -63,7 +63,7 @@ def main():
     res = {}
     for src_name, base in (("hbm", slots_dev.data_ptr()), ("host", host.device_address())):
         sp = u64([base + int(p) * page for p in perm])
-        for eng in ("ldg", "ldg256", "tma"):
+        for eng in ("ldg", "ldg256", "ldg16", "tma"):
             for mc in (0, 16, 32, 64):
                 med, mn = timeit(lambda: F.kv_gather(sp, page, dst=dst, engine=eng, max_ctas=mc))
                 res[f"kv_{src_name}_{eng}_ctas{mc}"] = {"us": med * 1e6, "GBps": nb / med / 1e9}
@@ -86,7 +86,7 @@ def main():
         sp = u64([base + i * esz for i in range(ne)])
         dp = u64([edst.data_ptr() + i * esz for i in range(ne)])
         sz = u64([esz] * ne)
-        for eng in ("ldg", "ldg256", "tma"):
+        for eng in ("ldg", "ldg256", "ldg16", "tma"):
             for mc in (0, 16, 32, 64):
                 med, mn = timeit(lambda: F.batch_copy(sp, dp, sz, engine=eng, max_ctas=mc), iters=5)
                 res[f"exp_{src_name}_{eng}_ctas{mc}"] = {"ms": med * 1e3, "GBps": ne * esz / med / 1e9}
@@ -97,7 +97,7 @@ def main():
             med, mn = timeit(lambda: F.ce_batch_copy(hs, hd, hz, batched=bool(bt)), iters=5)
             res[f"exp_{src_name}_ce{'batch' if bt else 'loop'}"] = {"ms": med * 1e3, "GBps": ne * esz / med / 1e9}
         # single-expert latency
-        for eng in ("ldg", "ldg256", "tma"):
+        for eng in ("ldg", "ldg256", "ldg16", "tma"):
             med, mn = timeit(lambda: F.batch_copy(sp[:1], dp[:1], sz[:1], engine=eng), iters=20)
             res[f"lat1_{src_name}_{eng}_us"] = med * 1e6
         med, mn = timeit(lambda: F.ce_batch_copy(hs[:1], hd[:1], hz[:1], batched=False), iters=20)
