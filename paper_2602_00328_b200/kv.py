@@ -481,10 +481,25 @@ class KVCacheManager:
         for i, bid in enumerate(block_ids):
             bases[i], strides[i] = self._page_base(self.table[bid])
         src = bases + np.uint64(layer) * strides
-        d_src = torch.from_numpy(src.view(np.int64)).to(self.dev)
+        s = N.stream_handle(stream) if stream is not None else self.stream
+        pinned, d_src = self._stage_u64(src, s)   # async, stream-ordered: no host stall
         from . import fetch as F
-        F.kv_gather(d_src, self.page, dst=dst, engine=self.engine, max_ctas=self.max_ctas,
-                    stream=stream if stream is not None else self.stream)
+        F.kv_gather(d_src, self.page, dst=dst, engine=self.engine, max_ctas=self.max_ctas, stream=s)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.ExternalStream(s, device=self.dev))
+        self._staged.append((ev, pinned, d_src))   # alive until the gather that reads them is done
+
+    def _stage_u64(self, arr: np.ndarray, stream: int) -> tuple[torch.Tensor, torch.Tensor]:
+        """Upload a host u64 array through pinned memory on `stream`; the
+        caller keeps both buffers referenced until its consumer completes."""
+        from collections import deque
+        keep = self.__dict__.setdefault("_staged", deque())
+        while keep and keep[0][0].query():
+            keep.popleft()
+        pinned = torch.from_numpy(arr.view(np.int64)).pin_memory()
+        dev = torch.empty(pinned.numel(), dtype=torch.int64, device=self.dev)
+        N.call("hv_memcpy_h2d", dev.data_ptr(), pinned.data_ptr(), pinned.numel() * 8, stream)
+        return pinned, dev
 
     def block_pages_local(self, bid: int) -> torch.Tensor:
         b = self.table[bid]
