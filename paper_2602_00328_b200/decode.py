@@ -33,6 +33,7 @@ import torch
 import torch.nn.functional as TF
 
 from . import _native as N
+from ._nvtx import annotate
 from .moe import ExpertFetcher
 
 
@@ -175,6 +176,7 @@ class MoEDecoder:
         return ev
 
     # ---------------------------------------------------------------- step
+    @annotate("harvest.decode_step")
     def step(self, x: torch.Tensor) -> torch.Tensor:
         """One decode step over all layers; returns the new hidden states.
         Residency changes (revocation callbacks, re-placement arrivals) seen

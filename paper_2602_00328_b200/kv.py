@@ -34,6 +34,7 @@ import numpy as np
 import torch
 
 from . import _native as N
+from ._nvtx import annotate
 from .interconnect import LinkSpec, transfer_time
 from .pool import HostTier
 from .runtime import AllocationHints, Durability, HarvestHandle, RevokeReason, stable_hash64
@@ -315,6 +316,7 @@ class KVCacheManager:
         self.rt.harvest_register_cb(h, lambda hh, reason, idx=idx: self._on_revoke(idx, reason))
         return idx, slab.free.pop()
 
+    @annotate("harvest.kv_evict")
     def evict(self, bytes_needed: int) -> list[tuple[int, str, str]]:
         """Move LRU/FIFO/tail blocks out of local HBM: to a peer slab when one can
         be harvested (Backed blocks also keep a host copy), else to host.
@@ -390,6 +392,7 @@ class KVCacheManager:
         t_host = transfer_time(link, block.entries * self.m.bytes_per_entry)
         return "FetchFromHost" if t_host <= block.entries * self.m.recompute_time_per_entry else "Recompute"
 
+    @annotate("harvest.kv_reload")
     def reload(self, block_ids) -> dict:
         """Bring blocks to LocalHBM from their resident tier in ONE K1 launch.
         Revoked-peer blocks resolve through resolve_fallback; Lossy blocks
@@ -473,6 +476,7 @@ class KVCacheManager:
                 self.rt.harvest_free(s.handle)
 
     # ------------------------------------------------------------ the per-layer gather (C1)
+    @annotate("harvest.kv_gather_layer")
     def gather_layer(self, layer: int, block_ids, dst: torch.Tensor, stream=None) -> None:
         """K1: page `layer` of every listed block -> dst[i] (contiguous), read
         from wherever the block is resident (local / peer / host)."""

@@ -25,6 +25,7 @@ import torch
 
 from . import _native as N
 from . import fetch as F
+from ._nvtx import annotate
 from .memalloc import Segment, Tier
 from .runtime import AllocationHints, Durability, HarvestHandle, HarvestRuntime, stable_hash64
 
@@ -285,6 +286,7 @@ class ExpertFetcher:
             out.append((int(e), "peer" if (t == 1 and h is not None and self.rt.is_live(h)) else "host"))
         return out
 
+    @annotate("harvest.issue_fetches")
     def issue_fetches(self, layer: int, experts, dst_ptrs) -> "FetchBatch":
         experts = np.asarray(experts, dtype=np.int64)
         dst_ptrs = np.asarray(dst_ptrs, dtype=np.uint64)
