@@ -179,6 +179,16 @@ int hv_kv_gather_table(const uint64_t* d_slot_bases, const uint64_t* d_locs,
                        uint32_t n_pages, uint64_t page_bytes, int engine,
                        int max_ctas, void* stream);
 
+/* K1 over a block table with per-layer strides (a paged KV cache moved whole
+ * blocks at a time: evict / reload).  Page (l, b), for
+ * l < n_layers and b < n_blocks, is copied from
+ *   d_src_base[b] + l * d_src_stride[b]  to  d_dst_base[b] + l * d_dst_stride[b].
+ * Four n_blocks-long arrays describe n_blocks * n_layers pages. */
+int hv_kv_gather_blocks(const uint64_t* d_src_base, const uint64_t* d_src_stride,
+                        const uint64_t* d_dst_base, const uint64_t* d_dst_stride,
+                        uint32_t n_blocks, uint32_t n_layers, uint64_t page_bytes,
+                        int engine, int max_ctas, void* stream);
+
 /* K2: variable-size batched fetch (expert weights, placement copy-in):
  * d_src[i] -> d_dst[i], d_bytes[i] bytes, for i < n.  One launch for a whole
  * pipeline stage (moe.py:282-313). */

@@ -174,6 +174,41 @@ struct PageResolver {
   }
 };
 
+// Strided block pages (K1 over a block table, the layout of a paged KV cache):
+// page p = l * n_blocks + b (layer-major), with
+//   src = src_base[b] + l * src_stride[b],  dst = dst_base[b] + l * dst_stride[b].
+// Four n_blocks-long arrays describe n_blocks * n_layers pages.
+struct BlockResolver {
+  const uint64_t* src_base;
+  const uint64_t* src_stride;
+  const uint64_t* dst_base;
+  const uint64_t* dst_stride;
+  uint64_t page_bytes;
+  uint32_t chunks_per_page;
+  uint32_t n_blocks;
+  uint32_t n_layers;
+  uint32_t chunk;
+
+  __device__ __forceinline__ uint32_t setup(void*) const { return n_blocks * n_layers * chunks_per_page; }
+  __device__ __forceinline__ ChunkRef at(uint32_t c, uint32_t& hint) const {
+    (void)hint;
+    const uint32_t page = c / chunks_per_page;
+    const uint32_t ci = c - page * chunks_per_page;
+    const uint32_t l = page / n_blocks;
+    const uint32_t b = page - l * n_blocks;
+    const uint64_t s = __ldg(src_base + b) + (uint64_t)l * __ldg(src_stride + b);
+    const uint64_t d = __ldg(dst_base + b) + (uint64_t)l * __ldg(dst_stride + b);
+    ChunkRef r;
+    r.off = (uint64_t)ci * chunk;
+    const uint64_t rem = page_bytes - r.off;
+    r.len = rem < chunk ? (uint32_t)rem : chunk;
+    r.src = reinterpret_cast<const char*>(s) + r.off;
+    r.dst = reinterpret_cast<char*>(d) + r.off;
+    r.obj = page;
+    return r;
+  }
+};
+
 // Variable-size descriptors (K2).  The per-CTA prefix of chunk counts lives
 // in shared memory; a warp's successive chunks are monotone in c, so the
 // object index is found by a short forward probe before falling back to
@@ -535,6 +570,19 @@ __global__ void __launch_bounds__(kTmaThreads) page_copy_tma(PageResolver<kTable
   tma_loop(res, total, nullptr, dyn_smem, bars);
 }
 
+__global__ void __launch_bounds__(kTmaThreads) block_copy_tma(BlockResolver res) {
+  extern __shared__ __align__(128) char dyn_smem[];
+  __shared__ __align__(8) uint64_t bars[kTmaStages];
+  const uint32_t total = res.setup(nullptr);
+  tma_loop(res, total, nullptr, dyn_smem, bars);
+}
+
+template <bool kL2Hint, int kUnroll>
+__global__ void __launch_bounds__(kLdgThreads) block_copy_ldg(BlockResolver res) {
+  const uint32_t total = res.setup(nullptr);
+  warp_loop(res, total, CopyOpT<kL2Hint, kUnroll>{}, nullptr);
+}
+
 __global__ void __launch_bounds__(kTmaThreads) desc_copy_tma(DescResolver res) {
   extern __shared__ __align__(128) char dyn_smem[];
   __shared__ __align__(8) uint64_t bars[kTmaStages];
@@ -579,6 +627,8 @@ int set_tma_attrs() {
       e = cudaFuncSetAttribute(page_copy_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(desc_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(block_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
     st = hv_cuda_status(e);
     (void)cudaGetLastError();
   });
@@ -618,6 +668,35 @@ int launch_pages(PageResolver<kTable> res, int engine, int max_ctas, void* strea
         <<<ldg_grid(dev, total, max_ctas), kLdgThreads, 0, (cudaStream_t)stream>>>(res);
   } else {
     return HV_E_INVALID;
+  }
+  HV_CUDA(cudaGetLastError());
+  hv::note_launch();
+  return HV_OK;
+}
+
+int launch_blocks(BlockResolver res, int engine, int max_ctas, void* stream) {
+  int dev = 0;
+  int st = hv::bind_stream_device(stream, &dev);
+  if (st) return st;
+  if (res.n_blocks == 0 || res.n_layers == 0 || res.page_bytes == 0) return HV_OK;
+  engine = pick_engine(engine);
+  uint32_t chunk = kLdgChunk;
+  if (engine == HV_ENGINE_TMA) chunk = kTmaChunk;
+  else if (engine == HV_ENGINE_LDG16) chunk = kLdgDeepChunk;
+  else if (engine != HV_ENGINE_LDG && engine != HV_ENGINE_LDG256) return HV_E_INVALID;
+  res.chunk = chunk;
+  res.chunks_per_page = (uint32_t)((res.page_bytes + chunk - 1) / chunk);
+  const uint64_t total = (uint64_t)res.n_blocks * res.n_layers * res.chunks_per_page;
+  if (total >= 0xffffffffull) return HV_E_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (engine == HV_ENGINE_TMA) {
+    if ((st = set_tma_attrs())) return st;
+    block_copy_tma<<<tma_grid(dev, total, max_ctas), kTmaThreads, kTmaSmem, s>>>(res);
+  } else {
+    const int g = ldg_grid(dev, total, max_ctas);
+    if (engine == HV_ENGINE_LDG256) block_copy_ldg<true, kLdgUnroll><<<g, kLdgThreads, 0, s>>>(res);
+    else if (engine == HV_ENGINE_LDG16) block_copy_ldg<false, kLdgDeepUnroll><<<g, kLdgThreads, 0, s>>>(res);
+    else block_copy_ldg<false, kLdgUnroll><<<g, kLdgThreads, 0, s>>>(res);
   }
   HV_CUDA(cudaGetLastError());
   hv::note_launch();
@@ -780,6 +859,21 @@ HV_EXPORT int hv_kv_gather_table(const uint64_t* d_slot_bases, const uint64_t* d
   r.page_bytes = page_bytes;
   r.n_pages = n_pages;
   return launch_pages(r, engine, max_ctas, stream);
+}
+
+HV_EXPORT int hv_kv_gather_blocks(const uint64_t* d_src_base, const uint64_t* d_src_stride,
+                                  const uint64_t* d_dst_base, const uint64_t* d_dst_stride, uint32_t n_blocks,
+                                  uint32_t n_layers, uint64_t page_bytes, int engine, int max_ctas, void* stream) {
+  HV_CHECK_ARG(n_blocks == 0 || (d_src_base && d_src_stride && d_dst_base && d_dst_stride));
+  BlockResolver r{};
+  r.src_base = d_src_base;
+  r.src_stride = d_src_stride;
+  r.dst_base = d_dst_base;
+  r.dst_stride = d_dst_stride;
+  r.page_bytes = page_bytes;
+  r.n_blocks = n_blocks;
+  r.n_layers = n_layers;
+  return launch_blocks(r, engine, max_ctas, stream);
 }
 
 HV_EXPORT int hv_batch_copy(const uint64_t* d_src, const uint64_t* d_dst, const uint64_t* d_bytes, uint32_t n,

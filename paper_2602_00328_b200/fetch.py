@@ -68,6 +68,19 @@ def kv_gather_table(slot_bases: torch.Tensor, locs: torch.Tensor, page_bytes: in
            n, page_bytes, _engine(engine), max_ctas, N.stream_handle(stream))
 
 
+def kv_gather_blocks(src_base: torch.Tensor, src_stride: torch.Tensor, dst_base: torch.Tensor,
+                     dst_stride: torch.Tensor, n_layers: int, page_bytes: int, engine="auto", max_ctas: int = 0,
+                     stream=None) -> None:
+    """K1 over a block table with per-layer strides: page (l, b) goes from
+    src_base[b] + l*src_stride[b] to dst_base[b] + l*dst_stride[b]."""
+    n = src_base.numel()
+    if not (src_stride.numel() == dst_base.numel() == dst_stride.numel() == n):
+        raise ValueError("block arrays must have equal length")
+    N.call("hv_kv_gather_blocks", _dev_u64(src_base, "src_base"), _dev_u64(src_stride, "src_stride"),
+           _dev_u64(dst_base, "dst_base"), _dev_u64(dst_stride, "dst_stride"), n, n_layers, page_bytes,
+           _engine(engine), max_ctas, N.stream_handle(stream))
+
+
 def batch_copy(src_ptrs: torch.Tensor, dst_ptrs: torch.Tensor, sizes: torch.Tensor,
                engine="auto", max_ctas: int = 0, stream=None) -> None:
     n = src_ptrs.numel()

@@ -175,25 +175,23 @@ class KVCacheManager:
     def _host_base(self, host_slot: int) -> tuple[int, int]:
         return self.host.device_address(host_slot * self.page), self.host_blocks * self.page
 
-    def _pages(self, bases: np.ndarray, strides: np.ndarray, layers=None) -> np.ndarray:
-        """Page addresses [len(layers) x n_blocks] flattened layer-major."""
-        layers = np.arange(self.L, dtype=np.uint64) if layers is None else np.asarray(layers, dtype=np.uint64)
-        return (bases[None, :] + layers[:, None] * strides[None, :]).reshape(-1)
-
-    def _launch_pages(self, src: np.ndarray, dst: np.ndarray, handles=(), on_done=None) -> None:
-        """One K1 launch over per-page pointers; drain tracked on `handles`."""
-        if len(src) == 0:
+    def _launch_blocks(self, src_b, src_s, dst_b, dst_s, handles=(), on_done=None) -> None:
+        """One K1 launch (hv_kv_gather_blocks) moving every layer of each
+        listed block: page (l, b) from src_b[b] + l*src_s[b] to dst_b[b] +
+        l*dst_s[b].  Only the four per-block arrays are uploaded (pinned,
+        stream-ordered on the fetch stream); drain tracked on `handles`."""
+        n = len(src_b)
+        if n == 0:
             if on_done:
                 on_done()
             return
-        both = torch.from_numpy(np.concatenate([src, dst]).view(np.int64)).pin_memory()
-        # stream-ordered upload of the pointer arrays on the fetch stream
-        dbuf = torch.empty(both.numel(), dtype=torch.int64, device=self.dev)
-        N.call("hv_memcpy_h2d", dbuf.data_ptr(), both.data_ptr(), both.numel() * 8, self.stream)
+        arrs = np.concatenate([np.asarray(x, dtype=np.uint64) for x in (src_b, src_s, dst_b, dst_s)])
+        pinned = torch.from_numpy(arrs.view(np.int64)).pin_memory()
+        dbuf = torch.empty(pinned.numel(), dtype=torch.int64, device=self.dev)
+        N.call("hv_memcpy_h2d", dbuf.data_ptr(), pinned.data_ptr(), pinned.numel() * 8, self.stream)
         batch = self.rt.begin_reads(list(handles)) if handles else None
-        n = len(src)
 
-        def _done(_x, batch=batch, keep=(both, dbuf)):
+        def _done(_x, batch=batch, keep=(pinned, dbuf)):
             if batch is not None:
                 self.rt.end_reads(batch)
             if on_done:
@@ -203,11 +201,13 @@ class KVCacheManager:
         if timing is not None:  # kernel-only time of this launch, on the fetch stream
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record(torch.cuda.ExternalStream(self.stream, device=self.dev))
-        self.sys.engine.launch_pages(dbuf.data_ptr(), n, self.page, dst_page_ptrs_dev=dbuf.data_ptr() + 8 * n,
-                                     callbacks=[_done])
+        p = dbuf.data_ptr()
+        N.call("hv_kv_gather_blocks", p, p + 8 * n, p + 16 * n, p + 24 * n, n, self.L, self.page,
+               self.engine, self.max_ctas, self.stream)
+        self.sys.engine.track([_done])
         if timing is not None:
             ev1.record(torch.cuda.ExternalStream(self.stream, device=self.dev))
-            timing.append((ev0, ev1, n * self.page))
+            timing.append((ev0, ev1, n * self.L * self.page))
 
     # ------------------------------------------------------------ append
     def append_kv(self, sequence_id: int, tokens: int, durability: Durability | None = None) -> list[int]:
@@ -354,9 +354,7 @@ class KVCacheManager:
                 moves.append((b.block_id, "LocalHBM", "HostDRAM"))
             self.sys.loop.record("kv_evict", block=b.block_id, to=moves[-1][2])
         if src_b:
-            src = self._pages(np.array(src_b, dtype=np.uint64), np.array(src_s, dtype=np.uint64))
-            dst = self._pages(np.array(dst_b, dtype=np.uint64), np.array(dst_s, dtype=np.uint64))
-            self._launch_pages(src, dst, handles)
+            self._launch_blocks(src_b, src_s, dst_b, dst_s, handles)
             # freed local slots are reusable only after the copies drained them
             self.sys.engine.synchronize()
             self.sys.loop.poll()
@@ -453,9 +451,8 @@ class KVCacheManager:
         self.stats["reload_peer"] += len(plan_peer)
         self.stats["reload_host"] += len(plan_host)
         if k:
-            src = self._pages(src_b[:k], src_s[:k])
-            dst = self._pages(dst_b[:k], np.full(k, self.local_blocks * page, dtype=np.uint64))
-            self._launch_pages(src, dst, handles)
+            self._launch_blocks(src_b[:k], src_s[:k], dst_b[:k], np.full(k, self.local_blocks * page, dtype=np.uint64),
+                                handles)
         # old peer slots become reusable only now: any later write into them is
         # stream-ordered after this launch's reads (same fetch stream)
         for slab_i, slot in vacated:

@@ -165,23 +165,24 @@ class HarvestPeerHandler(OffloadingHandler):
             kind = ("PEER", "GPU")
         else:
             return False
-        layers = np.arange(self.L, dtype=np.uint64)[:, None]
-        sp = (sb[None, :] + layers * ss[None, :]).reshape(-1)
-        dp = (db[None, :] + layers * ds[None, :]).reshape(-1)
-        both = torch.from_numpy(np.concatenate([sp, dp]).view(np.int64)).pin_memory()
-        dbuf = torch.empty(both.numel(), dtype=torch.int64, device=self.dev)
-        N.call("hv_memcpy_h2d", dbuf.data_ptr(), both.data_ptr(), both.numel() * 8, self.stream)
+        # one K1 launch over the block table: page (l, b) at base[b] + l*stride[b]
+        nb = len(sb)
+        arrs = np.concatenate([np.broadcast_to(np.asarray(x, dtype=np.uint64), (nb,)) for x in (sb, ss, db, ds)])
+        pinned = torch.from_numpy(arrs.view(np.int64)).pin_memory()
+        dbuf = torch.empty(pinned.numel(), dtype=torch.int64, device=self.dev)
+        N.call("hv_memcpy_h2d", dbuf.data_ptr(), pinned.data_ptr(), pinned.numel() * 8, self.stream)
         batch = self.rt.begin_reads(handles) if handles else None
-        n = len(sp)
-        nbytes = n * self.page
+        nbytes = nb * self.L * self.page
 
-        def _finish(_x, keep=(both, dbuf), batch=batch):
+        def _finish(_x, keep=(pinned, dbuf), batch=batch):
             if batch is not None:
                 self.rt.end_reads(batch)
             self._done.append(TransferResult(job_id, True, nbytes, time.perf_counter() - t0, kind))
 
-        self.sys.engine.launch_pages(dbuf.data_ptr(), n, self.page, dst_page_ptrs_dev=dbuf.data_ptr() + 8 * n,
-                                     callbacks=[_finish])
+        p = dbuf.data_ptr()
+        N.call("hv_kv_gather_blocks", p, p + 8 * nb, p + 16 * nb, p + 24 * nb, nb, self.L, self.page,
+               self.sys.engine.engine, self.sys.engine.max_ctas, self.stream)
+        self.sys.engine.track([_finish])
         self._jobs[job_id] = kind
         return True
 
