@@ -39,7 +39,7 @@ sys.path.insert(0, REPO)
 
 from benchlib.common import (KV_SLAB_BLOCKS, KV_TOKENS, METRIC, SEED, emit, kv_slab_bytes, load_traffic, model, routing, workload_config)  # noqa: E402
 from benchlib.compare import (autotune, measure_pcie_h2d, probe_engines_on_peer, same_run_comparisons)  # noqa: E402
-from benchlib.cpu import (cpu_gather_sample, cpu_host_copy, run_reference)  # noqa: E402
+from benchlib.cpu import (cpu_gather_sample, cpu_host_copy, reference_simulator, run_reference)  # noqa: E402
 from benchlib.phases import (churn_phase, host_offload_decode, kv_long_context, phi_phase, run_decode)  # noqa: E402
 
 
@@ -352,6 +352,10 @@ def run_b200(a):
             cpu = {"value": gbps, "unit": "GB/s", "cores": threads, "kind": "port",
                    "sample": f"{layers} layer-fetches ({moved / 1e9:.1f} GB) of the same routing, memcpy gather "
                              f"from a host expert table (oracle/hv_oracle.c), {secs:.1f} s, {threads} threads"}
+        try:
+            refsim = reference_simulator(m, world - 1)
+        except Exception as e:  # report, never lose the main line
+            refsim = {"error": repr(e)[:300]}
         line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
@@ -364,7 +368,7 @@ def run_b200(a):
                 "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
                 "clocks": {**clk.summary(), "first_attempt_rejected": remeasured},
                 "latency_ms_per_layer_fetch": statistics.median(launch_ms), "decode": decode,
-                "kv_long_context_128k": kvlc, **extra}
+                "kv_long_context_128k": kvlc, "reference_simulator": refsim, **extra}
     barrier()
     sysm.close()
     for p in imported:

@@ -91,5 +91,54 @@ def run_reference(a):
                              "sample": f"first 4 of {m.num_layers} layers of each decode step "
                                        f"(memcpy gather, oracle/hv_oracle.c, {threads} threads)"},
             "e2e": {"value": gbps, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    try:
+        line["reference_simulator"] = reference_simulator(m, max(0, a.gpus - 1))
+    except Exception as e:
+        line["reference_simulator"] = {"error": repr(e)[:300]}
     emit(line, a)
     return 0
+
+
+def reference_simulator(m, n_peers: int, steps: int = 4) -> dict:
+    """The reference's own fetch path, unmodified, timed on one host core:
+    ``harvestsim.moe.simulate_decode`` (moe.py:343-351) with the workload's
+    model shape, every expert offloaded (moe.py:354-383) to the host tier
+    (n_peers == 0) or placed on n_peers modeled peers.  It moves no bytes: the
+    result is its Python cost per ``app_transfer`` (runtime.py:320-364) and
+    the decode rate its calibrated model (profiles.py:51-57, H100) predicts.
+    Imported from the pip-installed copy under baseline/_ref (never from
+    /root/reference, which does not exist on the GPU box)."""
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "harvestsim")):
+        return {"unavailable": "baseline/_ref/harvestsim not installed"}
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    from harvestsim import moe as RM, profiles as RP
+    from harvestsim.events import Simulator
+    from harvestsim.memalloc import Tier
+    from harvestsim.runtime import HarvestRuntime
+    prof = RP.MoEProfile(m.name, num_layers=m.num_layers, num_experts=m.num_experts, top_k=m.top_k,
+                         expert_size=m.expert_size, compute_time_per_microbatch=0.0)
+    pipe = RM.PipelineConfig(microbatch_tokens=32, num_microbatches=steps)
+    trace = RM.generate_routing(prof, pipe, 0.0, 0, 2)  # skew 0 = uniform routing, as bench's N(0,1) logits
+    sim = Simulator()
+    topo = RP.build_topology(RP.PAPER_H100, num_peers=n_peers)
+    rt = HarvestRuntime(sim, topo)
+    host_id = topo.devices[-1].device_id
+    res = RM.ExpertResidency(prof)
+    t0 = time.perf_counter()
+    RM.place_offloaded(sim, rt, prof, res, trace, 100.0, Tier.PEER_HBM if n_peers else Tier.HOST_DRAM, host_id)
+    t_place = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    met = RM.simulate_decode(sim, rt, prof, pipe, trace, res, host_id)
+    wall = time.perf_counter() - t0
+    moved = met.reads * m.expert_size
+    return {"impl": "harvestsim (reference, unmodified, baseline/_ref)", "cores": 1,
+            "tier": "peer" if n_peers else "host", "modeled_peers": n_peers, "decode_steps": steps,
+            "fetches": met.reads, "read_errors": met.read_errors,
+            "wall_s": wall, "wall_us_per_fetch": 1e6 * wall / max(1, met.reads),
+            "placement_wall_s": t_place,
+            "modeled_decode_s": met.decode_time, "modeled_tok_s": met.tokens_per_s,
+            "modeled_GBps": moved / met.decode_time / 1e9 if met.decode_time > 0 else None,
+            "note": "simulator: moves no bytes; modeled numbers use its H100 calibration (55 GB/s host, "
+                    "495 GB/s peer) with zero compute time, so they are link-model predictions"}
