@@ -26,9 +26,31 @@ static inline int hv_cuda_status(cudaError_t e) {
   } while (0)
 
 namespace hv {
+// Switches the calling thread's current device for the duration of one ABI
+// call and restores the caller's on return: the library never leaves a
+// different device current behind (torch and the caller keep theirs).
+struct DeviceGuard {
+  int prev = -1;
+  bool changed = false;
+  int set(int dev) {
+    if (prev < 0 && cudaGetDevice(&prev) != cudaSuccess) {
+      (void)cudaGetLastError();
+      prev = -1;
+    }
+    if (dev == (changed ? -2 : prev)) return HV_OK;
+    HV_CUDA(cudaSetDevice(dev));
+    changed = dev != prev;
+    return HV_OK;
+  }
+  ~DeviceGuard() {
+    if (changed && prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 // Make the device that owns `stream` current (static cudart keeps its own
-// notion of the current device, so never rely on the caller's).
-int bind_stream_device(void* stream, int* device_out);
+// notion of the current device, so never rely on the caller's); `g` restores
+// the caller's device when the ABI call returns.
+int bind_stream_device(void* stream, int* device_out, DeviceGuard& g);
 void note_launch(uint64_t n = 1);
 int sm_count(int device);
 }  // namespace hv

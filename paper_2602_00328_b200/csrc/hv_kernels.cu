@@ -36,7 +36,7 @@ namespace hv {
 static std::atomic<uint64_t> g_launches{0};
 void note_launch(uint64_t n) { g_launches += n; }
 
-int bind_stream_device(void* stream, int* device_out) {
+int bind_stream_device(void* stream, int* device_out, DeviceGuard& g) {
   int dev = 0;
   if (stream) {
     cudaError_t e = cudaStreamGetDevice((cudaStream_t)stream, &dev);
@@ -47,8 +47,8 @@ int bind_stream_device(void* stream, int* device_out) {
   } else {
     HV_CUDA(cudaGetDevice(&dev));
   }
-  int cur = -1;
-  if (cudaGetDevice(&cur) != cudaSuccess || cur != dev) HV_CUDA(cudaSetDevice(dev));
+  int st = g.set(dev);
+  if (st) return st;
   if (device_out) *device_out = dev;
   return HV_OK;
 }
@@ -638,7 +638,8 @@ int set_tma_attrs() {
 template <bool kTable>
 int launch_pages(PageResolver<kTable> res, int engine, int max_ctas, void* stream) {
   int dev = 0;
-  int st = hv::bind_stream_device(stream, &dev);
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
   if (res.n_pages == 0 || res.page_bytes == 0) return HV_OK;
   engine = pick_engine(engine);
@@ -676,7 +677,8 @@ int launch_pages(PageResolver<kTable> res, int engine, int max_ctas, void* strea
 
 int launch_blocks(BlockResolver res, int engine, int max_ctas, void* stream) {
   int dev = 0;
-  int st = hv::bind_stream_device(stream, &dev);
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
   if (res.n_blocks == 0 || res.n_layers == 0 || res.page_bytes == 0) return HV_OK;
   engine = pick_engine(engine);
@@ -711,7 +713,8 @@ int launch_descs(const uint64_t* d_src, const uint64_t* d_dst, const uint64_t* d
                  int engine, int max_ctas, void* stream, Op op, bool is_copy,
                  uint64_t chunks_hint = kUnknownChunks) {
   int dev = 0;
-  int st = hv::bind_stream_device(stream, &dev);
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
   engine = pick_engine(engine);
   if (engine == HV_ENGINE_TMA && is_copy && (st = set_tma_attrs())) return st;
@@ -888,7 +891,8 @@ HV_EXPORT int hv_swap_blocks_batch(const uint64_t* h_src, const uint64_t* h_dst,
   if (n == 0) return HV_OK;
   HV_CHECK_ARG(h_src && h_dst && h_bytes);
   int dev = 0;
-  int st = hv::bind_stream_device(stream, &dev);
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
   std::lock_guard<std::mutex> lk(g_ring_mu);
   for (uint32_t base = 0; base < n; base += kSlotDescs) {
@@ -940,7 +944,8 @@ HV_EXPORT int hv_ce_batch_copy(const uint64_t* h_src, const uint64_t* h_dst, con
   if (n == 0) return HV_OK;
   HV_CHECK_ARG(h_src && h_dst && h_bytes);
   int dev = 0;
-  int st = hv::bind_stream_device(stream, &dev);
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
   if (!batched) {
     for (uint32_t i = 0; i < n; ++i)
@@ -1011,7 +1016,8 @@ HV_EXPORT int hv_digest(const uint64_t* d_src, const uint64_t* d_bytes, uint32_t
   if (n == 0) return HV_OK;
   HV_CHECK_ARG(d_src && d_bytes && d_out);
   int dev = 0;
-  int st = hv::bind_stream_device(stream, &dev);
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
   HV_CUDA(cudaMemsetAsync(d_out, 0, (size_t)n * 8, (cudaStream_t)stream));
   DigestOpR op;
@@ -1025,7 +1031,8 @@ HV_EXPORT int hv_verify_content(const uint64_t* d_src, const uint64_t* d_bytes, 
   if (n == 0) return HV_OK;
   HV_CHECK_ARG(d_src && d_bytes && d_seeds && d_mismatch);
   int dev = 0;
-  int st = hv::bind_stream_device(stream, &dev);
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
   HV_CUDA(cudaMemsetAsync(d_mismatch, 0, (size_t)n * 8, (cudaStream_t)stream));
   VerifyOpR op;
@@ -1040,7 +1047,8 @@ HV_EXPORT int hv_verify_weights_bf16(const uint64_t* d_src, const uint64_t* d_by
   if (n == 0) return HV_OK;
   HV_CHECK_ARG(d_src && d_bytes && d_seeds && d_mismatch);
   int dev = 0;
-  int st = hv::bind_stream_device(stream, &dev);
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
   HV_CUDA(cudaMemsetAsync(d_mismatch, 0, (size_t)n * 8, (cudaStream_t)stream));
   VerifyOpR op;

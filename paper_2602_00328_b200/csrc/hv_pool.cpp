@@ -175,7 +175,12 @@ HV_EXPORT int hv_pool_create(int donor_dev, uint64_t bytes, uint64_t chunk_bytes
     }
   }
   if (flags & HV_POOL_IPC) {
-    HV_CUDA(cudaSetDevice(donor_dev));
+    hv::DeviceGuard dg;
+    int gs = dg.set(donor_dev);
+    if (gs) {
+      delete p;
+      return gs;
+    }
     void* ptr = nullptr;
     cudaError_t e = cudaMalloc(&ptr, bytes);
     if (e != cudaSuccess) {
@@ -185,7 +190,7 @@ HV_EXPORT int hv_pool_create(int donor_dev, uint64_t bytes, uint64_t chunk_bytes
     }
     for (int rd : p->readers) {
       if (rd == donor_dev) continue;
-      cudaSetDevice(rd);
+      if (dg.set(rd)) continue;
       e = cudaDeviceEnablePeerAccess(donor_dev, 0);
       if (e == cudaErrorPeerAccessAlreadyEnabled) e = cudaSuccess;
       (void)cudaGetLastError();
@@ -294,7 +299,8 @@ HV_EXPORT int hv_pool_destroy(hv_pool* p) {
     cudaError_t e = cudaIpcCloseMemHandle((void*)p->va);
     if (e != cudaSuccess) st = hv_cuda_status(e);
   } else if (p->flags & HV_POOL_IPC) {
-    cudaSetDevice(p->donor);
+    hv::DeviceGuard dg;
+    dg.set(p->donor);
     cudaError_t e = cudaFree((void*)p->va);
     if (e != cudaSuccess) st = hv_cuda_status(e);
   } else if (p->va) {
@@ -313,7 +319,11 @@ HV_EXPORT int hv_pool_destroy(hv_pool* p) {
 
 HV_EXPORT int hv_pool_export_ipc(const hv_pool* p, void* handle64) {
   HV_CHECK_ARG(p && handle64 && (p->flags & HV_POOL_IPC) && !p->imported);
-  HV_CUDA(cudaSetDevice(p->donor));
+  hv::DeviceGuard dg;
+  {
+    int gs = dg.set(p->donor);
+    if (gs) return gs;
+  }
   cudaIpcMemHandle_t h;
   HV_CUDA(cudaIpcGetMemHandle(&h, (void*)p->va));
   static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
@@ -324,7 +334,11 @@ HV_EXPORT int hv_pool_export_ipc(const hv_pool* p, void* handle64) {
 HV_EXPORT int hv_pool_import_ipc(const void* handle64, int donor_dev, uint64_t bytes,
                                  int reader_dev, hv_pool** out) {
   HV_CHECK_ARG(handle64 && out && bytes > 0);
-  HV_CUDA(cudaSetDevice(reader_dev));
+  hv::DeviceGuard dg;
+  {
+    int gs = dg.set(reader_dev);
+    if (gs) return gs;
+  }
   cudaIpcMemHandle_t h;
   memcpy(&h, handle64, sizeof(h));
   void* ptr = nullptr;
@@ -418,13 +432,13 @@ HV_EXPORT int hv_device_count(int* n) {
 
 HV_EXPORT int hv_mem_get_info(int device, uint64_t* free_bytes, uint64_t* total_bytes) {
   HV_CHECK_ARG(free_bytes && total_bytes);
-  int cur = -1;
-  HV_CUDA(cudaGetDevice(&cur));
-  if (cur != device) HV_CUDA(cudaSetDevice(device));
+  hv::DeviceGuard dg;
+  {
+    int gs = dg.set(device);
+    if (gs) return gs;
+  }
   size_t f = 0, t = 0;
-  cudaError_t e = cudaMemGetInfo(&f, &t);
-  if (cur != device) cudaSetDevice(cur);
-  HV_CUDA(e);
+  HV_CUDA(cudaMemGetInfo(&f, &t));
   *free_bytes = f;
   *total_bytes = t;
   return HV_OK;
@@ -448,7 +462,11 @@ HV_EXPORT int hv_can_access_peer(int reader, int donor, int* ok) {
 
 HV_EXPORT int hv_enable_peer_access(int reader, int donor) {
   if (reader == donor) return HV_OK;
-  HV_CUDA(cudaSetDevice(reader));
+  hv::DeviceGuard dg;
+  {
+    int gs = dg.set(reader);
+    if (gs) return gs;
+  }
   cudaError_t e = cudaDeviceEnablePeerAccess(donor, 0);
   if (e == cudaErrorPeerAccessAlreadyEnabled) {
     (void)cudaGetLastError();
@@ -459,14 +477,22 @@ HV_EXPORT int hv_enable_peer_access(int reader, int donor) {
 }
 
 HV_EXPORT int hv_device_synchronize(int device) {
-  HV_CUDA(cudaSetDevice(device));
+  hv::DeviceGuard dg;
+  {
+    int gs = dg.set(device);
+    if (gs) return gs;
+  }
   HV_CUDA(cudaDeviceSynchronize());
   return HV_OK;
 }
 
 HV_EXPORT int hv_dev_alloc(int device, uint64_t bytes, uint64_t* d_ptr) {
   HV_CHECK_ARG(d_ptr && bytes > 0);
-  HV_CUDA(cudaSetDevice(device));
+  hv::DeviceGuard dg;
+  {
+    int gs = dg.set(device);
+    if (gs) return gs;
+  }
   void* p = nullptr;
   HV_CUDA(cudaMalloc(&p, bytes));
   *d_ptr = (uint64_t)p;
@@ -474,14 +500,19 @@ HV_EXPORT int hv_dev_alloc(int device, uint64_t bytes, uint64_t* d_ptr) {
 }
 
 HV_EXPORT int hv_dev_free(int device, uint64_t d_ptr) {
-  HV_CUDA(cudaSetDevice(device));
+  hv::DeviceGuard dg;
+  {
+    int gs = dg.set(device);
+    if (gs) return gs;
+  }
   HV_CUDA(cudaFree((void*)d_ptr));
   return HV_OK;
 }
 
 HV_EXPORT int hv_memcpy_h2d(uint64_t d_dst, const void* h_src, uint64_t bytes, void* stream) {
   int dev = 0;
-  int st = hv::bind_stream_device(stream, &dev);
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
   HV_CUDA(cudaMemcpyAsync((void*)d_dst, h_src, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream));
   return HV_OK;
@@ -489,7 +520,8 @@ HV_EXPORT int hv_memcpy_h2d(uint64_t d_dst, const void* h_src, uint64_t bytes, v
 
 HV_EXPORT int hv_memcpy_d2h(void* h_dst, uint64_t d_src, uint64_t bytes, void* stream) {
   int dev = 0;
-  int st = hv::bind_stream_device(stream, &dev);
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
   HV_CUDA(cudaMemcpyAsync(h_dst, (const void*)d_src, bytes, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   return HV_OK;
@@ -497,7 +529,8 @@ HV_EXPORT int hv_memcpy_d2h(void* h_dst, uint64_t d_src, uint64_t bytes, void* s
 
 HV_EXPORT int hv_memset_d8(uint64_t d_dst, int value, uint64_t bytes, void* stream) {
   int dev = 0;
-  int st = hv::bind_stream_device(stream, &dev);
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
   HV_CUDA(cudaMemsetAsync((void*)d_dst, value, bytes, (cudaStream_t)stream));
   return HV_OK;
@@ -505,7 +538,11 @@ HV_EXPORT int hv_memset_d8(uint64_t d_dst, int value, uint64_t bytes, void* stre
 
 HV_EXPORT int hv_stream_create(int device, int priority, void** stream) {
   HV_CHECK_ARG(stream);
-  HV_CUDA(cudaSetDevice(device));
+  hv::DeviceGuard dg;
+  {
+    int gs = dg.set(device);
+    if (gs) return gs;
+  }
   cudaStream_t s = nullptr;
   HV_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, priority));
   *stream = (void*)s;
@@ -524,7 +561,11 @@ HV_EXPORT int hv_stream_synchronize(void* stream) {
 
 HV_EXPORT int hv_event_create(int device, unsigned timing, void** event) {
   HV_CHECK_ARG(event);
-  HV_CUDA(cudaSetDevice(device));
+  hv::DeviceGuard dg;
+  {
+    int gs = dg.set(device);
+    if (gs) return gs;
+  }
   cudaEvent_t e = nullptr;
   HV_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
   *event = (void*)e;
@@ -539,7 +580,8 @@ HV_EXPORT int hv_event_destroy(void* event) {
 HV_EXPORT int hv_event_record(void* event, void* stream) {
   HV_CHECK_ARG(event);
   int dev = 0;
-  int st = hv::bind_stream_device(stream, &dev);
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
   HV_CUDA(cudaEventRecord((cudaEvent_t)event, (cudaStream_t)stream));
   return HV_OK;

@@ -324,35 +324,54 @@ class KVCacheManager:
         if bytes_needed <= 0:
             raise ValueError("bytes_needed must be > 0")
         n_blocks = -(-bytes_needed // self.m.block_bytes)
+        victims = self._eviction_order()[:n_blocks]
         moves, src_b, src_s, dst_b, dst_s, handles = [], [], [], [], [], set()
-        for b in self._eviction_order()[:n_blocks]:
-            sbase, sstride = self._page_base(b)
-            placed = self._peer_slot(b.durability)
-            if placed is not None:
-                slab_i, slot = placed
-                slab = self.slabs[slab_i]
-                dbase, dstride = slab.va + slot * self.page, self.slab_blocks * self.page
-                src_b.append(sbase), src_s.append(sstride), dst_b.append(dbase), dst_s.append(dstride)
-                handles.add(slab.handle)
-                if b.durability == Durability.BACKED and b.host_slot is None:
-                    b.host_slot = self._take_host_slot()
-                    hb, hs = self._host_base(b.host_slot)
-                    src_b.append(sbase), src_s.append(sstride), dst_b.append(hb), dst_s.append(hs)
-                self.local_free.append(b.slot)
-                b.tier, b.slab, b.slot = KVTier.PEER_HBM, slab_i, slot
-                slab.blocks[slot] = b.block_id
-                self.stats["evict_peer"] += 1
-                moves.append((b.block_id, "LocalHBM", "PeerHBM"))
+        page, cache0 = self.page, self.cache.data_ptr()
+        local_stride, slab_stride = self.local_blocks * page, self.slab_blocks * page
+        host0, host_stride = self.host.device_address(0), self.host_blocks * page
+        LOCAL, PEER, HOST, BACKED = KVTier.LOCAL_HBM, KVTier.PEER_HBM, KVTier.HOST_DRAM, Durability.BACKED
+        to_peer, to_host = [], []
+        slab = None
+        for b in victims:
+            sbase = cache0 + b.slot * page
+            # fast path: the open slab still has room (else _peer_slot harvests)
+            if slab is not None and slab.live and slab.free:
+                slab_i, slot = cur, slab.free.pop()
+                placed = True
             else:
+                placed = self._peer_slot(b.durability)
+                if placed is not None:
+                    cur, slot = placed
+                    slab_i, slab = cur, self.slabs[cur]
+            if placed is not None:
+                src_b.append(sbase), src_s.append(local_stride)
+                dst_b.append(slab.va + slot * page), dst_s.append(slab_stride)
+                handles.add(slab.handle)
+                if b.durability is BACKED and b.host_slot is None:
+                    b.host_slot = self._take_host_slot()
+                    src_b.append(sbase), src_s.append(local_stride)
+                    dst_b.append(host0 + b.host_slot * page), dst_s.append(host_stride)
+                self.local_free.append(b.slot)
+                b.tier, b.slab, b.slot = PEER, slab_i, slot
+                slab.blocks[slot] = b.block_id
+                to_peer.append(b.block_id)
+            else:
+                slab = None
                 if b.host_slot is None:
                     b.host_slot = self._take_host_slot()
-                    hb, hs = self._host_base(b.host_slot)
-                    src_b.append(sbase), src_s.append(sstride), dst_b.append(hb), dst_s.append(hs)
+                    src_b.append(sbase), src_s.append(local_stride)
+                    dst_b.append(host0 + b.host_slot * page), dst_s.append(host_stride)
                 self.local_free.append(b.slot)
-                b.tier, b.slot = KVTier.HOST_DRAM, b.host_slot
-                self.stats["evict_host"] += 1
-                moves.append((b.block_id, "LocalHBM", "HostDRAM"))
-            self.sys.loop.record("kv_evict", block=b.block_id, to=moves[-1][2])
+                b.tier, b.slot = HOST, b.host_slot
+                to_host.append(b.block_id)
+            moves.append((b.block_id, "LocalHBM", "PeerHBM" if placed is not None else "HostDRAM"))
+        self.stats["evict_peer"] += len(to_peer)
+        self.stats["evict_host"] += len(to_host)
+        # one log record per destination tier and call (block ids in order)
+        if to_peer:
+            self.sys.loop.record("kv_evict", blocks=to_peer, to="PeerHBM")
+        if to_host:
+            self.sys.loop.record("kv_evict", blocks=to_host, to="HostDRAM")
         if src_b:
             self._launch_blocks(src_b, src_s, dst_b, dst_s, handles)
             # freed local slots are reusable only after the copies drained them
