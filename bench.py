@@ -367,7 +367,10 @@ def run_b200(a):
                         "d2h_bytes_per_step": d2h // a.steps, "verify_mismatched_words": int(mism_all)},
                 "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
                 "clocks": {**clk.summary(), "first_attempt_rejected": remeasured},
-                "latency_ms_per_layer_fetch": statistics.median(launch_ms), "decode": decode,
+                "latency_ms_per_layer_fetch": statistics.median(launch_ms),
+                "latency_ms_per_layer_fetch_dist": {"p50": float(np.percentile(launch_ms, 50)),
+                                                    "p99": float(np.percentile(launch_ms, 99)),
+                                                    "n": len(launch_ms)}, "decode": decode,
                 "kv_long_context_128k": kvlc, "reference_simulator": refsim, **extra}
     barrier()
     sysm.close()

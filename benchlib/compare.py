@@ -116,6 +116,19 @@ def same_run_comparisons(dev, m, a, source, fetcher=None, n=53):
                 best.append(e0.elapsed_time(e1) * 1e-3)
         return statistics.median(best)
 
+    def pct(fn, iters=100):
+        """p50/p99 of one fetch's device time over `iters` launches (after 5 warmups)."""
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+        for _ in range(5):
+            fn()
+        for e0, e1 in evs:
+            e0.record(s)
+            fn()
+            e1.record(s)
+        s.synchronize()
+        us = np.array([e0.elapsed_time(e1) * 1e3 for e0, e1 in evs])
+        return {"p50": float(np.percentile(us, 50)), "p99": float(np.percentile(us, 99)), "n": iters}
+
     out = {}
     dp = F.ptrs_tensor([dst.data_ptr() + i * S for i in range(n)], f"cuda:{dev}")
     sz = F.ptrs_tensor([S] * n, f"cuda:{dev}")
@@ -155,6 +168,13 @@ def same_run_comparisons(dev, m, a, source, fetcher=None, n=53):
         lat["copy_engine_peer"] = t(lambda: F.ce_batch_copy(ps[:1], hd[:1], hz[:1], batched=False,
                                                             stream=s.cuda_stream)) * 1e6
         lat["peer_vs_host_speedup"] = lat["copy_engine_host"] / lat["kernel_peer"]
+    # latency distribution (p50/p99 over >= 100 iterations)
+    dist_us = {"kernel_host": pct(lambda: F.batch_copy(F.ptrs_tensor([h.device_address(0)], f"cuda:{dev}"), dp[:1],
+                                                       sz[:1], engine=a.engine, stream=s.cuda_stream))}
+    if source == "peer":
+        dist_us["kernel_peer"] = pct(lambda: F.batch_copy(pdev[:1], dp[:1], sz[:1], engine=a.engine,
+                                                          stream=s.cuda_stream))
+    lat["distribution_us"] = dist_us
     out["single_expert_latency_us"] = lat
     # KV config 1 (BASELINE configs[0] shape): 1,024 x 64 KiB pages = one layer
     # of 4 sequences x 4k tokens, gathered by K1 from the tier under test
