@@ -39,7 +39,7 @@ sys.path.insert(0, REPO)
 
 from benchlib.common import (KV_SLAB_BLOCKS, KV_TOKENS, METRIC, SEED, emit, kv_slab_bytes, load_traffic, model, routing, workload_config)  # noqa: E402
 from benchlib.compare import (autotune, measure_pcie_h2d, probe_engines_on_peer, same_run_comparisons)  # noqa: E402
-from benchlib.cpu import (cpu_gather_sample, cpu_host_copy, reference_simulator, run_reference)  # noqa: E402
+from benchlib.cpu import (cpu_gather_sample, cpu_host_copy, cpu_model, reference_simulator, run_reference)  # noqa: E402
 from benchlib.phases import (churn_phase, host_offload_decode, kv_long_context, phi_phase, run_decode)  # noqa: E402
 
 
@@ -352,6 +352,9 @@ def run_b200(a):
             cpu = {"value": gbps, "unit": "GB/s", "cores": threads, "kind": "port",
                    "sample": f"{layers} layer-fetches ({moved / 1e9:.1f} GB) of the same routing, memcpy gather "
                              f"from a host expert table (oracle/hv_oracle.c), {secs:.1f} s, {threads} threads"}
+            g1, s1, l1, _ = cpu_gather_sample(m, hc, routes[a.warmup:], min(5.0, a.cpu_baseline_s), 1)
+            cpu["single_thread"] = {"value": g1, "unit": "GB/s", "cores": 1, "sample": f"{l1} layer-fetches, {s1:.1f} s"}
+            cpu["cpu_model"] = cpu_model()
         try:
             refsim = reference_simulator(m, world - 1)
         except Exception as e:  # report, never lose the main line

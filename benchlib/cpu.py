@@ -34,6 +34,16 @@ def cpu_gather_sample(m, host_buf, route_steps, seconds, threads):
                     dt = time.perf_counter() - t0
                     return moved / dt / 1e9, dt, layers, moved
 
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def host_nexp(m, host_buf):
     return (host_buf.size // m.expert_size) if isinstance(host_buf, np.ndarray) else m.num_layers * m.num_experts
 
@@ -87,7 +97,7 @@ def run_reference(a):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * dt / a.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic", "config": workload_config(m, 1, "host"),
-            "cpu_baseline": {"value": gbps, "unit": "GB/s", "cores": threads, "kind": "port",
+            "cpu_baseline": {"value": gbps, "unit": "GB/s", "cores": threads, "kind": "port", "cpu_model": cpu_model(),
                              "sample": f"first 4 of {m.num_layers} layers of each decode step "
                                        f"(memcpy gather, oracle/hv_oracle.c, {threads} threads)"},
             "e2e": {"value": gbps, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

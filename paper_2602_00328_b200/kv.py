@@ -20,10 +20,11 @@ KV tensors, so page (l, b) of block b lives at ``base[b] + l * stride[b]``:
 Peer memory is taken in slabs of ``slab_blocks`` blocks through
 ``harvest_alloc`` (one revocable handle per slab, not per 64 KiB page); a slab
 revocation invalidates its blocks: Backed blocks fall back to their host copy,
-Lossy blocks become NotMaterialized (recompute).  Every data movement of a call
-(all pages of all blocks, all layers) is ONE K1 launch with per-page
-source/destination pointers resolved from the table on the host (vectorised)
-and uploaded once.
+Lossy blocks become NotMaterialized (recompute).  Every data movement of an
+evict/reload call (all pages of all blocks, all layers) is ONE K1 launch
+(``hv_kv_gather_blocks``) over four per-block arrays (source base/stride,
+destination base/stride) resolved from the table on the host and uploaded
+once; the per-layer gather resolves one pointer per page.
 """
 from __future__ import annotations
 

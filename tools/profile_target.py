@@ -1,5 +1,5 @@
 """Short, ncu-friendly driver: a few launches of each fetch kernel at the
-bench shapes.  Usage: python tools/profile_target.py [host|hbm|kv] [engine]"""
+bench shapes.  Usage: python tools/profile_target.py [host|hbm|kv|blocks] [engine]"""
 import os
 import sys
 
@@ -30,6 +30,17 @@ def main():
         sz = F.ptrs_tensor([S] * n, dev)
         for _ in range(reps):
             F.batch_copy(sp, dp, sz, engine=eng)
+    elif what == "blocks":  # KV reload slice: 256 blocks x 32 layers x 64 KiB, [layer][slot] slabs -> cache
+        page, L, nb, slab = 65536, 32, 256, 64
+        slabs = [torch.empty(L * slab * page, dtype=torch.uint8, device=dev) for _ in range(nb // slab)]
+        cache = torch.empty(L * nb * page, dtype=torch.uint8, device=dev)
+        order = np.random.default_rng(0).permutation(nb)
+        sb = F.ptrs_tensor([slabs[o // slab].data_ptr() + (o % slab) * page for o in order], dev)
+        ss = F.ptrs_tensor([slab * page] * nb, dev)
+        db = F.ptrs_tensor([cache.data_ptr() + i * page for i in range(nb)], dev)
+        ds = F.ptrs_tensor([nb * page] * nb, dev)
+        for _ in range(reps):
+            F.kv_gather_blocks(sb, ss, db, ds, L, page, engine=eng)
     else:  # KV config 1: 1024 pages x 64 KiB from 4096 HBM slots
         page, npg, nslots = 65536, 1024, 4096
         slots = torch.empty(nslots * page, dtype=torch.uint8, device=dev)
