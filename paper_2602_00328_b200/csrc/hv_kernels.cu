@@ -637,11 +637,11 @@ int set_tma_attrs() {
 
 template <bool kTable>
 int launch_pages(PageResolver<kTable> res, int engine, int max_ctas, void* stream) {
+  if (res.n_pages == 0 || res.page_bytes == 0) return HV_OK;  // empty: no device work, no device needed
   int dev = 0;
   hv::DeviceGuard dg;
   int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
-  if (res.n_pages == 0 || res.page_bytes == 0) return HV_OK;
   engine = pick_engine(engine);
   if (engine == HV_ENGINE_TMA) {
     if ((st = set_tma_attrs())) return st;
@@ -676,11 +676,11 @@ int launch_pages(PageResolver<kTable> res, int engine, int max_ctas, void* strea
 }
 
 int launch_blocks(BlockResolver res, int engine, int max_ctas, void* stream) {
+  if (res.n_blocks == 0 || res.n_layers == 0 || res.page_bytes == 0) return HV_OK;
   int dev = 0;
   hv::DeviceGuard dg;
   int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
-  if (res.n_blocks == 0 || res.n_layers == 0 || res.page_bytes == 0) return HV_OK;
   engine = pick_engine(engine);
   uint32_t chunk = kLdgChunk;
   if (engine == HV_ENGINE_TMA) chunk = kTmaChunk;

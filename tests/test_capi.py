@@ -94,3 +94,51 @@ def test_allocator_errors_spec():
     with pytest.raises(ValueError):
         M.alloc_best_fit(st, 0)
     assert M.alloc_best_fit(st, 81) is None
+
+
+def test_launch_entry_points_validate_arguments_without_a_gpu():
+    """Argument errors are reported as HV_E_INVALID before any device work,
+    and empty batches are no-ops (so both hold on a CPU-only host)."""
+    lib = N.load()
+    INV = N.HV_E_INVALID
+    page = 65536
+    # K1 pointer form: pages but no source / no destination
+    assert lib.hv_kv_gather(0, 0, 0, 5, page, 0, 0, None) == INV
+    assert lib.hv_kv_gather(0x1000, 0, 0, 5, page, 0, 0, None) == INV
+    assert lib.hv_kv_gather(0, 0, 0, 0, page, 0, 0, None) == N.HV_OK
+    assert lib.hv_kv_gather(0x1000, 0, 0x2000, (1 << 30) + 1, page, 0, 0, None) == INV
+    # K1 table and block-table forms
+    assert lib.hv_kv_gather_table(0, 0x1000, 0x2000, 0, 3, page, 0, 0, None) == INV
+    assert lib.hv_kv_gather_table(0, 0, 0, 0, 0, page, 0, 0, None) == N.HV_OK
+    assert lib.hv_kv_gather_blocks(0x1000, 0x1000, 0, 0x1000, 4, 32, page, 0, 0, None) == INV
+    assert lib.hv_kv_gather_blocks(0, 0, 0, 0, 0, 32, page, 0, 0, None) == N.HV_OK
+    assert lib.hv_kv_gather_blocks(0x1000, 0x1000, 0x1000, 0x1000, 4, 0, page, 0, 0, None) == N.HV_OK
+    # K2 and the host-array forms
+    assert lib.hv_batch_copy(0, 0x1000, 0x1000, 2, 0, 0, None) == INV
+    assert lib.hv_batch_copy(0, 0, 0, 0, 0, 0, None) == N.HV_OK
+    assert lib.hv_swap_blocks_batch(None, None, None, 3, 0, 0, None) == INV
+    assert lib.hv_ce_batch_copy(None, None, None, 3, 1, None) == INV
+    # content kernels
+    assert lib.hv_fill_content(0, 0x1000, 0x1000, 1, None) == INV
+    assert lib.hv_digest(0x1000, 0x1000, 1, 0, None) == INV
+    assert lib.hv_verify_content(0x1000, 0x1000, 0x1000, 1, 0, None) == INV
+    # the Python layer raises the matching exception type
+    with pytest.raises(N.HarvestNativeError) as ei:
+        N.call("hv_batch_copy", 0, 0x1000, 0x1000, 2, 0, 0, None)
+    assert ei.value.status == INV
+
+
+def test_fetch_wrappers_reject_bad_tensors_without_a_gpu():
+    import torch
+    from paper_2602_00328_b200 import fetch as F
+    cpu = torch.zeros(4, dtype=torch.int64)
+    with pytest.raises(ValueError, match="CUDA"):
+        F.kv_gather(cpu, 65536, dst_page_ptrs=cpu)
+    with pytest.raises(ValueError, match="need dst"):
+        F.kv_gather(cpu, 65536)
+    with pytest.raises(ValueError, match="equal length"):
+        F.kv_gather_blocks(cpu, cpu[:3], cpu, cpu, 32, 65536)
+    with pytest.raises(ValueError, match="equal length"):
+        F.batch_copy(cpu, cpu[:2], cpu)
+    with pytest.raises(ValueError, match="length mismatch"):
+        F.swap_blocks_batch([1, 2], [3], [4, 5])
