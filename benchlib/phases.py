@@ -149,36 +149,65 @@ def churn_phase(world, rank, dev, a, dist, barrier, layers=8, seconds=2.0):
             except Exception as e:
                 out = {"rank": rank, "error": repr(e)[:200]}
         dist.all_gather_object(handles, mine)
-    try:
-        if rank in C:
-            out = _churn_compute(world, rank, dev, a, m, C, D, per_reader, handles, imported, seconds)
-    except Exception as e:  # every rank still reaches the collectives below
-        out = {"rank": rank, "error": repr(e)[:300]}
+    from paper_2602_00328_b200.runtime import Policy, PolicyKind
+    # the reference's placement policies under the same churn (runtime.py:169-196):
+    # BestFit is the headline; Stability skips donors with many recent
+    # revocations; Fairness token-buckets the re-placement copy-in bytes
+    policies = {"BestFit": Policy(),
+                "Stability": Policy(kind=PolicyKind.STABILITY, stability_window_s=0.2,
+                                    stability_max_revocations=L * E // 4),
+                "Fairness": Policy(kind=PolicyKind.FAIRNESS, fairness_budget_bytes_per_s=4e9,
+                                   fairness_burst_bytes=1e9)}
+    outs = {}
+    for name, pol in policies.items():
+        try:
+            if rank in C:
+                outs[name] = _churn_compute(world, rank, dev, a, m, C, D, per_reader, handles, imported, seconds,
+                                            policy=pol)
+        except Exception as e:  # every rank still reaches the collectives below
+            outs[name] = {"rank": rank, "error": repr(e)[:300]}
+        imported.clear()
+    if out is not None:  # donor-side setup failure
+        outs = {name: out for name in policies}
     results = [None] * world
     if world > 1:
         barrier()
-        dist.all_gather_object(results, out)
+        dist.all_gather_object(results, outs)
         if pool is not None:
             pool.close()
     else:
-        results = [out]
-    comp = [r for r in results if r and "error" not in r]
-    errs = [r for r in results if r and "error" in r]
+        results = [outs]
+
+    def summary(name):
+        rs = [r.get(name) for r in results if r]
+        comp = [r for r in rs if r and "error" not in r]
+        errs = [r for r in rs if r and "error" in r]
+        res = {"tokens_per_s_all_compute_ranks": sum(r["tokens_per_s"] for r in comp),
+               "all_outputs_bit_identical": bool(comp) and all(r["outputs_bit_identical_to_all_local"] for r in comp),
+               "total_revocations": sum(r["revocations"] for r in comp),
+               "total_re_placements": sum(r["re_placements"] for r in comp),
+               "total_release_ordering_violations": sum(r["release_ordering_violations"] for r in comp)}
+        return res, comp, errs
+
+    head, comp, errs = summary("BestFit")
     res = {"model": f"{m.name} slice: {L} layers x {E} experts x {S} B (Qwen-shaped, bf16)",
            "compute_ranks": C, "donor_ranks": D if D else "self (VMM pool on the compute GPU)",
            "timeline": "markov_availability levels 0/25/50/100% of the donated bytes, 50 ms mean sojourn, "
                        f"seed 5+donor, {seconds} s",
-           "tokens_per_s_all_compute_ranks": sum(r["tokens_per_s"] for r in comp),
-           "all_outputs_bit_identical": bool(comp) and all(r["outputs_bit_identical_to_all_local"] for r in comp),
-           "total_revocations": sum(r["revocations"] for r in comp),
-           "total_re_placements": sum(r["re_placements"] for r in comp),
-           "total_release_ordering_violations": sum(r["release_ordering_violations"] for r in comp),
-           "per_rank": comp}
+           "policy": "BestFit", **head, "per_rank": comp,
+           "policy_comparison": {}}
     if errs:
         res["errors"] = errs
+    for name in policies:
+        if name == "BestFit":
+            continue
+        h2, _c2, e2 = summary(name)
+        res["policy_comparison"][name] = {**h2, "policy": repr(policies[name])}
+        if e2:
+            res["policy_comparison"][name]["errors"] = e2
     return res
 
-def _churn_compute(world, rank, dev, a, m, C, D, per_reader, handles, imported, seconds):
+def _churn_compute(world, rank, dev, a, m, C, D, per_reader, handles, imported, seconds, policy=None):
     """Compute-rank side of churn_phase (no collectives inside)."""
     import torch
     from paper_2602_00328_b200.churn import ChurnDriver, expert_tier_counts, markov_availability
@@ -193,7 +222,7 @@ def _churn_compute(world, rank, dev, a, m, C, D, per_reader, handles, imported, 
         host = HostTier(L * E * S)
         if world == 1:
             sysm = HarvestSystem(dev, donors=[dev], donor_bytes=per_reader, host_tier=host, local_bytes=1,
-                                 engine=a.engine, max_ctas=a.max_ctas)
+                                 engine=a.engine, max_ctas=a.max_ctas, policy=policy)
         else:
             views = {}
             for i, d in enumerate(D, start=1):
@@ -201,7 +230,7 @@ def _churn_compute(world, rank, dev, a, m, C, D, per_reader, handles, imported, 
                 imported.append(p)
                 views[i] = p.view(C.index(rank) * per_reader, per_reader)
             sysm = HarvestSystem(dev, pools=views, host_tier=host, local_bytes=1, engine=a.engine,
-                                 max_ctas=a.max_ctas)
+                                 max_ctas=a.max_ctas, policy=policy)
         rt = sysm.runtime
         store = ExpertStore(m, sysm.host_id, host)
         store.fill_host(dev, weights=True)
