@@ -43,6 +43,26 @@ def run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, micro
         dec.trace = True
         dec.step(h)
         out["overlap"] = dec.overlap_report()
+    else:  # the same step as one CUDA graph replay (no per-launch host cost)
+        try:
+            h_eager = dec.step(h).clone()
+            dec.capture_graph()
+            same = bool(torch.equal(dec.step(h).view(torch.int16), h_eager.view(torch.int16)))
+            torch.cuda.synchronize()
+            barrier()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(cur)
+            hg = h_eager
+            for _ in range(steps):
+                hg = dec.step(hg)
+            g1.record(cur)
+            g1.synchronize()
+            dtg = max_over_ranks(g0.elapsed_time(g1) * 1e-3)
+            out["cuda_graph"] = {"tokens_per_s": TOKENS * steps * world / dtg,
+                                 "ms_per_decode_step": dtg / steps * 1e3,
+                                 "replay_equals_eager_bitwise": same}
+        except Exception as e:  # report, never lose the line
+            out["cuda_graph"] = {"error": repr(e)[:300]}
     del dec
     return out
 

@@ -38,13 +38,20 @@ void note_launch(uint64_t n) { g_launches += n; }
 
 int bind_stream_device(void* stream, int* device_out, DeviceGuard& g) {
   int dev = 0;
-  if (stream) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (stream && cudaStreamIsCapturing((cudaStream_t)stream, &cap) != cudaSuccess) {
+    (void)cudaGetLastError();
+    cap = cudaStreamCaptureStatusNone;
+  }
+  if (stream && cap == cudaStreamCaptureStatusNone) {
     cudaError_t e = cudaStreamGetDevice((cudaStream_t)stream, &dev);
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
       return hv_cuda_status(e);
     }
   } else {
+    // legacy stream, or a stream under CUDA-graph capture: cudaStreamGetDevice
+    // invalidates a capture, and a capturing stream belongs to the current device
     HV_CUDA(cudaGetDevice(&dev));
   }
   int st = g.set(dev);

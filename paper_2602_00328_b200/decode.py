@@ -87,16 +87,20 @@ class MoEDecoder:
         self._n_stages = n
 
     # ---------------------------------------------------------------- tables
-    def sync_tables(self) -> None:
-        """Upload the residency address table and fetch mask (call after
-        placement or revocation changed ExpertFetcher's tables)."""
+    def _table_host(self) -> tuple[torch.Tensor, torch.Tensor]:
         # LOCAL experts are staged from their resident copy in HBM (a device-
         # local copy); PEER/HOST experts are the fetches the reference counts
         src = np.where(self.f.tier == 0, self.f.local_addr, self.f.src_addr).astype(np.uint64)
         if np.any(src == 0):
             raise ValueError("an expert has no source address (LOCAL tier needs ExpertFetcher(local_addr=...))")
-        new_addr = torch.from_numpy(src.view(np.int64).copy())
-        new_fetchable = torch.from_numpy((self.f.tier != 0).copy())
+        return torch.from_numpy(src.view(np.int64).copy()), torch.from_numpy((self.f.tier != 0).copy())
+
+    def sync_tables(self) -> None:
+        """Upload the residency address table and fetch mask (call after
+        placement or revocation changed ExpertFetcher's tables)."""
+        if getattr(self, "_graph", None) is not None:
+            return self._sync_tables_in_place()
+        new_addr, new_fetchable = self._table_host()
         if getattr(self, "addr", None) is None:
             # two device copies of the table: in-flight fetch kernels read the
             # current one through raw pointers while the next one is written
@@ -113,6 +117,20 @@ class MoEDecoder:
             self.fetchable.copy_(new_fetchable)
             self._addr_cur = nxt
             self.addr = self._addr_bufs[nxt]
+        self.layer_handles = [[h for (l, _e), h in self.f.handles.items() if l == layer] for layer in range(self.L)]
+        self._table_version = getattr(self.f, "version", 0)
+
+    def _sync_tables_in_place(self) -> None:
+        """Graph mode: the captured kernels read one fixed table, so the new
+        table is copied into it on the replay stream, ordered after every
+        earlier replay and before the next (no host synchronisation)."""
+        new_addr, new_fetchable = self._table_host()
+        cur = torch.cuda.current_stream(self.dev)
+        pinned = new_addr.pin_memory()
+        with torch.cuda.stream(cur):
+            self.addr.copy_(pinned, non_blocking=True)
+            self.fetchable.copy_(new_fetchable.pin_memory(), non_blocking=True)
+        self._staged_tables = (pinned, cur.record_event())   # keep the source alive until copied
         self.layer_handles = [[h for (l, _e), h in self.f.handles.items() if l == layer] for layer in range(self.L)]
         self._table_version = getattr(self.f, "version", 0)
 
@@ -168,7 +186,7 @@ class MoEDecoder:
             fe.record(self.fetch)
             self._tr.setdefault(s, {})["fetch"] = (fs, fe)
         handles = self.layer_handles[layer]
-        if handles:
+        if handles and not self._capturing:   # graph mode: tracked per replay instead
             batch = self.rt.begin_reads(handles)
             self.f.engine.track([lambda _x, b=batch: self.rt.end_reads(b)])
         ev = torch.cuda.Event()
@@ -176,14 +194,67 @@ class MoEDecoder:
         return ev
 
     # ---------------------------------------------------------------- step
+    _capturing = False
+    _graph = None
+
     @annotate("harvest.decode_step")
     def step(self, x: torch.Tensor) -> torch.Tensor:
         """One decode step over all layers; returns the new hidden states.
         Residency changes (revocation callbacks, re-placement arrivals) seen
         since the last step are uploaded first; within a step the table is a
-        snapshot, and reads of a handle revoked meanwhile extend its drain."""
+        snapshot, and reads of a handle revoked meanwhile extend its drain.
+        After capture_graph() the step is one CUDA graph replay."""
         if getattr(self.f, "version", 0) != self._table_version:
             self.sync_tables()
+        if self._graph is not None:
+            return self._replay(x)
+        return self._step_eager(x)
+
+    def capture_graph(self) -> None:
+        """Capture one decode step (every stage's router, top-k, fetch plan,
+        K2 fetch and expert FFN, on both streams) as a CUDA graph; later
+        step() calls replay it.  Inputs are copied into a static buffer; the
+        output tensor returned by step() is reused by the next replay."""
+        if self.trace:
+            raise ValueError("trace mode records per-launch events; capture without trace")
+        if self._graph is not None:
+            return
+        self._graph_in = self.x0.clone()
+        cur = torch.cuda.current_stream(self.dev)
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(cur)
+        self._capturing = True
+        try:
+            with torch.cuda.stream(side):            # warm-up outside capture (allocator, cuBLAS handles)
+                for _ in range(2):
+                    self._step_eager(self._graph_in)
+            cur.wait_stream(side)
+            torch.cuda.synchronize(self.dev)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._graph_out = self._step_eager(self._graph_in)
+        finally:
+            self._capturing = False
+        torch.cuda.synchronize(self.dev)
+        self._graph = g
+
+    def _replay(self, x: torch.Tensor) -> torch.Tensor:
+        cur = torch.cuda.current_stream(self.dev)
+        if x.data_ptr() != self._graph_in.data_ptr():
+            self._graph_in.copy_(x)
+        # drain bookkeeping for every peer handle the step may read
+        handles = [h for hs in self.layer_handles for h in hs]
+        batch = self.rt.begin_reads(handles) if handles else None
+        self._graph.replay()
+        done = torch.cuda.Event()
+        done.record(cur)
+        self._addr_done[self._addr_cur] = done
+        if batch is not None:
+            self.fetch.wait_stream(cur)              # the tracking event fires after the replay
+            self.f.engine.track([lambda _x, b=batch: self.rt.end_reads(b)])
+        return self._graph_out
+
+    def _step_eager(self, x: torch.Tensor) -> torch.Tensor:
         hs = list(x.view(self.nmb, self.tmb, self.H).clone().unbind(0))
         cur = torch.cuda.current_stream(self.dev)
         self.compute.wait_stream(cur)

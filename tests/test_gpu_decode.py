@@ -143,3 +143,32 @@ def test_decode_survives_revocation_midway():
     assert torch.equal(h.view(torch.int16), h2.view(torch.int16))
     sysm.close()
     sys2.close()
+
+
+@pytest.mark.parametrize("microbatches", [1, 2])
+def test_graph_replay_equals_eager_and_all_local(microbatches):
+    """capture_graph(): every later step is one CUDA graph replay (router,
+    device-side fetch plan, K2 fetch on the fetch stream, expert FFN).  A
+    revocation between replays updates the captured address table in place;
+    outputs stay bit-identical to the all-local eager run."""
+    from paper_2602_00328_b200.runtime import RevokeReason
+    model = _tiny()
+    sysm, store, res, fetcher, dec = _setup(model, peer_experts=12, microbatches=microbatches)
+    dec.capture_graph()
+    h = dec.step(dec.x0)
+    h = dec.step(h)
+    for hdl in list(fetcher.handles.values()):
+        sysm.runtime.revoke(hdl, RevokeReason.PRESSURE)
+    sysm.loop.run()                     # drain (waits on the replay's event) -> residency -> host
+    assert not fetcher.handles
+    h = dec.step(h)                     # version changed: in-place table update, then replay
+    out = h.clone()
+    torch.cuda.synchronize()
+    sys2, dec2, _keep = _all_local(model, 16, microbatches, 0, store)
+    out2 = dec2.decode(3)
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int16), out2.view(torch.int16))
+    from paper_2602_00328_b200.verify import verify_release_ordering
+    assert verify_release_ordering(sysm.loop.log) == []
+    sysm.close()
+    sys2.close()

@@ -1,0 +1,3 @@
+set -x
+timeout 600 python -m pytest tests/test_gpu_decode.py -q -m gpu -x > gpurun_out/r43_tests.log 2>&1; tail -15 gpurun_out/r43_tests.log
+HV_BENCH_QWEN_LAYERS=8 HV_DEVICE_MAP=0,0 timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29525 bench.py --gpus 2 --steps 3 --warmup 3 --dist-backend gloo --no-cpu-baseline --no-kv --no-phi --no-churn --no-host-compare > gpurun_out/r43_bench2.json 2> gpurun_out/r43_bench2.err; echo rc=$?
