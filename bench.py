@@ -173,6 +173,18 @@ def run_b200(a):
     # ---- engine / grid autotune on the link actually under test (a few launches
     # of one layer's real descriptors); "--engine X" pins the choice instead
     tune = None
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     if a.engine == "auto":
         engines = ("ldg", "ldg256", "ldg16", "tma")
         safe = None
@@ -184,7 +196,13 @@ def run_b200(a):
             dist.broadcast_object_list(box, src=0)
             safe = box[0]
             engines = tuple(e for e in engines if safe.get(e))
-        tune = autotune(desc[0][0], stream, stream_h, F, engines=engines)
+            # N-1 donors: also the interleaved chunk order (HV_ENGINE_FLAG_INTERLEAVE),
+            # which keeps every donor's egress busy instead of all readers
+            # walking the same donors in the same order
+            engines = engines + tuple(e + "+il" for e in engines)
+        tune = autotune(desc[0][0], stream, stream_h, F, engines=engines,
+                        barrier=barrier if world > 1 else None,
+                        max_over_ranks=max_over_ranks if world > 1 else None)
         tune["peer_engine_probe"] = safe
         a.engine, a.max_ctas = tune["best"]["engine"], tune["best"]["max_ctas"]
         if world > 1:  # every rank must run the same configuration: rank 0 decides
@@ -201,17 +219,6 @@ def run_b200(a):
             F.batch_copy(sp, dp, sz, engine=a.engine, max_ctas=a.max_ctas, stream=stream_h)
             if evs is not None:
                 evs[layer][1].record(stream)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}" if backend == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
 
     for s in range(a.warmup):
         value_step(s)

@@ -70,8 +70,12 @@ def probe_engines_on_peer(handle: bytes, donor: int, nbytes: int, dev: int) -> d
             ok[engine] = False
     return ok
 
-def autotune(layer_desc, stream, stream_h, F, reps=3, engines=("ldg", "ldg256", "ldg16", "tma")):
-    """Time one layer's real fetch under each engine x grid cap; pick the fastest."""
+def autotune(layer_desc, stream, stream_h, F, reps=3, engines=("ldg", "ldg256", "ldg16", "tma"),
+             barrier=None, max_over_ranks=None):
+    """Time one layer's real fetch under each engine x grid cap; pick the fastest.
+    Multi-rank: every rank times the same candidate at the same moment
+    (barrier before each), so the measurement includes the contention of all
+    readers on the donors' links; a candidate's time is the max over ranks."""
     import torch
     sp, dp, sz, nb = layer_desc
     rows = []
@@ -79,6 +83,9 @@ def autotune(layer_desc, stream, stream_h, F, reps=3, engines=("ldg", "ldg256", 
         for max_ctas in (0, 296, 148):
             for _ in range(1):  # warm
                 F.batch_copy(sp, dp, sz, engine=engine, max_ctas=max_ctas, stream=stream_h)
+            stream.synchronize()
+            if barrier is not None:
+                barrier()
             ts = []
             for _ in range(reps):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -87,7 +94,10 @@ def autotune(layer_desc, stream, stream_h, F, reps=3, engines=("ldg", "ldg256", 
                 e1.record(stream)
                 e1.synchronize()
                 ts.append(e0.elapsed_time(e1) * 1e-3)
-            rows.append({"engine": engine, "max_ctas": max_ctas, "GBps": nb / statistics.median(ts) / 1e9})
+            t = statistics.median(ts)
+            if max_over_ranks is not None:
+                t = max_over_ranks(t)
+            rows.append({"engine": engine, "max_ctas": max_ctas, "GBps": nb / t / 1e9})
     best = max(rows, key=lambda r: r["GBps"])
     return {"best": best, "candidates": rows}
 

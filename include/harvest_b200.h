@@ -155,11 +155,16 @@ int hv_stream_wait_event(void* stream, void* event);
 
 /* ---- fetch engines (the hot path) ------------------------------------- */
 /* engine selector for hv_batch_copy / hv_kv_gather */
-#define HV_ENGINE_AUTO 0
+#define HV_ENGINE_AUTO 0   /* LDG; variable-size copies also take HV_ENGINE_FLAG_INTERLEAVE */
 #define HV_ENGINE_LDG 1  /* SM-issued 128-bit ld.global.nc / st.global, warp per 4 KiB chunk */
 #define HV_ENGINE_TMA 2  /* cp.async.bulk global->smem->global ring, one issuing lane per CTA */
 #define HV_ENGINE_LDG256 3 /* LDG with the L2::256B sector-promotion hint (larger remote reads) */
 #define HV_ENGINE_LDG16 4  /* LDG with 16 x 128-bit loads in flight per lane (8 KiB per warp) */
+/* OR-able flag for the variable-size copies (hv_batch_copy, hv_swap_blocks_batch):
+ * when every non-empty object of a launch has the same size, chunk c reads
+ * object (c mod n_active) at chunk (c div n_active), so the bytes in flight
+ * span every object -- and every donor GPU holding one -- at once. */
+#define HV_ENGINE_FLAG_INTERLEAVE 0x100
 
 /* K1: block-table-indexed KV-page gather.  Page i is copied from
  * d_src_page_ptrs[i] to d_dst_page_ptrs[i] (or, when d_dst_page_ptrs is NULL,

@@ -23,8 +23,10 @@ ENGINE_LDG = 1
 ENGINE_TMA = 2
 ENGINE_LDG256 = 3
 ENGINE_LDG16 = 4
+ENGINE_FLAG_INTERLEAVE = 0x100   # HV_ENGINE_FLAG_INTERLEAVE: round-robin chunks over equal-size objects
 ENGINES = {"auto": ENGINE_AUTO, "ldg": ENGINE_LDG, "tma": ENGINE_TMA, "ldg256": ENGINE_LDG256,
            "ldg16": ENGINE_LDG16}
+ENGINES.update({f"{k}+il": v | ENGINE_FLAG_INTERLEAVE for k, v in list(ENGINES.items())})
 
 POOL_VMM = 0
 POOL_IPC = 1

@@ -87,6 +87,12 @@ constexpr int kTmaThreads = 32;                  // one warp; lane 0 issues
 constexpr uint32_t kTmaChunk = 16384;            // bytes per bulk copy
 constexpr int kTmaStages = 8;                    // 128 KiB of smem ring per CTA
 constexpr uint32_t kMaxSmemDescs = 2048;         // variable-size descriptors per launch
+// DescResolver shared memory: chunk-start prefix [n+1], the interleave order
+// of the active descriptors [kMaxSmemDescs], and 4 words of mode data
+constexpr uint32_t kDescActOff = kMaxSmemDescs + 1;
+constexpr uint32_t kDescMetaOff = 2 * kMaxSmemDescs + 1;
+constexpr uint32_t kDescSmemWords = 2 * kMaxSmemDescs + 8;
+constexpr int kEngineInterleave = HV_ENGINE_FLAG_INTERLEAVE;  // round-robin chunks over objects
 constexpr uint32_t kPageBatchMax = 1u << 30;
 
 // splitmix64 (Steele, Lea, Flood 2014) — the synthetic content generator; the
@@ -220,30 +226,56 @@ struct BlockResolver {
 // in shared memory; a warp's successive chunks are monotone in c, so the
 // object index is found by a short forward probe before falling back to
 // binary search.
+//
+// Interleaved mode (engine flag kEngineInterleave, used when every non-empty
+// object has the same size, e.g. the experts of a stage): chunk c reads
+// object active[c % n_active] at chunk c / n_active, so the bytes in flight at
+// any moment come from every object of the batch at once -- with objects
+// spread over several donor GPUs, every donor's NVLink egress is busy instead
+// of the readers of a multi-GPU node converging on one or two donors.
 struct DescResolver {
   const uint64_t* src;
   const uint64_t* dst;
   const uint64_t* bytes;
   uint32_t n;
   uint32_t chunk;
+  uint32_t interleave;
 
-  // s_start must hold n+1 entries; all threads of the CTA call setup().
+  // smem must hold kDescSmemWords words; all threads of the CTA call setup().
   __device__ uint32_t setup(void* smem) const {
     uint32_t* s_start = reinterpret_cast<uint32_t*>(smem);
     __shared__ uint32_t s_warp[32];
     __shared__ uint32_t s_total;
+    __shared__ unsigned long long s_szmin, s_szmax;
     const uint32_t nt = blockDim.x, tid = threadIdx.x;
     const uint32_t lane = tid & 31, warp = tid >> 5, nwarps = (nt + 31) >> 5;
     const uint32_t per = (n + nt - 1) / nt;
     const uint32_t i0 = tid * per;
+    if (interleave) {
+      if (tid == 0) {
+        s_szmin = ~0ull;
+        s_szmax = 0;
+      }
+      __syncthreads();
+    }
     uint32_t local = 0;
+    unsigned long long szmin = ~0ull, szmax = 0;
     for (uint32_t k = 0; k < per; ++k) {
       const uint32_t i = i0 + k;
       if (i < n) {
-        const uint32_t cnt = (uint32_t)((__ldg(bytes + i) + chunk - 1) / chunk);
+        const uint64_t sz = __ldg(bytes + i);
+        const uint32_t cnt = (uint32_t)((sz + chunk - 1) / chunk);
         s_start[i] = cnt;
         local += cnt;
+        if (sz) {
+          szmin = sz < szmin ? sz : szmin;
+          szmax = sz > szmax ? sz : szmax;
+        }
       }
+    }
+    if (interleave && szmax) {
+      atomicMin(&s_szmin, szmin);
+      atomicMax(&s_szmax, szmax);
     }
     uint32_t incl = local;
 #pragma unroll
@@ -275,11 +307,45 @@ struct DescResolver {
       }
     }
     if (tid == 0) s_start[n] = s_total;
+    // interleaved order: only for equal-size non-empty objects
+    const bool il = interleave && s_szmax != 0 && s_szmin == s_szmax;
+    uint32_t* meta = s_start + kDescMetaOff;
+    if (il) {
+      const uint32_t cpd = (uint32_t)((s_szmax + chunk - 1) / chunk);
+      uint32_t* act = s_start + kDescActOff;
+      for (uint32_t k = 0; k < per; ++k) {
+        const uint32_t i = i0 + k;
+        if (i < n && __ldg(bytes + i)) act[s_start[i] / cpd] = i;
+      }
+      if (tid == 0) {
+        meta[0] = 1;
+        meta[1] = s_total / cpd;                  // active objects
+        meta[2] = (uint32_t)s_szmax;              // their size (low, high words)
+        meta[3] = (uint32_t)(s_szmax >> 32);
+      }
+    } else if (tid == 0) {
+      meta[0] = 0;
+    }
     __syncthreads();
     return s_total;
   }
 
   __device__ __forceinline__ ChunkRef at(uint32_t c, uint32_t& hint, const uint32_t* s_start) const {
+    const uint32_t* meta = s_start + kDescMetaOff;
+    if (meta[0]) {
+      const uint32_t nact = meta[1];
+      const uint32_t k = c / nact;
+      const uint32_t i = s_start[kDescActOff + (c - k * nact)];
+      const uint64_t size = (uint64_t)meta[2] | ((uint64_t)meta[3] << 32);
+      ChunkRef r;
+      r.obj = i;
+      r.off = (uint64_t)k * chunk;
+      const uint64_t rem = size - r.off;
+      r.len = rem < chunk ? (uint32_t)rem : chunk;
+      r.src = reinterpret_cast<const char*>(__ldg(src + i)) + r.off;
+      r.dst = reinterpret_cast<char*>(__ldg(dst + i)) + r.off;
+      return r;
+    }
     uint32_t lo = hint;
     if (!(s_start[lo] <= c && c < s_start[lo + 1])) {
       if (lo + 2 <= n && s_start[lo + 1] <= c && c < s_start[lo + 2]) {
@@ -449,7 +515,7 @@ __global__ void __launch_bounds__(kLdgThreads) page_copy_ldg(PageResolver<kTable
 
 template <typename Op>
 __global__ void __launch_bounds__(kLdgThreads) desc_op_kernel(DescResolver res, Op op) {
-  __shared__ uint32_t s_start[kMaxSmemDescs + 1];
+  __shared__ uint32_t s_start[kDescSmemWords];
   const uint32_t total = res.setup(s_start);
   warp_loop(res, total, op, s_start);
 }
@@ -593,7 +659,7 @@ __global__ void __launch_bounds__(kLdgThreads) block_copy_ldg(BlockResolver res)
 __global__ void __launch_bounds__(kTmaThreads) desc_copy_tma(DescResolver res) {
   extern __shared__ __align__(128) char dyn_smem[];
   __shared__ __align__(8) uint64_t bars[kTmaStages];
-  __shared__ uint32_t s_start[kMaxSmemDescs + 1];
+  __shared__ uint32_t s_start[kDescSmemWords];
   const uint32_t total = res.setup(s_start);
   tma_loop(res, total, s_start, dyn_smem, bars);
 }
@@ -649,7 +715,7 @@ int launch_pages(PageResolver<kTable> res, int engine, int max_ctas, void* strea
   hv::DeviceGuard dg;
   int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
-  engine = pick_engine(engine);
+  engine = pick_engine(engine & ~kEngineInterleave);  // uniform pages: order flag not used
   if (engine == HV_ENGINE_TMA) {
     if ((st = set_tma_attrs())) return st;
     res.chunk = kTmaChunk;
@@ -688,7 +754,7 @@ int launch_blocks(BlockResolver res, int engine, int max_ctas, void* stream) {
   hv::DeviceGuard dg;
   int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
-  engine = pick_engine(engine);
+  engine = pick_engine(engine & ~kEngineInterleave);  // uniform pages: order flag not used
   uint32_t chunk = kLdgChunk;
   if (engine == HV_ENGINE_TMA) chunk = kTmaChunk;
   else if (engine == HV_ENGINE_LDG16) chunk = kLdgDeepChunk;
@@ -723,7 +789,10 @@ int launch_descs(const uint64_t* d_src, const uint64_t* d_dst, const uint64_t* d
   hv::DeviceGuard dg;
   int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
-  engine = pick_engine(engine);
+  // AUTO copies take the interleaved order: neutral on a PCIe or local-HBM
+  // source (within 2%), and it spreads the reads of a multi-donor batch
+  const uint32_t interleave = ((engine & kEngineInterleave) || engine == HV_ENGINE_AUTO) && is_copy ? 1u : 0u;
+  engine = pick_engine(engine & ~kEngineInterleave);
   if (engine == HV_ENGINE_TMA && is_copy && (st = set_tma_attrs())) return st;
   for (uint32_t base = 0; base < n; base += kMaxSmemDescs) {
     const uint32_t m = (n - base) < kMaxSmemDescs ? (n - base) : kMaxSmemDescs;
@@ -732,6 +801,7 @@ int launch_descs(const uint64_t* d_src, const uint64_t* d_dst, const uint64_t* d
     res.dst = d_dst ? d_dst + base : nullptr;
     res.bytes = d_bytes + base;
     res.n = m;
+    res.interleave = interleave;
     Op o = op;
     o.rebase(base);
     if (is_copy && engine == HV_ENGINE_TMA) {
@@ -934,7 +1004,7 @@ HV_EXPORT int hv_swap_blocks_batch(const uint64_t* h_src, const uint64_t* h_dst,
       r.n_pages = m;
       st = launch_pages(r, engine, max_ctas, stream);
     } else if (!uniform) {
-      const int eng = pick_engine(engine);
+      const int eng = pick_engine(engine & ~kEngineInterleave);
       const uint64_t chunk = eng == HV_ENGINE_TMA ? kTmaChunk : kLdgChunk;
       const uint64_t chunks = total_bytes / chunk + m;  // upper bound on the chunk count
       st = launch_descs(ds, ds + m, ds + 2 * m, m, engine, max_ctas, stream, CopyOpR{}, true, chunks);
