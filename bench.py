@@ -136,7 +136,10 @@ def run_b200(a):
         # no donor's NVLink egress serves a whole layer alone
         for layer in range(L):
             for e in range(E):
-                pref = [1 + (layer * E + e) % (world - 1)]
+                # offset by rank: at the same expert index different ranks
+                # prefer different GPUs (others_r[(k + r) mod (N-1)] is a
+                # permutation over r), so lockstep readers do not collide
+                pref = [1 + (layer * E + e + rank) % (world - 1)]
                 h = rt.harvest_alloc(S, AllocationHints(preferred_devices=pref, durability=Durability.BACKED,
                                                         client_id="moe"))
                 assert h is not None, "donor capacity exhausted"

@@ -363,7 +363,7 @@ def phi_phase(world, rank, dev, a, dist, barrier, max_over_ranks, batches=(1, 16
         ptrs, seeds = [], []
         for layer in range(L):
             for e in range(E):
-                h = rt.harvest_alloc(S, AllocationHints(preferred_devices=[1 + (layer * E + e) % (world - 1)],
+                h = rt.harvest_alloc(S, AllocationHints(preferred_devices=[1 + (layer * E + e + rank) % (world - 1)],
                                                         durability=Durability.BACKED, client_id="moe"))
                 if h is None:
                     raise RuntimeError("donor capacity exhausted")
