@@ -73,10 +73,9 @@ def run_b200(a):
     import torch.distributed as dist
     from paper_2602_00328_b200 import _native as N
     from paper_2602_00328_b200 import fetch as F
-    from paper_2602_00328_b200.memalloc import Tier
+    from paper_2602_00328_b200.cluster import DonorLayout, RankGroup, per_reader_bytes, place_experts
     from paper_2602_00328_b200.moe import ExpertFetcher, ExpertResidency, ExpertStore, expert_content
     from paper_2602_00328_b200.pool import HostTier, PeerPool
-    from paper_2602_00328_b200.runtime import AllocationHints, Durability
     from paper_2602_00328_b200.system import HarvestSystem
     from tools.clocks import ClockSampler
 
@@ -94,6 +93,7 @@ def run_b200(a):
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
         else:
             dist.init_process_group(backend)
+    group = RankGroup(world, rank, device=f"cuda:{dev}" if backend == "nccl" else None)
     m = model()
     L, E, S = m.num_layers, m.num_experts, m.expert_size
     routes = routing(m, a.warmup + a.steps, seed=SEED + 1000 * rank)
@@ -109,50 +109,33 @@ def run_b200(a):
         residency = ExpertResidency(m)       # every expert HOST_DRAM
     else:
         source = "peer"
-        others = [r for r in range(world) if r != rank]
-        per_reader = math.ceil(L * E / (world - 1)) * S
+        per_reader = per_reader_bytes(L * E, S, world - 1)
         if not a.no_kv:  # room for config 4's 128k-token KV sequence (128 slabs of 128 MiB)
             per_reader += math.ceil((KV_TOKENS // 16) / KV_SLAB_BLOCKS / (world - 1)) * kv_slab_bytes()
-        my_pool = PeerPool(dev, per_reader * (world - 1), readers=[dev], mode="ipc")
-        handles = [None] * world
-        dist.all_gather_object(handles, my_pool.export_ipc())
+        layout = DonorLayout.symmetric(world, per_reader)
+        others = layout.donors_of(rank)
+        my_pool = PeerPool(dev, layout.slab_bytes(rank), readers=[dev], mode="ipc")
+        handles = group.all_gather(my_pool.export_ipc())
         views = {}
-        for i, d in enumerate(others, start=1):
-            p = PeerPool.import_ipc(handles[d], d, per_reader * (world - 1), dev)
+        for d in others:
+            p = PeerPool.import_ipc(handles[d], d, layout.slab_bytes(d), dev)
             imported.append(p)
-            # my section of donor d: my position among d's readers
-            pos = [r for r in range(world) if r != d].index(rank)
-            views[i] = p.view(pos * per_reader, per_reader)
+            views[layout.peer_index(rank, d)] = p.view(*layout.section(d, rank))
         sysm = HarvestSystem(dev, pools=views, local_bytes=1, engine=a.engine, max_ctas=a.max_ctas,
                              log_transfers=False)
         store = ExpertStore(m, sysm.host_id, None)
         residency = ExpertResidency(m)
         rt = sysm.runtime
-        # placement: the runtime's own harvest_alloc decisions (runtime.py:198-235);
+        # placement: the runtime's own harvest_alloc decisions (runtime.py:198-235)
+        # with a rank-offset round-robin donor preference (cluster.preferred_peer);
         # the copy-in is the synthetic-content fill written over NVLink
-        ptrs, seeds = [], []
-        # round-robin preference (the reference's preferred_devices hint,
-        # runtime.py:205-214) so every layer's experts span all N-1 donors and
-        # no donor's NVLink egress serves a whole layer alone
-        for layer in range(L):
-            for e in range(E):
-                # offset by rank: at the same expert index different ranks
-                # prefer different GPUs (others_r[(k + r) mod (N-1)] is a
-                # permutation over r), so lockstep readers do not collide
-                pref = [1 + (layer * E + e + rank) % (world - 1)]
-                h = rt.harvest_alloc(S, AllocationHints(preferred_devices=pref, durability=Durability.BACKED,
-                                                        client_id="moe"))
-                assert h is not None, "donor capacity exhausted"
-                rt.set_tag(h, ("expert", layer, e))
-                rt.write_peer(h, ("expert", layer, e), expert_content(m, layer, e))
-                residency.set_tier(layer, e, Tier.PEER_HBM, h)
-                ptrs.append(rt.address(h))
-                seeds.append(expert_content(m, layer, e))
+        placed, seeds = place_experts(rt, m, residency, rank, world - 1)
+        ptrs = [rt.address(h) for h in placed]
         for i in range(0, len(ptrs), 120):
             F.fill_weights_bf16(F.ptrs_tensor(ptrs[i:i + 120], f"cuda:{dev}"),
                            F.ptrs_tensor([S] * len(ptrs[i:i + 120]), f"cuda:{dev}"), seeds[i:i + 120])
         torch.cuda.synchronize()
-        dist.barrier()
+        group.barrier()
 
     fetcher = ExpertFetcher(sysm.runtime, m, residency, store)
     stream_h = sysm.engine.stream
@@ -177,16 +160,8 @@ def run_b200(a):
     # of one layer's real descriptors); "--engine X" pins the choice instead
     tune = None
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}" if backend == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    barrier = group.barrier
+    max_over_ranks = group.max
 
     if a.engine == "auto":
         engines = ("ldg", "ldg256", "ldg16", "tma")
@@ -194,10 +169,8 @@ def run_b200(a):
         if world > 1:  # engines other than LDG are proven on a peer pointer first, out of process
             if rank == 0:
                 d = others[0]
-                safe = probe_engines_on_peer(handles[d], d, per_reader * (world - 1), dev)
-            box = [safe]
-            dist.broadcast_object_list(box, src=0)
-            safe = box[0]
+                safe = probe_engines_on_peer(handles[d], d, layout.slab_bytes(d), dev)
+            safe = group.decide(safe)
             engines = tuple(e for e in engines if safe.get(e))
             # N-1 donors: also the interleaved chunk order (HV_ENGINE_FLAG_INTERLEAVE),
             # which keeps every donor's egress busy instead of all readers
@@ -208,10 +181,8 @@ def run_b200(a):
                         max_over_ranks=max_over_ranks if world > 1 else None)
         tune["peer_engine_probe"] = safe
         a.engine, a.max_ctas = tune["best"]["engine"], tune["best"]["max_ctas"]
-        if world > 1:  # every rank must run the same configuration: rank 0 decides
-            choice = [a.engine, a.max_ctas]
-            dist.broadcast_object_list(choice, src=0)
-            a.engine, a.max_ctas = choice
+        # every rank must run the same configuration: rank 0 decides
+        a.engine, a.max_ctas = group.decide([a.engine, a.max_ctas])
         fetcher.engine.engine = N.ENGINES[a.engine]
         fetcher.engine.max_ctas = a.max_ctas
 
@@ -242,11 +213,7 @@ def run_b200(a):
             t1.synchronize()
         torch.cuda.synchronize()
         bad = clk.summary().get("rejected", False)
-        if world > 1:  # every rank re-measures if any rank saw a bad reason
-            flag = [bool(bad)]
-            flags = [None] * world
-            dist.all_gather_object(flags, flag)
-            bad = any(f[0] for f in flags)
+        bad = group.any(bad)  # every rank re-measures if any rank saw a bad reason
         if not bad:
             break
         remeasured = clk.summary()  # hw/thermal slowdown seen: keep the record, measure once more

@@ -152,19 +152,21 @@ def churn_phase(world, rank, dev, a, dist, barrier, layers=8, seconds=2.0):
     m = MoEProfile(q.name, layers, q.num_experts, q.top_k, q.expert_size, hidden=q.hidden,
                    intermediate=q.intermediate)
     L, E, S = m.num_layers, m.num_experts, m.expert_size
+    from paper_2602_00328_b200.cluster import DonorLayout, per_reader_bytes
     if world == 1:
         C, D = [0], []
+        per_reader = per_reader_bytes(L * E, S, 1)
+        layout = None
     else:
-        C, D = list(range(world // 2)), list(range(world // 2, world))
-    n_don = max(1, len(D))
-    per_reader = math.ceil(L * E / n_don) * S
+        layout = DonorLayout.split_roles(world, per_reader_bytes(L * E, S, world - world // 2))
+        C, D, per_reader = list(layout.compute), list(layout.donors), layout.per_reader
     pool, imported, out = None, [], None
     handles = [None] * world
     if world > 1:
         mine = None
         if rank in D:
             try:
-                pool = PeerPool(dev, per_reader * len(C), readers=[dev], mode="ipc")
+                pool = PeerPool(dev, layout.slab_bytes(rank), readers=[dev], mode="ipc")
                 mine = pool.export_ipc()
             except Exception as e:
                 out = {"rank": rank, "error": repr(e)[:200]}
@@ -182,8 +184,8 @@ def churn_phase(world, rank, dev, a, dist, barrier, layers=8, seconds=2.0):
     for name, pol in policies.items():
         try:
             if rank in C:
-                outs[name] = _churn_compute(world, rank, dev, a, m, C, D, per_reader, handles, imported, seconds,
-                                            policy=pol)
+                outs[name] = _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported,
+                                            seconds, policy=pol)
         except Exception as e:  # every rank still reaches the collectives below
             outs[name] = {"rank": rank, "error": repr(e)[:300]}
         imported.clear()
@@ -227,7 +229,7 @@ def churn_phase(world, rank, dev, a, dist, barrier, layers=8, seconds=2.0):
             res["policy_comparison"][name]["errors"] = e2
     return res
 
-def _churn_compute(world, rank, dev, a, m, C, D, per_reader, handles, imported, seconds, policy=None):
+def _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported, seconds, policy=None):
     """Compute-rank side of churn_phase (no collectives inside)."""
     import torch
     from paper_2602_00328_b200.churn import ChurnDriver, expert_tier_counts, markov_availability
@@ -245,10 +247,10 @@ def _churn_compute(world, rank, dev, a, m, C, D, per_reader, handles, imported, 
                                  engine=a.engine, max_ctas=a.max_ctas, policy=policy)
         else:
             views = {}
-            for i, d in enumerate(D, start=1):
-                p = PeerPool.import_ipc(handles[d], d, per_reader * len(C), dev)
+            for d in layout.donors_of(rank):
+                p = PeerPool.import_ipc(handles[d], d, layout.slab_bytes(d), dev)
                 imported.append(p)
-                views[i] = p.view(C.index(rank) * per_reader, per_reader)
+                views[layout.peer_index(rank, d)] = p.view(*layout.section(d, rank))
             sysm = HarvestSystem(dev, pools=views, host_tier=host, local_bytes=1, engine=a.engine,
                                  max_ctas=a.max_ctas, policy=policy)
         rt = sysm.runtime
@@ -271,7 +273,7 @@ def _churn_compute(world, rank, dev, a, m, C, D, per_reader, handles, imported, 
         h = dec.step(dec.x0)
         torch.cuda.synchronize()
         GB_levels = [0, per_reader // 4, per_reader // 2, per_reader]
-        donors = D if D else [dev]
+        donors = layout.donors_of(rank) if layout else [dev]
         drv = ChurnDriver(sysm, {i: markov_availability(GB_levels, [0.05] * 4, seed=5 + d, horizon=seconds)
                                  for i, d in enumerate(donors, start=1)})
         drv.start()
@@ -322,26 +324,23 @@ def phi_phase(world, rank, dev, a, dist, barrier, max_over_ranks, batches=(1, 16
     Collective-safe: local work is guarded, every rank reaches every collective."""
     import torch
     from paper_2602_00328_b200 import fetch as F
+    from paper_2602_00328_b200.cluster import DonorLayout, per_reader_bytes, place_experts
     from paper_2602_00328_b200.decode import MoEDecoder
-    from paper_2602_00328_b200.memalloc import Tier
-    from paper_2602_00328_b200.moe import (PHI35_MOE, ExpertFetcher, ExpertResidency, ExpertStore, MoEProfile,
-                                           expert_content)
+    from paper_2602_00328_b200.moe import PHI35_MOE, ExpertFetcher, ExpertResidency, ExpertStore, MoEProfile
     from paper_2602_00328_b200.pool import HostTier, PeerPool
-    from paper_2602_00328_b200.runtime import AllocationHints, Durability
     from paper_2602_00328_b200.system import HarvestSystem
     m = PHI35_MOE
     if a.phi_layers != m.num_layers:
         m = MoEProfile(m.name, a.phi_layers, m.num_experts, m.top_k, m.expert_size, hidden=m.hidden,
                        intermediate=m.intermediate)
     L, E, S = m.num_layers, m.num_experts, m.expert_size
-    others = [r for r in range(world) if r != rank]
-    per_reader = math.ceil(L * E / (world - 1)) * S
+    layout = DonorLayout.symmetric(world, per_reader_bytes(L * E, S, world - 1))
     out = {"model": f"{m.name}: {L} layers x {E} experts x {S} B, top-{m.top_k}", "donors_per_rank": world - 1}
     errors = []
     pool = sysm = fetcher = None
     imported = []
     try:
-        pool = PeerPool(dev, per_reader * (world - 1), readers=[dev], mode="ipc")
+        pool = PeerPool(dev, layout.slab_bytes(rank), readers=[dev], mode="ipc")
         my_handle = pool.export_ipc()
     except Exception as e:
         errors.append(repr(e)[:200])
@@ -352,24 +351,16 @@ def phi_phase(world, rank, dev, a, dist, barrier, max_over_ranks, batches=(1, 16
         if any(h is None for h in handles):
             raise RuntimeError("a donor failed to create its pool")
         views = {}
-        for i, d in enumerate(others, start=1):
-            p = PeerPool.import_ipc(handles[d], d, per_reader * (world - 1), dev)
+        for d in layout.donors_of(rank):
+            p = PeerPool.import_ipc(handles[d], d, layout.slab_bytes(d), dev)
             imported.append(p)
-            views[i] = p.view([r for r in range(world) if r != d].index(rank) * per_reader, per_reader)
+            views[layout.peer_index(rank, d)] = p.view(*layout.section(d, rank))
         sysm = HarvestSystem(dev, pools=views, local_bytes=1, engine=a.engine, max_ctas=a.max_ctas,
                              log_transfers=False)
         rt = sysm.runtime
         res = ExpertResidency(m)
-        ptrs, seeds = [], []
-        for layer in range(L):
-            for e in range(E):
-                h = rt.harvest_alloc(S, AllocationHints(preferred_devices=[1 + (layer * E + e + rank) % (world - 1)],
-                                                        durability=Durability.BACKED, client_id="moe"))
-                if h is None:
-                    raise RuntimeError("donor capacity exhausted")
-                res.set_tier(layer, e, Tier.PEER_HBM, h)
-                ptrs.append(rt.address(h))
-                seeds.append(expert_content(m, layer, e))
+        placed, seeds = place_experts(rt, m, res, rank, world - 1)
+        ptrs = [rt.address(h) for h in placed]
         for i in range(0, len(ptrs), 32):
             F.fill_weights_bf16(F.ptrs_tensor(ptrs[i:i + 32], f"cuda:{dev}"),
                                 F.ptrs_tensor([S] * len(ptrs[i:i + 32]), f"cuda:{dev}"), seeds[i:i + 32])
