@@ -95,3 +95,33 @@ def test_no_peer_capacity_goes_to_host():
     _check_all(kv, m)
     kv.close()
     sysm.close()
+
+
+@pytest.mark.parametrize("chunk", [1, 3, 5])
+def test_chunked_launches_evict_and_reload(chunk):
+    """evict()/reload() launch K1 every `launch_chunk_blocks` blocks, pipelined
+    with the host-side resolution; bytes, tiers and the drain bookkeeping must
+    not depend on the chunking (peer and host sources mixed within a call)."""
+    from paper_2602_00328_b200.kv import KVTier
+    sysm, kv, m = _mk(local_blocks=16, slab_blocks=2, donor_slabs=2, durability="BACKED")
+    kv.launch_chunk_blocks = chunk
+    kv.timing = []
+    kv.append_kv(0, 16 * 16)
+    moves = kv.evict(12 * m.block_bytes)                   # 4 blocks to peer (+host copies), 8 to host
+    assert len(moves) == 12
+    assert {t for _, _, t in moves} == {"PeerHBM", "HostDRAM"}
+    n_launch = len(kv.timing)
+    assert n_launch >= 2 if chunk < 12 else n_launch == 1
+    _check_all(kv, m)
+    ids = [b.block_id for b in kv.table.values() if b.tier != KVTier.LOCAL_HBM]
+    kv.timing = []
+    plan = kv.reload(ids)
+    assert plan["peer"] and plan["host"] and not plan["recompute"]
+    assert len(kv.timing) == -(-len(ids) // chunk)
+    kv.sys.engine.synchronize()
+    sysm.loop.run()
+    assert all(kv.table[i].tier == KVTier.LOCAL_HBM for i in ids)
+    _check_all(kv, m)
+    assert refcheck.verify_release_ordering(sysm.loop.log) == []
+    kv.close()
+    sysm.close()
