@@ -125,3 +125,49 @@ def test_chunked_launches_evict_and_reload(chunk):
     assert refcheck.verify_release_ordering(sysm.loop.log) == []
     kv.close()
     sysm.close()
+
+
+@pytest.mark.parametrize("seed", range(50))
+def test_kv_correctness_independence(seed):
+    """SPEC.md acceptance #3, KV half: random append / evict / reload with every
+    peer slab revoked at a random point (Lossy and Backed sequences mixed);
+    the final bytes of every page equal the zero-peer-capacity result, i.e.
+    the oracle content of (layer, sequence, block)."""
+    import random
+    from paper_2602_00328_b200.kv import KVTier
+    from paper_2602_00328_b200.runtime import Durability, RevokeReason
+    rng = random.Random(seed)
+    sysm, kv, m = _mk(local_blocks=12, host_blocks=256, slab_blocks=2, donor_slabs=3,
+                      durability=rng.choice(["LOSSY", "BACKED"]))
+    kv.launch_chunk_blocks = rng.choice([1, 2, 64])
+    revoked = 0
+    for _ in range(12):
+        r = rng.random()
+        if r < 0.4:
+            kv.append_kv(rng.randrange(4), rng.randint(1, 40), durability=rng.choice(list(Durability)))
+        elif r < 0.6 and kv.table:
+            kv.evict(rng.randint(1, 4) * m.block_bytes)
+        elif r < 0.8 and kv.table:
+            ids = rng.sample(sorted(kv.table), min(len(kv.table), rng.randint(1, 6)))
+            kv.reload(ids)
+        live = [s for s in kv.slabs if s.live]
+        if live and rng.random() < 0.5:
+            sysm.runtime.revoke(rng.choice(live).handle, RevokeReason.EXTERNAL_RECLAIM)
+            revoked += 1
+        sysm.loop.poll()
+    for s in kv.slabs:  # every remaining slab is revoked too
+        if s.live:
+            sysm.runtime.revoke(s.handle, RevokeReason.EXTERNAL_RECLAIM)
+            revoked += 1
+    kv.sys.engine.synchronize()
+    sysm.loop.run()
+    assert all(b.tier != KVTier.PEER_HBM for b in kv.table.values())
+    lost = sorted(i for i, b in kv.table.items() if b.tier == KVTier.NOT_MATERIALIZED)
+    for k in range(0, len(lost), 6):   # Lossy-lost blocks are recomputed (local room for 6 at a time)
+        kv.reload(lost[k:k + 6])
+    kv.sys.engine.synchronize()
+    sysm.loop.run()
+    _check_all(kv, m)
+    assert refcheck.verify_release_ordering(sysm.loop.log) == []
+    kv.close()
+    sysm.close()
