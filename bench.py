@@ -25,7 +25,6 @@ memcpy gather from the host-authoritative copy) on the box's host cores.
 from __future__ import annotations
 
 import argparse
-import json
 import math
 import os
 import statistics

@@ -2,13 +2,8 @@
 from __future__ import annotations
 
 import json
-import math
 import os
-import statistics
 import sys
-import time
-
-import numpy as np
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if REPO not in sys.path:

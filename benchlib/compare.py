@@ -2,11 +2,9 @@
 from __future__ import annotations
 
 import json
-import math
 import os
 import statistics
 import sys
-import time
 
 import numpy as np
 

@@ -3,10 +3,7 @@
 Test infrastructure use of oracle/ is confined to this module, as the contract allows."""
 from __future__ import annotations
 
-import json
-import math
 import os
-import statistics
 import sys
 import time
 

@@ -2,11 +2,7 @@
 (configs[3]) and donor churn (configs[4])."""
 from __future__ import annotations
 
-import json
 import math
-import os
-import statistics
-import sys
 import time
 
 import numpy as np
@@ -69,7 +65,6 @@ def run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, micro
 def host_offload_decode(m, dev, a, microbatches=1, steps=3, warm=2):
     """The same decode with every expert served from pinned host DRAM (the
     CPU-offload baseline of PAPER.md §4.5), on this GPU."""
-    import torch
     from paper_2602_00328_b200.moe import ExpertFetcher, ExpertResidency, ExpertStore
     from paper_2602_00328_b200.pool import HostTier
     from paper_2602_00328_b200.system import HarvestSystem
@@ -88,7 +83,6 @@ def kv_long_context(sysm, source, a):
     HBM to harvested peer slabs (N>1, Lossy) or the host tier (N=1, Backed),
     then reloaded with ONE K1 launch of 262,144 pages.  Reports the kernel
     time, the end-to-end reload() time, and a content check of sampled pages."""
-    import torch
     from paper_2602_00328_b200 import fetch as F
     from paper_2602_00328_b200.kv import LLAMA3_8B, KVCacheManager, kv_seed
     from paper_2602_00328_b200.runtime import Durability
@@ -141,15 +135,8 @@ def churn_phase(world, rank, dev, a, dist, barrier, layers=8, seconds=2.0):
     host copy and are re-placed by rebalance (moe.py:155-197) when capacity
     returns.  Decode outputs are compared bit-for-bit with an all-local run.
     N=1: the compute GPU donates to itself through a VMM pool."""
-    import torch
-    from paper_2602_00328_b200.churn import ChurnDriver, expert_tier_counts, markov_availability
-    from paper_2602_00328_b200.decode import MoEDecoder
-    from paper_2602_00328_b200.memalloc import Tier
-    from paper_2602_00328_b200.moe import (QWEN15_MOE_A27B, ExpertFetcher, ExpertResidency, ExpertStore,
-                                           MoEProfile, rebalance)
-    from paper_2602_00328_b200.pool import HostTier, PeerPool
-    from paper_2602_00328_b200.system import HarvestSystem
-    from paper_2602_00328_b200.verify import verify_release_ordering
+    from paper_2602_00328_b200.moe import QWEN15_MOE_A27B, MoEProfile
+    from paper_2602_00328_b200.pool import PeerPool
     q = QWEN15_MOE_A27B
     m = MoEProfile(q.name, layers, q.num_experts, q.top_k, q.expert_size, hidden=q.hidden,
                    intermediate=q.intermediate)
@@ -242,80 +229,79 @@ def _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported
     from paper_2602_00328_b200.system import HarvestSystem
     from paper_2602_00328_b200.verify import verify_release_ordering
     L, E, S = m.num_layers, m.num_experts, m.expert_size
-    if True:
-        host = HostTier(L * E * S)
-        if world == 1:
-            sysm = HarvestSystem(dev, donors=[dev], donor_bytes=per_reader, host_tier=host, local_bytes=1,
-                                 engine=a.engine, max_ctas=a.max_ctas, policy=policy)
-        else:
-            views = {}
-            for d in layout.donors_of(rank):
-                p = PeerPool.import_ipc(handles[d], d, layout.slab_bytes(d), dev)
-                imported.append(p)
-                views[layout.peer_index(rank, d)] = p.view(*layout.section(d, rank))
-            sysm = HarvestSystem(dev, pools=views, host_tier=host, local_bytes=1, engine=a.engine,
-                                 max_ctas=a.max_ctas, policy=policy)
-        rt = sysm.runtime
-        store = ExpertStore(m, sysm.host_id, host)
-        store.fill_host(dev, weights=True)
-        res = ExpertResidency(m)
-        counts = np.ones((L, E), dtype=np.int64)
-        migrated = [0]
+    host = HostTier(L * E * S)
+    if world == 1:
+        sysm = HarvestSystem(dev, donors=[dev], donor_bytes=per_reader, host_tier=host, local_bytes=1,
+                             engine=a.engine, max_ctas=a.max_ctas, policy=policy)
+    else:
+        views = {}
+        for d in layout.donors_of(rank):
+            p = PeerPool.import_ipc(handles[d], d, layout.slab_bytes(d), dev)
+            imported.append(p)
+            views[layout.peer_index(rank, d)] = p.view(*layout.section(d, rank))
+        sysm = HarvestSystem(dev, pools=views, host_tier=host, local_bytes=1, engine=a.engine,
+                             max_ctas=a.max_ctas, policy=policy)
+    rt = sysm.runtime
+    store = ExpertStore(m, sysm.host_id, host)
+    store.fill_host(dev, weights=True)
+    res = ExpertResidency(m)
+    counts = np.ones((L, E), dtype=np.int64)
+    migrated = [0]
 
-        def replace():
-            mig = rebalance(sysm.loop, rt, m, res, counts, sysm.host_id, store=store)
-            migrated[0] += len(mig)
-            return mig
+    def replace():
+        mig = rebalance(sysm.loop, rt, m, res, counts, sysm.host_id, store=store)
+        migrated[0] += len(mig)
+        return mig
 
-        replace()
-        sysm.loop.run()
-        placed0 = expert_tier_counts(res)["PeerHBM"]
-        dec = MoEDecoder(ExpertFetcher(rt, m, res, store), tokens=TOKENS, microbatches=1, seed=13,
-                         engine=a.engine, max_ctas=a.max_ctas)
-        h = dec.step(dec.x0)
-        torch.cuda.synchronize()
-        GB_levels = [0, per_reader // 4, per_reader // 2, per_reader]
-        donors = layout.donors_of(rank) if layout else [dev]
-        drv = ChurnDriver(sysm, {i: markov_availability(GB_levels, [0.05] * 4, seed=5 + d, horizon=seconds)
-                                 for i, d in enumerate(donors, start=1)})
-        drv.start()
-        steps, peer_min, peer_max = 1, placed0, placed0
-        t0 = time.perf_counter()
-        while time.perf_counter() - t0 < seconds:
-            h = dec.step(h)
-            steps += 1
-            drv.tick(replace)
-            pc = expert_tier_counts(res)["PeerHBM"]
-            peer_min, peer_max = min(peer_min, pc), max(peer_max, pc)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-        sysm.loop.run()
-        log = sysm.loop.log
-        # all-local reference run of the same number of steps
-        resident = torch.from_numpy(host.view()[:L * E * S].copy()).to(f"cuda:{dev}")
-        lres = ExpertResidency(m)
-        for layer in range(L):
-            for e in range(E):
-                lres.set_tier(layer, e, Tier.LOCAL_HBM)
-        lsys = HarvestSystem(dev, host_bytes=1, local_bytes=1, log_transfers=False)
-        lf = ExpertFetcher(lsys.runtime, m, lres, ExpertStore(m, lsys.host_id, None),
-                           local_addr=[[resident.data_ptr() + (l * E + e) * S for e in range(E)] for l in range(L)])
-        ldec = MoEDecoder(lf, tokens=TOKENS, microbatches=1, seed=13)
-        h2 = ldec.x0
-        for _ in range(steps):
-            h2 = ldec.step(h2)
-        torch.cuda.synchronize()
-        out = {"rank": rank, "decode_steps": steps - 1, "tokens_per_s": TOKENS * (steps - 1) / wall,
-               "availability_steps": len(log.of_kind("availability_step")),
-               "revocations": len(log.of_kind("revoke_begin")), "re_placements": migrated[0] - placed0,
-               "peer_resident_experts_min_max": [peer_min, peer_max], "experts": L * E,
-               "release_ordering_violations": len(verify_release_ordering(log)),
-               "outputs_bit_identical_to_all_local": bool(torch.equal(h.view(torch.int16), h2.view(torch.int16)))}
-        del dec, ldec, resident
-        lsys.close()
-        sysm.close()
-        for p in imported:
-            p.close()
+    replace()
+    sysm.loop.run()
+    placed0 = expert_tier_counts(res)["PeerHBM"]
+    dec = MoEDecoder(ExpertFetcher(rt, m, res, store), tokens=TOKENS, microbatches=1, seed=13,
+                     engine=a.engine, max_ctas=a.max_ctas)
+    h = dec.step(dec.x0)
+    torch.cuda.synchronize()
+    GB_levels = [0, per_reader // 4, per_reader // 2, per_reader]
+    donors = layout.donors_of(rank) if layout else [dev]
+    drv = ChurnDriver(sysm, {i: markov_availability(GB_levels, [0.05] * 4, seed=5 + d, horizon=seconds)
+                             for i, d in enumerate(donors, start=1)})
+    drv.start()
+    steps, peer_min, peer_max = 1, placed0, placed0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        h = dec.step(h)
+        steps += 1
+        drv.tick(replace)
+        pc = expert_tier_counts(res)["PeerHBM"]
+        peer_min, peer_max = min(peer_min, pc), max(peer_max, pc)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    sysm.loop.run()
+    log = sysm.loop.log
+    # all-local reference run of the same number of steps
+    resident = torch.from_numpy(host.view()[:L * E * S].copy()).to(f"cuda:{dev}")
+    lres = ExpertResidency(m)
+    for layer in range(L):
+        for e in range(E):
+            lres.set_tier(layer, e, Tier.LOCAL_HBM)
+    lsys = HarvestSystem(dev, host_bytes=1, local_bytes=1, log_transfers=False)
+    lf = ExpertFetcher(lsys.runtime, m, lres, ExpertStore(m, lsys.host_id, None),
+                       local_addr=[[resident.data_ptr() + (l * E + e) * S for e in range(E)] for l in range(L)])
+    ldec = MoEDecoder(lf, tokens=TOKENS, microbatches=1, seed=13)
+    h2 = ldec.x0
+    for _ in range(steps):
+        h2 = ldec.step(h2)
+    torch.cuda.synchronize()
+    out = {"rank": rank, "decode_steps": steps - 1, "tokens_per_s": TOKENS * (steps - 1) / wall,
+           "availability_steps": len(log.of_kind("availability_step")),
+           "revocations": len(log.of_kind("revoke_begin")), "re_placements": migrated[0] - placed0,
+           "peer_resident_experts_min_max": [peer_min, peer_max], "experts": L * E,
+           "release_ordering_violations": len(verify_release_ordering(log)),
+           "outputs_bit_identical_to_all_local": bool(torch.equal(h.view(torch.int16), h2.view(torch.int16)))}
+    del dec, ldec, resident
+    lsys.close()
+    sysm.close()
+    for p in imported:
+        p.close()
     return out
 
 def phi_phase(world, rank, dev, a, dist, barrier, max_over_ranks, batches=(1, 16, 64)):

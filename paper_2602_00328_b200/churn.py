@@ -21,8 +21,6 @@ from __future__ import annotations
 import random
 from dataclasses import dataclass, field
 
-import numpy as np
-
 from .memalloc import Tier
 
 

@@ -47,7 +47,7 @@ def test_donor_monitor_reclaims_under_cotenant_pressure():
 
 
 def test_decode_under_churn_matches_all_local():
-    from paper_2602_00328_b200.churn import AvailabilityProcess, ChurnDriver, expert_tier_counts
+    from paper_2602_00328_b200.churn import expert_tier_counts
     from paper_2602_00328_b200.decode import MoEDecoder
     from paper_2602_00328_b200.moe import ExpertFetcher, ExpertResidency, ExpertStore, rebalance
     from paper_2602_00328_b200.system import HarvestSystem

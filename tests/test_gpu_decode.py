@@ -14,7 +14,6 @@ RS = 256.0  # residual scale: makes the tiny MoE delta visible in bf16 (power of
 
 def _setup(model, peer_experts, microbatches=2, tokens=16, seed=0):
     from paper_2602_00328_b200.decode import MoEDecoder
-    from paper_2602_00328_b200.memalloc import Tier
     from paper_2602_00328_b200.moe import ExpertFetcher, ExpertResidency, ExpertStore, rebalance
     from paper_2602_00328_b200.system import HarvestSystem
     L, E, S = model.num_layers, model.num_experts, model.expert_size

@@ -1,7 +1,6 @@
 """vLLM OffloadingHandler contract (worker.py:26-75) over the harvested peer
 tier: store GPU blocks to PEER, load them back to other GPU blocks, bytes
 identical; a revoked slab makes the load complete with success=False."""
-import numpy as np
 import pytest
 import torch
 

@@ -7,7 +7,6 @@ flushing L2 between iterations (256 MiB write).
 import json
 import os
 import sys
-import time
 
 import numpy as np
 import torch
