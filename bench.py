@@ -288,6 +288,12 @@ def run_b200(a):
                                                                  "ms_per_decode_step", "outputs_finite",
                                                                  "overlap")}
     decode["pipelined_2_microbatches"]["fetch_max_ctas"] = a.overlap_max_ctas
+    # the same decode consuming every expert in place (fused fetch + FFN)
+    try:
+        decode["fused"] = run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, microbatches=1,
+                                     fused=True)
+    except Exception as e:  # report, never lose the line (every rank reaches the same collectives)
+        decode["fused"] = {"error": repr(e)[:300]}
     sysm.loop.run()
     kvlc = None
     if not a.no_kv:

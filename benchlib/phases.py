@@ -11,14 +11,14 @@ from benchlib.common import KV_SLAB_BLOCKS, KV_TOKENS, TOKENS
 
 
 def run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, microbatches=2, steps=3, warm=2,
-               max_ctas=None):
+               max_ctas=None, fused=False):
     """MoE decode tokens/s: batch 32 split into `microbatches`, layer-major
     stages, each stage's experts fetched one stage ahead (K2, device-side
     plan) while the previous stage's SwiGLU experts run on the compute stream."""
     import torch
     from paper_2602_00328_b200.decode import MoEDecoder
     dec = MoEDecoder(fetcher, tokens=TOKENS, microbatches=microbatches, seed=7, engine=a.engine,
-                     max_ctas=a.max_ctas if max_ctas is None else max_ctas)
+                     max_ctas=a.max_ctas if max_ctas is None else max_ctas, fused=fused)
     h = dec.decode(warm)
     torch.cuda.synchronize()
     barrier()
@@ -35,7 +35,10 @@ def run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, micro
            "outputs_finite": bool(torch.isfinite(h.float()).all()),
            "model": f"{m.num_layers} MoE layers (router + top-{m.top_k} + SwiGLU experts, bf16); "
                     "attention not modeled"}
-    if microbatches > 1:  # one extra, traced step: device-clock proof of fetch/compute overlap
+    if fused:
+        out["mode"] = ("fused: experts consumed in place (hv_expert_ffn_gate_up/down stream weight tiles from "
+                       "the resident copy into mma.sync; no K2 staging copy)")
+    if microbatches > 1 and not fused:  # one extra, traced step: device-clock proof of fetch/compute overlap
         dec.trace = True
         dec.step(h)
         out["overlap"] = dec.overlap_report()

@@ -213,6 +213,25 @@ int hv_swap_blocks_batch(const uint64_t* h_src, const uint64_t* h_dst,
 int hv_ce_batch_copy(const uint64_t* h_src, const uint64_t* h_dst,
                      const uint64_t* h_bytes, uint32_t n, int batched, void* stream);
 
+/* ---- fused consumer: expert FFN over the expert's resident copy ---------- */
+/* The decode stage's compute (moe.py:315-340) reading each expert object in
+ * place -- donor HBM over NVLink, pinned host over PCIe, or local HBM --
+ * instead of after a K2 fetch into local staging: weight tiles stream through
+ * shared memory (cp.async) into mma.sync, so the transfer overlaps the math
+ * and the bytes cross the link once.  Object layout: gate [I][H], up [I][H],
+ * down [H][I], bf16.  Routed pairs are sorted by expert: expert e (of
+ * n_experts) owns pairs d_offs[e] .. d_offs[e] + d_counts[e] - 1, at most
+ * hv_expert_ffn_max_tokens() of them.  Requires H % 64 == 0 and I % 64 == 0.
+ *   gate_up: act[p][i] = silu(gate[i] . x[tok[p]]) * (up[i] . x[tok[p]])  (bf16 [P][I])
+ *   down:    y[p][h]   = down[h] . act[p]                                  (fp32 [P][H]) */
+int hv_expert_ffn_gate_up(const uint64_t* d_w_addr, const int32_t* d_counts, const int32_t* d_offs,
+                          const int32_t* d_tok, const void* d_x, void* d_act, uint32_t n_experts,
+                          uint32_t hidden, uint32_t intermediate, void* stream);
+int hv_expert_ffn_down(const uint64_t* d_w_addr, const int32_t* d_counts, const int32_t* d_offs,
+                       const void* d_act, float* d_y, uint32_t n_experts, uint32_t hidden,
+                       uint32_t intermediate, void* stream);
+int hv_expert_ffn_max_tokens(int* out);
+
 /* ---- synthetic content (test / bench inputs) --------------------------- */
 /* byte j of object = byte (j%8) (little-endian) of splitmix64 word j/8:
  *   w_i = fmix(seed + (i+1)*0x9E3779B97F4A7C15)

@@ -114,6 +114,9 @@ _SIGS = {
     "hv_verify_content": [u64, u64, u64, u32, u64, vp],
     "hv_verify_weights_bf16": [u64, u64, u64, u32, u64, vp],
     "hv_launch_count": [P64],
+    "hv_expert_ffn_gate_up": [u64, u64, u64, u64, u64, u64, u32, u32, u32, vp],
+    "hv_expert_ffn_down": [u64, u64, u64, u64, u64, u32, u32, u32, vp],
+    "hv_expert_ffn_max_tokens": [C.POINTER(i32)],
 }
 _RESTYPES = {"hv_error_string": C.c_char_p}
 
@@ -167,6 +170,13 @@ def device_count() -> int:
     n = C.c_int(0)
     call("hv_device_count", C.byref(n))
     return n.value
+
+
+def c_int_out(name: str) -> int:
+    """Call an entry point of the form int f(int* out) and return *out."""
+    v = C.c_int(0)
+    call(name, C.byref(v))
+    return v.value
 
 
 def launch_count() -> int:

@@ -1,0 +1,284 @@
+// Fused expert FFN over the expert's resident copy (sm_100a).
+//
+// The reference's decode stage fetches every activated expert into local
+// memory and then computes with it (moe.py:282-340: _issue_fetches, then the
+// stage's compute once all fetches arrived).  On an NVSwitch node the expert
+// can instead be consumed where it lies: these kernels stream each weight
+// tile straight from the expert object's address -- donor HBM over NVLink,
+// pinned host DRAM over PCIe, or local HBM -- into shared memory and multiply
+// it there, so the transfer overlaps the math tile by tile and the bytes cross
+// the link exactly once, with no staging write and re-read in local HBM.
+//
+// Decode is weight-bandwidth bound (a handful of tokens per expert), so the
+// kernels are built like the fetch kernels: deep cp.async (16-byte LDGSTS)
+// pipelines keep tens of KiB per SM in flight, and the tensor cores
+// (mma.sync m16n8k16 bf16 -> fp32) only have to keep up with the link.
+// Tile shape, measured on B200 with experts in local HBM (tools/fused_probe.py,
+// weight GB/s of the activated experts, Qwen1.5-MoE stage / Phi-3.5 batch 16):
+//   k-tile 128 x 4 stages (192 KiB smem, 1 CTA/SM): 3,365 / 3,673
+//   k-tile  64 x 4 stages ( 96 KiB smem, 2 CTAs/SM): 4,667 / 4,967   <- default
+//   k-tile  64 x 6 stages: 3,480 / 3,742;  k-tile 32 x 8 stages: 3,786 / 4,141
+// Two resident CTAs per SM hide each other's pipeline fill and drain.
+//
+// Layout of an expert object (the same one K2 moves): gate [I][H], up [I][H],
+// down [H][I], bf16, row-major.  Routed (token, expert) pairs are sorted by
+// expert on the device; expert e owns pairs offs[e] .. offs[e]+counts[e]-1.
+//
+//   hv_expert_ffn_gate_up: act[p][i] = silu(gate[i] . x[tok[p]]) * (up[i] . x[tok[p]])
+//   hv_expert_ffn_down:    y[p][h]   = down[h] . act[p]          (fp32)
+// The top-k combine (a fixed-order weighted sum per token) is the caller's.
+#include <cuda_bf16.h>
+
+#include "hv_common.h"
+
+namespace {
+
+constexpr int kWarps = 4;
+constexpr int kThreads = kWarps * 32;
+constexpr int kRows = 16 * kWarps;   // weight rows per CTA (16 per warp: one mma M tile)
+#ifndef HV_FFN_KT
+#define HV_FFN_KT 64
+#endif
+#ifndef HV_FFN_STAGES
+#define HV_FFN_STAGES 4
+#endif
+constexpr int kKT = HV_FFN_KT;       // k columns per pipeline stage (64: 128 B per row)
+constexpr int kRowBytes = kKT * 2;
+constexpr int kChunksPerRow = kRowBytes / 16;
+constexpr int kMaxTok = 64;          // routed tokens per expert per launch (8 mma N groups)
+constexpr int kGroups = kMaxTok / 8;
+constexpr int kStages = HV_FFN_STAGES;
+
+template <int NMAT>
+struct Smem {
+  static constexpr int kW = NMAT * kRows * kRowBytes;   // weight tiles of one stage
+  static constexpr int kX = kMaxTok * kRowBytes;        // activation tile of one stage
+  static constexpr int kStage = kW + kX;
+  static constexpr int kTotal = kStages * kStage;
+};
+
+struct FfnArgs {
+  const uint64_t* w_addr;   // [E] base address of each expert object (any tier)
+  const int32_t* counts;    // [E] routed pairs of expert e
+  const int32_t* offs;      // [E] first sorted pair of expert e
+  const int32_t* tok;       // [P] activation row of each sorted pair (nullptr: row = pair)
+  const __nv_bfloat16* x;   // activations, K columns per row
+  void* out;                // NMAT=2: bf16 [P][rows]; NMAT=1: fp32 [P][rows]
+  uint64_t w_off0, w_off1;  // byte offsets of the matrices inside the object
+  int rows, K;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// 16-byte chunk c of tile row r lives at chunk (c ^ (r & 7)): ldmatrix's eight
+// row addresses then hit eight different bank groups
+__device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * kRowBytes + ((c ^ (r & 7)) << 4)); }
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0, %1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// Grid: (rows / kRows, E).  CTA (rb, e) computes rows [rb*64, rb*64+64) of
+// NMAT matrices of expert e against its n routed activation rows.
+template <int NMAT>
+__global__ void __launch_bounds__(kThreads) expert_ffn_kernel(FfnArgs a) {
+  const int e = blockIdx.y;
+  const int n = a.counts[e];
+  if (n <= 0) return;
+  extern __shared__ __align__(128) char smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int row0 = blockIdx.x * kRows;
+  const int p0 = a.offs[e];
+  const int ng = (n + 7) >> 3;
+  const char* obj = reinterpret_cast<const char*>(a.w_addr[e]);
+  const char* wsrc[2] = {obj + a.w_off0 + (size_t)row0 * a.K * 2, obj + a.w_off1 + (size_t)row0 * a.K * 2};
+  const size_t wstride = (size_t)a.K * 2;
+  const size_t xstride = (size_t)a.K * 2;
+  const int ktiles = a.K / kKT;
+
+  // activation rows beyond n inside the last N group must hold finite values
+  for (int s = 0; s < kStages; ++s) {
+    char* xs = smem + s * Smem<NMAT>::kStage + Smem<NMAT>::kW;
+    for (int i = tid; i < (ng * 8 - n) * kChunksPerRow; i += kThreads) {
+      const int r = n + i / kChunksPerRow, c = i % kChunksPerRow;
+      *reinterpret_cast<uint4*>(xs + swz(r, c)) = make_uint4(0, 0, 0, 0);
+    }
+  }
+  // per-thread activation row pointers are recomputed per stage from the pair list
+  auto load_stage = [&](int kt, int s) {
+    char* base = smem + s * Smem<NMAT>::kStage;
+    const size_t kb = (size_t)kt * kRowBytes;
+#pragma unroll
+    for (int m = 0; m < NMAT; ++m) {
+      const uint32_t ws = smem_u32(base + m * kRows * kRowBytes);
+#pragma unroll 4
+      for (int i = tid; i < kRows * kChunksPerRow; i += kThreads) {
+        const int r = i / kChunksPerRow, c = i % kChunksPerRow;
+        cp_async16(ws + swz(r, c), wsrc[m] + r * wstride + kb + c * 16);
+      }
+    }
+    const uint32_t xs = smem_u32(base + Smem<NMAT>::kW);
+    for (int i = tid; i < n * kChunksPerRow; i += kThreads) {
+      const int r = i / kChunksPerRow, c = i % kChunksPerRow;
+      const int row = a.tok ? a.tok[p0 + r] : p0 + r;
+      cp_async16(xs + swz(r, c), reinterpret_cast<const char*>(a.x) + row * xstride + kb + c * 16);
+    }
+  };
+
+  float acc[NMAT][kGroups][4];
+#pragma unroll
+  for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+    for (int g = 0; g < kGroups; ++g)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[m][g][j] = 0.f;
+
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < ktiles) load_stage(s, s);
+    cp_commit();
+  }
+  // ldmatrix lane roles
+  const int a_row = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;  // A: x4 = rows 0-7/8-15 x k 0-7/8-15
+  const int a_kc = lane >> 4;
+  const int b_row = lane & 7;                                       // B: x2 = tokens 0-7 x k 0-7/8-15
+  const int b_kc = (lane >> 3) & 1;
+
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_wait<kStages - 2>();
+    __syncthreads();
+    // refill the stage consumed one iteration ago
+    const int nk = kt + kStages - 1;
+    if (nk < ktiles) load_stage(nk, nk % kStages);
+    cp_commit();
+    const char* base = smem + (kt % kStages) * Smem<NMAT>::kStage;
+    const uint32_t xs = smem_u32(base + Smem<NMAT>::kW);
+#pragma unroll
+    for (int kk = 0; kk < kKT / 16; ++kk) {
+      uint32_t af[NMAT][4];
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m)
+        ldsm_x4(smem_u32(base + m * kRows * kRowBytes) + swz(a_row, kk * 2 + a_kc), af[m][0], af[m][1], af[m][2],
+                af[m][3]);
+#pragma unroll
+      for (int g = 0; g < kGroups; ++g) {
+        if (g < ng) {
+          uint32_t b0, b1;
+          ldsm_x2(xs + swz(g * 8 + b_row, kk * 2 + b_kc), b0, b1);
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m) mma_bf16(acc[m][g], af[m][0], af[m][1], af[m][2], af[m][3], b0, b1);
+        }
+      }
+    }
+  }
+  cp_wait<0>();
+
+  // epilogue: d0 (row r, tok 2c), d1 (r, 2c+1), d2 (r+8, 2c), d3 (r+8, 2c+1)
+  const int r = row0 + warp * 16 + (lane >> 2);
+  const int c2 = (lane & 3) * 2;
+#pragma unroll
+  for (int g = 0; g < kGroups; ++g) {
+    if (g >= ng) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int t = g * 8 + c2 + (j & 1);
+      const int row = r + (j >> 1) * 8;
+      if (t >= n) continue;
+      const size_t o = (size_t)(p0 + t) * a.rows + row;
+      if constexpr (NMAT == 2) {
+        const float gv = acc[0][g][j], uv = acc[1][g][j];
+        const float act = gv / (1.f + __expf(-gv)) * uv;
+        reinterpret_cast<__nv_bfloat16*>(a.out)[o] = __float2bfloat16_rn(act);
+      } else {
+        reinterpret_cast<float*>(a.out)[o] = acc[0][g][j];
+      }
+    }
+  }
+}
+
+template <int NMAT>
+int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
+  if (n_experts == 0) return HV_OK;
+  HV_CHECK_ARG(a.w_addr && a.counts && a.offs && a.x && a.out);
+  HV_CHECK_ARG(a.rows > 0 && a.K > 0 && a.rows % kRows == 0 && a.K % kKT == 0);
+  HV_CHECK_ARG(n_experts <= 65535u);
+  int dev = 0;
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
+  if (st) return st;
+  static bool attr_set[64] = {};
+  if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+    HV_CUDA(cudaFuncSetAttribute(expert_ffn_kernel<NMAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Smem<NMAT>::kTotal));
+    attr_set[dev] = true;
+  }
+  dim3 grid(a.rows / kRows, n_experts);
+  expert_ffn_kernel<NMAT><<<grid, kThreads, Smem<NMAT>::kTotal, (cudaStream_t)stream>>>(a);
+  HV_CUDA(cudaGetLastError());
+  hv::note_launch();
+  return HV_OK;
+}
+
+}  // namespace
+
+HV_EXPORT int hv_expert_ffn_gate_up(const uint64_t* d_w_addr, const int32_t* d_counts, const int32_t* d_offs,
+                                    const int32_t* d_tok, const void* d_x, void* d_act, uint32_t n_experts,
+                                    uint32_t hidden, uint32_t intermediate, void* stream) {
+  HV_CHECK_ARG(d_tok != nullptr || n_experts == 0);
+  FfnArgs a{};
+  a.w_addr = d_w_addr;
+  a.counts = d_counts;
+  a.offs = d_offs;
+  a.tok = d_tok;
+  a.x = reinterpret_cast<const __nv_bfloat16*>(d_x);
+  a.out = d_act;
+  a.w_off0 = 0;
+  a.w_off1 = (uint64_t)intermediate * hidden * 2;
+  a.rows = (int)intermediate;
+  a.K = (int)hidden;
+  return launch_ffn<2>(a, n_experts, stream);
+}
+
+HV_EXPORT int hv_expert_ffn_down(const uint64_t* d_w_addr, const int32_t* d_counts, const int32_t* d_offs,
+                                 const void* d_act, float* d_y, uint32_t n_experts, uint32_t hidden,
+                                 uint32_t intermediate, void* stream) {
+  FfnArgs a{};
+  a.w_addr = d_w_addr;
+  a.counts = d_counts;
+  a.offs = d_offs;
+  a.tok = nullptr;
+  a.x = reinterpret_cast<const __nv_bfloat16*>(d_act);
+  a.out = d_y;
+  a.w_off0 = (uint64_t)intermediate * hidden * 4;
+  a.w_off1 = 0;
+  a.rows = (int)hidden;
+  a.K = (int)intermediate;
+  return launch_ffn<1>(a, n_experts, stream);
+}
+
+HV_EXPORT int hv_expert_ffn_max_tokens(int* out) {
+  HV_CHECK_ARG(out);
+  *out = kMaxTok;
+  return HV_OK;
+}

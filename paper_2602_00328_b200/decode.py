@@ -25,6 +25,14 @@ B200-native choices:
 - Drain: a stage may read any peer handle of its layer, so all of them join
   the stage's in-flight set (a superset of the reference's per-expert sets,
   which keeps drain-before-free).
+
+fused=True consumes each expert where it lies instead (csrc/hv_ffn.cu): the
+routed (token, expert) pairs are sorted by expert on the device and two
+kernels stream the gate/up and down weight tiles straight from the resident
+copy (donor HBM over NVLink, host over PCIe, local HBM) into mma.sync, then a
+fixed-order top-k combine.  No staging buffer and no K2 launch; the bytes
+cross the link once and the transfer overlaps the math tile by tile.  The
+drain set of a fused step is every peer handle the step may read.
 """
 from __future__ import annotations
 
@@ -40,7 +48,7 @@ from .moe import ExpertFetcher
 class MoEDecoder:
     def __init__(self, fetcher: ExpertFetcher, tokens: int, microbatches: int = 1, seed: int = 0,
                  engine: str = "auto", max_ctas: int = 0, router_scale: float = 0.5,
-                 residual_scale: float = 1.0, trace: bool = False):
+                 residual_scale: float = 1.0, trace: bool = False, fused: bool = False):
         m = fetcher.model
         if not (m.hidden and m.intermediate):
             raise ValueError("model profile needs hidden/intermediate sizes")
@@ -67,7 +75,16 @@ class MoEDecoder:
         # at most K experts can be active in one stage: K compact staging slots
         # per buffer; expert e goes to slot rank(e) among the active ones
         self.K = min(self.E, (tokens // microbatches) * m.top_k)
-        self.staging = [torch.zeros(self.K, self.S, dtype=torch.uint8, device=self.dev) for _ in range(2)]
+        self.fused = fused
+        if fused:
+            mt = N.c_int_out("hv_expert_ffn_max_tokens")
+            if self.tmb > mt:
+                raise ValueError(f"fused decode: at most {mt} tokens per micro-batch")
+            if self.I % 64 or self.H % 64:
+                raise ValueError("fused decode needs hidden and intermediate sizes that are multiples of 64")
+        # fused mode reads experts in place: no staging copies
+        self.staging = [torch.zeros(0 if fused else self.K, self.S, dtype=torch.uint8, device=self.dev)
+                        for _ in range(2)]
         self.slot_base = [b.data_ptr() for b in self.staging]
         self.dst_ptrs = [torch.zeros(self.E, dtype=torch.int64, device=self.dev) for _ in range(2)]
         self.idx_ext = [torch.zeros(self.K + 1, dtype=torch.int64, device=self.dev) for _ in range(2)]
@@ -208,6 +225,8 @@ class MoEDecoder:
             self.sync_tables()
         if self._graph is not None:
             return self._replay(x)
+        if self.fused:
+            return self._step_fused(x)
         return self._step_eager(x)
 
     def capture_graph(self) -> None:
@@ -225,14 +244,15 @@ class MoEDecoder:
         side.wait_stream(cur)
         self._capturing = True
         try:
+            body = self._step_fused if self.fused else self._step_eager
             with torch.cuda.stream(side):            # warm-up outside capture (allocator, cuBLAS handles)
                 for _ in range(2):
-                    self._step_eager(self._graph_in)
+                    body(self._graph_in)
             cur.wait_stream(side)
             torch.cuda.synchronize(self.dev)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                self._graph_out = self._step_eager(self._graph_in)
+                self._graph_out = body(self._graph_in)
         finally:
             self._capturing = False
         torch.cuda.synchronize(self.dev)
@@ -301,6 +321,66 @@ class MoEDecoder:
         done = torch.cuda.Event()
         done.record(cur)              # every fetch of this step read self.addr before this point
         self._addr_done[self._addr_cur] = done
+        return torch.stack(hs).view(self.T, self.H)
+
+    # ---------------------------------------------------------------- fused
+    def _route_pairs(self, h: torch.Tensor, layer: int):
+        """Router -> top-k -> routed pairs sorted by expert, all on the device:
+        counts/offsets per expert, the token row of each sorted pair, and the
+        sorted position of pair (t, j) for the combine."""
+        k = self.m.top_k
+        logits = (h @ self.router[layer].t()).float()
+        topv, topi = logits.topk(k, dim=1)
+        probs = torch.softmax(topv, dim=1)
+        flat = topi.reshape(-1)
+        order = torch.argsort(flat, stable=True)
+        counts = torch.zeros(self.E, dtype=torch.int32, device=self.dev)
+        counts.scatter_add_(0, flat, torch.ones_like(flat, dtype=torch.int32))
+        offs = (torch.cumsum(counts, 0, dtype=torch.int32) - counts)
+        tok = torch.div(order, k, rounding_mode="floor").to(torch.int32)
+        pos = torch.empty_like(order)
+        pos[order] = torch.arange(order.numel(), device=self.dev)
+        return probs, counts, offs, tok, pos
+
+    def _ffn_fused(self, h: torch.Tensor, layer: int) -> torch.Tensor:
+        probs, counts, offs, tok, pos = self._route_pairs(h, layer)
+        P, H, I = pos.numel(), self.H, self.I
+        act = torch.empty(P, I, dtype=torch.bfloat16, device=self.dev)
+        y = torch.empty(P, H, dtype=torch.float32, device=self.dev)
+        stream = torch.cuda.current_stream(self.dev).cuda_stream
+        w = self.addr[layer].data_ptr()
+        N.call("hv_expert_ffn_gate_up", w, counts.data_ptr(), offs.data_ptr(), tok.data_ptr(), h.data_ptr(),
+               act.data_ptr(), self.E, H, I, stream)
+        N.call("hv_expert_ffn_down", w, counts.data_ptr(), offs.data_ptr(), act.data_ptr(), y.data_ptr(), self.E,
+               H, I, stream)
+        # top-k combine in a fixed order (deterministic, no atomics)
+        yt = y.index_select(0, pos).view(h.shape[0], self.m.top_k, H)
+        return (yt * probs.unsqueeze(-1)).sum(1).to(h.dtype)
+
+    def _step_fused(self, x: torch.Tensor) -> torch.Tensor:
+        hs = list(x.view(self.nmb, self.tmb, self.H).clone().unbind(0))
+        cur = torch.cuda.current_stream(self.dev)
+        self.compute.wait_stream(cur)
+        handles = [hh for hl in self.layer_handles for hh in hl]
+        batch = self.rt.begin_reads(handles) if (handles and not self._capturing) else None
+        with torch.cuda.stream(self.compute):
+            for s, (layer, mb) in enumerate(self.stages):
+                if self.trace:
+                    cs = torch.cuda.Event(enable_timing=True)
+                    cs.record(self.compute)
+                y = self._ffn_fused(hs[mb], layer)
+                if self.trace:
+                    ce = torch.cuda.Event(enable_timing=True)
+                    ce.record(self.compute)
+                    self._tr.setdefault(s, {})["fused"] = (cs, ce)
+                hs[mb] = hs[mb] + (y * self.residual_scale if self.residual_scale != 1.0 else y)
+        cur.wait_stream(self.compute)
+        done = torch.cuda.Event()
+        done.record(cur)
+        self._addr_done[self._addr_cur] = done
+        if batch is not None:               # the drain completes when the step's reads have
+            self.fetch.wait_stream(cur)
+            self.f.engine.track([lambda _x, b=batch: self.rt.end_reads(b)])
         return torch.stack(hs).view(self.T, self.H)
 
     def overlap_report(self) -> dict:

@@ -171,3 +171,122 @@ def test_graph_replay_equals_eager_and_all_local(microbatches):
     assert verify_release_ordering(sysm.loop.log) == []
     sysm.close()
     sys2.close()
+
+
+# ---------------------------------------------------------------- fused expert FFN (csrc/hv_ffn.cu)
+
+@pytest.mark.parametrize("H,I,counts", [(256, 128, [3, 0, 1, 8, 64, 17]), (2048, 1408, [2, 5, 0, 1, 9, 33]),
+                                        (4096, 6400, [1, 0, 2])])
+def test_fused_ffn_kernels_match_fp32(H, I, counts):
+    """hv_expert_ffn_gate_up / hv_expert_ffn_down against fp32 torch on random
+    bf16 experts, ragged token counts (0 .. 64 per expert), tokens gathered
+    through an arbitrary pair -> row map.  Tolerance: act is rounded to bf16
+    (rel 2^-8) and both GEMVs accumulate in fp32: |err| <= 1e-2 * max|ref|."""
+    from paper_2602_00328_b200 import _native as N
+    g = torch.Generator().manual_seed(H + I)
+    E, T = len(counts), 64
+    S = 3 * H * I * 2
+    W = (torch.randn(E, 3 * H * I, generator=g) * 0.03).to(torch.bfloat16).cuda()
+    x = (torch.randn(T, H, generator=g)).to(torch.bfloat16).cuda()
+    cnt = torch.tensor(counts, dtype=torch.int32)
+    offs = torch.cumsum(cnt, 0, dtype=torch.int32) - cnt
+    P = int(cnt.sum())
+    tok = torch.cat([torch.randperm(T, generator=g)[:c] for c in counts]).to(torch.int32)
+    addr = torch.tensor([W[e].data_ptr() for e in range(E)], dtype=torch.int64).cuda()
+    cnt_d, offs_d, tok_d = cnt.cuda(), offs.cuda(), tok.cuda()
+    act = torch.full((P, I), float("nan"), dtype=torch.bfloat16, device="cuda")
+    y = torch.full((P, H), float("nan"), dtype=torch.float32, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    N.call("hv_expert_ffn_gate_up", addr.data_ptr(), cnt_d.data_ptr(), offs_d.data_ptr(), tok_d.data_ptr(),
+           x.data_ptr(), act.data_ptr(), E, H, I, s)
+    N.call("hv_expert_ffn_down", addr.data_ptr(), cnt_d.data_ptr(), offs_d.data_ptr(), act.data_ptr(),
+           y.data_ptr(), E, H, I, s)
+    torch.cuda.synchronize()
+    Wf, xf = W.float().cpu(), x.float().cpu()
+    for e in range(E):
+        gate, up = Wf[e, :I * H].view(I, H), Wf[e, I * H:2 * I * H].view(I, H)
+        down = Wf[e, 2 * I * H:].view(H, I)
+        for j in range(counts[e]):
+            p = int(offs[e]) + j
+            xt = xf[int(tok[p])]
+            a_ref = torch.nn.functional.silu(gate @ xt) * (up @ xt)
+            a_got = act[p].float().cpu()
+            assert (a_got - a_ref).abs().max() <= 1e-2 * a_ref.abs().max(), (e, j)
+            y_ref = down @ a_got                        # exact bf16 inputs the kernel saw
+            assert (y[p].cpu() - y_ref).abs().max() <= 1e-3 * y_ref.abs().max() + 1e-6, (e, j)
+    assert S == W[0].numel() * 2
+
+
+@pytest.mark.parametrize("microbatches", [1, 2])
+def test_fused_decode_offloaded_equals_all_local(microbatches):
+    """fused=True reads half the experts from the donor pool and half from the
+    pinned host tier in place; outputs are bit-identical to the fused all-local
+    run, and within tolerance of the staged (K2 + cuBLAS) decoder."""
+    from paper_2602_00328_b200.decode import MoEDecoder
+    model = _tiny()
+    L, E = model.num_layers, model.num_experts
+    sysm, store, res, fetcher, dec = _setup(model, peer_experts=L * E // 2, microbatches=microbatches)
+    fdec = MoEDecoder(fetcher, tokens=16, microbatches=microbatches, seed=0, residual_scale=RS, fused=True)
+    out = fdec.decode(3)
+    staged = dec.decode(3)
+    torch.cuda.synchronize()
+    sys2, _dec2, keep = _all_local(model, 16, microbatches, 0, store)
+    ldec = MoEDecoder(_dec2.f, tokens=16, microbatches=microbatches, seed=0, residual_scale=RS, fused=True)
+    out2 = ldec.decode(3)
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int16), out2.view(torch.int16))
+    x0 = fdec.x0.float()
+    d_f, d_s = out.float() - x0, staged.float() - x0
+    assert (d_f - d_s).abs().max() <= 5e-2 * d_s.abs().max()
+    from paper_2602_00328_b200.verify import verify_release_ordering
+    sysm.loop.run()
+    assert verify_release_ordering(sysm.loop.log) == []
+    sysm.close()
+    sys2.close()
+
+
+def test_fused_decode_matches_fp32_reference():
+    from paper_2602_00328_b200.decode import MoEDecoder
+    model = _tiny()
+    sysm, store, res, fetcher, dec = _setup(model, peer_experts=6, microbatches=2)
+    fdec = MoEDecoder(fetcher, tokens=16, microbatches=2, seed=0, residual_scale=RS, fused=True)
+    out = fdec.decode(1)
+    torch.cuda.synchronize()
+    ref = _torch_reference(model, fdec, fdec.x0, 1)
+    x0 = fdec.x0.float().cpu()
+    d_gpu, d_ref = out.float().cpu() - x0, ref - x0
+    scale = d_ref.abs().max().item()
+    err = (d_gpu - d_ref).abs().max().item()
+    assert err <= 5e-2 * scale, (err, scale)      # same tolerance as the staged decoder
+    sysm.loop.run()
+    sysm.close()
+
+
+def test_fused_graph_replay_with_revocation():
+    """Fused step captured as one CUDA graph; revoking every peer expert between
+    replays re-points the captured address table at the host copies (in place);
+    outputs stay bit-identical to the fused all-local eager run, and the
+    drains wait for the replays that read the revoked slabs."""
+    from paper_2602_00328_b200.decode import MoEDecoder
+    from paper_2602_00328_b200.runtime import RevokeReason
+    from paper_2602_00328_b200.verify import verify_release_ordering
+    model = _tiny()
+    sysm, store, res, fetcher, _dec = _setup(model, peer_experts=12, microbatches=2)
+    dec = MoEDecoder(fetcher, tokens=16, microbatches=2, seed=0, residual_scale=RS, fused=True)
+    dec.capture_graph()
+    h = dec.step(dec.x0)
+    h = dec.step(h)
+    for hdl in list(fetcher.handles.values()):
+        sysm.runtime.revoke(hdl, RevokeReason.PRESSURE)
+    sysm.loop.run()
+    assert not fetcher.handles
+    out = dec.step(h).clone()
+    torch.cuda.synchronize()
+    sys2, _dec2, keep = _all_local(model, 16, 2, 0, store)
+    ldec = MoEDecoder(_dec2.f, tokens=16, microbatches=2, seed=0, residual_scale=RS, fused=True)
+    out2 = ldec.decode(3)
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int16), out2.view(torch.int16))
+    assert verify_release_ordering(sysm.loop.log) == []
+    sysm.close()
+    sys2.close()
