@@ -122,6 +122,15 @@ def test_launch_entry_points_validate_arguments_without_a_gpu():
     assert lib.hv_fill_content(0, 0x1000, 0x1000, 1, None) == INV
     assert lib.hv_digest(0x1000, 0x1000, 1, 0, None) == INV
     assert lib.hv_verify_content(0x1000, 0x1000, 0x1000, 1, 0, None) == INV
+    # fused expert FFN: empty launches are no-ops; bad shapes / missing tables are rejected
+    A = 0x1000
+    assert lib.hv_expert_ffn_gate_up(A, A, A, A, A, A, 0, 2048, 1408, None) == N.HV_OK
+    assert lib.hv_expert_ffn_gate_up(A, A, A, 0, A, A, 4, 2048, 1408, None) == INV      # no pair -> row map
+    assert lib.hv_expert_ffn_gate_up(A, A, A, A, A, A, 4, 2048, 1400, None) == INV      # I % 64
+    assert lib.hv_expert_ffn_down(A, A, A, A, A, 4, 2000, 1408, None) == INV            # H % 64
+    assert lib.hv_expert_ffn_down(0, A, A, A, A, 4, 2048, 1408, None) == INV            # no address table
+    assert lib.hv_expert_ffn_down(A, A, A, A, A, 70000, 2048, 1408, None) == INV        # grid.y limit
+    assert N.c_int_out("hv_expert_ffn_max_tokens") == 64
     # the Python layer raises the matching exception type
     with pytest.raises(N.HarvestNativeError) as ei:
         N.call("hv_batch_copy", 0, 0x1000, 0x1000, 2, 0, 0, None)
