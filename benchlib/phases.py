@@ -361,13 +361,13 @@ def phi_phase(world, rank, dev, a, dist, barrier, max_over_ranks, batches=(1, 16
         errors.append(repr(e)[:200])
         fetcher = None
     barrier()
-    for b in batches:
-        dt_local, finite = float("inf"), False
-        dec = None
+    def timed_decode(b, fused):
+        """3 timed steps after 1 warm step; max over ranks (collective-safe)."""
+        dt_local, finite, dec = float("inf"), False, None
         try:
             if fetcher is None:
                 raise RuntimeError("setup failed")
-            dec = MoEDecoder(fetcher, tokens=b, microbatches=1, seed=11)
+            dec = MoEDecoder(fetcher, tokens=b, microbatches=1, seed=11, fused=fused)
             h = dec.decode(1)
             torch.cuda.synchronize()
         except Exception as e:
@@ -386,12 +386,19 @@ def phi_phase(world, rank, dev, a, dist, barrier, max_over_ranks, batches=(1, 16
                 finite = bool(torch.isfinite(h.float()).all())
         except Exception as e:
             errors.append(repr(e)[:200])
-        dt = max_over_ranks(dt_local)
+        del dec
+        torch.cuda.empty_cache()
+        return max_over_ranks(dt_local), finite
+
+    for b in batches:
+        dt, finite = timed_decode(b, False)
         if math.isfinite(dt):
             out[f"batch{b}"] = {"tokens_per_s": b * 3 * world / dt, "per_rank_tokens_per_s": b * 3 / dt,
                                 "ms_per_layer": dt / 3 / L * 1e3, "outputs_finite": finite}
-        del dec
-        torch.cuda.empty_cache()
+        dtf, finite_f = timed_decode(b, True)   # experts consumed in place (hv_expert_ffn_*)
+        if math.isfinite(dtf) and f"batch{b}" in out:
+            out[f"batch{b}"]["fused"] = {"tokens_per_s": b * 3 * world / dtf, "ms_per_layer": dtf / 3 / L * 1e3,
+                                         "outputs_finite": finite_f}
     if sysm is not None:
         sysm.loop.run()
     if rank == 0 and not a.no_host_compare:

@@ -41,6 +41,27 @@ def main():
         ds = F.ptrs_tensor([nb * page] * nb, dev)
         for _ in range(reps):
             F.kv_gather_blocks(sb, ss, db, ds, L, page, engine=eng)
+    elif what == "fused":  # fused expert FFN at the Qwen1.5-MoE stage shape, experts in HBM
+        from paper_2602_00328_b200 import _native as N
+        E, T, k, H, I = 60, 32, 4, 2048, 1408
+        S = 3 * H * I * 2
+        W = (torch.randn(E * S // 2, device=dev) * 0.02).to(torch.bfloat16)
+        h = torch.randn(T, H, device=dev).to(torch.bfloat16)
+        topi = torch.randn(T, E, device=dev).topk(k, dim=1).indices.reshape(-1)
+        order = torch.argsort(topi, stable=True)
+        counts = torch.zeros(E, dtype=torch.int32, device=dev).scatter_add_(0, topi, torch.ones_like(topi, dtype=torch.int32))
+        offs = torch.cumsum(counts, 0, dtype=torch.int32) - counts
+        tok = torch.div(order, k, rounding_mode="floor").to(torch.int32)
+        addr = torch.tensor([W.data_ptr() + e * S for e in range(E)], dtype=torch.int64, device=dev)
+        act = torch.empty(T * k, I, dtype=torch.bfloat16, device=dev)
+        y = torch.empty(T * k, H, dtype=torch.float32, device=dev)
+        s = torch.cuda.current_stream().cuda_stream
+        for _ in range(reps):
+            N.call("hv_expert_ffn_gate_up", addr.data_ptr(), counts.data_ptr(), offs.data_ptr(), tok.data_ptr(),
+                   h.data_ptr(), act.data_ptr(), E, H, I, s)
+            N.call("hv_expert_ffn_down", addr.data_ptr(), counts.data_ptr(), offs.data_ptr(), act.data_ptr(),
+                   y.data_ptr(), E, H, I, s)
+        print("active experts", int((counts > 0).sum()))
     else:  # KV config 1: 1024 pages x 64 KiB from 4096 HBM slots
         page, npg, nslots = 65536, 1024, 4096
         slots = torch.empty(nslots * page, dtype=torch.uint8, device=dev)
