@@ -312,6 +312,9 @@ def run_b200(a):
         decode["host_offload"] = host_offload_decode(m, dev, a)
         decode["speedup_vs_host_offload_per_gpu"] = (decode["per_rank_tokens_per_s"]
                                                      / decode["host_offload"]["tokens_per_s"])
+        if "best" in decode:
+            decode["best"]["speedup_vs_host_offload_per_gpu"] = (decode["best"]["tokens_per_s"] / world
+                                                                 / decode["host_offload"]["tokens_per_s"])
     barrier()
 
     if rank == 0:
