@@ -13,12 +13,19 @@
 // kernels are built like the fetch kernels: deep cp.async (16-byte LDGSTS)
 // pipelines keep tens of KiB per SM in flight, and the tensor cores
 // (mma.sync m16n8k16 bf16 -> fp32) only have to keep up with the link.
-// Tile shape, measured on B200 with experts in local HBM (tools/fused_probe.py,
-// weight GB/s of the activated experts, Qwen1.5-MoE stage / Phi-3.5 batch 16):
-//   k-tile 128 x 4 stages (192 KiB smem, 1 CTA/SM): 3,365 / 3,673
-//   k-tile  64 x 4 stages ( 96 KiB smem, 2 CTAs/SM): 4,667 / 4,967   <- default
-//   k-tile  64 x 6 stages: 3,480 / 3,742;  k-tile 32 x 8 stages: 3,786 / 4,141
-// Two resident CTAs per SM hide each other's pipeline fill and drain.
+// Tile shape and schedule, measured on B200 with experts in local HBM
+// (tools/fused_probe.py, weight GB/s of the activated experts, Qwen1.5-MoE
+// stage / Phi-3.5 batch 16 / batch 1):
+//   one CTA per (row block, expert):
+//     k-tile 128 x 4 stages (192 KiB smem, 1 CTA/SM): 3,365 / 3,673 / 2,754
+//     k-tile  64 x 4 stages ( 96 KiB smem, 2 CTAs/SM): 4,667 / 4,967 / 2,767
+//     k-tile  64 x 6 stages: 3,480 / 3,742;  k-tile 32 x 8 stages: 3,786 / 4,141
+//   persistent (SMs x resident CTAs walking the items, ring across items):
+//     k-tile  64 x 4 stages: 4,554 / 4,549 / 1,718
+//     k-tile  64 x 3 stages ( 72 KiB smem, 3 CTAs/SM): 4,925 / 5,110 / 2,999  <- default
+//     k-tile 128 x 3 stages: 3,424 / 3,462 / 2,267
+// More resident CTAs per SM hide each other's stalls; the persistent ring
+// removes the per-item pipeline fill and drain.
 //
 // Layout of an expert object (the same one K2 moves): gate [I][H], up [I][H],
 // down [H][I], bf16, row-major.  Routed (token, expert) pairs are sorted by
@@ -39,8 +46,11 @@ constexpr int kRows = 16 * kWarps;   // weight rows per CTA (16 per warp: one mm
 #ifndef HV_FFN_KT
 #define HV_FFN_KT 64
 #endif
+#ifndef HV_FFN_PERSISTENT
+#define HV_FFN_PERSISTENT 1
+#endif
 #ifndef HV_FFN_STAGES
-#define HV_FFN_STAGES 4
+#define HV_FFN_STAGES 3
 #endif
 constexpr int kKT = HV_FFN_KT;       // k columns per pipeline stage (64: 128 B per row)
 constexpr int kRowBytes = kKT * 2;
@@ -217,6 +227,160 @@ __global__ void __launch_bounds__(kThreads) expert_ffn_kernel(FfnArgs a) {
   }
 }
 
+// Persistent form: a grid of (SMs x resident CTAs) walks the work items
+// (expert e, row block rb), item = e * RB + rb, round-robin.  The cp.async
+// ring runs across item boundaries: while the last k-tiles of one item are
+// multiplied, the first tiles of the next are already in flight, so no CTA
+// pays a pipeline fill/drain per item.  Items of experts without routed
+// tokens are skipped.
+struct ItemCursor {
+  int item, kt, n, p0, row0;
+  const char* w0;
+  const char* w1;
+};
+
+template <int NMAT>
+__device__ __forceinline__ void cursor_seek(ItemCursor& c, const FfnArgs& a, int rb_count, int n_items) {
+  while (c.item < n_items) {
+    const int e = c.item / rb_count;
+    const int n = a.counts[e];
+    if (n > 0) {
+      c.n = n < kMaxTok ? n : kMaxTok;
+      c.p0 = a.offs[e];
+      c.row0 = (c.item - e * rb_count) * kRows;
+      const char* obj = reinterpret_cast<const char*>(a.w_addr[e]);
+      c.w0 = obj + a.w_off0 + (size_t)c.row0 * a.K * 2;
+      c.w1 = obj + a.w_off1 + (size_t)c.row0 * a.K * 2;
+      c.kt = 0;
+      return;
+    }
+    c.item += gridDim.x;
+  }
+}
+
+template <int NMAT>
+__global__ void __launch_bounds__(kThreads) expert_ffn_persistent(FfnArgs a, int n_items) {
+  extern __shared__ __align__(128) char smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rb_count = a.rows / kRows;
+  const int ktiles = a.K / kKT;
+  const size_t wstride = (size_t)a.K * 2, xstride = (size_t)a.K * 2;
+  // every activation row of every stage starts finite; later stale rows are
+  // earlier activations (finite) and only feed output columns that are dropped
+  for (int i = tid; i < kStages * Smem<NMAT>::kX / 16; i += kThreads) {
+    const int s = i / (Smem<NMAT>::kX / 16), o = i % (Smem<NMAT>::kX / 16);
+    *reinterpret_cast<uint4*>(smem + s * Smem<NMAT>::kStage + Smem<NMAT>::kW + o * 16) = make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+
+  ItemCursor ld{(int)blockIdx.x, 0, 0, 0, 0, nullptr, nullptr};
+  cursor_seek<NMAT>(ld, a, rb_count, n_items);
+  ItemCursor cs = ld;
+  auto advance = [&](ItemCursor& c) {
+    if (++c.kt == ktiles) {
+      c.item += gridDim.x;
+      cursor_seek<NMAT>(c, a, rb_count, n_items);
+    }
+  };
+  auto load_stage = [&](const ItemCursor& c, int s) {
+    char* base = smem + s * Smem<NMAT>::kStage;
+    const size_t kb = (size_t)c.kt * kRowBytes;
+#pragma unroll
+    for (int m = 0; m < NMAT; ++m) {
+      const uint32_t ws = smem_u32(base + m * kRows * kRowBytes);
+      const char* src = m == 0 ? c.w0 : c.w1;
+#pragma unroll 4
+      for (int i = tid; i < kRows * kChunksPerRow; i += kThreads) {
+        const int r = i / kChunksPerRow, ch = i % kChunksPerRow;
+        cp_async16(ws + swz(r, ch), src + r * wstride + kb + ch * 16);
+      }
+    }
+    const uint32_t xs = smem_u32(base + Smem<NMAT>::kW);
+    for (int i = tid; i < c.n * kChunksPerRow; i += kThreads) {
+      const int r = i / kChunksPerRow, ch = i % kChunksPerRow;
+      const int row = a.tok ? a.tok[c.p0 + r] : c.p0 + r;
+      cp_async16(xs + swz(r, ch), reinterpret_cast<const char*>(a.x) + row * xstride + kb + ch * 16);
+    }
+  };
+
+  float acc[NMAT][kGroups][4];
+#pragma unroll
+  for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+    for (int g = 0; g < kGroups; ++g)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[m][g][j] = 0.f;
+
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (ld.item < n_items) {
+      load_stage(ld, s);
+      advance(ld);
+    }
+    cp_commit();
+  }
+  const int a_row = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+  const int a_kc = lane >> 4;
+  const int b_row = lane & 7;
+  const int b_kc = (lane >> 3) & 1;
+  int stage = 0, lstage = kStages - 1;
+  while (cs.item < n_items) {
+    cp_wait<kStages - 2>();
+    __syncthreads();
+    if (ld.item < n_items) {
+      load_stage(ld, lstage);
+      advance(ld);
+    }
+    cp_commit();
+    lstage = lstage + 1 == kStages ? 0 : lstage + 1;
+    const char* base = smem + stage * Smem<NMAT>::kStage;
+    const uint32_t xs = smem_u32(base + Smem<NMAT>::kW);
+    const int ng = (cs.n + 7) >> 3;
+#pragma unroll
+    for (int kk = 0; kk < kKT / 16; ++kk) {
+      uint32_t af[NMAT][4];
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m)
+        ldsm_x4(smem_u32(base + m * kRows * kRowBytes) + swz(a_row, kk * 2 + a_kc), af[m][0], af[m][1], af[m][2],
+                af[m][3]);
+#pragma unroll
+      for (int g = 0; g < kGroups; ++g) {
+        if (g < ng) {
+          uint32_t b0, b1;
+          ldsm_x2(xs + swz(g * 8 + b_row, kk * 2 + b_kc), b0, b1);
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m) mma_bf16(acc[m][g], af[m][0], af[m][1], af[m][2], af[m][3], b0, b1);
+        }
+      }
+    }
+    stage = stage + 1 == kStages ? 0 : stage + 1;
+    if (cs.kt == ktiles - 1) {  // item complete: epilogue, then the next item's tiles are already in flight
+      const int r = cs.row0 + warp * 16 + (lane >> 2);
+      const int c2 = (lane & 3) * 2;
+#pragma unroll
+      for (int g = 0; g < kGroups; ++g) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int t = g * 8 + c2 + (j & 1);
+          if (g < ng && t < cs.n) {
+            const size_t o = (size_t)(cs.p0 + t) * a.rows + r + (j >> 1) * 8;
+            if constexpr (NMAT == 2) {
+              const float gv = acc[0][g][j], uv = acc[1][g][j];
+              reinterpret_cast<__nv_bfloat16*>(a.out)[o] = __float2bfloat16_rn(gv / (1.f + __expf(-gv)) * uv);
+            } else {
+              reinterpret_cast<float*>(a.out)[o] = acc[0][g][j];
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m) acc[m][g][j] = 0.f;
+        }
+      }
+    }
+    advance(cs);
+  }
+  cp_wait<0>();
+}
+
 template <int NMAT>
 int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
   if (n_experts == 0) return HV_OK;
@@ -233,8 +397,24 @@ int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
                                  Smem<NMAT>::kTotal));
     attr_set[dev] = true;
   }
+#if HV_FFN_PERSISTENT
+  static int resident[64] = {};
+  if (dev >= 0 && dev < 64 && !resident[dev]) {
+    int r = 0;
+    HV_CUDA(cudaFuncSetAttribute(expert_ffn_persistent<NMAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Smem<NMAT>::kTotal));
+    HV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, expert_ffn_persistent<NMAT>, kThreads,
+                                                          Smem<NMAT>::kTotal));
+    resident[dev] = r > 0 ? r : 1;
+  }
+  const int n_items = (int)(a.rows / kRows) * (int)n_experts;
+  int g = hv::sm_count(dev) * (dev >= 0 && dev < 64 ? resident[dev] : 1);
+  if (g > n_items) g = n_items;
+  expert_ffn_persistent<NMAT><<<g, kThreads, Smem<NMAT>::kTotal, (cudaStream_t)stream>>>(a, n_items);
+#else
   dim3 grid(a.rows / kRows, n_experts);
   expert_ffn_kernel<NMAT><<<grid, kThreads, Smem<NMAT>::kTotal, (cudaStream_t)stream>>>(a);
+#endif
   HV_CUDA(cudaGetLastError());
   hv::note_launch();
   return HV_OK;
