@@ -77,6 +77,8 @@ def run_b200(a):
     from paper_2602_00328_b200.pool import HostTier, PeerPool
     from paper_2602_00328_b200.system import HarvestSystem
     from tools.clocks import ClockSampler
+    from tools.nvlink_counters import NvlinkCounters
+    from tools.nvlink_counters import delta as nvlink_delta
 
     world = a.gpus
     rank = int(os.environ.get("RANK", "0"))
@@ -203,14 +205,19 @@ def run_b200(a):
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     remeasured = None
+    nvl = NvlinkCounters(dev)
     for attempt in range(2):
         with ClockSampler(dev) as clk:
+            nv0 = nvl.snapshot()
             t0.record(stream)
             for k in range(a.steps):
                 value_step(a.warmup + k, step_events[k])
             t1.record(stream)
             t1.synchronize()
+            nv1 = nvl.snapshot()
         torch.cuda.synchronize()
+        # hardware NVLink byte counters of this GPU over the timed region
+        nvlink = nvlink_delta(nv0, nv1, t0.elapsed_time(t1) * 1e-3)
         bad = clk.summary().get("rejected", False)
         bad = group.any(bad)  # every rank re-measures if any rank saw a bad reason
         if not bad:
@@ -275,6 +282,7 @@ def run_b200(a):
     e2e_dt = max_over_ranks(max(wall, e0.elapsed_time(e1) * 1e-3))
     e2e_value = total_bytes / e2e_dt / 1e9
     mism_all = max_over_ranks(float(mism))
+    nvlink_all = group.all_gather(nvlink)
 
     # ---- MoE decode tokens/s through the pipelined decoder (moe.py:211-340)
     del desc
@@ -367,7 +375,12 @@ def run_b200(a):
                 "latency_ms_per_layer_fetch_dist": {"p50": float(np.percentile(launch_ms, 50)),
                                                     "p99": float(np.percentile(launch_ms, 99)),
                                                     "n": len(launch_ms)}, "decode": decode,
-                "kv_long_context_128k": kvlc, "reference_simulator": refsim, **extra}
+                "kv_long_context_128k": kvlc, "reference_simulator": refsim,
+                "nvlink_counters_timed_region": {
+                    "per_rank": nvlink_all,
+                    "note": "NVML per-link NVLink data counters of each rank's GPU, read before/after the timed "
+                            "fetch steps (rx = bytes this GPU pulled from donors, tx = bytes it served)"},
+                **extra}
     barrier()
     sysm.close()
     for p in imported:
