@@ -36,7 +36,8 @@ class NvlinkCounters:
                     self.links = vals[2]
                     break
             if self.family is None:
-                self.error = "no NVLink counter family readable on this GPU"
+                self.error = (f"NVLink byte counters not readable on this GPU (NVML return {self._last_ret} on "
+                              f"{nv.nvmlDeviceGetFieldValues.__name__}; 3 = NOT_SUPPORTED)")
         except Exception as e:  # NVML missing or unsupported
             self.error = repr(e)[:200]
 
@@ -45,12 +46,14 @@ class NvlinkCounters:
         _name, rx_id, tx_id, scale = fam
         rx = tx = 0
         links = 0
+        self._last_ret = None
         for link in range(MAX_LINKS):
             try:
                 r = nv.nvmlDeviceGetFieldValues(self._h, [(rx_id, link), (tx_id, link)])
             except Exception:
                 continue
             if r[0].nvmlReturn != 0 or r[1].nvmlReturn != 0:
+                self._last_ret = r[0].nvmlReturn or r[1].nvmlReturn
                 continue
             rx += _value(r[0]) * scale
             tx += _value(r[1]) * scale
