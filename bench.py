@@ -39,7 +39,8 @@ sys.path.insert(0, REPO)
 from benchlib.common import (KV_SLAB_BLOCKS, KV_TOKENS, METRIC, SEED, emit, kv_slab_bytes, load_traffic, model, routing, workload_config)  # noqa: E402
 from benchlib.compare import (autotune, measure_pcie_h2d, probe_engines_on_peer, same_run_comparisons)  # noqa: E402
 from benchlib.cpu import (cpu_gather_sample, cpu_host_copy, cpu_model, reference_simulator, run_reference)  # noqa: E402
-from benchlib.phases import (churn_phase, host_offload_decode, kv_long_context, phi_phase, run_decode)  # noqa: E402
+from benchlib.phases import (churn_phase, host_offload_decode, kv_decode_config1, kv_long_context, phi_phase,  # noqa: E402
+                             run_decode)
 
 
 def parse():
@@ -312,7 +313,12 @@ def run_b200(a):
         decode["best"] = {"mode": best, "tokens_per_s": modes[best]}
     sysm.loop.run()
     kvlc = None
+    kvd1 = None
     if not a.no_kv:
+        try:
+            kvd1 = kv_decode_config1(sysm, source, a)
+        except Exception as e:  # report, never lose the line
+            kvd1 = {"error": repr(e)[:300]}
         kvlc = kv_long_context(sysm, source, a)
         kvlc["reload_kernel_GBps_all_ranks_min"] = -max_over_ranks(-kvlc["reload_kernel_GBps"])
     barrier()
@@ -375,7 +381,7 @@ def run_b200(a):
                 "latency_ms_per_layer_fetch_dist": {"p50": float(np.percentile(launch_ms, 50)),
                                                     "p99": float(np.percentile(launch_ms, 99)),
                                                     "n": len(launch_ms)}, "decode": decode,
-                "kv_long_context_128k": kvlc, "reference_simulator": refsim,
+                "kv_long_context_128k": kvlc, "kv_decode_config1": kvd1, "reference_simulator": refsim,
                 "nvlink_counters_timed_region": {
                     "per_rank": nvlink_all,
                     "note": "NVML per-link NVLink data counters of each rank's GPU, read before/after the timed "

@@ -94,7 +94,7 @@ def kv_long_context(sysm, source, a):
     host = source == "host"
     kv = KVCacheManager(sysm, m, local_blocks=nblk, host_blocks=nblk if host else 1, slab_blocks=KV_SLAB_BLOCKS,
                         durability=Durability.BACKED if host else Durability.LOSSY, engine=a.engine,
-                        max_ctas=a.max_ctas)
+                        max_ctas=a.max_ctas, content="fp16")
     kv.append_kv(0, KV_TOKENS)
     t0 = time.perf_counter()
     kv.timing = []
@@ -118,13 +118,79 @@ def kv_long_context(sysm, source, a):
     sample = [(int(l), int(b)) for l, b in zip(rng.integers(0, m.num_layers, 64), rng.integers(0, nblk, 64))]
     ptrs = [kv.cache[l, kv.table[b].slot].data_ptr() for l, b in sample]
     bad = F.verify_content(F.ptrs_tensor(ptrs, kv.dev), F.ptrs_tensor([m.page_bytes] * len(ptrs), kv.dev),
-                           [kv_seed(l, 0, kv.table[b].index) for l, b in sample])
+                           [kv_seed(l, 0, kv.table[b].index) for l, b in sample], weights=True)
     out = {"sequence_tokens": KV_TOKENS, "blocks": nblk, "pages": nblk * m.num_layers, "bytes": nb,
            "evicted_to": where, "reload_from": {k: len(v) for k, v in plan.items()},
            "reload_kernel_ms": ms, "reload_launches": len(kv.timing), "reload_kernel_GBps": nb / (ms * 1e-3) / 1e9,
            "reload_e2e_ms": wall * 1e3, "evict_kernel_ms": e_ev0.elapsed_time(e_ev1),
            "evict_e2e_ms": evict_wall * 1e3, "sampled_pages_mismatched_words": int(bad.sum()),
            "model": "llama-3-8b: 32 layers x 8 KV heads x 128 x fp16, 16-token blocks"}
+    # decode attention over the whole 128k context, KV local vs in the tier
+    out["decode_attention"] = _kv_decode_measure(kv, [0], sysm, steps=2)
+    kv.close()
+    return out
+
+
+def _kv_decode_measure(kv, seqs, sysm, steps=3, q_heads=32):
+    """KVAttentionDecoder over the given sequences: one timed run with every
+    block local, then everything evicted to the tier (peer slabs at N>1, host
+    at N=1) and the same steps again; the tiered outputs must equal the
+    all-local ones bit for bit."""
+    import torch
+    from paper_2602_00328_b200.kv_decode import KVAttentionDecoder
+    dec = KVAttentionDecoder(kv, seqs, q_heads=q_heads, seed=1)
+
+    def timed():
+        o = dec.step()
+        torch.cuda.synchronize()
+        cur = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cur)
+        for _ in range(steps):
+            o = dec.step()
+        e1.record(cur)
+        e1.synchronize()
+        return o, e0.elapsed_time(e1) / steps
+
+    local_out, local_ms = timed()
+    local_out = local_out.clone()
+    moves = kv.evict(len(dec.ids) * kv.m.block_bytes)
+    where = {}
+    for _bid, _frm, to in moves:
+        where[to] = where.get(to, 0) + 1
+    tier_out, tier_ms = timed()
+    dec.trace = True
+    dec.step()
+    ov = dec.overlap_report()
+    sysm.loop.run()
+    nbytes = len(dec.ids) * kv.m.block_bytes
+    return {"batch": len(seqs), "context_tokens": dec.T, "kv_bytes_per_step": nbytes, "kv_in": where,
+            "tier_ms_per_step": tier_ms, "tier_tokens_per_s": len(seqs) / (tier_ms * 1e-3),
+            "tier_kv_GBps": nbytes / (tier_ms * 1e-3) / 1e9,
+            "local_ms_per_step": local_ms, "local_tokens_per_s": len(seqs) / (local_ms * 1e-3),
+            "outputs_bit_identical_to_all_local": bool(torch.equal(tier_out.view(torch.int16),
+                                                                   local_out.view(torch.int16))),
+            "outputs_finite": bool(torch.isfinite(tier_out.float()).all()),
+            "overlap_traced_step": ov,
+            "model": f"{kv.m.name}: GQA {q_heads} q heads over {kv.m.kv_heads} KV heads, per-layer K1 gather "
+                     "(fetch stream) overlapped with attention (compute stream)"}
+
+
+def kv_decode_config1(sysm, source, a, batch=4, context=4096):
+    """BASELINE configs[0] shape on the GPU: 4 sequences x 4k tokens of
+    Llama-3-8B-shaped KV (1,024 blocks, 2 GiB), decode attention with the
+    KV in local HBM and then in the tier (peer slabs at N>1, host at N=1)."""
+    from paper_2602_00328_b200.kv import LLAMA3_8B, KVCacheManager
+    from paper_2602_00328_b200.runtime import Durability
+    m = LLAMA3_8B
+    nblk = batch * context // m.block_tokens
+    host = source == "host"
+    kv = KVCacheManager(sysm, m, local_blocks=nblk, host_blocks=nblk if host else 1, slab_blocks=KV_SLAB_BLOCKS,
+                        durability=Durability.BACKED if host else Durability.LOSSY, engine=a.engine,
+                        max_ctas=a.max_ctas, content="fp16")
+    for s in range(batch):
+        kv.append_kv(s, context)
+    out = _kv_decode_measure(kv, list(range(batch)), sysm)
     kv.close()
     return out
 

@@ -136,9 +136,15 @@ class KVCacheManager:
     def __init__(self, system, model: KVModelSpec, local_blocks: int, host_blocks: int,
                  policy: OffloadPolicy | None = None, slab_blocks: int = 32,
                  durability: Durability = Durability.LOSSY, engine: str = "auto", max_ctas: int = 0,
-                 spread: bool = True):
+                 spread: bool = True, content: str = "raw"):
         self.sys = system
         self.spread = spread
+        # page content: "raw" splitmix bytes, or "fp16" -- the same keyed stream
+        # with every 16-bit lane mapped to a finite fp16 value (+-[1, 1.125)),
+        # for consumers that compute on the KV (kv_decode)
+        if content not in ("raw", "fp16"):
+            raise ValueError("content must be 'raw' or 'fp16'")
+        self.content = content
         self.rt = system.runtime
         self.m = model
         self.policy = policy or OffloadPolicy()
@@ -271,7 +277,8 @@ class KVCacheManager:
                 seeds.append(kv_seed(layer, b.sequence_id, b.index))
         from . import fetch as F
         torch.cuda.synchronize(self.sys.compute)  # slots may be targets of pending copies
-        F.fill_content(F.ptrs_tensor(ptrs, self.dev), F.ptrs_tensor([self.page] * len(ptrs), self.dev), seeds)
+        fill = F.fill_weights_bf16 if self.content == "fp16" else F.fill_content
+        fill(F.ptrs_tensor(ptrs, self.dev), F.ptrs_tensor([self.page] * len(ptrs), self.dev), seeds)
         torch.cuda.synchronize(self.sys.compute)
 
     def _local_used(self) -> int:
@@ -530,6 +537,23 @@ class KVCacheManager:
         ev = torch.cuda.Event()
         ev.record(torch.cuda.ExternalStream(s, device=self.dev))
         self._staged.append((ev, pinned, d_src))   # alive until the gather that reads them is done
+
+    def page_table(self, block_ids) -> tuple[np.ndarray, np.ndarray, list]:
+        """Where every listed block's pages are right now: page (l, b) is at
+        base[b] + l * stride[b] in the block's resident tier (local, peer slab
+        or host).  Also returns the live peer-slab handles those pages are read
+        from, for the reader's drain set.  Blocks must be materialized."""
+        n = len(block_ids)
+        bases = np.empty(n, dtype=np.uint64)
+        strides = np.empty(n, dtype=np.uint64)
+        handles = {}
+        for i, bid in enumerate(block_ids):
+            b = self.table[bid]
+            bases[i], strides[i] = self._page_base(b)
+            if b.tier == KVTier.PEER_HBM:
+                h = self.slabs[b.slab].handle
+                handles[h.key()] = h
+        return bases, strides, list(handles.values())
 
     def _stage_u64(self, arr: np.ndarray, stream: int) -> tuple[torch.Tensor, torch.Tensor]:
         """Upload a host u64 array through pinned memory on `stream`; the

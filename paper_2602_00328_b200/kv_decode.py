@@ -1,0 +1,149 @@
+"""Decode attention over a paged KV cache whose blocks live in any Harvest tier.
+
+The reference's KV module stops at moving blocks: reload
+brings them back to local HBM, and the paper's KV experiment (Fig 7,
+SPEC.md:426-434) reports the reload latency alone.  This is the consumer that
+turns K1 into decode tokens/s: for every layer, K1 gathers that layer's page
+of every block of every sequence -- from local HBM, a donor's slab over
+NVLink, or the pinned host tier -- into a contiguous double buffer on the
+fetch stream, and grouped-query attention for that layer runs on the compute
+stream while the next layer's gather is in flight.
+
+Unlike the MoE stage (routing of layer l+1 needs layer l's output), the KV
+pages of every layer are known before the step starts, so the gathers run
+ahead of the attention, bounded only by the two buffers: the step takes
+max(sum of gathers, sum of attention) plus one stage.
+
+Per step the block table is resolved once on the host
+(KVCacheManager.page_table) and uploaded once; the per-layer source arrays
+are one device-side broadcast, so each layer costs one K1 launch and no host
+work.  The peer slabs read by the step form its drain set (begin_reads
+before, the step's CUDA event after), so a revocation mid-step waits for the
+gathers that read the slab.
+
+Page layout (one layer of one 16-token block): K [16][kv_heads][head_dim]
+then V [16][kv_heads][head_dim], fp16.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.nn.functional as TF
+
+from . import _native as N
+from . import fetch as F
+
+
+class KVAttentionDecoder:
+    def __init__(self, kv, sequences, q_heads: int, tokens: int | None = None, seed: int = 0,
+                 engine: str | None = None, max_ctas: int | None = None, trace: bool = False):
+        """``sequences``: sequence ids of the batch, all with the same token
+        count (``tokens``, default: the first sequence's).  Queries are
+        synthetic: one random fp16 query per (layer, sequence, q head)."""
+        m = kv.m
+        if q_heads % m.kv_heads:
+            raise ValueError("q_heads must be a multiple of kv_heads (grouped-query attention)")
+        self.kv, self.m = kv, m
+        self.seqs = list(sequences)
+        self.B, self.L, self.Hq = len(self.seqs), m.num_layers, q_heads
+        blocks = [kv.seq_blocks[s] for s in self.seqs]
+        self.nb = len(blocks[0])
+        if any(len(b) != self.nb for b in blocks):
+            raise ValueError("all sequences of the batch need the same number of blocks")
+        full = self.nb * m.block_tokens
+        last = kv.table[blocks[0][-1]].entries
+        self.T = tokens if tokens is not None else full - m.block_tokens + last
+        self.ids = [bid for b in blocks for bid in b]            # sequence-major block order
+        self.dev = torch.device(kv.dev)
+        self.engine = engine if engine is not None else kv.engine
+        self.max_ctas = kv.max_ctas if max_ctas is None else max_ctas
+        self.page = m.page_bytes
+        n = len(self.ids)
+        self.bufs = [torch.empty(n * self.page, dtype=torch.uint8, device=self.dev) for _ in range(2)]
+        g = torch.Generator().manual_seed(seed)
+        self.q = (torch.randn(self.L, self.B, q_heads, 1, m.head_dim, generator=g)).to(torch.float16).to(self.dev)
+        self.fetch_h = kv.stream
+        self.fetch = torch.cuda.ExternalStream(kv.stream, device=self.dev)
+        self.compute = torch.cuda.Stream(self.dev)
+        self.trace = trace
+        self._tr: dict = {}
+        self._keep: list = []
+
+    def _sources(self) -> tuple[torch.Tensor, list]:
+        """[L, n] page addresses of this step (one upload, one broadcast)."""
+        bases, strides, handles = self.kv.page_table(self.ids)
+        tab = torch.from_numpy(np.stack([bases, strides]).view(np.int64)).pin_memory()
+        d = torch.empty(tab.shape, dtype=torch.int64, device=self.dev)
+        N.call("hv_memcpy_h2d", d.data_ptr(), tab.data_ptr(), tab.numel() * 8, self.fetch_h)
+        layers = torch.arange(self.L, dtype=torch.int64, device=self.dev).unsqueeze(1)
+        with torch.cuda.stream(self.fetch):
+            src = d[0].unsqueeze(0) + layers * d[1].unsqueeze(0)
+        self._keep = (self._keep + [(tab, d)])[-2:]   # the last two steps' uploads stay alive
+        return src, handles
+
+    def _attend(self, layer: int, buf: torch.Tensor) -> torch.Tensor:
+        m = self.m
+        pages = buf.view(torch.float16).view(self.B, self.nb, 2, m.block_tokens, m.kv_heads, m.head_dim)
+        k = pages[:, :, 0].reshape(self.B, self.nb * m.block_tokens, m.kv_heads, m.head_dim)[:, :self.T]
+        v = pages[:, :, 1].reshape(self.B, self.nb * m.block_tokens, m.kv_heads, m.head_dim)[:, :self.T]
+        return TF.scaled_dot_product_attention(self.q[layer], k.transpose(1, 2), v.transpose(1, 2),
+                                               enable_gqa=True)                 # [B, Hq, 1, D]
+
+    def step(self) -> torch.Tensor:
+        """One decode step over all layers: returns the attention outputs [L, B, Hq, D]."""
+        rt = self.kv.rt
+        from .kv import KVTier
+        lost = [bid for bid in self.ids if self.kv.table[bid].tier is KVTier.NOT_MATERIALIZED]
+        if lost:                            # Lossy blocks revoked since the last step: recompute
+            self.kv.reload(lost)
+        cur = torch.cuda.current_stream(self.dev)
+        self.fetch.wait_stream(cur)
+        self.compute.wait_stream(cur)
+        src, handles = self._sources()
+        batch = rt.begin_reads(handles) if handles else None
+        outs = [None] * self.L
+        consumed = [None, None]
+        for layer in range(self.L):
+            b = layer % 2
+            if consumed[b] is not None:
+                self.fetch.wait_event(consumed[b])
+            if self.trace:
+                f0 = torch.cuda.Event(enable_timing=True)
+                f0.record(self.fetch)
+            F.kv_gather(src[layer], self.page, dst=self.bufs[b], engine=self.engine, max_ctas=self.max_ctas,
+                        stream=self.fetch_h)
+            got = torch.cuda.Event(enable_timing=self.trace)
+            got.record(self.fetch)
+            with torch.cuda.stream(self.compute):
+                self.compute.wait_event(got)
+                if self.trace:
+                    c0 = torch.cuda.Event(enable_timing=True)
+                    c0.record(self.compute)
+                outs[layer] = self._attend(layer, self.bufs[b])
+                done = torch.cuda.Event(enable_timing=self.trace)
+                done.record(self.compute)
+                consumed[b] = done
+            if self.trace:
+                self._tr[layer] = {"fetch": (f0, got), "compute": (c0, done)}
+        cur.wait_stream(self.compute)
+        cur.wait_stream(self.fetch)
+        if batch is not None:               # drain completes when the step's gathers have
+            fin = torch.cuda.Event()
+            fin.record(cur)
+            self.fetch.wait_event(fin)
+            self.kv.sys.engine.track([lambda _x, bt=batch: rt.end_reads(bt)])
+        return torch.stack([o.squeeze(2) for o in outs])
+
+    def overlap_report(self) -> dict:
+        """Device-clock gather / attention intervals of the last traced step."""
+        torch.cuda.synchronize(self.dev)
+        if not self._tr:
+            return {}
+        base = self._tr[0]["fetch"][0]
+        iv = {l: {k: (base.elapsed_time(a), base.elapsed_time(b)) for k, (a, b) in v.items()}
+              for l, v in self._tr.items()}
+        fetch_ms = sum(v["fetch"][1] - v["fetch"][0] for v in iv.values())
+        comp_ms = sum(v["compute"][1] - v["compute"][0] for v in iv.values())
+        span = max(v["compute"][1] for v in iv.values())
+        return {"layers": len(iv), "gather_ms": fetch_ms, "attention_ms": comp_ms, "span_ms": span,
+                "serial_ms": fetch_ms + comp_ms}
