@@ -140,7 +140,7 @@ def _kv_decode_measure(kv, seqs, sysm, steps=3, q_heads=32):
     from paper_2602_00328_b200.kv_decode import KVAttentionDecoder
     dec = KVAttentionDecoder(kv, seqs, q_heads=q_heads, seed=1)
 
-    def timed():
+    def timed(dec=dec):
         o = dec.step()
         torch.cuda.synchronize()
         cur = torch.cuda.current_stream()
@@ -154,6 +154,8 @@ def _kv_decode_measure(kv, seqs, sysm, steps=3, q_heads=32):
 
     local_out, local_ms = timed()
     local_out = local_out.clone()
+    kv.sys.engine.synchronize()
+    sysm.loop.run()          # slabs emptied by an earlier reload go back to their donors first
     moves = kv.evict(len(dec.ids) * kv.m.block_bytes)
     where = {}
     for _bid, _frm, to in moves:
@@ -162,6 +164,9 @@ def _kv_decode_measure(kv, seqs, sysm, steps=3, q_heads=32):
     dec.trace = True
     dec.step()
     ov = dec.overlap_report()
+    # the same attention straight over the resident pages (no K1 gather)
+    fdec = KVAttentionDecoder(kv, seqs, q_heads=q_heads, seed=1, fused=True)
+    fused_out, fused_ms = timed(fdec)
     sysm.loop.run()
     nbytes = len(dec.ids) * kv.m.block_bytes
     return {"batch": len(seqs), "context_tokens": dec.T, "kv_bytes_per_step": nbytes, "kv_in": where,
@@ -171,6 +176,10 @@ def _kv_decode_measure(kv, seqs, sysm, steps=3, q_heads=32):
             "outputs_bit_identical_to_all_local": bool(torch.equal(tier_out.view(torch.int16),
                                                                    local_out.view(torch.int16))),
             "outputs_finite": bool(torch.isfinite(tier_out.float()).all()),
+            "fused_in_place": {"ms_per_step": fused_ms, "tokens_per_s": len(seqs) / (fused_ms * 1e-3),
+                               "kv_GBps": nbytes / (fused_ms * 1e-3) / 1e9,
+                               "outputs_bit_identical_to_gathered": bool(torch.equal(fused_out, tier_out))},
+            "attention": "hv_paged_decode_attention (split-K flash decoding over page pointers)",
             "overlap_traced_step": ov,
             "model": f"{kv.m.name}: GQA {q_heads} q heads over {kv.m.kv_heads} KV heads, per-layer K1 gather "
                      "(fetch stream) overlapped with attention (compute stream)"}

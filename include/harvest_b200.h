@@ -232,6 +232,22 @@ int hv_expert_ffn_down(const uint64_t* d_w_addr, const int32_t* d_counts, const 
                        uint32_t intermediate, void* stream);
 int hv_expert_ffn_max_tokens(int* out);
 
+/* ---- paged decode attention over KV pages in any tier -------------------- */
+/* One query token per sequence, grouped-query (q_heads = g * kv_heads,
+ * g in {1, 2, 4, 8}), head_dim 64 or 128, 16-token blocks.  d_page_ptrs holds
+ * one page pointer per block (this layer), sequence-major; sequence b owns
+ * blocks d_seq_start[b] .. d_seq_start[b+1]-1 and d_seq_tokens[b] tokens.
+ * Page layout: K [16][kv_heads][D] then V [16][kv_heads][D], fp16.  Pages
+ * may be a K1-gathered buffer or the pages in place (local, peer, host).
+ * d_q: [batch][q_heads][D] fp16; d_out: [batch][q_heads][D] fp32;
+ * d_part: workspace of batch*kv_heads*splits*g*(D+2) floats.  Flash-decoding
+ * over `splits` block ranges per (sequence, KV head), merged in a fixed
+ * order: the result depends only on the bytes. */
+int hv_paged_decode_attention(const uint64_t* d_page_ptrs, const int32_t* d_seq_start,
+                              const int32_t* d_seq_tokens, const void* d_q, float* d_out, float* d_part,
+                              uint32_t batch, uint32_t q_heads, uint32_t kv_heads, uint32_t head_dim,
+                              uint32_t block_tokens, uint32_t splits, float scale, void* stream);
+
 /* ---- synthetic content (test / bench inputs) --------------------------- */
 /* byte j of object = byte (j%8) (little-endian) of splitmix64 word j/8:
  *   w_i = fmix(seed + (i+1)*0x9E3779B97F4A7C15)

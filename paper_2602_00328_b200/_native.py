@@ -117,6 +117,7 @@ _SIGS = {
     "hv_expert_ffn_gate_up": [u64, u64, u64, u64, u64, u64, u32, u32, u32, vp],
     "hv_expert_ffn_down": [u64, u64, u64, u64, u64, u32, u32, u32, vp],
     "hv_expert_ffn_max_tokens": [C.POINTER(i32)],
+    "hv_paged_decode_attention": [u64, u64, u64, u64, u64, u64, u32, u32, u32, u32, u32, u32, C.c_float, vp],
 }
 _RESTYPES = {"hv_error_string": C.c_char_p}
 

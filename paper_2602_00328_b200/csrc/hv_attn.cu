@@ -1,0 +1,279 @@
+// Paged decode attention over KV pages wherever they live (sm_100a).
+//
+// The consumer of K1 for the KV path (kv_decode.py): one query token per
+// sequence attends to its whole context, grouped-query (g = q_heads/kv_heads
+// query heads share one KV head).  Pages are addressed through a per-layer
+// table of raw page pointers -- local HBM, a donor's slab over NVLink, or the
+// pinned host tier -- so the kernel can run over a K1-gathered buffer or
+// directly over the pages in place (the fused mode: each KV byte crosses the
+// link once and is never written locally).
+//
+// Page layout (one layer of one block): K [T_b][kv_heads][D] then
+// V [T_b][kv_heads][D], fp16, T_b = 16 tokens.
+//
+// Flash-decoding: grid (splits, kv_heads, B).  A CTA owns a contiguous range
+// of its sequence's blocks; its 4 warps take the range's blocks round-robin
+// and keep an online-softmax state (running max, sum, fp32 accumulator) for
+// the g query heads.  Per block a warp:
+//   QK: lane (t = lane/2, half = lane%2) dots D/2 dims of K[t] with the g
+//       queries (fp32, from shared memory); one shuffle joins the halves;
+//   softmax: max / sum over the 16 tokens by shuffles, rescale of the state;
+//   PV: lane owns D/32 output dims and accumulates p[h][t] * V[t] over the
+//       16 tokens (probabilities broadcast through shared memory).
+// The next block's K/V slices are loaded into registers before the current
+// block is processed (two blocks in flight per warp).  The warps merge in
+// shared memory and each CTA writes a partial (m, l, acc) per query head;
+// hv_paged_decode_attention's second kernel merges the splits in a fixed
+// order (deterministic: no atomics), so the result depends only on the bytes.
+#include <cuda_fp16.h>
+#include <math.h>
+
+#include "hv_common.h"
+
+namespace {
+
+constexpr int kAttnWarps = 4;
+constexpr int kBlockTok = 16;
+
+template <int D>
+struct Frag {
+  static constexpr int kHalf = D / 2;            // dims per lane in QK
+  static constexpr int kQkVec = kHalf / 8;       // uint4 loads per lane (8 halves each)
+  static constexpr int kPvDims = D / 32;         // dims per lane in PV
+};
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int D>
+struct BlockRegs {
+  uint4 k[Frag<D>::kQkVec];                      // K[t][half] slice of this lane
+  uint32_t v[kBlockTok][Frag<D>::kPvDims / 2];   // V[t][my dims] for every token (half2 packed)
+};
+
+template <int D>
+__device__ __forceinline__ void load_block(BlockRegs<D>& r, const char* page, int kvh, int h, int lane) {
+  const int t = lane >> 1, half = lane & 1;
+  const size_t row = (size_t)kvh * D * 2;       // bytes per token row (all heads)
+  const char* kp = page + t * row + (size_t)h * D * 2 + half * Frag<D>::kHalf * 2;
+#pragma unroll
+  for (int i = 0; i < Frag<D>::kQkVec; ++i) r.k[i] = __ldg(reinterpret_cast<const uint4*>(kp) + i);
+  const char* vbase = page + kBlockTok * row + (size_t)h * D * 2 + lane * Frag<D>::kPvDims * 2;
+#pragma unroll
+  for (int t2 = 0; t2 < kBlockTok; ++t2) {
+    if constexpr (Frag<D>::kPvDims == 4) {
+      const uint2 x = __ldg(reinterpret_cast<const uint2*>(vbase + t2 * row));
+      r.v[t2][0] = x.x;
+      r.v[t2][1] = x.y;
+    } else {
+      r.v[t2][0] = __ldg(reinterpret_cast<const uint32_t*>(vbase + t2 * row));
+    }
+  }
+}
+
+template <int D, int G>
+__global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_split(
+    const uint64_t* __restrict__ pages, const int32_t* __restrict__ seq_start, const int32_t* __restrict__ seq_tokens,
+    const __half* __restrict__ q, float* __restrict__ part, int kvh, int splits, float scale) {
+  const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int q_heads = kvh * G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ __align__(16) float s_q[G][D];
+  __shared__ float s_p[kAttnWarps][G][kBlockTok];
+  __shared__ float s_m[kAttnWarps][G], s_l[kAttnWarps][G];
+  __shared__ float s_acc[kAttnWarps][G][D];
+
+  for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
+    const int hh = i / D, d = i % D;
+    s_q[hh][d] = __half2float(q[((size_t)b * q_heads + h * G + hh) * D + d]) * scale;
+  }
+  __syncthreads();
+
+  const int b0 = seq_start[b], nblk = seq_start[b + 1] - b0, ntok = seq_tokens[b];
+  const int per = (nblk + splits - 1) / splits;
+  const int lo = split * per, hi = min(nblk, lo + per);
+
+  float m[G], l[G], acc[G][Frag<D>::kPvDims];
+#pragma unroll
+  for (int hh = 0; hh < G; ++hh) {
+    m[hh] = -INFINITY;
+    l[hh] = 0.f;
+#pragma unroll
+    for (int j = 0; j < Frag<D>::kPvDims; ++j) acc[hh][j] = 0.f;
+  }
+  const int t = lane >> 1, half = lane & 1;
+  BlockRegs<D> cur, nxt;
+  int blk = lo + warp;
+  if (blk < hi) load_block<D>(cur, reinterpret_cast<const char*>(pages[b0 + blk]), kvh, h, lane);
+  for (; blk < hi; blk += kAttnWarps) {
+    const int nb = blk + kAttnWarps;
+    if (nb < hi) load_block<D>(nxt, reinterpret_cast<const char*>(pages[b0 + nb]), kvh, h, lane);
+    // QK: token t of this block against the G queries (this lane: half of the dims)
+    float s[G];
+#pragma unroll
+    for (int hh = 0; hh < G; ++hh) s[hh] = 0.f;
+#pragma unroll
+    for (int i = 0; i < Frag<D>::kQkVec; ++i) {
+      const __half2* hp = reinterpret_cast<const __half2*>(&cur.k[i]);
+      float kf[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __half22float2(hp[j]);
+        kf[2 * j] = f.x;
+        kf[2 * j + 1] = f.y;
+      }
+#pragma unroll
+      for (int hh = 0; hh < G; ++hh) {
+        const float4* qv = reinterpret_cast<const float4*>(&s_q[hh][half * Frag<D>::kHalf + i * 8]);
+        const float4 qa = qv[0], qb = qv[1];
+        float a = s[hh];
+        a = fmaf(kf[0], qa.x, a); a = fmaf(kf[1], qa.y, a); a = fmaf(kf[2], qa.z, a); a = fmaf(kf[3], qa.w, a);
+        a = fmaf(kf[4], qb.x, a); a = fmaf(kf[5], qb.y, a); a = fmaf(kf[6], qb.z, a); a = fmaf(kf[7], qb.w, a);
+        s[hh] = a;
+      }
+    }
+    const bool valid = blk * kBlockTok + t < ntok;
+#pragma unroll
+    for (int hh = 0; hh < G; ++hh) {
+      float sc = s[hh] + __shfl_xor_sync(0xffffffffu, s[hh], 1);
+      sc = valid ? sc : -INFINITY;
+      const float mn = fmaxf(m[hh], warp_max(sc));
+      const float p = valid ? __expf(sc - mn) : 0.f;
+      const float bs = warp_sum(p) * 0.5f;        // every token is counted by its two lanes
+      const float corr = __expf(m[hh] - mn);      // 0 on the first block (m = -inf)
+      l[hh] = l[hh] * corr + bs;
+      m[hh] = mn;
+#pragma unroll
+      for (int j = 0; j < Frag<D>::kPvDims; ++j) acc[hh][j] *= corr;
+      if (half == 0) s_p[warp][hh][t] = p;
+    }
+    __syncwarp();
+    // PV: this lane owns dims [lane * kPvDims, +kPvDims)
+#pragma unroll
+    for (int t2 = 0; t2 < kBlockTok; ++t2) {
+      float vf[Frag<D>::kPvDims];
+#pragma unroll
+      for (int j = 0; j < Frag<D>::kPvDims / 2; ++j) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&cur.v[t2][j]));
+        vf[2 * j] = f.x;
+        vf[2 * j + 1] = f.y;
+      }
+#pragma unroll
+      for (int hh = 0; hh < G; ++hh) {
+        const float p = s_p[warp][hh][t2];
+#pragma unroll
+        for (int j = 0; j < Frag<D>::kPvDims; ++j) acc[hh][j] = fmaf(p, vf[j], acc[hh][j]);
+      }
+    }
+    __syncwarp();
+    cur = nxt;
+  }
+  // merge the warps of this CTA (fixed order)
+#pragma unroll
+  for (int hh = 0; hh < G; ++hh) {
+    if (lane == 0) {
+      s_m[warp][hh] = m[hh];
+      s_l[warp][hh] = l[hh];
+    }
+#pragma unroll
+    for (int j = 0; j < Frag<D>::kPvDims; ++j) s_acc[warp][hh][lane * Frag<D>::kPvDims + j] = acc[hh][j];
+  }
+  __syncthreads();
+  // partial layout: [B][kvh][splits][G][D + 2] = acc[D], m, l
+  for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
+    const int hh = i / D, d = i % D;
+    float M = -INFINITY;
+    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, s_m[w][hh]);
+    float L = 0.f, A = 0.f;
+    for (int w = 0; w < kAttnWarps; ++w) {
+      const float c = s_m[w][hh] == -INFINITY ? 0.f : __expf(s_m[w][hh] - M);
+      L += s_l[w][hh] * c;
+      A += s_acc[w][hh][d] * c;
+    }
+    float* o = part + ((((size_t)b * kvh + h) * splits + split) * G + hh) * (D + 2);
+    o[d] = A;
+    if (d == 0) {
+      o[D] = M;
+      o[D + 1] = L;
+    }
+  }
+}
+
+// out[b][qh][d] = sum_s acc_s[d] e^(m_s - M) / sum_s l_s e^(m_s - M), splits in order
+template <int D>
+__global__ void paged_decode_combine(const float* __restrict__ part, float* __restrict__ out, int q_heads, int kvh,
+                                     int splits) {
+  const int qh = blockIdx.x, b = blockIdx.y, d = threadIdx.x;
+  const int g = q_heads / kvh, h = qh / g, hh = qh % g;
+  const float* base = part + (((size_t)b * kvh + h) * splits) * g * (D + 2);
+  float M = -INFINITY;
+  for (int s = 0; s < splits; ++s) M = fmaxf(M, base[((size_t)s * g + hh) * (D + 2) + D]);
+  float L = 0.f, A = 0.f;
+  for (int s = 0; s < splits; ++s) {
+    const float* p = base + ((size_t)s * g + hh) * (D + 2);
+    const float c = p[D] == -INFINITY ? 0.f : __expf(p[D] - M);
+    L += p[D + 1] * c;
+    A += p[d] * c;
+  }
+  out[((size_t)b * q_heads + qh) * D + d] = L > 0.f ? A / L : 0.f;
+}
+
+template <int D, int G>
+int launch_attn(const uint64_t* pages, const int32_t* seq_start, const int32_t* seq_tokens, const void* q,
+                float* out, float* part, uint32_t B, uint32_t kvh, uint32_t splits, float scale, cudaStream_t s) {
+  dim3 grid(splits, kvh, B);
+  paged_decode_split<D, G><<<grid, kAttnWarps * 32, 0, s>>>(pages, seq_start, seq_tokens,
+                                                             reinterpret_cast<const __half*>(q), part, (int)kvh,
+                                                             (int)splits, scale);
+  HV_CUDA(cudaGetLastError());
+  paged_decode_combine<D><<<dim3(kvh * G, B), D, 0, s>>>(part, out, (int)(kvh * G), (int)kvh, (int)splits);
+  HV_CUDA(cudaGetLastError());
+  hv::note_launch(2);
+  return HV_OK;
+}
+
+template <int D>
+int launch_attn_g(uint32_t g, const uint64_t* pages, const int32_t* seq_start, const int32_t* seq_tokens,
+                  const void* q, float* out, float* part, uint32_t B, uint32_t kvh, uint32_t splits, float scale,
+                  cudaStream_t s) {
+  switch (g) {
+    case 1: return launch_attn<D, 1>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s);
+    case 2: return launch_attn<D, 2>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s);
+    case 4: return launch_attn<D, 4>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s);
+    case 8: return launch_attn<D, 8>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s);
+    default: return HV_E_INVALID;
+  }
+}
+
+}  // namespace
+
+HV_EXPORT int hv_paged_decode_attention(const uint64_t* d_page_ptrs, const int32_t* d_seq_start,
+                                        const int32_t* d_seq_tokens, const void* d_q, float* d_out, float* d_part,
+                                        uint32_t batch, uint32_t q_heads, uint32_t kv_heads, uint32_t head_dim,
+                                        uint32_t block_tokens, uint32_t splits, float scale, void* stream) {
+  if (batch == 0) return HV_OK;
+  HV_CHECK_ARG(d_page_ptrs && d_seq_start && d_seq_tokens && d_q && d_out && d_part);
+  HV_CHECK_ARG(kv_heads > 0 && q_heads % kv_heads == 0);
+  HV_CHECK_ARG(head_dim == 64 || head_dim == 128);
+  HV_CHECK_ARG(block_tokens == (uint32_t)kBlockTok);
+  HV_CHECK_ARG(splits >= 1 && splits <= 1024 && batch <= 65535u && kv_heads <= 65535u);
+  int dev = 0;
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint32_t g = q_heads / kv_heads;
+  if (head_dim == 128)
+    return launch_attn_g<128>(g, d_page_ptrs, d_seq_start, d_seq_tokens, d_q, d_out, d_part, batch, kv_heads, splits,
+                              scale, s);
+  return launch_attn_g<64>(g, d_page_ptrs, d_seq_start, d_seq_tokens, d_q, d_out, d_part, batch, kv_heads, splits,
+                           scale, s);
+}

@@ -38,7 +38,7 @@ from . import _native as N
 from ._nvtx import annotate
 from .interconnect import LinkSpec, transfer_time
 from .pool import HostTier
-from .runtime import AllocationHints, Durability, HarvestHandle, RevokeReason, stable_hash64
+from .runtime import AllocationHints, Durability, HarvestHandle, RevokeReason, StaleHandleError, stable_hash64
 
 
 class KVTier(enum.Enum):
@@ -573,7 +573,16 @@ class KVCacheManager:
         return self.cache[:, b.slot, :]
 
     def close(self) -> None:
+        """Give every harvested slab back to its donor (freed once drained) and
+        release the host tier."""
         self.sys.engine.synchronize()
+        for s in self.slabs:
+            if s.live:
+                s.live = False
+                try:
+                    self.rt.harvest_free(s.handle)
+                except StaleHandleError:   # already revoking or released: the runtime finishes it
+                    pass
         self.sys.loop.run()
         self.host.close()
 

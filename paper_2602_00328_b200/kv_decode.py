@@ -21,14 +21,22 @@ work.  The peer slabs read by the step form its drain set (begin_reads
 before, the step's CUDA event after), so a revocation mid-step waits for the
 gathers that read the slab.
 
+The attention is hv_paged_decode_attention (csrc/hv_attn.cu), a split-K
+flash-decoding kernel over a table of page pointers.  fused=True skips K1:
+the attention reads every page where it lies (peer slab over NVLink, host
+over PCIe, local HBM), so each KV byte crosses the link once and is never
+written locally.  Both modes run the same kernel on the same bytes, so their
+outputs are bit-identical.
+
 Page layout (one layer of one 16-token block): K [16][kv_heads][head_dim]
 then V [16][kv_heads][head_dim], fp16.
 """
 from __future__ import annotations
 
+import math
+
 import numpy as np
 import torch
-import torch.nn.functional as TF
 
 from . import _native as N
 from . import fetch as F
@@ -36,7 +44,8 @@ from . import fetch as F
 
 class KVAttentionDecoder:
     def __init__(self, kv, sequences, q_heads: int, tokens: int | None = None, seed: int = 0,
-                 engine: str | None = None, max_ctas: int | None = None, trace: bool = False):
+                 engine: str | None = None, max_ctas: int | None = None, trace: bool = False,
+                 fused: bool = False, splits: int | None = None):
         """``sequences``: sequence ids of the batch, all with the same token
         count (``tokens``, default: the first sequence's).  Queries are
         synthetic: one random fp16 query per (layer, sequence, q head)."""
@@ -56,12 +65,29 @@ class KVAttentionDecoder:
         self.ids = [bid for b in blocks for bid in b]            # sequence-major block order
         self.dev = torch.device(kv.dev)
         self.engine = engine if engine is not None else kv.engine
-        self.max_ctas = kv.max_ctas if max_ctas is None else max_ctas
+        # the gathers share the SMs with the attention kernels: by default the
+        # K1 grid is capped (64 CTAs = 4 MiB in flight, enough for PCIe and
+        # NVLink) so attention of layer l runs beside the gather of layer l+1
+        self.max_ctas = 64 if max_ctas is None else max_ctas
         self.page = m.page_bytes
+        self.fused = fused
         n = len(self.ids)
-        self.bufs = [torch.empty(n * self.page, dtype=torch.uint8, device=self.dev) for _ in range(2)]
+        self.bufs = [] if fused else [torch.empty(n * self.page, dtype=torch.uint8, device=self.dev)
+                                      for _ in range(2)]
+        # gather mode: the attention's page table is the gathered buffer
+        self.buf_pages = [torch.arange(n, dtype=torch.int64, device=self.dev) * self.page + b.data_ptr()
+                          for b in self.bufs]
         g = torch.Generator().manual_seed(seed)
-        self.q = (torch.randn(self.L, self.B, q_heads, 1, m.head_dim, generator=g)).to(torch.float16).to(self.dev)
+        self.q = (torch.randn(self.L, self.B, q_heads, m.head_dim, generator=g)).to(torch.float16).to(self.dev)
+        self.seq_start = (torch.arange(self.B + 1, dtype=torch.int32) * self.nb).to(self.dev)
+        self.seq_tokens = torch.full((self.B,), self.T, dtype=torch.int32, device=self.dev)
+        # flash-decoding splits: about four resident CTAs per SM over (sequence, KV head, split)
+        sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
+        self.splits = splits or max(1, min(self.nb, math.ceil(4 * sms / (self.B * m.kv_heads))))
+        g_heads = q_heads // m.kv_heads
+        self.part = torch.empty(self.B * m.kv_heads * self.splits * g_heads * (m.head_dim + 2), dtype=torch.float32,
+                                device=self.dev)
+        self.scale = 1.0 / math.sqrt(m.head_dim)
         self.fetch_h = kv.stream
         self.fetch = torch.cuda.ExternalStream(kv.stream, device=self.dev)
         self.compute = torch.cuda.Stream(self.dev)
@@ -81,13 +107,14 @@ class KVAttentionDecoder:
         self._keep = (self._keep + [(tab, d)])[-2:]   # the last two steps' uploads stay alive
         return src, handles
 
-    def _attend(self, layer: int, buf: torch.Tensor) -> torch.Tensor:
+    def _attend(self, layer: int, pages: torch.Tensor) -> torch.Tensor:
+        """hv_paged_decode_attention over the page table `pages` [n] (int64)."""
         m = self.m
-        pages = buf.view(torch.float16).view(self.B, self.nb, 2, m.block_tokens, m.kv_heads, m.head_dim)
-        k = pages[:, :, 0].reshape(self.B, self.nb * m.block_tokens, m.kv_heads, m.head_dim)[:, :self.T]
-        v = pages[:, :, 1].reshape(self.B, self.nb * m.block_tokens, m.kv_heads, m.head_dim)[:, :self.T]
-        return TF.scaled_dot_product_attention(self.q[layer], k.transpose(1, 2), v.transpose(1, 2),
-                                               enable_gqa=True)                 # [B, Hq, 1, D]
+        out = torch.empty(self.B, self.Hq, m.head_dim, dtype=torch.float32, device=self.dev)
+        N.call("hv_paged_decode_attention", pages.data_ptr(), self.seq_start.data_ptr(), self.seq_tokens.data_ptr(),
+               self.q[layer].data_ptr(), out.data_ptr(), self.part.data_ptr(), self.B, self.Hq, m.kv_heads,
+               m.head_dim, m.block_tokens, self.splits, self.scale, torch.cuda.current_stream(self.dev).cuda_stream)
+        return out
 
     def step(self) -> torch.Tensor:
         """One decode step over all layers: returns the attention outputs [L, B, Hq, D]."""
@@ -102,6 +129,19 @@ class KVAttentionDecoder:
         src, handles = self._sources()
         batch = rt.begin_reads(handles) if handles else None
         outs = [None] * self.L
+        if self.fused:                      # attention straight over the resident pages
+            with torch.cuda.stream(self.compute):
+                self.compute.wait_stream(self.fetch)     # the page table upload
+                for layer in range(self.L):
+                    if self.trace:
+                        c0 = torch.cuda.Event(enable_timing=True)
+                        c0.record(self.compute)
+                    outs[layer] = self._attend(layer, src[layer])
+                    if self.trace:
+                        c1 = torch.cuda.Event(enable_timing=True)
+                        c1.record(self.compute)
+                        self._tr[layer] = {"fetch": (c0, c0), "compute": (c0, c1)}
+            return self._finish(cur, batch, outs)
         consumed = [None, None]
         for layer in range(self.L):
             b = layer % 2
@@ -119,20 +159,24 @@ class KVAttentionDecoder:
                 if self.trace:
                     c0 = torch.cuda.Event(enable_timing=True)
                     c0.record(self.compute)
-                outs[layer] = self._attend(layer, self.bufs[b])
+                outs[layer] = self._attend(layer, self.buf_pages[b])
                 done = torch.cuda.Event(enable_timing=self.trace)
                 done.record(self.compute)
                 consumed[b] = done
             if self.trace:
                 self._tr[layer] = {"fetch": (f0, got), "compute": (c0, done)}
+        return self._finish(cur, batch, outs)
+
+    def _finish(self, cur, batch, outs) -> torch.Tensor:
         cur.wait_stream(self.compute)
         cur.wait_stream(self.fetch)
-        if batch is not None:               # drain completes when the step's gathers have
+        if batch is not None:               # the drain completes when the step's reads have
             fin = torch.cuda.Event()
             fin.record(cur)
             self.fetch.wait_event(fin)
+            rt = self.kv.rt
             self.kv.sys.engine.track([lambda _x, bt=batch: rt.end_reads(bt)])
-        return torch.stack([o.squeeze(2) for o in outs])
+        return torch.stack(outs)
 
     def overlap_report(self) -> dict:
         """Device-clock gather / attention intervals of the last traced step."""
