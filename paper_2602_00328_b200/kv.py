@@ -198,7 +198,9 @@ class KVCacheManager:
             return
         arrs = np.concatenate([np.asarray(x, dtype=np.uint64) for x in (src_b, src_s, dst_b, dst_s)])
         pinned = torch.from_numpy(arrs.view(np.int64)).pin_memory()
-        dbuf = torch.empty(pinned.numel(), dtype=torch.int64, device=self.dev)
+        # allocated in the fetch stream's pool: the first writer is that stream
+        with torch.cuda.stream(torch.cuda.ExternalStream(self.stream, device=self.dev)):
+            dbuf = torch.empty(pinned.numel(), dtype=torch.int64, device=self.dev)
         N.call("hv_memcpy_h2d", dbuf.data_ptr(), pinned.data_ptr(), pinned.numel() * 8, self.stream)
         batch = self.rt.begin_reads(list(handles)) if handles else None
 
@@ -563,7 +565,8 @@ class KVCacheManager:
         while keep and keep[0][0].query():
             keep.popleft()
         pinned = torch.from_numpy(arr.view(np.int64)).pin_memory()
-        dev = torch.empty(pinned.numel(), dtype=torch.int64, device=self.dev)
+        with torch.cuda.stream(torch.cuda.ExternalStream(stream, device=self.dev)):   # the writer's pool
+            dev = torch.empty(pinned.numel(), dtype=torch.int64, device=self.dev)
         N.call("hv_memcpy_h2d", dev.data_ptr(), pinned.data_ptr(), pinned.numel() * 8, stream)
         return pinned, dev
 

@@ -99,11 +99,16 @@ class KVAttentionDecoder:
         """[L, n] page addresses of this step (one upload, one broadcast)."""
         bases, strides, handles = self.kv.page_table(self.ids)
         tab = torch.from_numpy(np.stack([bases, strides]).view(np.int64)).pin_memory()
-        d = torch.empty(tab.shape, dtype=torch.int64, device=self.dev)
-        N.call("hv_memcpy_h2d", d.data_ptr(), tab.data_ptr(), tab.numel() * 8, self.fetch_h)
-        layers = torch.arange(self.L, dtype=torch.int64, device=self.dev).unsqueeze(1)
+        # every tensor of the table is allocated and written on the fetch
+        # stream, the stream that first reads it (the caching allocator
+        # reuses a block only in stream order of the stream it belongs to)
         with torch.cuda.stream(self.fetch):
+            d = torch.empty(tab.shape, dtype=torch.int64, device=self.dev)
+            N.call("hv_memcpy_h2d", d.data_ptr(), tab.data_ptr(), tab.numel() * 8, self.fetch_h)
+            layers = torch.arange(self.L, dtype=torch.int64, device=self.dev).unsqueeze(1)
             src = d[0].unsqueeze(0) + layers * d[1].unsqueeze(0)
+        if self.fused:                      # read by the attention on the compute stream
+            src.record_stream(self.compute)
         self._keep = (self._keep + [(tab, d)])[-2:]   # the last two steps' uploads stay alive
         return src, handles
 

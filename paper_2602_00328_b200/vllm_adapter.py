@@ -169,7 +169,8 @@ class HarvestPeerHandler(OffloadingHandler):
         nb = len(sb)
         arrs = np.concatenate([np.broadcast_to(np.asarray(x, dtype=np.uint64), (nb,)) for x in (sb, ss, db, ds)])
         pinned = torch.from_numpy(arrs.view(np.int64)).pin_memory()
-        dbuf = torch.empty(pinned.numel(), dtype=torch.int64, device=self.dev)
+        with torch.cuda.stream(torch.cuda.ExternalStream(self.stream, device=self.dev)):   # the writer's pool
+            dbuf = torch.empty(pinned.numel(), dtype=torch.int64, device=self.dev)
         N.call("hv_memcpy_h2d", dbuf.data_ptr(), pinned.data_ptr(), pinned.numel() * 8, self.stream)
         batch = self.rt.begin_reads(handles) if handles else None
         nbytes = nb * self.L * self.page
