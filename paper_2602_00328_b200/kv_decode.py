@@ -81,9 +81,13 @@ class KVAttentionDecoder:
         self.q = (torch.randn(self.L, self.B, q_heads, m.head_dim, generator=g)).to(torch.float16).to(self.dev)
         self.seq_start = (torch.arange(self.B + 1, dtype=torch.int32) * self.nb).to(self.dev)
         self.seq_tokens = torch.full((self.B,), self.T, dtype=torch.int32, device=self.dev)
-        # flash-decoding splits: about four resident CTAs per SM over (sequence, KV head, split)
+        # flash-decoding splits: one wave of (sequence, KV head, split) CTAs at
+        # the kernel's two resident CTAs per SM.  Measured on B200 (tools/
+        # attn_probe.py, HBM pages): 4 x 4k: 8 splits 36 us, 19: 41, 64: 56;
+        # 1 x 128k: 37 splits 199 us, 74: 216, 296: 304 -- fewer, longer
+        # splits amortize the partial write and merge
         sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
-        self.splits = splits or max(1, min(self.nb, math.ceil(4 * sms / (self.B * m.kv_heads))))
+        self.splits = splits or max(1, min(self.nb, math.ceil(2 * sms / (self.B * m.kv_heads))))
         g_heads = q_heads // m.kv_heads
         self.part = torch.empty(self.B * m.kv_heads * self.splits * g_heads * (m.head_dim + 2), dtype=torch.float32,
                                 device=self.dev)

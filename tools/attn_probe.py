@@ -1,0 +1,50 @@
+"""hv_paged_decode_attention alone, pages in local HBM (scattered), Llama-3-8B
+KV shapes: config 1 (4 x 4k) and config 4 (1 x 128k).  Prints JSON: us per
+layer and KV GB/s, for several split counts."""
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2602_00328_b200 import _native as N  # noqa: E402
+
+
+def run(B, ctx, splits_list, kvh=8, g=4, D=128):
+    nb = ctx // 16
+    n = B * nb
+    page = 2 * 16 * kvh * D * 2
+    pool = torch.empty(n, page, dtype=torch.uint8, device="cuda")
+    pool.view(torch.float16).normal_(0, 0.5)
+    perm = torch.randperm(n)
+    ptrs = (perm.to("cuda") * page + pool.data_ptr()).to(torch.int64)
+    start = (torch.arange(B + 1, dtype=torch.int32) * nb).cuda()
+    tok = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
+    q = torch.randn(B, kvh * g, D, device="cuda").to(torch.float16)
+    out = torch.empty(B, kvh * g, D, device="cuda")
+    res = {}
+    for sp in splits_list:
+        part = torch.empty(B * kvh * sp * g * (D + 2), device="cuda")
+        s = torch.cuda.current_stream().cuda_stream
+
+        def f():
+            N.call("hv_paged_decode_attention", ptrs.data_ptr(), start.data_ptr(), tok.data_ptr(), q.data_ptr(),
+                   out.data_ptr(), part.data_ptr(), B, kvh * g, kvh, D, 16, sp, 1 / D ** 0.5, s)
+        for _ in range(3):
+            f()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(20):
+            f()
+        e1.record()
+        e1.synchronize()
+        us = e0.elapsed_time(e1) / 20 * 1e3
+        res[f"splits{sp}"] = {"us": us, "GBps": n * page / (us * 1e-6) / 1e9}
+    return res
+
+
+if __name__ == "__main__":
+    out = {"config1_4x4k": run(4, 4096, [8, 19, 32, 64]), "config4_1x128k": run(1, 131072, [37, 74, 148, 296])}
+    print(json.dumps(out, indent=1))
