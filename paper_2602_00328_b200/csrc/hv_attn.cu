@@ -79,6 +79,44 @@ __device__ __forceinline__ void load_block(BlockRegs<D>& r, const char* page, in
   }
 }
 
+// merge the warps of a CTA (fixed order) and write its partial state:
+// [B][kvh][splits][G][D + 2] = acc[D], m, l
+template <int D, int G>
+__device__ __forceinline__ void merge_and_write(const float (&m)[G], const float (&l)[G],
+                                                const float (&acc)[G][D / 32], float* __restrict__ part, int b, int h,
+                                                int kvh, int split, int splits) {
+  __shared__ float s_m[kAttnWarps][G], s_l[kAttnWarps][G];
+  __shared__ float s_acc[kAttnWarps][G][D];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int hh = 0; hh < G; ++hh) {
+    if (lane == 0) {
+      s_m[warp][hh] = m[hh];
+      s_l[warp][hh] = l[hh];
+    }
+#pragma unroll
+    for (int j = 0; j < D / 32; ++j) s_acc[warp][hh][lane * (D / 32) + j] = acc[hh][j];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
+    const int hh = i / D, d = i % D;
+    float M = -INFINITY;
+    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, s_m[w][hh]);
+    float L = 0.f, A = 0.f;
+    for (int w = 0; w < kAttnWarps; ++w) {
+      const float c = s_m[w][hh] == -INFINITY ? 0.f : __expf(s_m[w][hh] - M);
+      L += s_l[w][hh] * c;
+      A += s_acc[w][hh][d] * c;
+    }
+    float* o = part + ((((size_t)b * kvh + h) * splits + split) * G + hh) * (D + 2);
+    o[d] = A;
+    if (d == 0) {
+      o[D] = M;
+      o[D + 1] = L;
+    }
+  }
+}
+
 template <int D, int G>
 __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_split(
     const uint64_t* __restrict__ pages, const int32_t* __restrict__ seq_start, const int32_t* __restrict__ seq_tokens,
@@ -88,8 +126,6 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_split(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ __align__(16) float s_q[G][D];
   __shared__ float s_p[kAttnWarps][G][kBlockTok];
-  __shared__ float s_m[kAttnWarps][G], s_l[kAttnWarps][G];
-  __shared__ float s_acc[kAttnWarps][G][D];
 
   for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
     const int hh = i / D, d = i % D;
@@ -176,35 +212,169 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_split(
     __syncwarp();
     cur = nxt;
   }
-  // merge the warps of this CTA (fixed order)
+  merge_and_write<D, G>(m, l, acc, part, b, h, kvh, split, splits);
+}
+
+// Measured on B200, pages in local HBM (tools/attn_probe.py, KV GB/s at the
+// best split count; 4 x 4k / 1 x 128k): register prefetch 1,841 / 2,514;
+// ring of 2 stages 2,082 / 3,192; 3 stages 2,172 / 3,229 (default);
+// 4 stages 1,579 / 2,222 (one resident CTA per SM).
+//
+// Same math, K/V streamed through a per-warp shared-memory ring with
+// cp.async (S blocks in flight per warp, no register staging): fewer
+// registers (more resident warps) and a deeper prefetch.  K and V rows of
+// the head are stored with 16-byte chunk c of row r at c ^ (r & 7), so the
+// QK reads (lane pairs on one row) and the PV reads (a whole row across the
+// warp) are bank-conflict free.
+template <int D>
+struct Ring {
+  static constexpr int kRow = D * 2;                    // bytes of one token row of one head
+  static constexpr int kChunks = kRow / 16;
+  static constexpr int kTile = kBlockTok * kRow;        // K or V of one block-head
+  static constexpr int kStage = 2 * kTile;
+};
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_wait_n() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int D>
+__device__ __forceinline__ uint32_t rswz(int r, int c) {
+  return (uint32_t)(r * Ring<D>::kRow + ((c ^ (r & 7)) << 4));
+}
+
+template <int D>
+__device__ __forceinline__ void ring_load(char* stage, const char* page, int kvh, int h, int lane) {
+  const size_t row = (size_t)kvh * D * 2;
+  const char* kb = page + (size_t)h * D * 2;
+  const char* vb = kb + kBlockTok * row;
+  const uint32_t sk = smem_addr(stage), sv = sk + Ring<D>::kTile;
 #pragma unroll
-  for (int hh = 0; hh < G; ++hh) {
-    if (lane == 0) {
-      s_m[warp][hh] = m[hh];
-      s_l[warp][hh] = l[hh];
-    }
-#pragma unroll
-    for (int j = 0; j < Frag<D>::kPvDims; ++j) s_acc[warp][hh][lane * Frag<D>::kPvDims + j] = acc[hh][j];
+  for (int i = lane; i < kBlockTok * Ring<D>::kChunks; i += 32) {
+    const int r = i / Ring<D>::kChunks, c = i % Ring<D>::kChunks;
+    cp16(sk + rswz<D>(r, c), kb + r * row + c * 16);
+    cp16(sv + rswz<D>(r, c), vb + r * row + c * 16);
   }
-  __syncthreads();
-  // partial layout: [B][kvh][splits][G][D + 2] = acc[D], m, l
+}
+
+template <int D, int G, int S>
+__global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_split_ring(
+    const uint64_t* __restrict__ pages, const int32_t* __restrict__ seq_start, const int32_t* __restrict__ seq_tokens,
+    const __half* __restrict__ q, float* __restrict__ part, int kvh, int splits, float scale) {
+  extern __shared__ __align__(128) char ring_smem[];
+  const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int q_heads = kvh * G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ __align__(16) float s_q[G][D];
+  __shared__ float s_p[kAttnWarps][G][kBlockTok];
+  char* my_ring = ring_smem + (size_t)warp * S * Ring<D>::kStage;
+
   for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
     const int hh = i / D, d = i % D;
-    float M = -INFINITY;
-    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, s_m[w][hh]);
-    float L = 0.f, A = 0.f;
-    for (int w = 0; w < kAttnWarps; ++w) {
-      const float c = s_m[w][hh] == -INFINITY ? 0.f : __expf(s_m[w][hh] - M);
-      L += s_l[w][hh] * c;
-      A += s_acc[w][hh][d] * c;
-    }
-    float* o = part + ((((size_t)b * kvh + h) * splits + split) * G + hh) * (D + 2);
-    o[d] = A;
-    if (d == 0) {
-      o[D] = M;
-      o[D + 1] = L;
-    }
+    s_q[hh][d] = __half2float(q[((size_t)b * q_heads + h * G + hh) * D + d]) * scale;
   }
+  __syncthreads();
+
+  const int b0 = seq_start[b], nblk = seq_start[b + 1] - b0, ntok = seq_tokens[b];
+  const int per = (nblk + splits - 1) / splits;
+  const int lo = split * per, hi = min(nblk, lo + per);
+  // this warp's blocks: lo + warp, lo + warp + 4, ...
+  const int mine = lo + warp < hi ? (hi - (lo + warp) + kAttnWarps - 1) / kAttnWarps : 0;
+
+  float m[G], l[G], acc[G][Frag<D>::kPvDims];
+#pragma unroll
+  for (int hh = 0; hh < G; ++hh) {
+    m[hh] = -INFINITY;
+    l[hh] = 0.f;
+#pragma unroll
+    for (int j = 0; j < Frag<D>::kPvDims; ++j) acc[hh][j] = 0.f;
+  }
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (s < mine) ring_load<D>(my_ring + s * Ring<D>::kStage,
+                               reinterpret_cast<const char*>(pages[b0 + lo + warp + s * kAttnWarps]), kvh, h, lane);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  const int t = lane >> 1, half = lane & 1;
+  for (int it = 0; it < mine; ++it) {
+    cp_wait_n<S - 2>();
+    __syncwarp();
+    {  // refill the stage consumed one iteration ago
+      const int nx = it + S - 1;
+      if (nx < mine)
+        ring_load<D>(my_ring + (nx % S) * Ring<D>::kStage,
+                     reinterpret_cast<const char*>(pages[b0 + lo + warp + nx * kAttnWarps]), kvh, h, lane);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    const char* st = my_ring + (it % S) * Ring<D>::kStage;
+    const int blk = lo + warp + it * kAttnWarps;
+    float s_[G];
+#pragma unroll
+    for (int hh = 0; hh < G; ++hh) s_[hh] = 0.f;
+#pragma unroll
+    for (int i = 0; i < Frag<D>::kQkVec; ++i) {
+      const uint4 kv4 = *reinterpret_cast<const uint4*>(st + rswz<D>(t, half * Frag<D>::kQkVec + i));
+      const __half2* hp = reinterpret_cast<const __half2*>(&kv4);
+      float kf[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __half22float2(hp[j]);
+        kf[2 * j] = f.x;
+        kf[2 * j + 1] = f.y;
+      }
+#pragma unroll
+      for (int hh = 0; hh < G; ++hh) {
+        const float4* qv = reinterpret_cast<const float4*>(&s_q[hh][half * Frag<D>::kHalf + i * 8]);
+        const float4 qa = qv[0], qb = qv[1];
+        float a0 = fmaf(kf[0], qa.x, fmaf(kf[1], qa.y, fmaf(kf[2], qa.z, kf[3] * qa.w)));
+        float a1 = fmaf(kf[4], qb.x, fmaf(kf[5], qb.y, fmaf(kf[6], qb.z, kf[7] * qb.w)));
+        s_[hh] += a0 + a1;
+      }
+    }
+    const bool valid = blk * kBlockTok + t < ntok;
+#pragma unroll
+    for (int hh = 0; hh < G; ++hh) {
+      float sc = s_[hh] + __shfl_xor_sync(0xffffffffu, s_[hh], 1);
+      sc = valid ? sc : -INFINITY;
+      const float mn = fmaxf(m[hh], warp_max(sc));
+      const float p = valid ? __expf(sc - mn) : 0.f;
+      const float bs = warp_sum(p) * 0.5f;
+      const float corr = __expf(m[hh] - mn);
+      l[hh] = l[hh] * corr + bs;
+      m[hh] = mn;
+#pragma unroll
+      for (int j = 0; j < Frag<D>::kPvDims; ++j) acc[hh][j] *= corr;
+      if (half == 0) s_p[warp][hh][t] = p;
+    }
+    __syncwarp();
+    const char* vt = st + Ring<D>::kTile;
+    const int vchunk = lane * Frag<D>::kPvDims * 2 / 16, voff = (lane * Frag<D>::kPvDims * 2) % 16;
+#pragma unroll
+    for (int t2 = 0; t2 < kBlockTok; ++t2) {
+      float vf[Frag<D>::kPvDims];
+      const char* vp = vt + rswz<D>(t2, vchunk) + voff;
+      if constexpr (Frag<D>::kPvDims == 4) {
+        const uint2 x = *reinterpret_cast<const uint2*>(vp);
+        const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&x.x));
+        const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&x.y));
+        vf[0] = f0.x; vf[1] = f0.y; vf[2] = f1.x; vf[3] = f1.y;
+      } else {
+        const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(vp));
+        vf[0] = f0.x; vf[1] = f0.y;
+      }
+#pragma unroll
+      for (int hh = 0; hh < G; ++hh) {
+        const float p = s_p[warp][hh][t2];
+#pragma unroll
+        for (int j = 0; j < Frag<D>::kPvDims; ++j) acc[hh][j] = fmaf(p, vf[j], acc[hh][j]);
+      }
+    }
+    __syncwarp();
+  }
+  cp_wait_n<0>();
+  merge_and_write<D, G>(m, l, acc, part, b, h, kvh, split, splits);
 }
 
 // out[b][qh][d] = sum_s acc_s[d] e^(m_s - M) / sum_s l_s e^(m_s - M), splits in order
@@ -226,13 +396,30 @@ __global__ void paged_decode_combine(const float* __restrict__ part, float* __re
   out[((size_t)b * q_heads + qh) * D + d] = L > 0.f ? A / L : 0.f;
 }
 
+#ifndef HV_ATTN_RING
+#define HV_ATTN_RING 3
+#endif
+
 template <int D, int G>
 int launch_attn(const uint64_t* pages, const int32_t* seq_start, const int32_t* seq_tokens, const void* q,
                 float* out, float* part, uint32_t B, uint32_t kvh, uint32_t splits, float scale, cudaStream_t s) {
   dim3 grid(splits, kvh, B);
+#if HV_ATTN_RING
+  constexpr int kS = HV_ATTN_RING;
+  constexpr size_t smem = (size_t)kAttnWarps * kS * Ring<D>::kStage;
+  static bool attr = false;
+  if (!attr) {
+    HV_CUDA(cudaFuncSetAttribute(paged_decode_split_ring<D, G, kS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr = true;
+  }
+  paged_decode_split_ring<D, G, kS><<<grid, kAttnWarps * 32, smem, s>>>(
+      pages, seq_start, seq_tokens, reinterpret_cast<const __half*>(q), part, (int)kvh, (int)splits, scale);
+#else
   paged_decode_split<D, G><<<grid, kAttnWarps * 32, 0, s>>>(pages, seq_start, seq_tokens,
                                                              reinterpret_cast<const __half*>(q), part, (int)kvh,
                                                              (int)splits, scale);
+#endif
   HV_CUDA(cudaGetLastError());
   paged_decode_combine<D><<<dim3(kvh * G, B), D, 0, s>>>(part, out, (int)(kvh * G), (int)kvh, (int)splits);
   HV_CUDA(cudaGetLastError());
