@@ -1,0 +1,9 @@
+set -x
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r68_smoke.log 2>&1; tail -1 gpurun_out/r68_smoke.log
+timeout 1500 python -m pytest tests -q -m gpu > gpurun_out/r68_tests.log 2>&1; tail -2 gpurun_out/r68_tests.log
+timeout 900 compute-sanitizer --tool memcheck --leak-check no --error-exitcode 9 python -m pytest tests/test_gpu_kv_decode.py -q -m gpu -x > gpurun_out/r68_memcheck.log 2>&1; echo "memcheck rc=$?"; tail -2 gpurun_out/r68_memcheck.log
+timeout 900 compute-sanitizer --tool racecheck --error-exitcode 9 python tools/kv_decode_repro.py 2 1024 > gpurun_out/r68_racecheck.log 2>&1; echo "racecheck rc=$?"; tail -2 gpurun_out/r68_racecheck.log
+timeout 1200 python bench.py > gpurun_out/r68_bench.json 2> gpurun_out/r68_bench.err; echo rc=$?; tail -3 gpurun_out/r68_bench.err
+timeout 600 python bench.py --impl reference > gpurun_out/r68_ref.json 2> gpurun_out/r68_ref.err; echo rc=$?
+HV_BENCH_QWEN_LAYERS=8 HV_DEVICE_MAP=0,0 timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29525 bench.py --gpus 2 --steps 3 --warmup 3 --dist-backend gloo --phi-layers 4 > gpurun_out/r68_bench2.json 2> gpurun_out/r68_bench2.err; echo rc=$?; tail -3 gpurun_out/r68_bench2.err
