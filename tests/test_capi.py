@@ -131,6 +131,16 @@ def test_launch_entry_points_validate_arguments_without_a_gpu():
     assert lib.hv_expert_ffn_down(0, A, A, A, A, 4, 2048, 1408, None) == INV            # no address table
     assert lib.hv_expert_ffn_down(A, A, A, A, A, 70000, 2048, 1408, None) == INV        # grid.y limit
     assert N.c_int_out("hv_expert_ffn_max_tokens") == 64
+    # paged decode attention: empty batch is a no-op; unsupported shapes are rejected
+    def attn(batch=2, qh=32, kvh=8, d=128, bt=16, splits=4, ptr=A):
+        return lib.hv_paged_decode_attention(ptr, A, A, A, A, A, batch, qh, kvh, d, bt, splits, 0.1, None)
+    assert attn(batch=0) == N.HV_OK
+    assert attn(ptr=0) == INV                # no page table
+    assert attn(qh=30) == INV                # q heads not a multiple of KV heads
+    assert attn(qh=8 * 16) == INV            # group of 16 query heads per KV head
+    assert attn(d=96) == INV                 # head_dim 64 or 128 only
+    assert attn(bt=32) == INV                # 16-token blocks
+    assert attn(splits=0) == INV
     # the Python layer raises the matching exception type
     with pytest.raises(N.HarvestNativeError) as ei:
         N.call("hv_batch_copy", 0, 0x1000, 0x1000, 2, 0, 0, None)
