@@ -449,6 +449,10 @@ HV_EXPORT int hv_paged_decode_attention(const uint64_t* d_page_ptrs, const int32
   if (batch == 0) return HV_OK;
   HV_CHECK_ARG(d_page_ptrs && d_seq_start && d_seq_tokens && d_q && d_out && d_part);
   HV_CHECK_ARG(kv_heads > 0 && q_heads % kv_heads == 0);
+  {
+    const uint32_t g = q_heads / kv_heads;   // grouped-query sizes with a compiled kernel
+    HV_CHECK_ARG(g == 1 || g == 2 || g == 4 || g == 8);
+  }
   HV_CHECK_ARG(head_dim == 64 || head_dim == 128);
   HV_CHECK_ARG(block_tokens == (uint32_t)kBlockTok);
   HV_CHECK_ARG(splits >= 1 && splits <= 1024 && batch <= 65535u && kv_heads <= 65535u);
