@@ -218,7 +218,9 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_split(
 // Measured on B200, pages in local HBM (tools/attn_probe.py, KV GB/s at the
 // best split count; 4 x 4k / 1 x 128k): register prefetch 1,841 / 2,514;
 // ring of 2 stages 2,082 / 3,192; 3 stages 2,172 / 3,229 (default);
-// 4 stages 1,579 / 2,222 (one resident CTA per SM).
+// 4 stages 1,579 / 2,222 (one resident CTA per SM).  One warp per KV head
+// with all heads of a page in one CTA (whole-page streaming) measured
+// 1,874 / 2,942: HBM row locality is not the limit, per-warp latency is.
 //
 // Same math, K/V streamed through a per-warp shared-memory ring with
 // cp.async (S blocks in flight per warp, no register staging): fewer
@@ -259,6 +261,76 @@ __device__ __forceinline__ void ring_load(char* stage, const char* page, int kvh
   }
 }
 
+// One 16-token block of one KV head, staged in shared memory at `st` (K tile
+// then V tile, swizzled rows), folded into the warp's online-softmax state.
+template <int D, int G>
+__device__ __forceinline__ void attend_block(const char* st, int blk, int ntok, const float (*s_q)[D],
+                                             float (*s_p)[kBlockTok], float (&m)[G], float (&l)[G],
+                                             float (&acc)[G][D / 32], int lane) {
+  const int t = lane >> 1, half = lane & 1;
+    float s_[G];
+#pragma unroll
+    for (int hh = 0; hh < G; ++hh) s_[hh] = 0.f;
+#pragma unroll
+    for (int i = 0; i < Frag<D>::kQkVec; ++i) {
+      const uint4 kv4 = *reinterpret_cast<const uint4*>(st + rswz<D>(t, half * Frag<D>::kQkVec + i));
+      const __half2* hp = reinterpret_cast<const __half2*>(&kv4);
+      float kf[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __half22float2(hp[j]);
+        kf[2 * j] = f.x;
+        kf[2 * j + 1] = f.y;
+      }
+#pragma unroll
+      for (int hh = 0; hh < G; ++hh) {
+        const float4* qv = reinterpret_cast<const float4*>(&s_q[hh][half * Frag<D>::kHalf + i * 8]);
+        const float4 qa = qv[0], qb = qv[1];
+        float a0 = fmaf(kf[0], qa.x, fmaf(kf[1], qa.y, fmaf(kf[2], qa.z, kf[3] * qa.w)));
+        float a1 = fmaf(kf[4], qb.x, fmaf(kf[5], qb.y, fmaf(kf[6], qb.z, kf[7] * qb.w)));
+        s_[hh] += a0 + a1;
+      }
+    }
+    const bool valid = blk * kBlockTok + t < ntok;
+#pragma unroll
+    for (int hh = 0; hh < G; ++hh) {
+      float sc = s_[hh] + __shfl_xor_sync(0xffffffffu, s_[hh], 1);
+      sc = valid ? sc : -INFINITY;
+      const float mn = fmaxf(m[hh], warp_max(sc));
+      const float p = valid ? __expf(sc - mn) : 0.f;
+      const float bs = warp_sum(p) * 0.5f;
+      const float corr = __expf(m[hh] - mn);
+      l[hh] = l[hh] * corr + bs;
+      m[hh] = mn;
+#pragma unroll
+      for (int j = 0; j < Frag<D>::kPvDims; ++j) acc[hh][j] *= corr;
+      if (half == 0) s_p[hh][t] = p;
+    }
+    __syncwarp();
+    const char* vt = st + Ring<D>::kTile;
+    const int vchunk = lane * Frag<D>::kPvDims * 2 / 16, voff = (lane * Frag<D>::kPvDims * 2) % 16;
+#pragma unroll
+    for (int t2 = 0; t2 < kBlockTok; ++t2) {
+      float vf[Frag<D>::kPvDims];
+      const char* vp = vt + rswz<D>(t2, vchunk) + voff;
+      if constexpr (Frag<D>::kPvDims == 4) {
+        const uint2 x = *reinterpret_cast<const uint2*>(vp);
+        const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&x.x));
+        const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&x.y));
+        vf[0] = f0.x; vf[1] = f0.y; vf[2] = f1.x; vf[3] = f1.y;
+      } else {
+        const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(vp));
+        vf[0] = f0.x; vf[1] = f0.y;
+      }
+#pragma unroll
+      for (int hh = 0; hh < G; ++hh) {
+        const float p = s_p[hh][t2];
+#pragma unroll
+        for (int j = 0; j < Frag<D>::kPvDims; ++j) acc[hh][j] = fmaf(p, vf[j], acc[hh][j]);
+      }
+    }
+}
+
 template <int D, int G, int S>
 __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_split_ring(
     const uint64_t* __restrict__ pages, const int32_t* __restrict__ seq_start, const int32_t* __restrict__ seq_tokens,
@@ -297,7 +369,6 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_split_ring(
                                reinterpret_cast<const char*>(pages[b0 + lo + warp + s * kAttnWarps]), kvh, h, lane);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  const int t = lane >> 1, half = lane & 1;
   for (int it = 0; it < mine; ++it) {
     cp_wait_n<S - 2>();
     __syncwarp();
@@ -308,69 +379,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_split_ring(
                      reinterpret_cast<const char*>(pages[b0 + lo + warp + nx * kAttnWarps]), kvh, h, lane);
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    const char* st = my_ring + (it % S) * Ring<D>::kStage;
-    const int blk = lo + warp + it * kAttnWarps;
-    float s_[G];
-#pragma unroll
-    for (int hh = 0; hh < G; ++hh) s_[hh] = 0.f;
-#pragma unroll
-    for (int i = 0; i < Frag<D>::kQkVec; ++i) {
-      const uint4 kv4 = *reinterpret_cast<const uint4*>(st + rswz<D>(t, half * Frag<D>::kQkVec + i));
-      const __half2* hp = reinterpret_cast<const __half2*>(&kv4);
-      float kf[8];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 f = __half22float2(hp[j]);
-        kf[2 * j] = f.x;
-        kf[2 * j + 1] = f.y;
-      }
-#pragma unroll
-      for (int hh = 0; hh < G; ++hh) {
-        const float4* qv = reinterpret_cast<const float4*>(&s_q[hh][half * Frag<D>::kHalf + i * 8]);
-        const float4 qa = qv[0], qb = qv[1];
-        float a0 = fmaf(kf[0], qa.x, fmaf(kf[1], qa.y, fmaf(kf[2], qa.z, kf[3] * qa.w)));
-        float a1 = fmaf(kf[4], qb.x, fmaf(kf[5], qb.y, fmaf(kf[6], qb.z, kf[7] * qb.w)));
-        s_[hh] += a0 + a1;
-      }
-    }
-    const bool valid = blk * kBlockTok + t < ntok;
-#pragma unroll
-    for (int hh = 0; hh < G; ++hh) {
-      float sc = s_[hh] + __shfl_xor_sync(0xffffffffu, s_[hh], 1);
-      sc = valid ? sc : -INFINITY;
-      const float mn = fmaxf(m[hh], warp_max(sc));
-      const float p = valid ? __expf(sc - mn) : 0.f;
-      const float bs = warp_sum(p) * 0.5f;
-      const float corr = __expf(m[hh] - mn);
-      l[hh] = l[hh] * corr + bs;
-      m[hh] = mn;
-#pragma unroll
-      for (int j = 0; j < Frag<D>::kPvDims; ++j) acc[hh][j] *= corr;
-      if (half == 0) s_p[warp][hh][t] = p;
-    }
-    __syncwarp();
-    const char* vt = st + Ring<D>::kTile;
-    const int vchunk = lane * Frag<D>::kPvDims * 2 / 16, voff = (lane * Frag<D>::kPvDims * 2) % 16;
-#pragma unroll
-    for (int t2 = 0; t2 < kBlockTok; ++t2) {
-      float vf[Frag<D>::kPvDims];
-      const char* vp = vt + rswz<D>(t2, vchunk) + voff;
-      if constexpr (Frag<D>::kPvDims == 4) {
-        const uint2 x = *reinterpret_cast<const uint2*>(vp);
-        const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&x.x));
-        const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&x.y));
-        vf[0] = f0.x; vf[1] = f0.y; vf[2] = f1.x; vf[3] = f1.y;
-      } else {
-        const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(vp));
-        vf[0] = f0.x; vf[1] = f0.y;
-      }
-#pragma unroll
-      for (int hh = 0; hh < G; ++hh) {
-        const float p = s_p[warp][hh][t2];
-#pragma unroll
-        for (int j = 0; j < Frag<D>::kPvDims; ++j) acc[hh][j] = fmaf(p, vf[j], acc[hh][j]);
-      }
-    }
+    attend_block<D, G>(my_ring + (it % S) * Ring<D>::kStage, lo + warp + it * kAttnWarps, ntok, s_q, s_p[warp], m,
+                       l, acc, lane);
     __syncwarp();
   }
   cp_wait_n<0>();
