@@ -42,15 +42,48 @@ struct Frag {
   static constexpr int kPvDims = D / 32;         // dims per lane in PV
 };
 
-__device__ __forceinline__ float warp_max(float v) {
+
+// Online-softmax update for one 16-token block, all G query heads at once.
+// Lanes 2t and 2t+1 hold the two halves of token t's dot products; after the
+// xor-1 shuffle both hold the full score.  The block max and sum reduce over
+// lane bits 1-4 only (each token once), and the G heads' shuffles are
+// interleaved, so the dependent chain is 1 + 4 + 4 shuffles per block rather
+// than 11 per head.
+template <int G, int PV>
+__device__ __forceinline__ void block_softmax(const float (&s)[G], bool valid, float (&m)[G], float (&l)[G],
+                                              float (&acc)[G][PV], float (*s_p)[kBlockTok], int t, int half) {
+  float sc[G], red[G];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__device__ __forceinline__ float warp_sum(float v) {
+  for (int hh = 0; hh < G; ++hh) {
+    sc[hh] = s[hh] + __shfl_xor_sync(0xffffffffu, s[hh], 1);
+    sc[hh] = valid ? sc[hh] : -INFINITY;
+    red[hh] = sc[hh];
+  }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+  for (int o = 2; o < 32; o <<= 1)
+#pragma unroll
+    for (int hh = 0; hh < G; ++hh) red[hh] = fmaxf(red[hh], __shfl_xor_sync(0xffffffffu, red[hh], o));
+  float p[G];
+#pragma unroll
+  for (int hh = 0; hh < G; ++hh) {
+    const float mn = fmaxf(m[hh], red[hh]);
+    p[hh] = valid ? __expf(sc[hh] - mn) : 0.f;
+    const float corr = __expf(m[hh] - mn);      // 0 on the first block (m = -inf)
+    m[hh] = mn;
+    l[hh] *= corr;
+#pragma unroll
+    for (int j = 0; j < PV; ++j) acc[hh][j] *= corr;
+    red[hh] = p[hh];
+  }
+#pragma unroll
+  for (int o = 2; o < 32; o <<= 1)
+#pragma unroll
+    for (int hh = 0; hh < G; ++hh) red[hh] += __shfl_xor_sync(0xffffffffu, red[hh], o);
+#pragma unroll
+  for (int hh = 0; hh < G; ++hh) {
+    l[hh] += red[hh];
+    if (half == 0) s_p[hh][t] = p[hh];
+  }
 }
 
 template <int D>
@@ -177,20 +210,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_split(
       }
     }
     const bool valid = blk * kBlockTok + t < ntok;
-#pragma unroll
-    for (int hh = 0; hh < G; ++hh) {
-      float sc = s[hh] + __shfl_xor_sync(0xffffffffu, s[hh], 1);
-      sc = valid ? sc : -INFINITY;
-      const float mn = fmaxf(m[hh], warp_max(sc));
-      const float p = valid ? __expf(sc - mn) : 0.f;
-      const float bs = warp_sum(p) * 0.5f;        // every token is counted by its two lanes
-      const float corr = __expf(m[hh] - mn);      // 0 on the first block (m = -inf)
-      l[hh] = l[hh] * corr + bs;
-      m[hh] = mn;
-#pragma unroll
-      for (int j = 0; j < Frag<D>::kPvDims; ++j) acc[hh][j] *= corr;
-      if (half == 0) s_p[warp][hh][t] = p;
-    }
+    block_softmax<G, Frag<D>::kPvDims>(s, valid, m, l, acc, s_p[warp], t, half);
     __syncwarp();
     // PV: this lane owns dims [lane * kPvDims, +kPvDims)
 #pragma unroll
@@ -292,20 +312,7 @@ __device__ __forceinline__ void attend_block(const char* st, int blk, int ntok, 
       }
     }
     const bool valid = blk * kBlockTok + t < ntok;
-#pragma unroll
-    for (int hh = 0; hh < G; ++hh) {
-      float sc = s_[hh] + __shfl_xor_sync(0xffffffffu, s_[hh], 1);
-      sc = valid ? sc : -INFINITY;
-      const float mn = fmaxf(m[hh], warp_max(sc));
-      const float p = valid ? __expf(sc - mn) : 0.f;
-      const float bs = warp_sum(p) * 0.5f;
-      const float corr = __expf(m[hh] - mn);
-      l[hh] = l[hh] * corr + bs;
-      m[hh] = mn;
-#pragma unroll
-      for (int j = 0; j < Frag<D>::kPvDims; ++j) acc[hh][j] *= corr;
-      if (half == 0) s_p[hh][t] = p;
-    }
+    block_softmax<G, Frag<D>::kPvDims>(s_, valid, m, l, acc, s_p, t, half);
     __syncwarp();
     const char* vt = st + Ring<D>::kTile;
     const int vchunk = lane * Frag<D>::kPvDims * 2 / 16, voff = (lane * Frag<D>::kPvDims * 2) % 16;
