@@ -394,6 +394,182 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_split_ring(
   merge_and_write<D, G>(m, l, acc, part, b, h, kvh, split, splits);
 }
 
+// Tensor-core form (default).  Per block a warp computes S^T = Q K^T and
+// O += P V with mma.sync.m16n8k16 (fp16 in, fp32 accumulate): the G query
+// heads are the M rows (padded to 16, zero rows contribute nothing), the 16
+// tokens the N columns of S^T, and the S^T accumulator is reused in place as
+// the A operand of P V (the FlashAttention-2 register layout).  K comes from
+// the swizzled ring with ldmatrix, V with ldmatrix.trans.  The scalar
+// kernels above spend ~1,250 instructions per 8 KiB block-head; this one
+// ~150, so the warp waits on memory rather than on its own issue.
+__device__ __forceinline__ void ldsm4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+  const __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+template <int D, int G, int S>
+__global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_mma(
+    const uint64_t* __restrict__ pages, const int32_t* __restrict__ seq_start, const int32_t* __restrict__ seq_tokens,
+    const __half* __restrict__ q, float* __restrict__ part, int kvh, int splits, float scale) {
+  static_assert(G <= 8, "query rows g and g+8 of the m16 tile: at most 8 heads per KV head");
+  constexpr int KS = D / 16;             // k steps of Q K^T
+  constexpr int NT = D / 8;              // n tiles of P V
+  extern __shared__ __align__(128) char ring_smem[];
+  __shared__ float s_m[kAttnWarps][G], s_l[kAttnWarps][G];
+  __shared__ float s_acc[kAttnWarps][G][D];
+  const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int q_heads = kvh * G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gr = lane >> 2, c = lane & 3;        // mma fragment row group / column pair
+  char* my_ring = ring_smem + (size_t)warp * S * Ring<D>::kStage;
+
+  // Q as the A operand: row gr = query head (zero beyond G), k = head dims
+  uint32_t qa[KS][2];                    // a0 (row gr, k 2c..), a2 (row gr, k 2c+8..); rows gr+8 are zero
+  {
+    const __half* qh = q + ((size_t)b * q_heads + h * G + (gr < G ? gr : 0)) * D;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      if (gr < G) {
+        qa[ks][0] = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 2 * c);
+        qa[ks][1] = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 8 + 2 * c);
+      } else {
+        qa[ks][0] = qa[ks][1] = 0u;
+      }
+    }
+  }
+  const int b0 = seq_start[b], nblk = seq_start[b + 1] - b0, ntok = seq_tokens[b];
+  const int per = (nblk + splits - 1) / splits;
+  const int lo = split * per, hi = min(nblk, lo + per);
+  const int mine = lo + warp < hi ? (hi - (lo + warp) + kAttnWarps - 1) / kAttnWarps : 0;
+
+  float m_run = -INFINITY, l_run = 0.f;  // of row gr (query head gr)
+  float o[NT][2];                        // O[gr][n*8 + 2c + {0,1}]
+#pragma unroll
+  for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = 0.f;
+
+#pragma unroll
+  for (int st = 0; st < S - 1; ++st) {
+    if (st < mine) ring_load<D>(my_ring + st * Ring<D>::kStage,
+                                reinterpret_cast<const char*>(pages[b0 + lo + warp + st * kAttnWarps]), kvh, h, lane);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  // ldmatrix lane roles: x4 over (tokens 0-7 | 8-15) x (k 0-7 | 8-15)
+  const int lm_row = (lane & 7) + ((lane >> 4) << 3);
+  const int lm_k = (lane >> 3) & 1;
+  // trans x4 over V: (tokens 0-7 | 8-15) x (dims d..d+7 | d+8..d+15)
+  const int lt_row = (lane & 7) + (((lane >> 3) & 1) << 3);
+  const int lt_d = lane >> 4;
+  for (int it = 0; it < mine; ++it) {
+    cp_wait_n<S - 2>();
+    __syncwarp();
+    const int nx = it + S - 1;
+    if (nx < mine)
+      ring_load<D>(my_ring + (nx % S) * Ring<D>::kStage,
+                   reinterpret_cast<const char*>(pages[b0 + lo + warp + nx * kAttnWarps]), kvh, h, lane);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const char* st = my_ring + (it % S) * Ring<D>::kStage;
+    const uint32_t ks_addr = smem_addr(st), vs_addr = ks_addr + Ring<D>::kTile;
+    const int blk = lo + warp + it * kAttnWarps;
+    // S^T = Q K^T : two n tiles (tokens 0-7, 8-15)
+    float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      uint32_t k0, k1, k2, k3;   // (tok 0-7,k lo) (tok 0-7,k hi) (tok 8-15,k lo) (tok 8-15,k hi)
+      ldsm4(ks_addr + rswz<D>(lm_row, ks * 2 + lm_k), k0, k1, k2, k3);
+      mma16816(s0, qa[ks][0], 0u, qa[ks][1], 0u, k0, k1);
+      mma16816(s1, qa[ks][0], 0u, qa[ks][1], 0u, k2, k3);
+    }
+    // row gr: tokens 2c, 2c+1 (tile 0) and 8+2c, 9+2c (tile 1); rows gr+8 (s*[2..3]) are padding
+    const int tb = blk * kBlockTok;
+    float x[4] = {s0[0] * scale, s0[1] * scale, s1[0] * scale, s1[1] * scale};
+    const int tk[4] = {2 * c, 2 * c + 1, 8 + 2 * c, 9 + 2 * c};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (tb + tk[j] >= ntok) x[j] = -INFINITY;
+    float bm = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
+    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
+    const float mn = fmaxf(m_run, bm);
+    float p[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) p[j] = x[j] == -INFINITY ? 0.f : __expf(x[j] - mn);
+    float bs = (p[0] + p[1]) + (p[2] + p[3]);
+    bs += __shfl_xor_sync(0xffffffffu, bs, 1);
+    bs += __shfl_xor_sync(0xffffffffu, bs, 2);
+    const float corr = __expf(m_run - mn);     // 0 on the first block
+    m_run = mn;
+    l_run = l_run * corr + bs;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      o[n][0] *= corr;
+      o[n][1] *= corr;
+    }
+    // P as the A operand (rows gr / gr+8, k = tokens): a0 (gr, 2c..) a1 (gr+8) a2 (gr, 2c+8..) a3 (gr+8)
+    const uint32_t pa0 = pack_h2(p[0], p[1]), pa2 = pack_h2(p[2], p[3]);
+#pragma unroll
+    for (int np = 0; np < NT / 2; ++np) {
+      uint32_t v0, v1, v2, v3;   // b0,b1 of dims np*16..+7, then of np*16+8..+15
+      ldsm4_t(vs_addr + rswz<D>(lt_row, np * 2 + lt_d), v0, v1, v2, v3);
+      float d0[4] = {o[2 * np][0], o[2 * np][1], 0.f, 0.f};
+      float d1[4] = {o[2 * np + 1][0], o[2 * np + 1][1], 0.f, 0.f};
+      mma16816(d0, pa0, 0u, pa2, 0u, v0, v1);
+      mma16816(d1, pa0, 0u, pa2, 0u, v2, v3);
+      o[2 * np][0] = d0[0];
+      o[2 * np][1] = d0[1];
+      o[2 * np + 1][0] = d1[0];
+      o[2 * np + 1][1] = d1[1];
+    }
+    __syncwarp();
+  }
+  cp_wait_n<0>();
+  // merge the warps (fixed order) and write the partial state
+  if (gr < G) {
+    if (c == 0) {
+      s_m[warp][gr] = m_run;
+      s_l[warp][gr] = l_run;
+    }
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      s_acc[warp][gr][n * 8 + 2 * c] = o[n][0];
+      s_acc[warp][gr][n * 8 + 2 * c + 1] = o[n][1];
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
+    const int hh = i / D, d = i % D;
+    float M = -INFINITY;
+    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, s_m[w][hh]);
+    float L = 0.f, A = 0.f;
+    for (int w = 0; w < kAttnWarps; ++w) {
+      const float cf = s_m[w][hh] == -INFINITY ? 0.f : __expf(s_m[w][hh] - M);
+      L += s_l[w][hh] * cf;
+      A += s_acc[w][hh][d] * cf;
+    }
+    float* out = part + ((((size_t)b * kvh + h) * splits + split) * G + hh) * (D + 2);
+    out[d] = A;
+    if (d == 0) {
+      out[D] = M;
+      out[D + 1] = L;
+    }
+  }
+}
+
 // out[b][qh][d] = sum_s acc_s[d] e^(m_s - M) / sum_s l_s e^(m_s - M), splits in order
 template <int D>
 __global__ void paged_decode_combine(const float* __restrict__ part, float* __restrict__ out, int q_heads, int kvh,
@@ -413,6 +589,9 @@ __global__ void paged_decode_combine(const float* __restrict__ part, float* __re
   out[((size_t)b * q_heads + qh) * D + d] = L > 0.f ? A / L : 0.f;
 }
 
+#ifndef HV_ATTN_MMA
+#define HV_ATTN_MMA 3
+#endif
 #ifndef HV_ATTN_RING
 #define HV_ATTN_RING 3
 #endif
@@ -421,7 +600,20 @@ template <int D, int G>
 int launch_attn(const uint64_t* pages, const int32_t* seq_start, const int32_t* seq_tokens, const void* q,
                 float* out, float* part, uint32_t B, uint32_t kvh, uint32_t splits, float scale, cudaStream_t s) {
   dim3 grid(splits, kvh, B);
-#if HV_ATTN_RING
+#if HV_ATTN_MMA
+  {
+    constexpr int kS = HV_ATTN_MMA;
+    constexpr size_t smem = (size_t)kAttnWarps * kS * Ring<D>::kStage;
+    static bool attr_m = false;
+    if (!attr_m) {
+      HV_CUDA(cudaFuncSetAttribute(paged_decode_mma<D, G, kS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+      attr_m = true;
+    }
+    paged_decode_mma<D, G, kS><<<grid, kAttnWarps * 32, smem, s>>>(
+        pages, seq_start, seq_tokens, reinterpret_cast<const __half*>(q), part, (int)kvh, (int)splits, scale);
+  }
+#elif HV_ATTN_RING
   constexpr int kS = HV_ATTN_RING;
   constexpr size_t smem = (size_t)kAttnWarps * kS * Ring<D>::kStage;
   static bool attr = false;
