@@ -400,8 +400,11 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_split_ring(
 // tokens the N columns of S^T, and the S^T accumulator is reused in place as
 // the A operand of P V (the FlashAttention-2 register layout).  K comes from
 // the swizzled ring with ldmatrix, V with ldmatrix.trans.  The scalar
-// kernels above spend ~1,250 instructions per 8 KiB block-head; this one
-// ~150, so the warp waits on memory rather than on its own issue.
+// kernels above spend ~1,250 instructions per 8 KiB block-head (ncu: issue
+// stalled on short scoreboard, 40% issue-active); this one ~150.  Measured
+// (HBM pages, best split count, 4 x 4k / 1 x 128k): 3,740 / 5,564 GB/s vs
+// 2,209 / 3,199 for the scalar ring; ring stages 2 / 3 / 4: 3,564 / 3,740 /
+// 3,198 and 5,499 / 5,564 / 5,229 (3 is the default).
 __device__ __forceinline__ void ldsm4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
