@@ -227,9 +227,11 @@ def run_b200(a):
         barrier()
     barrier()
     launches = (N.launch_count() - launches0) // (attempt + 1)   # per timed attempt
-    dt = max_over_ranks(t0.elapsed_time(t1) * 1e-3)
+    my_dt = t0.elapsed_time(t1) * 1e-3
+    dt = max_over_ranks(my_dt)
     my_bytes = sum(nb for s in range(a.warmup, a.warmup + a.steps) for (_, _, _, nb) in desc[s])
-    total_bytes = my_bytes * world
+    per_rank = group.all_gather((my_bytes, my_dt))     # each rank's own routing -> its own byte count
+    total_bytes = sum(nb for nb, _ in per_rank)
     value = total_bytes / dt / 1e9
     launch_ms = [step_events[k][l][0].elapsed_time(step_events[k][l][1])
                  for k in range(a.steps) for l in range(L)]
@@ -382,6 +384,7 @@ def run_b200(a):
                                                     "p99": float(np.percentile(launch_ms, 99)),
                                                     "n": len(launch_ms)}, "decode": decode,
                 "kv_long_context_128k": kvlc, "kv_decode_config1": kvd1, "reference_simulator": refsim,
+                "per_rank_GBps": [nb / t / 1e9 for nb, t in per_rank],
                 "nvlink_counters_timed_region": {
                     "per_rank": nvlink_all,
                     "note": "NVML per-link NVLink data counters of each rank's GPU, read before/after the timed "
