@@ -46,9 +46,10 @@ class KVAttentionDecoder:
     def __init__(self, kv, sequences, q_heads: int, tokens: int | None = None, seed: int = 0,
                  engine: str | None = None, max_ctas: int | None = None, trace: bool = False,
                  fused: bool = False, splits: int | None = None):
-        """``sequences``: sequence ids of the batch, all with the same token
-        count (``tokens``, default: the first sequence's).  Queries are
-        synthetic: one random fp16 query per (layer, sequence, q head)."""
+        """``sequences``: sequence ids of the batch (any lengths; each attends
+        over all of its tokens, or the first ``tokens`` of each when given).
+        Queries are synthetic: one random fp16 query per (layer, sequence,
+        q head)."""
         m = kv.m
         if q_heads % m.kv_heads:
             raise ValueError("q_heads must be a multiple of kv_heads (grouped-query attention)")
@@ -56,12 +57,11 @@ class KVAttentionDecoder:
         self.seqs = list(sequences)
         self.B, self.L, self.Hq = len(self.seqs), m.num_layers, q_heads
         blocks = [kv.seq_blocks[s] for s in self.seqs]
-        self.nb = len(blocks[0])
-        if any(len(b) != self.nb for b in blocks):
-            raise ValueError("all sequences of the batch need the same number of blocks")
-        full = self.nb * m.block_tokens
-        last = kv.table[blocks[0][-1]].entries
-        self.T = tokens if tokens is not None else full - m.block_tokens + last
+        if any(not b for b in blocks):
+            raise ValueError("every sequence of the batch needs at least one block")
+        lens = [sum(kv.table[bid].entries for bid in b) for b in blocks]
+        self.tokens = [min(n, tokens) if tokens is not None else n for n in lens]
+        self.T = max(self.tokens)
         self.ids = [bid for b in blocks for bid in b]            # sequence-major block order
         self.dev = torch.device(kv.dev)
         self.engine = engine if engine is not None else kv.engine
@@ -79,8 +79,10 @@ class KVAttentionDecoder:
                           for b in self.bufs]
         g = torch.Generator().manual_seed(seed)
         self.q = (torch.randn(self.L, self.B, q_heads, m.head_dim, generator=g)).to(torch.float16).to(self.dev)
-        self.seq_start = (torch.arange(self.B + 1, dtype=torch.int32) * self.nb).to(self.dev)
-        self.seq_tokens = torch.full((self.B,), self.T, dtype=torch.int32, device=self.dev)
+        starts = np.concatenate([[0], np.cumsum([len(b) for b in blocks])]).astype(np.int32)
+        self.seq_start = torch.from_numpy(starts).to(self.dev)
+        self.seq_tokens = torch.tensor(self.tokens, dtype=torch.int32, device=self.dev)
+        self.nb = max(len(b) for b in blocks)
         # flash-decoding splits: one wave of (sequence, KV head, split) CTAs at
         # the kernel's two resident CTAs per SM.  Measured on B200 (tools/
         # attn_probe.py, HBM pages): 4 x 4k: 8 splits 36 us, 19: 41, 64: 56;

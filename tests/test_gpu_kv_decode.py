@@ -17,7 +17,7 @@ def _model():
     return KVModelSpec("tiny-kv", num_layers=3, kv_heads=2, head_dim=64)
 
 
-def _cache(local_blocks, donor_slabs, durability="BACKED", seqs=2, tokens=50):
+def _cache(local_blocks, donor_slabs, durability="BACKED", seqs=2, tokens=50, lengths=None):
     from paper_2602_00328_b200.kv import KVCacheManager
     from paper_2602_00328_b200.runtime import Durability
     from paper_2602_00328_b200.system import HarvestSystem
@@ -28,7 +28,7 @@ def _cache(local_blocks, donor_slabs, durability="BACKED", seqs=2, tokens=50):
     kv = KVCacheManager(sysm, m, local_blocks, host_blocks=64, slab_blocks=slab_blocks,
                         durability=Durability[durability], content="fp16")
     for s in range(seqs):
-        kv.append_kv(s, tokens)
+        kv.append_kv(s, lengths[s] if lengths else tokens)
     return sysm, kv, m
 
 
@@ -41,8 +41,8 @@ def _reference(kv, m, dec):
                      for bid in kv.seq_blocks[s]]
             a = torch.from_numpy(np.concatenate(pages).view(np.float16).astype(np.float32))
             a = a.view(len(pages), 2, m.block_tokens, m.kv_heads, m.head_dim)
-            k = a[:, 0].reshape(-1, m.kv_heads, m.head_dim)[:dec.T]
-            v = a[:, 1].reshape(-1, m.kv_heads, m.head_dim)[:dec.T]
+            k = a[:, 0].reshape(-1, m.kv_heads, m.head_dim)[:dec.tokens[bi]]
+            v = a[:, 1].reshape(-1, m.kv_heads, m.head_dim)[:dec.tokens[bi]]
             q = dec.q[layer, bi].float().cpu()                             # [Hq, D]
             g = dec.Hq // m.kv_heads
             kk = k.repeat_interleave(g, dim=1).transpose(0, 1)             # [Hq, T, D]
@@ -151,4 +151,21 @@ def test_fused_in_place_equals_gathered():
     assert (a - c).abs().max().item() <= 1e-5          # another split count: same math, other order
     sysm.loop.run()
     assert verify_release_ordering(sysm.loop.log) == []
+    kv.close(); sysm.close()
+
+
+def test_ragged_batch_in_place_matches_fp32():
+    """Sequences of different lengths in one batch (per-sequence block ranges
+    and token counts), pages spread over local, peer and host."""
+    from paper_2602_00328_b200.kv_decode import KVAttentionDecoder
+    sysm, kv, m = _cache(local_blocks=4, donor_slabs=1, seqs=3, lengths=[50, 17, 96])
+    dec = KVAttentionDecoder(kv, [0, 1, 2], q_heads=4, seed=9, fused=True)
+    assert dec.tokens == [50, 17, 96]
+    out = dec.step()
+    gat = KVAttentionDecoder(kv, [0, 1, 2], q_heads=4, seed=9).step()
+    torch.cuda.synchronize()
+    assert torch.equal(out, gat)
+    ref = _reference(kv, m, dec)
+    assert (out.float().cpu() - ref).abs().max().item() <= 2e-2
+    sysm.loop.run()
     kv.close(); sysm.close()
