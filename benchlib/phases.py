@@ -84,7 +84,7 @@ def kv_long_context(sysm, source, a):
     """Config 4: a 128k-token Llama-3-8B sequence (8,192 blocks x 32 layers x
     64 KiB = 16 GiB) is appended (KV produced locally), evicted out of local
     HBM to harvested peer slabs (N>1, Lossy) or the host tier (N=1, Backed),
-    then reloaded with ONE K1 launch of 262,144 pages.  Reports the kernel
+    then reloaded (262,144 pages, K1 launched per 1,024 blocks).  Reports the kernel
     time, the end-to-end reload() time, and a content check of sampled pages."""
     from paper_2602_00328_b200 import fetch as F
     from paper_2602_00328_b200.kv import LLAMA3_8B, KVCacheManager, kv_seed

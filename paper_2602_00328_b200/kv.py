@@ -20,11 +20,12 @@ KV tensors, so page (l, b) of block b lives at ``base[b] + l * stride[b]``:
 Peer memory is taken in slabs of ``slab_blocks`` blocks through
 ``harvest_alloc`` (one revocable handle per slab, not per 64 KiB page); a slab
 revocation invalidates its blocks: Backed blocks fall back to their host copy,
-Lossy blocks become NotMaterialized (recompute).  Every data movement of an
-evict/reload call (all pages of all blocks, all layers) is ONE K1 launch
+Lossy blocks become NotMaterialized (recompute).  The data movement of an
+evict/reload call (all pages of all blocks, all layers) is K1
 (``hv_kv_gather_blocks``) over four per-block arrays (source base/stride,
-destination base/stride) resolved from the table on the host and uploaded
-once; the per-layer gather resolves one pointer per page.
+destination base/stride) resolved from the table on the host, launched every
+``launch_chunk_blocks`` blocks so the device copies one chunk while the host
+resolves the next; the per-layer gather resolves one pointer per page.
 """
 from __future__ import annotations
 
@@ -334,7 +335,7 @@ class KVCacheManager:
     def evict(self, bytes_needed: int) -> list[tuple[int, str, str]]:
         """Move LRU/FIFO/tail blocks out of local HBM: to a peer slab when one can
         be harvested (Backed blocks also keep a host copy), else to host.
-        All page copies of the call are one K1 launch."""
+        The page copies go out as K1 launches of launch_chunk_blocks blocks."""
         if bytes_needed <= 0:
             raise ValueError("bytes_needed must be > 0")
         n_blocks = -(-bytes_needed // self.m.block_bytes)
@@ -432,7 +433,8 @@ class KVCacheManager:
 
     @annotate("harvest.kv_reload")
     def reload(self, block_ids) -> dict:
-        """Bring blocks to LocalHBM from their resident tier in ONE K1 launch.
+        """Bring blocks to LocalHBM from their resident tier (K1, one launch per
+        launch_chunk_blocks resolved blocks, pipelined with the resolution).
         Revoked-peer blocks resolve through resolve_fallback; Lossy blocks
         without a host copy are recomputed (content regenerated)."""
         table, LOCAL, PEER, HOST, NM = self.table, KVTier.LOCAL_HBM, KVTier.PEER_HBM, KVTier.HOST_DRAM, \
