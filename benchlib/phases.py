@@ -167,6 +167,14 @@ def _kv_decode_measure(kv, seqs, sysm, steps=3, q_heads=32):
     # the same attention straight over the resident pages (no K1 gather)
     fdec = KVAttentionDecoder(kv, seqs, q_heads=q_heads, seed=1, fused=True)
     fused_out, fused_ms = timed(fdec)
+    graphs = {}
+    for name, fz in (("gather", False), ("in_place", True)):   # each step one upload + one graph replay
+        gdec = KVAttentionDecoder(kv, seqs, q_heads=q_heads, seed=1, fused=fz)
+        gdec.capture_graph()
+        g_out, g_ms = timed(gdec)
+        graphs[name] = {"ms_per_step": g_ms, "tokens_per_s": len(seqs) / (g_ms * 1e-3),
+                        "outputs_bit_identical_to_eager": bool(torch.equal(g_out, tier_out))}
+        del gdec
     sysm.loop.run()
     nbytes = len(dec.ids) * kv.m.block_bytes
     return {"batch": len(seqs), "context_tokens": dec.T, "kv_bytes_per_step": nbytes, "kv_in": where,
@@ -179,7 +187,8 @@ def _kv_decode_measure(kv, seqs, sysm, steps=3, q_heads=32):
             "fused_in_place": {"ms_per_step": fused_ms, "tokens_per_s": len(seqs) / (fused_ms * 1e-3),
                                "kv_GBps": nbytes / (fused_ms * 1e-3) / 1e9,
                                "outputs_bit_identical_to_gathered": bool(torch.equal(fused_out, tier_out))},
-            "attention": "hv_paged_decode_attention (split-K flash decoding over page pointers)",
+            "cuda_graph": graphs,
+            "attention": "hv_paged_decode_attention (split-K flash decoding over page pointers, tensor cores)",
             "overlap_traced_step": ov,
             "model": f"{kv.m.name}: GQA {q_heads} q heads over {kv.m.kv_heads} KV heads, per-layer K1 gather "
                      "(fetch stream) overlapped with attention (compute stream)"}

@@ -99,24 +99,18 @@ class KVAttentionDecoder:
         self.compute = torch.cuda.Stream(self.dev)
         self.trace = trace
         self._tr: dict = {}
-        self._keep: list = []
+        self._graph = None
+        self._tab_dev = torch.empty(2, len(self.ids), dtype=torch.int64, device=self.dev)
+        self._layers = torch.arange(self.L, dtype=torch.int64, device=self.dev).unsqueeze(1)
 
-    def _sources(self) -> tuple[torch.Tensor, list]:
-        """[L, n] page addresses of this step (one upload, one broadcast)."""
+    def _upload_table(self) -> list:
+        """Resolve the block table on the host and copy it (pinned, async) into
+        the decoder's device table on the current stream, ordered after every
+        earlier step and before this one.  Returns the peer handles read."""
         bases, strides, handles = self.kv.page_table(self.ids)
         tab = torch.from_numpy(np.stack([bases, strides]).view(np.int64)).pin_memory()
-        # every tensor of the table is allocated and written on the fetch
-        # stream, the stream that first reads it (the caching allocator
-        # reuses a block only in stream order of the stream it belongs to)
-        with torch.cuda.stream(self.fetch):
-            d = torch.empty(tab.shape, dtype=torch.int64, device=self.dev)
-            N.call("hv_memcpy_h2d", d.data_ptr(), tab.data_ptr(), tab.numel() * 8, self.fetch_h)
-            layers = torch.arange(self.L, dtype=torch.int64, device=self.dev).unsqueeze(1)
-            src = d[0].unsqueeze(0) + layers * d[1].unsqueeze(0)
-        if self.fused:                      # read by the attention on the compute stream
-            src.record_stream(self.compute)
-        self._keep = (self._keep + [(tab, d)])[-2:]   # the last two steps' uploads stay alive
-        return src, handles
+        self._tab_dev.copy_(tab, non_blocking=True)
+        return handles
 
     def _attend(self, layer: int, pages: torch.Tensor) -> torch.Tensor:
         """hv_paged_decode_attention over the page table `pages` [n] (int64)."""
@@ -127,22 +121,23 @@ class KVAttentionDecoder:
                m.head_dim, m.block_tokens, self.splits, self.scale, torch.cuda.current_stream(self.dev).cuda_stream)
         return out
 
-    def step(self) -> torch.Tensor:
-        """One decode step over all layers: returns the attention outputs [L, B, Hq, D]."""
-        rt = self.kv.rt
-        from .kv import KVTier
-        lost = [bid for bid in self.ids if self.kv.table[bid].tier is KVTier.NOT_MATERIALIZED]
-        if lost:                            # Lossy blocks revoked since the last step: recompute
-            self.kv.reload(lost)
+    def _run(self) -> torch.Tensor:
+        """The device work of a step over the uploaded table: per-layer page
+        addresses (one broadcast), then the gathers and attention (or the
+        attention alone, in place).  Host-free, so it can be graph-captured."""
         cur = torch.cuda.current_stream(self.dev)
         self.fetch.wait_stream(cur)
         self.compute.wait_stream(cur)
-        src, handles = self._sources()
-        batch = rt.begin_reads(handles) if handles else None
+        # allocated on the stream that writes them first; the in-place
+        # attention reads them on the compute stream after a stream wait
+        with torch.cuda.stream(self.fetch):
+            src = self._tab_dev[0].unsqueeze(0) + self._layers * self._tab_dev[1].unsqueeze(0)
         outs = [None] * self.L
         if self.fused:                      # attention straight over the resident pages
             with torch.cuda.stream(self.compute):
-                self.compute.wait_stream(self.fetch)     # the page table upload
+                self.compute.wait_stream(self.fetch)
+                if not torch.cuda.is_current_stream_capturing():   # graph pools are never recycled mid-replay
+                    src.record_stream(self.compute)
                 for layer in range(self.L):
                     if self.trace:
                         c0 = torch.cuda.Event(enable_timing=True)
@@ -152,42 +147,78 @@ class KVAttentionDecoder:
                         c1 = torch.cuda.Event(enable_timing=True)
                         c1.record(self.compute)
                         self._tr[layer] = {"fetch": (c0, c0), "compute": (c0, c1)}
-            return self._finish(cur, batch, outs)
-        consumed = [None, None]
-        for layer in range(self.L):
-            b = layer % 2
-            if consumed[b] is not None:
-                self.fetch.wait_event(consumed[b])
-            if self.trace:
-                f0 = torch.cuda.Event(enable_timing=True)
-                f0.record(self.fetch)
-            F.kv_gather(src[layer], self.page, dst=self.bufs[b], engine=self.engine, max_ctas=self.max_ctas,
-                        stream=self.fetch_h)
-            got = torch.cuda.Event(enable_timing=self.trace)
-            got.record(self.fetch)
-            with torch.cuda.stream(self.compute):
-                self.compute.wait_event(got)
+        else:
+            consumed = [None, None]
+            for layer in range(self.L):
+                b = layer % 2
+                if consumed[b] is not None:
+                    self.fetch.wait_event(consumed[b])
                 if self.trace:
-                    c0 = torch.cuda.Event(enable_timing=True)
-                    c0.record(self.compute)
-                outs[layer] = self._attend(layer, self.buf_pages[b])
-                done = torch.cuda.Event(enable_timing=self.trace)
-                done.record(self.compute)
-                consumed[b] = done
-            if self.trace:
-                self._tr[layer] = {"fetch": (f0, got), "compute": (c0, done)}
-        return self._finish(cur, batch, outs)
-
-    def _finish(self, cur, batch, outs) -> torch.Tensor:
+                    f0 = torch.cuda.Event(enable_timing=True)
+                    f0.record(self.fetch)
+                F.kv_gather(src[layer], self.page, dst=self.bufs[b], engine=self.engine, max_ctas=self.max_ctas,
+                            stream=self.fetch_h)
+                got = torch.cuda.Event(enable_timing=self.trace)
+                got.record(self.fetch)
+                with torch.cuda.stream(self.compute):
+                    self.compute.wait_event(got)
+                    if self.trace:
+                        c0 = torch.cuda.Event(enable_timing=True)
+                        c0.record(self.compute)
+                    outs[layer] = self._attend(layer, self.buf_pages[b])
+                    done = torch.cuda.Event(enable_timing=self.trace)
+                    done.record(self.compute)
+                    consumed[b] = done
+                if self.trace:
+                    self._tr[layer] = {"fetch": (f0, got), "compute": (c0, done)}
         cur.wait_stream(self.compute)
         cur.wait_stream(self.fetch)
+        return torch.stack(outs)
+
+    def step(self) -> torch.Tensor:
+        """One decode step over all layers: returns the attention outputs
+        [L, B, Hq, D] (after capture_graph(), a buffer the next step reuses)."""
+        from .kv import KVTier
+        rt = self.kv.rt
+        lost = [bid for bid in self.ids if self.kv.table[bid].tier is KVTier.NOT_MATERIALIZED]
+        if lost:                            # Lossy blocks revoked since the last step: recompute
+            self.kv.reload(lost)
+        handles = self._upload_table()
+        batch = rt.begin_reads(handles) if handles else None
+        if self._graph is not None:
+            self._graph.replay()
+            out = self._graph_out
+        else:
+            out = self._run()
         if batch is not None:               # the drain completes when the step's reads have
             fin = torch.cuda.Event()
-            fin.record(cur)
+            fin.record(torch.cuda.current_stream(self.dev))
             self.fetch.wait_event(fin)
-            rt = self.kv.rt
             self.kv.sys.engine.track([lambda _x, bt=batch: rt.end_reads(bt)])
-        return torch.stack(outs)
+        return out
+
+    def capture_graph(self) -> None:
+        """Capture the device work of a step (the table broadcast, every K1
+        gather and K5 attention, both streams) as one CUDA graph; each later
+        step() is the table upload plus one replay."""
+        if self.trace:
+            raise ValueError("trace mode records per-launch events; capture without trace")
+        if self._graph is not None:
+            return
+        self._upload_table()
+        cur = torch.cuda.current_stream(self.dev)
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):       # warm-up outside capture (allocator, lazy attributes)
+            for _ in range(2):
+                self._run()
+        cur.wait_stream(side)
+        torch.cuda.synchronize(self.dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._graph_out = self._run()
+        torch.cuda.synchronize(self.dev)
+        self._graph = g
 
     def overlap_report(self) -> dict:
         """Device-clock gather / attention intervals of the last traced step."""

@@ -169,3 +169,29 @@ def test_ragged_batch_in_place_matches_fp32():
     assert (out.float().cpu() - ref).abs().max().item() <= 2e-2
     sysm.loop.run()
     kv.close(); sysm.close()
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_graph_replay_equals_eager_across_revocation(fused):
+    """capture_graph(): a step is one table upload plus one CUDA graph replay
+    (broadcast, K1 gathers, K5 attention on two streams).  Revoking every
+    slab between replays re-points the uploaded table at the host copies;
+    outputs stay bit-identical to eager steps, and drains wait for replays."""
+    from paper_2602_00328_b200.kv_decode import KVAttentionDecoder
+    from paper_2602_00328_b200.runtime import RevokeReason
+    from paper_2602_00328_b200.verify import verify_release_ordering
+    sysm, kv, m = _cache(local_blocks=4, donor_slabs=1)
+    eager = KVAttentionDecoder(kv, [0, 1], q_heads=4, seed=4, fused=fused).step().clone()
+    dec = KVAttentionDecoder(kv, [0, 1], q_heads=4, seed=4, fused=fused)
+    dec.capture_graph()
+    assert torch.equal(dec.step(), eager)
+    for s in kv.slabs:
+        if s.live:
+            sysm.runtime.revoke(s.handle, RevokeReason.EXTERNAL_RECLAIM)
+    sysm.loop.run()
+    again = dec.step().clone()
+    torch.cuda.synchronize()
+    assert torch.equal(again, eager)
+    sysm.loop.run()
+    assert verify_release_ordering(sysm.loop.log) == []
+    kv.close(); sysm.close()
