@@ -256,17 +256,20 @@ def churn_phase(world, rank, dev, a, dist, barrier, layers=8, seconds=2.0):
                                     stability_max_revocations=L * E // 4),
                 "Fairness": Policy(kind=PolicyKind.FAIRNESS, fairness_budget_bytes_per_s=4e9,
                                    fairness_burst_bytes=1e9)}
+    # the same BestFit timeline with the fused decoder (experts consumed in
+    # place: peer experts over the link, revoked ones from the host copy)
+    runs = [(name, pol, False) for name, pol in policies.items()] + [("BestFit_fused", Policy(), True)]
     outs = {}
-    for name, pol in policies.items():
+    for name, pol, fused in runs:
         try:
             if rank in C:
                 outs[name] = _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported,
-                                            seconds, policy=pol)
+                                            seconds, policy=pol, fused=fused)
         except Exception as e:  # every rank still reaches the collectives below
             outs[name] = {"rank": rank, "error": repr(e)[:300]}
         imported.clear()
     if out is not None:  # donor-side setup failure
-        outs = {name: out for name in policies}
+        outs = {name: out for name, _p, _f in runs}
     results = [None] * world
     if world > 1:
         barrier()
@@ -303,9 +306,14 @@ def churn_phase(world, rank, dev, a, dist, barrier, layers=8, seconds=2.0):
         res["policy_comparison"][name] = {**h2, "policy": repr(policies[name])}
         if e2:
             res["policy_comparison"][name]["errors"] = e2
+    hf, _cf, ef = summary("BestFit_fused")
+    res["fused_decoder"] = {**hf, "policy": "BestFit", "decoder": "MoEDecoder(fused=True): experts read in place"}
+    if ef:
+        res["fused_decoder"]["errors"] = ef
     return res
 
-def _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported, seconds, policy=None):
+def _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported, seconds, policy=None,
+                   fused=False):
     """Compute-rank side of churn_phase (no collectives inside)."""
     import torch
     from paper_2602_00328_b200.churn import ChurnDriver, expert_tier_counts, markov_availability
@@ -344,7 +352,7 @@ def _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported
     sysm.loop.run()
     placed0 = expert_tier_counts(res)["PeerHBM"]
     dec = MoEDecoder(ExpertFetcher(rt, m, res, store), tokens=TOKENS, microbatches=1, seed=13,
-                     engine=a.engine, max_ctas=a.max_ctas)
+                     engine=a.engine, max_ctas=a.max_ctas, fused=fused)
     h = dec.step(dec.x0)
     torch.cuda.synchronize()
     GB_levels = [0, per_reader // 4, per_reader // 2, per_reader]
@@ -373,7 +381,7 @@ def _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported
     lsys = HarvestSystem(dev, host_bytes=1, local_bytes=1, log_transfers=False)
     lf = ExpertFetcher(lsys.runtime, m, lres, ExpertStore(m, lsys.host_id, None),
                        local_addr=[[resident.data_ptr() + (l * E + e) * S for e in range(E)] for l in range(L)])
-    ldec = MoEDecoder(lf, tokens=TOKENS, microbatches=1, seed=13)
+    ldec = MoEDecoder(lf, tokens=TOKENS, microbatches=1, seed=13, fused=fused)
     h2 = ldec.x0
     for _ in range(steps):
         h2 = ldec.step(h2)
