@@ -306,8 +306,9 @@ def churn_phase(world, rank, dev, a, dist, barrier, layers=8, seconds=2.0):
         res["policy_comparison"][name] = {**h2, "policy": repr(policies[name])}
         if e2:
             res["policy_comparison"][name]["errors"] = e2
-    hf, _cf, ef = summary("BestFit_fused")
-    res["fused_decoder"] = {**hf, "policy": "BestFit", "decoder": "MoEDecoder(fused=True): experts read in place"}
+    hf, cf, ef = summary("BestFit_fused")
+    res["fused_decoder"] = {**hf, "policy": "BestFit", "decoder": "MoEDecoder(fused=True): experts read in place",
+                            "per_rank": cf}
     if ef:
         res["fused_decoder"]["errors"] = ef
     return res
@@ -360,14 +361,14 @@ def _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported
     drv = ChurnDriver(sysm, {i: markov_availability(GB_levels, [0.05] * 4, seed=5 + d, horizon=seconds)
                              for i, d in enumerate(donors, start=1)})
     drv.start()
-    steps, peer_min, peer_max = 1, placed0, placed0
+    steps, peer_min, peer_max, peer_sum = 1, placed0, placed0, 0
     t0 = time.perf_counter()
     while time.perf_counter() - t0 < seconds:
         h = dec.step(h)
         steps += 1
         drv.tick(replace)
         pc = expert_tier_counts(res)["PeerHBM"]
-        peer_min, peer_max = min(peer_min, pc), max(peer_max, pc)
+        peer_min, peer_max, peer_sum = min(peer_min, pc), max(peer_max, pc), peer_sum + pc
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     sysm.loop.run()
