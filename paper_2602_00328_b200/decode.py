@@ -221,6 +221,7 @@ class MoEDecoder:
         since the last step are uploaded first; within a step the table is a
         snapshot, and reads of a handle revoked meanwhile extend its drain.
         After capture_graph() the step is one CUDA graph replay."""
+        self._settle_releases()
         if getattr(self.f, "version", 0) != self._table_version:
             self.sync_tables()
         if self._graph is not None:
@@ -228,6 +229,21 @@ class MoEDecoder:
         if self.fused:
             return self._step_fused(x)
         return self._step_eager(x)
+
+    def _settle_releases(self) -> None:
+        """A revoke/free that began on a handle this decoder reads is drained
+        before the next step: wait for the reads already enqueued, let the
+        runtime finish the release (invalidate -> callback -> free; the
+        callback moves residency to the host copy), so the next step's table
+        no longer names the handle.  Without this, steps enqueued back to back
+        keep the handle's in-flight set non-empty and the drain never ends."""
+        ep = self.rt.release_epoch
+        if ep == getattr(self, "_release_seen", 0):
+            return
+        self._release_seen = ep
+        if any(self.rt.is_draining(h) for hs in self.layer_handles for h in hs):
+            torch.cuda.synchronize(self.dev)
+            self.rt.sim.poll() if hasattr(self.rt.sim, "poll") else self.rt.sim.run()
 
     def capture_graph(self) -> None:
         """Capture one decode step (every stage's router, top-k, fetch plan,

@@ -180,6 +180,15 @@ class KVAttentionDecoder:
         [L, B, Hq, D] (after capture_graph(), a buffer the next step reuses)."""
         from .kv import KVTier
         rt = self.kv.rt
+        # a slab whose release began is drained before this step reads the
+        # table (see MoEDecoder._settle_releases): the callbacks then move its
+        # blocks to the host copy (Backed) or mark them lost (Lossy)
+        if rt.release_epoch != getattr(self, "_release_seen", 0):
+            self._release_seen = rt.release_epoch
+            if any(not s.live or rt.is_draining(s.handle) for s in self.kv.slabs
+                   if s.blocks and any(self.kv.table[b].tier is KVTier.PEER_HBM for b in s.blocks.values())):
+                torch.cuda.synchronize(self.dev)
+                self.kv.sys.loop.poll()
         lost = [bid for bid in self.ids if self.kv.table[bid].tier is KVTier.NOT_MATERIALIZED]
         if lost:                            # Lossy blocks revoked since the last step: recompute
             self.kv.reload(lost)

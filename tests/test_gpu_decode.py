@@ -290,3 +290,36 @@ def test_fused_graph_replay_with_revocation():
     assert verify_release_ordering(sysm.loop.log) == []
     sysm.close()
     sys2.close()
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_revocation_completes_while_steps_stream(fused):
+    """Steps enqueued back to back (no host sync between them) must not starve
+    a revocation: the next step drains it (callbacks fire inside step()), stops
+    reading the donor, and the outputs stay equal to the all-local run."""
+    from paper_2602_00328_b200.decode import MoEDecoder
+    from paper_2602_00328_b200.runtime import RevokeReason
+    from paper_2602_00328_b200.verify import verify_release_ordering
+    model = _tiny()
+    sysm, store, res, fetcher, _d = _setup(model, peer_experts=12, microbatches=1)
+    dec = MoEDecoder(fetcher, tokens=16, microbatches=1, seed=0, residual_scale=RS, fused=fused)
+    h = dec.step(dec.x0)
+    h = dec.step(h)
+    revoked = list(fetcher.handles.values())
+    assert revoked
+    for hdl in revoked:
+        sysm.runtime.revoke(hdl, RevokeReason.PRESSURE)
+    for _ in range(3):                       # no loop.run()/synchronize from the test
+        h = dec.step(h)
+    assert not fetcher.handles               # every revocation finished inside step()
+    assert all(sysm.runtime.lookup(x) is None for x in revoked)
+    torch.cuda.synchronize()
+    sys2, ldec0, _keep = _all_local(model, 16, 1, 0, store)
+    ldec = MoEDecoder(ldec0.f, tokens=16, microbatches=1, seed=0, residual_scale=RS, fused=fused)
+    out2 = ldec.decode(5)
+    torch.cuda.synchronize()
+    assert torch.equal(h.view(torch.int16), out2.view(torch.int16))
+    sysm.loop.run()
+    assert verify_release_ordering(sysm.loop.log) == []
+    sysm.close()
+    sys2.close()

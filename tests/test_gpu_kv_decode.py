@@ -195,3 +195,24 @@ def test_graph_replay_equals_eager_across_revocation(fused):
     sysm.loop.run()
     assert verify_release_ordering(sysm.loop.log) == []
     kv.close(); sysm.close()
+
+
+@pytest.mark.parametrize("durability", ["BACKED", "LOSSY"])
+def test_kv_revocation_completes_while_steps_stream(durability):
+    """Decode steps back to back with a revocation issued between them: the
+    next step drains the slab (no host sync by the caller), later steps read
+    the host copy / recompute, and the outputs do not change."""
+    from paper_2602_00328_b200.kv_decode import KVAttentionDecoder
+    from paper_2602_00328_b200.runtime import RevokeReason
+    sysm, kv, m = _cache(local_blocks=4, donor_slabs=2, durability=durability)
+    dec = KVAttentionDecoder(kv, [0, 1], q_heads=4, seed=2, fused=True)
+    first = dec.step().clone()
+    live = [s for s in kv.slabs if s.live]
+    for s in live:
+        sysm.runtime.revoke(s.handle, RevokeReason.EXTERNAL_RECLAIM)
+    for _ in range(3):
+        out = dec.step()
+    assert all(sysm.runtime.lookup(s.handle) is None for s in live)
+    torch.cuda.synchronize()
+    assert torch.equal(out, first)
+    kv.close(); sysm.close()
