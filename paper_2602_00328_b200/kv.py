@@ -528,18 +528,21 @@ class KVCacheManager:
     @annotate("harvest.kv_gather_layer")
     def gather_layer(self, layer: int, block_ids, dst: torch.Tensor, stream=None) -> None:
         """K1: page `layer` of every listed block -> dst[i] (contiguous), read
-        from wherever the block is resident (local / peer / host)."""
-        bases = np.empty(len(block_ids), dtype=np.uint64)
-        strides = np.empty(len(block_ids), dtype=np.uint64)
-        for i, bid in enumerate(block_ids):
-            bases[i], strides[i] = self._page_base(self.table[bid])
+        from wherever the block is resident (local / peer / host).  The peer
+        slabs read join the drain set until the gather completes."""
+        bases, strides, handles = self.page_table(block_ids)
         src = bases + np.uint64(layer) * strides
         s = N.stream_handle(stream) if stream is not None else self.stream
         pinned, d_src = self._stage_u64(src, s)   # async, stream-ordered: no host stall
+        batch = self.rt.begin_reads(handles) if handles else None
         from . import fetch as F
         F.kv_gather(d_src, self.page, dst=dst, engine=self.engine, max_ctas=self.max_ctas, stream=s)
         ev = torch.cuda.Event()
         ev.record(torch.cuda.ExternalStream(s, device=self.dev))
+        if batch is not None:                     # drain: released when the gather is done
+            if s != self.stream:
+                N.call("hv_stream_wait_event", self.stream, ev.cuda_event)
+            self.sys.engine.track([lambda _x, b=batch: self.rt.end_reads(b)])
         self._staged.append((ev, pinned, d_src))   # alive until the gather that reads them is done
 
     def page_table(self, block_ids) -> tuple[np.ndarray, np.ndarray, list]:

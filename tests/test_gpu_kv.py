@@ -171,3 +171,33 @@ def test_kv_correctness_independence(seed):
     assert refcheck.verify_release_ordering(sysm.loop.log) == []
     kv.close()
     sysm.close()
+
+
+def test_gather_layer_reads_are_drained_before_release():
+    """gather_layer's peer reads join the slab's drain set: a revocation issued
+    right after the launch finishes only after the gather, whose bytes are
+    intact (the VMM chunks are unmapped only after the drain)."""
+    import numpy as np
+    from paper_2602_00328_b200.kv import KVTier
+    from paper_2602_00328_b200.runtime import RevokeReason
+    sysm, kv, m = _mk(local_blocks=4, slab_blocks=4, donor_slabs=2, durability="BACKED")
+    kv.append_kv(0, 16 * 8)
+    peer = [b.block_id for b in kv.table.values() if b.tier == KVTier.PEER_HBM]
+    assert peer
+    dst = torch.empty(len(peer) * m.page_bytes, dtype=torch.uint8, device="cuda")
+    for layer in range(m.num_layers):
+        kv.gather_layer(layer, peer, dst)
+        for s in kv.slabs:
+            if s.live:
+                sysm.runtime.revoke(s.handle, RevokeReason.EXTERNAL_RECLAIM)
+        sysm.loop.run()                       # waits for the gather, then releases
+        got = dst.cpu().numpy().reshape(len(peer), m.page_bytes)
+        for i, bid in enumerate(peer):
+            b = kv.table[bid]
+            want = O.content(O.kv_seed(layer, b.sequence_id, b.index), m.page_bytes)
+            assert np.array_equal(got[i], want), (layer, bid)
+        if layer == 0:                        # later layers read the Backed host copies
+            assert all(kv.table[bid].tier == KVTier.HOST_DRAM for bid in peer)
+    assert refcheck.verify_release_ordering(sysm.loop.log) == []
+    kv.close()
+    sysm.close()
