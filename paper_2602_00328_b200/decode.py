@@ -82,9 +82,10 @@ class MoEDecoder:
                 raise ValueError(f"fused decode: at most {mt} tokens per micro-batch")
             if self.I % 64 or self.H % 64:
                 raise ValueError("fused decode needs hidden and intermediate sizes that are multiples of 64")
-        # fused mode reads experts in place: no staging copies
-        self.staging = [torch.zeros(0 if fused else self.K, self.S, dtype=torch.uint8, device=self.dev)
-                        for _ in range(2)]
+        # fused mode reads peer / local experts in place; only host-tier
+        # experts are staged (one buffer: K2 and K4 run in order on one stream)
+        self.staging = [torch.zeros(self.K, self.S, dtype=torch.uint8, device=self.dev)
+                        for _ in range(1 if fused else 2)]
         self.slot_base = [b.data_ptr() for b in self.staging]
         self.dst_ptrs = [torch.zeros(self.E, dtype=torch.int64, device=self.dev) for _ in range(2)]
         self.idx_ext = [torch.zeros(self.K + 1, dtype=torch.int64, device=self.dev) for _ in range(2)]
@@ -126,15 +127,18 @@ class MoEDecoder:
             self._addr_cur = 0
             self.addr = self._addr_bufs[0]
             self.fetchable = new_fetchable.to(self.dev)
+            self.hosttier = torch.from_numpy(self.f.tier == 2).to(self.dev)
         else:
             nxt = 1 - self._addr_cur
             if self._addr_done[nxt] is not None:
                 self._addr_done[nxt].synchronize()   # last step that read buffer nxt is done
             self._addr_bufs[nxt].copy_(new_addr)
             self.fetchable.copy_(new_fetchable)
+            self.hosttier.copy_(torch.from_numpy(self.f.tier == 2))
             self._addr_cur = nxt
             self.addr = self._addr_bufs[nxt]
         self.layer_handles = [[h for (l, _e), h in self.f.handles.items() if l == layer] for layer in range(self.L)]
+        self._any_host = (self.f.tier == 2).any(axis=1).tolist()
         self._table_version = getattr(self.f, "version", 0)
 
     def _sync_tables_in_place(self) -> None:
@@ -147,8 +151,10 @@ class MoEDecoder:
         with torch.cuda.stream(cur):
             self.addr.copy_(pinned, non_blocking=True)
             self.fetchable.copy_(new_fetchable.pin_memory(), non_blocking=True)
+            self.hosttier.copy_(torch.from_numpy(self.f.tier == 2).pin_memory(), non_blocking=True)
         self._staged_tables = (pinned, cur.record_event())   # keep the source alive until copied
         self.layer_handles = [[h for (l, _e), h in self.f.handles.items() if l == layer] for layer in range(self.L)]
+        self._any_host = (self.f.tier == 2).any(axis=1).tolist()
         self._table_version = getattr(self.f, "version", 0)
 
     # ---------------------------------------------------------------- pieces
@@ -364,7 +370,19 @@ class MoEDecoder:
         act = torch.empty(P, I, dtype=torch.bfloat16, device=self.dev)
         y = torch.empty(P, H, dtype=torch.float32, device=self.dev)
         stream = torch.cuda.current_stream(self.dev).cuda_stream
-        w = self.addr[layer].data_ptr()
+        addr = self.addr[layer]
+        if self._capturing or self._any_host[layer]:
+            # host-tier experts: K2 over PCIe into compact local slots first
+            # (sequential reads, the PCIe-efficient path), then K4 reads those
+            # slots and every peer / local expert in place
+            stage = (counts > 0) & self.hosttier[layer]
+            rank = torch.cumsum(stage.to(torch.int64), 0) - 1
+            dst = torch.where(stage, rank * self.S + self.slot_base[0], 0)
+            sizes = torch.where(stage, self.S, 0)
+            N.call("hv_batch_copy", addr.data_ptr(), dst.data_ptr(), sizes.data_ptr(), self.E, self.engine_id,
+                   self.max_ctas, stream)
+            addr = torch.where(stage, dst, addr)
+        w = addr.data_ptr()
         N.call("hv_expert_ffn_gate_up", w, counts.data_ptr(), offs.data_ptr(), tok.data_ptr(), h.data_ptr(),
                act.data_ptr(), self.E, H, I, stream)
         N.call("hv_expert_ffn_down", w, counts.data_ptr(), offs.data_ptr(), act.data_ptr(), y.data_ptr(), self.E,
