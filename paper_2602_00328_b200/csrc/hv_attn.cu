@@ -12,19 +12,16 @@
 // V [T_b][kv_heads][D], fp16, T_b = 16 tokens.
 //
 // Flash-decoding: grid (splits, kv_heads, B).  A CTA owns a contiguous range
-// of its sequence's blocks; its 4 warps take the range's blocks round-robin
-// and keep an online-softmax state (running max, sum, fp32 accumulator) for
-// the g query heads.  Per block a warp:
-//   QK: lane (t = lane/2, half = lane%2) dots D/2 dims of K[t] with the g
-//       queries (fp32, from shared memory); one shuffle joins the halves;
-//   softmax: max / sum over the 16 tokens by shuffles, rescale of the state;
-//   PV: lane owns D/32 output dims and accumulates p[h][t] * V[t] over the
-//       16 tokens (probabilities broadcast through shared memory).
-// The next block's K/V slices are loaded into registers before the current
-// block is processed (two blocks in flight per warp).  The warps merge in
-// shared memory and each CTA writes a partial (m, l, acc) per query head;
+// of its sequence's blocks; its 4 warps take the range's blocks round-robin.
+// Each warp streams its blocks' K/V slices through a 3-stage cp.async ring in
+// shared memory and folds every 16-token block into an online-softmax state
+// (running max, sum, fp32 accumulator) for the g query heads, with the
+// products on tensor cores (paged_decode_mma).  The warps merge in shared
+// memory and each CTA writes a partial (m, l, acc) per query head;
 // hv_paged_decode_attention's second kernel merges the splits in a fixed
 // order (deterministic: no atomics), so the result depends only on the bytes.
+// A scalar-FMA form of the same ring (paged_decode_split_ring) is kept as the
+// measured baseline (build with -DHV_ATTN_MMA=0).
 #include <cuda_fp16.h>
 #include <math.h>
 
@@ -86,31 +83,6 @@ __device__ __forceinline__ void block_softmax(const float (&s)[G], bool valid, f
   }
 }
 
-template <int D>
-struct BlockRegs {
-  uint4 k[Frag<D>::kQkVec];                      // K[t][half] slice of this lane
-  uint32_t v[kBlockTok][Frag<D>::kPvDims / 2];   // V[t][my dims] for every token (half2 packed)
-};
-
-template <int D>
-__device__ __forceinline__ void load_block(BlockRegs<D>& r, const char* page, int kvh, int h, int lane) {
-  const int t = lane >> 1, half = lane & 1;
-  const size_t row = (size_t)kvh * D * 2;       // bytes per token row (all heads)
-  const char* kp = page + t * row + (size_t)h * D * 2 + half * Frag<D>::kHalf * 2;
-#pragma unroll
-  for (int i = 0; i < Frag<D>::kQkVec; ++i) r.k[i] = __ldg(reinterpret_cast<const uint4*>(kp) + i);
-  const char* vbase = page + kBlockTok * row + (size_t)h * D * 2 + lane * Frag<D>::kPvDims * 2;
-#pragma unroll
-  for (int t2 = 0; t2 < kBlockTok; ++t2) {
-    if constexpr (Frag<D>::kPvDims == 4) {
-      const uint2 x = __ldg(reinterpret_cast<const uint2*>(vbase + t2 * row));
-      r.v[t2][0] = x.x;
-      r.v[t2][1] = x.y;
-    } else {
-      r.v[t2][0] = __ldg(reinterpret_cast<const uint32_t*>(vbase + t2 * row));
-    }
-  }
-}
 
 // merge the warps of a CTA (fixed order) and write its partial state:
 // [B][kvh][splits][G][D + 2] = acc[D], m, l
@@ -148,91 +120,6 @@ __device__ __forceinline__ void merge_and_write(const float (&m)[G], const float
       o[D + 1] = L;
     }
   }
-}
-
-template <int D, int G>
-__global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_split(
-    const uint64_t* __restrict__ pages, const int32_t* __restrict__ seq_start, const int32_t* __restrict__ seq_tokens,
-    const __half* __restrict__ q, float* __restrict__ part, int kvh, int splits, float scale) {
-  const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int q_heads = kvh * G;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __shared__ __align__(16) float s_q[G][D];
-  __shared__ float s_p[kAttnWarps][G][kBlockTok];
-
-  for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
-    const int hh = i / D, d = i % D;
-    s_q[hh][d] = __half2float(q[((size_t)b * q_heads + h * G + hh) * D + d]) * scale;
-  }
-  __syncthreads();
-
-  const int b0 = seq_start[b], nblk = seq_start[b + 1] - b0, ntok = seq_tokens[b];
-  const int per = (nblk + splits - 1) / splits;
-  const int lo = split * per, hi = min(nblk, lo + per);
-
-  float m[G], l[G], acc[G][Frag<D>::kPvDims];
-#pragma unroll
-  for (int hh = 0; hh < G; ++hh) {
-    m[hh] = -INFINITY;
-    l[hh] = 0.f;
-#pragma unroll
-    for (int j = 0; j < Frag<D>::kPvDims; ++j) acc[hh][j] = 0.f;
-  }
-  const int t = lane >> 1, half = lane & 1;
-  BlockRegs<D> cur, nxt;
-  int blk = lo + warp;
-  if (blk < hi) load_block<D>(cur, reinterpret_cast<const char*>(pages[b0 + blk]), kvh, h, lane);
-  for (; blk < hi; blk += kAttnWarps) {
-    const int nb = blk + kAttnWarps;
-    if (nb < hi) load_block<D>(nxt, reinterpret_cast<const char*>(pages[b0 + nb]), kvh, h, lane);
-    // QK: token t of this block against the G queries (this lane: half of the dims)
-    float s[G];
-#pragma unroll
-    for (int hh = 0; hh < G; ++hh) s[hh] = 0.f;
-#pragma unroll
-    for (int i = 0; i < Frag<D>::kQkVec; ++i) {
-      const __half2* hp = reinterpret_cast<const __half2*>(&cur.k[i]);
-      float kf[8];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 f = __half22float2(hp[j]);
-        kf[2 * j] = f.x;
-        kf[2 * j + 1] = f.y;
-      }
-#pragma unroll
-      for (int hh = 0; hh < G; ++hh) {
-        const float4* qv = reinterpret_cast<const float4*>(&s_q[hh][half * Frag<D>::kHalf + i * 8]);
-        const float4 qa = qv[0], qb = qv[1];
-        float a = s[hh];
-        a = fmaf(kf[0], qa.x, a); a = fmaf(kf[1], qa.y, a); a = fmaf(kf[2], qa.z, a); a = fmaf(kf[3], qa.w, a);
-        a = fmaf(kf[4], qb.x, a); a = fmaf(kf[5], qb.y, a); a = fmaf(kf[6], qb.z, a); a = fmaf(kf[7], qb.w, a);
-        s[hh] = a;
-      }
-    }
-    const bool valid = blk * kBlockTok + t < ntok;
-    block_softmax<G, Frag<D>::kPvDims>(s, valid, m, l, acc, s_p[warp], t, half);
-    __syncwarp();
-    // PV: this lane owns dims [lane * kPvDims, +kPvDims)
-#pragma unroll
-    for (int t2 = 0; t2 < kBlockTok; ++t2) {
-      float vf[Frag<D>::kPvDims];
-#pragma unroll
-      for (int j = 0; j < Frag<D>::kPvDims / 2; ++j) {
-        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&cur.v[t2][j]));
-        vf[2 * j] = f.x;
-        vf[2 * j + 1] = f.y;
-      }
-#pragma unroll
-      for (int hh = 0; hh < G; ++hh) {
-        const float p = s_p[warp][hh][t2];
-#pragma unroll
-        for (int j = 0; j < Frag<D>::kPvDims; ++j) acc[hh][j] = fmaf(p, vf[j], acc[hh][j]);
-      }
-    }
-    __syncwarp();
-    cur = nxt;
-  }
-  merge_and_write<D, G>(m, l, acc, part, b, h, kvh, split, splits);
 }
 
 // Measured on B200, pages in local HBM (tools/attn_probe.py, KV GB/s at the
@@ -596,7 +483,7 @@ __global__ void paged_decode_combine(const float* __restrict__ part, float* __re
 #define HV_ATTN_MMA 3
 #endif
 #ifndef HV_ATTN_RING
-#define HV_ATTN_RING 3
+#define HV_ATTN_RING 3   // stages of the scalar kernel, built only with HV_ATTN_MMA=0
 #endif
 
 template <int D, int G>
@@ -616,7 +503,7 @@ int launch_attn(const uint64_t* pages, const int32_t* seq_start, const int32_t* 
     paged_decode_mma<D, G, kS><<<grid, kAttnWarps * 32, smem, s>>>(
         pages, seq_start, seq_tokens, reinterpret_cast<const __half*>(q), part, (int)kvh, (int)splits, scale);
   }
-#elif HV_ATTN_RING
+#else
   constexpr int kS = HV_ATTN_RING;
   constexpr size_t smem = (size_t)kAttnWarps * kS * Ring<D>::kStage;
   static bool attr = false;
@@ -627,10 +514,6 @@ int launch_attn(const uint64_t* pages, const int32_t* seq_start, const int32_t* 
   }
   paged_decode_split_ring<D, G, kS><<<grid, kAttnWarps * 32, smem, s>>>(
       pages, seq_start, seq_tokens, reinterpret_cast<const __half*>(q), part, (int)kvh, (int)splits, scale);
-#else
-  paged_decode_split<D, G><<<grid, kAttnWarps * 32, 0, s>>>(pages, seq_start, seq_tokens,
-                                                             reinterpret_cast<const __half*>(q), part, (int)kvh,
-                                                             (int)splits, scale);
 #endif
   HV_CUDA(cudaGetLastError());
   paged_decode_combine<D><<<dim3(kvh * G, B), D, 0, s>>>(part, out, (int)(kvh * G), (int)kvh, (int)splits);
