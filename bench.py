@@ -354,7 +354,9 @@ def run_b200(a):
         roof["mean_launch_ms"] = statistics.mean(launch_ms)
         extra = same_run_comparisons(dev, m, a, source, fetcher)
         cpu = None
-        if not a.no_cpu_baseline:
+        if world > 1:   # the CPU restatement is timed on rank 0 at N=1 only (contract)
+            cpu = {"skipped": "timed in the N=1 run (rank 0, host cores)"}
+        elif not a.no_cpu_baseline:
             threads = os.cpu_count() or 1
             hc = cpu_host_copy(m, 4 * E)
             gbps, secs, layers, moved = cpu_gather_sample(m, hc, routes[a.warmup:], a.cpu_baseline_s, threads)
