@@ -424,10 +424,37 @@ def run_b200(a):
         if rank == 0:
             line["churn_config5"] = churn
     if rank == 0:
+        line["north_star_targets"] = north_star_targets(line, world)
         emit(line, a)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+def north_star_targets(line, world):
+    """BASELINE.json north_star targets read off this line (measured values
+    only; a target whose inputs this N does not produce says so)."""
+    out = {}
+    roof = line.get("roofline") or {}
+    if world > 1:
+        out["peer_fetch_frac_of_nvlink"] = {"value": roof.get("frac"), "target": ">= 0.80",
+                                            "source": "roofline.achieved / 770 GB/s per direction"}
+    else:
+        out["peer_fetch_frac_of_nvlink"] = {"value": None, "note": "N=1 has no donor: host tier only"}
+    lat = line.get("single_expert_latency_us") or {}
+    out["fetch_latency_host_over_peer"] = {"value": lat.get("peer_vs_host_speedup"), "target": ">= 5",
+                                           "source": "single 17.3 MB expert, K2 kernel, host vs peer"}
+    kv = line.get("kv_config1_layer_gather") or {}
+    out["kv_page_fetch_host_over_peer"] = {"value": kv.get("peer_vs_host_speedup"), "target": ">= 5",
+                                           "source": "config-1 layer gather, 1,024 x 64 KiB pages"}
+    dec = (line.get("decode") or {}).get("best") or {}
+    out["moe_decode_vs_host_offload"] = {"value": dec.get("speedup_vs_host_offload_per_gpu"), "target": ">= 1.5",
+                                         "mode": dec.get("mode"),
+                                         "source": "per-GPU decode tok/s, peer tiers vs the same GPU's host offload"}
+    out["bit_exact"] = {"fetch_verify_mismatched_words": (line.get("e2e") or {}).get("verify_mismatched_words"),
+                        "decode_outputs_equal_all_local_under_churn":
+                            (line.get("churn_config5") or {}).get("all_outputs_bit_identical")}
+    return out
+
 
 def main():
     a = parse()
