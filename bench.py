@@ -450,6 +450,9 @@ def north_star_targets(line, world):
     out["moe_decode_vs_host_offload"] = {"value": dec.get("speedup_vs_host_offload_per_gpu"), "target": ">= 1.5",
                                          "mode": dec.get("mode"),
                                          "source": "per-GPU decode tok/s, peer tiers vs the same GPU's host offload"}
+    if os.environ.get("HV_DEVICE_MAP"):
+        out["stand_in"] = ("HV_DEVICE_MAP: several ranks share one GPU and the 'peers' are IPC imports of "
+                           "that GPU's own HBM, so link fractions and ratios here are HBM, not NVLink, figures")
     out["bit_exact"] = {"fetch_verify_mismatched_words": (line.get("e2e") or {}).get("verify_mismatched_words"),
                         "decode_outputs_equal_all_local_under_churn":
                             (line.get("churn_config5") or {}).get("all_outputs_bit_identical")}
