@@ -25,7 +25,9 @@
 //     k-tile  64 x 3 stages ( 72 KiB smem, 3 CTAs/SM): 4,925 / 5,110 / 2,999  <- default
 //     k-tile 128 x 3 stages: 3,424 / 3,462 / 2,267
 // More resident CTAs per SM hide each other's stalls; the persistent ring
-// removes the per-item pipeline fill and drain.
+// removes the per-item pipeline fill and drain.  A deeper ring for the down
+// kernel alone (HV_FFN_STAGES_DOWN 4 / 6 / 8) costs resident CTAs and lowers
+// its rate (down: 4,224 / 3,329 / 2,154 vs 4,543 GB/s at 3, Qwen stage).
 //
 // Layout of an expert object (the same one K2 moves): gate [I][H], up [I][H],
 // down [H][I], bf16, row-major.  Routed (token, expert) pairs are sorted by
@@ -49,6 +51,9 @@ constexpr int kRows = 16 * kWarps;   // weight rows per CTA (16 per warp: one mm
 #ifndef HV_FFN_PERSISTENT
 #define HV_FFN_PERSISTENT 1
 #endif
+#ifndef HV_FFN_STAGES_DOWN
+#define HV_FFN_STAGES_DOWN 3
+#endif
 #ifndef HV_FFN_STAGES
 #define HV_FFN_STAGES 3
 #endif
@@ -57,14 +62,14 @@ constexpr int kRowBytes = kKT * 2;
 constexpr int kChunksPerRow = kRowBytes / 16;
 constexpr int kMaxTok = 64;          // routed tokens per expert per launch (8 mma N groups)
 constexpr int kGroups = kMaxTok / 8;
-constexpr int kStages = HV_FFN_STAGES;
 
 template <int NMAT>
 struct Smem {
+  static constexpr int kS = NMAT == 2 ? HV_FFN_STAGES : HV_FFN_STAGES_DOWN;   // ring stages
   static constexpr int kW = NMAT * kRows * kRowBytes;   // weight tiles of one stage
   static constexpr int kX = kMaxTok * kRowBytes;        // activation tile of one stage
   static constexpr int kStage = kW + kX;
-  static constexpr int kTotal = kStages * kStage;
+  static constexpr int kTotal = kS * kStage;
 };
 
 struct FfnArgs {
@@ -128,7 +133,7 @@ __global__ void __launch_bounds__(kThreads) expert_ffn_kernel(FfnArgs a) {
   const int ktiles = a.K / kKT;
 
   // activation rows beyond n inside the last N group must hold finite values
-  for (int s = 0; s < kStages; ++s) {
+  for (int s = 0; s < Smem<NMAT>::kS; ++s) {
     char* xs = smem + s * Smem<NMAT>::kStage + Smem<NMAT>::kW;
     for (int i = tid; i < (ng * 8 - n) * kChunksPerRow; i += kThreads) {
       const int r = n + i / kChunksPerRow, c = i % kChunksPerRow;
@@ -165,7 +170,7 @@ __global__ void __launch_bounds__(kThreads) expert_ffn_kernel(FfnArgs a) {
       for (int j = 0; j < 4; ++j) acc[m][g][j] = 0.f;
 
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) {
+  for (int s = 0; s < Smem<NMAT>::kS - 1; ++s) {
     if (s < ktiles) load_stage(s, s);
     cp_commit();
   }
@@ -176,13 +181,13 @@ __global__ void __launch_bounds__(kThreads) expert_ffn_kernel(FfnArgs a) {
   const int b_kc = (lane >> 3) & 1;
 
   for (int kt = 0; kt < ktiles; ++kt) {
-    cp_wait<kStages - 2>();
+    cp_wait<Smem<NMAT>::kS - 2>();
     __syncthreads();
     // refill the stage consumed one iteration ago
-    const int nk = kt + kStages - 1;
-    if (nk < ktiles) load_stage(nk, nk % kStages);
+    const int nk = kt + Smem<NMAT>::kS - 1;
+    if (nk < ktiles) load_stage(nk, nk % Smem<NMAT>::kS);
     cp_commit();
-    const char* base = smem + (kt % kStages) * Smem<NMAT>::kStage;
+    const char* base = smem + (kt % Smem<NMAT>::kS) * Smem<NMAT>::kStage;
     const uint32_t xs = smem_u32(base + Smem<NMAT>::kW);
 #pragma unroll
     for (int kk = 0; kk < kKT / 16; ++kk) {
@@ -267,7 +272,7 @@ __global__ void __launch_bounds__(kThreads) expert_ffn_persistent(FfnArgs a, int
   const size_t wstride = (size_t)a.K * 2, xstride = (size_t)a.K * 2;
   // every activation row of every stage starts finite; later stale rows are
   // earlier activations (finite) and only feed output columns that are dropped
-  for (int i = tid; i < kStages * Smem<NMAT>::kX / 16; i += kThreads) {
+  for (int i = tid; i < Smem<NMAT>::kS * Smem<NMAT>::kX / 16; i += kThreads) {
     const int s = i / (Smem<NMAT>::kX / 16), o = i % (Smem<NMAT>::kX / 16);
     *reinterpret_cast<uint4*>(smem + s * Smem<NMAT>::kStage + Smem<NMAT>::kW + o * 16) = make_uint4(0, 0, 0, 0);
   }
@@ -312,7 +317,7 @@ __global__ void __launch_bounds__(kThreads) expert_ffn_persistent(FfnArgs a, int
       for (int j = 0; j < 4; ++j) acc[m][g][j] = 0.f;
 
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) {
+  for (int s = 0; s < Smem<NMAT>::kS - 1; ++s) {
     if (ld.item < n_items) {
       load_stage(ld, s);
       advance(ld);
@@ -323,16 +328,16 @@ __global__ void __launch_bounds__(kThreads) expert_ffn_persistent(FfnArgs a, int
   const int a_kc = lane >> 4;
   const int b_row = lane & 7;
   const int b_kc = (lane >> 3) & 1;
-  int stage = 0, lstage = kStages - 1;
+  int stage = 0, lstage = Smem<NMAT>::kS - 1;
   while (cs.item < n_items) {
-    cp_wait<kStages - 2>();
+    cp_wait<Smem<NMAT>::kS - 2>();
     __syncthreads();
     if (ld.item < n_items) {
       load_stage(ld, lstage);
       advance(ld);
     }
     cp_commit();
-    lstage = lstage + 1 == kStages ? 0 : lstage + 1;
+    lstage = lstage + 1 == Smem<NMAT>::kS ? 0 : lstage + 1;
     const char* base = smem + stage * Smem<NMAT>::kStage;
     const uint32_t xs = smem_u32(base + Smem<NMAT>::kW);
     const int ng = (cs.n + 7) >> 3;
@@ -353,7 +358,7 @@ __global__ void __launch_bounds__(kThreads) expert_ffn_persistent(FfnArgs a, int
         }
       }
     }
-    stage = stage + 1 == kStages ? 0 : stage + 1;
+    stage = stage + 1 == Smem<NMAT>::kS ? 0 : stage + 1;
     if (cs.kt == ktiles - 1) {  // item complete: epilogue, then the next item's tiles are already in flight
       const int r = cs.row0 + warp * 16 + (lane >> 2);
       const int c2 = (lane & 3) * 2;
