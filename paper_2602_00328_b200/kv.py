@@ -309,10 +309,10 @@ class KVCacheManager:
 
     def _peer_slot(self, durability: Durability) -> tuple[int, int] | None:
         cur = getattr(self, "_open_slab", 0)
-        if cur < len(self.slabs) and self.slabs[cur].live and self.slabs[cur].free:
+        if cur < len(self.slabs) and self._writable(self.slabs[cur]):
             return cur, self.slabs[cur].free.pop()
         for i, s in enumerate(self.slabs):
-            if s.live and s.free:
+            if self._writable(s):
                 self._open_slab = i
                 return i, s.free.pop()
         peers = [st.spec.device_id for st in self.rt.peer_states()]
@@ -352,7 +352,7 @@ class KVCacheManager:
         for b in victims:
             sbase = cache0 + b.slot * page
             # fast path: the open slab still has room (else _peer_slot harvests)
-            if slab is not None and slab.live and slab.free:
+            if slab is not None and self._writable(slab):
                 slab_i, slot = cur, slab.free.pop()
                 placed = True
             else:
@@ -518,9 +518,17 @@ class KVCacheManager:
         self._release_empty_slabs()
         return plan
 
+    def _writable(self, s: _Slab) -> bool:
+        """A slab can take new blocks while it has free slots and no release of
+        its handle has begun (a revoking slab is being drained; writing into it
+        would only extend the drain and lose the block at the callback)."""
+        return s.live and bool(s.free) and not self.rt.is_draining(s.handle)
+
     def _release_empty_slabs(self) -> None:
         for s in self.slabs:
             if s.live and not s.blocks and len(s.free) == self.slab_blocks:
+                if self.rt.is_draining(s.handle):
+                    continue                 # a revoke is already releasing it; its callback marks it dead
                 s.live = False
                 self.rt.harvest_free(s.handle)
 

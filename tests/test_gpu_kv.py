@@ -201,3 +201,29 @@ def test_gather_layer_reads_are_drained_before_release():
     assert refcheck.verify_release_ordering(sysm.loop.log) == []
     kv.close()
     sysm.close()
+
+
+def test_slab_emptied_while_revoking_is_left_to_the_revocation():
+    """A slab whose revoke is still draining (a read holds it) can be emptied
+    by a reload: the manager must neither free it (it is not LIVE) nor place
+    new blocks in it; the revocation finishes it once the read ends."""
+    from paper_2602_00328_b200.kv import KVTier
+    from paper_2602_00328_b200.runtime import RevokeReason
+    sysm, kv, m = _mk(local_blocks=8, slab_blocks=2, donor_slabs=2, durability="BACKED")
+    kv.append_kv(0, 16 * 10)                              # 2 blocks evicted into a slab
+    peer = [b for b in kv.table.values() if b.tier == KVTier.PEER_HBM]
+    assert peer
+    slab = kv.slabs[peer[0].slab]
+    hold = sysm.runtime.begin_reads([slab.handle])         # an in-flight read keeps the drain open
+    sysm.runtime.revoke(slab.handle, RevokeReason.EXTERNAL_RECLAIM)
+    assert sysm.runtime.is_draining(slab.handle)
+    kv.reload([b.block_id for b in peer if b.slab == kv.slabs.index(slab)])   # empties it: no free, no raise
+    kv.append_kv(1, 16 * 4)                                # evictions must avoid the draining slab
+    assert all(b.slab != kv.slabs.index(slab) for b in kv.table.values() if b.tier == KVTier.PEER_HBM)
+    sysm.runtime.end_reads(hold)
+    sysm.loop.run()
+    assert sysm.runtime.lookup(slab.handle) is None and not slab.live
+    _check_all(kv, m)
+    assert refcheck.verify_release_ordering(sysm.loop.log) == []
+    kv.close()
+    sysm.close()
