@@ -454,14 +454,18 @@ def phi_phase(world, rank, dev, a, dist, barrier, max_over_ranks, batches=(1, 16
         errors.append(repr(e)[:200])
         fetcher = None
     barrier()
-    def timed_decode(b, fused):
-        """3 timed steps after 1 warm step; max over ranks (collective-safe)."""
+    def timed_decode(b, fused, graph=False):
+        """3 timed steps after 1 warm step (or after capture_graph());
+        max over ranks (collective-safe)."""
         dt_local, finite, dec = float("inf"), False, None
         try:
             if fetcher is None:
                 raise RuntimeError("setup failed")
             dec = MoEDecoder(fetcher, tokens=b, microbatches=1, seed=11, fused=fused)
             h = dec.decode(1)
+            if graph:
+                dec.capture_graph()
+                h = dec.step(h).clone()
             torch.cuda.synchronize()
         except Exception as e:
             errors.append(repr(e)[:200])
@@ -492,6 +496,10 @@ def phi_phase(world, rank, dev, a, dist, barrier, max_over_ranks, batches=(1, 16
         if math.isfinite(dtf) and f"batch{b}" in out:
             out[f"batch{b}"]["fused"] = {"tokens_per_s": b * 3 * world / dtf, "ms_per_layer": dtf / 3 / L * 1e3,
                                          "outputs_finite": finite_f}
+        dtg, finite_g = timed_decode(b, True, graph=True)   # the same, one CUDA graph replay per step
+        if math.isfinite(dtg) and f"batch{b}" in out:
+            out[f"batch{b}"]["fused_cuda_graph"] = {"tokens_per_s": b * 3 * world / dtg,
+                                                    "ms_per_layer": dtg / 3 / L * 1e3, "outputs_finite": finite_g}
     if sysm is not None:
         sysm.loop.run()
     if rank == 0 and not a.no_host_compare:
