@@ -188,6 +188,9 @@ def _kv_decode_measure(kv, seqs, sysm, steps=3, q_heads=32):
                                "kv_GBps": nbytes / (fused_ms * 1e-3) / 1e9,
                                "outputs_bit_identical_to_gathered": bool(torch.equal(fused_out, tier_out))},
             "cuda_graph": graphs,
+            "best": max(([("gather", len(seqs) / (tier_ms * 1e-3)), ("in_place", len(seqs) / (fused_ms * 1e-3))]
+                         + [(f"{k}_cuda_graph", v["tokens_per_s"]) for k, v in graphs.items()]),
+                        key=lambda kv_: kv_[1]),
             "attention": "hv_paged_decode_attention (split-K flash decoding over page pointers, tensor cores)",
             "overlap_traced_step": ov,
             "model": f"{kv.m.name}: GQA {q_heads} q heads over {kv.m.kv_heads} KV heads, per-layer K1 gather "
