@@ -418,7 +418,8 @@ def run_b200(a):
         del staging
         torch.cuda.empty_cache()
         try:
-            churn = churn_phase(world, rank, dev, a, dist, barrier)
+            churn = churn_phase(world, rank, dev, a, dist, barrier,
+                                seconds=float(os.environ.get("HV_CHURN_SECONDS", "2.0")))
         except Exception as e:
             churn = {"error": repr(e)[:300]}
         if rank == 0:
