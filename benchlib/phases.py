@@ -261,7 +261,8 @@ def churn_phase(world, rank, dev, a, dist, barrier, layers=8, seconds=2.0):
                                    fairness_burst_bytes=1e9)}
     # the same BestFit timeline with the fused decoder (experts consumed in
     # place: peer experts over the link, revoked ones from the host copy)
-    runs = [(name, pol, False) for name, pol in policies.items()] + [("BestFit_fused", Policy(), True)]
+    runs = ([(name, pol, False) for name, pol in policies.items()] + [("BestFit_fused", Policy(), True)]
+            + [("BestFit_fused_graph", Policy(), "graph")])
     outs = {}
     for name, pol, fused in runs:
         try:
@@ -309,11 +310,13 @@ def churn_phase(world, rank, dev, a, dist, barrier, layers=8, seconds=2.0):
         res["policy_comparison"][name] = {**h2, "policy": repr(policies[name])}
         if e2:
             res["policy_comparison"][name]["errors"] = e2
-    hf, cf, ef = summary("BestFit_fused")
-    res["fused_decoder"] = {**hf, "policy": "BestFit", "decoder": "MoEDecoder(fused=True): experts read in place",
-                            "per_rank": cf}
-    if ef:
-        res["fused_decoder"]["errors"] = ef
+    for key, name, desc in (("fused_decoder", "BestFit_fused", "MoEDecoder(fused=True): experts read in place"),
+                            ("fused_decoder_cuda_graph", "BestFit_fused_graph",
+                             "the same, each step one CUDA graph replay (tables patched in place)")):
+        hf, cf, ef = summary(name)
+        res[key] = {**hf, "policy": "BestFit", "decoder": desc, "per_rank": cf}
+        if ef:
+            res[key]["errors"] = ef
     return res
 
 def _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported, seconds, policy=None,
@@ -356,19 +359,27 @@ def _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported
     sysm.loop.run()
     placed0 = expert_tier_counts(res)["PeerHBM"]
     dec = MoEDecoder(ExpertFetcher(rt, m, res, store), tokens=TOKENS, microbatches=1, seed=13,
-                     engine=a.engine, max_ctas=a.max_ctas, fused=fused)
+                     engine=a.engine, max_ctas=a.max_ctas, fused=bool(fused))
     h = dec.step(dec.x0)
+    if fused == "graph":        # every later step is one replay; residency changes patch its tables in place
+        dec.capture_graph()
+        h = dec.step(h).clone()
+        step_offset = 1
+    else:
+        step_offset = 0
     torch.cuda.synchronize()
     GB_levels = [0, per_reader // 4, per_reader // 2, per_reader]
     donors = layout.donors_of(rank) if layout else [dev]
     drv = ChurnDriver(sysm, {i: markov_availability(GB_levels, [0.05] * 4, seed=5 + d, horizon=seconds)
                              for i, d in enumerate(donors, start=1)})
     drv.start()
-    steps, peer_min, peer_max, peer_sum = 1, placed0, placed0, 0
+    steps, peer_min, peer_max, peer_sum = 1 + step_offset, placed0, placed0, 0   # steps applied to h so far
+    loop_steps = 0
     t0 = time.perf_counter()
     while time.perf_counter() - t0 < seconds:
         h = dec.step(h)
         steps += 1
+        loop_steps += 1
         drv.tick(replace)
         pc = expert_tier_counts(res)["PeerHBM"]
         peer_min, peer_max, peer_sum = min(peer_min, pc), max(peer_max, pc), peer_sum + pc
@@ -385,15 +396,16 @@ def _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported
     lsys = HarvestSystem(dev, host_bytes=1, local_bytes=1, log_transfers=False)
     lf = ExpertFetcher(lsys.runtime, m, lres, ExpertStore(m, lsys.host_id, None),
                        local_addr=[[resident.data_ptr() + (l * E + e) * S for e in range(E)] for l in range(L)])
-    ldec = MoEDecoder(lf, tokens=TOKENS, microbatches=1, seed=13, fused=fused)
+    ldec = MoEDecoder(lf, tokens=TOKENS, microbatches=1, seed=13, fused=bool(fused))
     h2 = ldec.x0
     for _ in range(steps):
         h2 = ldec.step(h2)
     torch.cuda.synchronize()
-    out = {"rank": rank, "decode_steps": steps - 1, "tokens_per_s": TOKENS * (steps - 1) / wall,
+    out = {"rank": rank, "decode_steps": loop_steps, "tokens_per_s": TOKENS * loop_steps / wall,
            "availability_steps": len(log.of_kind("availability_step")),
            "revocations": len(log.of_kind("revoke_begin")), "re_placements": migrated[0] - placed0,
            "peer_resident_experts_min_max": [peer_min, peer_max], "experts": L * E,
+           "peer_resident_experts_mean_over_steps": peer_sum / max(1, loop_steps),
            "release_ordering_violations": len(verify_release_ordering(log)),
            "outputs_bit_identical_to_all_local": bool(torch.equal(h.view(torch.int16), h2.view(torch.int16)))}
     del dec, ldec, resident
