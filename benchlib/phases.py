@@ -381,6 +381,7 @@ def _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported
         steps += 1
         loop_steps += 1
         drv.tick(replace)
+        sysm.loop.poll()            # arrivals of finished copy-ins flip residency before counting
         pc = expert_tier_counts(res)["PeerHBM"]
         peer_min, peer_max, peer_sum = min(peer_min, pc), max(peer_max, pc), peer_sum + pc
     torch.cuda.synchronize()
