@@ -162,12 +162,19 @@ struct PageResolver {
   uint32_t chunks_per_page;
   uint32_t n_pages;
   uint32_t chunk;
+  uint32_t interleave;      // HV_ENGINE_FLAG_INTERLEAVE: chunk c reads page c % n at chunk c / n
 
   __device__ __forceinline__ uint32_t setup(void*) const { return n_pages * chunks_per_page; }
   __device__ __forceinline__ ChunkRef at(uint32_t c, uint32_t& hint) const {
     (void)hint;
-    const uint32_t page = c / chunks_per_page;
-    const uint32_t ci = c - page * chunks_per_page;
+    uint32_t page, ci;
+    if (interleave) {
+      ci = c / n_pages;
+      page = c - ci * n_pages;
+    } else {
+      page = c / chunks_per_page;
+      ci = c - page * chunks_per_page;
+    }
     uint64_t s;
     if (kTable) {
       const uint64_t loc = __ldg(locs + page);
@@ -715,7 +722,8 @@ int launch_pages(PageResolver<kTable> res, int engine, int max_ctas, void* strea
   hv::DeviceGuard dg;
   int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
-  engine = pick_engine(engine & ~kEngineInterleave);  // uniform pages: order flag not used
+  res.interleave = (engine & kEngineInterleave) ? 1u : 0u;   // explicit flag only (AUTO pages stay linear)
+  engine = pick_engine(engine & ~kEngineInterleave);
   if (engine == HV_ENGINE_TMA) {
     if ((st = set_tma_attrs())) return st;
     res.chunk = kTmaChunk;
@@ -1002,7 +1010,10 @@ HV_EXPORT int hv_swap_blocks_batch(const uint64_t* h_src, const uint64_t* h_dst,
       r.dst_base = 0;
       r.page_bytes = h_bytes[base];
       r.n_pages = m;
-      st = launch_pages(r, engine, max_ctas, stream);
+      // equal-size objects (a stage's experts): AUTO takes the interleaved
+      // order, as hv_batch_copy does, so readers spread over every donor
+      st = launch_pages(r, engine == HV_ENGINE_AUTO ? (HV_ENGINE_AUTO | kEngineInterleave) : engine, max_ctas,
+                        stream);
     } else if (!uniform) {
       const int eng = pick_engine(engine & ~kEngineInterleave);
       const uint64_t chunk = eng == HV_ENGINE_TMA ? kTmaChunk : kLdgChunk;
