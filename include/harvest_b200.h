@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define HV_ABI_VERSION 2   /* 2: hv_paged_decode_attention workspace carries merge counters */
+#define HV_ABI_VERSION 1
 
 /* ---- status codes ------------------------------------------------------ */
 #define HV_OK 0
@@ -240,12 +240,9 @@ int hv_expert_ffn_max_tokens(int* out);
  * Page layout: K [16][kv_heads][D] then V [16][kv_heads][D], fp16.  Pages
  * may be a K1-gathered buffer or the pages in place (local, peer, host).
  * d_q: [batch][q_heads][D] fp16; d_out: [batch][q_heads][D] fp32;
- * d_part: workspace of batch*kv_heads*splits*g*(D+2) floats followed by
- * batch*kv_heads 32-bit counters, zero-initialised once by the caller (every
- * call returns the counters to zero, so the workspace can be reused and
- * graph-captured).  Flash-decoding over `splits` block ranges per (sequence,
- * KV head); the last CTA of each merges the splits in split order, so the
- * result depends only on the bytes.  One kernel launch. */
+ * d_part: workspace of batch*kv_heads*splits*g*(D+2) floats.  Flash-decoding
+ * over `splits` block ranges per (sequence, KV head), merged in a fixed
+ * order: the result depends only on the bytes. */
 int hv_paged_decode_attention(const uint64_t* d_page_ptrs, const int32_t* d_seq_start,
                               const int32_t* d_seq_tokens, const void* d_q, float* d_out, float* d_part,
                               uint32_t batch, uint32_t q_heads, uint32_t kv_heads, uint32_t head_dim,

@@ -19,8 +19,7 @@
 // products on tensor cores (paged_decode_mma).  The warps merge in shared
 // memory and each CTA writes a partial (m, l, acc) per query head;
 // hv_paged_decode_attention's second kernel merges the splits in a fixed
-// order (deterministic: the last CTA of each (sequence, KV head) merges every
-// split in split order), so the result depends only on the bytes.
+// order (deterministic: no atomics), so the result depends only on the bytes.
 // A scalar-FMA form of the same ring (paged_decode_split_ring) is kept as the
 // measured baseline (build with -DHV_ATTN_MMA=0).
 #include <cuda_fp16.h>
@@ -317,8 +316,7 @@ __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
 template <int D, int G, int S>
 __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_mma(
     const uint64_t* __restrict__ pages, const int32_t* __restrict__ seq_start, const int32_t* __restrict__ seq_tokens,
-    const __half* __restrict__ q, float* __restrict__ part, float* __restrict__ out_final,
-    unsigned* __restrict__ counters, int kvh, int splits, float scale) {
+    const __half* __restrict__ q, float* __restrict__ part, int kvh, int splits, float scale) {
   static_assert(G <= 8, "query rows g and g+8 of the m16 tile: at most 8 heads per KV head");
   constexpr int KS = D / 16;             // k steps of Q K^T
   constexpr int NT = D / 8;              // n tiles of P V
@@ -460,32 +458,6 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_mma(
       out[D + 1] = L;
     }
   }
-  // the last CTA of (b, h) to finish merges every split, in split order
-  // (threadFenceReduction pattern: the result does not depend on which CTA
-  // is last), writes the output, and returns the counter to zero
-  __shared__ unsigned s_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&counters[b * kvh + h], 1u) == (unsigned)splits - 1u;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const float* base = part + (((size_t)b * kvh + h) * splits) * G * (D + 2);
-  for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
-    const int hh = i / D, d = i % D;
-    float M = -INFINITY;
-    for (int s2 = 0; s2 < splits; ++s2) M = fmaxf(M, __ldcg(base + ((size_t)s2 * G + hh) * (D + 2) + D));
-    float L = 0.f, A = 0.f;
-    for (int s2 = 0; s2 < splits; ++s2) {
-      const float* pp = base + ((size_t)s2 * G + hh) * (D + 2);
-      const float mm = __ldcg(pp + D);
-      const float cf = mm == -INFINITY ? 0.f : __expf(mm - M);
-      L += __ldcg(pp + D + 1) * cf;
-      A += __ldcg(pp + d) * cf;
-    }
-    out_final[((size_t)b * q_heads + h * G + hh) * D + d] = L > 0.f ? A / L : 0.f;
-  }
-  if (threadIdx.x == 0) counters[b * kvh + h] = 0u;
 }
 
 // out[b][qh][d] = sum_s acc_s[d] e^(m_s - M) / sum_s l_s e^(m_s - M), splits in order
@@ -528,15 +500,8 @@ int launch_attn(const uint64_t* pages, const int32_t* seq_start, const int32_t* 
                                    (int)smem));
       attr_m = true;
     }
-    // the split-merge happens inside (last CTA per (sequence, KV head)):
-    // counters follow the partials in the caller's zero-initialised workspace
-    unsigned* counters = reinterpret_cast<unsigned*>(part + (size_t)B * kvh * splits * G * (D + 2));
     paged_decode_mma<D, G, kS><<<grid, kAttnWarps * 32, smem, s>>>(
-        pages, seq_start, seq_tokens, reinterpret_cast<const __half*>(q), part, out, counters, (int)kvh,
-        (int)splits, scale);
-    HV_CUDA(cudaGetLastError());
-    hv::note_launch(1);
-    return HV_OK;
+        pages, seq_start, seq_tokens, reinterpret_cast<const __half*>(q), part, (int)kvh, (int)splits, scale);
   }
 #else
   constexpr int kS = HV_ATTN_RING;

@@ -91,10 +91,8 @@ class KVAttentionDecoder:
         sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self.splits = splits or max(1, min(self.nb, math.ceil(2 * sms / (self.B * m.kv_heads))))
         g_heads = q_heads // m.kv_heads
-        # partials + one merge counter per (sequence, KV head); zeroed once,
-        # the kernel returns the counters to zero after every call
-        self.part = torch.zeros(self.B * m.kv_heads * self.splits * g_heads * (m.head_dim + 2)
-                                + self.B * m.kv_heads, dtype=torch.float32, device=self.dev)
+        self.part = torch.empty(self.B * m.kv_heads * self.splits * g_heads * (m.head_dim + 2), dtype=torch.float32,
+                                device=self.dev)
         self.scale = 1.0 / math.sqrt(m.head_dim)
         self.fetch_h = kv.stream
         self.fetch = torch.cuda.ExternalStream(kv.stream, device=self.dev)

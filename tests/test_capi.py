@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(N.exported_symbols())
-    assert lib.hv_abi_version() == 2
+    assert lib.hv_abi_version() == 1
 
 
 def test_error_strings_and_no_device_behaviour():

@@ -25,7 +25,7 @@ def run(B, ctx, splits_list, kvh=8, g=4, D=128):
     out = torch.empty(B, kvh * g, D, device="cuda")
     res = {}
     for sp in splits_list:
-        part = torch.zeros(B * kvh * sp * g * (D + 2) + B * kvh, device="cuda")   # + merge counters
+        part = torch.empty(B * kvh * sp * g * (D + 2), device="cuda")
         s = torch.cuda.current_stream().cuda_stream
 
         def f():
