@@ -21,7 +21,11 @@
 // hv_paged_decode_attention's second kernel merges the splits in a fixed
 // order (deterministic: no atomics), so the result depends only on the bytes.
 // A scalar-FMA form of the same ring (paged_decode_split_ring) is kept as the
-// measured baseline (build with -DHV_ATTN_MMA=0).
+// measured baseline (build with -DHV_ATTN_MMA=0).  Merging the splits inside
+// the attention kernel (the last CTA of each (sequence, KV head) merging in
+// split order, threadFenceReduction style) was measured and dropped: one CTA
+// walking all splits serially costs more than the second launch
+// (4 x 4k: 2,928 vs 3,740 GB/s; 1 x 128k: 4,425 vs 5,564).
 #include <cuda_fp16.h>
 #include <math.h>
 
