@@ -2,9 +2,12 @@
 
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
 
-Reads /root/reference/pkg/src (read-only) — never at test or bench time; the
-GPU box only sees the committed JSON files.  Every fixture records the
-reference file:line whose behaviour it captures.
+Reads /root/reference/pkg/src (read-only; or HARVEST_REFERENCE).  The GPU
+box only sees the committed JSON files.  On CPU,
+tests/test_differential_reference.py also drives these runners against the
+pip-installed copy under baseline/_ref (when present) on fresh random
+scripts.  Every fixture records the reference file:line whose behaviour it
+captures.
 """
 from __future__ import annotations
 

@@ -55,3 +55,53 @@ def test_random_script_matches_reference(cfg, seed):
     assert P._norm(cbs) == P._norm(want["callbacks"])
     assert P._norm(P.log_of(loop)) == P._norm(want["log"])
     assert want["release_violations"] == [] and want["writeback_violations"] == []
+
+
+MOE_CASES = [  # (layers, experts, top_k, expert_size, tokens, microbatches, fraction, tier, cap_experts, peers)
+    (6, 12, 2, 1 << 20, 8, 2, 50, "PeerHBM", 20, 1),
+    (6, 12, 2, 1 << 20, 8, 2, 100, "PeerHBM", 30, 3),
+    (4, 60, 4, 17_301_504, 32, 2, 100, "PeerHBM", 40, 7),
+    (4, 60, 4, 17_301_504, 32, 1, 75, "PeerHBM", 200, 2),
+    (8, 16, 2, 157_286_400, 16, 2, 100, "PeerHBM", 9, 7),
+    (5, 8, 2, 3 << 20, 4, 2, 25, "HostDRAM", 4, 1),
+]
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("case", MOE_CASES, ids=[f"moe{i}" for i in range(len(MOE_CASES))])
+def test_random_moe_placement_and_plan_match_reference(case, seed):
+    """place_offloaded / rebalance residency (every handle key) and the serving
+    tier + handle of every fetch of the decode, for fresh routing seeds,
+    shapes, offload fractions, donor counts and capacities (some run out)."""
+    import numpy as np
+    mg = _golden_tools()
+    from paper_2602_00328_b200 import moe as M
+    from paper_2602_00328_b200.events import VirtualLoop
+    from paper_2602_00328_b200.memalloc import Tier
+    from paper_2602_00328_b200.runtime import HarvestRuntime
+    from tests.test_moe_parity import paper_h100_topology
+    L, E, K, S, T, nmb, fraction, tier, cap_experts, peers = case
+    ref_model = mg.moe.MoEProfile("diff", num_layers=L, num_experts=E, top_k=K, expert_size=S,
+                                  compute_time_per_microbatch=1e-3)
+    pipe = mg.moe.PipelineConfig(microbatch_tokens=T, num_microbatches=nmb)
+    c = mg.fetch_plan(ref_model, pipe, fraction, mg.Tier(tier), cap_experts * S, peers, 100 + seed)
+    model = M.MoEProfile("diff", L, E, K, S, 1e-3)
+    active = [[tuple(x) for x in row] for row in c["active"]]
+    trace = M.RoutingTrace(len(active), L, E, active, np.array(c["counts"], dtype=np.int64))
+    topo, host_id = paper_h100_topology(peers, cap_experts * S)
+    loop = VirtualLoop()
+    rt = HarvestRuntime(loop, topo)
+    res = M.ExpertResidency(model)
+    M.place_offloaded(loop, rt, model, res, trace, fraction, Tier(tier), host_id)
+    got = {f"{l},{e}": [ent.tier.value, None if ent.handle is None else list(ent.handle.key())]
+           for (l, e), ent in res.entries.items()}
+    assert got == c["residency"]
+    fetcher = M.ExpertFetcher(rt, model, res, M.ExpertStore(model, host_id, None))
+    plan = []
+    for layer in range(L):
+        for mb in range(len(active)):
+            for e, t in fetcher.plan(layer, active[mb][layer]):
+                h = fetcher.handles.get((layer, e)) if t == "peer" else None
+                plan.append([layer, e, t, None if h is None else list(h.key())])
+    assert plan == c["fetches"]
+    assert c["read_errors"] == 0
