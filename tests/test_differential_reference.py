@@ -105,3 +105,30 @@ def test_random_moe_placement_and_plan_match_reference(case, seed):
                 plan.append([layer, e, t, None if h is None else list(h.key())])
     assert plan == c["fetches"]
     assert c["read_errors"] == 0
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_availability_timelines_match_reference(seed):
+    """churn.markov_availability / availability_from_trace against the
+    reference's traces.py:171-213 on fresh parameters: identical steps and
+    identical level_at on a probe grid."""
+    mg = _golden_tools()
+    from paper_2602_00328_b200 import churn as C
+    rng = random.Random(seed)
+    n = rng.randint(1, 5)
+    levels = [rng.randint(0, 1 << 34) for _ in range(n)]
+    soj = [rng.choice([0.01, 0.05, 0.2, 1.0]) for _ in range(n)]
+    horizon = rng.choice([0.5, 2.0, 10.0])
+    want = mg.traces.markov_availability(levels, soj, seed, horizon)
+    got = C.markov_availability(levels, soj, seed, horizon)
+    assert [tuple(s) for s in got.steps] == [tuple(s) for s in want.steps]
+    recs = [(rng.uniform(0, 100), rng.random()) for _ in range(rng.randint(1, 30))]
+    cap = rng.choice([80 << 30, 180 << 30])
+    res, head = rng.choice([0, 1 << 30]), rng.choice([0, 2 << 30])
+    scale = rng.choice([1.0, 0.01])
+    want2 = mg.traces.availability_from_trace(
+        [mg.traces.SnapshotRecord("m", t, int(u * cap), cap) for t, u in recs], cap, scale, res, head)
+    got2 = C.availability_from_trace([(t, int(u * cap) / cap) for t, u in recs], cap, scale, res, head)
+    assert [tuple(s) for s in got2.steps] == [tuple(s) for s in want2.steps]
+    for t in [x * horizon / 17 for x in range(18)]:
+        assert got.level_at(t) == want.level_at(t)
