@@ -132,3 +132,24 @@ def test_availability_timelines_match_reference(seed):
     assert [tuple(s) for s in got2.steps] == [tuple(s) for s in want2.steps]
     for t in [x * horizon / 17 for x in range(18)]:
         assert got.level_at(t) == want.level_at(t)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_calibrate_matches_reference(seed):
+    """interconnect.calibrate / calibration_rms / transfer_time (interconnect.py:51-54,
+    :168-221) on fresh noisy latency curves: the same fit to 1e-12 relative."""
+    mg = _golden_tools()
+    from harvestsim import interconnect as RI
+    from paper_2602_00328_b200 import interconnect as I
+    rng = random.Random(seed)
+    fc, bw = rng.uniform(1e-6, 50e-6), rng.uniform(10e9, 900e9)
+    pts = [(s, (fc + s / bw) * (1 + rng.uniform(-0.02, 0.02)))
+           for s in sorted(rng.sample(range(4096, 64 << 20), rng.randint(2, 12)))]
+    want = RI.calibrate(pts)
+    got = I.calibrate(pts)
+    assert got == pytest.approx(want, rel=1e-12)
+    assert I.calibration_rms(pts, *got) == pytest.approx(RI.calibration_rms(pts, *want), rel=1e-12)
+    link_r = RI.LinkSpec(RI.LinkKind.PEER_LINK, fc, bw, endpoints=(0, 1))
+    link_o = I.LinkSpec(I.LinkKind.PEER_LINK, fc, bw, endpoints=(0, 1))
+    for s in (1, 65536, 17_301_504):
+        assert I.transfer_time(link_o, s) == RI.transfer_time(link_r, s)
