@@ -352,7 +352,10 @@ def run_b200(a):
                                       f"({tr['report']}), algorithmic {tr['algorithmic_bytes_per_launch']:.0f} B/launch")
         roof["bytes_per_launch"] = bytes_per_launch
         roof["mean_launch_ms"] = statistics.mean(launch_ms)
-        extra = same_run_comparisons(dev, m, a, source, fetcher)
+        try:   # rank-0 local work only (no collectives inside): a failure is reported, never fatal
+            extra = same_run_comparisons(dev, m, a, source, fetcher)
+        except Exception as e:
+            extra = {"same_run_comparisons_error": repr(e)[:300]}
         cpu = None
         if world > 1:   # the CPU restatement is timed on rank 0 at N=1 only (contract)
             cpu = {"skipped": "timed in the N=1 run (rank 0, host cores)"}
