@@ -321,8 +321,11 @@ def run_b200(a):
             kvd1 = kv_decode_config1(sysm, source, a)
         except Exception as e:  # report, never lose the line
             kvd1 = {"error": repr(e)[:300]}
-        kvlc = kv_long_context(sysm, source, a)
-        kvlc["reload_kernel_GBps_all_ranks_min"] = -max_over_ranks(-kvlc["reload_kernel_GBps"])
+        try:
+            kvlc = kv_long_context(sysm, source, a)
+        except Exception as e:   # reported; every rank still reaches the collective below
+            kvlc = {"error": repr(e)[:300]}
+        kvlc["reload_kernel_GBps_all_ranks_min"] = -max_over_ranks(-kvlc.get("reload_kernel_GBps", 0.0))
     barrier()
     if world > 1 and rank == 0 and not a.no_host_compare:
         decode["host_offload"] = host_offload_decode(m, dev, a)
