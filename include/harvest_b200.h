@@ -221,7 +221,10 @@ int hv_ce_batch_copy(const uint64_t* h_src, const uint64_t* h_dst,
  * and the bytes cross the link once.  Object layout: gate [I][H], up [I][H],
  * down [H][I], bf16.  Routed pairs are sorted by expert: expert e (of
  * n_experts) owns pairs d_offs[e] .. d_offs[e] + d_counts[e] - 1, at most
- * hv_expert_ffn_max_tokens() of them.  Requires H % 64 == 0 and I % 64 == 0.
+ * hv_expert_ffn_max_tokens() of them.  Requires H % 64 == 0 and I % 64 == 0,
+ * expert objects and activation rows 16-byte aligned (cp.async granules;
+ * expert sizes that are multiples of 16, as every bf16 [I][H] stack is, keep
+ * the runtime's segment bases aligned).
  *   gate_up: act[p][i] = silu(gate[i] . x[tok[p]]) * (up[i] . x[tok[p]])  (bf16 [P][I])
  *   down:    y[p][h]   = down[h] . act[p]                                  (fp32 [P][H]) */
 int hv_expert_ffn_gate_up(const uint64_t* d_w_addr, const int32_t* d_counts, const int32_t* d_offs,
@@ -238,7 +241,8 @@ int hv_expert_ffn_max_tokens(int* out);
  * one page pointer per block (this layer), sequence-major; sequence b owns
  * blocks d_seq_start[b] .. d_seq_start[b+1]-1 and d_seq_tokens[b] tokens.
  * Page layout: K [16][kv_heads][D] then V [16][kv_heads][D], fp16.  Pages
- * may be a K1-gathered buffer or the pages in place (local, peer, host).
+ * may be a K1-gathered buffer or the pages in place (local, peer, host);
+ * each page 16-byte aligned.
  * d_q: [batch][q_heads][D] fp16; d_out: [batch][q_heads][D] fp32;
  * d_part: workspace of batch*kv_heads*splits*g*(D+2) floats.  Flash-decoding
  * over `splits` block ranges per (sequence, KV head), merged in a fixed
