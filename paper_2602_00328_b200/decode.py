@@ -111,6 +111,8 @@ class MoEDecoder:
         src = np.where(self.f.tier == 0, self.f.local_addr, self.f.src_addr).astype(np.uint64)
         if np.any(src == 0):
             raise ValueError("an expert has no source address (LOCAL tier needs ExpertFetcher(local_addr=...))")
+        if self.fused and np.any(src % 16):
+            raise ValueError("fused decode reads experts with 16-byte cp.async: expert objects must be 16-byte aligned")
         return torch.from_numpy(src.view(np.int64).copy()), torch.from_numpy((self.f.tier != 0).copy())
 
     def sync_tables(self) -> None:

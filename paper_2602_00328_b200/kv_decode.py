@@ -108,6 +108,8 @@ class KVAttentionDecoder:
         the decoder's device table on the current stream, ordered after every
         earlier step and before this one.  Returns the peer handles read."""
         bases, strides, handles = self.kv.page_table(self.ids)
+        if np.any(bases % 16) or np.any(strides % 16):
+            raise ValueError("paged attention reads 16-byte granules: KV pages must be 16-byte aligned")
         tab = torch.from_numpy(np.stack([bases, strides]).view(np.int64)).pin_memory()
         self._tab_dev.copy_(tab, non_blocking=True)
         return handles
