@@ -152,7 +152,9 @@ def _kv_decode_measure(kv, seqs, sysm, steps=3, q_heads=32):
         e1.synchronize()
         return o, e0.elapsed_time(e1) / steps
 
-    local_out, local_ms = timed()
+    # all-local baseline: attention straight over the local pages (no gather),
+    # the same kernel on the same bytes as every tiered mode below
+    local_out, local_ms = timed(KVAttentionDecoder(kv, seqs, q_heads=q_heads, seed=1, fused=True))
     local_out = local_out.clone()
     kv.sys.engine.synchronize()
     sysm.loop.run()          # slabs emptied by an earlier reload go back to their donors first

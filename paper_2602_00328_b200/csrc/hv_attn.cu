@@ -33,7 +33,10 @@
 
 namespace {
 
-constexpr int kAttnWarps = 4;
+#ifndef HV_ATTN_WARPS
+#define HV_ATTN_WARPS 8
+#endif
+constexpr int kAttnWarps = HV_ATTN_WARPS;   // warps per CTA, each walking its own blocks of the split
 constexpr int kBlockTok = 16;
 
 template <int D>
@@ -129,7 +132,10 @@ __device__ __forceinline__ void merge_and_write(const float (&m)[G], const float
 // Measured on B200, pages in local HBM (tools/attn_probe.py, KV GB/s at the
 // best split count; 4 x 4k / 1 x 128k): register prefetch 1,841 / 2,514;
 // ring of 2 stages 2,082 / 3,192; 3 stages 2,172 / 3,229 (default);
-// 4 stages 1,579 / 2,222 (one resident CTA per SM).  One warp per KV head
+// 4 stages 1,579 / 2,222 (one resident CTA per SM).  Tensor-core form, warps
+// per CTA (best split count each): 2 warps 3,358 / 5,308; 4 warps 3,695 /
+// 5,550; 8 warps 3,988 / 5,900 (default: one 8-warp CTA per SM, splits =
+// SMs / (sequences x KV heads), fewer CTAs to merge).  One warp per KV head
 // with all heads of a page in one CTA (whole-page streaming) measured
 // 1,874 / 2,942: HBM row locality is not the limit, per-warp latency is.
 //

@@ -83,13 +83,13 @@ class KVAttentionDecoder:
         self.seq_start = torch.from_numpy(starts).to(self.dev)
         self.seq_tokens = torch.tensor(self.tokens, dtype=torch.int32, device=self.dev)
         self.nb = max(len(b) for b in blocks)
-        # flash-decoding splits: one wave of (sequence, KV head, split) CTAs at
-        # the kernel's two resident CTAs per SM.  Measured on B200 (tools/
-        # attn_probe.py, HBM pages): 4 x 4k: 8 splits 36 us, 19: 41, 64: 56;
-        # 1 x 128k: 37 splits 199 us, 74: 216, 296: 304 -- fewer, longer
+        # flash-decoding splits: one wave of (sequence, KV head, split) CTAs,
+        # one 8-warp CTA per SM.  Measured on B200 (tools/attn_probe.py, HBM
+        # pages, KV GB/s): 4 x 4k: 4 splits 3,988, 8: 3,313, 19: 2,339;
+        # 1 x 128k: 18 splits 5,900, 37: 5,227, 74: 4,568 -- fewer, longer
         # splits amortize the partial write and merge
         sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
-        self.splits = splits or max(1, min(self.nb, math.ceil(2 * sms / (self.B * m.kv_heads))))
+        self.splits = splits or max(1, min(self.nb, sms // (self.B * m.kv_heads)))
         g_heads = q_heads // m.kv_heads
         self.part = torch.empty(self.B * m.kv_heads * self.splits * g_heads * (m.head_dim + 2), dtype=torch.float32,
                                 device=self.dev)

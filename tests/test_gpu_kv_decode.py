@@ -103,7 +103,7 @@ def test_kv_decode_survives_revocation(durability):
     kv.close(); sysm.close()
 
 
-@pytest.mark.parametrize("D,kvh,g", [(128, 2, 4), (64, 2, 2), (128, 8, 4), (64, 1, 8)])
+@pytest.mark.parametrize("D,kvh,g", [(128, 2, 4), (64, 2, 2), (128, 8, 4), (64, 1, 8), (128, 1, 8), (128, 4, 1)])
 @pytest.mark.parametrize("splits", [1, 3, 64])
 def test_paged_attention_kernel_matches_fp32(D, kvh, g, splits):
     """hv_paged_decode_attention on scattered pages: ragged sequence lengths

@@ -46,6 +46,6 @@ def run(B, ctx, splits_list, kvh=8, g=4, D=128):
 
 
 if __name__ == "__main__":
-    out = {"config1_4x4k": run(4, 4096, [2, 4, 8, 19, 37]),
+    out = {"config1_4x4k": run(4, 4096, [2, 4, 8, 10, 19, 37]),
            "config4_1x128k": run(1, 131072, [9, 18, 37, 74, 148])}
     print(json.dumps(out, indent=1))
