@@ -25,6 +25,7 @@ memcpy gather from the host-authoritative copy) on the box's host cores.
 from __future__ import annotations
 
 import argparse
+import json
 import math
 import os
 import statistics
@@ -473,7 +474,13 @@ def main():
     a = parse()
     if a.impl == "reference":
         return run_reference(a)
-    return run_b200(a)
+    try:
+        return run_b200(a)
+    except Exception as e:   # say what failed on stdout (rank 0), then fail the run
+        if int(os.environ.get("RANK", "0")) == 0:
+            print(json.dumps({"metric": METRIC, "value": None, "n_gpus": a.gpus, "error": repr(e)[:500]}),
+                  flush=True)
+        raise
 
 
 if __name__ == "__main__":
