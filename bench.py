@@ -276,7 +276,7 @@ def run_b200(a):
         bad, n_last = e2e_step(s, True)
         mism += bad
         d2h += 8 * n_last
-        h2d += 16 * n_last       # the verify launch's pointer and size arrays
+        h2d += 24 * n_last       # the verify launch's pointer, size and seed arrays
         # hv_swap_blocks_batch uploads (src, dst) per expert for equal sizes: 16 B each
         h2d += sum(16 * len(routes[s][layer]) for layer in range(L))
         sysm.loop.poll()
