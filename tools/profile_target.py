@@ -41,6 +41,24 @@ def main():
         ds = F.ptrs_tensor([nb * page] * nb, dev)
         for _ in range(reps):
             F.kv_gather_blocks(sb, ss, db, ds, L, page, engine=eng)
+    elif what == "attn":  # K5 paged decode attention, 1 x 128k Llama-3-8B context, pages scattered in HBM
+        from paper_2602_00328_b200 import _native as N
+        B, ctx, kvh, g, D = 1, 131072, 8, 4, 128
+        nb = ctx // 16
+        page = 2 * 16 * kvh * D * 2
+        pool = torch.empty(nb, page, dtype=torch.uint8, device=dev)
+        pool.view(torch.float16).normal_(0, 0.5)
+        ptrs = (torch.randperm(nb, device=dev) * page + pool.data_ptr()).to(torch.int64)
+        start = torch.tensor([0, nb], dtype=torch.int32, device=dev)
+        tok = torch.tensor([ctx], dtype=torch.int32, device=dev)
+        q = torch.randn(B, kvh * g, D, device=dev).to(torch.float16)
+        out = torch.empty(B, kvh * g, D, device=dev)
+        splits = torch.cuda.get_device_properties(0).multi_processor_count // (B * kvh)
+        part = torch.empty(B * kvh * splits * g * (D + 2), device=dev)
+        s = torch.cuda.current_stream().cuda_stream
+        for _ in range(reps):
+            N.call("hv_paged_decode_attention", ptrs.data_ptr(), start.data_ptr(), tok.data_ptr(), q.data_ptr(),
+                   out.data_ptr(), part.data_ptr(), B, kvh * g, kvh, D, 16, splits, 1 / D ** 0.5, s)
     elif what == "fused":  # fused expert FFN at the Qwen1.5-MoE stage shape, experts in HBM
         from paper_2602_00328_b200 import _native as N
         E, T, k, H, I = 60, 32, 4, 2048, 1408
