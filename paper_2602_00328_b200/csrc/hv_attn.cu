@@ -502,28 +502,23 @@ template <int D, int G>
 int launch_attn(const uint64_t* pages, const int32_t* seq_start, const int32_t* seq_tokens, const void* q,
                 float* out, float* part, uint32_t B, uint32_t kvh, uint32_t splits, float scale, cudaStream_t s) {
   dim3 grid(splits, kvh, B);
+  int dev = 0;   // made current by the caller (bind_stream_device)
+  HV_CUDA(cudaGetDevice(&dev));
+  int st;
 #if HV_ATTN_MMA
   {
     constexpr int kS = HV_ATTN_MMA;
     constexpr size_t smem = (size_t)kAttnWarps * kS * Ring<D>::kStage;
-    static bool attr_m = false;
-    if (!attr_m) {
-      HV_CUDA(cudaFuncSetAttribute(paged_decode_mma<D, G, kS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-      attr_m = true;
-    }
+    st = hv::kernel_attr<paged_decode_mma<D, G, kS>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (st) return st;
     paged_decode_mma<D, G, kS><<<grid, kAttnWarps * 32, smem, s>>>(
         pages, seq_start, seq_tokens, reinterpret_cast<const __half*>(q), part, (int)kvh, (int)splits, scale);
   }
 #else
   constexpr int kS = HV_ATTN_RING;
   constexpr size_t smem = (size_t)kAttnWarps * kS * Ring<D>::kStage;
-  static bool attr = false;
-  if (!attr) {
-    HV_CUDA(cudaFuncSetAttribute(paged_decode_split_ring<D, G, kS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    attr = true;
-  }
+  st = hv::kernel_attr<paged_decode_split_ring<D, G, kS>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (st) return st;
   paged_decode_split_ring<D, G, kS><<<grid, kAttnWarps * 32, smem, s>>>(
       pages, seq_start, seq_tokens, reinterpret_cast<const __half*>(q), part, (int)kvh, (int)splits, scale);
 #endif

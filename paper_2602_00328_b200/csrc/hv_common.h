@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/harvest_b200.h"
 
 #define HV_EXPORT extern "C" __attribute__((visibility("default")))
@@ -53,4 +55,18 @@ struct DeviceGuard {
 int bind_stream_device(void* stream, int* device_out, DeviceGuard& g);
 void note_launch(uint64_t n = 1);
 int sm_count(int device);
+
+// Function attributes belong to a kernel in one device's context, so they
+// are set once per (kernel, device).  `Fn` is the kernel; the caller has made
+// `dev` current.
+template <auto Fn>
+int kernel_attr(int dev, cudaFuncAttribute attr, int value) {
+  static std::atomic<uint64_t> done{0};
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return HV_OK;
+  HV_CUDA(cudaFuncSetAttribute(Fn, attr, value));
+  done.fetch_or(bit, std::memory_order_acq_rel);
+  return HV_OK;
+}
+
 }  // namespace hv

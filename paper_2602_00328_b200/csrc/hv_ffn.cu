@@ -396,18 +396,15 @@ int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
   hv::DeviceGuard dg;
   int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
-  static bool attr_set[64] = {};
-  if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-    HV_CUDA(cudaFuncSetAttribute(expert_ffn_kernel<NMAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Smem<NMAT>::kTotal));
-    attr_set[dev] = true;
-  }
+  st = hv::kernel_attr<expert_ffn_kernel<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<NMAT>::kTotal);
+  if (st) return st;
 #if HV_FFN_PERSISTENT
   static int resident[64] = {};
   if (dev >= 0 && dev < 64 && !resident[dev]) {
     int r = 0;
-    HV_CUDA(cudaFuncSetAttribute(expert_ffn_persistent<NMAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Smem<NMAT>::kTotal));
+    st = hv::kernel_attr<expert_ffn_persistent<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      Smem<NMAT>::kTotal);
+    if (st) return st;
     HV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, expert_ffn_persistent<NMAT>, kThreads,
                                                           Smem<NMAT>::kTotal));
     resident[dev] = r > 0 ? r : 1;

@@ -698,20 +698,13 @@ int tma_grid(int dev, uint64_t chunks, int max_ctas) {
   return (int)(g < 1 ? 1 : g);
 }
 
-int set_tma_attrs() {
-  static std::once_flag once;
-  static int st = HV_OK;
-  std::call_once(once, [] {
-    cudaError_t e = cudaFuncSetAttribute(page_copy_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(page_copy_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(desc_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(block_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
-    st = hv_cuda_status(e);
-    (void)cudaGetLastError();
-  });
+int set_tma_attrs(int dev) {
+  const int smem = (int)kTmaSmem;
+  const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  int st = hv::kernel_attr<page_copy_tma<false>>(dev, a, smem);
+  if (!st) st = hv::kernel_attr<page_copy_tma<true>>(dev, a, smem);
+  if (!st) st = hv::kernel_attr<desc_copy_tma>(dev, a, smem);
+  if (!st) st = hv::kernel_attr<block_copy_tma>(dev, a, smem);
   return st;
 }
 
@@ -725,7 +718,7 @@ int launch_pages(PageResolver<kTable> res, int engine, int max_ctas, void* strea
   res.interleave = (engine & kEngineInterleave) ? 1u : 0u;   // explicit flag only (AUTO pages stay linear)
   engine = pick_engine(engine & ~kEngineInterleave);
   if (engine == HV_ENGINE_TMA) {
-    if ((st = set_tma_attrs())) return st;
+    if ((st = set_tma_attrs(dev))) return st;
     res.chunk = kTmaChunk;
     res.chunks_per_page = (uint32_t)((res.page_bytes + kTmaChunk - 1) / kTmaChunk);
     const uint64_t total = (uint64_t)res.n_pages * res.chunks_per_page;
@@ -737,10 +730,11 @@ int launch_pages(PageResolver<kTable> res, int engine, int max_ctas, void* strea
     const uint64_t total = (uint64_t)res.n_pages * res.chunks_per_page;
     if (total >= 0xffffffffull) return HV_E_INVALID;
     const int g = ldg_grid(dev, total, max_ctas);
-    if (engine == HV_ENGINE_LDG256)
+    if (engine == HV_ENGINE_LDG256) {
       page_copy_ldg<kTable, true><<<g, kLdgThreads, 0, (cudaStream_t)stream>>>(res);
-    else
+    } else {
       page_copy_ldg<kTable, false><<<g, kLdgThreads, 0, (cudaStream_t)stream>>>(res);
+    }
   } else if (engine == HV_ENGINE_LDG16) {
     res.chunk = kLdgDeepChunk;
     res.chunks_per_page = (uint32_t)((res.page_bytes + kLdgDeepChunk - 1) / kLdgDeepChunk);
@@ -773,13 +767,17 @@ int launch_blocks(BlockResolver res, int engine, int max_ctas, void* stream) {
   if (total >= 0xffffffffull) return HV_E_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   if (engine == HV_ENGINE_TMA) {
-    if ((st = set_tma_attrs())) return st;
+    if ((st = set_tma_attrs(dev))) return st;
     block_copy_tma<<<tma_grid(dev, total, max_ctas), kTmaThreads, kTmaSmem, s>>>(res);
   } else {
     const int g = ldg_grid(dev, total, max_ctas);
-    if (engine == HV_ENGINE_LDG256) block_copy_ldg<true, kLdgUnroll><<<g, kLdgThreads, 0, s>>>(res);
-    else if (engine == HV_ENGINE_LDG16) block_copy_ldg<false, kLdgDeepUnroll><<<g, kLdgThreads, 0, s>>>(res);
-    else block_copy_ldg<false, kLdgUnroll><<<g, kLdgThreads, 0, s>>>(res);
+    if (engine == HV_ENGINE_LDG256) {
+      block_copy_ldg<true, kLdgUnroll><<<g, kLdgThreads, 0, s>>>(res);
+    } else if (engine == HV_ENGINE_LDG16) {
+      block_copy_ldg<false, kLdgDeepUnroll><<<g, kLdgThreads, 0, s>>>(res);
+    } else {
+      block_copy_ldg<false, kLdgUnroll><<<g, kLdgThreads, 0, s>>>(res);
+    }
   }
   HV_CUDA(cudaGetLastError());
   hv::note_launch();
@@ -801,7 +799,7 @@ int launch_descs(const uint64_t* d_src, const uint64_t* d_dst, const uint64_t* d
   // source (within 2%), and it spreads the reads of a multi-donor batch
   const uint32_t interleave = ((engine & kEngineInterleave) || engine == HV_ENGINE_AUTO) && is_copy ? 1u : 0u;
   engine = pick_engine(engine & ~kEngineInterleave);
-  if (engine == HV_ENGINE_TMA && is_copy && (st = set_tma_attrs())) return st;
+  if (engine == HV_ENGINE_TMA && is_copy && (st = set_tma_attrs(dev))) return st;
   for (uint32_t base = 0; base < n; base += kMaxSmemDescs) {
     const uint32_t m = (n - base) < kMaxSmemDescs ? (n - base) : kMaxSmemDescs;
     DescResolver res;

@@ -151,6 +151,7 @@ class KVAttentionDecoder:
                         self._tr[layer] = {"fetch": (c0, c0), "compute": (c0, c1)}
         else:
             consumed = [None, None]
+            timed_ev = not torch.cuda.is_current_stream_capturing()
             for layer in range(self.L):
                 b = layer % 2
                 if consumed[b] is not None:
@@ -160,7 +161,13 @@ class KVAttentionDecoder:
                     f0.record(self.fetch)
                 F.kv_gather(src[layer], self.page, dst=self.bufs[b], engine=self.engine, max_ctas=self.max_ctas,
                             stream=self.fetch_h)
-                got = torch.cuda.Event(enable_timing=self.trace)
+                # timing-enabled events on purpose (eager steps): with them
+                # the gathers and the attention overlap; with light events the
+                # pair serializes (128k context, K1 capped at 64 CTAs: 10.5 vs
+                # 18.0 ms per step, tools/event_probe.py).  Likely mechanism:
+                # the heavier record delays K5 of layer l, so K1 of layer l+1
+                # places its CTAs first instead of queueing behind K5's.
+                got = torch.cuda.Event(enable_timing=timed_ev)
                 got.record(self.fetch)
                 with torch.cuda.stream(self.compute):
                     self.compute.wait_event(got)
@@ -168,7 +175,7 @@ class KVAttentionDecoder:
                         c0 = torch.cuda.Event(enable_timing=True)
                         c0.record(self.compute)
                     outs[layer] = self._attend(layer, self.buf_pages[b])
-                    done = torch.cuda.Event(enable_timing=self.trace)
+                    done = torch.cuda.Event(enable_timing=timed_ev)
                     done.record(self.compute)
                     consumed[b] = done
                 if self.trace:
