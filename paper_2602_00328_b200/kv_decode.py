@@ -43,6 +43,10 @@ from . import fetch as F
 
 
 class KVAttentionDecoder:
+    # gather-mode issue policy (see _run); class-level so probes can A/B them
+    issue_ahead = True      # issue K1 of layer l+1 before K5 of layer l
+    timed_events = True     # timing-enabled stream events in eager steps
+
     def __init__(self, kv, sequences, q_heads: int, tokens: int | None = None, seed: int = 0,
                  engine: str | None = None, max_ctas: int | None = None, trace: bool = False,
                  fused: bool = False, splits: int | None = None):
@@ -150,36 +154,49 @@ class KVAttentionDecoder:
                         c1.record(self.compute)
                         self._tr[layer] = {"fetch": (c0, c0), "compute": (c0, c1)}
         else:
+            # K1 of layer l+1 and K5 of layer l become ready together (when K1
+            # of layer l completes); the step overlaps them only if K1 places
+            # its CTAs first, otherwise the pair serializes (128k context, K1
+            # capped at 64 CTAs: 18.0 vs 10.5 ms per step).  So the gather of
+            # layer l+1 is issued before the attention of layer l, and eager
+            # steps record timing-enabled events, whose heavier record delays
+            # K5's start (tools/event_probe.py).
             consumed = [None, None]
-            timed_ev = not torch.cuda.is_current_stream_capturing()
-            for layer in range(self.L):
+            got = [None] * self.L
+            timed_ev = self.timed_events and not torch.cuda.is_current_stream_capturing()
+
+            def gather(layer):
                 b = layer % 2
                 if consumed[b] is not None:
                     self.fetch.wait_event(consumed[b])
                 if self.trace:
                     f0 = torch.cuda.Event(enable_timing=True)
                     f0.record(self.fetch)
+                    self._tr[layer] = {"fetch": (f0, None)}
                 F.kv_gather(src[layer], self.page, dst=self.bufs[b], engine=self.engine, max_ctas=self.max_ctas,
                             stream=self.fetch_h)
-                # timing-enabled events on purpose (eager steps): with them
-                # the gathers and the attention overlap; with light events the
-                # pair serializes (128k context, K1 capped at 64 CTAs: 10.5 vs
-                # 18.0 ms per step, tools/event_probe.py).  Likely mechanism:
-                # the heavier record delays K5 of layer l, so K1 of layer l+1
-                # places its CTAs first instead of queueing behind K5's.
-                got = torch.cuda.Event(enable_timing=timed_ev)
-                got.record(self.fetch)
+                got[layer] = torch.cuda.Event(enable_timing=timed_ev or self.trace)
+                got[layer].record(self.fetch)
+                if self.trace:
+                    self._tr[layer]["fetch"] = (f0, got[layer])
+
+            ahead = 1 if self.issue_ahead else 0
+            for layer in range(min(ahead, self.L)):
+                gather(layer)
+            for layer in range(self.L):
+                if layer + ahead < self.L:
+                    gather(layer + ahead)
                 with torch.cuda.stream(self.compute):
-                    self.compute.wait_event(got)
+                    self.compute.wait_event(got[layer])
                     if self.trace:
                         c0 = torch.cuda.Event(enable_timing=True)
                         c0.record(self.compute)
-                    outs[layer] = self._attend(layer, self.buf_pages[b])
-                    done = torch.cuda.Event(enable_timing=timed_ev)
+                    outs[layer] = self._attend(layer, self.buf_pages[layer % 2])
+                    done = torch.cuda.Event(enable_timing=timed_ev or self.trace)
                     done.record(self.compute)
-                    consumed[b] = done
+                    consumed[layer % 2] = done
                 if self.trace:
-                    self._tr[layer] = {"fetch": (f0, got), "compute": (c0, done)}
+                    self._tr[layer]["compute"] = (c0, done)
         cur.wait_stream(self.compute)
         cur.wait_stream(self.fetch)
         return torch.stack(outs)
