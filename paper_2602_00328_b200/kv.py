@@ -101,8 +101,27 @@ class OffloadPolicy:
             raise ValueError("watermark must be in (0, 1]")
 
 
+# Residency version: bumped by every change of where a block's pages are
+# (tier, slot, slab, host slot) or of a slab's mapping, so a reader that caches
+# a resolved page table (kv_decode) re-resolves exactly when it must.  Tracked
+# at the attribute level, so no mutation path can skip it.
+_residency = [0]
+_RESIDENCY_FIELDS = frozenset(("tier", "slot", "slab", "host_slot", "va", "live", "handle"))
+
+
+def residency_version() -> int:
+    return _residency[0]
+
+
+class _Tracked:
+    def __setattr__(self, name, value):
+        if name in _RESIDENCY_FIELDS:
+            _residency[0] += 1
+        object.__setattr__(self, name, value)
+
+
 @dataclass
-class KVBlock:
+class KVBlock(_Tracked):
     """SPEC.md:376-383 (one BlockTable entry)."""
     block_id: int
     sequence_id: int
@@ -123,7 +142,7 @@ def kv_seed(layer: int, seq: int, block_index: int) -> int:
 
 
 @dataclass
-class _Slab:
+class _Slab(_Tracked):
     handle: HarvestHandle
     va: int
     free: list = field(default_factory=list)

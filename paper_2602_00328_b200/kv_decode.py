@@ -40,6 +40,7 @@ import torch
 
 from . import _native as N
 from . import fetch as F
+from .kv import residency_version
 
 
 class KVAttentionDecoder:
@@ -105,17 +106,25 @@ class KVAttentionDecoder:
         self._tr: dict = {}
         self._graph = None
         self._tab_dev = torch.empty(2, len(self.ids), dtype=torch.int64, device=self.dev)
+        self._tab_version, self._tab_handles = None, []
         self._layers = torch.arange(self.L, dtype=torch.int64, device=self.dev).unsqueeze(1)
 
     def _upload_table(self) -> list:
         """Resolve the block table on the host and copy it (pinned, async) into
         the decoder's device table on the current stream, ordered after every
-        earlier step and before this one.  Returns the peer handles read."""
+        earlier step and before this one.  Returns the peer handles read.
+        Skipped while the KV residency version is unchanged (kv.residency_version:
+        every tier/slot/slab change bumps it), so a steady decode step costs no
+        host-side table walk."""
+        ver = residency_version()
+        if ver == self._tab_version:        # no block moved since the last upload
+            return self._tab_handles
         bases, strides, handles = self.kv.page_table(self.ids)
         if np.any(bases % 16) or np.any(strides % 16):
             raise ValueError("paged attention reads 16-byte granules: KV pages must be 16-byte aligned")
         tab = torch.from_numpy(np.stack([bases, strides]).view(np.int64)).pin_memory()
         self._tab_dev.copy_(tab, non_blocking=True)
+        self._tab_version, self._tab_handles = ver, handles
         return handles
 
     def _attend(self, layer: int, pages: torch.Tensor) -> torch.Tensor:
@@ -215,9 +224,10 @@ class KVAttentionDecoder:
                    if s.blocks and any(self.kv.table[b].tier is KVTier.PEER_HBM for b in s.blocks.values())):
                 torch.cuda.synchronize(self.dev)
                 self.kv.sys.loop.poll()
-        lost = [bid for bid in self.ids if self.kv.table[bid].tier is KVTier.NOT_MATERIALIZED]
-        if lost:                            # Lossy blocks revoked since the last step: recompute
-            self.kv.reload(lost)
+        if residency_version() != self._tab_version:
+            lost = [bid for bid in self.ids if self.kv.table[bid].tier is KVTier.NOT_MATERIALIZED]
+            if lost:                        # Lossy blocks revoked since the last step: recompute
+                self.kv.reload(lost)
         handles = self._upload_table()
         batch = rt.begin_reads(handles) if handles else None
         if self._graph is not None:

@@ -199,3 +199,25 @@ def test_resolve_fallback_picks_the_cheaper_option_100_cells():
             assert KVCacheManager.resolve_fallback(stub, lossy, host_link=link) == "Recompute"
             cells += 1
     assert cells == 100
+
+
+def test_kv_residency_version_tracks_every_placement_change():
+    """kv.residency_version (the page-table cache key of kv_decode) must move
+    on every change of where a block's pages are, and only then."""
+    from paper_2602_00328_b200 import kv as K
+    b = K.KVBlock(0, 0, 0, 16, R.Durability.LOSSY)
+    v = K.residency_version()
+    b.last_access = 1.0
+    b.entries = 8
+    assert K.residency_version() == v
+    for name, value in (("tier", K.KVTier.PEER_HBM), ("slot", 3), ("slab", 1), ("host_slot", 7)):
+        setattr(b, name, value)
+        assert K.residency_version() > v, name
+        v = K.residency_version()
+    s = K._Slab(None, 4096)
+    assert K.residency_version() > v
+    v = K.residency_version()
+    s.blocks[0] = 0
+    assert K.residency_version() == v
+    s.live = False
+    assert K.residency_version() > v
