@@ -28,9 +28,10 @@
 // removes the per-item pipeline fill and drain.  A deeper ring for the down
 // kernel alone (HV_FFN_STAGES_DOWN 4 / 6 / 8) costs resident CTAs and lowers
 // its rate (down: 4,224 / 3,329 / 2,154 vs 4,543 GB/s at 3, Qwen stage).
-// 128-row down CTAs (8 warps; 2-3 CTAs/SM, 3-5 stages) left the Qwen stage
-// unchanged (4,443 vs 4,441 GB/s) and moved Phi-3.5 by -5% (batch 16) to
-// +39% (batch 1), so the down kernel keeps the gate/up geometry (run r119).
+// 128-row down CTAs (8 warps; 2-3 CTAs/SM, 3-5 stages) were slower than
+// these 64-row ones on every shape (Qwen stage 3,155-4,443 vs 4,474 GB/s,
+// Phi-3.5 batch 1 1,536-1,750 vs 2,022; runs r119 and r121), so the down
+// kernel keeps the gate/up geometry.
 //
 // Layout of an expert object (the same one K2 moves): gate [I][H], up [I][H],
 // down [H][I], bf16, row-major.  Routed (token, expert) pairs are sorted by
