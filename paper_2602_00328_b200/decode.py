@@ -36,6 +36,8 @@ drain set of a fused step is every peer handle the step may read.
 """
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 import torch
 import torch.nn.functional as TF
@@ -163,6 +165,8 @@ class MoEDecoder:
     def _route(self, h: torch.Tensor, layer: int, slot: int) -> None:
         logits = (h @ self.router[layer].t()).float()
         topv, topi = logits.topk(self.m.top_k, dim=1)
+        if self._counts is not None:
+            self._counts[layer].index_add_(0, topi.reshape(-1), torch.ones_like(topi.reshape(-1)))
         probs = torch.softmax(topv, dim=1)
         comb = self.comb[slot]
         comb.zero_()
@@ -221,6 +225,19 @@ class MoEDecoder:
     # ---------------------------------------------------------------- step
     _capturing = False
     _graph = None
+    _counts = None
+
+    def routing_counts(self, x: torch.Tensor | None = None) -> np.ndarray:
+        """Expert activation counts [L, E] of one eager step from ``x`` (the
+        decoder's input by default): the ``RoutingTrace.counts`` that
+        ``place_offloaded`` ranks experts by (moe.py:354-383)."""
+        self._counts = torch.zeros(self.L, self.E, dtype=torch.int64, device=self.dev)
+        try:
+            x = self.x0 if x is None else x
+            self._step_fused(x) if self.fused else self._step_eager(x)
+            return self._counts.cpu().numpy()
+        finally:
+            self._counts = None
 
     @annotate("harvest.decode_step")
     def step(self, x: torch.Tensor) -> torch.Tensor:
@@ -355,6 +372,8 @@ class MoEDecoder:
         k = self.m.top_k
         logits = (h @ self.router[layer].t()).float()
         topv, topi = logits.topk(k, dim=1)
+        if self._counts is not None:
+            self._counts[layer].index_add_(0, topi.reshape(-1), torch.ones_like(topi.reshape(-1)))
         probs = torch.softmax(topv, dim=1)
         flat = topi.reshape(-1)
         order = torch.argsort(flat, stable=True)
@@ -448,3 +467,92 @@ class MoEDecoder:
             h = self.step(h)
             self.rt.sim.poll() if hasattr(self.rt.sim, "poll") else None
         return h
+
+
+# ------------------------------------------------------------------ sweep
+@dataclass(frozen=True)
+class SweepRow:
+    """moe.py:386-391.  ``stall_s``: fetch time the FFN did not hide, from a
+    traced step's device clock (staged mode; None for fused, which has no
+    separate fetch)."""
+    fraction_pct: float
+    tier: str
+    tokens_per_s: float
+    stall_s: float | None
+
+
+def offload_sweep(system, model, fractions, tier, tokens: int = 32, microbatches: int = 2, seed: int = 0,
+                  fused: bool = False, graph: bool = True, steps: int = 5, warmup: int = 2,
+                  content_seed: int = 0) -> list[SweepRow]:
+    """moe.offload_sweep (moe.py:394-415) on real decode: for each offload
+    fraction, the coldest experts of every layer (ranked by the routing
+    counts of one all-local step) go to ``tier`` -- PEER_HBM through
+    ``place_offloaded``'s rebalance onto ``system``'s donor pools, HOST_DRAM
+    read from the pinned host tier -- the rest stay LOCAL in a resident HBM
+    copy, and a ``MoEDecoder`` is timed on the device clock.  Every
+    fraction's output must equal the all-local output bit for bit (raises
+    otherwise).  Peer handles are freed between fractions."""
+    from .memalloc import Tier
+    from .moe import ExpertResidency, ExpertStore, RoutingTrace, place_offloaded
+    from .runtime import StaleHandleError
+    if tier not in (Tier.PEER_HBM, Tier.HOST_DRAM):
+        raise ValueError(f"offload tier must be peer or host, got {tier}")
+    L, E, S = model.num_layers, model.num_experts, model.expert_size
+    rt, loop = system.runtime, system.loop
+    store = ExpertStore(model, system.host_id, system.host)
+    store.fill_host(system.compute, weights=True)
+    dev = torch.device(f"cuda:{system.compute}")
+    resident = torch.from_numpy(system.host.view()[:L * E * S].copy()).to(dev)
+    local_addr = [[resident.data_ptr() + (layer * E + e) * S for e in range(E)] for layer in range(L)]
+
+    def decoder(residency):
+        f = ExpertFetcher(rt, model, residency, store, local_addr=local_addr)
+        return MoEDecoder(f, tokens=tokens, microbatches=microbatches, seed=seed, fused=fused)
+
+    local = ExpertResidency(model)
+    for layer in range(L):
+        for e in range(E):
+            local.set_tier(layer, e, Tier.LOCAL_HBM)
+    d0 = decoder(local)
+    counts = d0.routing_counts()
+    want = d0.step(d0.x0).clone()
+    trace = RoutingTrace(1, L, E, [], counts)
+    rows = []
+    for fraction in fractions:
+        residency = ExpertResidency(model)
+        place_offloaded(loop, rt, model, residency, trace, fraction, tier, system.host_id, store=store)
+        dec = decoder(residency)
+        got = dec.step(dec.x0)
+        if not torch.equal(got, want):
+            raise RuntimeError(f"offload_sweep: output at {fraction}% differs from the all-local decode")
+        stall = None
+        if not fused:
+            tr = MoEDecoder(dec.f, tokens=tokens, microbatches=microbatches, seed=seed, trace=True)
+            tr.step(tr.x0)
+            rep = tr.overlap_report()
+            stall = max(0.0, rep["span_ms"] - rep["compute_ms"]) * 1e-3 if rep else None
+            del tr
+        if graph:
+            dec.capture_graph()
+        for _ in range(warmup):
+            dec.step(dec.x0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record()
+        for _ in range(steps):
+            dec.step(dec.x0)
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        rows.append(SweepRow(fraction, "peer" if tier == Tier.PEER_HBM else "host", tokens / (ms * 1e-3), stall))
+        del dec
+        torch.cuda.synchronize(dev)
+        loop.run()
+        for ent in residency.entries.values():
+            if ent.handle is not None:
+                try:
+                    rt.harvest_free(ent.handle)
+                except StaleHandleError:
+                    pass
+        loop.run()
+    return rows

@@ -323,3 +323,27 @@ def test_revocation_completes_while_steps_stream(fused):
     assert verify_release_ordering(sysm.loop.log) == []
     sysm.close()
     sys2.close()
+
+
+@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("tier", ["peer", "host"])
+def test_offload_sweep_every_fraction_equals_all_local(tier, fused):
+    """decode.offload_sweep (moe.offload_sweep, moe.py:394-415, on real
+    decode): each fraction's output is bit-identical to the all-local decode
+    (checked inside, raises otherwise); one row per fraction; peer handles
+    are returned between fractions."""
+    from paper_2602_00328_b200.decode import offload_sweep
+    from paper_2602_00328_b200.memalloc import Tier
+    from paper_2602_00328_b200.system import HarvestSystem
+    model = _tiny()
+    L, E, S = model.num_layers, model.num_experts, model.expert_size
+    sysm = HarvestSystem(0, donors=[0] if tier == "peer" else [], donor_bytes=L * E * S + (4 << 20),
+                         host_bytes=L * E * S, local_bytes=1 << 20)
+    rows = offload_sweep(sysm, model, [0, 25, 50, 100], Tier.PEER_HBM if tier == "peer" else Tier.HOST_DRAM,
+                         tokens=16, microbatches=2, fused=fused, steps=2, warmup=1)
+    assert [r.fraction_pct for r in rows] == [0, 25, 50, 100]
+    assert all(r.tier == tier and r.tokens_per_s > 0 for r in rows)
+    assert all((r.stall_s is None) == fused for r in rows)
+    if tier == "peer":                      # every peer handle went back to its donor
+        assert not sysm.runtime.placement
+        assert sysm.runtime.occupied_bytes(1) == 0
