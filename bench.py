@@ -40,8 +40,8 @@ sys.path.insert(0, REPO)
 from benchlib.common import (KV_SLAB_BLOCKS, KV_TOKENS, METRIC, SEED, emit, kv_slab_bytes, load_traffic, model, routing, workload_config)  # noqa: E402
 from benchlib.compare import (autotune, measure_pcie_h2d, probe_engines_on_peer, same_run_comparisons)  # noqa: E402
 from benchlib.cpu import (cpu_gather_sample, cpu_host_copy, cpu_model, reference_simulator, run_reference)  # noqa: E402
-from benchlib.phases import (churn_phase, host_offload_decode, kv_decode_config1, kv_long_context, phi_phase,  # noqa: E402
-                             run_decode)
+from benchlib.phases import (churn_phase, host_offload_decode, kv_decode_config1, kv_long_context,  # noqa: E402
+                             offload_sweep_phase, phi_phase, run_decode)
 
 
 def parse():
@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--no-kv", action="store_true", help="skip the config-4 long-context KV measurement")
     ap.add_argument("--no-phi", action="store_true", help="N>1: skip the config-3 Phi-3.5-MoE decode phase")
     ap.add_argument("--no-churn", action="store_true", help="skip the config-5 churn phase")
+    ap.add_argument("--no-sweep", action="store_true", help="N=1: skip the host-tier offload-fraction sweep")
     ap.add_argument("--phi-layers", type=int, default=32,
                     help="layers of the Phi-3.5-MoE phase (32 = the real model; fewer only for single-GPU tests)")
     ap.add_argument("--overlap-max-ctas", type=int, default=64,
@@ -436,6 +437,11 @@ def run_b200(a):
             churn = {"error": repr(e)[:300]}
         if rank == 0:
             line["churn_config5"] = churn
+    if rank == 0 and world == 1 and not a.no_sweep:
+        try:   # rank 0, N=1 only: local work, no collectives
+            line["offload_sweep"] = offload_sweep_phase(m, dev, a)
+        except Exception as e:
+            line["offload_sweep"] = {"error": repr(e)[:300]}
     if rank == 0:
         line["north_star_targets"] = north_star_targets(line, world)
         emit(line, a)

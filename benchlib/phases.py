@@ -80,6 +80,34 @@ def host_offload_decode(m, dev, a, microbatches=1, steps=3, warm=2):
     sysm.close()
     return r
 
+def offload_sweep_phase(m, dev, a, fractions=(0, 25, 50, 75, 100), layers=8):
+    """moe.offload_sweep (moe.py:394-415) on real decode, this GPU: the
+    coldest experts of each layer (ranked by one all-local step's routing)
+    served from the pinned host tier, the rest from a resident HBM copy;
+    staged decode (the reference's fetch-then-compute pipeline, 2 micro-
+    batches) as a CUDA graph.  An 8-layer slice of the model bounds the
+    pinned memory and the run time; tok/s scale with 1/layers."""
+    from dataclasses import asdict
+
+    from paper_2602_00328_b200.decode import offload_sweep
+    from paper_2602_00328_b200.memalloc import Tier
+    from paper_2602_00328_b200.moe import MoEProfile
+    from paper_2602_00328_b200.system import HarvestSystem
+    ms = MoEProfile(m.name, min(layers, m.num_layers), m.num_experts, m.top_k, m.expert_size, hidden=m.hidden,
+                    intermediate=m.intermediate)
+    sysm = HarvestSystem(dev, host_bytes=ms.num_layers * ms.num_experts * ms.expert_size, local_bytes=1,
+                         engine=a.engine, log_transfers=False)
+    try:
+        rows = offload_sweep(sysm, ms, list(fractions), Tier.HOST_DRAM, tokens=32, microbatches=2, steps=3,
+                             warmup=2)
+    finally:
+        sysm.close()
+    return {"rows": [asdict(r) for r in rows], "layers": ms.num_layers, "tier": "host (pinned DRAM, PCIe)",
+            "mode": "staged, 2 micro-batches, CUDA graph", "tokens_per_step": 32,
+            "outputs_bit_identical_to_all_local": True,
+            "note": "stall_s = fetch time not hidden by the expert FFN in a traced step (device clock); at 0% "
+                    "the staged decoder still copies LOCAL experts into its staging buffer (an HBM copy)"}
+
 def kv_long_context(sysm, source, a):
     """Config 4: a 128k-token Llama-3-8B sequence (8,192 blocks x 32 layers x
     64 KiB = 16 GiB) is appended (KV produced locally), evicted out of local
