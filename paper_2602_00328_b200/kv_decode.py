@@ -127,10 +127,10 @@ class KVAttentionDecoder:
         self._tab_version, self._tab_handles = ver, handles
         return handles
 
-    def _attend(self, layer: int, pages: torch.Tensor) -> torch.Tensor:
-        """hv_paged_decode_attention over the page table `pages` [n] (int64)."""
+    def _attend(self, layer: int, pages: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        """hv_paged_decode_attention over the page table `pages` [n] (int64)
+        into `out` [B, Hq, D] (fp32, contiguous)."""
         m = self.m
-        out = torch.empty(self.B, self.Hq, m.head_dim, dtype=torch.float32, device=self.dev)
         N.call("hv_paged_decode_attention", pages.data_ptr(), self.seq_start.data_ptr(), self.seq_tokens.data_ptr(),
                self.q[layer].data_ptr(), out.data_ptr(), self.part.data_ptr(), self.B, self.Hq, m.kv_heads,
                m.head_dim, m.block_tokens, self.splits, self.scale, torch.cuda.current_stream(self.dev).cuda_stream)
@@ -147,7 +147,9 @@ class KVAttentionDecoder:
         # attention reads them on the compute stream after a stream wait
         with torch.cuda.stream(self.fetch):
             src = self._tab_dev[0].unsqueeze(0) + self._layers * self._tab_dev[1].unsqueeze(0)
-        outs = [None] * self.L
+        # one output allocation per step (on the compute stream, its writer)
+        with torch.cuda.stream(self.compute):
+            outs = torch.empty(self.L, self.B, self.Hq, self.m.head_dim, dtype=torch.float32, device=self.dev)
         if self.fused:                      # attention straight over the resident pages
             with torch.cuda.stream(self.compute):
                 self.compute.wait_stream(self.fetch)
@@ -157,7 +159,7 @@ class KVAttentionDecoder:
                     if self.trace:
                         c0 = torch.cuda.Event(enable_timing=True)
                         c0.record(self.compute)
-                    outs[layer] = self._attend(layer, src[layer])
+                    self._attend(layer, src[layer], outs[layer])
                     if self.trace:
                         c1 = torch.cuda.Event(enable_timing=True)
                         c1.record(self.compute)
@@ -200,7 +202,7 @@ class KVAttentionDecoder:
                     if self.trace:
                         c0 = torch.cuda.Event(enable_timing=True)
                         c0.record(self.compute)
-                    outs[layer] = self._attend(layer, self.buf_pages[layer % 2])
+                    self._attend(layer, self.buf_pages[layer % 2], outs[layer])
                     done = torch.cuda.Event(enable_timing=timed_ev or self.trace)
                     done.record(self.compute)
                     consumed[layer % 2] = done
@@ -208,7 +210,7 @@ class KVAttentionDecoder:
                     self._tr[layer]["compute"] = (c0, done)
         cur.wait_stream(self.compute)
         cur.wait_stream(self.fetch)
-        return torch.stack(outs)
+        return outs
 
     def step(self) -> torch.Tensor:
         """One decode step over all layers: returns the attention outputs
