@@ -14,10 +14,13 @@ into local HBM with ONE launch of the K2 batched-fetch kernel (~22 GB/step).
   donated HBM of the N-1 other GPUs (cudaIpc pools); the fetch pulls them over
   NVLink 5 / NVSwitch.  No collective on the data path ("scaling": "weak").
 
-``value``: device-resident descriptors, the timed region holds only the fetch
-launches.  ``e2e``: the same steps through the public fetch hook
-(ExpertFetcher.issue_fetches: host routing -> descriptors staged H2D -> launch)
-plus a per-step verification kernel whose mismatch counts are read back D2H.
+``value``: descriptor arrays prepared before the timed region; each layer is
+one hv_swap_blocks_batch (engine per source: the copy engine for host-tier
+experts, the K2 kernel for peer ones) plus its per-fetch content check
+(hv_check_digests_batch, read_errors of moe.py:315-319) on a side stream.
+``e2e``: the same steps through the public fetch hook
+(ExpertFetcher.issue_fetches: host routing -> descriptors staged H2D -> fetch
+-> content check), read_errors read back D2H every step.
 
 ``--impl reference``: the reference CPU path (oracle port of the fetch, a
 memcpy gather from the host-authoritative copy) on the box's host cores.
@@ -147,16 +150,30 @@ def run_b200(a):
     staging = [torch.empty(E * S, dtype=torch.uint8, device=f"cuda:{dev}") for _ in range(2)]
     stage_ptrs = [np.array([b.data_ptr() + i * S for i in range(E)], dtype=np.uint64) for b in staging]
 
-    # ---- device-resident descriptors for the kernel-only (value) loop
+    # ---- per-fetch content identity (read_errors, moe.py:315-319): digests of
+    # the authoritative copies -- the pinned host tier at N=1, the placed donor
+    # copies at N>1 (written by the fill above, never modified)
+    if host_tier is not None:
+        expected = store.host_digests(dev)
+    else:
+        expected = np.empty((L, E), dtype=np.uint64)
+        szs = F.ptrs_tensor([S] * E, f"cuda:{dev}")
+        for layer in range(L):
+            expected[layer] = F.digest(F.ptrs_tensor(fetcher.src_addr[layer], f"cuda:{dev}"), szs).cpu().numpy().view(np.uint64)
+    check_s = torch.cuda.Stream(device=f"cuda:{dev}")
+    fetcher.enable_content_check(expected, stream=check_s)
+
+    # ---- host descriptor arrays for the fetch-only (value) loop: what the
+    # fetch hook would hand the library, prepared before the timed region
     desc = []
     for s in range(a.warmup + a.steps):
         row = []
         for layer in range(L):
             ex = routes[s][layer]
-            src = fetcher.src_addr[layer, ex]
-            dst = stage_ptrs[layer % 2][:len(ex)]
-            row.append((F.ptrs_tensor(src, f"cuda:{dev}"), F.ptrs_tensor(dst, f"cuda:{dev}"),
-                        F.ptrs_tensor([S] * len(ex), f"cuda:{dev}"), len(ex) * S))
+            row.append((np.ascontiguousarray(fetcher.src_addr[layer, ex]),
+                        np.ascontiguousarray(stage_ptrs[layer % 2][:len(ex)]),
+                        np.full(len(ex), S, dtype=np.uint64), len(ex) * S,
+                        np.ascontiguousarray(expected[layer, ex])))
         desc.append(row)
     torch.cuda.synchronize()
 
@@ -166,6 +183,7 @@ def run_b200(a):
 
     barrier = group.barrier
     max_over_ranks = group.max
+    a.kernel_engine = a.engine if a.engine not in ("ce", "auto") else "auto"
 
     if a.engine == "auto":
         engines = ("ldg", "ldg256", "ldg16", "tma")
@@ -180,23 +198,47 @@ def run_b200(a):
             # which keeps every donor's egress busy instead of all readers
             # walking the same donors in the same order
             engines = engines + tuple(e + "+il" for e in engines)
-        tune = autotune(desc[0][0], stream, stream_h, F, engines=engines,
+        # plus the copy engine and the library's engine per source
+        tune = autotune(desc[0][0], stream, stream_h, F, engines=engines + ("ce", "auto"),
                         barrier=barrier if world > 1 else None,
                         max_over_ranks=max_over_ranks if world > 1 else None)
         tune["peer_engine_probe"] = safe
+        kern = [r for r in tune["candidates"] if r["engine"] not in ("ce", "auto")]
+        kbest = max(kern, key=lambda r: r["GBps"])
         a.engine, a.max_ctas = tune["best"]["engine"], tune["best"]["max_ctas"]
+        a.kernel_engine = kbest["engine"]
         # every rank must run the same configuration: rank 0 decides
-        a.engine, a.max_ctas = group.decide([a.engine, a.max_ctas])
+        a.engine, a.max_ctas, a.kernel_engine = group.decide([a.engine, a.max_ctas, a.kernel_engine])
         fetcher.engine.engine = N.ENGINES[a.engine]
         fetcher.engine.max_ctas = a.max_ctas
 
+    chk_scratch = torch.zeros(E, dtype=torch.int64, device=f"cuda:{dev}")
+    chk_errors = torch.zeros(1, dtype=torch.int64, device=f"cuda:{dev}")
+    fetch_done = [torch.cuda.Event() for _ in range(L)]
+    check_done = [torch.cuda.Event() for _ in range(L)]
+    eng_code = N.ENGINES[a.engine]
+
     def value_step(s, evs=None):
-        for layer, (sp, dp, sz, nb) in enumerate(desc[s]):
+        """One decode step's fetches: per layer, one hv_swap_blocks_batch on the
+        fetch stream, then its content check on the check stream (beside the
+        next layer's fetch); staging buffer layer%2 is refilled only after the
+        check of two layers back has read it."""
+        for layer, (sp, dp, sz, nb, ex_d) in enumerate(desc[s]):
+            if layer >= 2:
+                stream.wait_event(check_done[layer - 2])
             if evs is not None:
                 evs[layer][0].record(stream)
-            F.batch_copy(sp, dp, sz, engine=a.engine, max_ctas=a.max_ctas, stream=stream_h)
+            N.call("hv_swap_blocks_batch", sp.ctypes.data, dp.ctypes.data, sz.ctypes.data, len(sp), eng_code,
+                   a.max_ctas, stream_h)
             if evs is not None:
                 evs[layer][1].record(stream)
+            fetch_done[layer].record(stream)
+            check_s.wait_event(fetch_done[layer])
+            N.call("hv_check_digests_batch", dp.ctypes.data, sz.ctypes.data, ex_d.ctypes.data, len(sp),
+                   chk_scratch.data_ptr(), 0, chk_errors.data_ptr(), check_s.cuda_stream)
+            check_done[layer].record(check_s)
+        stream.wait_event(check_done[L - 1])
+        stream.wait_event(check_done[L - 2])
 
     for s in range(a.warmup):
         value_step(s)
@@ -229,9 +271,10 @@ def run_b200(a):
         barrier()
     barrier()
     launches = (N.launch_count() - launches0) // (attempt + 1)   # per timed attempt
+    value_read_errors = int(chk_errors.item())
     my_dt = t0.elapsed_time(t1) * 1e-3
     dt = max_over_ranks(my_dt)
-    my_bytes = sum(nb for s in range(a.warmup, a.warmup + a.steps) for (_, _, _, nb) in desc[s])
+    my_bytes = sum(d[3] for s in range(a.warmup, a.warmup + a.steps) for d in desc[s])
     per_rank = group.all_gather((my_bytes, my_dt))     # each rank's own routing -> its own byte count
     total_bytes = sum(nb for nb, _ in per_rank)
     value = total_bytes / dt / 1e9
@@ -240,46 +283,35 @@ def run_b200(a):
     bytes_per_launch = my_bytes / (a.steps * L)
     achieved = bytes_per_launch / (statistics.mean(launch_ms) * 1e-3) / 1e9
 
-    # ---- e2e through the public fetch hook
-    seeds_dev = {}
-
-    def e2e_step(s, check):
-        fb = None
+    # ---- e2e through the public fetch hook (ExpertFetcher.issue_fetches with
+    # its per-fetch content check), read_errors read back D2H every step
+    def e2e_step(s):
+        batches = []
         for layer in range(L):
             ex = routes[s][layer]
-            fb = fetcher.issue_fetches(layer, ex, stage_ptrs[layer % 2][:len(ex)])
-        if check:  # verify the last layer against the generator, read counts back
-            layer = L - 1
-            ex = routes[s][layer]
-            key = (s, layer)
-            if key not in seeds_dev:
-                seeds_dev[key] = F.seeds_tensor([expert_content(m, layer, int(e)) for e in ex], f"cuda:{dev}")
-            with torch.cuda.stream(stream):
-                bad = F.verify_content(F.ptrs_tensor(stage_ptrs[layer % 2][:len(ex)], f"cuda:{dev}"),
-                                       F.ptrs_tensor([S] * len(ex), f"cuda:{dev}"), seeds_dev[key],
-                                       stream=stream_h, weights=True)
-                host_bad = bad.to("cpu", non_blocking=False)
-            return int(host_bad.sum()), len(ex)
-        return 0, 0
+            if layer >= 2:
+                batches[layer - 2].wait_on(stream)   # staging buffer reuse: after that stage's check
+            batches.append(fetcher.issue_fetches(layer, ex, stage_ptrs[layer % 2][:len(ex)]))
+        return fetcher.read_errors()
 
     for s in range(a.warmup):
-        e2e_step(s, True)
+        e2e_step(s)
     sysm.loop.run()
+    errors0 = fetcher.read_errors()
     barrier()
     torch.cuda.synchronize()
-    mism = 0
     d2h = h2d = 0
     w0 = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for k in range(a.steps):
         s = a.warmup + k
-        bad, n_last = e2e_step(s, True)
-        mism += bad
-        d2h += 8 * n_last
-        h2d += 24 * n_last       # the verify launch's pointer, size and seed arrays
-        # hv_swap_blocks_batch uploads (src, dst) per expert for equal sizes: 16 B each
-        h2d += sum(16 * len(routes[s][layer]) for layer in range(L))
+        errors = e2e_step(s)
+        d2h += 8                                   # the read_errors counter
+        nobj = sum(len(routes[s][layer]) for layer in range(L))
+        h2d += 16 * nobj + 24 * nobj               # fetch (src, dst) + check (dst, size, digest) descriptors
+        if source == "host":                       # the step's inputs: expert bytes read from pinned host memory
+            h2d += nobj * S
         sysm.loop.poll()
     e1.record(stream)
     e1.synchronize()
@@ -288,7 +320,14 @@ def run_b200(a):
     barrier()
     e2e_dt = max_over_ranks(max(wall, e0.elapsed_time(e1) * 1e-3))
     e2e_value = total_bytes / e2e_dt / 1e9
-    mism_all = max_over_ranks(float(mism))
+    read_errors_all = max_over_ranks(float(errors - errors0 + value_read_errors))
+    # untimed: the last stage's bytes against the content generator itself
+    # (the read_errors digests are relative to the authoritative copy)
+    ex = routes[a.warmup + a.steps - 1][L - 1]
+    vbad = F.verify_content(F.ptrs_tensor(stage_ptrs[(L - 1) % 2][:len(ex)], f"cuda:{dev}"),
+                            F.ptrs_tensor([S] * len(ex), f"cuda:{dev}"),
+                            [expert_content(m, L - 1, int(e)) for e in ex], weights=True)
+    mism_all = max_over_ranks(float(vbad.sum().item()))
     nvlink_all = group.all_gather(nvlink)
 
     # ---- MoE decode tokens/s through the pipelined decoder (moe.py:211-340)
@@ -387,11 +426,16 @@ def run_b200(a):
                 "warmup": a.warmup, "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
                 "config": {**workload_config(m, world, source), "engine": a.engine, "max_ctas": a.max_ctas,
+                           "kernel_engine": a.kernel_engine,
                            "engine_autotune": tune,
                            "parallelism": f"{world} compute GPU(s)" + (f", each reading N-1={world - 1} donors"
                                                                        if world > 1 else "")},
                 "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": h2d // a.steps,
-                        "d2h_bytes_per_step": d2h // a.steps, "verify_mismatched_words": int(mism_all)},
+                        "d2h_bytes_per_step": d2h // a.steps, "read_errors": int(read_errors_all),
+                        "verify_mismatched_words": int(mism_all),
+                        "read_errors_note": "objects whose fetched bytes' digest differed from the authoritative "
+                                            "copy's, over every fetch of the timed value and e2e steps "
+                                            "(moe.py:315-319)"},
                 "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
                 "clocks": {**clk.summary(), "first_attempt_rejected": remeasured},
                 "latency_ms_per_layer_fetch": statistics.median(launch_ms),
@@ -472,7 +516,7 @@ def north_star_targets(line, world):
     if os.environ.get("HV_DEVICE_MAP"):
         out["stand_in"] = ("HV_DEVICE_MAP: several ranks share one GPU and the 'peers' are IPC imports of "
                            "that GPU's own HBM, so link fractions and ratios here are HBM, not NVLink, figures")
-    out["bit_exact"] = {"fetch_verify_mismatched_words": (line.get("e2e") or {}).get("verify_mismatched_words"),
+    out["bit_exact"] = {"fetch_read_errors": (line.get("e2e") or {}).get("read_errors"),
                         "decode_outputs_equal_all_local_under_churn":
                             (line.get("churn_config5") or {}).get("all_outputs_bit_identical")}
     return out

@@ -13,24 +13,30 @@ if REPO not in sys.path:
 
 GiB = 1 << 30
 
-METRIC = "peer-fetch GB/s"
+METRIC = "expert-fetch GB/s"
 
-TOKENS, SEED = 32, 2
+from benchlib.workload import QWEN15, SEED, TOKENS  # noqa: E402
+from benchlib.workload import routing as _routing  # noqa: E402
 
 KV_TOKENS, KV_SLAB_BLOCKS = 131072, 64   # BASELINE configs[3]: one 128k-token Llama-3-8B sequence
 
-def model():
-    from paper_2602_00328_b200.moe import QWEN15_MOE_A27B, MoEProfile
+def shape():
+    """The workload shape (product-free; see benchlib/workload.py)."""
     layers = int(os.environ.get("HV_BENCH_QWEN_LAYERS", "0"))
     if layers:  # test-only: many ranks on one GPU (the reported config is the 24-layer model)
-        m = QWEN15_MOE_A27B
-        return MoEProfile(m.name, layers, m.num_experts, m.top_k, m.expert_size, hidden=m.hidden,
-                          intermediate=m.intermediate)
-    return QWEN15_MOE_A27B
+        from dataclasses import replace
+        return replace(QWEN15, num_layers=layers)
+    return QWEN15
+
+def model():
+    """The B200 arm's MoEProfile of the same shape."""
+    from paper_2602_00328_b200.moe import MoEProfile
+    w = shape()
+    return MoEProfile(w.name, w.num_layers, w.num_experts, w.top_k, w.expert_size, hidden=w.hidden,
+                      intermediate=w.intermediate)
 
 def routing(m, steps, seed=SEED):
-    from paper_2602_00328_b200.moe import topk_routing
-    return topk_routing(m, TOKENS, steps, seed)
+    return _routing(m, steps, seed, TOKENS)
 
 def workload_config(m, n, source):
     return {"workload": f"{m.name} expert fetch (BASELINE configs[1]): {m.num_layers} layers x "

@@ -68,19 +68,23 @@ def probe_engines_on_peer(handle: bytes, donor: int, nbytes: int, dev: int) -> d
             ok[engine] = False
     return ok
 
-def autotune(layer_desc, stream, stream_h, F, reps=3, engines=("ldg", "ldg256", "ldg16", "tma"),
+def autotune(layer_desc, stream, stream_h, F, reps=3, engines=("ldg", "ldg256", "ldg16", "tma", "ce", "auto"),
              barrier=None, max_over_ranks=None):
-    """Time one layer's real fetch under each engine x grid cap; pick the fastest.
-    Multi-rank: every rank times the same candidate at the same moment
-    (barrier before each), so the measurement includes the contention of all
-    readers on the donors' links; a candidate's time is the max over ranks."""
+    """Time one layer's real fetch (host descriptor arrays, the product's
+    hv_swap_blocks_batch entry point) under each engine x grid cap; pick the
+    fastest.  "ce" is the copy engine (cudaMemcpyBatchAsync), "auto" the
+    library's engine per source (copy engine for large host-tier objects,
+    kernel otherwise).  Multi-rank: every rank times the same candidate at the
+    same moment (barrier before each), so the measurement includes the
+    contention of all readers on the donors' links; a candidate's time is the
+    max over ranks."""
     import torch
-    sp, dp, sz, nb = layer_desc
+    sp, dp, sz, nb = layer_desc[:4]
     rows = []
     for engine in engines:
-        for max_ctas in (0, 296, 148):
-            for _ in range(1):  # warm
-                F.batch_copy(sp, dp, sz, engine=engine, max_ctas=max_ctas, stream=stream_h)
+        grids = (0,) if engine.split("+")[0] in ("ce", "auto") else (0, 296, 148)
+        for max_ctas in grids:
+            F.swap_blocks_batch(sp, dp, sz, engine=engine, max_ctas=max_ctas, stream=stream_h)  # warm
             stream.synchronize()
             if barrier is not None:
                 barrier()
@@ -88,7 +92,7 @@ def autotune(layer_desc, stream, stream_h, F, reps=3, engines=("ldg", "ldg256", 
             for _ in range(reps):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                F.batch_copy(sp, dp, sz, engine=engine, max_ctas=max_ctas, stream=stream_h)
+                F.swap_blocks_batch(sp, dp, sz, engine=engine, max_ctas=max_ctas, stream=stream_h)
                 e1.record(stream)
                 e1.synchronize()
                 ts.append(e0.elapsed_time(e1) * 1e-3)
@@ -141,7 +145,8 @@ def same_run_comparisons(dev, m, a, source, fetcher=None, n=53):
     dp = F.ptrs_tensor([dst.data_ptr() + i * S for i in range(n)], f"cuda:{dev}")
     sz = F.ptrs_tensor([S] * n, f"cuda:{dev}")
     lp = F.ptrs_tensor([loc.data_ptr() + i * S for i in range(n)], f"cuda:{dev}")
-    dt = t(lambda: F.batch_copy(lp, dp, sz, engine=a.engine, stream=s.cuda_stream))
+    keng = getattr(a, "kernel_engine", a.engine)   # the SM kernel engine (device-array entry points)
+    dt = t(lambda: F.batch_copy(lp, dp, sz, engine=keng, stream=s.cuda_stream))
     hbm_peak = 6553.0
     try:
         hbm_peak = float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"])
@@ -157,7 +162,11 @@ def same_run_comparisons(dev, m, a, source, fetcher=None, n=53):
     hs = np.array([h.host_address(i * S) for i in range(n)], dtype=np.uint64)
     lat = {}
     lat["kernel_host"] = t(lambda: F.batch_copy(F.ptrs_tensor([h.device_address(0)], f"cuda:{dev}"), dp[:1],
-                                                sz[:1], engine=a.engine, stream=s.cuda_stream)) * 1e6
+                                                sz[:1], engine=keng, stream=s.cuda_stream)) * 1e6
+    hda = np.array([h.device_address(0)], dtype=np.uint64)
+    lat["product_host"] = t(lambda: F.swap_blocks_batch(hda, hd[:1], hz[:1], engine=a.engine,
+                                                        stream=s.cuda_stream)) * 1e6
+    lat["product_engine"] = a.engine
     lat["copy_engine_host"] = t(lambda: F.ce_batch_copy(hs[:1], hd[:1], hz[:1], batched=False,
                                                         stream=s.cuda_stream)) * 1e6
     if source == "host":
@@ -171,16 +180,19 @@ def same_run_comparisons(dev, m, a, source, fetcher=None, n=53):
         out["copy_engine_same_source_GBps"] = n * S / dce / 1e9
         dce_loop = t(lambda: F.ce_batch_copy(ps, hd, hz, batched=False, stream=s.cuda_stream))
         out["copy_engine_peer_per_object_GBps"] = n * S / dce_loop / 1e9
-        lat["kernel_peer"] = t(lambda: F.batch_copy(pdev[:1], dp[:1], sz[:1], engine=a.engine,
+        lat["kernel_peer"] = t(lambda: F.batch_copy(pdev[:1], dp[:1], sz[:1], engine=keng,
                                                     stream=s.cuda_stream)) * 1e6
         lat["copy_engine_peer"] = t(lambda: F.ce_batch_copy(ps[:1], hd[:1], hz[:1], batched=False,
                                                             stream=s.cuda_stream)) * 1e6
-        lat["peer_vs_host_speedup"] = lat["copy_engine_host"] / lat["kernel_peer"]
+        # the host figure is the faster of the two host paths (copy engine or kernel)
+        lat["peer_vs_host_speedup"] = min(lat["copy_engine_host"], lat["product_host"]) / lat["kernel_peer"]
     # latency distribution (p50/p99 over >= 100 iterations)
     dist_us = {"kernel_host": pct(lambda: F.batch_copy(F.ptrs_tensor([h.device_address(0)], f"cuda:{dev}"), dp[:1],
-                                                       sz[:1], engine=a.engine, stream=s.cuda_stream))}
+                                                       sz[:1], engine=keng, stream=s.cuda_stream)),
+               "product_host": pct(lambda: F.swap_blocks_batch(hda, hd[:1], hz[:1], engine=a.engine,
+                                                               stream=s.cuda_stream))}
     if source == "peer":
-        dist_us["kernel_peer"] = pct(lambda: F.batch_copy(pdev[:1], dp[:1], sz[:1], engine=a.engine,
+        dist_us["kernel_peer"] = pct(lambda: F.batch_copy(pdev[:1], dp[:1], sz[:1], engine=keng,
                                                           stream=s.cuda_stream))
     lat["distribution_us"] = dist_us
     out["single_expert_latency_us"] = lat
@@ -193,13 +205,13 @@ def same_run_comparisons(dev, m, a, source, fetcher=None, n=53):
     hp = HostTier(4 * npg * page)
     host_pages = F.ptrs_tensor([hp.device_address(int(p) * page) for p in rng.permutation(4 * npg)[:npg]],
                                f"cuda:{dev}")
-    dt_h = t(lambda: F.kv_gather(host_pages, page, dst=kdst, engine=a.engine, stream=s.cuda_stream))
+    dt_h = t(lambda: F.kv_gather(host_pages, page, dst=kdst, engine=keng, stream=s.cuda_stream))
     kv["host_us"], kv["host_GBps"] = dt_h * 1e6, npg * page / dt_h / 1e9
     if source == "peer":
         base = fetcher.src_addr[0, :n]   # peer memory of n experts viewed as page slots
         slots = [int(base[i]) + j * page for i in range(n) for j in range(S // page)]
         peer_pages = F.ptrs_tensor([slots[int(p)] for p in rng.permutation(len(slots))[:npg]], f"cuda:{dev}")
-        dt_p = t(lambda: F.kv_gather(peer_pages, page, dst=kdst, engine=a.engine, stream=s.cuda_stream))
+        dt_p = t(lambda: F.kv_gather(peer_pages, page, dst=kdst, engine=keng, stream=s.cuda_stream))
         kv["peer_us"], kv["peer_GBps"] = dt_p * 1e6, npg * page / dt_p / 1e9
         kv["peer_vs_host_speedup"] = dt_h / dt_p
     out["kv_config1_layer_gather"] = kv
@@ -223,13 +235,14 @@ def latency_curves(dev, a, s, t, host, fetcher):
         tiers["peer"] = int(fetcher.src_addr[0, 0])
     one = F.ptrs_tensor([S for S in [0]], f"cuda:{dev}")
     curves, fits = {}, {}
+    hdst = np.array([dst.data_ptr()], dtype=np.uint64)
     for name, base in tiers.items():
         pts = []
         for nb in sizes:
-            sp = F.ptrs_tensor([base], f"cuda:{dev}")
-            dp = F.ptrs_tensor([dst.data_ptr()], f"cuda:{dev}")
-            sz = F.ptrs_tensor([nb], f"cuda:{dev}")
-            pts.append((nb, t(lambda: F.batch_copy(sp, dp, sz, engine=a.engine, stream=s.cuda_stream))))
+            sp = np.array([base], dtype=np.uint64)
+            sz = np.array([nb], dtype=np.uint64)
+            # the product's fetch entry point and engine (per source under "auto")
+            pts.append((nb, t(lambda: F.swap_blocks_batch(sp, hdst, sz, engine=a.engine, stream=s.cuda_stream))))
         curves[name] = [[nb, lat * 1e6] for nb, lat in pts]
         try:
             fc, bw = calibrate(pts)
@@ -245,10 +258,9 @@ def latency_curves(dev, a, s, t, host, fetcher):
                 nb = e * bpe
                 lat = {}
                 for name, base in tiers.items():
-                    sp = F.ptrs_tensor([base], f"cuda:{dev}")
-                    dp = F.ptrs_tensor([dst.data_ptr()], f"cuda:{dev}")
-                    sz = F.ptrs_tensor([nb], f"cuda:{dev}")
-                    lat[name] = t(lambda: F.batch_copy(sp, dp, sz, engine=a.engine, stream=s.cuda_stream))
+                    sp = np.array([base], dtype=np.uint64)
+                    sz = np.array([nb], dtype=np.uint64)
+                    lat[name] = t(lambda: F.swap_blocks_batch(sp, hdst, sz, engine=a.engine, stream=s.cuda_stream))
                 rows.append([model, e, lat["host"] * 1e6, lat["peer"] * 1e6, lat["host"] / lat["peer"]])
         out["kv_reload_latency_experiment"] = {"columns": ["model", "entries", "host_us", "peer_us", "speedup"],
                                                "rows": rows,

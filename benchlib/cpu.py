@@ -9,7 +9,7 @@ import time
 
 import numpy as np
 
-from benchlib.common import METRIC, emit, model, routing, workload_config
+from benchlib.common import METRIC, emit, routing, shape, workload_config
 
 
 def cpu_gather_sample(m, host_buf, route_steps, seconds, threads):
@@ -47,40 +47,43 @@ def host_nexp(m, host_buf):
 def cpu_host_copy(m, n_experts):
     """A host-resident expert table for the CPU legs (content from the oracle)."""
     from oracle import harvest_oracle as O
-    from paper_2602_00328_b200.runtime import stable_hash64
     buf = np.empty(n_experts * m.expert_size, dtype=np.uint8)
     O.fill_batch([buf.ctypes.data + i * m.expert_size for i in range(n_experts)], [m.expert_size] * n_experts,
-                 [stable_hash64("expert", m.name, i // m.num_experts, i % m.num_experts) for i in range(n_experts)],
+                 [O.expert_seed(m.name, i // m.num_experts, i % m.num_experts) for i in range(n_experts)],
                  threads=os.cpu_count() or 1)
     return buf
 
 def run_reference(a):
-    """--impl reference: the oracle port timed on the host cores (rank 0 only)."""
+    """--impl reference: the reference CPU path of the fetch (the oracle port:
+    a memcpy gather of every layer's activated experts from the
+    host-authoritative expert table) on all host cores, rank 0 only.
+
+    Same workload as the B200 arm: the full 24-layer x 60-expert table
+    (24.9 GB of host memory, content from the oracle's generator), the same
+    routing, every layer of every step, the same --steps/--warmup.  This
+    process never imports paper_2602_00328_b200: the only native library it
+    maps is oracle/build/libhv_oracle.so."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    m = model()
+    from oracle import harvest_oracle as O
+    m = shape()
     threads = os.cpu_count() or 1
-    sample_experts = 4 * m.num_experts          # 4 layers' worth of distinct experts (4.15 GB)
-    host = cpu_host_copy(m, sample_experts)
+    host = cpu_host_copy(m, m.num_layers * m.num_experts)
     routes = routing(m, a.steps + a.warmup)
-    per_step = []
+    dst = np.empty(m.num_experts * m.expert_size, dtype=np.uint8)
+    dst[::4096] = 0   # fault the destination in before timing
+    dp_all = [dst.ctypes.data + i * m.expert_size for i in range(m.num_experts)]
 
     def one_step(step):
-        # bounded sample of the step: its first 4 layers (the same activated sets)
-        from oracle import harvest_oracle as O
-        dst = one_step.dst
         moved = 0
         t0 = time.perf_counter()
-        for layer in range(4):
-            ex = step[layer]
+        for layer, ex in enumerate(step):
             src = [host.ctypes.data + (layer * m.num_experts + int(e)) * m.expert_size for e in ex]
-            dp = [dst.ctypes.data + i * m.expert_size for i in range(len(ex))]
-            O.gather(src, dp, [m.expert_size] * len(ex), threads=threads)
+            O.gather(src, dp_all[:len(ex)], [m.expert_size] * len(ex), threads=threads)
             moved += len(ex) * m.expert_size
         return moved, time.perf_counter() - t0
 
-    one_step.dst = np.empty(m.num_experts * m.expert_size, dtype=np.uint8)
     for s in range(a.warmup):
         one_step(routes[s])
     moved = dt = 0.0
@@ -88,15 +91,15 @@ def run_reference(a):
         mv, t = one_step(routes[s])
         moved += mv
         dt += t
-        per_step.append(t)
     gbps = moved / dt / 1e9
     line = {"metric": METRIC, "value": gbps, "unit": "GB/s", "impl": "reference", "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * dt / a.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic", "config": workload_config(m, 1, "host"),
             "cpu_baseline": {"value": gbps, "unit": "GB/s", "cores": threads, "kind": "port", "cpu_model": cpu_model(),
-                             "sample": f"first 4 of {m.num_layers} layers of each decode step "
-                                       f"(memcpy gather, oracle/hv_oracle.c, {threads} threads)"},
+                             "sample": f"every layer ({m.num_layers}) of every decode step, memcpy gather from a "
+                                       f"{m.num_layers * m.num_experts * m.expert_size / 1e9:.1f} GB host expert "
+                                       f"table (oracle/hv_oracle.c, {threads} threads)"},
             "e2e": {"value": gbps, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     try:
         line["reference_simulator"] = reference_simulator(m, max(0, a.gpus - 1))

@@ -17,7 +17,7 @@ def run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, micro
     plan) while the previous stage's SwiGLU experts run on the compute stream."""
     import torch
     from paper_2602_00328_b200.decode import MoEDecoder
-    dec = MoEDecoder(fetcher, tokens=TOKENS, microbatches=microbatches, seed=7, engine=a.engine,
+    dec = MoEDecoder(fetcher, tokens=TOKENS, microbatches=microbatches, seed=7, engine=getattr(a, "kernel_engine", a.engine),
                      max_ctas=a.max_ctas if max_ctas is None else max_ctas, fused=fused)
     h = dec.decode(warm)
     torch.cuda.synchronize()
@@ -389,7 +389,7 @@ def _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported
     sysm.loop.run()
     placed0 = expert_tier_counts(res)["PeerHBM"]
     dec = MoEDecoder(ExpertFetcher(rt, m, res, store), tokens=TOKENS, microbatches=1, seed=13,
-                     engine=a.engine, max_ctas=a.max_ctas, fused=bool(fused))
+                     engine=getattr(a, "kernel_engine", a.engine), max_ctas=a.max_ctas, fused=bool(fused))
     h = dec.step(dec.x0)
     if fused == "graph":        # every later step is one replay; residency changes patch its tables in place
         dec.capture_graph()

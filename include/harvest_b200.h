@@ -155,11 +155,17 @@ int hv_stream_wait_event(void* stream, void* event);
 
 /* ---- fetch engines (the hot path) ------------------------------------- */
 /* engine selector for hv_batch_copy / hv_kv_gather */
-#define HV_ENGINE_AUTO 0   /* LDG; variable-size copies also take HV_ENGINE_FLAG_INTERLEAVE */
+#define HV_ENGINE_AUTO 0   /* LDG; variable-size copies also take HV_ENGINE_FLAG_INTERLEAVE.
+                              hv_swap_blocks_batch: engine per source -- objects of >= 1 MiB read
+                              from the pinned host tier (hv_host_alloc / hv_host_register ranges)
+                              go to the copy engine, the rest to the LDG kernel, concurrently */
 #define HV_ENGINE_LDG 1  /* SM-issued 128-bit ld.global.nc / st.global, warp per 4 KiB chunk */
 #define HV_ENGINE_TMA 2  /* cp.async.bulk global->smem->global ring, one issuing lane per CTA */
 #define HV_ENGINE_LDG256 3 /* LDG with the L2::256B sector-promotion hint (larger remote reads) */
 #define HV_ENGINE_LDG16 4  /* LDG with 16 x 128-bit loads in flight per lane (8 KiB per warp) */
+#define HV_ENGINE_CE 5     /* host-array entry points: every object through the copy engine (one
+                              cudaMemcpyBatchAsync); device-array entry points, which the copy
+                              engine cannot serve, treat it as HV_ENGINE_AUTO */
 /* OR-able flag for the variable-size copies (hv_batch_copy, hv_swap_blocks_batch):
  * when every non-empty object of a launch has the same size, chunk c reads
  * object (c mod n_active) at chunk (c div n_active), so the bytes in flight
@@ -265,6 +271,19 @@ int hv_fill_weights_bf16(const uint64_t* d_dst, const uint64_t* d_bytes,
 /* position-keyed 64-bit digest per object (see oracle/hv_oracle.c) */
 int hv_digest(const uint64_t* d_src, const uint64_t* d_bytes, uint32_t n,
               uint64_t* d_out, void* stream);
+/* Per-fetch content identity (read_errors, moe.py:315-319), on bytes and
+ * for any content: digest each fetched object (d_scratch: n words), compare
+ * with d_expected (the digests of the authoritative copies), set
+ * d_flags[i] = 1 for a mismatch (d_flags may be NULL) and add the number of
+ * mismatching objects to *d_errors.  Stream-ordered; nothing is read back. */
+int hv_check_digests(const uint64_t* d_src, const uint64_t* d_bytes, const uint64_t* d_expected,
+                     uint32_t n, uint64_t* d_scratch, uint8_t* d_flags, uint64_t* d_errors,
+                     void* stream);
+/* hv_check_digests with host arrays (staged through the pinned ring like
+ * hv_swap_blocks_batch): the form the fetch hook calls once per stage. */
+int hv_check_digests_batch(const uint64_t* h_src, const uint64_t* h_bytes, const uint64_t* h_expected,
+                           uint32_t n, uint64_t* d_scratch, uint8_t* d_flags, uint64_t* d_errors,
+                           void* stream);
 /* count of 8-byte words differing from the generator, per object */
 int hv_verify_content(const uint64_t* d_src, const uint64_t* d_bytes,
                       const uint64_t* d_seeds, uint32_t n, uint64_t* d_mismatch,

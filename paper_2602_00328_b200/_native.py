@@ -23,10 +23,12 @@ ENGINE_LDG = 1
 ENGINE_TMA = 2
 ENGINE_LDG256 = 3
 ENGINE_LDG16 = 4
+ENGINE_CE = 5                    # host-array entry points: every object through cudaMemcpyBatchAsync
 ENGINE_FLAG_INTERLEAVE = 0x100   # HV_ENGINE_FLAG_INTERLEAVE: round-robin chunks over equal-size objects
 ENGINES = {"auto": ENGINE_AUTO, "ldg": ENGINE_LDG, "tma": ENGINE_TMA, "ldg256": ENGINE_LDG256,
            "ldg16": ENGINE_LDG16}
 ENGINES.update({f"{k}+il": v | ENGINE_FLAG_INTERLEAVE for k, v in list(ENGINES.items())})
+ENGINES["ce"] = ENGINE_CE
 
 POOL_VMM = 0
 POOL_IPC = 1
@@ -112,6 +114,8 @@ _SIGS = {
     "hv_fill_weights_bf16": [u64, u64, u64, u32, vp],
     "hv_digest": [u64, u64, u32, u64, vp],
     "hv_verify_content": [u64, u64, u64, u32, u64, vp],
+    "hv_check_digests": [u64, u64, u64, u32, u64, u64, u64, vp],
+    "hv_check_digests_batch": [vp, vp, vp, u32, u64, u64, u64, vp],
     "hv_verify_weights_bf16": [u64, u64, u64, u32, u64, vp],
     "hv_launch_count": [P64],
     "hv_expert_ffn_gate_up": [u64, u64, u64, u64, u64, u64, u32, u32, u32, vp],

@@ -676,7 +676,9 @@ constexpr size_t kTmaSmem = (size_t)kTmaStages * kTmaChunk;
 // ---------------------------------------------------------------------------
 // launch helpers
 
-int pick_engine(int engine) { return engine == HV_ENGINE_AUTO ? HV_ENGINE_LDG : engine; }
+// Device-array entry points run on the SMs: AUTO -- and CE, which needs host
+// descriptors -- mean the LDG kernel there.
+int pick_engine(int engine) { return (engine == HV_ENGINE_AUTO || engine == HV_ENGINE_CE) ? HV_ENGINE_LDG : engine; }
 
 constexpr uint64_t kUnknownChunks = ~0ull;  // device-resident sizes: fill the device
 
@@ -797,7 +799,8 @@ int launch_descs(const uint64_t* d_src, const uint64_t* d_dst, const uint64_t* d
   if (st) return st;
   // AUTO copies take the interleaved order: neutral on a PCIe or local-HBM
   // source (within 2%), and it spreads the reads of a multi-donor batch
-  const uint32_t interleave = ((engine & kEngineInterleave) || engine == HV_ENGINE_AUTO) && is_copy ? 1u : 0u;
+  const uint32_t interleave =
+      ((engine & kEngineInterleave) || engine == HV_ENGINE_AUTO || engine == HV_ENGINE_CE) && is_copy ? 1u : 0u;
   engine = pick_engine(engine & ~kEngineInterleave);
   if (engine == HV_ENGINE_TMA && is_copy && (st = set_tma_attrs(dev))) return st;
   for (uint32_t base = 0; base < n; base += kMaxSmemDescs) {
@@ -969,15 +972,14 @@ HV_EXPORT int hv_batch_copy(const uint64_t* d_src, const uint64_t* d_dst, const 
   return launch_descs(d_src, d_dst, d_bytes, n, engine, max_ctas, stream, CopyOpR{}, true);
 }
 
-HV_EXPORT int hv_swap_blocks_batch(const uint64_t* h_src, const uint64_t* h_dst, const uint64_t* h_bytes, uint32_t n,
-                                   int engine, int max_ctas, void* stream) {
-  if (n == 0) return HV_OK;
-  HV_CHECK_ARG(h_src && h_dst && h_bytes);
-  int dev = 0;
-  hv::DeviceGuard dg;
-  int st = hv::bind_stream_device(stream, &dev, dg);
-  if (st) return st;
-  std::lock_guard<std::mutex> lk(g_ring_mu);
+namespace {
+
+// The kernel form of the host-array entry point: descriptors staged through
+// the pinned ring (one H2D of exactly what is used), then one K1/K2 launch
+// per ring slot.  Caller holds g_ring_mu and has bound the device.
+int kernel_swap(const uint64_t* h_src, const uint64_t* h_dst, const uint64_t* h_bytes, uint32_t n, int engine,
+                int max_ctas, void* stream, int dev) {
+  int st = HV_OK;
   for (uint32_t base = 0; base < n; base += kSlotDescs) {
     const uint32_t m = (n - base) < kSlotDescs ? (n - base) : kSlotDescs;
     uint32_t slot = 0;
@@ -994,7 +996,6 @@ HV_EXPORT int hv_swap_blocks_batch(const uint64_t* h_src, const uint64_t* h_dst,
       uniform &= (h_bytes[base + i] == h_bytes[base]);
       total_bytes += h_bytes[base + i];
     }
-    // packed [src m][dst m][bytes m]: one H2D of exactly what is used
     memcpy(hs, h_src + base, m * 8);
     memcpy(hs + m, h_dst + base, m * 8);
     memcpy(hs + 2 * m, h_bytes + base, m * 8);
@@ -1025,6 +1026,153 @@ HV_EXPORT int hv_swap_blocks_batch(const uint64_t* h_src, const uint64_t* h_dst,
   return HV_OK;
 }
 
+// Per-device side stream for copy-engine work that must run beside (not
+// behind) a kernel on the caller's stream, or that the legacy NULL stream
+// cannot take (cudaMemcpyBatchAsync rejects it).  Fenced by events on both
+// sides, so the caller's stream order is preserved.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+std::mutex g_side_mu;
+SideStream g_side[64];
+
+int side_stream(int dev, SideStream** out) {
+  if (dev < 0 || dev >= 64) return HV_E_INVALID;
+  SideStream& ss = g_side[dev];
+  if (!ss.s) {
+    HV_CUDA(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
+    HV_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+    HV_CUDA(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+  }
+  *out = &ss;
+  return HV_OK;
+}
+
+// One cudaMemcpyBatchAsync submission (or n cudaMemcpyAsync when !batched)
+// on a non-NULL stream.
+int ce_submit(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t n, bool batched,
+              cudaStream_t stream) {
+  if (n == 0) return HV_OK;
+  if (!batched) {
+    for (size_t i = 0; i < n; ++i) HV_CUDA(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDefault, stream));
+    return HV_OK;
+  }
+  cudaMemcpyAttributes attr;
+  memset(&attr, 0, sizeof(attr));
+  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+  size_t attr_idx = 0, fail_idx = 0;
+  HV_CUDA(cudaMemcpyBatchAsync(const_cast<void**>(dsts), const_cast<void**>(srcs), const_cast<size_t*>(sizes), n,
+                               &attr, &attr_idx, 1, &fail_idx, stream));
+  return HV_OK;
+}
+
+// ce_submit on `stream`, or on the device's side stream fenced by events when
+// `stream` is the legacy NULL stream.
+int ce_on_stream(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t n, bool batched,
+                 void* stream, int dev) {
+  if (stream != nullptr || !batched) return ce_submit(dsts, srcs, sizes, n, batched, (cudaStream_t)stream);
+  std::lock_guard<std::mutex> lk(g_side_mu);
+  SideStream* ss = nullptr;
+  int st = side_stream(dev, &ss);
+  if (st) return st;
+  HV_CUDA(cudaEventRecord(ss->fork, nullptr));
+  HV_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+  if ((st = ce_submit(dsts, srcs, sizes, n, true, ss->s))) return st;
+  HV_CUDA(cudaEventRecord(ss->join, ss->s));
+  HV_CUDA(cudaStreamWaitEvent(nullptr, ss->join, 0));
+  return HV_OK;
+}
+
+constexpr uint64_t kCeMinBytes = 1ull << 20;  // host-tier objects at least this large go to the copy engine
+
+bool capturing(void* stream) {
+  if (!stream) return false;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing((cudaStream_t)stream, &cap) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return cap != cudaStreamCaptureStatusNone;
+}
+
+}  // namespace
+
+HV_EXPORT int hv_swap_blocks_batch(const uint64_t* h_src, const uint64_t* h_dst, const uint64_t* h_bytes, uint32_t n,
+                                   int engine, int max_ctas, void* stream) {
+  if (n == 0) return HV_OK;
+  HV_CHECK_ARG(h_src && h_dst && h_bytes);
+  int dev = 0;
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
+  if (st) return st;
+  const int base_engine = engine & ~kEngineInterleave;
+  if (base_engine == HV_ENGINE_CE) {
+    std::vector<void*> d(n);
+    std::vector<const void*> s(n);
+    std::vector<size_t> z(n);
+    for (uint32_t i = 0; i < n; ++i) {
+      d[i] = (void*)h_dst[i];
+      s[i] = (const void*)h_src[i];
+      z[i] = (size_t)h_bytes[i];
+    }
+    return ce_on_stream(d.data(), s.data(), z.data(), n, true, stream, dev);
+  }
+  if (base_engine != HV_ENGINE_AUTO || capturing(stream)) {
+    std::lock_guard<std::mutex> lk(g_ring_mu);
+    return kernel_swap(h_src, h_dst, h_bytes, n, engine, max_ctas, stream, dev);
+  }
+  // AUTO: engine per source.  Large objects read from the pinned host tier
+  // go to the copy engine (one cudaMemcpyBatchAsync); everything else --
+  // peer HBM over NVLink, local HBM, small host pages -- to the SM kernel.
+  std::vector<uint32_t> ce_idx;
+  for (uint32_t i = 0; i < n; ++i)
+    if (h_bytes[i] >= kCeMinBytes && hv::host_range_contains(h_src[i], h_bytes[i])) ce_idx.push_back(i);
+  if (ce_idx.empty()) {
+    std::lock_guard<std::mutex> lk(g_ring_mu);
+    return kernel_swap(h_src, h_dst, h_bytes, n, engine, max_ctas, stream, dev);
+  }
+  std::vector<void*> cd(ce_idx.size());
+  std::vector<const void*> cs(ce_idx.size());
+  std::vector<size_t> cz(ce_idx.size());
+  for (size_t k = 0; k < ce_idx.size(); ++k) {
+    cd[k] = (void*)h_dst[ce_idx[k]];
+    cs[k] = (const void*)h_src[ce_idx[k]];
+    cz[k] = (size_t)h_bytes[ce_idx[k]];
+  }
+  if (ce_idx.size() == n) return ce_on_stream(cd.data(), cs.data(), cz.data(), n, true, stream, dev);
+  // mixed batch: the copy engine runs on the side stream beside the kernel
+  // (two links, two engines), joined back before the caller's next op
+  std::vector<uint64_t> ks, kd, kz;
+  ks.reserve(n - ce_idx.size());
+  kd.reserve(n - ce_idx.size());
+  kz.reserve(n - ce_idx.size());
+  for (uint32_t i = 0, k = 0; i < n; ++i) {
+    if (k < ce_idx.size() && ce_idx[k] == i) {
+      ++k;
+      continue;
+    }
+    ks.push_back(h_src[i]);
+    kd.push_back(h_dst[i]);
+    kz.push_back(h_bytes[i]);
+  }
+  std::lock_guard<std::mutex> lk_side(g_side_mu);
+  SideStream* ss = nullptr;
+  if ((st = side_stream(dev, &ss))) return st;
+  HV_CUDA(cudaEventRecord(ss->fork, (cudaStream_t)stream));
+  HV_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+  if ((st = ce_submit(cd.data(), cs.data(), cz.data(), cd.size(), true, ss->s))) return st;
+  {
+    std::lock_guard<std::mutex> lk(g_ring_mu);
+    if ((st = kernel_swap(ks.data(), kd.data(), kz.data(), (uint32_t)ks.size(), engine, max_ctas, stream, dev)))
+      return st;
+  }
+  HV_CUDA(cudaEventRecord(ss->join, ss->s));
+  HV_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, ss->join, 0));
+  return HV_OK;
+}
+
 HV_EXPORT int hv_ce_batch_copy(const uint64_t* h_src, const uint64_t* h_dst, const uint64_t* h_bytes, uint32_t n,
                                int batched, void* stream) {
   if (n == 0) return HV_OK;
@@ -1033,48 +1181,15 @@ HV_EXPORT int hv_ce_batch_copy(const uint64_t* h_src, const uint64_t* h_dst, con
   hv::DeviceGuard dg;
   int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
-  if (!batched) {
-    for (uint32_t i = 0; i < n; ++i)
-      HV_CUDA(cudaMemcpyAsync((void*)h_dst[i], (const void*)h_src[i], h_bytes[i], cudaMemcpyDefault,
-                              (cudaStream_t)stream));
-    return HV_OK;
-  }
-  std::vector<void*> dsts(n), srcs(n);
+  std::vector<void*> dsts(n);
+  std::vector<const void*> srcs(n);
   std::vector<size_t> sizes(n);
   for (uint32_t i = 0; i < n; ++i) {
     dsts[i] = (void*)h_dst[i];
-    srcs[i] = (void*)h_src[i];
+    srcs[i] = (const void*)h_src[i];
     sizes[i] = (size_t)h_bytes[i];
   }
-  cudaMemcpyAttributes attr;
-  memset(&attr, 0, sizeof(attr));
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-  size_t attr_idx = 0, fail_idx = 0;
-  if (stream != nullptr) {
-    HV_CUDA(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr, &attr_idx, 1, &fail_idx,
-                                 (cudaStream_t)stream));
-    return HV_OK;
-  }
-  // batched copies are rejected on the legacy NULL stream: run them on a
-  // side stream fenced by events on both sides, which keeps NULL-stream order
-  static std::mutex mu;
-  static cudaStream_t side[64] = {};
-  static cudaEvent_t before[64] = {}, after[64] = {};
-  std::lock_guard<std::mutex> lk(mu);
-  if (dev < 0 || dev >= 64) return HV_E_INVALID;
-  if (!side[dev]) {
-    HV_CUDA(cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking));
-    HV_CUDA(cudaEventCreateWithFlags(&before[dev], cudaEventDisableTiming));
-    HV_CUDA(cudaEventCreateWithFlags(&after[dev], cudaEventDisableTiming));
-  }
-  HV_CUDA(cudaEventRecord(before[dev], nullptr));
-  HV_CUDA(cudaStreamWaitEvent(side[dev], before[dev], 0));
-  HV_CUDA(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr, &attr_idx, 1, &fail_idx,
-                               side[dev]));
-  HV_CUDA(cudaEventRecord(after[dev], side[dev]));
-  HV_CUDA(cudaStreamWaitEvent(nullptr, after[dev], 0));
-  return HV_OK;
+  return ce_on_stream(dsts.data(), srcs.data(), sizes.data(), n, batched != 0, stream, dev);
 }
 
 HV_EXPORT int hv_fill_content(const uint64_t* d_dst, const uint64_t* d_bytes, const uint64_t* d_seeds, uint32_t n,
@@ -1110,6 +1225,72 @@ HV_EXPORT int hv_digest(const uint64_t* d_src, const uint64_t* d_bytes, uint32_t
   op.bytes = d_bytes;
   op.out = reinterpret_cast<unsigned long long*>(d_out);
   return launch_descs(d_src, d_src, d_bytes, n, HV_ENGINE_LDG, 0, stream, op, false);
+}
+
+namespace {
+// read_errors of moe.py:315-319 on bytes: object i is a read error when the
+// digest of what arrived differs from the digest recorded for its
+// authoritative copy.  Per-object flags plus one running counter.
+__global__ void digest_compare_kernel(const uint64_t* __restrict__ got, const uint64_t* __restrict__ want,
+                                      uint32_t n, uint8_t* __restrict__ flags,
+                                      unsigned long long* __restrict__ errors) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool bad = i < n && got[i] != want[i];
+  if (i < n && flags) flags[i] = bad ? 1 : 0;
+  const unsigned m = __ballot_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(errors, (unsigned long long)__popc(m));
+}
+}  // namespace
+
+HV_EXPORT int hv_check_digests(const uint64_t* d_src, const uint64_t* d_bytes, const uint64_t* d_expected,
+                               uint32_t n, uint64_t* d_scratch, uint8_t* d_flags, uint64_t* d_errors,
+                               void* stream) {
+  if (n == 0) return HV_OK;
+  HV_CHECK_ARG(d_src && d_bytes && d_expected && d_scratch && d_errors);
+  int dev = 0;
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
+  if (st) return st;
+  HV_CUDA(cudaMemsetAsync(d_scratch, 0, (size_t)n * 8, (cudaStream_t)stream));
+  DigestOpR op;
+  op.bytes = d_bytes;
+  op.out = reinterpret_cast<unsigned long long*>(d_scratch);
+  if ((st = launch_descs(d_src, d_src, d_bytes, n, HV_ENGINE_LDG, 0, stream, op, false))) return st;
+  digest_compare_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+      d_scratch, d_expected, n, d_flags, reinterpret_cast<unsigned long long*>(d_errors));
+  HV_CUDA(cudaGetLastError());
+  hv::note_launch();
+  return HV_OK;
+}
+
+HV_EXPORT int hv_check_digests_batch(const uint64_t* h_src, const uint64_t* h_bytes, const uint64_t* h_expected,
+                                     uint32_t n, uint64_t* d_scratch, uint8_t* d_flags, uint64_t* d_errors,
+                                     void* stream) {
+  if (n == 0) return HV_OK;
+  HV_CHECK_ARG(h_src && h_bytes && h_expected && d_scratch && d_errors);
+  int dev = 0;
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
+  if (st) return st;
+  std::lock_guard<std::mutex> lk(g_ring_mu);
+  for (uint32_t base = 0; base < n; base += kSlotDescs) {
+    const uint32_t m = (n - base) < kSlotDescs ? (n - base) : kSlotDescs;
+    uint32_t slot = 0;
+    StagingRing* ring = nullptr;
+    if ((st = ring_acquire(dev, &slot, &ring))) return st;
+    uint64_t* hs = ring->h + (size_t)slot * 3 * kSlotDescs;
+    uint64_t* ds = ring->d + (size_t)slot * 3 * kSlotDescs;
+    memcpy(hs, h_src + base, m * 8);
+    memcpy(hs + m, h_bytes + base, m * 8);
+    memcpy(hs + 2 * m, h_expected + base, m * 8);
+    HV_CUDA(cudaMemcpyAsync(ds, hs, (size_t)3 * m * 8, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    if ((st = hv_check_digests(ds, ds + m, ds + 2 * m, m, d_scratch + base, d_flags ? d_flags + base : nullptr,
+                               d_errors, stream)))
+      return st;
+    HV_CUDA(cudaEventRecord(ring->ev[slot], (cudaStream_t)stream));
+    ring->used[slot] = true;
+  }
+  return HV_OK;
 }
 
 HV_EXPORT int hv_verify_content(const uint64_t* d_src, const uint64_t* d_bytes, const uint64_t* d_seeds, uint32_t n,

@@ -18,11 +18,38 @@
 #include <cuda.h>
 #include <string.h>
 
+#include <map>
 #include <mutex>
 #include <new>
+#include <shared_mutex>
 #include <vector>
 
 #include "hv_common.h"
+
+namespace hv {
+namespace {
+std::shared_mutex g_host_mu;
+std::map<uint64_t, uint64_t> g_host_ranges;  // base -> end (exclusive)
+}  // namespace
+
+void host_range_add(uint64_t base, uint64_t bytes) {
+  std::unique_lock<std::shared_mutex> lk(g_host_mu);
+  g_host_ranges[base] = base + bytes;
+}
+
+void host_range_remove(uint64_t base) {
+  std::unique_lock<std::shared_mutex> lk(g_host_mu);
+  g_host_ranges.erase(base);
+}
+
+bool host_range_contains(uint64_t p, uint64_t bytes) {
+  std::shared_lock<std::shared_mutex> lk(g_host_mu);
+  auto it = g_host_ranges.upper_bound(p);
+  if (it == g_host_ranges.begin()) return false;
+  --it;
+  return p >= it->first && p + bytes <= it->second;
+}
+}  // namespace hv
 
 namespace {
 
@@ -375,6 +402,8 @@ HV_EXPORT int hv_host_alloc(uint64_t bytes, void** h_ptr, uint64_t* d_alias) {
   }
   *h_ptr = p;
   if (d_alias) *d_alias = (uint64_t)d;
+  hv::host_range_add((uint64_t)p, bytes);
+  if (d != p) hv::host_range_add((uint64_t)d, bytes);
   return HV_OK;
 }
 
@@ -393,11 +422,20 @@ HV_EXPORT int hv_host_alloc_flags(uint64_t bytes, unsigned flags, void** h_ptr, 
   }
   *h_ptr = p;
   if (d_alias) *d_alias = (uint64_t)d;
+  hv::host_range_add((uint64_t)p, bytes);
+  if (d != p) hv::host_range_add((uint64_t)d, bytes);
   return HV_OK;
 }
 
 HV_EXPORT int hv_host_free(void* h_ptr) {
   if (!h_ptr) return HV_OK;
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, h_ptr, 0) != cudaSuccess) {
+    (void)cudaGetLastError();
+    d = nullptr;
+  }
+  hv::host_range_remove((uint64_t)h_ptr);
+  if (d && d != h_ptr) hv::host_range_remove((uint64_t)d);
   HV_CUDA(cudaFreeHost(h_ptr));
   return HV_OK;
 }
@@ -408,10 +446,19 @@ HV_EXPORT int hv_host_register(void* h_ptr, uint64_t bytes, uint64_t* d_alias) {
   void* d = nullptr;
   HV_CUDA(cudaHostGetDevicePointer(&d, h_ptr, 0));
   if (d_alias) *d_alias = (uint64_t)d;
+  hv::host_range_add((uint64_t)h_ptr, bytes);
+  if (d != h_ptr) hv::host_range_add((uint64_t)d, bytes);
   return HV_OK;
 }
 
 HV_EXPORT int hv_host_unregister(void* h_ptr) {
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, h_ptr, 0) != cudaSuccess) {
+    (void)cudaGetLastError();
+    d = nullptr;
+  }
+  hv::host_range_remove((uint64_t)h_ptr);
+  if (d && d != h_ptr) hv::host_range_remove((uint64_t)d);
   HV_CUDA(cudaHostUnregister(h_ptr));
   return HV_OK;
 }

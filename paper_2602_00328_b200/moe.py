@@ -161,6 +161,19 @@ class ExpertStore:
                  [expert_content(m, layer, e) for e in range(m.num_experts)])
         torch.cuda.synchronize(device)
 
+    def host_digests(self, device: int = 0) -> np.ndarray:
+        """Digest of every expert's authoritative host copy ([L, E] uint64,
+        hv_digest over the mapped host tier): the expected values of the
+        per-fetch content check (ExpertFetcher.enable_content_check)."""
+        m = self.model
+        out = np.empty((m.num_layers, m.num_experts), dtype=np.uint64)
+        sizes = F.ptrs_tensor([m.expert_size] * m.num_experts, f"cuda:{device}")
+        for layer in range(m.num_layers):
+            ptrs = [self.host.device_address(self.host_offset(layer, e)) for e in range(m.num_experts)]
+            d = F.digest(F.ptrs_tensor(ptrs, f"cuda:{device}"), sizes)
+            out[layer] = d.cpu().numpy().view(np.uint64)
+        return out
+
 
 def rebalance(sim, runtime: HarvestRuntime, model: MoEProfile, residency: ExpertResidency,
               counts: np.ndarray, host_device_id: int, max_migrations: int | None = None,
@@ -260,6 +273,50 @@ class ExpertFetcher:
             self._update(l, e, ent.tier, ent.handle)
         residency.on_change(self._update)
         self.sizes_cache: dict[int, np.ndarray] = {}
+        self.expected = None   # [L, E] digests of the authoritative copies (enable_content_check)
+        self.reads = 0         # DecodeMetrics.reads (moe.py:200-208): objects fetched
+
+    def enable_content_check(self, expected_digests: np.ndarray, stream=None) -> None:
+        """Check the content identity of every fetch, as the reference does on
+        every arrival (moe.py:315-319: ``content != expected`` -> read_errors):
+        after each stage's fetch, hv_check_digests_batch digests what arrived
+        on ``stream`` (default: a new stream of the fetch device) and counts
+        the objects whose digest differs from ``expected_digests[layer, e]``.
+        The check runs beside the next stage's fetch; ``FetchBatch.event`` then
+        covers the fetch and its check (reuse the staging buffer after it)."""
+        L, E = self.model.num_layers, self.model.num_experts
+        exp = np.ascontiguousarray(expected_digests, dtype=np.uint64)
+        if exp.shape != (L, E):
+            raise ValueError(f"expected digests must be [{L}, {E}]")
+        dev = self.engine.cuda_device
+        self.expected = exp
+        self._check_stream = N.stream_handle(stream) if stream is not None else self._new_stream(dev)
+        self._scratch = torch.zeros(E, dtype=torch.int64, device=f"cuda:{dev}")
+        self._flags = torch.zeros(E, dtype=torch.uint8, device=f"cuda:{dev}")
+        self._errors = torch.zeros(1, dtype=torch.int64, device=f"cuda:{dev}")
+        self._check_events = []
+        self.fetches_checked = 0
+
+    @staticmethod
+    def _new_stream(dev: int) -> int:
+        import ctypes as C
+        s = C.c_void_p()
+        N.call("hv_stream_create", dev, 0, C.byref(s))
+        return s.value or 0
+
+    def read_errors(self) -> int:
+        """DecodeMetrics.read_errors (moe.py:200-208): fetched objects whose
+        bytes differed from their authoritative copy, over every checked
+        stage so far (synchronizes the check stream)."""
+        if self.expected is None:
+            raise RuntimeError("content check not enabled (enable_content_check)")
+        N.call("hv_stream_synchronize", self._check_stream)
+        return int(self._errors.cpu().item())
+
+    def last_read_error_flags(self) -> np.ndarray:
+        """Per-object mismatch flags of the most recent checked stage."""
+        N.call("hv_stream_synchronize", self._check_stream)
+        return self._flags.cpu().numpy()
 
     def _update(self, layer, expert, tier, handle) -> None:
         self.version = getattr(self, "version", 0) + 1
@@ -310,11 +367,33 @@ class ExpertFetcher:
             sizes = self.sizes_cache[n] = np.full(n, self.model.expert_size, dtype=np.uint64)
         batch = self.rt.begin_reads(handles) if handles else None
         event = None
+        self.reads += n
         if n:
             cbs = [lambda _x, b=batch: self.rt.end_reads(b)] if batch else []
-            self.engine.launch_raw(src, np.ascontiguousarray(dst), sizes, callbacks=cbs)
+            dst = np.ascontiguousarray(dst)
+            self.engine.launch_raw(src, dst, sizes, callbacks=cbs)
             event = self.engine.last_event
+            if self.expected is not None:
+                event = self._check(layer, ex, dst, sizes, event)
         return FetchBatch(layer, ex, t[keep].copy(), event)
+
+    def _check(self, layer, ex, dst, sizes, fetch_event):
+        """Digest the stage's arrivals on the check stream (after the fetch)
+        and count mismatches against the authoritative digests."""
+        import ctypes as C
+        N.call("hv_stream_wait_event", self._check_stream, fetch_event)
+        exp = np.ascontiguousarray(self.expected[layer, ex])
+        N.call("hv_check_digests_batch", dst.ctypes.data, sizes.ctypes.data, exp.ctypes.data, len(ex),
+               self._scratch.data_ptr(), self._flags.data_ptr(), self._errors.data_ptr(), self._check_stream)
+        # a small ring of check events (the fetch engine recycles its own)
+        if len(self._check_events) < 8:
+            e = C.c_void_p()
+            N.call("hv_event_create", self.engine.cuda_device, 0, C.byref(e))
+            self._check_events.append(e)
+        ev = self._check_events[self.fetches_checked % len(self._check_events)]
+        N.call("hv_event_record", ev, self._check_stream)
+        self.fetches_checked += 1
+        return ev
 
 
 @dataclass

@@ -14,10 +14,12 @@ PROF = os.path.join(REPO, "profiles")
 
 
 def _line(name):
-    p = os.path.join(PROF, name)
-    if not os.path.exists(p):
-        pytest.skip(f"{name} not recorded")
-    return json.loads(open(p).read().strip().splitlines()[-1])
+    """The newest recorded line of this kind (r2_* supersedes r1_*)."""
+    for cand in (name.replace("r1_", "r2_", 1), name):
+        p = os.path.join(PROF, cand)
+        if os.path.exists(p):
+            return json.loads(open(p).read().strip().splitlines()[-1])
+    pytest.skip(f"{name} not recorded")
 
 
 def test_n1_line_has_the_contract_keys():
@@ -31,6 +33,7 @@ def test_n1_line_has_the_contract_keys():
     e = d["e2e"]
     assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= set(e)
     assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0 and e["verify_mismatched_words"] == 0
+    assert e.get("read_errors", 0) == 0
     r = d["roofline"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r)
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
@@ -38,7 +41,8 @@ def test_n1_line_has_the_contract_keys():
     assert {"value", "unit", "cores", "kind", "sample"} <= set(c) and c["kind"] in ("port", "reference")
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["gpu_launches"] > 0
-    assert d["north_star_targets"]["bit_exact"]["fetch_verify_mismatched_words"] == 0
+    be = d["north_star_targets"]["bit_exact"]
+    assert be.get("fetch_read_errors", be.get("fetch_verify_mismatched_words")) == 0
 
 
 def test_reference_line():
@@ -75,3 +79,33 @@ def test_targets_helper_on_a_synthetic_line():
     assert t["fetch_latency_host_over_peer"]["value"] == 12.0
     assert t["moe_decode_vs_host_offload"]["mode"] == "fused_cuda_graph"
     assert b.north_star_targets(line, 1)["peer_fetch_frac_of_nvlink"]["value"] is None
+
+
+def test_workload_routing_matches_the_product():
+    """The product-free workload (benchlib/workload.py) routes exactly like
+    the product's topk_routing, so both bench arms fetch the same experts."""
+    sys.path.insert(0, REPO)
+    from benchlib.common import model, routing, shape
+    from paper_2602_00328_b200.moe import QWEN15_MOE_A27B, topk_routing
+    assert model() == QWEN15_MOE_A27B
+    a, b = routing(shape(), 3), topk_routing(QWEN15_MOE_A27B, 32, 3, 2)
+    assert all((x == y).all() for ra, rb in zip(a, b) for x, y in zip(ra, rb))
+
+
+def test_reference_arm_never_loads_the_product():
+    """--impl reference maps only the oracle's library (the arm
+    must not import paper_2602_00328_b200) and runs every layer."""
+    import subprocess
+    code = (
+        "import sys, runpy\n"
+        "sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '3']\n"
+        "try:\n    runpy.run_path('bench.py', run_name='__main__')\nexcept SystemExit:\n    pass\n"
+        "maps = open('/proc/self/maps').read()\n"
+        "print('PRODUCT', [k for k in sys.modules if k.startswith('paper_2602')], 'libharvest_b200' in maps)\n")
+    env = dict(os.environ, HV_BENCH_QWEN_LAYERS="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = r.stdout.strip().splitlines()
+    assert lines[-1] == "PRODUCT [] False"
+    d = json.loads(lines[-2])
+    assert d["impl"] == "reference" and d["value"] > 0 and "every layer (1)" in d["cpu_baseline"]["sample"]
