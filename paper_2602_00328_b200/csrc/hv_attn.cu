@@ -74,7 +74,9 @@ __device__ __forceinline__ void block_softmax(const float (&s)[G], bool valid, f
   for (int hh = 0; hh < G; ++hh) {
     const float mn = fmaxf(m[hh], red[hh]);
     p[hh] = valid ? __expf(sc[hh] - mn) : 0.f;
-    const float corr = __expf(m[hh] - mn);      // 0 on the first block (m = -inf)
+    // 0 on the first block (m = -inf); also when every token so far is masked
+    // (mn = -inf too), where exp(-inf - -inf) would be NaN
+    const float corr = m[hh] == -INFINITY ? 0.f : __expf(m[hh] - mn);
     m[hh] = mn;
     l[hh] *= corr;
 #pragma unroll
@@ -255,7 +257,9 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_split_ring(
   }
   __syncthreads();
 
-  const int b0 = seq_start[b], nblk = seq_start[b + 1] - b0, ntok = seq_tokens[b];
+  // blocks past the sequence's token count hold nothing to attend: not read
+  const int b0 = seq_start[b], ntok = seq_tokens[b];
+  const int nblk = min(seq_start[b + 1] - b0, (ntok + kBlockTok - 1) / kBlockTok);
   const int per = (nblk + splits - 1) / splits;
   const int lo = split * per, hi = min(nblk, lo + per);
   // this warp's blocks: lo + warp, lo + warp + 4, ...
@@ -355,7 +359,9 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_mma(
       }
     }
   }
-  const int b0 = seq_start[b], nblk = seq_start[b + 1] - b0, ntok = seq_tokens[b];
+  // blocks past the sequence's token count hold nothing to attend: not read
+  const int b0 = seq_start[b], ntok = seq_tokens[b];
+  const int nblk = min(seq_start[b + 1] - b0, (ntok + kBlockTok - 1) / kBlockTok);
   const int per = (nblk + splits - 1) / splits;
   const int lo = split * per, hi = min(nblk, lo + per);
   const int mine = lo + warp < hi ? (hi - (lo + warp) + kAttnWarps - 1) / kAttnWarps : 0;
@@ -414,7 +420,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_mma(
     float bs = (p[0] + p[1]) + (p[2] + p[3]);
     bs += __shfl_xor_sync(0xffffffffu, bs, 1);
     bs += __shfl_xor_sync(0xffffffffu, bs, 2);
-    const float corr = __expf(m_run - mn);     // 0 on the first block
+    const float corr = m_run == -INFINITY ? 0.f : __expf(m_run - mn);  // 0 on the first / all-masked blocks
     m_run = mn;
     l_run = l_run * corr + bs;
 #pragma unroll

@@ -260,6 +260,13 @@ class KVCacheManager:
                     self.reload([tail.block_id])
                 take = min(tokens, self.m.block_tokens - tail.entries)
                 tail.entries += take
+                if tail.host_slot is not None:
+                    # the host copy predates these entries: drop it, so the
+                    # next evict writes a fresh one instead of serving a stale
+                    # page after a fallback.  Reads of the slot
+                    # already enqueued precede any later write on the stream.
+                    self.host_free.append(tail.host_slot)
+                    tail.host_slot = None
                 tail.last_access = now
                 tokens -= take
                 touched.append(tail.block_id)
@@ -368,43 +375,57 @@ class KVCacheManager:
         slab = None
         chunk = max(1, int(self.launch_chunk_blocks))
         launched = 0
-        for b in victims:
-            sbase = cache0 + b.slot * page
-            # fast path: the open slab still has room (else _peer_slot harvests)
-            if slab is not None and self._writable(slab):
-                slab_i, slot = cur, slab.free.pop()
-                placed = True
-            else:
-                placed = self._peer_slot(b.durability)
+        err = None
+        try:
+            for b in victims:
+                sbase = cache0 + b.slot * page
+                # fast path: the open slab still has room (else _peer_slot harvests)
+                if slab is not None and self._writable(slab):
+                    slab_i, slot = cur, slab.free.pop()
+                    placed = True
+                else:
+                    placed = self._peer_slot(b.durability)
+                    if placed is not None:
+                        cur, slot = placed
+                        slab_i, slab = cur, self.slabs[cur]
                 if placed is not None:
-                    cur, slot = placed
-                    slab_i, slab = cur, self.slabs[cur]
-            if placed is not None:
-                src_b.append(sbase), src_s.append(local_stride)
-                dst_b.append(slab.va + slot * page), dst_s.append(slab_stride)
-                handles.add(slab.handle)
-                if b.durability is BACKED and b.host_slot is None:
-                    b.host_slot = self._take_host_slot()
+                    new_host = None
+                    if b.durability is BACKED and b.host_slot is None:
+                        try:
+                            new_host = self._take_host_slot()
+                        except TierExhausted:
+                            slab.free.append(slot)   # this victim stays local: return its slab slot
+                            raise
                     src_b.append(sbase), src_s.append(local_stride)
-                    dst_b.append(host0 + b.host_slot * page), dst_s.append(host_stride)
-                self.local_free.append(b.slot)
-                b.tier, b.slab, b.slot = PEER, slab_i, slot
-                slab.blocks[slot] = b.block_id
-                to_peer.append(b.block_id)
-            else:
-                slab = None
-                if b.host_slot is None:
-                    b.host_slot = self._take_host_slot()
-                    src_b.append(sbase), src_s.append(local_stride)
-                    dst_b.append(host0 + b.host_slot * page), dst_s.append(host_stride)
-                self.local_free.append(b.slot)
-                b.tier, b.slot = HOST, b.host_slot
-                to_host.append(b.block_id)
-            moves.append((b.block_id, "LocalHBM", "PeerHBM" if placed is not None else "HostDRAM"))
-            if len(src_b) - launched >= chunk:  # pipelined as in reload()
-                self._launch_blocks(src_b[launched:], src_s[launched:], dst_b[launched:], dst_s[launched:],
-                                    handles)
-                launched, handles = len(src_b), set()
+                    dst_b.append(slab.va + slot * page), dst_s.append(slab_stride)
+                    handles.add(slab.handle)
+                    if new_host is not None:
+                        b.host_slot = new_host
+                        src_b.append(sbase), src_s.append(local_stride)
+                        dst_b.append(host0 + b.host_slot * page), dst_s.append(host_stride)
+                    self.local_free.append(b.slot)
+                    b.tier, b.slab, b.slot = PEER, slab_i, slot
+                    slab.blocks[slot] = b.block_id
+                    to_peer.append(b.block_id)
+                else:
+                    slab = None
+                    if b.host_slot is None:
+                        b.host_slot = self._take_host_slot()   # raises before this victim changes
+                        src_b.append(sbase), src_s.append(local_stride)
+                        dst_b.append(host0 + b.host_slot * page), dst_s.append(host_stride)
+                    self.local_free.append(b.slot)
+                    b.tier, b.slot = HOST, b.host_slot
+                    to_host.append(b.block_id)
+                moves.append((b.block_id, "LocalHBM", "PeerHBM" if placed is not None else "HostDRAM"))
+                if len(src_b) - launched >= chunk:  # pipelined as in reload()
+                    self._launch_blocks(src_b[launched:], src_s[launched:], dst_b[launched:], dst_s[launched:],
+                                        handles)
+                    launched, handles = len(src_b), set()
+        except TierExhausted as e:
+            # the victims moved so far keep their new tiers: their copies are
+            # launched and drained below before the error propagates, so no
+            # table entry ever points at a page that was not written
+            err = e
         self.stats["evict_peer"] += len(to_peer)
         self.stats["evict_host"] += len(to_host)
         # one log record per destination tier and call (block ids in order)
@@ -418,6 +439,8 @@ class KVCacheManager:
             # freed local slots are reusable only after the copies drained them
             self.sys.engine.synchronize()
             self.sys.loop.poll()
+        if err is not None:
+            raise err
         return moves
 
     def _take_host_slot(self) -> int:

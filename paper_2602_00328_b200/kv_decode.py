@@ -237,10 +237,13 @@ class KVAttentionDecoder:
             out = self._graph_out
         else:
             out = self._run()
+        # the KV manager's later writes (evict / reload K1 on the fetch stream)
+        # must follow this step's reads of the pages -- in place (fused) the
+        # attention reads local, host and peer pages on the compute stream
+        fin = torch.cuda.Event()
+        fin.record(torch.cuda.current_stream(self.dev))
+        self.fetch.wait_event(fin)
         if batch is not None:               # the drain completes when the step's reads have
-            fin = torch.cuda.Event()
-            fin.record(torch.cuda.current_stream(self.dev))
-            self.fetch.wait_event(fin)
             self.kv.sys.engine.track([lambda _x, bt=batch: rt.end_reads(bt)])
         return out
 

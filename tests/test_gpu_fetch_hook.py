@@ -93,8 +93,13 @@ def test_issue_fetches_mixed_tiers_match_oracle(qwen_system):
     assert list(batch.experts) == [e for e, _ in plan]          # LOCAL skipped, order kept
     assert fetcher.reads - reads0 == len(plan)
     assert fetcher.read_errors() == err0 == 0
-    # fetched objects land in the first len(plan) slots of dst (keep-mask order)
-    assert _staged_bytes_ok(m, 0, batch.experts, staging, S)
+    # each fetched expert lands in the dst slot of its position in `active`
+    got = staging.cpu().numpy()
+    for i, e in enumerate(active):
+        if fetcher.tier[0, e] == 0:
+            continue
+        want = O.content(O.expert_seed(m.name, 0, int(e)), S)
+        assert np.array_equal(got[i * S:(i + 1) * S], want), e
 
 
 def test_issue_fetches_counts_read_errors(qwen_system):
@@ -222,7 +227,7 @@ def test_k1_config1_full_shape(tier):
     F.kv_gather_table(F.ptrs_tensor([base], "cuda"), F.ptrs_tensor([int(s) for s in flat], "cuda"), page,
                       dst=dst2.view(torch.uint8))
     torch.cuda.synchronize()
-    assert torch.equal(dst2, dst)
+    assert torch.equal(dst2.view(torch.uint8), dst.view(torch.uint8))    # bytes (fp16 NaN != NaN)
     if tier == "pool":
         src_mem.decommit(0, slots * page)
     src_mem.close()

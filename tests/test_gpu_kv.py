@@ -227,3 +227,55 @@ def test_slab_emptied_while_revoking_is_left_to_the_revocation():
     assert refcheck.verify_release_ordering(sysm.loop.log) == []
     kv.close()
     sysm.close()
+
+
+def test_evict_running_out_of_host_slots_leaves_a_consistent_table():
+    """TierExhausted partway through evict() must not leave table
+    entries pointing at pages that were never written, nor leak the slab slot
+    taken for the failing victim.  Here Backed blocks go to a peer slab and
+    need a host copy each; the host tier holds only 3, so the 4th victim
+    fails.  The first 3 are complete (bytes equal the oracle's), the failing
+    one is still local, and no slot is double-booked."""
+    from paper_2602_00328_b200.kv import KVTier, TierExhausted
+    sysm, kv, m = _mk(local_blocks=8, host_blocks=3, slab_blocks=8, donor_slabs=1, durability="BACKED")
+    kv.append_kv(0, 16 * 8)                        # fills local HBM, no eviction yet
+    free_before = sum(len(s.free) for s in kv.slabs)
+    with pytest.raises(TierExhausted):
+        kv.evict(6 * m.block_bytes)
+    peer = [b for b in kv.table.values() if b.tier == KVTier.PEER_HBM]
+    local = [b for b in kv.table.values() if b.tier == KVTier.LOCAL_HBM]
+    assert len(peer) == 3 and len(local) == 5
+    assert all(b.host_slot is not None for b in peer)
+    assert all(b.host_slot is None for b in local)
+    # slab slots: exactly the 3 moved blocks are booked
+    booked = sum(len(s.blocks) for s in kv.slabs)
+    assert booked == 3 and sum(len(s.free) for s in kv.slabs) + booked == len(kv.slabs) * 8
+    assert free_before == 0 or free_before - 3 == sum(len(s.free) for s in kv.slabs)
+    # local slots: the local blocks' slots are not on the free list
+    assert not ({b.slot for b in local} & set(kv.local_free))
+    _check_all(kv, m)
+    kv.close()
+    sysm.close()
+
+
+def test_host_copy_dropped_when_a_reloaded_block_grows():
+    """after reload, append_kv adds entries to the tail block; its
+    old host copy no longer matches and must not be served later.  The copy
+    is dropped and the next evict writes a fresh one."""
+    from paper_2602_00328_b200.kv import KVTier
+    sysm, kv, m = _mk(local_blocks=8, host_blocks=16, slab_blocks=4, donor_slabs=0, durability="BACKED")
+    kv.append_kv(0, 20)                            # blocks 0 (16) and 1 (4 entries, the open tail)
+    kv.evict(8 * m.block_bytes)                    # both to host (no donors)
+    tail = kv.table[1]
+    assert tail.tier == KVTier.HOST_DRAM and tail.host_slot is not None
+    old_slot = tail.host_slot
+    kv.append_kv(0, 3)                             # reloads the tail, then grows it
+    assert tail.tier == KVTier.LOCAL_HBM and tail.entries == 7
+    assert tail.host_slot is None and old_slot in kv.host_free
+    writes0 = kv.stats["evict_host"]
+    kv.evict(8 * m.block_bytes)
+    assert tail.tier == KVTier.HOST_DRAM and tail.host_slot is not None
+    assert kv.stats["evict_host"] > writes0
+    _check_all(kv, m)
+    kv.close()
+    sysm.close()

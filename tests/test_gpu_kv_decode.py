@@ -216,3 +216,62 @@ def test_kv_revocation_completes_while_steps_stream(durability):
     torch.cuda.synchronize()
     assert torch.equal(out, first)
     kv.close(); sysm.close()
+
+
+@pytest.mark.parametrize("splits", [1, 3, 64])
+def test_trailing_blocks_past_token_count(splits):
+    """a page table may list more blocks than a sequence's token
+    count covers (KVAttentionDecoder(tokens=...) keeps every block).  Blocks
+    past the tokens are neither read nor allowed to poison the softmax: with
+    several splits a warp's first block can be fully masked, which used to
+    give exp(-inf - -inf) = NaN.  A zero-token sequence yields zeros."""
+    from paper_2602_00328_b200 import _native as N
+    torch.manual_seed(11)
+    D, kvh, g = 128, 2, 4
+    tokens = [37, 5, 100, 0]
+    nblk = [8, 6, 10, 3]                       # far more blocks than the tokens need
+    n = sum(nblk)
+    pool = (torch.randn(n, 2 * 16 * kvh * D, device="cuda") * 0.5).to(torch.float16)
+    pool[torch.isnan(pool)] = 0
+    ptrs = torch.tensor([pool[i].data_ptr() for i in range(n)], dtype=torch.int64, device="cuda")
+    start = torch.tensor([0] + list(np.cumsum(nblk)), dtype=torch.int32, device="cuda")
+    tok = torch.tensor(tokens, dtype=torch.int32, device="cuda")
+    B, Hq = len(tokens), kvh * g
+    q = torch.randn(B, Hq, D, device="cuda").to(torch.float16)
+    out = torch.full((B, Hq, D), float("nan"), device="cuda")
+    part = torch.empty(B * kvh * splits * g * (D + 2), device="cuda")
+    scale = 1.0 / D ** 0.5
+    N.call("hv_paged_decode_attention", ptrs.data_ptr(), start.data_ptr(), tok.data_ptr(), q.data_ptr(),
+           out.data_ptr(), part.data_ptr(), B, Hq, kvh, D, 16, splits, scale, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
+    for b in range(B):
+        if tokens[b] == 0:
+            assert (out[b] == 0).all()
+            continue
+        pages = pool[int(start[b]):int(start[b + 1])].float().view(-1, 2, 16, kvh, D)
+        k = pages[:, 0].reshape(-1, kvh, D)[:tokens[b]].transpose(0, 1).repeat_interleave(g, dim=0)
+        v = pages[:, 1].reshape(-1, kvh, D)[:tokens[b]].transpose(0, 1).repeat_interleave(g, dim=0)
+        w = torch.softmax((k @ q[b].float().unsqueeze(-1)).squeeze(-1) * scale, dim=-1)
+        ref = (w.unsqueeze(-1) * v).sum(1)
+        assert (out[b] - ref).abs().max().item() <= 2e-3
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_decoder_with_tokens_shorter_than_sequences(fused):
+    """KVAttentionDecoder(tokens=20) over 96-token sequences: finite, equal
+    to the fp32 reference over the first 20 tokens, at several splits."""
+    from paper_2602_00328_b200.kv_decode import KVAttentionDecoder
+    sysm, kv, m = _cache(local_blocks=4, donor_slabs=1, seqs=2, tokens=96)
+    outs = []
+    for splits in (None, 4):
+        dec = KVAttentionDecoder(kv, [0, 1], q_heads=4, tokens=20, seed=5, fused=fused, splits=splits)
+        assert dec.tokens == [20, 20]
+        out = dec.step()
+        torch.cuda.synchronize()
+        assert torch.isfinite(out.float()).all()
+        ref = _reference(kv, m, dec)
+        assert (out.float().cpu() - ref).abs().max().item() <= 2e-2
+        outs.append(out)
+    sysm.loop.run()
+    kv.close(); sysm.close()

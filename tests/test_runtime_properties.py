@@ -76,3 +76,33 @@ def test_random_schedules_keep_invariants(ops, kind):
             raise AssertionError("stale handle accepted")
         except R.StaleHandleError:
             pass
+
+
+def test_fairness_tokens_not_spent_when_donor_commit_fails():
+    """a donor HBM shortfall (pool.commit fails after the
+    best-fit decision) returns None like NoCapacity and must not drain the
+    client's fairness budget; the next allocation still fits the burst."""
+    from paper_2602_00328_b200 import _native as N
+    GiB = 1 << 30
+
+    class FlakyPool:
+        def __init__(self):
+            self.fail = True
+
+        def commit(self, base, size):
+            if self.fail:
+                raise N.HarvestNativeError(-1000 - 2, "hv_pool_commit")
+
+        def decommit(self, base, size):
+            pass
+
+    loop = VirtualLoop()
+    pool = FlakyPool()
+    pol = R.Policy(R.PolicyKind.FAIRNESS, fairness_budget_bytes_per_s=0.0, fairness_burst_bytes=float(GiB))
+    rt = R.HarvestRuntime(loop, topo([(4 * GiB, 0, 0)]), pol, pools={1: pool})
+    hints = R.AllocationHints(client_id="c")
+    assert rt.harvest_alloc(GiB, hints) is None          # commit failed
+    pool.fail = False
+    h = rt.harvest_alloc(GiB, hints)                      # the whole burst is still there
+    assert h is not None
+    assert rt.harvest_alloc(1, hints) is None             # and now it is spent
