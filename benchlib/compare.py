@@ -216,6 +216,10 @@ def same_run_comparisons(dev, m, a, source, fetcher=None, n=53):
         kv["peer_vs_host_speedup"] = dt_h / dt_p
     out["kv_config1_layer_gather"] = kv
     out.update(latency_curves(dev, a, s, t, h, fetcher if source == "peer" else None))
+    try:
+        out["kv_fallback_measured"] = kv_fallback_measured(dev, h)
+    except Exception as e:   # reported, never fatal
+        out["kv_fallback_measured"] = {"error": repr(e)[:300]}
     hp.close()
     h.close()
     return out
@@ -267,3 +271,25 @@ def latency_curves(dev, a, s, t, host, fetcher):
                                                "paper_h100": "kimi-k2 5.42x@100 -> 5.68x@8000 (PAPER.md:319)"}
     del one
     return out
+
+
+def kv_fallback_measured(dev, host):
+    """§8(f)4: resolve_fallback on B200-measured costs --
+    the host link refit with calibrate() from real fetch latencies, and the
+    Llama-3-8B recompute cost (chunked prefill through all 32 layers) -- with
+    the decision boundary solved for both the SPEC's linear rate and the
+    measured curve."""
+    from paper_2602_00328_b200.costs import LLAMA3_8B_DENSE, fallback_crossover, measure_host_link, measure_recompute
+    from paper_2602_00328_b200.kv import LLAMA3_8B
+    link, fit = measure_host_link(host, dev)
+    curve = measure_recompute(LLAMA3_8B_DENSE, chunks=(16, 64, 256, 1024, 4096), device=dev)
+    bpe = LLAMA3_8B.bytes_per_entry
+    rate = curve.per_entry_rate
+    return {"model": LLAMA3_8B.name, "bytes_per_entry": bpe, "host_link": fit,
+            "recompute_prefill_us": [[e, t * 1e6] for e, t in curve.points],
+            "recompute_us_per_entry_large_chunk": rate * 1e6,
+            "host_fetch_us_per_entry": bpe / link.bandwidth * 1e6,
+            "crossover_linear_rate": fallback_crossover(link, bpe, rate),
+            "crossover_measured_curve": fallback_crossover(link, bpe, curve),
+            "note": "recompute = prefill of the block's tokens through every layer (attention over the chunk "
+                    "only: a lower bound); FetchFromHost iff host transfer_time <= recompute time"}

@@ -469,9 +469,23 @@ class KVCacheManager:
         entries * recompute_time_per_entry, else Recompute; no host copy -> Recompute."""
         if block.host_slot is None:
             return "Recompute"
-        link = host_link or self.sys.topology.link_between(0, self.sys.host_id)
+        link = host_link or getattr(self, "host_link", None) or self.sys.topology.link_between(0, self.sys.host_id)
+        rec = getattr(self, "recompute", None)
+        if rec is None:
+            rec = self.m.recompute_time_per_entry
         t_host = transfer_time(link, block.entries * self.m.bytes_per_entry)
-        return "FetchFromHost" if t_host <= block.entries * self.m.recompute_time_per_entry else "Recompute"
+        t_rec = rec(block.entries) if callable(rec) else block.entries * rec
+        return "FetchFromHost" if t_host <= t_rec else "Recompute"
+
+    def set_costs(self, host_link: LinkSpec | None = None, recompute=None) -> None:
+        """Base resolve_fallback on measured costs (costs.measure_host_link /
+        costs.measure_recompute): ``host_link`` replaces the topology's
+        constant host link, ``recompute`` the model's recompute_time_per_entry
+        (seconds per entry, or a callable entries -> seconds)."""
+        if host_link is not None:
+            self.host_link = host_link
+        if recompute is not None:
+            self.recompute = recompute
 
     @annotate("harvest.kv_reload")
     def reload(self, block_ids) -> dict:

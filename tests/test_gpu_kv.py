@@ -279,3 +279,35 @@ def test_host_copy_dropped_when_a_reloaded_block_grows():
     _check_all(kv, m)
     kv.close()
     sysm.close()
+
+
+def test_fallback_on_measured_costs():
+    """§8(f)4: measure the host link (calibrate() refit of real fetch
+    latencies) and a recompute curve (chunked prefill of a small dense
+    shape) on this GPU, hand them to the KV manager, and check its decision
+    equals the SPEC rule evaluated on the same measured numbers on both sides
+    of the solved crossover."""
+    from paper_2602_00328_b200.costs import DenseShape, fallback_crossover, fetch_wins, measure_host_link, \
+        measure_recompute
+    from paper_2602_00328_b200.kv import KVBlock, KVTier
+    from paper_2602_00328_b200.runtime import Durability
+    sysm, kv, m = _mk(durability="BACKED")
+    from paper_2602_00328_b200.pool import HostTier
+    ht = HostTier(16 << 20)
+    link, fit = measure_host_link(ht, 0)
+    assert 1e-6 < link.fixed_cost < 1e-3 and 10e9 < link.bandwidth < 80e9, fit
+    shape = DenseShape("tiny", num_layers=2, hidden=512, q_heads=8, kv_heads=2, head_dim=64, intermediate=1024)
+    curve = measure_recompute(shape, chunks=(16, 64, 256), iters=2)
+    assert all(t > 0 for _, t in curve.points)
+    kv.set_costs(host_link=link, recompute=curve)
+    out = fallback_crossover(link, m.bytes_per_entry, curve, max_entries=4096)
+    probe = [1, 16, 64, 256, 4096]
+    for f in out["flips"]:
+        probe += list(f.values())
+    for e in probe:
+        b = KVBlock(0, 0, 0, e, Durability.BACKED, KVTier.NOT_MATERIALIZED, host_slot=0)
+        want = "FetchFromHost" if fetch_wins(link, e, m.bytes_per_entry, curve) else "Recompute"
+        assert kv.resolve_fallback(b) == want
+    ht.close()
+    kv.close()
+    sysm.close()
