@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--out", default=None)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--pool-mode", default="remote", choices=["remote", "ipc"],
+                    help="N>1 donor pools: VMM chunks donated over Unix sockets, or cudaIpc slabs")
     ap.add_argument("--no-kv", action="store_true", help="skip the config-4 long-context KV measurement")
     ap.add_argument("--no-phi", action="store_true", help="N>1: skip the config-3 Phi-3.5-MoE decode phase")
     ap.add_argument("--no-churn", action="store_true", help="skip the config-5 churn phase")
@@ -80,7 +82,7 @@ def run_b200(a):
     from paper_2602_00328_b200 import fetch as F
     from paper_2602_00328_b200.cluster import DonorLayout, RankGroup, per_reader_bytes, place_experts
     from paper_2602_00328_b200.moe import ExpertFetcher, ExpertResidency, ExpertStore, expert_content
-    from paper_2602_00328_b200.pool import HostTier, PeerPool
+    from paper_2602_00328_b200.pool import HostTier, NodePools
     from paper_2602_00328_b200.system import HarvestSystem
     from tools.clocks import ClockSampler
     from tools.nvlink_counters import NvlinkCounters
@@ -93,6 +95,9 @@ def run_b200(a):
     # multi-process IPC path on a single-GPU box; use --dist-backend gloo)
     dmap = os.environ.get("HV_DEVICE_MAP")
     dev = int(dmap.split(",")[local]) if dmap else local
+
+    def device_of(r):   # the CUDA device of rank r (one node: local rank = rank)
+        return int(dmap.split(",")[r]) if dmap else r
     torch.cuda.set_device(dev)
     backend = a.dist_backend
     if world > 1:
@@ -101,10 +106,11 @@ def run_b200(a):
         else:
             dist.init_process_group(backend)
     group = RankGroup(world, rank, device=f"cuda:{dev}" if backend == "nccl" else None)
+    a.group, a.device_of = group, device_of     # for the multi-rank phases
     m = model()
     L, E, S = m.num_layers, m.num_experts, m.expert_size
     routes = routing(m, a.warmup + a.steps, seed=SEED + 1000 * rank)
-    imported, host_tier = [], None
+    host_tier, node = None, None
 
     if world == 1:
         source = "host"
@@ -121,13 +127,10 @@ def run_b200(a):
             per_reader += math.ceil((KV_TOKENS // 16) / KV_SLAB_BLOCKS / (world - 1)) * kv_slab_bytes()
         layout = DonorLayout.symmetric(world, per_reader)
         others = layout.donors_of(rank)
-        my_pool = PeerPool(dev, layout.slab_bytes(rank), readers=[dev], mode="ipc")
-        handles = group.all_gather(my_pool.export_ipc())
-        views = {}
-        for d in others:
-            p = PeerPool.import_ipc(handles[d], d, layout.slab_bytes(d), dev)
-            imported.append(p)
-            views[layout.peer_index(rank, d)] = p.view(*layout.section(d, rank))
+        # donor pools: VMM chunks donated per reader over Unix sockets (HBM
+        # goes back to the donor on free / revoke), or cudaIpc slabs
+        node = NodePools(group, layout, rank, device_of, mode=a.pool_mode, tag="main")
+        views = node.views
         sysm = HarvestSystem(dev, pools=views, local_bytes=1, engine=a.engine, max_ctas=a.max_ctas,
                              log_transfers=False)
         store = ExpertStore(m, sysm.host_id, None)
@@ -191,7 +194,7 @@ def run_b200(a):
         if world > 1:  # engines other than LDG are proven on a peer pointer first, out of process
             if rank == 0:
                 d = others[0]
-                safe = probe_engines_on_peer(handles[d], d, layout.slab_bytes(d), dev)
+                safe = probe_engines_on_peer(node, d, device_of(d), dev)
             safe = group.decide(safe)
             engines = tuple(e for e in engines if safe.get(e))
             # N-1 donors: also the interleaved chunk order (HV_ENGINE_FLAG_INTERLEAVE),
@@ -451,11 +454,13 @@ def run_b200(a):
                 **extra}
     barrier()
     sysm.close()
-    for p in imported:
-        p.close()
+    if node is not None:
+        pool_info = {"mode": node.mode, "setup_error": node.error}
+        node.close()
+        if rank == 0:
+            line["config"]["donor_pools"] = pool_info
     barrier()
     if world > 1:
-        del my_pool  # every reader closed its import above
         import gc
         gc.collect()
         torch.cuda.synchronize()

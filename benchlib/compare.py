@@ -37,13 +37,21 @@ import json, sys
 sys.path.insert(0, {repo!r})
 import torch
 from paper_2602_00328_b200 import fetch as F
-from paper_2602_00328_b200.pool import PeerPool
-p = PeerPool.import_ipc(bytes.fromhex({handle!r}), {donor}, {nbytes}, {dev})
-n = 4 << 20
+from paper_2602_00328_b200.pool import PeerPool, RemotePool
+if {mode!r} == "remote":
+    p = RemotePool({path!r}, {donor}, {chunk}, {chunk}, {dev})
+    p.commit(0, {chunk})
+    va = p.va
+else:
+    p = PeerPool.import_ipc(bytes.fromhex({handle!r}), {donor}, {nbytes}, {dev})
+    va = p.va
+n = min(4 << 20, {chunk})
 a = torch.empty(n, dtype=torch.uint8, device="cuda:{dev}")
 b = torch.empty(n, dtype=torch.uint8, device="cuda:{dev}")
-src = F.ptrs_tensor([p.va], "cuda:{dev}")
+src = F.ptrs_tensor([va], "cuda:{dev}")
 sz = F.ptrs_tensor([n], "cuda:{dev}")
+if {mode!r} == "remote":   # a fresh chunk of its own: give it content (the IPC slab is only read)
+    F.fill_content(src, sz, [7])
 F.batch_copy(src, F.ptrs_tensor([a.data_ptr()], "cuda:{dev}"), sz, engine="ldg")
 F.batch_copy(src, F.ptrs_tensor([b.data_ptr()], "cuda:{dev}"), sz, engine={engine!r})
 torch.cuda.synchronize()
@@ -51,16 +59,24 @@ print(json.dumps({{"ok": bool(torch.equal(a, b))}}))
 p.close()
 """
 
-def probe_engines_on_peer(handle: bytes, donor: int, nbytes: int, dev: int) -> dict:
+def probe_engines_on_peer(node, donor_rank: int, donor_dev: int, dev: int) -> dict:
     """Run each non-LDG engine on a real peer pointer in a throw-away child
-    process: a fault there cannot poison this process's CUDA context."""
+    process: a fault there cannot poison this process's CUDA context.  The
+    child maps one chunk of the donor through the node's pool mechanism
+    (a RemotePool connection to the donor's server, or the IPC slab)."""
     import subprocess
+    from paper_2602_00328_b200.pool import _socket_path
     # the LDG family issues the same LDG.E.128 loads (hint / unroll differ):
     # only the bulk-copy (TMA) engine is proven out of process
     ok = {"ldg": True, "ldg256": True, "ldg16": True}
+    remote = node.mode == "remote"
+    own = node._readers[node.layout.donors_of(node.rank).index(donor_rank)]
     for engine in ("tma",):
-        code = PROBE_CHILD.format(repo=REPO, handle=handle.hex(), donor=donor, nbytes=nbytes, dev=dev,
-                                  engine=engine)
+        code = PROBE_CHILD.format(repo=REPO, mode=node.mode, path=_socket_path("main", donor_rank),
+                                  handle="" if remote else node.ipc_handles[donor_rank].hex(),
+                                  donor=donor_dev, nbytes=node.layout.slab_bytes(donor_rank),
+                                  chunk=getattr(own, "chunk_bytes", 32 << 20) if remote else 4 << 20,
+                                  dev=dev, engine=engine)
         try:
             r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=180)
             ok[engine] = r.returncode == 0 and '"ok": true' in r.stdout

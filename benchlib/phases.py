@@ -256,7 +256,7 @@ def churn_phase(world, rank, dev, a, dist, barrier, layers=8, seconds=2.0):
     returns.  Decode outputs are compared bit-for-bit with an all-local run.
     N=1: the compute GPU donates to itself through a VMM pool."""
     from paper_2602_00328_b200.moe import QWEN15_MOE_A27B, MoEProfile
-    from paper_2602_00328_b200.pool import PeerPool
+    from paper_2602_00328_b200.pool import NodePools
     q = QWEN15_MOE_A27B
     m = MoEProfile(q.name, layers, q.num_experts, q.top_k, q.expert_size, hidden=q.hidden,
                    intermediate=q.intermediate)
@@ -269,17 +269,7 @@ def churn_phase(world, rank, dev, a, dist, barrier, layers=8, seconds=2.0):
     else:
         layout = DonorLayout.split_roles(world, per_reader_bytes(L * E, S, world - world // 2))
         C, D, per_reader = list(layout.compute), list(layout.donors), layout.per_reader
-    pool, imported, out = None, [], None
-    handles = [None] * world
-    if world > 1:
-        mine = None
-        if rank in D:
-            try:
-                pool = PeerPool(dev, layout.slab_bytes(rank), readers=[dev], mode="ipc")
-                mine = pool.export_ipc()
-            except Exception as e:
-                out = {"rank": rank, "error": repr(e)[:200]}
-        dist.all_gather_object(handles, mine)
+    out = None
     from paper_2602_00328_b200.runtime import Policy, PolicyKind
     # the reference's placement policies under the same churn (runtime.py:169-196):
     # BestFit is the headline; Stability skips donors with many recent
@@ -293,23 +283,29 @@ def churn_phase(world, rank, dev, a, dist, barrier, layers=8, seconds=2.0):
     # place: peer experts over the link, revoked ones from the host copy)
     runs = ([(name, pol, False) for name, pol in policies.items()] + [("BestFit_fused", Policy(), True)]
             + [("BestFit_fused_graph", Policy(), "graph")])
-    outs = {}
-    for name, pol, fused in runs:
+    outs, lending = {}, {}
+    for i, (name, pol, fused) in enumerate(runs):
+        node = None
+        if world > 1:   # fresh donor pools per run: every run starts from empty donors
+            node = NodePools(a.group, layout, rank, a.device_of, mode=a.pool_mode, tag=f"churn{i}")
         try:
             if rank in C:
-                outs[name] = _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported,
-                                            seconds, policy=pol, fused=fused)
+                if node is not None and node.error:
+                    raise RuntimeError(node.error)
+                outs[name] = _churn_compute(world, rank, dev, a, m, layout, per_reader, node, seconds,
+                                            policy=pol, fused=fused)
         except Exception as e:  # every rank still reaches the collectives below
             outs[name] = {"rank": rank, "error": repr(e)[:300]}
-        imported.clear()
-    if out is not None:  # donor-side setup failure
-        outs = {name: out for name, _p, _f in runs}
+        if node is not None:
+            node.close()          # readers close, barrier, then the donors' servers stop
+            if rank in D:
+                lending[name] = {"mode": node.mode, **node.donor_stats()}
+    if lending:
+        outs["_donor_lending"] = lending
     results = [None] * world
     if world > 1:
         barrier()
         dist.all_gather_object(results, outs)
-        if pool is not None:
-            pool.close()
     else:
         results = [outs]
 
@@ -330,6 +326,8 @@ def churn_phase(world, rank, dev, a, dist, barrier, layers=8, seconds=2.0):
            "timeline": "markov_availability levels 0/25/50/100% of the donated bytes, 50 ms mean sojourn, "
                        f"seed 5+donor, {seconds} s",
            "policy": "BestFit", **head, "per_rank": comp,
+           "donor_lending": {str(r): x["_donor_lending"] for r, x in enumerate(results)
+                             if x and "_donor_lending" in x},
            "policy_comparison": {}}
     if errs:
         res["errors"] = errs
@@ -349,7 +347,7 @@ def churn_phase(world, rank, dev, a, dist, barrier, layers=8, seconds=2.0):
             res[key]["errors"] = ef
     return res
 
-def _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported, seconds, policy=None,
+def _churn_compute(world, rank, dev, a, m, layout, per_reader, node, seconds, policy=None,
                    fused=False):
     """Compute-rank side of churn_phase (no collectives inside)."""
     import torch
@@ -366,12 +364,7 @@ def _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported
         sysm = HarvestSystem(dev, donors=[dev], donor_bytes=per_reader, host_tier=host, local_bytes=1,
                              engine=a.engine, max_ctas=a.max_ctas, policy=policy)
     else:
-        views = {}
-        for d in layout.donors_of(rank):
-            p = PeerPool.import_ipc(handles[d], d, layout.slab_bytes(d), dev)
-            imported.append(p)
-            views[layout.peer_index(rank, d)] = p.view(*layout.section(d, rank))
-        sysm = HarvestSystem(dev, pools=views, host_tier=host, local_bytes=1, engine=a.engine,
+        sysm = HarvestSystem(dev, pools=dict(node.views), host_tier=host, local_bytes=1, engine=a.engine,
                              max_ctas=a.max_ctas, policy=policy)
     rt = sysm.runtime
     store = ExpertStore(m, sysm.host_id, host)
@@ -442,8 +435,6 @@ def _churn_compute(world, rank, dev, a, m, layout, per_reader, handles, imported
     del dec, ldec, resident
     lsys.close()
     sysm.close()
-    for p in imported:
-        p.close()
     return out
 
 def phi_phase(world, rank, dev, a, dist, barrier, max_over_ranks, batches=(1, 16, 64)):
@@ -457,7 +448,7 @@ def phi_phase(world, rank, dev, a, dist, barrier, max_over_ranks, batches=(1, 16
     from paper_2602_00328_b200.cluster import DonorLayout, per_reader_bytes, place_experts
     from paper_2602_00328_b200.decode import MoEDecoder
     from paper_2602_00328_b200.moe import PHI35_MOE, ExpertFetcher, ExpertResidency, ExpertStore, MoEProfile
-    from paper_2602_00328_b200.pool import HostTier, PeerPool
+    from paper_2602_00328_b200.pool import HostTier, NodePools
     from paper_2602_00328_b200.system import HarvestSystem
     m = PHI35_MOE
     if a.phi_layers != m.num_layers:
@@ -467,24 +458,12 @@ def phi_phase(world, rank, dev, a, dist, barrier, max_over_ranks, batches=(1, 16
     layout = DonorLayout.symmetric(world, per_reader_bytes(L * E, S, world - 1))
     out = {"model": f"{m.name}: {L} layers x {E} experts x {S} B, top-{m.top_k}", "donors_per_rank": world - 1}
     errors = []
-    pool = sysm = fetcher = None
-    imported = []
+    node = sysm = fetcher = None
     try:
-        pool = PeerPool(dev, layout.slab_bytes(rank), readers=[dev], mode="ipc")
-        my_handle = pool.export_ipc()
-    except Exception as e:
-        errors.append(repr(e)[:200])
-        my_handle = None
-    handles = [None] * world
-    dist.all_gather_object(handles, my_handle)
-    try:
-        if any(h is None for h in handles):
-            raise RuntimeError("a donor failed to create its pool")
-        views = {}
-        for d in layout.donors_of(rank):
-            p = PeerPool.import_ipc(handles[d], d, layout.slab_bytes(d), dev)
-            imported.append(p)
-            views[layout.peer_index(rank, d)] = p.view(*layout.section(d, rank))
+        node = NodePools(a.group, layout, rank, a.device_of, mode=a.pool_mode, tag="phi")
+        if node.error:
+            errors.append(node.error)
+        views = node.views
         sysm = HarvestSystem(dev, pools=views, local_bytes=1, engine=a.engine, max_ctas=a.max_ctas,
                              log_transfers=False)
         rt = sysm.runtime
@@ -575,13 +554,14 @@ def phi_phase(world, rank, dev, a, dist, barrier, max_over_ranks, batches=(1, 16
     try:
         if sysm is not None:
             sysm.close()
-        for p in imported:
-            p.close()
     except Exception as e:
         errors.append(repr(e)[:200])
     barrier()
-    if pool is not None:
-        pool.close()
+    if node is not None:
+        out["donor_pools"] = node.mode
+        node.close()
+    else:
+        barrier()        # NodePools.close()'s barrier on the ranks that have one
     all_err = [None] * world
     dist.all_gather_object(all_err, errors)
     if any(all_err):

@@ -15,7 +15,7 @@
  *     (memalloc.py:90-138), allocated_bytes (:86)     decisions, O(log n) per call)
  *   DeviceState / init_device (memalloc.py:67-79)   hv_seg_create
  *   "switches to that device context, and          hv_pool_* (per-donor VMM pool:
- *     allocates memory" (PAPER.md:184), the          cuMemCreate/cuMemMap/
+ *     allocates memory" (PAPER.md:196), the          cuMemCreate/cuMemMap/
  *     peer tier of Topology (interconnect.py:57)     cuMemSetAccess, or cudaIpc)
  *   HOST_DRAM tier (memalloc.py:14-17)              hv_host_alloc (pinned, mapped)
  *   app_transfer -> schedule_transfer ->            hv_kv_gather (K1), hv_batch_copy
@@ -101,6 +101,8 @@ typedef struct hv_pool hv_pool;
 #define HV_POOL_VMM 0u   /* cuMemAddressReserve + on-demand cuMemCreate/cuMemMap */
 #define HV_POOL_IPC 1u   /* one cudaMalloc slab, exportable with cudaIpc          */
 #define HV_POOL_EAGER 2u /* VMM: commit the whole range at creation               */
+#define HV_POOL_REMOTE 4u /* VMM VA range only: chunks come from a donor process as
+                             POSIX FDs (hv_pool_map_fd / hv_pool_unmap_chunk)       */
 /* Reserve `bytes` of donor-resident memory, readable and writable by the
  * donor and every device in reader_devs.  VMM pools commit physical chunks of
  * `chunk_bytes` (rounded to the allocation granularity) on demand. */
@@ -111,7 +113,7 @@ int hv_pool_destroy(hv_pool* p);
 int hv_pool_info(const hv_pool* p, uint64_t* va, uint64_t* bytes,
                  uint64_t* chunk_bytes, int* donor_dev);
 /* back [offset, offset+bytes) with physical donor memory (refcounted per
- * chunk); the harvest_alloc side of "allocates memory" (PAPER.md:184) */
+ * chunk); the harvest_alloc side of "allocates memory" (PAPER.md:196) */
 int hv_pool_commit(hv_pool* p, uint64_t offset, uint64_t bytes);
 /* drop the refcount; chunks reaching zero are unmapped and released back to
  * the donor.  Callers must have drained every reader first (runtime.py:396). */
@@ -121,6 +123,20 @@ int hv_pool_committed_bytes(const hv_pool* p, uint64_t* out);
 int hv_pool_export_ipc(const hv_pool* p, void* handle64);
 int hv_pool_import_ipc(const void* handle64, int donor_dev, uint64_t bytes,
                        int reader_dev, hv_pool** out);
+
+/* Cross-process VMM donation (one process per GPU).  The donor process
+ * creates a physical chunk on its GPU with a shareable POSIX-FD handle and
+ * sends the FD to a reader (pool.DonorServer, SCM_RIGHTS over a Unix
+ * socket); the reader maps it into an HV_POOL_REMOTE pool.  Revocation or
+ * free: the reader unmaps (hv_pool_unmap_chunk), the donor releases its
+ * handle (hv_chunk_release), and the HBM returns to the donor GPU -- the
+ * reference's free_segment at the end of an ordered release
+ * (runtime.py:396-411).  Granularity: hv_chunk_granularity. */
+int hv_chunk_granularity(int device, uint64_t* out);
+int hv_chunk_create_shareable(int device, uint64_t bytes, uint64_t* handle, int* fd);
+int hv_chunk_release(uint64_t handle);
+int hv_pool_map_fd(hv_pool* p, uint64_t chunk_index, int fd);
+int hv_pool_unmap_chunk(hv_pool* p, uint64_t chunk_index);
 
 /* ---- host tier: pinned, portable, mapped ------------------------------- */
 int hv_host_alloc(uint64_t bytes, void** h_ptr, uint64_t* d_alias);

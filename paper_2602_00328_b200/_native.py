@@ -33,6 +33,7 @@ ENGINES["ce"] = ENGINE_CE
 POOL_VMM = 0
 POOL_IPC = 1
 POOL_EAGER = 2
+POOL_REMOTE = 4
 
 
 class HarvestNativeError(RuntimeError):
@@ -84,6 +85,11 @@ _SIGS = {
     "hv_pool_committed_bytes": [vp, P64],
     "hv_pool_export_ipc": [vp, vp],
     "hv_pool_import_ipc": [vp, i32, u64, i32, C.POINTER(vp)],
+    "hv_chunk_granularity": [i32, P64],
+    "hv_chunk_create_shareable": [i32, u64, P64, C.POINTER(i32)],
+    "hv_chunk_release": [u64],
+    "hv_pool_map_fd": [vp, u64, i32],
+    "hv_pool_unmap_chunk": [vp, u64],
     "hv_host_alloc": [u64, C.POINTER(vp), P64],
     "hv_host_alloc_flags": [u64, C.c_uint, C.POINTER(vp), P64],
     "hv_host_free": [vp],

@@ -9,7 +9,7 @@
 //     mapped (cuMemMap) and opened to the readers (cuMemSetAccess) only while
 //     a live segment overlaps them.  Memory goes back to the donor the moment
 //     the last overlapping segment is released, which is what "harvest" means
-//     on a shared box (PAPER.md:184, runtime.py:396-411).
+//     on a shared box (PAPER.md:196, runtime.py:396-411).
 //   HV_POOL_IPC — one cudaMalloc slab exportable with cudaIpcGetMemHandle, for
 //     the one-process-per-GPU launch (torchrun) where readers live in other
 //     processes.
@@ -64,6 +64,8 @@ struct DriverApi {
   decltype(&cuMemMap) map = nullptr;
   decltype(&cuMemUnmap) unmap = nullptr;
   decltype(&cuMemSetAccess) setAccess = nullptr;
+  decltype(&cuMemExportToShareableHandle) exportHandle = nullptr;
+  decltype(&cuMemImportFromShareableHandle) importHandle = nullptr;
 };
 
 std::once_flag g_driver_once;
@@ -95,6 +97,8 @@ int driver() {
     if (!st) st = resolve("cuMemMap", &d.map);
     if (!st) st = resolve("cuMemUnmap", &d.unmap);
     if (!st) st = resolve("cuMemSetAccess", &d.setAccess);
+    if (!st) st = resolve("cuMemExportToShareableHandle", &d.exportHandle);
+    if (!st) st = resolve("cuMemImportFromShareableHandle", &d.importHandle);
     d.status = st;
     d.loaded = (st == HV_OK);
     g_driver = d;
@@ -239,6 +243,7 @@ HV_EXPORT int hv_pool_create(int donor_dev, uint64_t bytes, uint64_t chunk_bytes
   prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   prop.location.id = donor_dev;
+  if (flags & HV_POOL_REMOTE) prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
   size_t gran = 0;
   CUresult r = g_driver.getGranularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED);
   if (r != CUDA_SUCCESS || gran == 0) {
@@ -257,7 +262,7 @@ HV_EXPORT int hv_pool_create(int donor_dev, uint64_t bytes, uint64_t chunk_bytes
     delete p;
     return cu_status(r);
   }
-  if (flags & HV_POOL_EAGER) {
+  if ((flags & HV_POOL_EAGER) && !(flags & HV_POOL_REMOTE)) {
     st = hv_pool_commit(p, 0, bytes);
     if (st) {
       hv_pool_destroy(p);
@@ -272,6 +277,7 @@ HV_EXPORT int hv_pool_commit(hv_pool* p, uint64_t offset, uint64_t bytes) {
   HV_CHECK_ARG(p != nullptr);
   HV_CHECK_ARG(offset <= p->bytes && bytes <= p->bytes - offset);
   if ((p->flags & HV_POOL_IPC) || p->imported || bytes == 0) return HV_OK;
+  if (p->flags & HV_POOL_REMOTE) return HV_E_INVALID;   // chunks arrive as FDs (hv_pool_map_fd)
   const uint64_t c0 = offset / p->chunk, c1 = (offset + bytes - 1) / p->chunk;
   for (uint64_t ci = c0; ci <= c1; ++ci) {
     if (p->refs[ci] == 0) {
@@ -291,6 +297,7 @@ HV_EXPORT int hv_pool_decommit(hv_pool* p, uint64_t offset, uint64_t bytes) {
   HV_CHECK_ARG(p != nullptr);
   HV_CHECK_ARG(offset <= p->bytes && bytes <= p->bytes - offset);
   if ((p->flags & HV_POOL_IPC) || p->imported || bytes == 0) return HV_OK;
+  if (p->flags & HV_POOL_REMOTE) return HV_E_INVALID;
   const uint64_t c0 = offset / p->chunk, c1 = (offset + bytes - 1) / p->chunk;
   for (uint64_t ci = c0; ci <= c1; ++ci) HV_CHECK_ARG(p->refs[ci] > 0);
   int st = HV_OK;
@@ -332,7 +339,7 @@ HV_EXPORT int hv_pool_destroy(hv_pool* p) {
     if (e != cudaSuccess) st = hv_cuda_status(e);
   } else if (p->va) {
     for (uint64_t ci = 0; ci < p->handles.size(); ++ci)
-      if (p->refs[ci] > 0) {
+      if (p->refs[ci] > 0 || p->handles[ci] != 0) {
         int s2 = unmap_chunk(p, ci);
         if (s2 && !st) st = s2;
       }
@@ -385,6 +392,106 @@ HV_EXPORT int hv_pool_import_ipc(const void* handle64, int donor_dev, uint64_t b
   p->committed = bytes;
   *out = p;
   return HV_OK;
+}
+
+// ---- cross-process VMM donation (POSIX file descriptors) -------------------
+//
+// One process per GPU: a donor process creates each physical chunk on its
+// own GPU with a shareable handle and passes the file descriptor to the
+// reader over a Unix socket (pool.DonorServer, SCM_RIGHTS); the reader maps
+// it into a VA range it reserved (HV_POOL_REMOTE) and opens it to its own
+// device.  Releasing is the reverse: the reader unmaps and drops its handle,
+// the donor drops its own, and the HBM goes back to the donor GPU -- the
+// multi-process form of the single-process commit/decommit above.
+
+HV_EXPORT int hv_chunk_granularity(int device, uint64_t* out) {
+  HV_CHECK_ARG(out);
+  int st = driver();
+  if (st) return st;
+  CUmemAllocationProp prop;
+  memset(&prop, 0, sizeof(prop));
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = device;
+  prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  size_t g = 0;
+  HV_CU(g_driver.getGranularity(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+  *out = g;
+  return HV_OK;
+}
+
+HV_EXPORT int hv_chunk_create_shareable(int device, uint64_t bytes, uint64_t* handle_out, int* fd_out) {
+  HV_CHECK_ARG(handle_out && fd_out && bytes > 0);
+  int st = driver();
+  if (st) return st;
+  hv::DeviceGuard dg;
+  if ((st = dg.set(device))) return st;
+  CUmemAllocationProp prop;
+  memset(&prop, 0, sizeof(prop));
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = device;
+  prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  CUmemGenericAllocationHandle h = 0;
+  HV_CU(g_driver.create(&h, bytes, &prop, 0));
+  int fd = -1;
+  CUresult r = g_driver.exportHandle(&fd, h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0);
+  if (r != CUDA_SUCCESS) {
+    g_driver.release(h);
+    return cu_status(r);
+  }
+  *handle_out = (uint64_t)h;
+  *fd_out = fd;
+  return HV_OK;
+}
+
+HV_EXPORT int hv_chunk_release(uint64_t handle) {
+  int st = driver();
+  if (st) return st;
+  HV_CU(g_driver.release((CUmemGenericAllocationHandle)handle));
+  return HV_OK;
+}
+
+HV_EXPORT int hv_pool_map_fd(hv_pool* p, uint64_t chunk_index, int fd) {
+  HV_CHECK_ARG(p && (p->flags & HV_POOL_REMOTE) && fd >= 0);
+  HV_CHECK_ARG(chunk_index < p->handles.size() && p->handles[chunk_index] == 0);
+  int st = driver();
+  if (st) return st;
+  CUmemGenericAllocationHandle h = 0;
+  HV_CU(g_driver.importHandle(&h, (void*)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR));
+  CUdeviceptr at = p->va + chunk_index * p->chunk;
+  CUresult r = g_driver.map(at, p->chunk, 0, h, 0);
+  if (r != CUDA_SUCCESS) {
+    g_driver.release(h);
+    return cu_status(r);
+  }
+  std::vector<CUmemAccessDesc> acc;
+  CUmemAccessDesc d;
+  memset(&d, 0, sizeof(d));
+  d.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  d.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  for (int rd : p->readers) {
+    d.location.id = rd;
+    acc.push_back(d);
+  }
+  r = g_driver.setAccess(at, p->chunk, acc.data(), acc.size());
+  if (r != CUDA_SUCCESS) {
+    g_driver.unmap(at, p->chunk);
+    g_driver.release(h);
+    return cu_status(r);
+  }
+  p->handles[chunk_index] = h;
+  p->refs[chunk_index] = 1;
+  p->committed += p->chunk;
+  return HV_OK;
+}
+
+HV_EXPORT int hv_pool_unmap_chunk(hv_pool* p, uint64_t chunk_index) {
+  HV_CHECK_ARG(p && (p->flags & HV_POOL_REMOTE) && chunk_index < p->handles.size());
+  HV_CHECK_ARG(p->handles[chunk_index] != 0);
+  int st = unmap_chunk(p, chunk_index);
+  p->refs[chunk_index] = 0;
+  return st;
 }
 
 // ---- host tier ------------------------------------------------------------
