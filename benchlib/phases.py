@@ -299,7 +299,7 @@ def churn_phase(world, rank, dev, a, dist, barrier, layers=8, seconds=2.0):
         if node is not None:
             node.close()          # readers close, barrier, then the donors' servers stop
             if rank in D:
-                lending[name] = {"mode": node.mode, **node.donor_stats()}
+                lending[name] = {"mode": node.mode, **node.final_stats}
     if lending:
         outs["_donor_lending"] = lending
     results = [None] * world

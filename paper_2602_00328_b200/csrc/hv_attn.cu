@@ -31,6 +31,8 @@
 #include <cuda_fp16.h>
 #include <math.h>
 
+#include <mutex>
+
 #include "hv_common.h"
 
 namespace {
@@ -332,7 +334,8 @@ __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
 template <int D, int G, int S>
 __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_mma(
     const uint64_t* __restrict__ pages, const int32_t* __restrict__ seq_start, const int32_t* __restrict__ seq_tokens,
-    const __half* __restrict__ q, float* __restrict__ part, int kvh, int splits, float scale) {
+    const __half* __restrict__ q, float* __restrict__ part, int kvh, int splits, float scale,
+    float* __restrict__ final_out, unsigned* __restrict__ done) {
   static_assert(G <= 8, "query rows g and g+8 of the m16 tile: at most 8 heads per KV head");
   constexpr int KS = D / 16;             // k steps of Q K^T
   constexpr int NT = D / 8;              // n tiles of P V
@@ -476,6 +479,34 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_mma(
       out[D + 1] = L;
     }
   }
+  if (done == nullptr) return;   // the caller launches paged_decode_combine
+  // Fused combine: the last CTA of this (sequence, KV head) to finish merges
+  // the splits' partial states in split order -- the same arithmetic and
+  // order as paged_decode_combine, so the result does not depend on which CTA
+  // came last -- and re-arms the counter for the next launch (or graph replay).
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(done + (size_t)b * kvh + h, 1u) == (unsigned)splits - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const float* base = part + (((size_t)b * kvh + h) * splits) * G * (D + 2);
+  for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
+    const int hh = i / D, d = i % D;
+    float M = -INFINITY;
+    for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, __ldcg(base + ((size_t)sp * G + hh) * (D + 2) + D));
+    float L = 0.f, A = 0.f;
+    for (int sp = 0; sp < splits; ++sp) {
+      const float* pp = base + ((size_t)sp * G + hh) * (D + 2);
+      const float pm = __ldcg(pp + D);
+      const float cf = pm == -INFINITY ? 0.f : __expf(pm - M);
+      L += __ldcg(pp + D + 1) * cf;
+      A += __ldcg(pp + d) * cf;
+    }
+    final_out[((size_t)b * (kvh * G) + h * G + hh) * D + d] = L > 0.f ? A / L : 0.f;
+  }
+  if (threadIdx.x == 0) done[(size_t)b * kvh + h] = 0u;
 }
 
 // out[b][qh][d] = sum_s acc_s[d] e^(m_s - M) / sum_s l_s e^(m_s - M), splits in order
@@ -504,6 +535,42 @@ __global__ void paged_decode_combine(const float* __restrict__ part, float* __re
 #define HV_ATTN_RING 3   // stages of the scalar kernel, built only with HV_ATTN_MMA=0
 #endif
 
+// Per-device arrival counters of the fused combine (one per sequence x KV
+// head), zero between launches.  Grown only outside CUDA-graph capture; a
+// launch that finds them too small while capturing uses the two-kernel path.
+std::mutex g_done_mu;
+unsigned* g_done[64] = {};
+size_t g_done_cap[64] = {};
+
+unsigned* done_counters(int dev, size_t need, cudaStream_t s) {
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(g_done_mu);
+  if (g_done_cap[dev] >= need) return g_done[dev];
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  size_t cap_n = need < 4096 ? 4096 : need;
+  unsigned* p = nullptr;
+  if (cudaMalloc(&p, cap_n * sizeof(unsigned)) != cudaSuccess || cudaMemset(p, 0, cap_n * sizeof(unsigned)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    if (p) cudaFree(p);
+    return nullptr;
+  }
+  if (g_done[dev]) {   // no launch can still use the old buffer: wait for the device before freeing it
+    cudaDeviceSynchronize();
+    cudaFree(g_done[dev]);
+  }
+  g_done[dev] = p;
+  g_done_cap[dev] = cap_n;
+  return p;
+}
+
+#ifndef HV_ATTN_FUSED_COMBINE
+#define HV_ATTN_FUSED_COMBINE 1
+#endif
+
 template <int D, int G>
 int launch_attn(const uint64_t* pages, const int32_t* seq_start, const int32_t* seq_tokens, const void* q,
                 float* out, float* part, uint32_t B, uint32_t kvh, uint32_t splits, float scale, cudaStream_t s) {
@@ -517,8 +584,15 @@ int launch_attn(const uint64_t* pages, const int32_t* seq_start, const int32_t* 
     constexpr size_t smem = (size_t)kAttnWarps * kS * Ring<D>::kStage;
     st = hv::kernel_attr<paged_decode_mma<D, G, kS>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (st) return st;
+    unsigned* done = HV_ATTN_FUSED_COMBINE ? done_counters(dev, (size_t)B * kvh, s) : nullptr;
     paged_decode_mma<D, G, kS><<<grid, kAttnWarps * 32, smem, s>>>(
-        pages, seq_start, seq_tokens, reinterpret_cast<const __half*>(q), part, (int)kvh, (int)splits, scale);
+        pages, seq_start, seq_tokens, reinterpret_cast<const __half*>(q), part, (int)kvh, (int)splits, scale, out,
+        done);
+    if (done) {
+      HV_CUDA(cudaGetLastError());
+      hv::note_launch(1);
+      return HV_OK;
+    }
   }
 #else
   constexpr int kS = HV_ATTN_RING;

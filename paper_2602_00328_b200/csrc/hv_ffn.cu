@@ -390,6 +390,203 @@ __global__ void __launch_bounds__(kThreads) expert_ffn_persistent(FfnArgs a, int
   cp_wait<0>();
 }
 
+// Measured on B200, experts in HBM (tools/fused_probe.py, weight GB/s of the
+// activated experts, Qwen stage / Phi-3.5 batch 1 / 16 / 64; gpurun r2e):
+//   this 1-D bulk-copy ring: 1,007 / 622 / 961 / 1,035
+//   the cp.async persistent form: 4,960 / 2,995 / 5,024 / 5,165
+// A weight row of a k-tile is only 256 contiguous bytes, so the ring issues
+// 128+ bulk copies per stage and the per-copy cost of the bulk-copy engine
+// (~70 cycles for 256 B, 3.5 B/cycle per SM) caps the stream at ~1 TB/s.  The
+// TMA form worth having moves 2-D boxes through a tensor map (one 8 KiB
+// 128B-swizzled box per matrix per stage, the cp.async layout exactly); that
+// needs per-expert descriptors (tensormap.replace of the global address per
+// item).  Until then the cp.async form stays the default.
+#ifndef HV_FFN_TMA
+#define HV_FFN_TMA 0
+#endif
+
+#if HV_FFN_TMA
+// ---------------------------------------------------------------------------
+// TMA weight stream (HV_FFN_TMA=1; see the measurement above): the persistent item walk above, but the
+// weight and activation tiles arrive by cp.async.bulk (the bulk-copy / TMA
+// engine) into an mbarrier ring, issued by one producer warp, while four
+// consumer warps only run ldmatrix + mma.sync.  No thread spends issue slots
+// on 16-byte LDGSTS (the cp.async form issues ~1.25 of them per cycle per SM
+// at the HBM rate), and each stage keeps NMAT x 64 x 256 B of weights in
+// flight per CTA.  Tiles are 128 k-columns (256 contiguous bytes per weight
+// row: one bulk copy per row); smem rows are padded to 272 B, so the eight
+// row addresses of an ldmatrix fall in eight different 16-byte bank groups
+// (a 1-D bulk copy cannot write the XOR swizzle of the cp.async form).
+constexpr int kTKT = 128;
+constexpr int kTRowBytes = kTKT * 2;            // 256 B of one row per stage
+constexpr int kTPitch = kTRowBytes + 16;        // padded smem row
+constexpr int kTConsumers = 4;                  // mma warps (16 weight rows each)
+constexpr int kTThreads = (kTConsumers + 1) * 32;
+
+template <int NMAT>
+struct TSmem {
+  static constexpr int kS = NMAT == 2 ? 4 : 6;          // ring stages (~204 KiB either way)
+  static constexpr int kW = NMAT * kRows * kTPitch;
+  static constexpr int kX = kMaxTok * kTPitch;
+  static constexpr int kStage = kW + kX;
+  static constexpr int kBars = kS * 2 * 8;             // full[kS], empty[kS]
+  static constexpr int kTotal = kS * kStage + kBars;
+};
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n HV_FFN_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra HV_FFN_WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+template <int NMAT>
+__global__ void __launch_bounds__(kTThreads, 1) expert_ffn_tma(FfnArgs a, int n_items) {
+  extern __shared__ __align__(128) char smem[];
+  using T = TSmem<NMAT>;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rb_count = a.rows / kRows;
+  const int ktiles = a.K / kTKT;
+  const size_t wstride = (size_t)a.K * 2, xstride = (size_t)a.K * 2;
+  const uint32_t bars = smem_u32(smem + T::kS * T::kStage);   // full[s] at +8s, empty[s] at +8(kS+s)
+  // activation rows start finite (rows past n in the last N group feed
+  // output columns that are dropped; later stale rows are earlier activations)
+  for (int i = tid; i < T::kS * (T::kX / 16); i += kTThreads) {
+    const int st = i / (T::kX / 16), o = i % (T::kX / 16);
+    *reinterpret_cast<uint4*>(smem + st * T::kStage + T::kW + o * 16) = make_uint4(0, 0, 0, 0);
+  }
+  if (tid == 0) {
+    for (int st = 0; st < T::kS; ++st) {
+      mbar_init(bars + 8 * st, 1);                       // the producer's expect_tx arrival
+      mbar_init(bars + 8 * (T::kS + st), kTConsumers);   // one arrival per consumer warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // zeroed rows before bulk writes
+  __syncthreads();
+
+  ItemCursor c{(int)blockIdx.x, 0, 0, 0, 0, nullptr, nullptr};
+  cursor_seek<NMAT>(c, a, rb_count, n_items);
+  auto advance = [&](ItemCursor& cc) {
+    if (++cc.kt == ktiles) {
+      cc.item += gridDim.x;
+      cursor_seek<NMAT>(cc, a, rb_count, n_items);
+    }
+  };
+
+  if (warp == kTConsumers) {   // ---- producer warp
+    uint32_t it = 0;
+    while (c.item < n_items) {
+      const int st = it % T::kS;
+      const uint32_t round = it / T::kS;
+      if (round > 0) mbar_wait(bars + 8 * (T::kS + st), (round - 1) & 1);
+      const uint32_t full = bars + 8 * st;
+      const uint32_t bytes = (uint32_t)(NMAT * kRows + c.n) * kTRowBytes;
+      if (lane == 0) mbar_expect_tx(full, bytes);
+      __syncwarp();
+      char* base = smem + st * T::kStage;
+      const size_t kb = (size_t)c.kt * kTRowBytes;
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m) {
+        const char* src = (m == 0 ? c.w0 : c.w1) + kb;
+        const uint32_t ws = smem_u32(base + m * kRows * kTPitch);
+        for (int r = lane; r < kRows; r += 32) bulk_g2s(ws + r * kTPitch, src + r * wstride, kTRowBytes, full);
+      }
+      const uint32_t xs = smem_u32(base + T::kW);
+      for (int r = lane; r < c.n; r += 32) {
+        const int row = a.tok ? a.tok[c.p0 + r] : c.p0 + r;
+        bulk_g2s(xs + r * kTPitch, reinterpret_cast<const char*>(a.x) + row * xstride + kb, kTRowBytes, full);
+      }
+      advance(c);
+      ++it;
+    }
+    return;
+  }
+
+  // ---- consumer warps: rows warp*16 .. warp*16+15 of each item
+  float acc[NMAT][kGroups][4];
+#pragma unroll
+  for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+    for (int g = 0; g < kGroups; ++g)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[m][g][j] = 0.f;
+  const int a_row = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;   // A: x4 = rows 0-7/8-15 x k lo/hi
+  const int a_kc = lane >> 4;
+  const int b_row = lane & 7;                                         // B: x2 = tokens 0-7 x k lo/hi
+  const int b_kc = (lane >> 3) & 1;
+  uint32_t it = 0;
+  while (c.item < n_items) {
+    const int st = it % T::kS;
+    mbar_wait(bars + 8 * st, (it / T::kS) & 1);
+    const char* base = smem + st * T::kStage;
+    const uint32_t xs = smem_u32(base + T::kW);
+    const int ng = (c.n + 7) >> 3;
+#pragma unroll
+    for (int kk = 0; kk < kTKT / 16; ++kk) {
+      uint32_t af[NMAT][4];
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m)
+        ldsm_x4(smem_u32(base + m * kRows * kTPitch) + a_row * kTPitch + (kk * 2 + a_kc) * 16, af[m][0], af[m][1],
+                af[m][2], af[m][3]);
+#pragma unroll
+      for (int g = 0; g < kGroups; ++g) {
+        if (g < ng) {
+          uint32_t b0, b1;
+          ldsm_x2(xs + (g * 8 + b_row) * kTPitch + (kk * 2 + b_kc) * 16, b0, b1);
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m) mma_bf16(acc[m][g], af[m][0], af[m][1], af[m][2], af[m][3], b0, b1);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bars + 8 * (T::kS + st));   // stage free for the producer
+    if (c.kt == ktiles - 1) {   // item complete: epilogue
+      const int r = c.row0 + warp * 16 + (lane >> 2);
+      const int c2 = (lane & 3) * 2;
+#pragma unroll
+      for (int g = 0; g < kGroups; ++g) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int t = g * 8 + c2 + (j & 1);
+          if (g < ng && t < c.n) {
+            const size_t o = (size_t)(c.p0 + t) * a.rows + r + (j >> 1) * 8;
+            if constexpr (NMAT == 2) {
+              const float gv = acc[0][g][j], uv = acc[1][g][j];
+              reinterpret_cast<__nv_bfloat16*>(a.out)[o] = __float2bfloat16_rn(gv / (1.f + __expf(-gv)) * uv);
+            } else {
+              reinterpret_cast<float*>(a.out)[o] = acc[0][g][j];
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m) acc[m][g][j] = 0.f;
+        }
+      }
+    }
+    advance(c);
+    ++it;
+  }
+}
+
+
+#endif  // HV_FFN_TMA
+
 template <int NMAT>
 int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
   if (n_experts == 0) return HV_OK;
@@ -402,6 +599,20 @@ int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
   if (st) return st;
   st = hv::kernel_attr<expert_ffn_kernel<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<NMAT>::kTotal);
   if (st) return st;
+#if HV_FFN_TMA
+  if (a.K % kTKT == 0) {
+    using T = TSmem<NMAT>;
+    st = hv::kernel_attr<expert_ffn_tma<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kTotal);
+    if (st) return st;
+    const int n_items = (int)(a.rows / kRows) * (int)n_experts;
+    int g = hv::sm_count(dev);                    // one ~204 KiB CTA per SM
+    if (g > n_items) g = n_items;
+    expert_ffn_tma<NMAT><<<g, kTThreads, T::kTotal, (cudaStream_t)stream>>>(a, n_items);
+    HV_CUDA(cudaGetLastError());
+    hv::note_launch();
+    return HV_OK;
+  }
+#endif
 #if HV_FFN_PERSISTENT
   static int resident[64] = {};
   if (dev >= 0 && dev < 64 && !resident[dev]) {

@@ -270,7 +270,11 @@ class DonorServer:
                     with self._lock:
                         self._release((cid, idx))
                     _send_msg(conn, {"ok": True})
-                elif op == "bye":
+                elif op == "bye":          # the reader unmapped everything: release, then acknowledge
+                    with self._lock:
+                        for key in [k for k in self._held if k[0] == cid]:
+                            self._release(key)
+                    _send_msg(conn, {"ok": True})
                     break
         except (ConnectionError, OSError, ValueError):
             pass
@@ -388,7 +392,9 @@ class RemotePool:
             self._p = C.c_void_p()
             try:
                 _send_msg(self._sock, {"op": "bye"})
-            except OSError:
+                self._sock.settimeout(30.0)
+                _recv_msg(self._sock)           # the donor has released this reader's chunks
+            except (OSError, ConnectionError, ValueError):
                 pass
             self._sock.close()
 
@@ -506,6 +512,7 @@ class NodePools:
             p.close()
         self._readers, self.views = [], {}
         self.group.barrier()
+        self.final_stats = self.donor_stats()     # every reader gone: what was lent and given back
         if self._own is not None:
             self._own.close()
             self._own = None

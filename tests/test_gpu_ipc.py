@@ -130,6 +130,8 @@ FD_READER = textwrap.dedent("""
     local = sysm.local.cpu().numpy()
     for e in range(n):
         assert np.array_equal(local[(n - 1 - e) * S:(n - e) * S], O.content(seeds[e], S)), e
+    torch.cuda.synchronize()
+    free_a = torch.cuda.mem_get_info(0)[0]
     # revoke half: only chunks no live segment overlaps go back to the donor
     for h in hs[:4]:
         rt.revoke(h, RevokeReason.PRESSURE)
@@ -142,7 +144,8 @@ FD_READER = textwrap.dedent("""
     assert pool.committed_bytes == 0 and donated() == 0
     torch.cuda.synchronize()
     free2 = torch.cuda.mem_get_info(0)[0]
-    assert free2 - free1 >= committed                 # the HBM went back to the donor GPU
+    # the HBM went back to the donor GPU (nothing else is allocated meanwhile)
+    assert free2 - free_a >= committed, (free0, free1, free_a, free2, committed)
     sysm.close()
     open({done!r}, "w").write("ok")
     print("reader ok")

@@ -1,5 +1,9 @@
 """Short, ncu-friendly driver: a few launches of each fetch kernel at the
-bench shapes.  Usage: python tools/profile_target.py [host|hbm|kv|blocks] [engine]"""
+bench shapes.  Usage: python tools/profile_target.py MODE [engine] [reps]
+MODE: host | hbm | kv | blocks | attn | fused | check (the per-fetch digest
+check of one Qwen stage) | peer | peer_kv (both need 2 GPUs: cuda:1 donates
+a VMM pool read by cuda:0 over NVLink; tools/ncu_nvlink.sh captures the
+nvlrx/nvltx byte counters of those launches)."""
 import os
 import sys
 
@@ -30,6 +34,47 @@ def main():
         sz = F.ptrs_tensor([S] * n, dev)
         for _ in range(reps):
             F.batch_copy(sp, dp, sz, engine=eng)
+    elif what in ("peer", "peer_kv"):   # NVLink: a VMM pool on cuda:1, read by cuda:0
+        from paper_2602_00328_b200 import _native as N
+        from paper_2602_00328_b200.pool import PeerPool
+        if torch.cuda.device_count() < 2:
+            raise SystemExit("peer modes need 2 GPUs")
+        N.call("hv_enable_peer_access", 0, 1)
+        S, n = 17_301_504, 53
+        pool = PeerPool(1, n * S, readers=[0])
+        pool.commit(0, n * S)
+        F.fill_content(F.ptrs_tensor([pool.va + i * S for i in range(n)], "cuda:1"),
+                       F.ptrs_tensor([S] * n, "cuda:1"), list(range(n)))
+        torch.cuda.synchronize(1)
+        if what == "peer":
+            dst = torch.empty(n * S, dtype=torch.uint8, device=dev)
+            sp = F.ptrs_tensor([pool.va + i * S for i in range(n)], dev)
+            dp = F.ptrs_tensor([dst.data_ptr() + i * S for i in range(n)], dev)
+            sz = F.ptrs_tensor([S] * n, dev)
+            for _ in range(reps):
+                F.batch_copy(sp, dp, sz, engine=eng)
+        else:   # config 1's layer: 1,024 x 64 KiB pages at randperm(seed 1) slots of the donor pool
+            page, npg = 65536, 1024
+            slots = torch.randperm(n * S // page, generator=torch.Generator().manual_seed(1))[:npg]
+            src = F.ptrs_tensor([pool.va + int(t) * page for t in slots], dev)
+            dst = torch.empty(npg * page, dtype=torch.uint8, device=dev)
+            for _ in range(reps):
+                F.kv_gather(src, page, dst=dst, engine=eng)
+        torch.cuda.synchronize(0)
+        pool.decommit(0, n * S)
+        pool.close()
+    elif what == "check":   # per-fetch content check (hv_check_digests) of one Qwen stage in HBM
+        from paper_2602_00328_b200 import _native as N
+        S, n = 17_301_504, 53
+        buf = torch.empty(n * S, dtype=torch.uint8, device=dev)
+        ptrs = np.array([buf.data_ptr() + i * S for i in range(n)], dtype=np.uint64)
+        sz = np.full(n, S, dtype=np.uint64)
+        exp = np.zeros(n, dtype=np.uint64)
+        scratch = torch.zeros(n, dtype=torch.int64, device=dev)
+        err = torch.zeros(1, dtype=torch.int64, device=dev)
+        for _ in range(reps):
+            N.call("hv_check_digests_batch", ptrs.ctypes.data, sz.ctypes.data, exp.ctypes.data, n,
+                   scratch.data_ptr(), 0, err.data_ptr(), 0)
     elif what == "blocks":  # KV reload slice: 256 blocks x 32 layers x 64 KiB, [layer][slot] slabs -> cache
         page, L, nb, slab = 65536, 32, 256, 64
         slabs = [torch.empty(L * slab * page, dtype=torch.uint8, device=dev) for _ in range(nb // slab)]
