@@ -40,7 +40,7 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-from benchlib.common import (KV_SLAB_BLOCKS, KV_TOKENS, METRIC, SEED, emit, kv_slab_bytes, load_traffic, model, routing, workload_config)  # noqa: E402
+from benchlib.common import (KV_SLAB_BLOCKS, KV_TOKENS, METRIC, SEED, emit, kv_slab_bytes, load_peaks, load_traffic, model, routing, workload_config)  # noqa: E402
 from benchlib.compare import (autotune, measure_pcie_h2d, probe_engines_on_peer, same_run_comparisons)  # noqa: E402
 from benchlib.cpu import (cpu_gather_sample, cpu_host_copy, cpu_model, reference_simulator, run_reference)  # noqa: E402
 from benchlib.phases import (churn_phase, host_offload_decode, kv_decode_config1, kv_long_context,  # noqa: E402
@@ -237,8 +237,12 @@ def run_b200(a):
                 evs[layer][1].record(stream)
             fetch_done[layer].record(stream)
             check_s.wait_event(fetch_done[layer])
+            if evs is not None:
+                evs[layer][2].record(check_s)
             N.call("hv_check_digests_batch", dp.ctypes.data, sz.ctypes.data, ex_d.ctypes.data, len(sp),
                    chk_scratch.data_ptr(), 0, chk_errors.data_ptr(), check_s.cuda_stream)
+            if evs is not None:
+                evs[layer][3].record(check_s)
             check_done[layer].record(check_s)
         stream.wait_event(check_done[L - 1])
         stream.wait_event(check_done[L - 2])
@@ -247,7 +251,7 @@ def run_b200(a):
         value_step(s)
     torch.cuda.synchronize()
     launches0 = N.launch_count()
-    step_events = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    step_events = [[tuple(torch.cuda.Event(enable_timing=True) for _ in range(4))
                     for _ in range(L)] for _ in range(a.steps)]
     barrier()
     torch.cuda.synchronize()
@@ -283,6 +287,8 @@ def run_b200(a):
     value = total_bytes / dt / 1e9
     launch_ms = [step_events[k][l][0].elapsed_time(step_events[k][l][1])
                  for k in range(a.steps) for l in range(L)]
+    check_ms = [step_events[k][l][2].elapsed_time(step_events[k][l][3])
+                for k in range(a.steps) for l in range(L)]
     bytes_per_launch = my_bytes / (a.steps * L)
     achieved = bytes_per_launch / (statistics.mean(launch_ms) * 1e-3) / 1e9
 
@@ -397,13 +403,34 @@ def run_b200(a):
                     "frac": achieved / peak,
                     "peak_source": "B200_PROFILING.md fallback: measured peer copy 770 GB/s per direction "
                                    "(900 nominal)"}
-        tr = load_traffic().get("batch_copy_" + source)
-        roof["traffic"] = tr["traffic_bytes_per_launch"] if tr else None
-        if tr:
-            roof["traffic_source"] = (f"profiles/traffic.json[{'batch_copy_' + source}]: one ncu --set full capture "
-                                      f"({tr['report']}), algorithmic {tr['algorithmic_bytes_per_launch']:.0f} B/launch")
+        roof["engine"] = a.engine
+        if a.engine in ("ce", "auto") and source == "host":
+            # the copy engine moves the host-tier experts: a DMA engine, not a
+            # kernel -- ncu has nothing to capture; the step's SM kernel is the
+            # per-fetch check, reported in roofline_check_kernel
+            roof["traffic"] = None
+            roof["traffic_source"] = ("copy engine (cudaMemcpyBatchAsync): not a kernel, no ncu capture; the same "
+                                      "bytes through the K2 kernel: profiles/traffic.json[batch_copy_host]")
+        else:
+            tr = load_traffic().get("batch_copy_" + source)
+            roof["traffic"] = tr["traffic_bytes_per_launch"] if tr else None
+            if tr:
+                roof["traffic_source"] = (f"profiles/traffic.json[{'batch_copy_' + source}]: one ncu --set full "
+                                          f"capture ({tr['report']}), algorithmic "
+                                          f"{tr['algorithmic_bytes_per_launch']:.0f} B/launch")
         roof["bytes_per_launch"] = bytes_per_launch
         roof["mean_launch_ms"] = statistics.mean(launch_ms)
+        hbm_peak = load_peaks().get("hbm_gbs")
+        chk_gbps = bytes_per_launch / (statistics.mean(check_ms) * 1e-3) / 1e9
+        trc = load_traffic().get("check_digests")
+        roof_check = {"kernel": "hv_check_digests (digest of every arrival + compare; desc_op_kernel<DigestOpR> + "
+                                "digest_compare_kernel)", "bound": "hbm", "achieved": chk_gbps,
+                      "peak": hbm_peak, "unit": "GB/s", "frac": chk_gbps / hbm_peak if hbm_peak else None,
+                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write; this kernel only reads)",
+                      "bytes_per_launch": bytes_per_launch, "mean_launch_ms": statistics.mean(check_ms),
+                      "traffic": trc["traffic_bytes_per_launch"] if trc else None}
+        if trc:
+            roof_check["traffic_source"] = f"profiles/traffic.json[check_digests] ({trc['report']})"
         try:   # rank-0 local work only (no collectives inside): a failure is reported, never fatal
             extra = same_run_comparisons(dev, m, a, source, fetcher)
         except Exception as e:
@@ -439,7 +466,8 @@ def run_b200(a):
                         "read_errors_note": "objects whose fetched bytes' digest differed from the authoritative "
                                             "copy's, over every fetch of the timed value and e2e steps "
                                             "(moe.py:315-319)"},
-                "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
+                "gpu_launches": launches, "roofline": roof, "roofline_check_kernel": roof_check,
+                "cpu_baseline": cpu,
                 "clocks": {**clk.summary(), "first_attempt_rejected": remeasured},
                 "latency_ms_per_layer_fetch": statistics.median(launch_ms),
                 "latency_ms_per_layer_fetch_dist": {"p50": float(np.percentile(launch_ms, 50)),

@@ -63,6 +63,28 @@ def load_traffic():
             return {}
     return {}
 
+def load_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "fallback": "B200_PROFILING.md fallback 6.65 TB/s"}
+
 def kv_slab_bytes():
     from paper_2602_00328_b200.kv import LLAMA3_8B
     return KV_SLAB_BLOCKS * LLAMA3_8B.block_bytes
+
+
+def reference_checkers():
+    """The reference's own event-log checkers (harvestsim/verify.py:25-88)
+    from the unmodified install under baseline/_ref -- the bench's checker
+    for release ordering under churn, never part of the measured path."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "harvestsim")):
+        def unavailable(_log):
+            return ["unchecked: baseline/_ref (the reference's verify.py) is not installed"]
+        return unavailable, unavailable
+    if ref not in sys.path:
+        sys.path.append(ref)
+    from harvestsim.verify import verify_no_runtime_writeback, verify_release_ordering
+    return verify_release_ordering, verify_no_runtime_writeback

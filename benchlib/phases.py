@@ -357,7 +357,8 @@ def _churn_compute(world, rank, dev, a, m, layout, per_reader, node, seconds, po
     from paper_2602_00328_b200.moe import ExpertFetcher, ExpertResidency, ExpertStore, rebalance
     from paper_2602_00328_b200.pool import HostTier, PeerPool
     from paper_2602_00328_b200.system import HarvestSystem
-    from paper_2602_00328_b200.verify import verify_release_ordering
+    from benchlib.common import reference_checkers
+    verify_release_ordering = reference_checkers()[0]
     L, E, S = m.num_layers, m.num_experts, m.expert_size
     host = HostTier(L * E * S)
     if world == 1:

@@ -24,7 +24,7 @@ from paper_2602_00328_b200 import runtime as R
 from paper_2602_00328_b200.events import VirtualLoop
 from paper_2602_00328_b200.interconnect import LinkKind, LinkSpec, transfer_time
 from paper_2602_00328_b200.memalloc import Segment, Tier
-from paper_2602_00328_b200.verify import verify_no_runtime_writeback, verify_release_ordering
+from tests.refcheck import verify_no_runtime_writeback, verify_release_ordering
 from tests.test_runtime_parity import topo
 
 MiB = 1 << 20

@@ -167,7 +167,7 @@ def test_graph_replay_equals_eager_and_all_local(microbatches):
     out2 = dec2.decode(3)
     torch.cuda.synchronize()
     assert torch.equal(out.view(torch.int16), out2.view(torch.int16))
-    from paper_2602_00328_b200.verify import verify_release_ordering
+    from tests.refcheck import verify_release_ordering
     assert verify_release_ordering(sysm.loop.log) == []
     sysm.close()
     sys2.close()
@@ -238,7 +238,7 @@ def test_fused_decode_offloaded_equals_all_local(microbatches):
     x0 = fdec.x0.float()
     d_f, d_s = out.float() - x0, staged.float() - x0
     assert (d_f - d_s).abs().max() <= 5e-2 * d_s.abs().max()
-    from paper_2602_00328_b200.verify import verify_release_ordering
+    from tests.refcheck import verify_release_ordering
     sysm.loop.run()
     assert verify_release_ordering(sysm.loop.log) == []
     sysm.close()
@@ -269,7 +269,7 @@ def test_fused_graph_replay_with_revocation():
     drains wait for the replays that read the revoked slabs."""
     from paper_2602_00328_b200.decode import MoEDecoder
     from paper_2602_00328_b200.runtime import RevokeReason
-    from paper_2602_00328_b200.verify import verify_release_ordering
+    from tests.refcheck import verify_release_ordering
     model = _tiny()
     sysm, store, res, fetcher, _dec = _setup(model, peer_experts=12, microbatches=2)
     dec = MoEDecoder(fetcher, tokens=16, microbatches=2, seed=0, residual_scale=RS, fused=True)
@@ -299,7 +299,7 @@ def test_revocation_completes_while_steps_stream(fused):
     reading the donor, and the outputs stay equal to the all-local run."""
     from paper_2602_00328_b200.decode import MoEDecoder
     from paper_2602_00328_b200.runtime import RevokeReason
-    from paper_2602_00328_b200.verify import verify_release_ordering
+    from tests.refcheck import verify_release_ordering
     model = _tiny()
     sysm, store, res, fetcher, _d = _setup(model, peer_experts=12, microbatches=1)
     dec = MoEDecoder(fetcher, tokens=16, microbatches=1, seed=0, residual_scale=RS, fused=fused)

@@ -55,7 +55,7 @@ def _reference(kv, m, dec):
 def test_tiered_kv_decode_equals_all_local_and_fp32():
     from paper_2602_00328_b200.kv import KVTier
     from paper_2602_00328_b200.kv_decode import KVAttentionDecoder
-    from paper_2602_00328_b200.verify import verify_release_ordering
+    from tests.refcheck import verify_release_ordering
     sysm, kv, m = _cache(local_blocks=4, donor_slabs=1)
     tiers = {b.tier for b in kv.table.values()}
     assert KVTier.PEER_HBM in tiers and KVTier.HOST_DRAM in tiers and KVTier.LOCAL_HBM in tiers
@@ -86,7 +86,7 @@ def test_kv_decode_survives_revocation(durability):
     Lossy ones are recomputed; outputs stay bit-identical."""
     from paper_2602_00328_b200.kv_decode import KVAttentionDecoder
     from paper_2602_00328_b200.runtime import RevokeReason
-    from paper_2602_00328_b200.verify import verify_release_ordering
+    from tests.refcheck import verify_release_ordering
     sysm, kv, m = _cache(local_blocks=4, donor_slabs=2, durability=durability)
     dec = KVAttentionDecoder(kv, [0, 1], q_heads=4, seed=5)
     first = dec.step().clone()
@@ -141,7 +141,7 @@ def test_fused_in_place_equals_gathered():
     """fused=True (attention over the pages where they lie, no K1) gives the
     same bits as the gathered mode; both read peer, host and local pages."""
     from paper_2602_00328_b200.kv_decode import KVAttentionDecoder
-    from paper_2602_00328_b200.verify import verify_release_ordering
+    from tests.refcheck import verify_release_ordering
     sysm, kv, m = _cache(local_blocks=4, donor_slabs=1)
     a = KVAttentionDecoder(kv, [0, 1], q_heads=4, seed=7).step()
     b = KVAttentionDecoder(kv, [0, 1], q_heads=4, seed=7, fused=True).step()
@@ -179,7 +179,7 @@ def test_graph_replay_equals_eager_across_revocation(fused):
     outputs stay bit-identical to eager steps, and drains wait for replays."""
     from paper_2602_00328_b200.kv_decode import KVAttentionDecoder
     from paper_2602_00328_b200.runtime import RevokeReason
-    from paper_2602_00328_b200.verify import verify_release_ordering
+    from tests.refcheck import verify_release_ordering
     sysm, kv, m = _cache(local_blocks=4, donor_slabs=1)
     eager = KVAttentionDecoder(kv, [0, 1], q_heads=4, seed=4, fused=fused).step().clone()
     dec = KVAttentionDecoder(kv, [0, 1], q_heads=4, seed=4, fused=fused)
