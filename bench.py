@@ -483,7 +483,7 @@ def run_b200(a):
     barrier()
     sysm.close()
     if node is not None:
-        pool_info = {"mode": node.mode, "setup_error": node.error}
+        pool_info = {"mode": node.mode, "setup_error": node.error, "fallback_reason": node.fallback_reason}
         node.close()
         if rank == 0:
             line["config"]["donor_pools"] = pool_info

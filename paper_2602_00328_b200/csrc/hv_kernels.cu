@@ -873,12 +873,33 @@ struct StagingRing {
 std::mutex g_ring_mu;
 StagingRing g_rings[64];
 
+// Descriptor upload by an SM kernel: the staging slot is mapped pinned
+// memory, and a copy-engine H2D of it would queue behind whatever bulk
+// copies the copy engines are running (a stage's 917 MB of host-tier
+// experts: ~16 ms), stalling a concurrent kernel fetch or content check.
+__global__ void upload_desc_kernel(const uint2* __restrict__ src, uint2* __restrict__ dst, uint32_t n8) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n8) dst[i] = src[i];
+}
+
+int upload_desc(const uint64_t* h, uint64_t* d, size_t words, cudaStream_t s) {
+  if (words == 0) return HV_OK;
+  const uint32_t n8 = (uint32_t)words;
+  upload_desc_kernel<<<(n8 + 255) / 256, 256, 0, s>>>(reinterpret_cast<const uint2*>(h), reinterpret_cast<uint2*>(d),
+                                                       n8);
+  HV_CUDA(cudaGetLastError());
+  hv::note_launch();
+  return HV_OK;
+}
+
 int ring_acquire(int dev, uint32_t* slot, StagingRing** ring) {
   if (dev < 0 || dev >= 64) return HV_E_INVALID;
   StagingRing& r = g_rings[dev];
   if (!r.init) {
     const size_t words = (size_t)kRingSlots * 3 * kSlotDescs;
-    HV_CUDA(cudaHostAlloc((void**)&r.h, words * 8, cudaHostAllocPortable));
+    // mapped: the descriptor upload is an SM kernel reading it over PCIe
+    // (upload_desc), never a DMA that would queue behind bulk copy-engine work
+    HV_CUDA(cudaHostAlloc((void**)&r.h, words * 8, cudaHostAllocPortable | cudaHostAllocMapped));
     HV_CUDA(cudaMalloc((void**)&r.d, words * 8));
     for (uint32_t i = 0; i < kRingSlots; ++i) HV_CUDA(cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming));
     r.init = true;
@@ -999,8 +1020,7 @@ int kernel_swap(const uint64_t* h_src, const uint64_t* h_dst, const uint64_t* h_
     memcpy(hs, h_src + base, m * 8);
     memcpy(hs + m, h_dst + base, m * 8);
     memcpy(hs + 2 * m, h_bytes + base, m * 8);
-    HV_CUDA(cudaMemcpyAsync(ds, hs, (size_t)(uniform ? 2 : 3) * m * 8, cudaMemcpyHostToDevice,
-                            (cudaStream_t)stream));
+    if ((st = upload_desc(hs, ds, (size_t)(uniform ? 2 : 3) * m, (cudaStream_t)stream))) return st;
     if (uniform && h_bytes[base] > 0) {
       PageResolver<false> r{};
       r.src = ds;
@@ -1283,7 +1303,7 @@ HV_EXPORT int hv_check_digests_batch(const uint64_t* h_src, const uint64_t* h_by
     memcpy(hs, h_src + base, m * 8);
     memcpy(hs + m, h_bytes + base, m * 8);
     memcpy(hs + 2 * m, h_expected + base, m * 8);
-    HV_CUDA(cudaMemcpyAsync(ds, hs, (size_t)3 * m * 8, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    if ((st = upload_desc(hs, ds, (size_t)3 * m, (cudaStream_t)stream))) return st;
     if ((st = hv_check_digests(ds, ds + m, ds + 2 * m, m, d_scratch + base, d_flags ? d_flags + base : nullptr,
                                d_errors, stream)))
       return st;

@@ -432,29 +432,41 @@ class NodePools:
         self.views: dict = {}
         self._own = None          # this rank's IPC slab or DonorServer
         self._readers = []        # pools this rank opened
-        self.error = None
+        self.error = None         # set when this rank has no usable pools
+        self.fallback_reason = None   # why the remote mode was abandoned (informational)
         self.mode = mode
         if mode == "remote":
-            ok = True
-            try:
-                self._open_remote(device_of, tag, chunk_bytes)
-            except Exception as e:   # noqa: BLE001 - reported, then the collective fallback
-                ok, self.error = False, repr(e)[:300]
-            if group.any(not ok):
+            # two phases (servers listen, then readers connect), each closed by
+            # a collective status check that doubles as the barrier between
+            # them: a failure anywhere sends every rank to the fallback at the
+            # same point, so no rank waits in a different collective
+            failed = False
+            for phase in (self._start_server, self._connect):
+                try:
+                    phase(device_of, tag, chunk_bytes)
+                except Exception as e:   # noqa: BLE001 - reported, then the collective fallback
+                    self.fallback_reason = self.fallback_reason or repr(e)[:300]
+                if group.any(self.fallback_reason is not None):
+                    failed = True
+                    break
+            if failed:
                 self._close_all()
                 self.mode = "ipc"
         if self.mode == "ipc":
             self._open_ipc()
 
-    def _open_remote(self, device_of, tag, chunk_bytes):
+    def _start_server(self, device_of, tag, chunk_bytes):
         lay, r = self.layout, self.rank
         self.section_bytes = -(-lay.per_reader // chunk_bytes) * chunk_bytes
         if r in lay.donors and lay.readers_of(r):
             self._own = DonorServer(self.dev, _socket_path(tag, r), chunk_bytes, budget=self.section_bytes)
-        self.group.barrier()                      # every server listens before anyone connects
+
+    def _connect(self, device_of, tag, chunk_bytes):
+        lay, r = self.layout, self.rank
         if r in lay.compute:
             for d in lay.donors_of(r):
-                p = RemotePool(_socket_path(tag, d), device_of(d), self.section_bytes, chunk_bytes, self.dev)
+                p = RemotePool(_socket_path(tag, d), device_of(d), self.section_bytes, chunk_bytes, self.dev,
+                               connect_timeout=30.0)
                 self._readers.append(p)
                 self.views[lay.peer_index(r, d)] = p
 

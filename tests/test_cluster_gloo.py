@@ -169,3 +169,74 @@ def test_multi_rank_placement_gloo(world, split):
     for k in range(n_obj):
         on = [dict((a[0], a[1]) for a in everything[r])[k] for r in lay.compute]
         assert len(set(on)) == len(on)
+
+
+# ---- NodePools: collective fallback and teardown (no GPU here)
+
+def _nodepools_main(rank, world, port, q, split):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2602_00328_b200.cluster import RankGroup
+        from paper_2602_00328_b200.pool import NodePools
+        g = RankGroup(world, rank)
+        lay = (DonorLayout.split_roles if split else DonorLayout.symmetric)(world, 64 << 20)
+        node = NodePools(g, lay, rank, lambda r: r, mode="remote", tag="cpu-test")
+        # no CUDA device: the remote setup fails somewhere, so EVERY rank falls
+        # back to ipc together (collective decision), which fails too; the
+        # error is recorded, no rank hangs, and close() stays collective
+        out = (node.mode, node.error is not None, len(node.views))
+        node.close()
+        g.barrier()
+        q.put(("ok", rank, out))
+    except BaseException as e:  # surface the failure to the parent
+        q.put(("error", rank, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,split", [(2, False), (4, True)])
+def test_nodepools_fall_back_together_and_close(world, split):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_nodepools_main, args=(r, world, port, q, split)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    msgs = []
+    while not q.empty():
+        msgs.append(q.get())
+    assert not [m for m in msgs if m[0] == "error"], msgs
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    outs = {m[1]: m[2] for m in msgs}
+    assert len(outs) == world
+    assert all(o[0] == "ipc" for o in outs.values())          # one decision for all ranks
+    assert all(o[2] == 0 for o in outs.values())              # and no half-built views
+
+
+def test_donation_socket_framing_passes_file_descriptors():
+    """The DonorServer / RemotePool wire format: length-prefixed JSON, with
+    the chunk's file descriptor riding on the reply (SCM_RIGHTS)."""
+    import socket as S
+    from paper_2602_00328_b200.pool import _recv_msg, _send_msg
+    a, b = S.socketpair(S.AF_UNIX, S.SOCK_STREAM)
+    r, w = os.pipe()
+    try:
+        _send_msg(a, {"op": "create", "chunk": 7})
+        assert _recv_msg(b) == {"op": "create", "chunk": 7}
+        _send_msg(b, {"ok": True, "bytes": 1 << 25}, fds=[w])
+        msg, fds = _recv_msg(a, want_fds=True)
+        assert msg == {"ok": True, "bytes": 1 << 25} and len(fds) == 1
+        os.write(fds[0], b"chunk")                             # the received fd is the pipe's write end
+        assert os.read(r, 5) == b"chunk"
+        os.close(fds[0])
+    finally:
+        for fd in (r, w):
+            os.close(fd)
+        a.close()
+        b.close()
