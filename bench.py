@@ -186,6 +186,8 @@ def run_b200(a):
 
     barrier = group.barrier
     max_over_ranks = group.max
+    chk_scratch = torch.zeros(E, dtype=torch.int64, device=f"cuda:{dev}")
+    chk_errors = torch.zeros(1, dtype=torch.int64, device=f"cuda:{dev}")
     a.kernel_engine = a.engine if a.engine not in ("ce", "auto") else "auto"
 
     if a.engine == "auto":
@@ -204,7 +206,8 @@ def run_b200(a):
         # plus the copy engine and the library's engine per source
         tune = autotune(desc[0][0], stream, stream_h, F, engines=engines + ("ce", "auto"),
                         barrier=barrier if world > 1 else None,
-                        max_over_ranks=max_over_ranks if world > 1 else None)
+                        max_over_ranks=max_over_ranks if world > 1 else None,
+                        checked=(chk_scratch, chk_errors) if source == "peer" else None)
         tune["peer_engine_probe"] = safe
         kern = [r for r in tune["candidates"] if r["engine"] not in ("ce", "auto")]
         kbest = max(kern, key=lambda r: r["GBps"])
@@ -215,11 +218,13 @@ def run_b200(a):
         fetcher.engine.engine = N.ENGINES[a.engine]
         fetcher.engine.max_ctas = a.max_ctas
 
-    chk_scratch = torch.zeros(E, dtype=torch.int64, device=f"cuda:{dev}")
-    chk_errors = torch.zeros(1, dtype=torch.int64, device=f"cuda:{dev}")
     fetch_done = [torch.cuda.Event() for _ in range(L)]
     check_done = [torch.cuda.Event() for _ in range(L)]
     eng_code = N.ENGINES[a.engine]
+    # the product's choice (ExpertFetcher.issue_fetches): a stage with peer
+    # experts is fetched and checked in one kernel pass; an all-host stage
+    # rides the copy engine with the digest on a side stream
+    fused_check = source == "peer"
 
     def value_step(s, evs=None):
         """One decode step's fetches: per layer, one hv_swap_blocks_batch on the
@@ -227,6 +232,15 @@ def run_b200(a):
         next layer's fetch); staging buffer layer%2 is refilled only after the
         check of two layers back has read it."""
         for layer, (sp, dp, sz, nb, ex_d) in enumerate(desc[s]):
+            if fused_check:   # peer tier: fetch + digest in one kernel pass, compare on the same stream
+                if evs is not None:
+                    evs[layer][0].record(stream)
+                N.call("hv_swap_blocks_batch_checked", sp.ctypes.data, dp.ctypes.data, sz.ctypes.data,
+                       ex_d.ctypes.data, len(sp), eng_code, a.max_ctas, chk_scratch.data_ptr(), 0,
+                       chk_errors.data_ptr(), stream_h)
+                if evs is not None:
+                    evs[layer][1].record(stream)
+                continue
             if layer >= 2:
                 stream.wait_event(check_done[layer - 2])
             if evs is not None:
@@ -244,8 +258,9 @@ def run_b200(a):
             if evs is not None:
                 evs[layer][3].record(check_s)
             check_done[layer].record(check_s)
-        stream.wait_event(check_done[L - 1])
-        stream.wait_event(check_done[L - 2])
+        if not fused_check:
+            stream.wait_event(check_done[L - 1])
+            stream.wait_event(check_done[L - 2])
 
     for s in range(a.warmup):
         value_step(s)
@@ -287,8 +302,8 @@ def run_b200(a):
     value = total_bytes / dt / 1e9
     launch_ms = [step_events[k][l][0].elapsed_time(step_events[k][l][1])
                  for k in range(a.steps) for l in range(L)]
-    check_ms = [step_events[k][l][2].elapsed_time(step_events[k][l][3])
-                for k in range(a.steps) for l in range(L)]
+    check_ms = None if fused_check else [step_events[k][l][2].elapsed_time(step_events[k][l][3])
+                                         for k in range(a.steps) for l in range(L)]
     bytes_per_launch = my_bytes / (a.steps * L)
     achieved = bytes_per_launch / (statistics.mean(launch_ms) * 1e-3) / 1e9
 
@@ -421,14 +436,20 @@ def run_b200(a):
         roof["bytes_per_launch"] = bytes_per_launch
         roof["mean_launch_ms"] = statistics.mean(launch_ms)
         hbm_peak = load_peaks().get("hbm_gbs")
-        chk_gbps = bytes_per_launch / (statistics.mean(check_ms) * 1e-3) / 1e9
         trc = load_traffic().get("check_digests")
-        roof_check = {"kernel": "hv_check_digests (digest of every arrival + compare; desc_op_kernel<DigestOpR> + "
-                                "digest_compare_kernel)", "bound": "hbm", "achieved": chk_gbps,
-                      "peak": hbm_peak, "unit": "GB/s", "frac": chk_gbps / hbm_peak if hbm_peak else None,
-                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write; this kernel only reads)",
-                      "bytes_per_launch": bytes_per_launch, "mean_launch_ms": statistics.mean(check_ms),
-                      "traffic": trc["traffic_bytes_per_launch"] if trc else None}
+        if check_ms is None:
+            roof_check = {"kernel": "fused into the fetch kernel (hv_swap_blocks_batch_checked: CopyDigestOp digests "
+                                    "every 16 B it moves); see roofline", "separate_launch": False}
+            trc = None
+        else:
+            chk_gbps = bytes_per_launch / (statistics.mean(check_ms) * 1e-3) / 1e9
+            roof_check = {"kernel": "hv_check_digests (digest of every arrival + compare; desc_op_kernel<DigestOpR> + "
+                                    "digest_compare_kernel), beside the copy engine on a side stream",
+                          "bound": "hbm", "achieved": chk_gbps,
+                          "peak": hbm_peak, "unit": "GB/s", "frac": chk_gbps / hbm_peak if hbm_peak else None,
+                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write; this kernel only reads)",
+                          "bytes_per_launch": bytes_per_launch, "mean_launch_ms": statistics.mean(check_ms),
+                          "traffic": trc["traffic_bytes_per_launch"] if trc else None}
         if trc:
             roof_check["traffic_source"] = f"profiles/traffic.json[check_digests] ({trc['report']})"
         try:   # rank-0 local work only (no collectives inside): a failure is reported, never fatal

@@ -85,7 +85,7 @@ def probe_engines_on_peer(node, donor_rank: int, donor_dev: int, dev: int) -> di
     return ok
 
 def autotune(layer_desc, stream, stream_h, F, reps=3, engines=("ldg", "ldg256", "ldg16", "tma", "ce", "auto"),
-             barrier=None, max_over_ranks=None):
+             barrier=None, max_over_ranks=None, checked=None):
     """Time one layer's real fetch (host descriptor arrays, the product's
     hv_swap_blocks_batch entry point) under each engine x grid cap; pick the
     fastest.  "ce" is the copy engine (cudaMemcpyBatchAsync), "auto" the
@@ -93,14 +93,26 @@ def autotune(layer_desc, stream, stream_h, F, reps=3, engines=("ldg", "ldg256", 
     kernel otherwise).  Multi-rank: every rank times the same candidate at the
     same moment (barrier before each), so the measurement includes the
     contention of all readers on the donors' links; a candidate's time is the
-    max over ranks."""
+    max over ranks.  ``checked=(scratch, errors)``: time the fetch with its
+    fused content check (hv_swap_blocks_batch_checked), the product's peer
+    path."""
     import torch
+    from paper_2602_00328_b200 import _native as N
     sp, dp, sz, nb = layer_desc[:4]
     rows = []
+
+    def launch(engine, max_ctas):
+        if checked is None:
+            F.swap_blocks_batch(sp, dp, sz, engine=engine, max_ctas=max_ctas, stream=stream_h)
+        else:
+            ex = layer_desc[4]
+            N.call("hv_swap_blocks_batch_checked", sp.ctypes.data, dp.ctypes.data, sz.ctypes.data, ex.ctypes.data,
+                   len(sp), N.ENGINES[engine], max_ctas, checked[0].data_ptr(), 0, checked[1].data_ptr(), stream_h)
+
     for engine in engines:
         grids = (0,) if engine.split("+")[0] in ("ce", "auto") else (0, 296, 148)
         for max_ctas in grids:
-            F.swap_blocks_batch(sp, dp, sz, engine=engine, max_ctas=max_ctas, stream=stream_h)  # warm
+            launch(engine, max_ctas)  # warm
             stream.synchronize()
             if barrier is not None:
                 barrier()
@@ -108,7 +120,7 @@ def autotune(layer_desc, stream, stream_h, F, reps=3, engines=("ldg", "ldg256", 
             for _ in range(reps):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                F.swap_blocks_batch(sp, dp, sz, engine=engine, max_ctas=max_ctas, stream=stream_h)
+                launch(engine, max_ctas)
                 e1.record(stream)
                 e1.synchronize()
                 ts.append(e0.elapsed_time(e1) * 1e-3)

@@ -300,6 +300,15 @@ int hv_check_digests(const uint64_t* d_src, const uint64_t* d_bytes, const uint6
 int hv_check_digests_batch(const uint64_t* h_src, const uint64_t* h_bytes, const uint64_t* h_expected,
                            uint32_t n, uint64_t* d_scratch, uint8_t* d_flags, uint64_t* d_errors,
                            void* stream);
+/* The fetch and its content check in one pass: hv_swap_blocks_batch's
+ * engine per source, where every object the SM kernel moves is digested by
+ * the same pass that copies it (no re-read, no second kernel), objects the
+ * copy engine moves (large host-tier ones) are digested on the side stream
+ * after their copy, and the digests are compared with h_expected as in
+ * hv_check_digests (flags, *d_errors += mismatches).  d_scratch: n words. */
+int hv_swap_blocks_batch_checked(const uint64_t* h_src, const uint64_t* h_dst, const uint64_t* h_bytes,
+                                 const uint64_t* h_expected, uint32_t n, int engine, int max_ctas,
+                                 uint64_t* d_scratch, uint8_t* d_flags, uint64_t* d_errors, void* stream);
 /* count of 8-byte words differing from the generator, per object */
 int hv_verify_content(const uint64_t* d_src, const uint64_t* d_bytes,
                       const uint64_t* d_seeds, uint32_t n, uint64_t* d_mismatch,

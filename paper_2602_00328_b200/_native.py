@@ -122,6 +122,7 @@ _SIGS = {
     "hv_verify_content": [u64, u64, u64, u32, u64, vp],
     "hv_check_digests": [u64, u64, u64, u32, u64, u64, u64, vp],
     "hv_check_digests_batch": [vp, vp, vp, u32, u64, u64, u64, vp],
+    "hv_swap_blocks_batch_checked": [vp, vp, vp, vp, u32, i32, i32, u64, u64, u64, vp],
     "hv_verify_weights_bf16": [u64, u64, u64, u32, u64, vp],
     "hv_launch_count": [P64],
     "hv_expert_ffn_gate_up": [u64, u64, u64, u64, u64, u64, u32, u32, u32, vp],

@@ -836,6 +836,51 @@ int launch_descs(const uint64_t* d_src, const uint64_t* d_dst, const uint64_t* d
   return HV_OK;
 }
 
+// Copy and content digest in one pass (the fetch and its per-fetch check,
+// moe.py:315-319, fused): every 16 bytes a lane moves are also folded into
+// the object's position-keyed digest, so checking what arrived costs no
+// second read of it and no second kernel competing for the SMs.  The digest
+// equals DigestOp's over the same bytes (objects 8-byte aligned).
+template <int kUnroll>
+struct CopyDigestOp {
+  const uint64_t* bytes;      // object sizes (the size term, as DigestOp)
+  unsigned long long* out;    // per-object digest accumulators (zeroed by the caller)
+  __device__ __forceinline__ void operator()(const ChunkRef& r, uint32_t lane) const {
+    const uint64_t w0 = r.off >> 3;
+    uint64_t acc = 0;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(r.src) | reinterpret_cast<uintptr_t>(r.dst)) & 15) == 0;
+    if (aligned && r.len == (uint32_t)kUnroll * 512u) {
+      uint4 v[kUnroll];
+#pragma unroll
+      for (int j = 0; j < kUnroll; ++j) v[j] = ld_stream(r.src + (j * 32 + lane) * 16);
+#pragma unroll
+      for (int j = 0; j < kUnroll; ++j) {
+        st_stream(r.dst + (j * 32 + lane) * 16, v[j]);
+        const uint64_t i = w0 + (uint64_t)(j * 32 + lane) * 2;
+        acc += digest_term(i, (uint64_t)v[j].x | ((uint64_t)v[j].y << 32));
+        acc += digest_term(i + 1, (uint64_t)v[j].z | ((uint64_t)v[j].w << 32));
+      }
+    } else {
+      copy_chunk_ldg<false, kUnroll>(r, lane);
+      const uint32_t nfull = r.len >> 3;
+      const uint64_t* s = reinterpret_cast<const uint64_t*>(r.src);
+      for (uint32_t k = lane; k < nfull; k += 32) acc += digest_term(w0 + k, s[k]);
+      const uint32_t tail = r.len & 7;
+      if (tail && lane == 0) acc += digest_term(w0 + nfull, load_word_tail(r.src + nfull * 8, tail));
+    }
+    if (r.off == 0 && lane == 0) acc += __ldg(bytes + r.obj);
+    acc = warp_sum(acc);
+    if (lane == 0) atomicAdd(out + r.obj, (unsigned long long)acc);
+  }
+};
+template <int kUnroll>
+struct CopyDigestOpR : CopyDigestOp<kUnroll> {
+  __host__ __device__ void rebase(uint32_t b) {
+    this->bytes += b;
+    this->out += b;
+  }
+};
+
 struct CopyOpR : CopyOp {
   __host__ __device__ void rebase(uint32_t) {}
 };
@@ -1308,6 +1353,149 @@ HV_EXPORT int hv_check_digests_batch(const uint64_t* h_src, const uint64_t* h_by
                                d_errors, stream)))
       return st;
     HV_CUDA(cudaEventRecord(ring->ev[slot], (cudaStream_t)stream));
+    ring->used[slot] = true;
+  }
+  return HV_OK;
+}
+
+HV_EXPORT int hv_swap_blocks_batch_checked(const uint64_t* h_src, const uint64_t* h_dst, const uint64_t* h_bytes,
+                                           const uint64_t* h_expected, uint32_t n, int engine, int max_ctas,
+                                           uint64_t* d_scratch, uint8_t* d_flags, uint64_t* d_errors,
+                                           void* stream) {
+  if (n == 0) return HV_OK;
+  HV_CHECK_ARG(h_src && h_dst && h_bytes && h_expected && d_scratch && d_errors);
+  int dev = 0;
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
+  if (st) return st;
+  cudaStream_t cs = (cudaStream_t)stream;
+  const int base_engine = engine & ~kEngineInterleave;
+  // engine per source, as hv_swap_blocks_batch: large host-tier objects ride
+  // the copy engine on the side stream and are digested there after their
+  // copy; everything else is copied AND digested by one SM kernel pass here
+  std::vector<uint32_t> ce_idx;
+  if ((base_engine == HV_ENGINE_AUTO || base_engine == HV_ENGINE_CE) && !capturing(stream)) {
+    for (uint32_t i = 0; i < n; ++i)
+      if (base_engine == HV_ENGINE_CE ||
+          (h_bytes[i] >= kCeMinBytes && hv::host_range_contains(h_src[i], h_bytes[i])))
+        ce_idx.push_back(i);
+  }
+  const bool deep = base_engine == HV_ENGINE_LDG16;
+  HV_CUDA(cudaMemsetAsync(d_scratch, 0, (size_t)n * 8, cs));
+  std::unique_lock<std::mutex> lk_side(g_side_mu, std::defer_lock);
+  SideStream* ss = nullptr;
+  if (!ce_idx.empty()) {
+    lk_side.lock();
+    if ((st = side_stream(dev, &ss))) return st;
+    HV_CUDA(cudaEventRecord(ss->fork, cs));   // after the scratch reset
+    HV_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+  }
+  std::lock_guard<std::mutex> lk(g_ring_mu);
+  // descriptors per launch: one ring slot of [src m][dst m][bytes m]
+  constexpr uint32_t kM = kSlotDescs;
+  std::vector<char> is_ce(n, 0);
+  for (uint32_t k : ce_idx) is_ce[k] = 1;
+  for (uint32_t base = 0; base < n; base += kM) {
+    const uint32_t m = (n - base) < kM ? (n - base) : kM;
+    uint32_t slot = 0;
+    StagingRing* ring = nullptr;
+    if ((st = ring_acquire(dev, &slot, &ring))) return st;
+    uint64_t* hs = ring->h + (size_t)slot * 3 * kSlotDescs;
+    uint64_t* ds = ring->d + (size_t)slot * 3 * kSlotDescs;
+    // kernel objects keep their sizes; CE objects get size 0 in the kernel's
+    // descriptors (skipped) and their digest from the side-stream pass below
+    memcpy(hs, h_src + base, m * 8);
+    memcpy(hs + m, h_dst + base, m * 8);
+    for (uint32_t i = 0; i < m; ++i) hs[2 * m + i] = is_ce[base + i] ? 0 : h_bytes[base + i];
+    if ((st = upload_desc(hs, ds, (size_t)3 * m, cs))) return st;
+    uint32_t n_kernel = 0;
+    for (uint32_t i = 0; i < m; ++i) n_kernel += !is_ce[base + i];
+    if (n_kernel) {
+      DescResolver res;
+      res.src = ds;
+      res.dst = ds + m;
+      res.bytes = ds + 2 * m;
+      res.n = m;
+      res.interleave = 1u;
+      res.chunk = deep ? kLdgDeepChunk : kLdgChunk;
+      uint64_t total = 0;
+      for (uint32_t i = 0; i < m; ++i) total += is_ce[base + i] ? 0 : h_bytes[base + i];
+      const uint64_t chunks = total / res.chunk + m;
+      const int g = ldg_grid(dev, chunks, max_ctas);
+      unsigned long long* out = reinterpret_cast<unsigned long long*>(d_scratch + base);
+      if (deep) {
+        CopyDigestOpR<kLdgDeepUnroll> op;
+        op.bytes = ds + 2 * m;
+        op.out = out;
+        desc_op_kernel<<<g, kLdgThreads, 0, cs>>>(res, op);
+      } else {
+        CopyDigestOpR<kLdgUnroll> op;
+        op.bytes = ds + 2 * m;
+        op.out = out;
+        desc_op_kernel<<<g, kLdgThreads, 0, cs>>>(res, op);
+      }
+      HV_CUDA(cudaGetLastError());
+      hv::note_launch();
+    }
+    HV_CUDA(cudaEventRecord(ring->ev[slot], cs));
+    ring->used[slot] = true;
+  }
+  if (!ce_idx.empty()) {
+    // side stream: one copy-engine batch, then the digest of what it moved
+    std::vector<void*> cd(ce_idx.size());
+    std::vector<const void*> csrc(ce_idx.size());
+    std::vector<size_t> cz(ce_idx.size());
+    std::vector<uint64_t> dd(ce_idx.size()), dz(ce_idx.size());
+    for (size_t k = 0; k < ce_idx.size(); ++k) {
+      cd[k] = (void*)h_dst[ce_idx[k]];
+      csrc[k] = (const void*)h_src[ce_idx[k]];
+      cz[k] = (size_t)h_bytes[ce_idx[k]];
+    }
+    if ((st = ce_submit(cd.data(), csrc.data(), cz.data(), cd.size(), true, ss->s))) return st;
+    // digest each CE object into its own scratch word: one DigestOp launch
+    // over [dst k][size k] with outputs scattered through a per-object index
+    for (size_t k = 0; k < ce_idx.size(); ++k) {
+      uint32_t slot = 0;
+      StagingRing* ring = nullptr;
+      // contiguous runs of CE indices share a launch
+      size_t e = k;
+      while (e + 1 < ce_idx.size() && ce_idx[e + 1] == ce_idx[e] + 1 && e + 1 - k < kSlotDescs) ++e;
+      const uint32_t m = (uint32_t)(e - k + 1);
+      if ((st = ring_acquire(dev, &slot, &ring))) return st;
+      uint64_t* hs = ring->h + (size_t)slot * 3 * kSlotDescs;
+      uint64_t* ds = ring->d + (size_t)slot * 3 * kSlotDescs;
+      for (uint32_t i = 0; i < m; ++i) {
+        hs[i] = h_dst[ce_idx[k + i]];
+        hs[m + i] = h_bytes[ce_idx[k + i]];
+      }
+      if ((st = upload_desc(hs, ds, (size_t)2 * m, ss->s))) return st;
+      DigestOpR op;
+      op.bytes = ds + m;
+      op.out = reinterpret_cast<unsigned long long*>(d_scratch + ce_idx[k]);
+      if ((st = launch_descs(ds, ds, ds + m, m, HV_ENGINE_LDG, 0, ss->s, op, false))) return st;
+      HV_CUDA(cudaEventRecord(ring->ev[slot], ss->s));
+      ring->used[slot] = true;
+      k = e;
+    }
+    HV_CUDA(cudaEventRecord(ss->join, ss->s));
+    HV_CUDA(cudaStreamWaitEvent(cs, ss->join, 0));
+  }
+  // compare every object's digest with its authoritative one (host array of
+  // expected values lives in the ring slots above; re-stage it contiguously)
+  for (uint32_t base = 0; base < n; base += kSlotDescs * 3) {
+    const uint32_t m = (n - base) < kSlotDescs * 3 ? (n - base) : kSlotDescs * 3;
+    uint32_t slot = 0;
+    StagingRing* ring = nullptr;
+    if ((st = ring_acquire(dev, &slot, &ring))) return st;
+    uint64_t* hs = ring->h + (size_t)slot * 3 * kSlotDescs;
+    uint64_t* ds = ring->d + (size_t)slot * 3 * kSlotDescs;
+    memcpy(hs, h_expected + base, m * 8);
+    if ((st = upload_desc(hs, ds, m, cs))) return st;
+    digest_compare_kernel<<<(m + 255) / 256, 256, 0, cs>>>(d_scratch + base, ds, m, d_flags ? d_flags + base : nullptr,
+                                                          reinterpret_cast<unsigned long long*>(d_errors));
+    HV_CUDA(cudaGetLastError());
+    hv::note_launch();
+    HV_CUDA(cudaEventRecord(ring->ev[slot], cs));
     ring->used[slot] = true;
   }
   return HV_OK;

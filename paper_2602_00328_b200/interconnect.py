@@ -280,6 +280,16 @@ class CudaTransferEngine:
         self.last_event = ev
         return xfers
 
+    def launch_raw_checked(self, src: np.ndarray, dst: np.ndarray, size: np.ndarray, expected: np.ndarray,
+                           d_scratch: int, d_flags: int, d_errors: int, callbacks=()):
+        """launch_raw plus the per-fetch content check fused into the same
+        pass (hv_swap_blocks_batch_checked): the digest of every arrival is
+        compared with ``expected`` and mismatches are added to *d_errors."""
+        n = len(src)
+        N.call("hv_swap_blocks_batch_checked", src.ctypes.data, dst.ctypes.data, size.ctypes.data,
+               expected.ctypes.data, n, self.engine, self.max_ctas, d_scratch, d_flags, d_errors, self.stream)
+        return self.track(callbacks)
+
     def launch_pages(self, src_page_ptrs_dev: int, n_pages: int, page_bytes: int, dst_base: int = 0,
                      dst_page_ptrs_dev: int = 0, callbacks=()):
         """K1 over device-resident page-pointer arrays; one event for the batch."""

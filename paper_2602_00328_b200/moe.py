@@ -294,6 +294,9 @@ class ExpertFetcher:
         self._scratch = torch.zeros(E, dtype=torch.int64, device=f"cuda:{dev}")
         self._flags = torch.zeros(E, dtype=torch.uint8, device=f"cuda:{dev}")
         self._errors = torch.zeros(1, dtype=torch.int64, device=f"cuda:{dev}")
+        self._fscratch = torch.zeros(E, dtype=torch.int64, device=f"cuda:{dev}")   # fused (fetch-stream) path
+        self._fflags = torch.zeros(E, dtype=torch.uint8, device=f"cuda:{dev}")
+        self._last_flags = self._flags
         self._check_events = []
         self.fetches_checked = 0
 
@@ -311,12 +314,14 @@ class ExpertFetcher:
         if self.expected is None:
             raise RuntimeError("content check not enabled (enable_content_check)")
         N.call("hv_stream_synchronize", self._check_stream)
+        self.engine.synchronize()
         return int(self._errors.cpu().item())
 
     def last_read_error_flags(self) -> np.ndarray:
         """Per-object mismatch flags of the most recent checked stage."""
         N.call("hv_stream_synchronize", self._check_stream)
-        return self._flags.cpu().numpy()
+        self.engine.synchronize()
+        return self._last_flags.cpu().numpy()
 
     def _update(self, layer, expert, tier, handle) -> None:
         self.version = getattr(self, "version", 0) + 1
@@ -371,10 +376,21 @@ class ExpertFetcher:
         if n:
             cbs = [lambda _x, b=batch: self.rt.end_reads(b)] if batch else []
             dst = np.ascontiguousarray(dst)
-            self.engine.launch_raw(src, dst, sizes, callbacks=cbs)
-            event = self.engine.last_event
-            if self.expected is not None:
-                event = self._check(layer, ex, dst, sizes, event)
+            if self.expected is not None and peer_mask.any():
+                # peer experts: the SM kernel copies and digests them in one
+                # pass (hv_swap_blocks_batch_checked); host-tier ones ride the
+                # copy engine and are digested after it, inside the same call
+                exp = np.ascontiguousarray(self.expected[layer, ex])
+                self.engine.launch_raw_checked(src, dst, sizes, exp, self._fscratch.data_ptr(),
+                                               self._fflags.data_ptr(), self._errors.data_ptr(), callbacks=cbs)
+                self._last_flags = self._fflags
+                event = self.engine.last_event
+            else:
+                self.engine.launch_raw(src, dst, sizes, callbacks=cbs)
+                event = self.engine.last_event
+                if self.expected is not None:
+                    event = self._check(layer, ex, dst, sizes, event)
+                    self._last_flags = self._flags
         return FetchBatch(layer, ex, t[keep].copy(), event)
 
     def _check(self, layer, ex, dst, sizes, fetch_event):

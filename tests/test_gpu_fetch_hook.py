@@ -265,3 +265,52 @@ def test_k2_phi35_expert_full_size(tier):
     if tier == "pool":
         src_mem.decommit(0, S)
     src_mem.close()
+
+
+@pytest.mark.parametrize("engine", ["auto", "ldg", "ldg16", "ce"])
+def test_fetch_and_check_in_one_pass(engine):
+    """hv_swap_blocks_batch_checked: the SM kernel copies and digests in one
+    pass (copy-engine objects are digested after their copy); bytes equal
+    the oracle's, digests are compared with the oracle's content digest, and
+    a corrupted source is flagged -- exactly one read error, at its index."""
+    from paper_2602_00328_b200 import _native as N
+    from paper_2602_00328_b200 import fetch as F
+    from paper_2602_00328_b200.pool import HostTier
+    sizes = [3 << 20, 65536, 17_301_504, 4096 + 8, (1 << 20) + 16, 8192, 2 << 20]
+    offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.uint64)
+    host = HostTier(sum(sizes))
+    hbm = torch.empty(sum(sizes), dtype=torch.uint8, device="cuda")
+    seeds = [O.stable_hash64("chk", i) for i in range(len(sizes))]
+    for i, (o, sz) in enumerate(zip(offs, sizes)):
+        host.view()[int(o):int(o) + sz] = O.content(seeds[i], sz)
+    F.fill_content(F.ptrs_tensor([hbm.data_ptr() + int(o) for o in offs], "cuda"), F.ptrs_tensor(sizes, "cuda"), seeds)
+    torch.cuda.synchronize()
+    src = np.array([host.device_address(int(o)) if i % 2 == 0 else hbm.data_ptr() + int(o)
+                    for i, o in enumerate(offs)], dtype=np.uint64)
+    out = torch.zeros(sum(sizes), dtype=torch.uint8, device="cuda")
+    dst = np.array([out.data_ptr() + int(o) for o in offs], dtype=np.uint64)
+    sz = np.array(sizes, dtype=np.uint64)
+    exp = np.array([O.content_digest(sd, n) for sd, n in zip(seeds, sizes)], dtype=np.uint64)
+    scratch = torch.zeros(len(sizes), dtype=torch.int64, device="cuda")
+    flags = torch.zeros(len(sizes), dtype=torch.uint8, device="cuda")
+    err = torch.zeros(1, dtype=torch.int64, device="cuda")
+    s = torch.cuda.Stream()
+
+    def run():
+        N.call("hv_swap_blocks_batch_checked", src.ctypes.data, dst.ctypes.data, sz.ctypes.data, exp.ctypes.data,
+               len(sizes), N.ENGINES[engine], 0, scratch.data_ptr(), flags.data_ptr(), err.data_ptr(), s.cuda_stream)
+        s.synchronize()
+
+    run()
+    got = out.cpu().numpy()
+    for i, (o, n) in enumerate(zip(offs, sizes)):
+        assert np.array_equal(got[int(o):int(o) + n], O.content(seeds[i], n)), i
+    assert int(err.item()) == 0 and int(flags.sum().item()) == 0
+    assert [int(x) for x in scratch.cpu().numpy().view(np.uint64)] == [int(x) for x in exp]
+    hbm[int(offs[3]) + 5] ^= 0x40                     # corrupt object 3 (an HBM source) at the source
+    host.view()[int(offs[2]) + 12345] ^= 0x01         # and object 2 (a host-tier source)
+    torch.cuda.synchronize()
+    run()
+    assert int(err.item()) == 2
+    assert list(flags.cpu().numpy()) == [0, 0, 1, 1, 0, 0, 0]
+    host.close()
