@@ -12,9 +12,10 @@ profile (profiles.py:58-64) and ``recompute_time_per_entry`` (a default of
 * ``measure_recompute``: the time to regenerate the KV of ``e`` entries --
   a chunked prefill of ``e`` tokens through every layer of the model's
   dense shape (QKV projection, causal attention over the chunk, output
-  projection, gated MLP; bf16 on cuBLAS / SDPA, random weights), which is
-  what recomputing a lost block costs the serving engine.  Attention over
-  an earlier prefix is not included, so this is a lower bound on recompute.
+  projection, gated MLP; bf16 on cuBLAS / SDPA flash, random weights, one
+  CUDA graph per chunk size), which is what recomputing a lost block costs
+  the serving engine.  Attention over an earlier prefix and launch overhead
+  are not included, so this is a lower bound on recompute.
 
 ``RecomputeCost`` holds the measured curve (entries -> seconds, linear
 interpolation, extrapolated at the measured large-chunk rate), and
@@ -180,26 +181,43 @@ def measure_recompute(shape: DenseShape = LLAMA3_8B_DENSE, chunks=(16, 64, 256, 
             q = qkv[:, :q_out].view(T, shape.q_heads, D).transpose(0, 1)
             k = qkv[:, q_out:q_out + kv_out].view(T, shape.kv_heads, D).transpose(0, 1)
             v = qkv[:, q_out + kv_out:].view(T, shape.kv_heads, D).transpose(0, 1)
-            a = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=rep > 1)
+            if rep > 1:   # grouped-query heads expanded so SDPA takes its fused (flash) kernel
+                k = k.repeat_interleave(rep, dim=0)
+                v = v.repeat_interleave(rep, dim=0)
+            a = torch.nn.functional.scaled_dot_product_attention(q.unsqueeze(0), k.unsqueeze(0), v.unsqueeze(0),
+                                                                 is_causal=True)[0]
             x = x + a.transpose(0, 1).reshape(T, q_out) @ p["o"]
             gu = x @ p["gu"]
             x = x + (torch.nn.functional.silu(gu[:, :I]) * gu[:, I:]) @ p["down"]
         return x
 
+    # device time of the prefill, captured as one CUDA graph per chunk size so
+    # the per-op launch cost of eager PyTorch (~300 ops) does not count: a
+    # lower bound on what recomputing the entries costs a serving engine
     pts = []
     with torch.no_grad():
         for T in chunks:
             x = torch.randn(T, H, device=dev, dtype=torch.bfloat16, generator=g)
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(side):
+                for _ in range(2):
+                    forward(x)
+            torch.cuda.current_stream(dev).wait_stream(side)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                forward(x)
             ts = []
             for i in range(iters + 1):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                forward(x)
+                graph.replay()
                 e1.record()
                 e1.synchronize()
                 if i:
                     ts.append(e0.elapsed_time(e1) * 1e-3)
             pts.append((int(T), float(np.median(ts))))
+            del graph
     del layers
     torch.cuda.empty_cache()
     return RecomputeCost(sorted(pts))
