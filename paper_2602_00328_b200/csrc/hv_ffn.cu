@@ -40,7 +40,10 @@
 //   hv_expert_ffn_gate_up: act[p][i] = silu(gate[i] . x[tok[p]]) * (up[i] . x[tok[p]])
 //   hv_expert_ffn_down:    y[p][h]   = down[h] . act[p]          (fp32)
 // The top-k combine (a fixed-order weighted sum per token) is the caller's.
+#include <cuda.h>
 #include <cuda_bf16.h>
+
+#include <mutex>
 
 #include "hv_common.h"
 
@@ -587,6 +590,273 @@ __global__ void __launch_bounds__(kTThreads, 1) expert_ffn_tma(FfnArgs a, int n_
 
 #endif  // HV_FFN_TMA
 
+// ---------------------------------------------------------------------------
+// 2-D tensor-map TMA weight stream (HV_FFN_TMA2D, default): per stage, one
+// cp.async.bulk.tensor box of 64 rows x 64 columns (8 KiB, 128B-swizzled --
+// exactly the cp.async form's smem layout) per matrix, issued by a producer
+// warp into an mbarrier ring; four consumer warps run ldmatrix + mma.sync.
+// Expert objects sit at arbitrary addresses (donor HBM, host tier, local),
+// so the producer derives each item's tensor map from a per-launch template
+// by replacing its global address (tensormap.replace on a shared-memory
+// copy, then a fenced copy to a per-CTA global slot: the TMA unit reads maps
+// from global memory).  S+1 slots per CTA: a slot is rewritten only after
+// every stage that used it has been consumed.  The activation rows of the
+// stage (the item's routed tokens) are gathered by the producer warp with
+// 16-byte loads into the swizzled x tile and signalled by a second arrival.
+#ifndef HV_FFN_TMA2D
+#define HV_FFN_TMA2D 1
+#endif
+#if HV_FFN_TMA2D
+constexpr int kT2Consumers = 4;
+constexpr int kT2Threads = (kT2Consumers + 1) * 32;
+constexpr int kT2Tile = kRows * kRowBytes;     // 8 KiB: one 64 x 64 bf16 box
+
+template <int NMAT>
+struct T2Smem {
+  static constexpr int kS = NMAT == 2 ? 6 : 8;              // ring stages
+  static constexpr int kStage = (NMAT + 1) * kT2Tile;       // W tiles then the x tile
+  static constexpr int kRing = kS * kStage;                 // 1024-aligned stages
+  static constexpr int kMaps = NMAT * 128;                  // smem staging of the item's maps
+  static constexpr int kBars = 2 * kS * 8;
+  static constexpr int kTotal = kRing + kMaps + kBars + 1024;   // + alignment slack
+  static constexpr int kSlots = kS + 1;                     // global map slots per CTA
+};
+
+__device__ __forceinline__ void t2_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n HV_T2_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra HV_T2_WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+template <int NMAT>
+__global__ void __launch_bounds__(kT2Threads, 1)
+    expert_ffn_tma2d(FfnArgs a, int n_items, const __grid_constant__ CUtensorMap tmpl0,
+                     const __grid_constant__ CUtensorMap tmpl1, CUtensorMap* __restrict__ ws) {
+  extern __shared__ __align__(128) char smem_raw[];
+  using T = T2Smem<NMAT>;
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  char* maps = smem + T::kRing;
+  const uint32_t bars = smem_u32(maps + T::kMaps);   // full[s] at +8s, empty[s] at +8(kS+s)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rb_count = a.rows / kRows;
+  const int ktiles = a.K / kKT;
+  for (int i = tid; i < T::kS * (kT2Tile / 16); i += kT2Threads) {   // x tiles start finite
+    const int st = i / (kT2Tile / 16), o = i % (kT2Tile / 16);
+    *reinterpret_cast<uint4*>(smem + st * T::kStage + NMAT * kT2Tile + o * 16) = make_uint4(0, 0, 0, 0);
+  }
+  if (tid == 0) {
+    for (int st = 0; st < T::kS; ++st) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bars + 8 * st), "r"(2) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bars + 8 * (T::kS + st)), "r"(kT2Consumers)
+                   : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+
+  ItemCursor c{(int)blockIdx.x, 0, 0, 0, 0, nullptr, nullptr};
+  cursor_seek<NMAT>(c, a, rb_count, n_items);
+  auto advance = [&](ItemCursor& cc) {
+    if (++cc.kt == ktiles) {
+      cc.item += gridDim.x;
+      cursor_seek<NMAT>(cc, a, rb_count, n_items);
+    }
+  };
+
+  if (warp == kT2Consumers) {   // ---- producer warp
+    CUtensorMap* my = ws + (size_t)blockIdx.x * T::kSlots * NMAT;
+    uint32_t it = 0, items = 0;
+    const CUtensorMap* gmap[2] = {nullptr, nullptr};
+    while (c.item < n_items) {
+      const int st = it % T::kS;
+      const uint32_t round = it / T::kS;
+      if (round > 0) t2_wait(bars + 8 * (T::kS + st), (round - 1) & 1);
+      if (c.kt == 0) {   // a new item: its matrices' tensor maps
+        const int slot = items % T::kSlots;
+        ++items;
+#pragma unroll
+        for (int m = 0; m < NMAT; ++m) {
+          const uint32_t* src = reinterpret_cast<const uint32_t*>(m == 0 ? &tmpl0 : &tmpl1);
+          reinterpret_cast<uint32_t*>(maps + m * 128)[lane] = src[lane];   // 128 B template
+          __syncwarp();
+          const uint64_t base = reinterpret_cast<uint64_t>(m == 0 ? c.w0 : c.w1) - (uint64_t)c.row0 * a.K * 2;
+          if (lane == 0)
+            asm volatile("tensormap.replace.tile.global_address.shared::cta.b1024.b64 [%0], %1;" ::"r"(
+                             smem_u32(maps + m * 128)),
+                         "l"(base)
+                         : "memory");
+          __syncwarp();
+          CUtensorMap* g = my + slot * NMAT + m;
+          asm volatile(
+              "tensormap.cp_fenceproxy.global.shared::cta.tensormap::generic.release.gpu.sync.aligned [%0], [%1], "
+              "128;" ::"l"(g),
+              "r"(smem_u32(maps + m * 128))
+              : "memory");
+          if (lane == 0)
+            asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(g) : "memory");
+          __syncwarp();
+          gmap[m] = g;
+        }
+      }
+      const uint32_t full = bars + 8 * st;
+      char* base = smem + st * T::kStage;
+      if (lane == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full), "r"(NMAT * kT2Tile)
+                     : "memory");
+#pragma unroll
+        for (int m = 0; m < NMAT; ++m)
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+              "%3}], [%4];" ::"r"(smem_u32(base + m * kT2Tile)),
+              "l"(gmap[m]), "r"(c.kt * kKT), "r"(c.row0), "r"(full)
+              : "memory");
+      }
+      // the stage's activation rows: 8 x 16 B per routed token, swizzled
+      char* xs = base + NMAT * kT2Tile;
+      const size_t kb = (size_t)c.kt * kRowBytes;
+      for (int i = lane; i < c.n * kChunksPerRow; i += 32) {
+        const int r = i / kChunksPerRow, ch = i % kChunksPerRow;
+        const int row = a.tok ? __ldg(a.tok + c.p0 + r) : c.p0 + r;
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(a.x) +
+                                                             (size_t)row * a.K * 2 + kb + ch * 16));
+        *reinterpret_cast<uint4*>(xs + swz(r, ch)) = v;
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(full) : "memory");
+      advance(c);
+      ++it;
+    }
+    return;
+  }
+
+  // ---- consumer warps
+  float acc[NMAT][kGroups][4];
+#pragma unroll
+  for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+    for (int g = 0; g < kGroups; ++g)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[m][g][j] = 0.f;
+  const int a_row = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+  const int a_kc = lane >> 4;
+  const int b_row = lane & 7;
+  const int b_kc = (lane >> 3) & 1;
+  uint32_t it = 0;
+  while (c.item < n_items) {
+    const int st = it % T::kS;
+    t2_wait(bars + 8 * st, (it / T::kS) & 1);
+    const char* base = smem + st * T::kStage;
+    const uint32_t xs = smem_u32(base + NMAT * kT2Tile);
+    const int ng = (c.n + 7) >> 3;
+#pragma unroll
+    for (int kk = 0; kk < kKT / 16; ++kk) {
+      uint32_t af[NMAT][4];
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m)
+        ldsm_x4(smem_u32(base + m * kT2Tile) + swz(a_row, kk * 2 + a_kc), af[m][0], af[m][1], af[m][2], af[m][3]);
+#pragma unroll
+      for (int g = 0; g < kGroups; ++g) {
+        if (g < ng) {
+          uint32_t b0, b1;
+          ldsm_x2(xs + swz(g * 8 + b_row, kk * 2 + b_kc), b0, b1);
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m) mma_bf16(acc[m][g], af[m][0], af[m][1], af[m][2], af[m][3], b0, b1);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bars + 8 * (T::kS + st)) : "memory");
+    if (c.kt == ktiles - 1) {
+      const int r = c.row0 + warp * 16 + (lane >> 2);
+      const int c2 = (lane & 3) * 2;
+#pragma unroll
+      for (int g = 0; g < kGroups; ++g) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int t = g * 8 + c2 + (j & 1);
+          if (g < ng && t < c.n) {
+            const size_t o = (size_t)(c.p0 + t) * a.rows + r + (j >> 1) * 8;
+            if constexpr (NMAT == 2) {
+              const float gv = acc[0][g][j], uv = acc[1][g][j];
+              reinterpret_cast<__nv_bfloat16*>(a.out)[o] = __float2bfloat16_rn(gv / (1.f + __expf(-gv)) * uv);
+            } else {
+              reinterpret_cast<float*>(a.out)[o] = acc[0][g][j];
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m) acc[m][g][j] = 0.f;
+        }
+      }
+    }
+    advance(c);
+    ++it;
+  }
+}
+
+// driver entry point of the tensor-map encoder (the library links cudart
+// statically and resolves driver symbols at run time)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      (void)cudaGetLastError();
+      return (EncodeTiledFn) nullptr;
+    }
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// [rows][K] bf16 matrix, boxes of 64 rows x 64 columns, 128B swizzle
+bool make_tmpl(CUtensorMap* m, void* any_base, int rows, int K) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)kKT, (cuuint32_t)kRows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, any_base, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+std::mutex g_ws_mu;
+CUtensorMap* g_ws[64] = {};
+size_t g_ws_n[64] = {};
+
+CUtensorMap* map_workspace(int dev, size_t n, cudaStream_t s) {
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  if (g_ws_n[dev] >= n) return g_ws[dev];
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    (void)cudaGetLastError();
+    return nullptr;   // cannot allocate under capture: the caller uses the cp.async kernel
+  }
+  CUtensorMap* p = nullptr;
+  if (cudaMalloc(&p, n * sizeof(CUtensorMap)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  if (g_ws[dev]) {
+    cudaDeviceSynchronize();
+    cudaFree(g_ws[dev]);
+  }
+  g_ws[dev] = p;
+  g_ws_n[dev] = n;
+  return p;
+}
+#endif  // HV_FFN_TMA2D
+
 template <int NMAT>
 int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
   if (n_experts == 0) return HV_OK;
@@ -599,6 +869,24 @@ int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
   if (st) return st;
   st = hv::kernel_attr<expert_ffn_kernel<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<NMAT>::kTotal);
   if (st) return st;
+#if HV_FFN_TMA2D
+  {
+    using T = T2Smem<NMAT>;
+    const int n_items = (int)(a.rows / kRows) * (int)n_experts;
+    int g = hv::sm_count(dev);                    // one ~150-200 KiB CTA per SM
+    if (g > n_items) g = n_items;
+    CUtensorMap t0, t1;
+    CUtensorMap* ws = map_workspace(dev, (size_t)hv::sm_count(dev) * T::kSlots * NMAT, (cudaStream_t)stream);
+    if (ws && make_tmpl(&t0, a.out, a.rows, a.K) && make_tmpl(&t1, a.out, a.rows, a.K)) {
+      st = hv::kernel_attr<expert_ffn_tma2d<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kTotal);
+      if (st) return st;
+      expert_ffn_tma2d<NMAT><<<g, kT2Threads, T::kTotal, (cudaStream_t)stream>>>(a, n_items, t0, t1, ws);
+      HV_CUDA(cudaGetLastError());
+      hv::note_launch();
+      return HV_OK;
+    }
+  }
+#endif
 #if HV_FFN_TMA
   if (a.K % kTKT == 0) {
     using T = TSmem<NMAT>;
