@@ -591,7 +591,7 @@ __global__ void __launch_bounds__(kTThreads, 1) expert_ffn_tma(FfnArgs a, int n_
 #endif  // HV_FFN_TMA
 
 // ---------------------------------------------------------------------------
-// 2-D tensor-map TMA weight stream (HV_FFN_TMA2D, default): per stage, one
+// 2-D tensor-map TMA weight stream (HV_FFN_TMA2D=1; measured below): per stage, one
 // cp.async.bulk.tensor box of 64 rows x 64 columns (8 KiB, 128B-swizzled --
 // exactly the cp.async form's smem layout) per matrix, issued by a producer
 // warp into an mbarrier ring; four consumer warps run ldmatrix + mma.sync.
@@ -603,8 +603,22 @@ __global__ void __launch_bounds__(kTThreads, 1) expert_ffn_tma(FfnArgs a, int n_
 // every stage that used it has been consumed.  The activation rows of the
 // stage (the item's routed tokens) are gathered by the producer warp with
 // 16-byte loads into the swizzled x tile and signalled by a second arrival.
+// Measured on B200 (tools/fused_probe.py, experts in HBM, weight GB/s,
+// Qwen stage gate_up / down; Phi-3.5 batch 1 / 16 / 64 whole FFN; r2k, r2l):
+//   one 160-thread CTA per SM, 6/8 stages, x by the producer's loads:
+//     2,202 / 1,515; 1,160 / 1,922 / 1,201   (4 consumer warps per SM cannot
+//     hide ldmatrix + mma latency; ncu: short-scoreboard stalls)
+//   three CTAs per SM, x by cp.async arriving on the stage barrier:
+//     2 stages: 5,229 / 3,447; 1,456 / 4,151 / 4,546
+//     3 stages: 5,213 / 3,450; 1,444 / 4,172 / 4,539
+//     4 stages: 3,952 / 2,614; 1,535 / 3,272 / 3,669
+//   the cp.async persistent form:   5,210 / 4,482; 2,990 / 5,054 / 5,132
+// The tensor-map stream matches cp.async on gate/up and loses on the down
+// projection and at batch 1, where items are short (22 k-tiles) or few and
+// the per-item map rewrite + fence and the single producer per CTA show.
+// So the cp.async form stays the default; HV_FFN_TMA2D=1 builds this one.
 #ifndef HV_FFN_TMA2D
-#define HV_FFN_TMA2D 1
+#define HV_FFN_TMA2D 0
 #endif
 #if HV_FFN_TMA2D
 constexpr int kT2Consumers = 4;
@@ -613,7 +627,10 @@ constexpr int kT2Tile = kRows * kRowBytes;     // 8 KiB: one 64 x 64 bf16 box
 
 template <int NMAT>
 struct T2Smem {
-  static constexpr int kS = NMAT == 2 ? 6 : 8;              // ring stages
+#ifndef HV_FFN_T2_STAGES
+#define HV_FFN_T2_STAGES 3
+#endif
+  static constexpr int kS = NMAT == 2 ? HV_FFN_T2_STAGES : HV_FFN_T2_STAGES + 1;   // ring stages
   static constexpr int kStage = (NMAT + 1) * kT2Tile;       // W tiles then the x tile
   static constexpr int kRing = kS * kStage;                 // 1024-aligned stages
   static constexpr int kMaps = NMAT * 128;                  // smem staging of the item's maps
@@ -632,7 +649,7 @@ __device__ __forceinline__ void t2_wait(uint32_t bar, uint32_t parity) {
 }
 
 template <int NMAT>
-__global__ void __launch_bounds__(kT2Threads, 1)
+__global__ void __launch_bounds__(kT2Threads, 3)
     expert_ffn_tma2d(FfnArgs a, int n_items, const __grid_constant__ CUtensorMap tmpl0,
                      const __grid_constant__ CUtensorMap tmpl1, CUtensorMap* __restrict__ ws) {
   extern __shared__ __align__(128) char smem_raw[];
@@ -649,7 +666,8 @@ __global__ void __launch_bounds__(kT2Threads, 1)
   }
   if (tid == 0) {
     for (int st = 0; st < T::kS; ++st) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bars + 8 * st), "r"(2) : "memory");
+      // full: the producer's expect_tx arrival + one cp.async-completion arrival per producer lane
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bars + 8 * st), "r"(33) : "memory");
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bars + 8 * (T::kS + st)), "r"(kT2Consumers)
                    : "memory");
     }
@@ -715,18 +733,17 @@ __global__ void __launch_bounds__(kT2Threads, 1)
               "l"(gmap[m]), "r"(c.kt * kKT), "r"(c.row0), "r"(full)
               : "memory");
       }
-      // the stage's activation rows: 8 x 16 B per routed token, swizzled
-      char* xs = base + NMAT * kT2Tile;
+      // the stage's activation rows: 8 x 16 B per routed token, swizzled, by
+      // cp.async; each lane's completion arrives on the stage's full barrier,
+      // so the producer never waits for these loads
+      const uint32_t xs = smem_u32(base + NMAT * kT2Tile);
       const size_t kb = (size_t)c.kt * kRowBytes;
       for (int i = lane; i < c.n * kChunksPerRow; i += 32) {
         const int r = i / kChunksPerRow, ch = i % kChunksPerRow;
         const int row = a.tok ? __ldg(a.tok + c.p0 + r) : c.p0 + r;
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(a.x) +
-                                                             (size_t)row * a.K * 2 + kb + ch * 16));
-        *reinterpret_cast<uint4*>(xs + swz(r, ch)) = v;
+        cp_async16(xs + swz(r, ch), reinterpret_cast<const char*>(a.x) + (size_t)row * a.K * 2 + kb + ch * 16);
       }
-      __syncwarp();
-      if (lane == 0) asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(full) : "memory");
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full) : "memory");
       advance(c);
       ++it;
     }
@@ -873,13 +890,20 @@ int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
   {
     using T = T2Smem<NMAT>;
     const int n_items = (int)(a.rows / kRows) * (int)n_experts;
-    int g = hv::sm_count(dev);                    // one ~150-200 KiB CTA per SM
+    st = hv::kernel_attr<expert_ffn_tma2d<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kTotal);
+    if (st) return st;
+    static int resident2[64] = {};   // CTAs per SM (several: the consumer warps of one CTA cannot hide mma latency)
+    if (dev >= 0 && dev < 64 && !resident2[dev]) {
+      int r = 0;
+      HV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, expert_ffn_tma2d<NMAT>, kT2Threads, T::kTotal));
+      resident2[dev] = r > 0 ? r : 1;
+    }
+    const int per_sm = dev >= 0 && dev < 64 ? resident2[dev] : 1;
+    int g = hv::sm_count(dev) * per_sm;
     if (g > n_items) g = n_items;
     CUtensorMap t0, t1;
-    CUtensorMap* ws = map_workspace(dev, (size_t)hv::sm_count(dev) * T::kSlots * NMAT, (cudaStream_t)stream);
+    CUtensorMap* ws = map_workspace(dev, (size_t)hv::sm_count(dev) * per_sm * T::kSlots * NMAT, (cudaStream_t)stream);
     if (ws && make_tmpl(&t0, a.out, a.rows, a.K) && make_tmpl(&t1, a.out, a.rows, a.K)) {
-      st = hv::kernel_attr<expert_ffn_tma2d<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kTotal);
-      if (st) return st;
       expert_ffn_tma2d<NMAT><<<g, kT2Threads, T::kTotal, (cudaStream_t)stream>>>(a, n_items, t0, t1, ws);
       HV_CUDA(cudaGetLastError());
       hv::note_launch();
