@@ -1,7 +1,7 @@
 """Short, ncu-friendly driver: a few launches of each fetch kernel at the
 bench shapes.  Usage: python tools/profile_target.py MODE [engine] [reps]
 MODE: host | hbm | kv | blocks | attn | fused | check (the per-fetch digest
-check of one Qwen stage) | peer | peer_kv (both need 2 GPUs: cuda:1 donates
+check of one Qwen stage) | checked (fetch + check fused, HBM) | peer | peer_kv (both need 2 GPUs: cuda:1 donates
 a VMM pool read by cuda:0 over NVLink; tools/ncu_nvlink.sh captures the
 nvlrx/nvltx byte counters of those launches)."""
 import os
@@ -63,6 +63,20 @@ def main():
         torch.cuda.synchronize(0)
         pool.decommit(0, n * S)
         pool.close()
+    elif what == "checked":   # the fetch with its content check fused (hv_swap_blocks_batch_checked), HBM -> HBM
+        from paper_2602_00328_b200 import _native as N
+        S, n = 17_301_504, 53
+        src = torch.empty(n * S, dtype=torch.uint8, device=dev)
+        dst = torch.empty(n * S, dtype=torch.uint8, device=dev)
+        sp = np.array([src.data_ptr() + i * S for i in range(n)], dtype=np.uint64)
+        dp = np.array([dst.data_ptr() + i * S for i in range(n)], dtype=np.uint64)
+        sz = np.full(n, S, dtype=np.uint64)
+        exp = np.zeros(n, dtype=np.uint64)
+        scratch = torch.zeros(n, dtype=torch.int64, device=dev)
+        err = torch.zeros(1, dtype=torch.int64, device=dev)
+        for _ in range(reps):
+            N.call("hv_swap_blocks_batch_checked", sp.ctypes.data, dp.ctypes.data, sz.ctypes.data, exp.ctypes.data, n,
+                   N.ENGINES[eng], 0, scratch.data_ptr(), 0, err.data_ptr(), 0)
     elif what == "check":   # per-fetch content check (hv_check_digests) of one Qwen stage in HBM
         from paper_2602_00328_b200 import _native as N
         S, n = 17_301_504, 53
