@@ -426,6 +426,17 @@ def run_b200(a):
             roof["traffic"] = None
             roof["traffic_source"] = ("copy engine (cudaMemcpyBatchAsync): not a kernel, no ncu capture; the same "
                                       "bytes through the K2 kernel: profiles/traffic.json[batch_copy_host]")
+        elif source == "peer":
+            # one GPU per gpurun call: no capture of a peer source exists; the
+            # same kernel on an HBM source is the nearest evidence
+            trh = load_traffic().get("checked_hbm_" + str(a.engine).split("+")[0])
+            roof["traffic"] = None
+            roof["traffic_source"] = ("no ncu capture of a peer (NVLink) source on a 1-GPU box; the same fused "
+                                      "fetch+check kernel on an HBM source: " +
+                                      (f"profiles/traffic.json[checked_hbm_{str(a.engine).split('+')[0]}] "
+                                       f"= {trh['traffic_bytes_per_launch']:.0f} B per "
+                                       f"{trh['algorithmic_bytes_per_launch']:.0f} algorithmic" if trh else
+                                       "not captured for this engine"))
         else:
             tr = load_traffic().get("batch_copy_" + source)
             roof["traffic"] = tr["traffic_bytes_per_launch"] if tr else None
