@@ -372,10 +372,17 @@ def run_b200(a):
                                      fused=True)
     except Exception as e:  # report, never lose the line (every rank reaches the same collectives)
         decode["fused"] = {"error": repr(e)[:300]}
+    if source == "host":   # N=1: the host-tier fetch through the copy engine (plan read back per stage)
+        try:
+            decode["host_plan"] = run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source,
+                                             microbatches=1, host_plan=True)
+        except Exception as e:
+            decode["host_plan"] = {"error": repr(e)[:300]}
     # the faster of the measured decode modes (each one bit-identical to its all-local run)
     modes = {"staged": decode.get("tokens_per_s"), "staged_cuda_graph": (decode.get("cuda_graph") or {}).get("tokens_per_s"),
              "fused": decode["fused"].get("tokens_per_s"),
-             "fused_cuda_graph": (decode["fused"].get("cuda_graph") or {}).get("tokens_per_s")}
+             "fused_cuda_graph": (decode["fused"].get("cuda_graph") or {}).get("tokens_per_s"),
+             "staged_host_plan": (decode.get("host_plan") or {}).get("tokens_per_s")}
     modes = {k: v for k, v in modes.items() if v}
     if modes:
         best = max(modes, key=modes.get)

@@ -50,7 +50,8 @@ from .moe import ExpertFetcher
 class MoEDecoder:
     def __init__(self, fetcher: ExpertFetcher, tokens: int, microbatches: int = 1, seed: int = 0,
                  engine: str = "auto", max_ctas: int = 0, router_scale: float = 0.5,
-                 residual_scale: float = 1.0, trace: bool = False, fused: bool = False):
+                 residual_scale: float = 1.0, trace: bool = False, fused: bool = False,
+                 host_plan: bool = False):
         m = fetcher.model
         if not (m.hidden and m.intermediate):
             raise ValueError("model profile needs hidden/intermediate sizes")
@@ -78,7 +79,15 @@ class MoEDecoder:
         # per buffer; expert e goes to slot rank(e) among the active ones
         self.K = min(self.E, (tokens // microbatches) * m.top_k)
         self.fused = fused
-        if fused:
+        # host_plan=True (staged, eager): each stage's fetch plan is read back
+        # to the host once its routing is done and handed to the library's
+        # engine per source, so host-tier experts ride the copy engine
+        # (55.5 GB/s over PCIe where the SM kernel reaches 51.4).  The host
+        # waits for each stage's router -- the stage's fetch cannot start
+        # before it anyway -- so this mode cannot be captured as a graph.
+        self.host_plan = host_plan
+        if host_plan and fused:
+            raise ValueError("host_plan applies to the staged decoder")
             mt = N.c_int_out("hv_expert_ffn_max_tokens")
             if self.tmb > mt:
                 raise ValueError(f"fused decode: at most {mt} tokens per micro-batch")
@@ -115,6 +124,7 @@ class MoEDecoder:
             raise ValueError("an expert has no source address (LOCAL tier needs ExpertFetcher(local_addr=...))")
         if self.fused and np.any(src % 16):
             raise ValueError("fused decode reads experts with 16-byte cp.async: expert objects must be 16-byte aligned")
+        self._addr_host = src.copy()
         return torch.from_numpy(src.view(np.int64).copy()), torch.from_numpy((self.f.tier != 0).copy())
 
     def sync_tables(self) -> None:
@@ -208,8 +218,18 @@ class MoEDecoder:
         if self.trace:
             fs = torch.cuda.Event(enable_timing=True)
             fs.record(self.fetch)
-        N.call("hv_batch_copy", self.addr[layer].data_ptr(), self.dst_ptrs[slot].data_ptr(),
-               self.sizes[slot].data_ptr(), self.E, self.engine_id, self.max_ctas, self.fetch_stream_h)
+        if self.host_plan and not self._capturing:
+            ready.synchronize()                       # this stage's routing (its fetch plan) is done
+            sizes = self.sizes[slot].cpu().numpy().view(np.uint64)
+            act = np.nonzero(sizes)[0]
+            src = np.ascontiguousarray(self._addr_host[layer, act])
+            dst = np.ascontiguousarray(self.dst_ptrs[slot].cpu().numpy().view(np.uint64)[act])
+            sz = np.ascontiguousarray(sizes[act])
+            N.call("hv_swap_blocks_batch", src.ctypes.data, dst.ctypes.data, sz.ctypes.data, len(act),
+                   N.ENGINE_AUTO, self.max_ctas, self.fetch_stream_h)
+        else:
+            N.call("hv_batch_copy", self.addr[layer].data_ptr(), self.dst_ptrs[slot].data_ptr(),
+                   self.sizes[slot].data_ptr(), self.E, self.engine_id, self.max_ctas, self.fetch_stream_h)
         if self.trace:
             fe = torch.cuda.Event(enable_timing=True)
             fe.record(self.fetch)
@@ -277,6 +297,8 @@ class MoEDecoder:
         output tensor returned by step() is reused by the next replay."""
         if self.trace:
             raise ValueError("trace mode records per-launch events; capture without trace")
+        if self.host_plan:
+            raise ValueError("host_plan reads each stage's plan back to the host: it cannot be captured")
         if self._graph is not None:
             return
         self._graph_in = self.x0.clone()

@@ -347,3 +347,33 @@ def test_offload_sweep_every_fraction_equals_all_local(tier, fused):
     if tier == "peer":                      # every peer handle went back to its donor
         assert not sysm.runtime.placement
         assert sysm.runtime.occupied_bytes(1) == 0
+
+
+@pytest.mark.parametrize("microbatches", [1, 2])
+def test_host_plan_decode_equals_device_plan_and_all_local(microbatches):
+    """MoEDecoder(host_plan=True): each stage's plan goes back to the host and
+    through the library's engine per source, so host-tier experts (1.5 MiB
+    here, above the copy-engine threshold) ride the copy engine and peer ones
+    the K2 kernel.  Outputs are bit-identical to the device-plan decoder and
+    to the all-local run."""
+    from paper_2602_00328_b200.decode import MoEDecoder
+    from paper_2602_00328_b200.moe import MoEProfile
+    H, I = 512, 512
+    model = MoEProfile("tiny-moe-ce", num_layers=2, num_experts=8, top_k=2, expert_size=3 * H * I * 2, hidden=H,
+                       intermediate=I)
+    L, E = model.num_layers, model.num_experts
+    sysm, store, res, fetcher, dec = _setup(model, peer_experts=L * E // 2, microbatches=microbatches)
+    hp = MoEDecoder(fetcher, tokens=16, microbatches=microbatches, seed=0, residual_scale=RS, host_plan=True)
+    out = dec.decode(2)
+    out_hp = hp.decode(2)
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int16), out_hp.view(torch.int16))
+    sys2, dec2, _keep = _all_local(model, 16, microbatches, 0, store)
+    out2 = dec2.decode(2)
+    torch.cuda.synchronize()
+    assert torch.equal(out_hp.view(torch.int16), out2.view(torch.int16))
+    with pytest.raises(ValueError):
+        hp.capture_graph()
+    sysm.loop.run()
+    sysm.close()
+    sys2.close()
