@@ -155,3 +155,34 @@ def verify_content(src_ptrs: torch.Tensor, sizes: torch.Tensor, seeds, stream=No
 def ptrs_tensor(ptrs, device) -> torch.Tensor:
     arr = np.asarray(ptrs, dtype=np.uint64).view(np.int64)
     return torch.from_numpy(arr.copy()).to(device)
+
+
+def layer_runs(src_b, src_s, dst_b, dst_s, page: int, n_layers: int, min_run_bytes: int = 1 << 20):
+    """Coalesce a block-table move (page (l, b) from src_b[b] + l*src_s[b] to
+    dst_b[b] + l*dst_s[b]) into contiguous runs: consecutive blocks whose
+    pages follow each other in both the source and the destination, with the
+    same layer strides, form one run per layer.  Returns host arrays
+    (src, dst, bytes) of the per-layer runs, or None when the runs are too
+    short to be worth it (average under ``min_run_bytes``).  Evicted blocks
+    of a sequence usually hold consecutive host slots, so a whole layer of a
+    reload is one run -- which the engine per source then hands to the copy
+    engine (hv_swap_blocks_batch AUTO)."""
+    sb, ss = np.asarray(src_b, dtype=np.uint64), np.asarray(src_s, dtype=np.uint64)
+    db, ds = np.asarray(dst_b, dtype=np.uint64), np.asarray(dst_s, dtype=np.uint64)
+    n = len(sb)
+    if n == 0:
+        return None
+    pg = np.uint64(page)
+    cont = np.ones(n, dtype=bool)
+    cont[0] = False
+    if n > 1:
+        cont[1:] = (sb[1:] == sb[:-1] + pg) & (db[1:] == db[:-1] + pg) & (ss[1:] == ss[:-1]) & (ds[1:] == ds[:-1])
+    starts = np.nonzero(~cont)[0]
+    lengths = np.diff(np.append(starts, n))
+    if lengths.mean() * page < min_run_bytes:
+        return None
+    lay = np.arange(n_layers, dtype=np.uint64)[:, None]
+    src = (sb[starts][None, :] + lay * ss[starts][None, :]).reshape(-1)
+    dst = (db[starts][None, :] + lay * ds[starts][None, :]).reshape(-1)
+    nbytes = np.broadcast_to(lengths.astype(np.uint64) * pg, (n_layers, len(starts))).reshape(-1)
+    return np.ascontiguousarray(src), np.ascontiguousarray(dst), np.ascontiguousarray(nbytes)

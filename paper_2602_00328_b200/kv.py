@@ -36,6 +36,7 @@ import numpy as np
 import torch
 
 from . import _native as N
+from . import fetch as F
 from ._nvtx import annotate
 from .interconnect import LinkSpec, transfer_time
 from .pool import HostTier
@@ -190,6 +191,9 @@ class KVCacheManager:
         # blocks = 2 GiB, ~2.7 ms over NVLink: far above launch cost, while
         # the host resolves the next chunk)
         self.launch_chunk_blocks = 1024
+        # block moves whose blocks are consecutive in source and destination go
+        # out as per-layer runs through the engine per source (F.layer_runs)
+        self.coalesce = True
         self.recomputed = 0
         self.stats = {"evict_peer": 0, "evict_host": 0, "reload_peer": 0, "reload_host": 0, "recompute": 0}
 
@@ -215,6 +219,31 @@ class KVCacheManager:
         if n == 0:
             if on_done:
                 on_done()
+            return
+        runs = F.layer_runs(src_b, src_s, dst_b, dst_s, self.page, self.L) if self.coalesce else None
+        if runs is not None:
+            # consecutive slots (a sequence evicted together): a few long
+            # per-layer runs through the engine per source -- the copy engine
+            # when they come from the pinned host tier
+            batch = self.rt.begin_reads(list(handles)) if handles else None
+
+            def _done_runs(_x, batch=batch):
+                if batch is not None:
+                    self.rt.end_reads(batch)
+                if on_done:
+                    on_done()
+
+            timing = getattr(self, "timing", None)
+            if timing is not None:
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ev0.record(torch.cuda.ExternalStream(self.stream, device=self.dev))
+            src, dst, nbytes = runs
+            N.call("hv_swap_blocks_batch", src.ctypes.data, dst.ctypes.data, nbytes.ctypes.data, len(src),
+                   self.engine, self.max_ctas, self.stream)
+            if timing is not None:
+                ev1.record(torch.cuda.ExternalStream(self.stream, device=self.dev))
+                timing.append((ev0, ev1, int(nbytes.sum())))
+            self.sys.engine.track([_done_runs])
             return
         arrs = np.concatenate([np.asarray(x, dtype=np.uint64) for x in (src_b, src_s, dst_b, dst_s)])
         pinned = torch.from_numpy(arrs.view(np.int64)).pin_memory()

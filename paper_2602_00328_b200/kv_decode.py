@@ -122,10 +122,27 @@ class KVAttentionDecoder:
         bases, strides, handles = self.kv.page_table(self.ids)
         if np.any(bases % 16) or np.any(strides % 16):
             raise ValueError("paged attention reads 16-byte granules: KV pages must be 16-byte aligned")
+        self._tab_host = (np.asarray(bases, dtype=np.uint64), np.asarray(strides, dtype=np.uint64))
+        self._runs = {}
         tab = torch.from_numpy(np.stack([bases, strides]).view(np.int64)).pin_memory()
         self._tab_dev.copy_(tab, non_blocking=True)
         self._tab_version, self._tab_handles = ver, handles
         return handles
+
+    def _gather_runs(self, layer: int):
+        """The layer's gather as contiguous runs (host arrays: source, offset in
+        the gather buffer, bytes), or None when the pages are scattered; cached
+        per uploaded table."""
+        if not getattr(self, "coalesce", True) or getattr(self, "_tab_host", None) is None:
+            return None
+        if layer not in self._runs:
+            bases, strides = self._tab_host
+            n = len(bases)
+            off = np.arange(n, dtype=np.uint64) * np.uint64(self.page)
+            r = F.layer_runs(bases + np.uint64(layer) * strides, np.zeros(n, dtype=np.uint64), off,
+                             np.zeros(n, dtype=np.uint64), self.page, 1)
+            self._runs[layer] = r
+        return self._runs[layer]
 
     def _attend(self, layer: int, pages: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
         """hv_paged_decode_attention over the page table `pages` [n] (int64)
@@ -184,8 +201,18 @@ class KVAttentionDecoder:
                     f0 = torch.cuda.Event(enable_timing=True)
                     f0.record(self.fetch)
                     self._tr[layer] = {"fetch": (f0, None)}
-                F.kv_gather(src[layer], self.page, dst=self.bufs[b], engine=self.engine, max_ctas=self.max_ctas,
-                            stream=self.fetch_h)
+                runs = None if torch.cuda.is_current_stream_capturing() else self._gather_runs(layer)
+                if runs is not None:
+                    # the layer's pages lie in a few long contiguous runs (a
+                    # sequence evicted together): the engine per source moves
+                    # them -- the copy engine from the pinned host tier
+                    rs, roff, rbytes = runs
+                    rd = roff + np.uint64(self.bufs[b].data_ptr())
+                    N.call("hv_swap_blocks_batch", rs.ctypes.data, rd.ctypes.data, rbytes.ctypes.data, len(rs),
+                           N.ENGINE_AUTO, self.max_ctas, self.fetch_h)
+                else:
+                    F.kv_gather(src[layer], self.page, dst=self.bufs[b], engine=self.engine, max_ctas=self.max_ctas,
+                                stream=self.fetch_h)
                 got[layer] = torch.cuda.Event(enable_timing=timed_ev or self.trace)
                 got[layer].record(self.fetch)
                 if self.trace:

@@ -83,3 +83,30 @@ def test_kv_manager_uses_the_measured_costs():
         assert kv.resolve_fallback(b) == want
     b = KVBlock(0, 0, 0, 16, Durability.LOSSY, KVTier.NOT_MATERIALIZED)
     assert kv.resolve_fallback(b) == "Recompute"
+
+
+def test_layer_runs_coalesces_consecutive_blocks():
+    """F.layer_runs: consecutive blocks contiguous in source and destination
+    (same layer strides) become one run per layer; a break starts a new run;
+    short average runs are left to the per-page kernel (None)."""
+    import numpy as np
+    from paper_2602_00328_b200 import fetch as F
+    page, L = 4096, 3
+    sb = [1000 * page + i * page for i in range(6)] + [5000 * page + i * page for i in range(4)]
+    db = [i * page for i in range(10)]
+    ss, ds = [64 * page] * 10, [16 * page] * 10
+    src, dst, nb = F.layer_runs(sb, ss, db, ds, page, L, min_run_bytes=4 * page)
+    assert len(src) == L * 2
+    want = []
+    for l in range(L):
+        want += [(1000 * page + l * 64 * page, l * 16 * page, 6 * page),
+                 (5000 * page + l * 64 * page, 6 * page + l * 16 * page, 4 * page)]
+    assert sorted(zip(src.tolist(), dst.tolist(), nb.tolist())) == sorted(want)
+    # every page is covered exactly once
+    assert int(nb.sum()) == 10 * L * page
+    assert F.layer_runs(sb, ss, db, ds, page, L, min_run_bytes=1 << 20) is None
+    # a stride change breaks a run even when the bases are contiguous
+    ss2 = list(ss)
+    ss2[3] = 32 * page
+    src2, _, nb2 = F.layer_runs(sb, ss2, db, ds, page, L, min_run_bytes=page)
+    assert len(src2) == L * 4 and int(nb2.sum()) == 10 * L * page
