@@ -533,7 +533,9 @@ class KVCacheManager:
         # see blocks that are already local, never the ones being reloaded
         limit = int(self.policy.local_watermark * self.local_blocks)
         if n and len(self.local_free) >= n and self._local_used() + n <= limit:
-            slots = self.local_free[-n:][::-1]          # bulk: no eviction needed
+            # bulk: no eviction needed; ascending slots keep consecutive
+            # blocks contiguous in the cache, so the move coalesces into runs
+            slots = sorted(self.local_free[-n:])
             del self.local_free[-n:]
         else:
             slots = [self._take_local_slot() for _ in need]
