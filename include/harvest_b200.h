@@ -173,8 +173,9 @@ int hv_stream_wait_event(void* stream, void* event);
 /* engine selector for hv_batch_copy / hv_kv_gather */
 #define HV_ENGINE_AUTO 0   /* LDG; variable-size copies also take HV_ENGINE_FLAG_INTERLEAVE.
                               hv_swap_blocks_batch: engine per source -- objects of >= 1 MiB read
-                              from the pinned host tier (hv_host_alloc / hv_host_register ranges)
-                              go to the copy engine, the rest to the LDG kernel, concurrently */
+                              from or written to the pinned host tier (hv_host_alloc /
+                              hv_host_register ranges) go to the copy engine, the rest to the LDG
+                              kernel, concurrently */
 #define HV_ENGINE_LDG 1  /* SM-issued 128-bit ld.global.nc / st.global, warp per 4 KiB chunk */
 #define HV_ENGINE_TMA 2  /* cp.async.bulk global->smem->global ring, one issuing lane per CTA */
 #define HV_ENGINE_LDG256 3 /* LDG with the L2::256B sector-promotion hint (larger remote reads) */

@@ -311,3 +311,41 @@ def test_fallback_on_measured_costs():
     ht.close()
     kv.close()
     sysm.close()
+
+
+def test_evict_reload_as_coalesced_runs_bit_exact():
+    """Blocks evicted together hold consecutive host slots, so evict and
+    reload go out as per-layer runs (F.layer_runs) through the engine per
+    source -- the copy engine to and from the pinned host tier once a run
+    reaches 1 MiB.  64 KiB pages (Llama-3-8B geometry, 2 layers), 48 blocks:
+    3 MiB runs.  Every page equals the oracle's before, after the evict (read
+    from the host copy) and after the reload."""
+    from paper_2602_00328_b200 import fetch as F
+    from paper_2602_00328_b200.kv import KVCacheManager, KVModelSpec, KVTier
+    from paper_2602_00328_b200.runtime import Durability
+    from paper_2602_00328_b200.system import HarvestSystem
+    m = KVModelSpec("runs", num_layers=2, kv_heads=8, head_dim=128)
+    assert m.page_bytes == 65536
+    sysm = HarvestSystem(0, host_bytes=1, local_bytes=1)
+    kv = KVCacheManager(sysm, m, local_blocks=64, host_blocks=64, slab_blocks=8, durability=Durability.BACKED)
+    kv.append_kv(0, 16 * 48)
+    ids = list(kv.seq_blocks[0])
+    bases, strides, _h = kv.page_table(ids)
+    n = len(ids)
+    runs = F.layer_runs(bases, strides, np.arange(n, dtype=np.uint64) * np.uint64(m.page_bytes),
+                        np.zeros(n, dtype=np.uint64), m.page_bytes, m.num_layers)
+    assert runs is not None and len(runs[0]) == m.num_layers   # one run per layer in the cache
+    _check_all(kv, m)
+    kv.evict(48 * m.block_bytes)
+    assert all(kv.table[b].tier == KVTier.HOST_DRAM for b in ids)
+    slots = [kv.table[b].host_slot for b in ids]
+    assert slots == sorted(slots) and slots[-1] - slots[0] == 47   # consecutive host slots
+    _check_all(kv, m)
+    kv.reload(ids)
+    kv.sys.engine.synchronize()
+    assert all(kv.table[b].tier == KVTier.LOCAL_HBM for b in ids)
+    local = [kv.table[b].slot for b in ids]
+    assert local == sorted(local)                            # ascending slots: coalescible
+    _check_all(kv, m)
+    kv.close()
+    sysm.close()
