@@ -217,6 +217,14 @@ int hv_kv_gather_blocks(const uint64_t* d_src_base, const uint64_t* d_src_stride
                         uint32_t n_blocks, uint32_t n_layers, uint64_t page_bytes,
                         int engine, int max_ctas, void* stream);
 
+/* hv_kv_gather_blocks with host arrays: staged through the library's pinned
+ * ring and uploaded by an SM kernel (never a DMA queued behind bulk
+ * copy-engine traffic), one launch per 1,536 blocks. */
+int hv_kv_gather_blocks_h(const uint64_t* h_src_base, const uint64_t* h_src_stride,
+                          const uint64_t* h_dst_base, const uint64_t* h_dst_stride,
+                          uint32_t n_blocks, uint32_t n_layers, uint64_t page_bytes,
+                          int engine, int max_ctas, void* stream);
+
 /* K2: variable-size batched fetch (expert weights, placement copy-in):
  * d_src[i] -> d_dst[i], d_bytes[i] bytes, for i < n.  One launch for a whole
  * pipeline stage (moe.py:282-313). */

@@ -113,6 +113,7 @@ _SIGS = {
     "hv_kv_gather": [u64, u64, u64, u32, u64, i32, i32, vp],
     "hv_kv_gather_table": [u64, u64, u64, u64, u32, u64, i32, i32, vp],
     "hv_kv_gather_blocks": [u64, u64, u64, u64, u32, u32, u64, i32, i32, vp],
+    "hv_kv_gather_blocks_h": [vp, vp, vp, vp, u32, u32, u64, i32, i32, vp],
     "hv_batch_copy": [u64, u64, u64, u32, i32, i32, vp],
     "hv_swap_blocks_batch": [vp, vp, vp, u32, i32, i32, vp],
     "hv_ce_batch_copy": [vp, vp, vp, u32, i32, vp],

@@ -1333,6 +1333,44 @@ HV_EXPORT int hv_check_digests(const uint64_t* d_src, const uint64_t* d_bytes, c
   return HV_OK;
 }
 
+HV_EXPORT int hv_kv_gather_blocks_h(const uint64_t* h_src_base, const uint64_t* h_src_stride,
+                                    const uint64_t* h_dst_base, const uint64_t* h_dst_stride, uint32_t n_blocks,
+                                    uint32_t n_layers, uint64_t page_bytes, int engine, int max_ctas, void* stream) {
+  if (n_blocks == 0) return HV_OK;
+  HV_CHECK_ARG(h_src_base && h_src_stride && h_dst_base && h_dst_stride);
+  int dev = 0;
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
+  if (st) return st;
+  std::lock_guard<std::mutex> lk(g_ring_mu);
+  constexpr uint32_t kM = kSlotDescs * 3 / 4;   // four words per block in one ring slot
+  for (uint32_t base = 0; base < n_blocks; base += kM) {
+    const uint32_t m = (n_blocks - base) < kM ? (n_blocks - base) : kM;
+    uint32_t slot = 0;
+    StagingRing* ring = nullptr;
+    if ((st = ring_acquire(dev, &slot, &ring))) return st;
+    uint64_t* hs = ring->h + (size_t)slot * 3 * kSlotDescs;
+    uint64_t* ds = ring->d + (size_t)slot * 3 * kSlotDescs;
+    memcpy(hs, h_src_base + base, m * 8);
+    memcpy(hs + m, h_src_stride + base, m * 8);
+    memcpy(hs + 2 * m, h_dst_base + base, m * 8);
+    memcpy(hs + 3 * m, h_dst_stride + base, m * 8);
+    if ((st = upload_desc(hs, ds, (size_t)4 * m, (cudaStream_t)stream))) return st;
+    BlockResolver r{};
+    r.src_base = ds;
+    r.src_stride = ds + m;
+    r.dst_base = ds + 2 * m;
+    r.dst_stride = ds + 3 * m;
+    r.page_bytes = page_bytes;
+    r.n_blocks = m;
+    r.n_layers = n_layers;
+    if ((st = launch_blocks(r, engine, max_ctas, stream))) return st;
+    HV_CUDA(cudaEventRecord(ring->ev[slot], (cudaStream_t)stream));
+    ring->used[slot] = true;
+  }
+  return HV_OK;
+}
+
 HV_EXPORT int hv_check_digests_batch(const uint64_t* h_src, const uint64_t* h_bytes, const uint64_t* h_expected,
                                      uint32_t n, uint64_t* d_scratch, uint8_t* d_flags, uint64_t* d_errors,
                                      void* stream) {

@@ -245,15 +245,10 @@ class KVCacheManager:
                 timing.append((ev0, ev1, int(nbytes.sum())))
             self.sys.engine.track([_done_runs])
             return
-        arrs = np.concatenate([np.asarray(x, dtype=np.uint64) for x in (src_b, src_s, dst_b, dst_s)])
-        pinned = torch.from_numpy(arrs.view(np.int64)).pin_memory()
-        # allocated in the fetch stream's pool: the first writer is that stream
-        with torch.cuda.stream(torch.cuda.ExternalStream(self.stream, device=self.dev)):
-            dbuf = torch.empty(pinned.numel(), dtype=torch.int64, device=self.dev)
-        N.call("hv_memcpy_h2d", dbuf.data_ptr(), pinned.data_ptr(), pinned.numel() * 8, self.stream)
+        arrs = [np.ascontiguousarray(x, dtype=np.uint64) for x in (src_b, src_s, dst_b, dst_s)]
         batch = self.rt.begin_reads(list(handles)) if handles else None
 
-        def _done(_x, batch=batch, keep=(pinned, dbuf)):
+        def _done(_x, batch=batch):
             if batch is not None:
                 self.rt.end_reads(batch)
             if on_done:
@@ -263,9 +258,10 @@ class KVCacheManager:
         if timing is not None:  # kernel-only time of this launch, on the fetch stream
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record(torch.cuda.ExternalStream(self.stream, device=self.dev))
-        p = dbuf.data_ptr()
-        N.call("hv_kv_gather_blocks", p, p + 8 * n, p + 16 * n, p + 24 * n, n, self.L, self.page,
-               self.engine, self.max_ctas, self.stream)
+        # the four per-block arrays go through the library's pinned ring (an SM
+        # kernel uploads them: no DMA queued behind copy-engine traffic)
+        N.call("hv_kv_gather_blocks_h", arrs[0].ctypes.data, arrs[1].ctypes.data, arrs[2].ctypes.data,
+               arrs[3].ctypes.data, n, self.L, self.page, self.engine, self.max_ctas, self.stream)
         self.sys.engine.track([_done])
         if timing is not None:
             ev1.record(torch.cuda.ExternalStream(self.stream, device=self.dev))

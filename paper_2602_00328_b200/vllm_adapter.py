@@ -264,16 +264,10 @@ class HarvestPeerHandler(OffloadingHandler):
             # one K1 launch over the block table: page (l, b) at base[b] + l*stride[b]
             gb, gs = gpu_pages[0], np.full(nb, self.layer_stride, dtype=np.uint64)
             pb, ps = peer_pages[0], np.full(nb, self.pool.layer_stride, dtype=np.uint64)
-            sb, ss, db, ds = (gb, gs, pb, ps) if kind[0] == "GPU" else (pb, ps, gb, gs)
-            arrs = np.concatenate([sb, ss, db, ds])
-            pinned = torch.from_numpy(arrs.view(np.int64)).pin_memory()
-            with torch.cuda.stream(torch.cuda.ExternalStream(self.stream, device=self.dev)):   # the writer's pool
-                dbuf = torch.empty(pinned.numel(), dtype=torch.int64, device=self.dev)
-            N.call("hv_memcpy_h2d", dbuf.data_ptr(), pinned.data_ptr(), pinned.numel() * 8, self.stream)
-            p = dbuf.data_ptr()
-            N.call("hv_kv_gather_blocks", p, p + 8 * nb, p + 16 * nb, p + 24 * nb, nb, self.L, self.page,
-                   self.sys.engine.engine, self.sys.engine.max_ctas, self.stream)
-            keep = (pinned, dbuf)
+            sb, ss, db, ds = [np.ascontiguousarray(x, dtype=np.uint64)
+                              for x in ((gb, gs, pb, ps) if kind[0] == "GPU" else (pb, ps, gb, gs))]
+            N.call("hv_kv_gather_blocks_h", sb.ctypes.data, ss.ctypes.data, db.ctypes.data, ds.ctypes.data, nb,
+                   self.L, self.page, self.sys.engine.engine, self.sys.engine.max_ctas, self.stream)
         else:
             # general layout: one launch over every page (per-page pointers and sizes)
             src_p, dst_p = (gpu_pages, peer_pages) if kind[0] == "GPU" else (peer_pages, gpu_pages)
