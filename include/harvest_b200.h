@@ -283,6 +283,20 @@ int hv_paged_decode_attention(const uint64_t* d_page_ptrs, const int32_t* d_seq_
                               uint32_t batch, uint32_t q_heads, uint32_t kv_heads, uint32_t head_dim,
                               uint32_t block_tokens, uint32_t splits, float scale, void* stream);
 
+/* hv_paged_decode_attention with flags.  HV_ATTN_OVERLAP_PREVIOUS launches
+ * the kernel with programmatic stream serialization: its CTAs start while
+ * the previous kernel on the stream drains, read pages / q / the sequence
+ * arrays, and wait for that kernel only before their first write.  The
+ * caller guarantees those inputs were not produced by the immediately
+ * preceding kernel on the stream (true for the layers of a decode step:
+ * the previous kernel is the previous layer's attention). */
+#define HV_ATTN_OVERLAP_PREVIOUS 1u
+int hv_paged_decode_attention_ex(const uint64_t* d_page_ptrs, const int32_t* d_seq_start,
+                                 const int32_t* d_seq_tokens, const void* d_q, float* d_out, float* d_part,
+                                 uint32_t batch, uint32_t q_heads, uint32_t kv_heads, uint32_t head_dim,
+                                 uint32_t block_tokens, uint32_t splits, float scale, unsigned flags,
+                                 void* stream);
+
 /* ---- synthetic content (test / bench inputs) --------------------------- */
 /* byte j of object = byte (j%8) (little-endian) of splitmix64 word j/8:
  *   w_i = fmix(seed + (i+1)*0x9E3779B97F4A7C15)

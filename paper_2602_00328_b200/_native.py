@@ -34,6 +34,7 @@ POOL_VMM = 0
 POOL_IPC = 1
 POOL_EAGER = 2
 POOL_REMOTE = 4
+ATTN_OVERLAP_PREVIOUS = 1        # HV_ATTN_OVERLAP_PREVIOUS: programmatic dependent launch of K5
 
 
 class HarvestNativeError(RuntimeError):
@@ -130,6 +131,8 @@ _SIGS = {
     "hv_expert_ffn_down": [u64, u64, u64, u64, u64, u32, u32, u32, vp],
     "hv_expert_ffn_max_tokens": [C.POINTER(i32)],
     "hv_paged_decode_attention": [u64, u64, u64, u64, u64, u64, u32, u32, u32, u32, u32, u32, C.c_float, vp],
+    "hv_paged_decode_attention_ex": [u64, u64, u64, u64, u64, u64, u32, u32, u32, u32, u32, u32, C.c_float,
+                                     C.c_uint, vp],
 }
 _RESTYPES = {"hv_error_string": C.c_char_p}
 

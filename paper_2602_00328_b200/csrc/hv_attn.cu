@@ -343,6 +343,9 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_mma(
   __shared__ float s_m[kAttnWarps][G], s_l[kAttnWarps][G];
   __shared__ float s_acc[kAttnWarps][G][D];
   const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  // let the next kernel on the stream (the next layer's attention, launched
+  // with HV_ATTN_OVERLAP_PREVIOUS) start its CTAs as ours drain
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int q_heads = kvh * G;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gr = lane >> 2, c = lane & 3;        // mma fragment row group / column pair
@@ -449,6 +452,10 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_mma(
     __syncwarp();
   }
   cp_wait_n<0>();
+  // programmatic dependent launch (HV_ATTN_OVERLAP_PREVIOUS): everything above
+  // read only inputs the caller vouched for; the writes below (partials, the
+  // merge counters, the output) wait for the previous kernel on the stream
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // merge the warps (fixed order) and write the partial state
   if (gr < G) {
     if (c == 0) {
@@ -573,7 +580,8 @@ unsigned* done_counters(int dev, size_t need, cudaStream_t s) {
 
 template <int D, int G>
 int launch_attn(const uint64_t* pages, const int32_t* seq_start, const int32_t* seq_tokens, const void* q,
-                float* out, float* part, uint32_t B, uint32_t kvh, uint32_t splits, float scale, cudaStream_t s) {
+                float* out, float* part, uint32_t B, uint32_t kvh, uint32_t splits, float scale, cudaStream_t s,
+                unsigned flags) {
   dim3 grid(splits, kvh, B);
   int dev = 0;   // made current by the caller (bind_stream_device)
   HV_CUDA(cudaGetDevice(&dev));
@@ -585,9 +593,18 @@ int launch_attn(const uint64_t* pages, const int32_t* seq_start, const int32_t* 
     st = hv::kernel_attr<paged_decode_mma<D, G, kS>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (st) return st;
     unsigned* done = HV_ATTN_FUSED_COMBINE ? done_counters(dev, (size_t)B * kvh, s) : nullptr;
-    paged_decode_mma<D, G, kS><<<grid, kAttnWarps * 32, smem, s>>>(
-        pages, seq_start, seq_tokens, reinterpret_cast<const __half*>(q), part, (int)kvh, (int)splits, scale, out,
-        done);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kAttnWarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (flags & HV_ATTN_OVERLAP_PREVIOUS) ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HV_CUDA(cudaLaunchKernelEx(&cfg, paged_decode_mma<D, G, kS>, pages, seq_start, seq_tokens,
+                               reinterpret_cast<const __half*>(q), part, (int)kvh, (int)splits, scale, out, done));
     if (done) {
       HV_CUDA(cudaGetLastError());
       hv::note_launch(1);
@@ -612,22 +629,23 @@ int launch_attn(const uint64_t* pages, const int32_t* seq_start, const int32_t* 
 template <int D>
 int launch_attn_g(uint32_t g, const uint64_t* pages, const int32_t* seq_start, const int32_t* seq_tokens,
                   const void* q, float* out, float* part, uint32_t B, uint32_t kvh, uint32_t splits, float scale,
-                  cudaStream_t s) {
+                  cudaStream_t s, unsigned flags) {
   switch (g) {
-    case 1: return launch_attn<D, 1>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s);
-    case 2: return launch_attn<D, 2>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s);
-    case 4: return launch_attn<D, 4>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s);
-    case 8: return launch_attn<D, 8>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s);
+    case 1: return launch_attn<D, 1>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s, flags);
+    case 2: return launch_attn<D, 2>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s, flags);
+    case 4: return launch_attn<D, 4>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s, flags);
+    case 8: return launch_attn<D, 8>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s, flags);
     default: return HV_E_INVALID;
   }
 }
 
 }  // namespace
 
-HV_EXPORT int hv_paged_decode_attention(const uint64_t* d_page_ptrs, const int32_t* d_seq_start,
-                                        const int32_t* d_seq_tokens, const void* d_q, float* d_out, float* d_part,
-                                        uint32_t batch, uint32_t q_heads, uint32_t kv_heads, uint32_t head_dim,
-                                        uint32_t block_tokens, uint32_t splits, float scale, void* stream) {
+HV_EXPORT int hv_paged_decode_attention_ex(const uint64_t* d_page_ptrs, const int32_t* d_seq_start,
+                                           const int32_t* d_seq_tokens, const void* d_q, float* d_out,
+                                           float* d_part, uint32_t batch, uint32_t q_heads, uint32_t kv_heads,
+                                           uint32_t head_dim, uint32_t block_tokens, uint32_t splits, float scale,
+                                           unsigned flags, void* stream) {
   if (batch == 0) return HV_OK;
   HV_CHECK_ARG(d_page_ptrs && d_seq_start && d_seq_tokens && d_q && d_out && d_part);
   HV_CHECK_ARG(kv_heads > 0 && q_heads % kv_heads == 0);
@@ -638,6 +656,7 @@ HV_EXPORT int hv_paged_decode_attention(const uint64_t* d_page_ptrs, const int32
   HV_CHECK_ARG(head_dim == 64 || head_dim == 128);
   HV_CHECK_ARG(block_tokens == (uint32_t)kBlockTok);
   HV_CHECK_ARG(splits >= 1 && splits <= 1024 && batch <= 65535u && kv_heads <= 65535u);
+  HV_CHECK_ARG((flags & ~(unsigned)HV_ATTN_OVERLAP_PREVIOUS) == 0);
   int dev = 0;
   hv::DeviceGuard dg;
   int st = hv::bind_stream_device(stream, &dev, dg);
@@ -646,7 +665,15 @@ HV_EXPORT int hv_paged_decode_attention(const uint64_t* d_page_ptrs, const int32
   const uint32_t g = q_heads / kv_heads;
   if (head_dim == 128)
     return launch_attn_g<128>(g, d_page_ptrs, d_seq_start, d_seq_tokens, d_q, d_out, d_part, batch, kv_heads, splits,
-                              scale, s);
+                              scale, s, flags);
   return launch_attn_g<64>(g, d_page_ptrs, d_seq_start, d_seq_tokens, d_q, d_out, d_part, batch, kv_heads, splits,
-                           scale, s);
+                           scale, s, flags);
+}
+
+HV_EXPORT int hv_paged_decode_attention(const uint64_t* d_page_ptrs, const int32_t* d_seq_start,
+                                        const int32_t* d_seq_tokens, const void* d_q, float* d_out, float* d_part,
+                                        uint32_t batch, uint32_t q_heads, uint32_t kv_heads, uint32_t head_dim,
+                                        uint32_t block_tokens, uint32_t splits, float scale, void* stream) {
+  return hv_paged_decode_attention_ex(d_page_ptrs, d_seq_start, d_seq_tokens, d_q, d_out, d_part, batch, q_heads,
+                                      kv_heads, head_dim, block_tokens, splits, scale, 0u, stream);
 }

@@ -47,6 +47,7 @@ class KVAttentionDecoder:
     # gather-mode issue policy (see _run); class-level so probes can A/B them
     issue_ahead = True      # issue K1 of layer l+1 before K5 of layer l
     timed_events = True     # timing-enabled stream events in eager steps
+    overlap_layers = True   # K5 of layer l+1 starts as K5 of layer l drains (HV_ATTN_OVERLAP_PREVIOUS)
 
     def __init__(self, kv, sequences, q_heads: int, tokens: int | None = None, seed: int = 0,
                  engine: str | None = None, max_ctas: int | None = None, trace: bool = False,
@@ -148,9 +149,14 @@ class KVAttentionDecoder:
         """hv_paged_decode_attention over the page table `pages` [n] (int64)
         into `out` [B, Hq, D] (fp32, contiguous)."""
         m = self.m
-        N.call("hv_paged_decode_attention", pages.data_ptr(), self.seq_start.data_ptr(), self.seq_tokens.data_ptr(),
-               self.q[layer].data_ptr(), out.data_ptr(), self.part.data_ptr(), self.B, self.Hq, m.kv_heads,
-               m.head_dim, m.block_tokens, self.splits, self.scale, torch.cuda.current_stream(self.dev).cuda_stream)
+        # the layers' attention kernels follow each other on the compute
+        # stream and read only the step's static inputs: each one may start
+        # while the previous layer's drains (programmatic dependent launch)
+        flags = N.ATTN_OVERLAP_PREVIOUS if (self.overlap_layers and layer > 0) else 0
+        N.call("hv_paged_decode_attention_ex", pages.data_ptr(), self.seq_start.data_ptr(),
+               self.seq_tokens.data_ptr(), self.q[layer].data_ptr(), out.data_ptr(), self.part.data_ptr(), self.B,
+               self.Hq, m.kv_heads, m.head_dim, m.block_tokens, self.splits, self.scale, flags,
+               torch.cuda.current_stream(self.dev).cuda_stream)
         return out
 
     def _run(self) -> torch.Tensor:

@@ -60,6 +60,9 @@ def case(batch, ctx):
 
 
 if __name__ == "__main__":
-    print(json.dumps({"config1_4x4k": case(4, 4096), "context_128k": case(1, 131072),
+    if "--no-overlap" in sys.argv:   # A/B of the programmatic dependent launch of K5 across layers
+        KVAttentionDecoder.overlap_layers = False
+    print(json.dumps({"overlap_layers": KVAttentionDecoder.overlap_layers,
+                      "config1_4x4k": case(4, 4096), "context_128k": case(1, 131072),
                       "note": "self-donor VMM pool: the peer tier is this GPU's HBM; outputs of every mode "
                               "bit-identical to the all-local run"}, indent=1))
