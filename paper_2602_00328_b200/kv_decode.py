@@ -149,10 +149,14 @@ class KVAttentionDecoder:
         """hv_paged_decode_attention over the page table `pages` [n] (int64)
         into `out` [B, Hq, D] (fp32, contiguous)."""
         m = self.m
-        # the layers' attention kernels follow each other on the compute
-        # stream and read only the step's static inputs: each one may start
-        # while the previous layer's drains (programmatic dependent launch)
-        flags = N.ATTN_OVERLAP_PREVIOUS if (self.overlap_layers and layer > 0) else 0
+        # in place, the layers' attention kernels follow each other on the
+        # compute stream and read only the step's static inputs: each one may
+        # start while the previous layer's drains (programmatic dependent
+        # launch).  Measured (tools/kv_decode_probe.py, r2u, CUDA graph):
+        # 4 x 4k 10,299 vs 6,658 tok/s, 128k 402 vs 337.  In gather mode an
+        # early attention CTA would hold SMs the next K1 gather needs (graph:
+        # 1,791 vs 3,235 tok/s), so there it stays off.
+        flags = N.ATTN_OVERLAP_PREVIOUS if (self.overlap_layers and self.fused and layer > 0) else 0
         N.call("hv_paged_decode_attention_ex", pages.data_ptr(), self.seq_start.data_ptr(),
                self.seq_tokens.data_ptr(), self.q[layer].data_ptr(), out.data_ptr(), self.part.data_ptr(), self.B,
                self.Hq, m.kv_heads, m.head_dim, m.block_tokens, self.splits, self.scale, flags,
