@@ -874,6 +874,218 @@ CUtensorMap* map_workspace(int dev, size_t n, cudaStream_t s) {
 }
 #endif  // HV_FFN_TMA2D
 
+// ---------------------------------------------------------------------------
+// Dynamically scheduled persistent form (HV_FFN_DYNAMIC, default).  The
+// static walk above hands CTA c the items c, c+G, c+2G...; with 1,792 down
+// items over 444 CTAs some CTAs get 5 items and others 4, so the slowest SM
+// carries ~24% more bytes than the mean.  Here every CTA claims its next
+// item from a global counter (atomicAdd) the moment its loader starts the
+// current one, so SMs that finish early take more: the makespan is the mean
+// plus at most one item.  Claimed item ids pass from the loader to the
+// compute side of the same CTA through a small shared-memory FIFO (the loader
+// runs up to S-1 stages, hence S-1 items, ahead).
+#ifndef HV_FFN_DYNAMIC
+#define HV_FFN_DYNAMIC 1
+#endif
+#if HV_FFN_DYNAMIC
+constexpr int kFifo = 16;
+
+struct ItemInfo {
+  int n, p0, row0;
+  const char* w0;
+  const char* w1;
+};
+
+__device__ __forceinline__ ItemInfo item_info(const FfnArgs& a, int item, int rb_count) {
+  const int e = item / rb_count;
+  const int n = a.counts[e];
+  ItemInfo it;
+  it.n = n < kMaxTok ? n : kMaxTok;
+  it.p0 = a.offs[e];
+  it.row0 = (item - e * rb_count) * kRows;
+  const char* obj = reinterpret_cast<const char*>(a.w_addr[e]);
+  it.w0 = obj + a.w_off0 + (size_t)it.row0 * a.K * 2;
+  it.w1 = obj + a.w_off1 + (size_t)it.row0 * a.K * 2;
+  return it;
+}
+
+// next item with routed tokens (or n_items when none is left); thread 0 only
+__device__ __forceinline__ int claim_item(const FfnArgs& a, unsigned* counter, int rb_count, int n_items) {
+  int id;
+  do {
+    id = (int)atomicAdd(counter, 1u);
+  } while (id < n_items && a.counts[id / rb_count] <= 0);
+  return id < n_items ? id : n_items;
+}
+
+template <int NMAT>
+__global__ void __launch_bounds__(kThreads) expert_ffn_dynamic(FfnArgs a, int n_items, unsigned* counter) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ int s_claim[2];      // the next claimed item, double-buffered by the loader's item parity
+  __shared__ int s_fifo[kFifo];   // items in the order the loader started them
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rb_count = a.rows / kRows;
+  const int ktiles = a.K / kKT;
+  const size_t wstride = (size_t)a.K * 2, xstride = (size_t)a.K * 2;
+  for (int i = tid; i < Smem<NMAT>::kS * Smem<NMAT>::kX / 16; i += kThreads) {
+    const int s = i / (Smem<NMAT>::kX / 16), o = i % (Smem<NMAT>::kX / 16);
+    *reinterpret_cast<uint4*>(smem + s * Smem<NMAT>::kStage + Smem<NMAT>::kW + o * 16) = make_uint4(0, 0, 0, 0);
+  }
+  if (tid == 0) s_claim[0] = claim_item(a, counter, rb_count, n_items);
+  __syncthreads();
+
+  // loader cursor (all threads, in lockstep)
+  int ld_cnt = 0, ld_kt = 0, ld_item;
+  ItemInfo ld;
+  auto ld_start = [&]() {   // begin the next claimed item (call between barriers)
+    ld_item = s_claim[ld_cnt & 1];
+    if (tid == 0) {
+      s_fifo[ld_cnt % kFifo] = ld_item;
+      if (ld_item < n_items) s_claim[(ld_cnt + 1) & 1] = claim_item(a, counter, rb_count, n_items);
+    }
+    ++ld_cnt;
+    ld_kt = 0;
+    if (ld_item < n_items) ld = item_info(a, ld_item, rb_count);
+  };
+  auto load_stage = [&](int s) {
+    char* base = smem + s * Smem<NMAT>::kStage;
+    const size_t kb = (size_t)ld_kt * kRowBytes;
+#pragma unroll
+    for (int m = 0; m < NMAT; ++m) {
+      const uint32_t ws = smem_u32(base + m * kRows * kRowBytes);
+      const char* src = m == 0 ? ld.w0 : ld.w1;
+#pragma unroll 4
+      for (int i = tid; i < kRows * kChunksPerRow; i += kThreads) {
+        const int r = i / kChunksPerRow, ch = i % kChunksPerRow;
+        cp_async16(ws + swz(r, ch), src + r * wstride + kb + ch * 16);
+      }
+    }
+    const uint32_t xs = smem_u32(base + Smem<NMAT>::kW);
+    for (int i = tid; i < ld.n * kChunksPerRow; i += kThreads) {
+      const int r = i / kChunksPerRow, ch = i % kChunksPerRow;
+      const int row = a.tok ? a.tok[ld.p0 + r] : ld.p0 + r;
+      cp_async16(xs + swz(r, ch), reinterpret_cast<const char*>(a.x) + row * xstride + kb + ch * 16);
+    }
+  };
+  auto ld_advance = [&]() {   // after a stage was issued; the next item's id was claimed a stage ago
+    if (++ld_kt == ktiles) {
+      __syncthreads();          // thread 0's claim of the next item is visible
+      ld_start();
+    }
+  };
+
+  float acc[NMAT][kGroups][4];
+#pragma unroll
+  for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+    for (int g = 0; g < kGroups; ++g)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[m][g][j] = 0.f;
+
+  ld_start();
+#pragma unroll
+  for (int s = 0; s < Smem<NMAT>::kS - 1; ++s) {
+    if (ld_item < n_items) {
+      load_stage(s);
+      ld_advance();
+    }
+    cp_commit();
+  }
+  const int a_row = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+  const int a_kc = lane >> 4;
+  const int b_row = lane & 7;
+  const int b_kc = (lane >> 3) & 1;
+  int stage = 0, lstage = Smem<NMAT>::kS - 1;
+  // compute cursor
+  int cs_cnt = 0, cs_kt = 0;
+  __syncthreads();
+  int cs_item = s_fifo[0];
+  ItemInfo cs = cs_item < n_items ? item_info(a, cs_item, rb_count) : ItemInfo{};
+  ++cs_cnt;
+  while (cs_item < n_items) {
+    cp_wait<Smem<NMAT>::kS - 2>();
+    __syncthreads();
+    if (ld_item < n_items) {
+      load_stage(lstage);
+      ld_advance();
+    }
+    cp_commit();
+    lstage = lstage + 1 == Smem<NMAT>::kS ? 0 : lstage + 1;
+    const char* base = smem + stage * Smem<NMAT>::kStage;
+    const uint32_t xs = smem_u32(base + Smem<NMAT>::kW);
+    const int ng = (cs.n + 7) >> 3;
+#pragma unroll
+    for (int kk = 0; kk < kKT / 16; ++kk) {
+      uint32_t af[NMAT][4];
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m)
+        ldsm_x4(smem_u32(base + m * kRows * kRowBytes) + swz(a_row, kk * 2 + a_kc), af[m][0], af[m][1], af[m][2],
+                af[m][3]);
+#pragma unroll
+      for (int g = 0; g < kGroups; ++g) {
+        if (g < ng) {
+          uint32_t b0, b1;
+          ldsm_x2(xs + swz(g * 8 + b_row, kk * 2 + b_kc), b0, b1);
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m) mma_bf16(acc[m][g], af[m][0], af[m][1], af[m][2], af[m][3], b0, b1);
+        }
+      }
+    }
+    stage = stage + 1 == Smem<NMAT>::kS ? 0 : stage + 1;
+    if (cs_kt == ktiles - 1) {  // item complete: epilogue
+      const int r = cs.row0 + warp * 16 + (lane >> 2);
+      const int c2 = (lane & 3) * 2;
+#pragma unroll
+      for (int g = 0; g < kGroups; ++g) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int t = g * 8 + c2 + (j & 1);
+          if (g < ng && t < cs.n) {
+            const size_t o = (size_t)(cs.p0 + t) * a.rows + r + (j >> 1) * 8;
+            if constexpr (NMAT == 2) {
+              const float gv = acc[0][g][j], uv = acc[1][g][j];
+              reinterpret_cast<__nv_bfloat16*>(a.out)[o] = __float2bfloat16_rn(gv / (1.f + __expf(-gv)) * uv);
+            } else {
+              reinterpret_cast<float*>(a.out)[o] = acc[0][g][j];
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m) acc[m][g][j] = 0.f;
+        }
+      }
+    }
+    if (++cs_kt == ktiles) {    // the loader started (and recorded) this next item stages ago
+      cs_kt = 0;
+      cs_item = s_fifo[cs_cnt % kFifo];
+      ++cs_cnt;
+      if (cs_item < n_items) cs = item_info(a, cs_item, rb_count);
+    }
+  }
+  cp_wait<0>();
+}
+
+std::mutex g_ctr_mu;
+unsigned* g_ctr[64] = {};
+
+unsigned* item_counter(int dev, cudaStream_t s) {
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(g_ctr_mu);
+  if (g_ctr[dev]) return g_ctr[dev];
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  unsigned* p = nullptr;
+  if (cudaMalloc(&p, 2 * sizeof(unsigned)) != cudaSuccess) {   // one counter per kernel of a stage
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  g_ctr[dev] = p;
+  return p;
+}
+#endif  // HV_FFN_DYNAMIC
+
 template <int NMAT>
 int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
   if (n_experts == 0) return HV_OK;
@@ -923,6 +1135,32 @@ int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
     HV_CUDA(cudaGetLastError());
     hv::note_launch();
     return HV_OK;
+  }
+#endif
+#if HV_FFN_DYNAMIC
+  {
+    unsigned* ctr = item_counter(dev, (cudaStream_t)stream);
+    if (ctr) {
+      ctr += NMAT == 2 ? 0 : 1;
+      static int resident_d[64] = {};
+      if (dev >= 0 && dev < 64 && !resident_d[dev]) {
+        int r = 0;
+        st = hv::kernel_attr<expert_ffn_dynamic<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       Smem<NMAT>::kTotal);
+        if (st) return st;
+        HV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, expert_ffn_dynamic<NMAT>, kThreads,
+                                                              Smem<NMAT>::kTotal));
+        resident_d[dev] = r > 0 ? r : 1;
+      }
+      const int n_items = (int)(a.rows / kRows) * (int)n_experts;
+      int g = hv::sm_count(dev) * (dev >= 0 && dev < 64 ? resident_d[dev] : 1);
+      if (g > n_items) g = n_items;
+      HV_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), (cudaStream_t)stream));
+      expert_ffn_dynamic<NMAT><<<g, kThreads, Smem<NMAT>::kTotal, (cudaStream_t)stream>>>(a, n_items, ctr);
+      HV_CUDA(cudaGetLastError());
+      hv::note_launch();
+      return HV_OK;
+    }
   }
 #endif
 #if HV_FFN_PERSISTENT
