@@ -875,7 +875,7 @@ CUtensorMap* map_workspace(int dev, size_t n, cudaStream_t s) {
 #endif  // HV_FFN_TMA2D
 
 // ---------------------------------------------------------------------------
-// Dynamically scheduled persistent form (HV_FFN_DYNAMIC, default).  The
+// Dynamically scheduled persistent form (HV_FFN_DYNAMIC=1; measured below).  The
 // static walk above hands CTA c the items c, c+G, c+2G...; with 1,792 down
 // items over 444 CTAs some CTAs get 5 items and others 4, so the slowest SM
 // carries ~24% more bytes than the mean.  Here every CTA claims its next
@@ -884,8 +884,14 @@ CUtensorMap* map_workspace(int dev, size_t n, cudaStream_t s) {
 // plus at most one item.  Claimed item ids pass from the loader to the
 // compute side of the same CTA through a small shared-memory FIFO (the loader
 // runs up to S-1 stages, hence S-1 items, ahead).
+// Measured (tools/fused_probe.py, HBM, weight GB/s, gpurun r2w): Qwen stage
+// gate_up / down 5,093 / 4,391 against the static walk's 5,195 / 4,470;
+// Phi-3.5 batch 1 / 16 / 64 whole FFN 1,481 / 4,704 / 4,939 vs 2,990 /
+// 4,973 / 5,201 -- the item imbalance is not what holds the down projection
+// back, and at batch 1 (2 active experts of 16) the claims that skip empty
+// experts cost more than they balance.  Built with HV_FFN_DYNAMIC=1 only.
 #ifndef HV_FFN_DYNAMIC
-#define HV_FFN_DYNAMIC 1
+#define HV_FFN_DYNAMIC 0
 #endif
 #if HV_FFN_DYNAMIC
 constexpr int kFifo = 16;
