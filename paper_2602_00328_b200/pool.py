@@ -285,6 +285,8 @@ class DonorServer:
             conn.close()
 
     def close(self):
+        """Stop serving; chunks still lent (a reader that never said goodbye)
+        are released here, so the donor always gets its HBM back."""
         self._stop = True
         try:
             self._srv.close()
@@ -293,6 +295,9 @@ class DonorServer:
                 _os.unlink(self.path)
             except FileNotFoundError:
                 pass
+            with self._lock:
+                for key in list(self._held):
+                    self._release(key)
 
 
 class RemotePool:
