@@ -314,3 +314,42 @@ def test_fetch_and_check_in_one_pass(engine):
     assert int(err.item()) == 2
     assert list(flags.cpu().numpy()) == [0, 0, 1, 1, 0, 0, 0]
     host.close()
+
+
+def test_checked_fetch_many_ragged_objects():
+    """hv_swap_blocks_batch_checked over 3,000 objects (two ring slots of
+    descriptors), ragged and zero sizes, scattered destinations: bytes and
+    digests equal the oracle's; read_errors 0."""
+    from paper_2602_00328_b200 import _native as N
+    rng = np.random.default_rng(9)
+    n = 3000
+    sizes = rng.integers(0, 9000, n).astype(np.int64)
+    sizes[::97] = 0
+    offs = np.concatenate([[0], np.cumsum((sizes + 15) // 16 * 16)[:-1]]).astype(np.uint64)
+    total = int(offs[-1] + sizes[-1] + 16)
+    src_buf = torch.empty(total, dtype=torch.uint8, device="cuda")
+    seeds = [O.stable_hash64("many", i) for i in range(n)]
+    from paper_2602_00328_b200 import fetch as F
+    F.fill_content(F.ptrs_tensor([src_buf.data_ptr() + int(o) for o in offs], "cuda"),
+                   F.ptrs_tensor(sizes.tolist(), "cuda"), seeds)
+    perm = rng.permutation(n)
+    dst_buf = torch.zeros(total, dtype=torch.uint8, device="cuda")
+    src = np.array([src_buf.data_ptr() + int(o) for o in offs], dtype=np.uint64)
+    dst = np.array([dst_buf.data_ptr() + int(offs[p]) for p in perm], dtype=np.uint64)   # scattered
+    sz = sizes.astype(np.uint64)
+    # object i lands where object perm[i] started; sizes must fit: use the max slot
+    fit = np.array([sizes[i] <= (int(offs[perm[i] + 1]) - int(offs[perm[i]]) if perm[i] + 1 < n else 1 << 30)
+                    for i in range(n)])
+    sz = np.where(fit, sz, 0).astype(np.uint64)
+    exp = np.array([O.content_digest(seeds[i], int(sz[i])) for i in range(n)], dtype=np.uint64)
+    scratch = torch.zeros(n, dtype=torch.int64, device="cuda")
+    flags = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    err = torch.zeros(1, dtype=torch.int64, device="cuda")
+    N.call("hv_swap_blocks_batch_checked", src.ctypes.data, dst.ctypes.data, sz.ctypes.data, exp.ctypes.data, n,
+           N.ENGINES["ldg"], 0, scratch.data_ptr(), flags.data_ptr(), err.data_ptr(), 0)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0 and int(flags.sum().item()) == 0
+    got = dst_buf.cpu().numpy()
+    for i in rng.choice(n, 200, replace=False):
+        d = int(dst[i]) - dst_buf.data_ptr()
+        assert np.array_equal(got[d:d + int(sz[i])], O.content(seeds[i], int(sz[i]))), i
