@@ -334,8 +334,12 @@ class RemotePool:
         self._lock = _threading.Lock()
 
     def _map(self, ci: int) -> None:
-        _send_msg(self._sock, {"op": "create", "chunk": int(ci)})
-        reply, fds = _recv_msg(self._sock, want_fds=True)
+        try:
+            _send_msg(self._sock, {"op": "create", "chunk": int(ci)})
+            reply, fds = _recv_msg(self._sock, want_fds=True)
+        except (OSError, ConnectionError, ValueError) as e:
+            # the donor process is gone: to the runtime this is NoCapacity
+            raise N.HarvestNativeError(N.HV_E_NOCAPACITY, f"donor unreachable: {e!r}") from e
         try:
             if not reply.get("ok"):
                 raise N.HarvestNativeError(N.HV_E_NOCAPACITY, f"donor refused chunk {ci}: {reply.get('error')}")
@@ -346,8 +350,11 @@ class RemotePool:
 
     def _unmap(self, ci: int) -> None:
         N.call("hv_pool_unmap_chunk", self._p, int(ci))
-        _send_msg(self._sock, {"op": "release", "chunk": int(ci)})
-        _recv_msg(self._sock)
+        try:
+            _send_msg(self._sock, {"op": "release", "chunk": int(ci)})
+            _recv_msg(self._sock)
+        except (OSError, ConnectionError, ValueError):
+            pass   # donor gone: its handle died with it; ours is released above
 
     def commit(self, offset: int, nbytes: int) -> None:
         if nbytes == 0:
