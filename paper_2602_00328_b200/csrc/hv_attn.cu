@@ -31,7 +31,9 @@
 #include <cuda_fp16.h>
 #include <math.h>
 
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "hv_common.h"
 
@@ -542,22 +544,32 @@ __global__ void paged_decode_combine(const float* __restrict__ part, float* __re
 #define HV_ATTN_RING 3   // stages of the scalar kernel, built only with HV_ATTN_MMA=0
 #endif
 
-// Per-device arrival counters of the fused combine (one per sequence x KV
-// head), zero between launches.  Grown only outside CUDA-graph capture; a
-// launch that finds them too small while capturing uses the two-kernel path.
+// Arrival counters of the fused combine (one per sequence x KV head), zero
+// between launches, one buffer per (device, stream): launches on one stream
+// are ordered (with HV_ATTN_OVERLAP_PREVIOUS a kernel touches the counters
+// only after griddepcontrol.wait), while kernels on different streams may run
+// at once and must not share them.  Allocated outside CUDA-graph capture
+// only; a launch that finds none while capturing (or beyond kMaxStreams
+// streams) uses the two-kernel path.
+struct DoneBuf {
+  unsigned* p = nullptr;
+  size_t cap = 0;
+};
 std::mutex g_done_mu;
-unsigned* g_done[64] = {};
-size_t g_done_cap[64] = {};
+std::map<std::pair<int, cudaStream_t>, DoneBuf> g_done;
+constexpr size_t kMaxStreams = 256;
 
 unsigned* done_counters(int dev, size_t need, cudaStream_t s) {
-  if (dev < 0 || dev >= 64) return nullptr;
   std::lock_guard<std::mutex> lk(g_done_mu);
-  if (g_done_cap[dev] >= need) return g_done[dev];
+  auto key = std::make_pair(dev, s);
+  auto it = g_done.find(key);
+  if (it != g_done.end() && it->second.cap >= need) return it->second.p;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
     (void)cudaGetLastError();
     return nullptr;
   }
+  if (it == g_done.end() && g_done.size() >= kMaxStreams) return nullptr;
   size_t cap_n = need < 4096 ? 4096 : need;
   unsigned* p = nullptr;
   if (cudaMalloc(&p, cap_n * sizeof(unsigned)) != cudaSuccess || cudaMemset(p, 0, cap_n * sizeof(unsigned)) != cudaSuccess) {
@@ -565,12 +577,11 @@ unsigned* done_counters(int dev, size_t need, cudaStream_t s) {
     if (p) cudaFree(p);
     return nullptr;
   }
-  if (g_done[dev]) {   // no launch can still use the old buffer: wait for the device before freeing it
-    cudaDeviceSynchronize();
-    cudaFree(g_done[dev]);
+  if (it != g_done.end() && it->second.p) {   // grown: no launch can still use the old buffer once the stream is idle
+    cudaStreamSynchronize(s);
+    cudaFree(it->second.p);
   }
-  g_done[dev] = p;
-  g_done_cap[dev] = cap_n;
+  g_done[key] = DoneBuf{p, cap_n};
   return p;
 }
 
