@@ -572,7 +572,10 @@ unsigned* done_counters(int dev, size_t need, cudaStream_t s) {
   if (it == g_done.end() && g_done.size() >= kMaxStreams) return nullptr;
   size_t cap_n = need < 4096 ? 4096 : need;
   unsigned* p = nullptr;
-  if (cudaMalloc(&p, cap_n * sizeof(unsigned)) != cudaSuccess || cudaMemset(p, 0, cap_n * sizeof(unsigned)) != cudaSuccess) {
+  // zeroed on the launching stream: ordered before this launch whatever the
+  // stream's flags (a legacy-stream memset does not order non-blocking streams)
+  if (cudaMalloc(&p, cap_n * sizeof(unsigned)) != cudaSuccess ||
+      cudaMemsetAsync(p, 0, cap_n * sizeof(unsigned), s) != cudaSuccess) {
     (void)cudaGetLastError();
     if (p) cudaFree(p);
     return nullptr;
