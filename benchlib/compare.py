@@ -70,14 +70,17 @@ def probe_engines_on_peer(node, donor_rank: int, donor_dev: int, dev: int) -> di
     # only the bulk-copy (TMA) engine is proven out of process
     ok = {"ldg": True, "ldg256": True, "ldg16": True}
     remote = node.mode == "remote"
-    own = node._readers[node.layout.donors_of(node.rank).index(donor_rank)]
+    try:
+        own = node._readers[node.layout.donors_of(node.rank).index(donor_rank)]
+    except (IndexError, ValueError):
+        return {**ok, "tma": False}
     for engine in ("tma",):
-        code = PROBE_CHILD.format(repo=REPO, mode=node.mode, path=_socket_path("main", donor_rank),
-                                  handle="" if remote else node.ipc_handles[donor_rank].hex(),
-                                  donor=donor_dev, nbytes=node.layout.slab_bytes(donor_rank),
-                                  chunk=getattr(own, "chunk_bytes", 32 << 20) if remote else 4 << 20,
-                                  dev=dev, engine=engine)
-        try:
+        try:   # any failure here (even building the child's script) only rules the engine out
+            code = PROBE_CHILD.format(repo=REPO, mode=node.mode, path=_socket_path("main", donor_rank),
+                                      handle="" if remote else node.ipc_handles[donor_rank].hex(),
+                                      donor=donor_dev, nbytes=node.layout.slab_bytes(donor_rank),
+                                      chunk=getattr(own, "chunk_bytes", 32 << 20) if remote else 4 << 20,
+                                      dev=dev, engine=engine)
             r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=180)
             ok[engine] = r.returncode == 0 and '"ok": true' in r.stdout
         except Exception:
