@@ -64,6 +64,9 @@ constexpr int kRows = 16 * kWarps;   // weight rows per CTA (16 per warp: one mm
 #ifndef HV_FFN_STAGES
 #define HV_FFN_STAGES 3
 #endif
+#ifndef HV_FFN_DOWN_PAIR
+#define HV_FFN_DOWN_PAIR 1
+#endif
 constexpr int kKT = HV_FFN_KT;       // k columns per pipeline stage (64: 128 B per row)
 constexpr int kRowBytes = kKT * 2;
 constexpr int kChunksPerRow = kRowBytes / 16;
@@ -88,6 +91,7 @@ struct FfnArgs {
   void* out;                // NMAT=2: bf16 [P][rows]; NMAT=1: fp32 [P][rows]
   uint64_t w_off0, w_off1;  // byte offsets of the matrices inside the object
   int rows, K;
+  int pair;                 // down projection as a pair of row blocks (NMAT=2 kernel, fp32 out, no SiLU)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -259,7 +263,7 @@ __device__ __forceinline__ void cursor_seek(ItemCursor& c, const FfnArgs& a, int
     if (n > 0) {
       c.n = n < kMaxTok ? n : kMaxTok;
       c.p0 = a.offs[e];
-      c.row0 = (c.item - e * rb_count) * kRows;
+      c.row0 = (c.item - e * rb_count) * kRows * (a.pair ? 2 : 1);
       const char* obj = reinterpret_cast<const char*>(a.w_addr[e]);
       c.w0 = obj + a.w_off0 + (size_t)c.row0 * a.K * 2;
       c.w1 = obj + a.w_off1 + (size_t)c.row0 * a.K * 2;
@@ -274,7 +278,7 @@ template <int NMAT>
 __global__ void __launch_bounds__(kThreads) expert_ffn_persistent(FfnArgs a, int n_items) {
   extern __shared__ __align__(128) char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int rb_count = a.rows / kRows;
+  const int rb_count = a.rows / (kRows * (a.pair ? 2 : 1));
   const int ktiles = a.K / kKT;
   const size_t wstride = (size_t)a.K * 2, xstride = (size_t)a.K * 2;
   // every activation row of every stage starts finite; later stale rows are
@@ -377,8 +381,13 @@ __global__ void __launch_bounds__(kThreads) expert_ffn_persistent(FfnArgs a, int
           if (g < ng && t < cs.n) {
             const size_t o = (size_t)(cs.p0 + t) * a.rows + r + (j >> 1) * 8;
             if constexpr (NMAT == 2) {
-              const float gv = acc[0][g][j], uv = acc[1][g][j];
-              reinterpret_cast<__nv_bfloat16*>(a.out)[o] = __float2bfloat16_rn(gv / (1.f + __expf(-gv)) * uv);
+              if (a.pair) {   // down, two row blocks: rows r and r + 64, fp32
+                reinterpret_cast<float*>(a.out)[o] = acc[0][g][j];
+                reinterpret_cast<float*>(a.out)[o + kRows] = acc[1][g][j];
+              } else {
+                const float gv = acc[0][g][j], uv = acc[1][g][j];
+                reinterpret_cast<__nv_bfloat16*>(a.out)[o] = __float2bfloat16_rn(gv / (1.f + __expf(-gv)) * uv);
+              }
             } else {
               reinterpret_cast<float*>(a.out)[o] = acc[0][g][j];
             }
@@ -1105,7 +1114,7 @@ int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
   st = hv::kernel_attr<expert_ffn_kernel<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<NMAT>::kTotal);
   if (st) return st;
 #if HV_FFN_TMA2D
-  {
+  if (!a.pair) {
     using T = T2Smem<NMAT>;
     const int n_items = (int)(a.rows / kRows) * (int)n_experts;
     st = hv::kernel_attr<expert_ffn_tma2d<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kTotal);
@@ -1130,7 +1139,7 @@ int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
   }
 #endif
 #if HV_FFN_TMA
-  if (a.K % kTKT == 0) {
+  if (a.K % kTKT == 0 && !a.pair) {
     using T = TSmem<NMAT>;
     st = hv::kernel_attr<expert_ffn_tma<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kTotal);
     if (st) return st;
@@ -1144,7 +1153,7 @@ int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
   }
 #endif
 #if HV_FFN_DYNAMIC
-  {
+  if (!a.pair) {
     unsigned* ctr = item_counter(dev, (cudaStream_t)stream);
     if (ctr) {
       ctr += NMAT == 2 ? 0 : 1;
@@ -1180,7 +1189,7 @@ int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
                                                           Smem<NMAT>::kTotal));
     resident[dev] = r > 0 ? r : 1;
   }
-  const int n_items = (int)(a.rows / kRows) * (int)n_experts;
+  const int n_items = (int)(a.rows / (kRows * (a.pair ? 2 : 1))) * (int)n_experts;
   int g = hv::sm_count(dev) * (dev >= 0 && dev < 64 ? resident[dev] : 1);
   if (g > n_items) g = n_items;
   expert_ffn_persistent<NMAT><<<g, kThreads, Smem<NMAT>::kTotal, (cudaStream_t)stream>>>(a, n_items);
@@ -1227,6 +1236,16 @@ HV_EXPORT int hv_expert_ffn_down(const uint64_t* d_w_addr, const int32_t* d_coun
   a.w_off1 = 0;
   a.rows = (int)hidden;
   a.K = (int)intermediate;
+#if HV_FFN_DOWN_PAIR && HV_FFN_PERSISTENT
+  if (hidden % (2 * kRows) == 0) {
+    // two 64-row blocks per item through the two-matrix kernel: every
+    // activation fragment (ldmatrix) and every barrier feeds two mma tiles, as
+    // in gate/up
+    a.pair = 1;
+    a.w_off1 = a.w_off0 + (uint64_t)kRows * intermediate * 2;
+    return launch_ffn<2>(a, n_experts, stream);
+  }
+#endif
   return launch_ffn<1>(a, n_experts, stream);
 }
 
