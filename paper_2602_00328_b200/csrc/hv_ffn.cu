@@ -64,8 +64,14 @@ constexpr int kRows = 16 * kWarps;   // weight rows per CTA (16 per warp: one mm
 #ifndef HV_FFN_STAGES
 #define HV_FFN_STAGES 3
 #endif
+// HV_FFN_DOWN_PAIR=1: the down projection as two 64-row blocks per item
+// through the two-matrix kernel (shared activation fragments and barriers).
+// Measured (r3a, weight GB/s, down alone): Qwen stage 4,485 vs 4,576, Phi-3.5
+// batch 1 / 16 / 64 1,632 / 4,209 / 4,390 vs 2,103 / 4,830 / 4,828 -- the
+// per-byte instruction and barrier overhead is not what limits the down
+// projection either.  Built as a variant only.
 #ifndef HV_FFN_DOWN_PAIR
-#define HV_FFN_DOWN_PAIR 1
+#define HV_FFN_DOWN_PAIR 0
 #endif
 constexpr int kKT = HV_FFN_KT;       // k columns per pipeline stage (64: 128 B per row)
 constexpr int kRowBytes = kKT * 2;
