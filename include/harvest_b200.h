@@ -265,6 +265,16 @@ int hv_expert_ffn_down(const uint64_t* d_w_addr, const int32_t* d_counts, const 
                        const void* d_act, float* d_y, uint32_t n_experts, uint32_t hidden,
                        uint32_t intermediate, void* stream);
 int hv_expert_ffn_max_tokens(int* out);
+/* hv_expert_ffn_down with flags.  HV_FFN_OVERLAP_PREVIOUS launches it with
+ * programmatic stream serialization right behind hv_expert_ffn_gate_up on the
+ * same stream: its CTAs start streaming expert weight tiles while gate/up
+ * drains and read d_act only after that kernel completes.  The caller
+ * guarantees d_w_addr / d_counts / d_offs were complete before gate/up
+ * started (they are its own inputs). */
+#define HV_FFN_OVERLAP_PREVIOUS 1u
+int hv_expert_ffn_down_ex(const uint64_t* d_w_addr, const int32_t* d_counts, const int32_t* d_offs,
+                          const void* d_act, float* d_y, uint32_t n_experts, uint32_t hidden,
+                          uint32_t intermediate, unsigned flags, void* stream);
 
 /* ---- paged decode attention over KV pages in any tier -------------------- */
 /* One query token per sequence, grouped-query (q_heads = g * kv_heads,

@@ -35,6 +35,7 @@ POOL_IPC = 1
 POOL_EAGER = 2
 POOL_REMOTE = 4
 ATTN_OVERLAP_PREVIOUS = 1        # HV_ATTN_OVERLAP_PREVIOUS: programmatic dependent launch of K5
+FFN_OVERLAP_PREVIOUS = 1         # HV_FFN_OVERLAP_PREVIOUS: K4 down behind gate/up
 
 
 class HarvestNativeError(RuntimeError):
@@ -130,6 +131,7 @@ _SIGS = {
     "hv_expert_ffn_gate_up": [u64, u64, u64, u64, u64, u64, u32, u32, u32, vp],
     "hv_expert_ffn_down": [u64, u64, u64, u64, u64, u32, u32, u32, vp],
     "hv_expert_ffn_max_tokens": [C.POINTER(i32)],
+    "hv_expert_ffn_down_ex": [u64, u64, u64, u64, u64, u32, u32, u32, C.c_uint, vp],
     "hv_paged_decode_attention": [u64, u64, u64, u64, u64, u64, u32, u32, u32, u32, u32, u32, C.c_float, vp],
     "hv_paged_decode_attention_ex": [u64, u64, u64, u64, u64, u64, u32, u32, u32, u32, u32, u32, C.c_float,
                                      C.c_uint, vp],

@@ -98,6 +98,7 @@ struct FfnArgs {
   uint64_t w_off0, w_off1;  // byte offsets of the matrices inside the object
   int rows, K;
   int pair;                 // down projection as a pair of row blocks (NMAT=2 kernel, fp32 out, no SiLU)
+  int wait_x;               // launched with programmatic serialization: x comes from the previous kernel
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(kThreads) expert_ffn_persistent(FfnArgs a, int
       cursor_seek<NMAT>(c, a, rb_count, n_items);
     }
   };
-  auto load_stage = [&](const ItemCursor& c, int s) {
+  auto load_weights = [&](const ItemCursor& c, int s) {
     char* base = smem + s * Smem<NMAT>::kStage;
     const size_t kb = (size_t)c.kt * kRowBytes;
 #pragma unroll
@@ -317,12 +318,19 @@ __global__ void __launch_bounds__(kThreads) expert_ffn_persistent(FfnArgs a, int
         cp_async16(ws + swz(r, ch), src + r * wstride + kb + ch * 16);
       }
     }
-    const uint32_t xs = smem_u32(base + Smem<NMAT>::kW);
+  };
+  auto load_x = [&](const ItemCursor& c, int s) {
+    const uint32_t xs = smem_u32(smem + s * Smem<NMAT>::kStage + Smem<NMAT>::kW);
+    const size_t kb = (size_t)c.kt * kRowBytes;
     for (int i = tid; i < c.n * kChunksPerRow; i += kThreads) {
       const int r = i / kChunksPerRow, ch = i % kChunksPerRow;
       const int row = a.tok ? a.tok[c.p0 + r] : c.p0 + r;
       cp_async16(xs + swz(r, ch), reinterpret_cast<const char*>(a.x) + row * xstride + kb + ch * 16);
     }
+  };
+  auto load_stage = [&](const ItemCursor& c, int s) {
+    load_weights(c, s);
+    load_x(c, s);
   };
 
   float acc[NMAT][kGroups][4];
@@ -333,13 +341,41 @@ __global__ void __launch_bounds__(kThreads) expert_ffn_persistent(FfnArgs a, int
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[m][g][j] = 0.f;
 
+  // the next kernel on the stream (the down projection after gate/up) may
+  // start as this one's CTAs drain
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (a.wait_x) {
+    // programmatic dependent launch: the expert weights do not depend on the
+    // previous kernel (gate/up), so the first stages' weight tiles stream in
+    // while it finishes; the activation rows it writes are loaded only after
+    // griddepcontrol.wait.  Commit groups stay in stage order: group 0 holds
+    // the early weights and stage 0's rows, group s stage s's rows.
+    ItemCursor pre = ld;
 #pragma unroll
-  for (int s = 0; s < Smem<NMAT>::kS - 1; ++s) {
-    if (ld.item < n_items) {
-      load_stage(ld, s);
-      advance(ld);
+    for (int s = 0; s < Smem<NMAT>::kS - 1; ++s) {
+      if (pre.item < n_items) {
+        load_weights(pre, s);
+        advance(pre);
+      }
     }
-    cp_commit();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#pragma unroll
+    for (int s = 0; s < Smem<NMAT>::kS - 1; ++s) {
+      if (ld.item < n_items) {
+        load_x(ld, s);
+        advance(ld);
+      }
+      cp_commit();
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < Smem<NMAT>::kS - 1; ++s) {
+      if (ld.item < n_items) {
+        load_stage(ld, s);
+        advance(ld);
+      }
+      cp_commit();
+    }
   }
   const int a_row = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
   const int a_kc = lane >> 4;
@@ -1198,7 +1234,19 @@ int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
   const int n_items = (int)(a.rows / (kRows * (a.pair ? 2 : 1))) * (int)n_experts;
   int g = hv::sm_count(dev) * (dev >= 0 && dev < 64 ? resident[dev] : 1);
   if (g > n_items) g = n_items;
-  expert_ffn_persistent<NMAT><<<g, kThreads, Smem<NMAT>::kTotal, (cudaStream_t)stream>>>(a, n_items);
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Smem<NMAT>::kTotal;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = a.wait_x ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HV_CUDA(cudaLaunchKernelEx(&cfg, expert_ffn_persistent<NMAT>, a, n_items));
+  }
 #else
   dim3 grid(a.rows / kRows, n_experts);
   expert_ffn_kernel<NMAT><<<grid, kThreads, Smem<NMAT>::kTotal, (cudaStream_t)stream>>>(a);
@@ -1231,7 +1279,17 @@ HV_EXPORT int hv_expert_ffn_gate_up(const uint64_t* d_w_addr, const int32_t* d_c
 HV_EXPORT int hv_expert_ffn_down(const uint64_t* d_w_addr, const int32_t* d_counts, const int32_t* d_offs,
                                  const void* d_act, float* d_y, uint32_t n_experts, uint32_t hidden,
                                  uint32_t intermediate, void* stream) {
+  return hv_expert_ffn_down_ex(d_w_addr, d_counts, d_offs, d_act, d_y, n_experts, hidden, intermediate, 0u, stream);
+}
+
+HV_EXPORT int hv_expert_ffn_down_ex(const uint64_t* d_w_addr, const int32_t* d_counts, const int32_t* d_offs,
+                                    const void* d_act, float* d_y, uint32_t n_experts, uint32_t hidden,
+                                    uint32_t intermediate, unsigned flags, void* stream) {
+  HV_CHECK_ARG((flags & ~(unsigned)HV_FFN_OVERLAP_PREVIOUS) == 0);
   FfnArgs a{};
+#if HV_FFN_PERSISTENT
+  a.wait_x = (flags & HV_FFN_OVERLAP_PREVIOUS) ? 1 : 0;
+#endif
   a.w_addr = d_w_addr;
   a.counts = d_counts;
   a.offs = d_offs;

@@ -62,9 +62,11 @@ def case(name, E, T, k, H, I, source):
         N.call("hv_expert_ffn_gate_up", addr.data_ptr(), counts.data_ptr(), offs.data_ptr(), tok.data_ptr(),
                h.data_ptr(), act.data_ptr(), E, H, I, s)
 
+    pdl = 0 if "--no-pdl" in sys.argv else N.FFN_OVERLAP_PREVIOUS
+
     def down():
-        N.call("hv_expert_ffn_down", addr.data_ptr(), counts.data_ptr(), offs.data_ptr(), act.data_ptr(),
-               y.data_ptr(), E, H, I, s)
+        N.call("hv_expert_ffn_down_ex", addr.data_ptr(), counts.data_ptr(), offs.data_ptr(), act.data_ptr(),
+               y.data_ptr(), E, H, I, pdl, s)
 
     def fused():
         gate_up()
