@@ -270,7 +270,8 @@ int hv_expert_ffn_max_tokens(int* out);
  * same stream: its CTAs start streaming expert weight tiles while gate/up
  * drains and read d_act only after that kernel completes.  The caller
  * guarantees d_w_addr / d_counts / d_offs were complete before gate/up
- * started (they are its own inputs). */
+ * started (they are its own inputs).  Measured on B200 it does not pay
+ * (Qwen stage 201.5 vs 195.4 us); the decoder uses the plain launch. */
 #define HV_FFN_OVERLAP_PREVIOUS 1u
 int hv_expert_ffn_down_ex(const uint64_t* d_w_addr, const int32_t* d_counts, const int32_t* d_offs,
                           const void* d_act, float* d_y, uint32_t n_experts, uint32_t hidden,

@@ -62,7 +62,7 @@ def case(name, E, T, k, H, I, source):
         N.call("hv_expert_ffn_gate_up", addr.data_ptr(), counts.data_ptr(), offs.data_ptr(), tok.data_ptr(),
                h.data_ptr(), act.data_ptr(), E, H, I, s)
 
-    pdl = 0 if "--no-pdl" in sys.argv else N.FFN_OVERLAP_PREVIOUS
+    pdl = N.FFN_OVERLAP_PREVIOUS if "--pdl" in sys.argv else 0
 
     def down():
         N.call("hv_expert_ffn_down_ex", addr.data_ptr(), counts.data_ptr(), offs.data_ptr(), act.data_ptr(),
