@@ -474,6 +474,12 @@ def run_b200(a):
             extra = same_run_comparisons(dev, m, a, source, fetcher)
         except Exception as e:
             extra = {"same_run_comparisons_error": repr(e)[:300]}
+        # the copy engine on the same source, measured in this run, beside the peak
+        # the fraction is taken against (a second, in-run ceiling for the reader)
+        ce = extra.get("copy_engine_same_source_GBps")
+        if ce:
+            roof["copy_engine_same_source_GBps"] = ce
+            roof["frac_of_copy_engine_same_source"] = achieved / ce
         cpu = None
         if world > 1:   # the CPU restatement is timed on rank 0 at N=1 only (contract)
             cpu = {"skipped": "timed in the N=1 run (rank 0, host cores)"}
