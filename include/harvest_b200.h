@@ -96,6 +96,43 @@ int hv_seg_free_list(const hv_seg* s, uint64_t* pairs, uint64_t* n);
 /* check_invariants (memalloc.py:141-159); HV_E_INVALID on violation */
 int hv_seg_check(const hv_seg* s);
 
+/* ---- native placement core (runtime.py:155-265) -------------------------
+ * Donor choice for harvest_alloc under the four policies, the Fairness token
+ * buckets (one per client index) and the Stability revocation windows.  The
+ * placer borrows each donor's hv_seg (the caller keeps ownership). Times are
+ * the runtime's clock in seconds. */
+typedef struct hv_placer hv_placer;
+#define HV_POLICY_BEST_FIT 0
+#define HV_POLICY_LOCALITY 1
+#define HV_POLICY_FAIRNESS 2
+#define HV_POLICY_STABILITY 3
+/* burst_bytes NaN = same as the budget (Policy.fairness_burst_bytes None) */
+int hv_placer_create(int policy_kind, double budget_bytes_per_s, double burst_bytes,
+                     double stability_window_s, int64_t stability_max_revocations,
+                     hv_placer** out);
+int hv_placer_destroy(hv_placer* p);
+/* hops = topology hops from the compute device (Locality's first key) */
+int hv_placer_add_donor(hv_placer* p, int device_id, hv_seg* seg, uint64_t ceiling, uint32_t hops);
+/* harvestable ceiling of a donor (runtime.py:476-487 sets it) */
+int hv_placer_set_ceiling(hv_placer* p, int device_id, uint64_t ceiling);
+int hv_placer_ceiling(hv_placer* p, int device_id, uint64_t* out);
+/* select_peer (runtime.py:169-196) over the listed donors: *device_out = the
+ * chosen id, or -1 with HV_E_NOCAPACITY.  Refills the client's bucket under
+ * Fairness, ages the revocation windows under Stability. */
+int hv_placer_select(hv_placer* p, uint64_t size, uint32_t client, double now,
+                     const int* candidates, int n_candidates, int* device_out);
+/* harvest_alloc's choice (runtime.py:198-214): the preferred donors first,
+ * then the others (all donors when n_preferred = 0), and the best-fit segment
+ * taken on the chosen donor.  Tokens are not spent (hv_placer_spend, after
+ * the donor's HBM is committed). */
+int hv_placer_alloc(hv_placer* p, uint64_t size, uint32_t client, double now,
+                    const int* preferred, int n_preferred, int* device_out, uint64_t* base_out);
+int hv_placer_spend(hv_placer* p, uint32_t client, uint64_t size, double now); /* runtime.py:252-254 */
+int hv_placer_tokens(hv_placer* p, uint32_t client, double now, double* out);  /* runtime.py:237-248 */
+/* a finished revocation on the donor (runtime.py:267-268) */
+int hv_placer_note_revocation(hv_placer* p, int device_id, double now);
+int hv_placer_churn(hv_placer* p, int device_id, double now, int64_t* out);   /* runtime.py:256-265 */
+
 /* ---- per-donor peer-memory pool ----------------------------------------- */
 typedef struct hv_pool hv_pool;
 #define HV_POOL_VMM 0u   /* cuMemAddressReserve + on-demand cuMemCreate/cuMemMap */

@@ -79,6 +79,17 @@ _SIGS = {
     "hv_seg_num_free": [vp, P64],
     "hv_seg_free_list": [vp, P64, P64],
     "hv_seg_check": [vp],
+    "hv_placer_create": [i32, C.c_double, C.c_double, C.c_double, C.c_int64, C.POINTER(vp)],
+    "hv_placer_destroy": [vp],
+    "hv_placer_add_donor": [vp, i32, vp, u64, u32],
+    "hv_placer_set_ceiling": [vp, i32, u64],
+    "hv_placer_ceiling": [vp, i32, P64],
+    "hv_placer_select": [vp, u64, u32, C.c_double, C.POINTER(i32), i32, C.POINTER(i32)],
+    "hv_placer_alloc": [vp, u64, u32, C.c_double, C.POINTER(i32), i32, C.POINTER(i32), P64],
+    "hv_placer_spend": [vp, u32, u64, C.c_double],
+    "hv_placer_tokens": [vp, u32, C.c_double, C.POINTER(C.c_double)],
+    "hv_placer_note_revocation": [vp, i32, C.c_double],
+    "hv_placer_churn": [vp, i32, C.c_double, C.POINTER(C.c_int64)],
     "hv_pool_create": [i32, u64, u64, C.POINTER(i32), i32, C.c_uint, C.POINTER(vp)],
     "hv_pool_destroy": [vp],
     "hv_pool_info": [vp, P64, P64, P64, C.POINTER(i32)],

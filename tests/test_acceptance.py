@@ -77,7 +77,7 @@ def test_revocation_ordering_10k_events():
                                 size=h.size, tag=("obj", h.key()), handle=h, payload=rng.getrandbits(64))
         elif r < 0.65:
             h = rng.choice(live)
-            if rt.lookup(h) is not None and h.key() in rt._peer_memory:
+            if rt.lookup(h) is not None and rt.has_content(h):
                 for _ in range(rng.randint(1, 3)):  # concurrent reads that must drain
                     rt.app_transfer(src=(h.device_id, Segment(h.base, h.size)), dst=(0, Segment(0, h.size)),
                                     size=h.size, tag=None, handle=h)

@@ -161,3 +161,77 @@ def test_fetch_wrappers_reject_bad_tensors_without_a_gpu():
         F.batch_copy(cpu, cpu[:2], cpu)
     with pytest.raises(ValueError, match="length mismatch"):
         F.swap_blocks_batch([1, 2], [3], [4, 5])
+
+
+def _placer(kind, budget=float("inf"), burst=float("nan"), window=10.0, maxrev=3):
+    h = C.c_void_p()
+    N.call("hv_placer_create", kind, budget, burst, window, maxrev, C.byref(h))
+    return h
+
+
+def test_native_placer_matches_oracle_selection_random():
+    """hv_placer_select / hv_placer_alloc against the oracle's restatement of
+    select_peer (runtime.py:155-196) on random donor states, BestFit and
+    Locality, random ceilings and candidate subsets."""
+    lib = N.load()
+    rng = random.Random(11)
+    for trial in range(60):
+        kind = rng.choice([0, 1])
+        p = _placer(kind)
+        states, cands, hops = {}, [], {}
+        for dev in rng.sample(range(1, 12), rng.randint(1, 6)):
+            st = M.init_device(M.DeviceSpec(dev, M.Tier.PEER_HBM, rng.randint(1, 64) << 20))
+            for _ in range(rng.randint(0, 12)):
+                seg = M.alloc_best_fit(st, rng.randint(1, 8) << 18)
+                if seg is not None and rng.random() < 0.4:
+                    M.free_segment(st, seg)
+            ceiling = rng.choice([st.spec.usable, rng.randint(0, st.spec.usable)])
+            hops[dev] = rng.randint(1, 3)
+            N.call("hv_placer_add_donor", p, dev, st._h, ceiling, hops[dev])
+            states[dev] = st
+            cands.append(dict(dev=dev, free_list=[(s.base, s.size) for s in st.free_list],
+                              allocated=M.allocated_bytes(st), ceiling=ceiling))
+        for _ in range(8):
+            size = rng.randint(1, 16) << 18
+            sub = [c for c in cands if rng.random() < 0.7]
+            want = O.select_device(sub, size, "Locality" if kind == 1 else "BestFit", hops) if sub else None
+            ids = (C.c_int * max(1, len(sub)))(*[c["dev"] for c in sub])
+            dev = C.c_int(-2)
+            st = lib.hv_placer_select(p, size, 0, 0.0, ids, len(sub), C.byref(dev))
+            assert (None if st == N.HV_E_NOCAPACITY else dev.value) == want
+        lib.hv_placer_destroy(p)
+
+
+def test_native_placer_token_bucket_and_revocation_window():
+    """runtime.py:237-265: a client's bucket starts full at the burst, refills
+    at the budget rate up to the burst; the Stability window drops
+    revocations older than the window."""
+    lib = N.load()
+    p = _placer(2, budget=100.0, burst=1000.0)
+    tok = C.c_double()
+    N.call("hv_placer_tokens", p, 0, 0.0, C.byref(tok))
+    assert tok.value == 1000.0
+    N.call("hv_placer_spend", p, 0, 900, 0.0)
+    N.call("hv_placer_tokens", p, 0, 2.0, C.byref(tok))
+    assert tok.value == 300.0
+    N.call("hv_placer_tokens", p, 0, 50.0, C.byref(tok))
+    assert tok.value == 1000.0
+    N.call("hv_placer_tokens", p, 7, 50.0, C.byref(tok))   # another client: its own full bucket
+    assert tok.value == 1000.0
+    lib.hv_placer_destroy(p)
+    p = _placer(3, window=2.0, maxrev=2)
+    st = M.init_device(M.DeviceSpec(4, M.Tier.PEER_HBM, 1 << 20))
+    N.call("hv_placer_add_donor", p, 4, st._h, 1 << 20, 1)
+    for t in (0.0, 1.0, 1.5):
+        N.call("hv_placer_note_revocation", p, 4, t)
+    n = C.c_int64()
+    N.call("hv_placer_churn", p, 4, 2.5, C.byref(n))
+    assert n.value == 2                                    # t=0.0 is older than 2.5 - 2.0
+    ids, dev = (C.c_int * 1)(4), C.c_int()
+    assert lib.hv_placer_select(p, 1024, 0, 2.5, ids, 1, C.byref(dev)) == N.HV_E_NOCAPACITY
+    assert lib.hv_placer_select(p, 1024, 0, 3.1, ids, 1, C.byref(dev)) == N.HV_OK and dev.value == 4
+    base = C.c_uint64()
+    assert lib.hv_placer_alloc(p, 1 << 20, 0, 3.1, None, 0, C.byref(dev), C.byref(base)) == N.HV_OK
+    assert (dev.value, base.value, M.allocated_bytes(st)) == (4, 0, 1 << 20)
+    assert lib.hv_placer_alloc(p, 1, 0, 3.1, None, 0, C.byref(dev), C.byref(base)) == N.HV_E_NOCAPACITY
+    lib.hv_placer_destroy(p)
