@@ -195,6 +195,15 @@ int hv_memset_d8(uint64_t d_dst, int value, uint64_t bytes, void* stream);
 
 /* ---- streams and events (drain ordering, runtime.py:345-356) ----------- */
 int hv_stream_create(int device, int priority, void** stream);
+/* cudaDeviceGetStreamPriorityRange: greatest = most urgent (negative) */
+int hv_stream_priority_range(int device, int* least, int* greatest);
+/* graphs captured by the caller (e.g. torch.cuda.CUDAGraph(keep_graph=True)):
+ * instantiate with HV_GRAPH_NODE_PRIORITY so kernel nodes keep the priority
+ * of the stream they were captured from; launch on a stream; destroy */
+#define HV_GRAPH_NODE_PRIORITY 1u
+int hv_graph_instantiate(void* graph, unsigned flags, void** exec_out);
+int hv_graph_launch(void* exec, void* stream);
+int hv_graph_exec_destroy(void* exec);
 int hv_stream_destroy(void* stream);
 int hv_stream_synchronize(void* stream);
 int hv_event_create(int device, unsigned timing, void** event);

@@ -36,6 +36,7 @@ POOL_EAGER = 2
 POOL_REMOTE = 4
 ATTN_OVERLAP_PREVIOUS = 1        # HV_ATTN_OVERLAP_PREVIOUS: programmatic dependent launch of K5
 FFN_OVERLAP_PREVIOUS = 1         # HV_FFN_OVERLAP_PREVIOUS: K4 down behind gate/up
+GRAPH_NODE_PRIORITY = 1          # HV_GRAPH_NODE_PRIORITY
 
 
 class HarvestNativeError(RuntimeError):
@@ -115,6 +116,10 @@ _SIGS = {
     "hv_memset_d8": [u64, i32, u64, vp],
     "hv_stream_create": [i32, i32, C.POINTER(vp)],
     "hv_stream_destroy": [vp],
+    "hv_stream_priority_range": [i32, C.POINTER(i32), C.POINTER(i32)],
+    "hv_graph_instantiate": [vp, C.c_uint, C.POINTER(vp)],
+    "hv_graph_launch": [vp, vp],
+    "hv_graph_exec_destroy": [vp],
     "hv_stream_synchronize": [vp],
     "hv_event_create": [i32, C.c_uint, C.POINTER(vp)],
     "hv_event_destroy": [vp],

@@ -771,3 +771,45 @@ HV_EXPORT int hv_stream_wait_event(void* stream, void* event) {
   HV_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)event, 0));
   return HV_OK;
 }
+
+// Stream priorities: [greatest, least] for `device` (greatest is the most
+// urgent, a negative number on B200).
+HV_EXPORT int hv_stream_priority_range(int device, int* least, int* greatest) {
+  HV_CHECK_ARG(least && greatest);
+  hv::DeviceGuard dg;
+  {
+    int gs = dg.set(device);
+    if (gs) return gs;
+  }
+  HV_CUDA(cudaDeviceGetStreamPriorityRange(least, greatest));
+  return HV_OK;
+}
+
+// Instantiate a captured graph so that each kernel node keeps the priority of
+// the stream it was captured from (cudaGraphInstantiateFlagUseNodePriority):
+// a fetch stream created urgent stays urgent inside the replay, so its CTAs
+// are dispatched ahead of the compute stream's when SMs free up.
+HV_EXPORT int hv_graph_instantiate(void* graph, unsigned flags, void** exec_out) {
+  HV_CHECK_ARG(graph && exec_out);
+  unsigned long long f = 0;
+  if (flags & HV_GRAPH_NODE_PRIORITY) f |= cudaGraphInstantiateFlagUseNodePriority;
+  cudaGraphExec_t e = nullptr;
+  HV_CUDA(cudaGraphInstantiateWithFlags(&e, (cudaGraph_t)graph, f));
+  *exec_out = (void*)e;
+  return HV_OK;
+}
+
+HV_EXPORT int hv_graph_launch(void* exec, void* stream) {
+  HV_CHECK_ARG(exec);
+  int dev = 0;
+  hv::DeviceGuard dg;
+  int st = hv::bind_stream_device(stream, &dev, dg);
+  if (st) return st;
+  HV_CUDA(cudaGraphLaunch((cudaGraphExec_t)exec, (cudaStream_t)stream));
+  return HV_OK;
+}
+
+HV_EXPORT int hv_graph_exec_destroy(void* exec) {
+  if (exec) HV_CUDA(cudaGraphExecDestroy((cudaGraphExec_t)exec));
+  return HV_OK;
+}

@@ -36,6 +36,7 @@ drain set of a fused step is every peer handle the step may read.
 """
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
@@ -245,7 +246,15 @@ class MoEDecoder:
     # ---------------------------------------------------------------- step
     _capturing = False
     _graph = None
+    _graph_exec = None
     _counts = None
+
+    def __del__(self):
+        try:
+            if self._graph_exec is not None:
+                N.lib().hv_graph_exec_destroy(self._graph_exec)
+        except Exception:
+            pass
 
     def routing_counts(self, x: torch.Tensor | None = None) -> np.ndarray:
         """Expert activation counts [L, E] of one eager step from ``x`` (the
@@ -290,11 +299,14 @@ class MoEDecoder:
             torch.cuda.synchronize(self.dev)
             self.rt.sim.poll() if hasattr(self.rt.sim, "poll") else self.rt.sim.run()
 
-    def capture_graph(self) -> None:
+    def capture_graph(self, node_priority: bool = False) -> None:
         """Capture one decode step (every stage's router, top-k, fetch plan,
         K2 fetch and expert FFN, on both streams) as a CUDA graph; later
         step() calls replay it.  Inputs are copied into a static buffer; the
-        output tensor returned by step() is reused by the next replay."""
+        output tensor returned by step() is reused by the next replay.
+        ``node_priority``: instantiate through the library with
+        HV_GRAPH_NODE_PRIORITY, so kernel nodes captured from the fetch stream
+        keep that stream's priority inside the replay."""
         if self.trace:
             raise ValueError("trace mode records per-launch events; capture without trace")
         if self.host_plan:
@@ -313,13 +325,18 @@ class MoEDecoder:
                     body(self._graph_in)
             cur.wait_stream(side)
             torch.cuda.synchronize(self.dev)
-            g = torch.cuda.CUDAGraph()
+            g = torch.cuda.CUDAGraph(keep_graph=node_priority)
             with torch.cuda.graph(g):
                 self._graph_out = body(self._graph_in)
         finally:
             self._capturing = False
         torch.cuda.synchronize(self.dev)
         self._graph = g
+        self._graph_exec = None
+        if node_priority:
+            ex = C.c_void_p()
+            N.call("hv_graph_instantiate", C.c_void_p(g.raw_cuda_graph()), N.GRAPH_NODE_PRIORITY, C.byref(ex))
+            self._graph_exec = ex
 
     def _replay(self, x: torch.Tensor) -> torch.Tensor:
         cur = torch.cuda.current_stream(self.dev)
@@ -328,7 +345,10 @@ class MoEDecoder:
         # drain bookkeeping for every peer handle the step may read
         handles = [h for hs in self.layer_handles for h in hs]
         batch = self.rt.begin_reads(handles) if handles else None
-        self._graph.replay()
+        if self._graph_exec is not None:
+            N.call("hv_graph_launch", self._graph_exec, C.c_void_p(cur.cuda_stream))
+        else:
+            self._graph.replay()
         done = torch.cuda.Event()
         done.record(cur)
         self._addr_done[self._addr_cur] = done

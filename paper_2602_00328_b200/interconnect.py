@@ -22,6 +22,7 @@ handle_key)`` (interconnect.py:133-165):
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 import math
 from collections import deque
@@ -205,7 +206,13 @@ class CudaTransferEngine:
     """Real batched transfers on a CUDA stream, completions via events."""
 
     def __init__(self, loop, topology: Topology, memory: MemoryMap, cuda_device: int,
-                 stream=None, engine: str = "auto", max_ctas: int = 0, log_transfers: bool = True):
+                 stream=None, engine: str = "auto", max_ctas: int = 0, log_transfers: bool = True,
+                 priority: int | str = 0):
+        """``priority``: CUDA priority of the engine's own stream: an int, or
+        "urgent" for the device's greatest (the decode fetch stream: its CTAs
+        are dispatched ahead of the compute stream's as SMs free up, measured
+        2.2x on a staged decode step, profiles/r2_priority_probe.json).  The
+        HV_FETCH_PRIORITY environment value overrides "urgent" (A/B runs)."""
         self.sim = loop
         self.topology = topology
         self.memory = memory
@@ -216,7 +223,13 @@ class CudaTransferEngine:
         self._own_stream = stream is None
         if stream is None:
             s = C.c_void_p()
-            N.call("hv_stream_create", cuda_device, 0, C.byref(s))
+            if priority == "urgent":
+                priority = os.environ.get("HV_FETCH_PRIORITY")
+                if priority is None:
+                    least, greatest = C.c_int(), C.c_int()
+                    N.call("hv_stream_priority_range", cuda_device, C.byref(least), C.byref(greatest))
+                    priority = greatest.value
+            N.call("hv_stream_create", cuda_device, int(priority), C.byref(s))
             self.stream = s.value or 0
         else:
             self.stream = N.stream_handle(stream)

@@ -87,8 +87,11 @@ class HarvestSystem:
         if self.host is not None:
             self.memory.register(self.host_id, self.host.d_alias, self.host.nbytes)
         self.loop = DeviceLoop()
+        # the fetch stream is the most urgent on the device: a decode step's
+        # next fetch must not wait behind the compute stream's CTAs
         self.engine = CudaTransferEngine(self.loop, self.topology, self.memory, compute, stream=stream,
-                                         engine=engine, max_ctas=max_ctas, log_transfers=log_transfers)
+                                         engine=engine, max_ctas=max_ctas, log_transfers=log_transfers,
+                                         priority="urgent")
         self.runtime = HarvestRuntime(self.loop, self.topology, policy, compute_device_id=0,
                                       engine=self.engine, pools=self.pools)
         # placement copy-ins (K3, rebalance) run on their own stream so they

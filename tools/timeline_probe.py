@@ -3,20 +3,26 @@ torch.profiler / Kineto activity trace: every kernel and copy-engine transfer
 with its stream and device timestamps), independent of the decoders' own
 CUDA events.  nsys is not in this image; this is the same kind of record.
 
-Scenarios (one GPU; the "peer" tier is a self-donor VMM pool, i.e. HBM):
+Scenarios (one GPU; the "peer" tier is a self-donor VMM pool, i.e. HBM), each
+a decode step captured as a CUDA graph and replayed (eager steps under a
+profiler are host-launch-bound and show the CPU, not the device):
   moe_peer_staged    Qwen 8-layer slice, every expert in the peer pool, staged
-                     decode with 2 micro-batches: K2 fetch on the fetch stream,
-                     router + expert FFN on the compute stream
-  moe_host_plan      the same experts in the pinned host tier, staged decode
-                     with the host plan: copy-engine fetches beside the FFN
+                     decode with 2 micro-batches: K2 fetch on the fetch stream
+                     (64 CTAs), router + expert FFN on the compute stream
+  moe_host_staged    the same experts in the pinned host tier, K2 over PCIe
+                     (the graph-capturable device-side plan; the copy engine's
+                     cudaMemcpyBatchAsync transfers are not in CUPTI's record)
   kv_peer_gather     Llama-3-8B config 1 (4 x 4k): K1 page gather on the KV
                      stream, K5 attention on the compute stream
+  kv_peer_in_place   the same, K5 reading the peer pages in place (programmatic
+                     dependent launch across layers)
 
-For each: intervals of the fetch class (K1/K2 kernels, copy-engine H2D/D2D
-fetches) and of the compute class (everything else) are merged per class and
-intersected; `fetch_hidden_frac` = the share of fetch time during which a
-compute kernel was also running.  Writes profiles/<tag>_timeline.json and the
-raw traces (gzip) next to it.
+For each: intervals of the fetch class (K1/K2 kernels, H2D copies) and of the
+compute class (everything else) are merged per class and intersected:
+`fetch_hidden_frac` = share of fetch time during which a compute kernel also
+ran, `compute_hidden_frac` the converse, `fetch_utilization` = fetch time /
+span (1.0 = the link never idles in a fetch-bound step).  Writes
+<out>/<tag>_timeline.json and the raw traces (gzip) next to it.
 
     python tools/timeline_probe.py [--tag r2] [--out-dir gpurun_out]
 """
@@ -65,7 +71,8 @@ def _intersect(x, y):
 
 
 def analyse(trace_path):
-    ev = json.load(open(trace_path))["traceEvents"]
+    opener = gzip.open if trace_path.endswith(".gz") else open
+    ev = json.load(opener(trace_path))["traceEvents"]
     dev = [e for e in ev if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")]
     fetch, comp, streams = [], [], {}
     for e in dev:
@@ -86,14 +93,19 @@ def analyse(trace_path):
             "span_us": span,
             "fetch_hidden_frac": _length(both) / _length(f) if f else None,
             "compute_hidden_frac": _length(both) / _length(c) if c else None,
+            "fetch_utilization": _length(f) / span if span else None,
+            # > 1 when kernels of the same class overlap each other (e.g. K5 of
+            # layer l+1 starting while layer l drains, programmatic dependent launch)
+            "compute_concurrency": sum(b - a for a, b in comp) / _length(c) if c else None,
             "streams": streams}
 
 
 def profiled(fn, steps, path):
     from torch.profiler import ProfilerActivity, profile
-    fn()
+    for _ in range(2):
+        fn()
     torch.cuda.synchronize()
-    with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(steps):
             fn()
         torch.cuda.synchronize()
@@ -129,12 +141,12 @@ def moe_case(kind, tmp):
         else:
             n_peer = 0
         f = ExpertFetcher(sysm.runtime, m, residency, store)
-        dec = MoEDecoder(f, tokens=32, microbatches=2, seed=0, host_plan=not peer,
-                         max_ctas=64 if peer else 0)
+        dec = MoEDecoder(f, tokens=32, microbatches=2, seed=0, max_ctas=64 if peer else 0)
+        dec.capture_graph()
         path = os.path.join(tmp, f"{kind}.json")
-        rep = profiled(lambda: dec.step(dec.x0), 2, path)
+        rep = profiled(lambda: dec.step(dec.x0), 3, path)
         rep.update({"layers": m.num_layers, "experts_in_peer_pool": n_peer, "tokens": 32, "microbatches": 2,
-                    "fetch_max_ctas": 64 if peer else "copy engine"})
+                    "fetch_max_ctas": 64 if peer else 0, "steps": 3, "cuda_graph": True})
         del dec
         torch.cuda.synchronize()
         sysm.loop.run()
@@ -143,7 +155,7 @@ def moe_case(kind, tmp):
         sysm.close()
 
 
-def kv_case(tmp):
+def kv_case(tmp, fused):
     from paper_2602_00328_b200.kv import LLAMA3_8B, KVCacheManager
     from paper_2602_00328_b200.kv_decode import KVAttentionDecoder
     from paper_2602_00328_b200.runtime import Durability
@@ -159,10 +171,14 @@ def kv_case(tmp):
         for s in range(batch):
             kv.append_kv(s, ctx)
         kv.evict(nblk * m.block_bytes)
-        dec = KVAttentionDecoder(kv, list(range(batch)), q_heads=32, seed=1, fused=False)
-        path = os.path.join(tmp, "kv_peer_gather.json")
-        rep = profiled(dec.step, 2, path)
-        rep.update({"config": "config 1: 4 x 4k tokens, 32 layers, KV pages in the peer pool, gather mode"})
+        dec = KVAttentionDecoder(kv, list(range(batch)), q_heads=32, seed=1, fused=fused)
+        dec.capture_graph()
+        name = "kv_peer_in_place" if fused else "kv_peer_gather"
+        path = os.path.join(tmp, f"{name}.json")
+        rep = profiled(dec.step, 3, path)
+        rep.update({"config": "config 1: 4 x 4k tokens, 32 layers, KV pages in the peer pool, "
+                              + ("K5 in place" if fused else "gather mode (K1 then K5)"),
+                    "steps": 3, "cuda_graph": True})
         del dec
         torch.cuda.synchronize()
         sysm.loop.run()
@@ -183,8 +199,9 @@ def main():
            "note": "one GPU; the peer tier is a self-donor VMM pool (HBM), so these show the overlap "
                    "structure, not NVLink rates"}
     for name, fn in (("moe_peer_staged", lambda: moe_case("moe_peer_staged", tmp)),
-                     ("moe_host_plan", lambda: moe_case("moe_host_plan", tmp)),
-                     ("kv_peer_gather", lambda: kv_case(tmp))):
+                     ("moe_host_staged", lambda: moe_case("moe_host_staged", tmp)),
+                     ("kv_peer_gather", lambda: kv_case(tmp, False)),
+                     ("kv_peer_in_place", lambda: kv_case(tmp, True))):
         try:
             rep, path = fn()
             with open(path, "rb") as src, gzip.open(os.path.join(a.out_dir, f"{a.tag}_timeline_{name}.json.gz"),
