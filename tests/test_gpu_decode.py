@@ -377,3 +377,32 @@ def test_host_plan_decode_equals_device_plan_and_all_local(microbatches):
     sysm.loop.run()
     sysm.close()
     sys2.close()
+
+
+def test_fetch_stream_is_urgent_and_node_priority_graph_equals_eager():
+    """The fetch engine's stream is created at the device's greatest priority
+    (a stage's fetch is dispatched ahead of the compute stream's CTAs,
+    profiles/r2_priority_probe.json); a graph instantiated by the library
+    with per-node priority (hv_graph_instantiate) replays bit-identically to
+    torch's instantiation and to the all-local eager run."""
+    import ctypes as C
+    from paper_2602_00328_b200 import _native as N
+    model = _tiny()
+    sysm, store, res, fetcher, dec = _setup(model, peer_experts=12, microbatches=2)
+    least, greatest = C.c_int(), C.c_int()
+    N.call("hv_stream_priority_range", 0, C.byref(least), C.byref(greatest))
+    assert torch.cuda.ExternalStream(sysm.engine.stream).priority == greatest.value
+    assert torch.cuda.ExternalStream(sysm.placement_engine.stream).priority == 0
+    dec.capture_graph(node_priority=True)
+    assert dec._graph_exec is not None
+    h = dec.step(dec.x0)
+    h = dec.step(h)
+    out = dec.step(h).clone()
+    torch.cuda.synchronize()
+    sys2, dec2, _keep = _all_local(model, 16, 2, 0, store)
+    out2 = dec2.decode(3)
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int16), out2.view(torch.int16))
+    del dec
+    sysm.close()
+    sys2.close()
