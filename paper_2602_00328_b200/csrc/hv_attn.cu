@@ -27,7 +27,12 @@
 // walking all splits serially costs more than the second launch
 // (4 x 4k: 2,928 vs 3,740 GB/s; 1 x 128k: 4,425 vs 5,564).  Unrolling the
 // merge kernel's split loops (8-deep) helped 1 x 128k by 2% and cost 4 x 4k
-// 12%: not kept.
+// 12%: not kept.  Holding each warp's page pointers in lane registers (32 per
+// coalesced load, read by shuffle when a block is queued, so no ring refill
+// waits on a dependent page-table load) measured (r4h, HBM pages rotated past
+// L2) 4 x 4k 3,458 vs 3,208 GB/s at 4 splits, 1 x 128k 5,434 vs 5,495 at 18,
+// and across a 32-layer graph step 10,374 vs 10,318 tok/s (4 x 4k) and 390 vs
+// 402 (128k): within noise where it counts, not kept.
 #include <cuda_fp16.h>
 #include <math.h>
 
