@@ -104,8 +104,11 @@ def main():
     out = {}
     srcs = [a for a in sys.argv[1:] if a in ("hbm", "host")] or ["hbm", "host"]
     for src in srcs:
-        for name, E, T, k, H, I in (("qwen_b32", 60, 32, 4, 2048, 1408), ("phi_b1", 16, 1, 2, 4096, 6400),
-                                    ("phi_b16", 16, 16, 2, 4096, 6400), ("phi_b64", 16, 64, 2, 4096, 6400)):
+        shapes = [("qwen_b32", 60, 32, 4, 2048, 1408), ("phi_b1", 16, 1, 2, 4096, 6400),
+                  ("phi_b16", 16, 16, 2, 4096, 6400), ("phi_b64", 16, 64, 2, 4096, 6400)]
+        if "swapped" in sys.argv:   # H and I exchanged: gate/up get K = 1,408, down K = 2,048
+            shapes = [("qwen_b32", 60, 32, 4, 2048, 1408), ("qwen_b32_swapped", 60, 32, 4, 1408, 2048)]
+        for name, E, T, k, H, I in shapes:
             out[f"{name}_{src}"] = case(name, E, T, k, H, I, src)
             torch.cuda.empty_cache()
     print(json.dumps(out, indent=1))
