@@ -11,8 +11,12 @@
 //
 // Decode is weight-bandwidth bound (a handful of tokens per expert), so the
 // kernels are built like the fetch kernels: deep cp.async (16-byte LDGSTS)
-// pipelines keep tens of KiB per SM in flight, and the tensor cores
-// (mma.sync m16n8k16 bf16 -> fp32) only have to keep up with the link.
+// pipelines keep tens of KiB per SM in flight, and the tensor cores only have
+// to keep up with the link.  The default (expert_ffn_umma, below) issues
+// tcgen05.mma from one thread with both operands read from shared memory by
+// descriptor and the accumulators in TMEM; the mma.sync m16n8k16 forms that
+// follow first are kept for shapes it does not take (rows % 128 != 0, the
+// programmatic-dependent down launch) and as the measured baseline.
 // Tile shape and schedule, measured on B200 with experts in local HBM
 // (tools/fused_probe.py, weight GB/s of the activated experts, Qwen1.5-MoE
 // stage / Phi-3.5 batch 16 / batch 1):
@@ -1143,6 +1147,296 @@ unsigned* item_counter(int dev, cudaStream_t s) {
 }
 #endif  // HV_FFN_DYNAMIC
 
+// ---------------------------------------------------------------------------
+// tcgen05 form (HV_FFN_UMMA): the same persistent item walk and the same
+// cp.async weight stream (16-byte LDGSTS into the 128B-swizzled K-major tile
+// the mma.sync form already uses, which is exactly UMMA's SWIZZLE_128B
+// canonical layout), but the products run on the 5th-generation tensor cores:
+// one thread issues tcgen05.mma with both operands read from shared memory
+// through descriptors, accumulating in TMEM.  The consumer warps of the
+// mma.sync form spend their issue slots on ldmatrix + mma.sync (ncu r4j: issue
+// active 31% / 45%, stalls on fixed-latency waits and the math pipe); here no
+// register fragment exists -- the MMA thread issues 4 instructions per matrix
+// per 64-column stage and the epilogue warps read the accumulators once per
+// item.
+//   warps 0-3  epilogue: tcgen05.ld of their TMEM lane quarter (weight rows),
+//              SiLU(gate) * up -> bf16 act, or fp32 y
+//   warps 4-5  producers: cp.async of the weight rows (M = 128 per item) and
+//              the item's activation rows; cp.async.mbarrier.arrive.noinc on
+//              the stage's full barrier
+//   warp 6     one elected lane issues tcgen05.mma (M = 128, N = n rounded up
+//              to 16, K = 16) and tcgen05.commit (stage free / item done)
+// TMEM: two accumulator buffers of 128 columns (gate at +0, up at +64), so
+// the epilogue of item i overlaps the MMAs of item i+1.
+// Measured (tools/fused_probe.py, experts in HBM, weight GB/s of the activated
+// experts; Qwen stage fused / gate_up / down, Phi-3.5 batch 1 / 16 / 64 fused):
+//   mma.sync persistent form (kept for rows % 128 != 0 and the PDL launch):
+//       4,956 / 5,216 / 4,516;  2,928 / 5,031 / 5,113
+//   this form, producer warps 2 / 4 / 6 / 8 (r4n, r4o):
+//       4,726 / 5,111 / 4,169;  2,259 / 4,690 / 5,092   (2: issue-bound producers)
+//       5,279 / 5,370 / 5,072;  3,154 / 5,472 / 5,633
+//       5,404 / 5,472 / 5,240;  3,373 / 5,615 / 5,733   <- default (6)
+//       5,345 / 5,382 / 5,179;  3,173 / 5,495 / 5,661
+// The first form resolved each activation row through the pair -> token map
+// in every stage (a dependent global load ahead of the stage's cp.async:
+// ncu r4m, long-scoreboard stalls dominant); the rows are now resolved once
+// per item.
+#ifndef HV_FFN_UMMA
+#define HV_FFN_UMMA 1
+#endif
+#if HV_FFN_UMMA
+constexpr int kURows = 128;                  // UMMA M: weight rows per item
+#ifndef HV_FFN_UMMA_PROD_WARPS
+#define HV_FFN_UMMA_PROD_WARPS 6
+#endif
+constexpr int kUEpiWarps = 4, kUProdWarps = HV_FFN_UMMA_PROD_WARPS;
+constexpr int kUThreads = (kUEpiWarps + kUProdWarps + 1) * 32;
+constexpr int kUProd = kUProdWarps * 32;
+template <int NMAT>
+struct USmem {
+  static constexpr int kS = NMAT == 2 ? 5 : 8;                 // ring stages
+  static constexpr int kWm = kURows * kRowBytes;               // one matrix tile: 16 KiB
+  static constexpr int kX = kMaxTok * kRowBytes;               // activation tile: 8 KiB
+  static constexpr int kStage = NMAT * kWm + kX;               // 1024-byte multiple
+  static constexpr int kTotal = kS * kStage + 1024;            // + alignment slack
+};
+
+__device__ __forceinline__ void u_mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void u_mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void u_mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n HV_U_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra HV_U_WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// SWIZZLE_128B K-major operand: 8-row groups 1024 B apart (SBO), LBO unused
+// (encoded 1), descriptor version 1 (sm100), layout type 2 = 128B swizzle
+__device__ __forceinline__ uint64_t umma_sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// kind::f16 instruction descriptor: f32 accumulate, bf16 A and B, both
+// K-major, N (multiple of 16 for M = 128), M = 128
+__device__ __forceinline__ uint32_t umma_idesc_bf16(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kURows >> 4) << 24);
+}
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct UCursor {
+  int item, n, p0, row0;
+  const char* w0;
+  const char* w1;
+};
+__device__ __forceinline__ void u_seek(UCursor& c, const FfnArgs& a, int rb_count, int n_items) {
+  while (c.item < n_items) {
+    const int e = c.item / rb_count;
+    const int n = a.counts[e];
+    if (n > 0) {
+      c.n = n < kMaxTok ? n : kMaxTok;
+      c.p0 = a.offs[e];
+      c.row0 = (c.item - e * rb_count) * kURows;
+      const char* obj = reinterpret_cast<const char*>(a.w_addr[e]);
+      c.w0 = obj + a.w_off0 + (size_t)c.row0 * a.K * 2;
+      c.w1 = obj + a.w_off1 + (size_t)c.row0 * a.K * 2;
+      return;
+    }
+    c.item += gridDim.x;
+  }
+}
+
+template <int NMAT>
+__global__ void __launch_bounds__(kUThreads, 1) expert_ffn_umma(FfnArgs a, int n_items) {
+  using U = USmem<NMAT>;
+  extern __shared__ __align__(1024) char u_smem_raw[];
+  // operand tiles must sit on 1024-byte boundaries (descriptor base offset 0)
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(u_smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full_bar[U::kS], empty_bar[U::kS], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rb_count = a.rows / kURows;
+  const int ktiles = a.K / kKT;
+  // activation rows past n inside the last N group start finite
+  for (int i = tid; i < U::kS * (U::kX / 16); i += kUThreads) {
+    const int s = i / (U::kX / 16), o = i % (U::kX / 16);
+    *reinterpret_cast<uint4*>(smem + s * U::kStage + NMAT * U::kWm + o * 16) = make_uint4(0, 0, 0, 0);
+  }
+  if (tid == 0) {
+    for (int s = 0; s < U::kS; ++s) {
+      u_mbar_init(smem_u32(&full_bar[s]), kUProd);   // one cp.async-completion arrival per producer thread
+      u_mbar_init(smem_u32(&empty_bar[s]), 1);       // tcgen05.commit of the stage's MMAs
+    }
+    for (int b = 0; b < 2; ++b) {
+      u_mbar_init(smem_u32(&tfull_bar[b]), 1);             // tcgen05.commit at the item's end
+      u_mbar_init(smem_u32(&tempty_bar[b]), kUEpiWarps * 32);  // every epilogue thread read its rows
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base_sh))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_sh;
+  const size_t wstride = (size_t)a.K * 2, xstride = (size_t)a.K * 2;
+
+  if (warp >= kUEpiWarps && warp < kUEpiWarps + kUProdWarps) {
+    // ---- producers
+    const int pt = tid - kUEpiWarps * 32;
+    UCursor c{(int)blockIdx.x, 0, 0, 0, nullptr, nullptr};
+    u_seek(c, a, rb_count, n_items);
+    uint32_t g = 0;
+    // this thread's activation rows: r = pt/8 + j*(kUProd/8), chunk pt%8 --
+    // their source rows are resolved once per item, not per stage
+    constexpr int kXPass = kUProd / kChunksPerRow;                 // rows covered per pass
+    constexpr int kXRows = (kMaxTok + kXPass - 1) / kXPass;
+    const int xr0 = pt / kChunksPerRow, xch = pt % kChunksPerRow;
+    while (c.item < n_items) {
+      const char* xsrc[kXRows];
+#pragma unroll
+      for (int j = 0; j < kXRows; ++j) {
+        const int r = xr0 + j * kXPass;
+        const int row = r < c.n ? (a.tok ? a.tok[c.p0 + r] : c.p0 + r) : 0;
+        xsrc[j] = reinterpret_cast<const char*>(a.x) + (size_t)row * xstride + xch * 16;
+      }
+      for (int kt = 0; kt < ktiles; ++kt, ++g) {
+        const int s = (int)(g % U::kS);
+        const uint32_t round = g / U::kS;
+        if (round > 0) u_mbar_wait(smem_u32(&empty_bar[s]), (round - 1) & 1);
+        char* base = smem + s * U::kStage;
+        const size_t kb = (size_t)kt * kRowBytes;
+#pragma unroll
+        for (int m = 0; m < NMAT; ++m) {
+          const uint32_t ws = smem_u32(base + m * U::kWm);
+          const char* src = m == 0 ? c.w0 : c.w1;
+#pragma unroll 4
+          for (int i = pt; i < kURows * kChunksPerRow; i += kUProd) {
+            const int r = i / kChunksPerRow, ch = i % kChunksPerRow;
+            cp_async16(ws + swz(r, ch), src + r * wstride + kb + ch * 16);
+          }
+        }
+        const uint32_t xs = smem_u32(base + NMAT * U::kWm);
+#pragma unroll
+        for (int j = 0; j < kXRows; ++j) {
+          const int r = xr0 + j * kXPass;
+          if (r < c.n) cp_async16(xs + swz(r, xch), xsrc[j] + kb);
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full_bar[s]))
+                     : "memory");
+      }
+      c.item += gridDim.x;
+      u_seek(c, a, rb_count, n_items);
+    }
+    cp_wait<0>();
+  } else if (warp == kUEpiWarps + kUProdWarps) {
+    // ---- MMA issue (one lane)
+    if (lane == 0) {
+      UCursor c{(int)blockIdx.x, 0, 0, 0, nullptr, nullptr};
+      u_seek(c, a, rb_count, n_items);
+      uint32_t g = 0, li = 0;
+      while (c.item < n_items) {
+        const uint32_t ab = li & 1, use = li >> 1;
+        if (use > 0) u_mbar_wait(smem_u32(&tempty_bar[ab]), (use - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int nn = c.n <= 16 ? 16 : ((c.n + 15) & ~15);
+        const uint32_t idesc = umma_idesc_bf16(nn);
+        for (int kt = 0; kt < ktiles; ++kt, ++g) {
+          const int s = (int)(g % U::kS);
+          u_mbar_wait(smem_u32(&full_bar[s]), (g / U::kS) & 1);
+          // the cp.async (generic proxy) writes of the stage, now visible to
+          // this thread, ordered before the tensor core's (async proxy) reads
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t base = smem_u32(smem + s * U::kStage);
+          const uint64_t bdesc = umma_sw128_desc(base + NMAT * U::kWm);
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m) {
+            const uint64_t adesc = umma_sw128_desc(base + m * U::kWm);
+#pragma unroll
+            for (int kk = 0; kk < kKT / 16; ++kk)   // K = 16 per instruction: +32 B inside the swizzle atom
+              umma_bf16(tmem + ab * 128 + m * 64, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc,
+                        (kt | kk) != 0);
+          }
+          umma_commit(smem_u32(&empty_bar[s]));   // the stage is free once these MMAs have read it
+        }
+        umma_commit(smem_u32(&tfull_bar[ab]));    // the item's accumulators are complete
+        ++li;
+        c.item += gridDim.x;
+        u_seek(c, a, rb_count, n_items);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---- epilogue: warp w reads TMEM lanes 32w..32w+31 = weight rows of the item
+    UCursor c{(int)blockIdx.x, 0, 0, 0, nullptr, nullptr};
+    u_seek(c, a, rb_count, n_items);
+    uint32_t li = 0;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    while (c.item < n_items) {
+      const uint32_t ab = li & 1;
+      u_mbar_wait(smem_u32(&tfull_bar[ab]), (li >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = c.row0 + warp * 32 + lane;
+      for (int j0 = 0; j0 < c.n; j0 += 8) {
+        float gv[8];
+        tmem_ld8(tmem + lane_base + ab * 128 + j0, gv);
+        if constexpr (NMAT == 2) {
+          float uv[8];
+          tmem_ld8(tmem + lane_base + ab * 128 + 64 + j0, uv);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j0 + j < c.n) {
+              const float x = gv[j];
+              reinterpret_cast<__nv_bfloat16*>(a.out)[(size_t)(c.p0 + j0 + j) * a.rows + row] =
+                  __float2bfloat16_rn(x / (1.f + __expf(-x)) * uv[j]);
+            }
+        } else {
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j0 + j < c.n) reinterpret_cast<float*>(a.out)[(size_t)(c.p0 + j0 + j) * a.rows + row] = gv[j];
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      u_mbar_arrive(smem_u32(&tempty_bar[ab]));
+      ++li;
+      c.item += gridDim.x;
+      u_seek(c, a, rb_count, n_items);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+}
+#endif  // HV_FFN_UMMA
+
 template <int NMAT>
 int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
   if (n_experts == 0) return HV_OK;
@@ -1155,6 +1449,20 @@ int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
   if (st) return st;
   st = hv::kernel_attr<expert_ffn_kernel<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<NMAT>::kTotal);
   if (st) return st;
+#if HV_FFN_UMMA
+  if (!a.pair && !a.wait_x && a.rows % kURows == 0) {
+    using U = USmem<NMAT>;
+    st = hv::kernel_attr<expert_ffn_umma<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, U::kTotal);
+    if (st) return st;
+    const int n_items = (int)(a.rows / kURows) * (int)n_experts;
+    int g = hv::sm_count(dev);                    // one ~200 KiB CTA per SM
+    if (g > n_items) g = n_items;
+    expert_ffn_umma<NMAT><<<g, kUThreads, U::kTotal, (cudaStream_t)stream>>>(a, n_items);
+    HV_CUDA(cudaGetLastError());
+    hv::note_launch();
+    return HV_OK;
+  }
+#endif
 #if HV_FFN_TMA2D
   if (!a.pair) {
     using T = T2Smem<NMAT>;
