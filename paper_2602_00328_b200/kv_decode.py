@@ -48,6 +48,7 @@ class KVAttentionDecoder:
     issue_ahead = True      # issue K1 of layer l+1 before K5 of layer l
     timed_events = True     # timing-enabled stream events in eager steps
     overlap_layers = True   # K5 of layer l+1 starts as K5 of layer l drains (HV_ATTN_OVERLAP_PREVIOUS)
+    overlap_gather = False  # the same in gather mode (measured slower, see _attend)
 
     def __init__(self, kv, sequences, q_heads: int, tokens: int | None = None, seed: int = 0,
                  engine: str | None = None, max_ctas: int | None = None, trace: bool = False,
@@ -155,8 +156,11 @@ class KVAttentionDecoder:
         # launch).  Measured (tools/kv_decode_probe.py, r2u, CUDA graph):
         # 4 x 4k 10,299 vs 6,658 tok/s, 128k 402 vs 337.  In gather mode an
         # early attention CTA would hold SMs the next K1 gather needs (graph:
-        # 1,791 vs 3,235 tok/s), so there it stays off.
-        flags = N.ATTN_OVERLAP_PREVIOUS if (self.overlap_layers and self.fused and layer > 0) else 0
+        # 1,791 vs 3,235 tok/s), so there it stays off; re-measured with the
+        # K1 stream at the greatest priority (r4s): 1,792 vs 3,244, 128k 59
+        # vs 108 -- priority orders dispatch, it cannot evict resident CTAs.
+        flags = N.ATTN_OVERLAP_PREVIOUS if (self.overlap_layers and (self.fused or self.overlap_gather)
+                                            and layer > 0) else 0
         N.call("hv_paged_decode_attention_ex", pages.data_ptr(), self.seq_start.data_ptr(),
                self.seq_tokens.data_ptr(), self.q[layer].data_ptr(), out.data_ptr(), self.part.data_ptr(), self.B,
                self.Hq, m.kv_heads, m.head_dim, m.block_tokens, self.splits, self.scale, flags,

@@ -62,6 +62,8 @@ def case(batch, ctx):
 if __name__ == "__main__":
     if "--no-overlap" in sys.argv:   # A/B of the programmatic dependent launch of K5 across layers
         KVAttentionDecoder.overlap_layers = False
+    if "--gather-pdl" in sys.argv:   # the same launch in gather mode
+        KVAttentionDecoder.overlap_gather = True
     print(json.dumps({"overlap_layers": KVAttentionDecoder.overlap_layers,
                       "config1_4x4k": case(4, 4096), "context_128k": case(1, 131072),
                       "note": "self-donor VMM pool: the peer tier is this GPU's HBM; outputs of every mode "
