@@ -500,11 +500,12 @@ def run_b200(a):
         line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-                "config": {**workload_config(m, world, source), "engine": a.engine, "max_ctas": a.max_ctas,
-                           "kernel_engine": a.kernel_engine,
-                           "engine_autotune": tune,
-                           "parallelism": f"{world} compute GPU(s)" + (f", each reading N-1={world - 1} donors"
-                                                                       if world > 1 else "")},
+                "config": workload_config(m, world),
+                "implementation": {"source_tier": source, "donors_per_rank": max(0, world - 1),
+                                   "engine": a.engine, "max_ctas": a.max_ctas, "kernel_engine": a.kernel_engine,
+                                   "engine_autotune": tune,
+                                   "parallelism": f"{world} compute GPU(s)" + (
+                                       f", each reading N-1={world - 1} donors" if world > 1 else "")},
                 "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": h2d // a.steps,
                         "d2h_bytes_per_step": d2h // a.steps, "read_errors": int(read_errors_all),
                         "verify_mismatched_words": int(mism_all),
@@ -531,7 +532,7 @@ def run_b200(a):
         pool_info = {"mode": node.mode, "setup_error": node.error, "fallback_reason": node.fallback_reason}
         node.close()
         if rank == 0:
-            line["config"]["donor_pools"] = pool_info
+            line["implementation"]["donor_pools"] = pool_info
     barrier()
     if world > 1:
         import gc

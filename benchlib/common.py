@@ -38,11 +38,18 @@ def model():
 def routing(m, steps, seed=SEED):
     return _routing(m, steps, seed, TOKENS)
 
-def workload_config(m, n, source):
+def workload_config(m, n, source=None):
+    """The workload both arms run (the same dict for the B200 arm and the
+    reference arm at the same N): model shape, routing, fetched bytes per
+    step and the N-GPU scenario.  Implementation details (source tier, fetch
+    engine, pools) are reported outside `config`."""
+    scenario = ("1 GPU: experts in the pinned host tier" if n <= 1 else
+                f"{n} GPUs, one process each: every GPU a compute GPU whose experts sit in the HBM of "
+                f"the N-1={n - 1} others")
     return {"workload": f"{m.name} expert fetch (BASELINE configs[1]): {m.num_layers} layers x "
                         f"{m.num_experts} experts x {m.expert_size} B, decode batch {TOKENS}, top-{m.top_k}, "
                         f"100% offloaded; one step = every layer's activated experts",
-            "source_tier": source, "donors_per_rank": max(0, n - 1),
+            "scenario": scenario,
             "l2": f"inputs larger than L2 (~{m.num_layers * 53 * m.expert_size / 1e9:.0f} GB fetched per step, "
                   "126 MB L2)",
             "routing": f"top-{m.top_k} of N(0,1) logits, seed {SEED}"}

@@ -95,7 +95,9 @@ def run_reference(a):
     line = {"metric": METRIC, "value": gbps, "unit": "GB/s", "impl": "reference", "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * dt / a.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic", "config": workload_config(m, 1, "host"),
+            "data": "synthetic", "config": workload_config(m, a.gpus),
+            "implementation": {"source_tier": "host DRAM (the reference CPU path: memcpy gather of the "
+                                              "host-authoritative expert table on rank 0)", "threads": threads},
             "cpu_baseline": {"value": gbps, "unit": "GB/s", "cores": threads, "kind": "port", "cpu_model": cpu_model(),
                              "sample": f"every layer ({m.num_layers}) of every decode step, memcpy gather from a "
                                        f"{m.num_layers * m.num_experts * m.expert_size / 1e9:.1f} GB host expert "
