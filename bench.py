@@ -431,7 +431,7 @@ def run_b200(a):
             # kernel -- ncu has nothing to capture; the step's SM kernel is the
             # per-fetch check, reported in roofline_check_kernel
             roof["traffic"] = None
-            roof["traffic_source"] = ("copy engine (cudaMemcpyBatchAsync): not a kernel, no ncu capture; the same "
+            roof["traffic_source"] = ("copy engine (cudaMemcpyAsync): not a kernel, no ncu capture; the same "
                                       "bytes through the K2 kernel: profiles/traffic.json[batch_copy_host]")
         elif source == "peer":
             # one GPU per gpurun call: no capture of a peer source exists; the

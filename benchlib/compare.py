@@ -91,7 +91,7 @@ def autotune(layer_desc, stream, stream_h, F, reps=3, engines=("ldg", "ldg256", 
              barrier=None, max_over_ranks=None, checked=None):
     """Time one layer's real fetch (host descriptor arrays, the product's
     hv_swap_blocks_batch entry point) under each engine x grid cap; pick the
-    fastest.  "ce" is the copy engine (cudaMemcpyBatchAsync), "auto" the
+    fastest.  "ce" is the copy engine (cudaMemcpyAsync per contiguous run), "auto" the
     library's engine per source (copy engine for large host-tier objects,
     kernel otherwise).  Multi-rank: every rank times the same candidate at the
     same moment (barrier before each), so the measurement includes the
@@ -136,7 +136,7 @@ def autotune(layer_desc, stream, stream_h, F, reps=3, engines=("ldg", "ldg256", 
 
 def same_run_comparisons(dev, m, a, source, fetcher=None, n=53):
     """Same-box comparisons for one layer's worth of experts (n x 17.3 MB):
-    the copy-engine paths on the same source (cudaMemcpyBatchAsync: the
+    the copy-engine paths on the same source (cudaMemcpyAsync: the
     paper's/vLLM's data path) and the same kernel on a local-HBM source
     against the HBM roofline (kernel quality independent of the link)."""
     import torch

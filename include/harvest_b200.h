@@ -226,8 +226,8 @@ int hv_stream_wait_event(void* stream, void* event);
 #define HV_ENGINE_TMA 2  /* cp.async.bulk global->smem->global ring, one issuing lane per CTA */
 #define HV_ENGINE_LDG256 3 /* LDG with the L2::256B sector-promotion hint (larger remote reads) */
 #define HV_ENGINE_LDG16 4  /* LDG with 16 x 128-bit loads in flight per lane (8 KiB per warp) */
-#define HV_ENGINE_CE 5     /* host-array entry points: every object through the copy engine (one
-                              cudaMemcpyBatchAsync); device-array entry points, which the copy
+#define HV_ENGINE_CE 5     /* host-array entry points: every object through the copy engine
+                              (cudaMemcpyAsync per contiguous run); device-array entry points, which the copy
                               engine cannot serve, treat it as HV_ENGINE_AUTO */
 /* OR-able flag for the variable-size copies (hv_batch_copy, hv_swap_blocks_batch):
  * when every non-empty object of a launch has the same size, chunk c reads
@@ -286,7 +286,8 @@ int hv_swap_blocks_batch(const uint64_t* h_src, const uint64_t* h_dst,
 
 /* Copy-engine baselines: per-object cudaMemcpyAsync (peer copies route over
  * NVLink via UVA, i.e. cudaMemcpyPeerAsync) when batched == 0,
- * one cudaMemcpyBatchAsync submission when batched == 1. Host arrays. */
+ * when batched == 1, objects whose source and destination both continue the
+ * previous object's are merged into one larger cudaMemcpyAsync. Host arrays. */
 int hv_ce_batch_copy(const uint64_t* h_src, const uint64_t* h_dst,
                      const uint64_t* h_bytes, uint32_t n, int batched, void* stream);
 

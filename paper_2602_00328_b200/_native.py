@@ -23,7 +23,7 @@ ENGINE_LDG = 1
 ENGINE_TMA = 2
 ENGINE_LDG256 = 3
 ENGINE_LDG16 = 4
-ENGINE_CE = 5                    # host-array entry points: every object through cudaMemcpyBatchAsync
+ENGINE_CE = 5                    # host-array entry points: every object through the copy engine (cudaMemcpyAsync per contiguous run)
 ENGINE_FLAG_INTERLEAVE = 0x100   # HV_ENGINE_FLAG_INTERLEAVE: round-robin chunks over equal-size objects
 ENGINES = {"auto": ENGINE_AUTO, "ldg": ENGINE_LDG, "tma": ENGINE_TMA, "ldg256": ENGINE_LDG256,
            "ldg16": ENGINE_LDG16}

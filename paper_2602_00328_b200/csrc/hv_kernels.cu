@@ -1092,9 +1092,8 @@ int kernel_swap(const uint64_t* h_src, const uint64_t* h_dst, const uint64_t* h_
 }
 
 // Per-device side stream for copy-engine work that must run beside (not
-// behind) a kernel on the caller's stream, or that the legacy NULL stream
-// cannot take (cudaMemcpyBatchAsync rejects it).  Fenced by events on both
-// sides, so the caller's stream order is preserved.
+// behind) a kernel on the caller's stream.  Fenced by events on both sides,
+// so the caller's stream order is preserved.
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
@@ -1114,40 +1113,29 @@ int side_stream(int dev, SideStream** out) {
   return HV_OK;
 }
 
-// One cudaMemcpyBatchAsync submission (or n cudaMemcpyAsync when !batched)
-// on a non-NULL stream.
-int ce_submit(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t n, bool batched,
+// Copy-engine submission on `stream`: one cudaMemcpyAsync per run.  With
+// `coalesce`, objects whose source and destination both continue the previous
+// object's (consecutive host slots into consecutive local slots, the layout
+// F.layer_runs and the decoder's compact staging produce) are merged into one
+// larger copy; otherwise every object is its own copy.  The DMA engine keeps
+// successive copies of one stream back to back: 17.3 MB experts lose ~1 us of
+// the ~311 us each takes on PCIe.
+int ce_submit(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t n, bool coalesce,
               cudaStream_t stream) {
-  if (n == 0) return HV_OK;
-  if (!batched) {
-    for (size_t i = 0; i < n; ++i) HV_CUDA(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDefault, stream));
-    return HV_OK;
+  size_t i = 0;
+  while (i < n) {
+    char* d = (char*)dsts[i];
+    const char* s = (const char*)srcs[i];
+    size_t z = sizes[i++];
+    while (coalesce && i < n && (char*)dsts[i] == d + z && (const char*)srcs[i] == s + z) z += sizes[i++];
+    if (z) HV_CUDA(cudaMemcpyAsync(d, s, z, cudaMemcpyDefault, stream));
   }
-  cudaMemcpyAttributes attr;
-  memset(&attr, 0, sizeof(attr));
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-  size_t attr_idx = 0, fail_idx = 0;
-  HV_CUDA(cudaMemcpyBatchAsync(const_cast<void**>(dsts), const_cast<void**>(srcs), const_cast<size_t*>(sizes), n,
-                               &attr, &attr_idx, 1, &fail_idx, stream));
   return HV_OK;
 }
 
-// ce_submit on `stream`, or on the device's side stream fenced by events when
-// `stream` is the legacy NULL stream.
-int ce_on_stream(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t n, bool batched,
-                 void* stream, int dev) {
-  if (stream != nullptr || !batched) return ce_submit(dsts, srcs, sizes, n, batched, (cudaStream_t)stream);
-  std::lock_guard<std::mutex> lk(g_side_mu);
-  SideStream* ss = nullptr;
-  int st = side_stream(dev, &ss);
-  if (st) return st;
-  HV_CUDA(cudaEventRecord(ss->fork, nullptr));
-  HV_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
-  if ((st = ce_submit(dsts, srcs, sizes, n, true, ss->s))) return st;
-  HV_CUDA(cudaEventRecord(ss->join, ss->s));
-  HV_CUDA(cudaStreamWaitEvent(nullptr, ss->join, 0));
-  return HV_OK;
+int ce_on_stream(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t n, bool coalesce,
+                 void* stream, int /*dev*/) {
+  return ce_submit(dsts, srcs, sizes, n, coalesce, (cudaStream_t)stream);
 }
 
 constexpr uint64_t kCeMinBytes = 1ull << 20;  // host-tier objects at least this large go to the copy engine
@@ -1189,7 +1177,7 @@ HV_EXPORT int hv_swap_blocks_batch(const uint64_t* h_src, const uint64_t* h_dst,
     return kernel_swap(h_src, h_dst, h_bytes, n, engine, max_ctas, stream, dev);
   }
   // AUTO: engine per source.  Large objects read from -- or written to --
-  // the pinned host tier go to the copy engine (one cudaMemcpyBatchAsync);
+  // the pinned host tier go to the copy engine (cudaMemcpyAsync per run);
   // everything else -- peer HBM over NVLink, local HBM, small host pages --
   // to the SM kernel.  Measured on B200 (tools/d2h_probe.py, r2q): 16 MiB
   // runs device->host 56.5 GB/s copy engine vs 52.3 SM stores; 64 KiB pages

@@ -11,8 +11,8 @@ own sm_100a kernels).  Reference call sites these replace:
                       host->peer placement copy-in of rebalance (moe.py:191-195)
 * ``swap_blocks_batch``  vLLM's offload data plane signature
                       (vllm/_custom_ops.py:2681-2703), host int64 arrays
-* ``ce_batch_copy``   copy-engine baselines (cudaMemcpyPeerAsync-per-object,
-                      cudaMemcpyBatchAsync), the paper's own data path
+* ``ce_batch_copy``   copy-engine baselines (cudaMemcpyPeerAsync per object,
+                      or per contiguous run), the paper's own data path
 """
 from __future__ import annotations
 
@@ -108,6 +108,9 @@ def swap_blocks_batch(src_ptrs, dst_ptrs, sizes, engine="auto", max_ctas: int = 
 
 
 def ce_batch_copy(src_ptrs, dst_ptrs, sizes, batched: bool = True, stream=None) -> None:
+    """Copy-engine baseline: one cudaMemcpyAsync per object, or with
+    ``batched`` one per run of objects whose source and destination are both
+    contiguous with the previous object's."""
     s, d, z = _host_u64(src_ptrs), _host_u64(dst_ptrs), _host_u64(sizes)
     if not (len(s) == len(d) == len(z)):
         raise ValueError("length mismatch")

@@ -84,7 +84,7 @@ def test_expert_fetch_from_donor_bit_exact(donor, engine):
 @pytest.mark.parametrize("donor", DONORS)
 def test_checked_fetch_and_copy_engine_from_donor(donor):
     """The fused fetch + content check (read_errors, moe.py:315-319) and the
-    copy engine (cudaMemcpyBatchAsync, the baseline of PAPER.md:200) on the
+    copy engine (cudaMemcpyAsync, the baseline of PAPER.md:200) on the
     donor's VA; one injected corruption on the donor is counted once."""
     from paper_2602_00328_b200 import fetch as F
     from paper_2602_00328_b200 import _native as N

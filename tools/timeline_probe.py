@@ -10,8 +10,7 @@ profiler are host-launch-bound and show the CPU, not the device):
                      decode with 2 micro-batches: K2 fetch on the fetch stream
                      (64 CTAs), router + expert FFN on the compute stream
   moe_host_staged    the same experts in the pinned host tier, K2 over PCIe
-                     (the graph-capturable device-side plan; the copy engine's
-                     cudaMemcpyBatchAsync transfers are not in CUPTI's record)
+                     (the graph-capturable device-side plan)
   kv_peer_gather     Llama-3-8B config 1 (4 x 4k): K1 page gather on the KV
                      stream, K5 attention on the compute stream
   kv_peer_in_place   the same, K5 reading the peer pages in place (programmatic
