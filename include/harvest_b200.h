@@ -349,6 +349,13 @@ int hv_paged_decode_attention(const uint64_t* d_page_ptrs, const int32_t* d_seq_
  * preceding kernel on the stream (true for the layers of a decode step:
  * the previous kernel is the previous layer's attention). */
 #define HV_ATTN_OVERLAP_PREVIOUS 1u
+/* HV_ATTN_BALANCED: balanced (stream-K) flash decoding.  `splits` is then the
+ * number of CTAs (one per SM is the intended size): the (sequence, KV head,
+ * 16-token block) units of the live blocks are cut into `splits` equal
+ * contiguous ranges, so every SM streams the same bytes whatever the
+ * sequence count; d_part must hold (splits + batch*kv_heads)*g*(D+2) floats;
+ * batch <= 256.  Deterministic for a given `splits`. */
+#define HV_ATTN_BALANCED 2u
 int hv_paged_decode_attention_ex(const uint64_t* d_page_ptrs, const int32_t* d_seq_start,
                                  const int32_t* d_seq_tokens, const void* d_q, float* d_out, float* d_part,
                                  uint32_t batch, uint32_t q_heads, uint32_t kv_heads, uint32_t head_dim,

@@ -35,6 +35,7 @@ POOL_IPC = 1
 POOL_EAGER = 2
 POOL_REMOTE = 4
 ATTN_OVERLAP_PREVIOUS = 1        # HV_ATTN_OVERLAP_PREVIOUS: programmatic dependent launch of K5
+ATTN_BALANCED = 2                # HV_ATTN_BALANCED: K5 as balanced (stream-K) ranges over `splits` CTAs
 FFN_OVERLAP_PREVIOUS = 1         # HV_FFN_OVERLAP_PREVIOUS: K4 down behind gate/up
 GRAPH_NODE_PRIORITY = 1          # HV_GRAPH_NODE_PRIORITY
 

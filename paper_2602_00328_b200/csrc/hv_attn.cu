@@ -338,6 +338,91 @@ __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
+// One 16-token block of one KV head, staged at `st` (K tile then V tile,
+// swizzled rows), folded into the warp's online-softmax state on tensor cores.
+// Lane (gr, c) owns query head gr (rows gr+8 are padding): its running max
+// and sum, and O[gr][n*8 + 2c + {0,1}].  `tb` is the block's first token.
+template <int D>
+__device__ __forceinline__ void mma_attend_block(const char* st, int tb, int ntok, const uint32_t (&qa)[D / 16][2],
+                                                 float scale, float& m_run, float& l_run, float (&o)[D / 8][2],
+                                                 int lane) {
+  constexpr int KS = D / 16, NT = D / 8;
+  const int c = lane & 3;
+  // ldmatrix lane roles: x4 over (tokens 0-7 | 8-15) x (k 0-7 | 8-15)
+  const int lm_row = (lane & 7) + ((lane >> 4) << 3);
+  const int lm_k = (lane >> 3) & 1;
+  // trans x4 over V: (tokens 0-7 | 8-15) x (dims d..d+7 | d+8..d+15)
+  const int lt_row = (lane & 7) + (((lane >> 3) & 1) << 3);
+  const int lt_d = lane >> 4;
+  const uint32_t ks_addr = smem_addr(st), vs_addr = ks_addr + Ring<D>::kTile;
+  // S^T = Q K^T : two n tiles (tokens 0-7, 8-15)
+  float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    uint32_t k0, k1, k2, k3;   // (tok 0-7,k lo) (tok 0-7,k hi) (tok 8-15,k lo) (tok 8-15,k hi)
+    ldsm4(ks_addr + rswz<D>(lm_row, ks * 2 + lm_k), k0, k1, k2, k3);
+    mma16816(s0, qa[ks][0], 0u, qa[ks][1], 0u, k0, k1);
+    mma16816(s1, qa[ks][0], 0u, qa[ks][1], 0u, k2, k3);
+  }
+  // row gr: tokens 2c, 2c+1 (tile 0) and 8+2c, 9+2c (tile 1); rows gr+8 (s*[2..3]) are padding
+  float x[4] = {s0[0] * scale, s0[1] * scale, s1[0] * scale, s1[1] * scale};
+  const int tk[4] = {2 * c, 2 * c + 1, 8 + 2 * c, 9 + 2 * c};
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (tb + tk[j] >= ntok) x[j] = -INFINITY;
+  float bm = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+  bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
+  bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
+  const float mn = fmaxf(m_run, bm);
+  float p[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) p[j] = x[j] == -INFINITY ? 0.f : __expf(x[j] - mn);
+  float bs = (p[0] + p[1]) + (p[2] + p[3]);
+  bs += __shfl_xor_sync(0xffffffffu, bs, 1);
+  bs += __shfl_xor_sync(0xffffffffu, bs, 2);
+  const float corr = m_run == -INFINITY ? 0.f : __expf(m_run - mn);  // 0 on the first / all-masked blocks
+  m_run = mn;
+  l_run = l_run * corr + bs;
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+    o[n][0] *= corr;
+    o[n][1] *= corr;
+  }
+  // P as the A operand (rows gr / gr+8, k = tokens): a0 (gr, 2c..) a1 (gr+8) a2 (gr, 2c+8..) a3 (gr+8)
+  const uint32_t pa0 = pack_h2(p[0], p[1]), pa2 = pack_h2(p[2], p[3]);
+#pragma unroll
+  for (int np = 0; np < NT / 2; ++np) {
+    uint32_t v0, v1, v2, v3;   // b0,b1 of dims np*16..+7, then of np*16+8..+15
+    ldsm4_t(vs_addr + rswz<D>(lt_row, np * 2 + lt_d), v0, v1, v2, v3);
+    float d0[4] = {o[2 * np][0], o[2 * np][1], 0.f, 0.f};
+    float d1[4] = {o[2 * np + 1][0], o[2 * np + 1][1], 0.f, 0.f};
+    mma16816(d0, pa0, 0u, pa2, 0u, v0, v1);
+    mma16816(d1, pa0, 0u, pa2, 0u, v2, v3);
+    o[2 * np][0] = d0[0];
+    o[2 * np][1] = d0[1];
+    o[2 * np + 1][0] = d1[0];
+    o[2 * np + 1][1] = d1[1];
+  }
+}
+
+// Q of (sequence b, KV head h) as the A operand: row gr = query head (zero
+// beyond G), k = head dims.  a0 (row gr, k 2c..), a2 (row gr, k 2c+8..).
+template <int D, int G>
+__device__ __forceinline__ void load_q_frag(const __half* __restrict__ q, int b, int h, int q_heads,
+                                            uint32_t (&qa)[D / 16][2], int lane) {
+  const int gr = lane >> 2, c = lane & 3;
+  const __half* qh = q + ((size_t)b * q_heads + h * G + (gr < G ? gr : 0)) * D;
+#pragma unroll
+  for (int ks = 0; ks < D / 16; ++ks) {
+    if (gr < G) {
+      qa[ks][0] = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 2 * c);
+      qa[ks][1] = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 8 + 2 * c);
+    } else {
+      qa[ks][0] = qa[ks][1] = 0u;
+    }
+  }
+}
+
 template <int D, int G, int S>
 __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_mma(
     const uint64_t* __restrict__ pages, const int32_t* __restrict__ seq_start, const int32_t* __restrict__ seq_tokens,
@@ -358,20 +443,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_mma(
   const int gr = lane >> 2, c = lane & 3;        // mma fragment row group / column pair
   char* my_ring = ring_smem + (size_t)warp * S * Ring<D>::kStage;
 
-  // Q as the A operand: row gr = query head (zero beyond G), k = head dims
-  uint32_t qa[KS][2];                    // a0 (row gr, k 2c..), a2 (row gr, k 2c+8..); rows gr+8 are zero
-  {
-    const __half* qh = q + ((size_t)b * q_heads + h * G + (gr < G ? gr : 0)) * D;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      if (gr < G) {
-        qa[ks][0] = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 2 * c);
-        qa[ks][1] = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 8 + 2 * c);
-      } else {
-        qa[ks][0] = qa[ks][1] = 0u;
-      }
-    }
-  }
+  uint32_t qa[KS][2];
+  load_q_frag<D, G>(q, b, h, q_heads, qa, lane);
   // blocks past the sequence's token count hold nothing to attend: not read
   const int b0 = seq_start[b], ntok = seq_tokens[b];
   const int nblk = min(seq_start[b + 1] - b0, (ntok + kBlockTok - 1) / kBlockTok);
@@ -390,12 +463,6 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_mma(
                                 reinterpret_cast<const char*>(pages[b0 + lo + warp + st * kAttnWarps]), kvh, h, lane);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  // ldmatrix lane roles: x4 over (tokens 0-7 | 8-15) x (k 0-7 | 8-15)
-  const int lm_row = (lane & 7) + ((lane >> 4) << 3);
-  const int lm_k = (lane >> 3) & 1;
-  // trans x4 over V: (tokens 0-7 | 8-15) x (dims d..d+7 | d+8..d+15)
-  const int lt_row = (lane & 7) + (((lane >> 3) & 1) << 3);
-  const int lt_d = lane >> 4;
   for (int it = 0; it < mine; ++it) {
     cp_wait_n<S - 2>();
     __syncwarp();
@@ -404,58 +471,9 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_mma(
       ring_load<D>(my_ring + (nx % S) * Ring<D>::kStage,
                    reinterpret_cast<const char*>(pages[b0 + lo + warp + nx * kAttnWarps]), kvh, h, lane);
     asm volatile("cp.async.commit_group;" ::: "memory");
-    const char* st = my_ring + (it % S) * Ring<D>::kStage;
-    const uint32_t ks_addr = smem_addr(st), vs_addr = ks_addr + Ring<D>::kTile;
     const int blk = lo + warp + it * kAttnWarps;
-    // S^T = Q K^T : two n tiles (tokens 0-7, 8-15)
-    float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      uint32_t k0, k1, k2, k3;   // (tok 0-7,k lo) (tok 0-7,k hi) (tok 8-15,k lo) (tok 8-15,k hi)
-      ldsm4(ks_addr + rswz<D>(lm_row, ks * 2 + lm_k), k0, k1, k2, k3);
-      mma16816(s0, qa[ks][0], 0u, qa[ks][1], 0u, k0, k1);
-      mma16816(s1, qa[ks][0], 0u, qa[ks][1], 0u, k2, k3);
-    }
-    // row gr: tokens 2c, 2c+1 (tile 0) and 8+2c, 9+2c (tile 1); rows gr+8 (s*[2..3]) are padding
-    const int tb = blk * kBlockTok;
-    float x[4] = {s0[0] * scale, s0[1] * scale, s1[0] * scale, s1[1] * scale};
-    const int tk[4] = {2 * c, 2 * c + 1, 8 + 2 * c, 9 + 2 * c};
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (tb + tk[j] >= ntok) x[j] = -INFINITY;
-    float bm = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
-    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
-    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
-    const float mn = fmaxf(m_run, bm);
-    float p[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) p[j] = x[j] == -INFINITY ? 0.f : __expf(x[j] - mn);
-    float bs = (p[0] + p[1]) + (p[2] + p[3]);
-    bs += __shfl_xor_sync(0xffffffffu, bs, 1);
-    bs += __shfl_xor_sync(0xffffffffu, bs, 2);
-    const float corr = m_run == -INFINITY ? 0.f : __expf(m_run - mn);  // 0 on the first / all-masked blocks
-    m_run = mn;
-    l_run = l_run * corr + bs;
-#pragma unroll
-    for (int n = 0; n < NT; ++n) {
-      o[n][0] *= corr;
-      o[n][1] *= corr;
-    }
-    // P as the A operand (rows gr / gr+8, k = tokens): a0 (gr, 2c..) a1 (gr+8) a2 (gr, 2c+8..) a3 (gr+8)
-    const uint32_t pa0 = pack_h2(p[0], p[1]), pa2 = pack_h2(p[2], p[3]);
-#pragma unroll
-    for (int np = 0; np < NT / 2; ++np) {
-      uint32_t v0, v1, v2, v3;   // b0,b1 of dims np*16..+7, then of np*16+8..+15
-      ldsm4_t(vs_addr + rswz<D>(lt_row, np * 2 + lt_d), v0, v1, v2, v3);
-      float d0[4] = {o[2 * np][0], o[2 * np][1], 0.f, 0.f};
-      float d1[4] = {o[2 * np + 1][0], o[2 * np + 1][1], 0.f, 0.f};
-      mma16816(d0, pa0, 0u, pa2, 0u, v0, v1);
-      mma16816(d1, pa0, 0u, pa2, 0u, v2, v3);
-      o[2 * np][0] = d0[0];
-      o[2 * np][1] = d0[1];
-      o[2 * np + 1][0] = d1[0];
-      o[2 * np + 1][1] = d1[1];
-    }
+    mma_attend_block<D>(my_ring + (it % S) * Ring<D>::kStage, blk * kBlockTok, ntok, qa, scale, m_run, l_run, o,
+                        lane);
     __syncwarp();
   }
   cp_wait_n<0>();
@@ -542,6 +560,267 @@ __global__ void paged_decode_combine(const float* __restrict__ part, float* __re
   out[((size_t)b * q_heads + qh) * D + d] = L > 0.f ? A / L : 0.f;
 }
 
+// ---- balanced (stream-K) form: HV_ATTN_BALANCED ---------------------------
+// The (split, KV head, sequence) grid gives every (sequence, KV head) pair the
+// same number of CTAs, so a few long sequences fill the machine only when
+// pairs x splits happens to be a multiple of the SM count: config 1 (4 x 4k,
+// 32 pairs) ran 4 splits = 128 CTAs on 148 SMs, and 5 splits a second, mostly
+// empty wave.  Here the work units -- (pair, 16-token block), pair-major over
+// the sequences' live blocks -- are cut into `n_cta` equal contiguous ranges,
+// one CTA each (one CTA per SM resident), so every SM streams the same number
+// of bytes.  A range covers the tail of one pair, whole pairs, and the head of
+// another; the CTA folds each pair's part (a segment) with all its warps
+// (units round-robin over warps, one cp.async ring per warp running across
+// segment boundaries, so the next segment's pages are in flight while the
+// warps merge), writes one partial state per segment into slot (cta + pair)
+// -- unique, since ranges are ordered -- and the last CTA to finish a pair
+// merges its partials in CTA order (deterministic; a pair inside one CTA is
+// written directly).  cta_of(u) = the CTA whose range holds unit u.
+__device__ __forceinline__ int cta_of(long long u, long long units, int n_cta) {
+  return (int)(((u + 1) * n_cta - 1) / units);
+}
+
+// merge `n` partial states (slots first .. first+n-1, in order) of one query
+// head and dim; returns the normalized output
+template <int D>
+__device__ __forceinline__ float merge_slots(const float* __restrict__ part, size_t first, int n, int G, int hh,
+                                             int d) {
+  float M = -INFINITY;
+  for (int i = 0; i < n; ++i) M = fmaxf(M, __ldcg(part + ((first + i) * G + hh) * (D + 2) + D));
+  float L = 0.f, A = 0.f;
+  for (int i = 0; i < n; ++i) {
+    const float* pp = part + ((first + i) * G + hh) * (D + 2);
+    const float pm = __ldcg(pp + D);
+    const float cf = pm == -INFINITY ? 0.f : __expf(pm - M);
+    L += __ldcg(pp + D + 1) * cf;
+    A += __ldcg(pp + d) * cf;
+  }
+  return L > 0.f ? A / L : 0.f;
+}
+
+template <int D, int G, int S>
+__global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_balanced(
+    const uint64_t* __restrict__ pages, const int32_t* __restrict__ seq_start, const int32_t* __restrict__ seq_tokens,
+    const __half* __restrict__ q, float* __restrict__ part, int B, int kvh, float scale,
+    float* __restrict__ final_out, unsigned* __restrict__ done) {
+  static_assert(G <= 8, "query rows g and g+8 of the m16 tile: at most 8 heads per KV head");
+  constexpr int NT = D / 8;
+  constexpr int W = kAttnWarps;
+  extern __shared__ __align__(128) char ring_smem[];
+  int* s_pre = reinterpret_cast<int*>(ring_smem + (size_t)W * S * Ring<D>::kStage);  // [B+1] units before sequence b
+  __shared__ float s_m[W][G], s_l[W][G];
+  __shared__ float s_acc[W][G][D];
+  __shared__ unsigned s_last;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int q_heads = kvh * G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gr = lane >> 2, c = lane & 3;
+  const int n_cta = gridDim.x, cta = blockIdx.x;
+  char* my_ring = ring_smem + (size_t)warp * S * Ring<D>::kStage;
+
+  if (warp == 0) {   // live blocks x kv heads per sequence, exclusive prefix
+    int run = 0;
+    for (int base = 0; base < B; base += 32) {
+      const int b = base + lane;
+      int nb = 0;
+      if (b < B) nb = max(0, min(seq_start[b + 1] - seq_start[b], (seq_tokens[b] + kBlockTok - 1) / kBlockTok)) * kvh;
+      int x = nb;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (b < B) s_pre[b] = run + x - nb;
+      run += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) s_pre[B] = run;
+  }
+  __syncthreads();
+  const long long units = s_pre[B];
+  const int u0 = (int)((long long)cta * units / n_cta), u1 = (int)((long long)(cta + 1) * units / n_cta);
+
+  // the pair holding unit u0: sequence by binary search over the prefix
+  int sb = 0, sh = 0;
+  if (u0 < u1) {
+    int lo = 0, hi = B - 1;   // last b with s_pre[b] <= u0 (then skip sequences with no units)
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_pre[mid] <= u0) lo = mid; else hi = mid - 1;
+    }
+    sb = lo;
+    while (s_pre[sb + 1] == s_pre[sb]) ++sb;
+    sh = (u0 - s_pre[sb]) / ((s_pre[sb + 1] - s_pre[sb]) / kvh);
+  }
+  // a cursor over this warp's units: (sequence, head, unit, segment end, pair's first unit)
+  struct Cur {
+    int b, h, u, e, q0;
+  };
+  // first unit of this warp at or after pair (b, h); u >= u1 when none is left
+  auto seek = [&](Cur& k, int b, int h) {
+    for (;;) {
+      while (b < B && s_pre[b + 1] == s_pre[b]) { ++b; h = 0; }
+      if (b >= B) { k.u = u1; return; }
+      const int nbk = (s_pre[b + 1] - s_pre[b]) / kvh;
+      const int q0 = s_pre[b] + h * nbk;
+      if (q0 >= u1) { k.u = u1; return; }
+      const int a = max(q0, u0), e = min(q0 + nbk, u1);
+      if (a + warp < e) {
+        k.b = b; k.h = h; k.u = a + warp; k.e = e; k.q0 = q0;
+        return;
+      }
+      if (++h == kvh) { ++b; h = 0; }
+    }
+  };
+  auto advance = [&](Cur& k) {
+    k.u += W;
+    if (k.u < k.e) return;
+    int b = k.b, h = k.h + 1;
+    if (h == kvh) { ++b; h = 0; }
+    seek(k, b, h);
+  };
+  auto load = [&](const Cur& k, int slot) {
+    ring_load<D>(my_ring + slot * Ring<D>::kStage,
+                 reinterpret_cast<const char*>(pages[seq_start[k.b] + (k.u - k.q0)]), kvh, k.h, lane);
+  };
+
+  Cur ld;
+  seek(ld, sb, sh);
+  if (u0 >= u1) ld.u = u1;
+  int n_loaded = 0, n_done = 0;
+#pragma unroll
+  for (int st = 0; st < S - 1; ++st) {
+    if (ld.u < u1) {
+      load(ld, n_loaded % S);
+      ++n_loaded;
+      advance(ld);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  bool waited = false;
+  // segments: the pairs this CTA's range touches, in order (every warp walks
+  // all of them so the CTA-wide merges line up)
+  int pb = sb, ph = sh;
+  while (u0 < u1) {
+    while (pb < B && s_pre[pb + 1] == s_pre[pb]) { ++pb; ph = 0; }
+    if (pb >= B) break;
+    const int nbk = (s_pre[pb + 1] - s_pre[pb]) / kvh;
+    const int q0 = s_pre[pb] + ph * nbk;
+    if (q0 >= u1) break;
+    const int a = max(q0, u0), e = min(q0 + nbk, u1);
+    const int ntok = seq_tokens[pb];
+    uint32_t qa[D / 16][2];
+    load_q_frag<D, G>(q, pb, ph, q_heads, qa, lane);
+    float m_run = -INFINITY, l_run = 0.f;
+    float o[NT][2];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = 0.f;
+    for (int u = a + warp; u < e; u += W) {
+      cp_wait_n<S - 2>();
+      __syncwarp();
+      if (ld.u < u1) {
+        load(ld, n_loaded % S);
+        ++n_loaded;
+        advance(ld);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      mma_attend_block<D>(my_ring + (n_done % S) * Ring<D>::kStage, (u - q0) * kBlockTok, ntok, qa, scale, m_run,
+                          l_run, o, lane);
+      ++n_done;
+      __syncwarp();
+    }
+    if (!waited) {   // HV_ATTN_OVERLAP_PREVIOUS: first write waits for the previous kernel
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      waited = true;
+    }
+    if (gr < G) {
+      if (c == 0) {
+        s_m[warp][gr] = m_run;
+        s_l[warp][gr] = l_run;
+      }
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        s_acc[warp][gr][n * 8 + 2 * c] = o[n][0];
+        s_acc[warp][gr][n * 8 + 2 * c + 1] = o[n][1];
+      }
+    }
+    __syncthreads();
+    const int pair = pb * kvh + ph;
+    const int c0 = cta_of(q0, units, n_cta), c1 = cta_of(q0 + nbk - 1, units, n_cta);
+    const bool alone = c0 == c1 && done != nullptr;
+    for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
+      const int hh = i / D, d = i % D;
+      float M = -INFINITY;
+      for (int w = 0; w < W; ++w) M = fmaxf(M, s_m[w][hh]);
+      float L = 0.f, A = 0.f;
+      for (int w = 0; w < W; ++w) {
+        const float cf = s_m[w][hh] == -INFINITY ? 0.f : __expf(s_m[w][hh] - M);
+        L += s_l[w][hh] * cf;
+        A += s_acc[w][hh][d] * cf;
+      }
+      if (alone) {
+        final_out[((size_t)pb * q_heads + ph * G + hh) * D + d] = L > 0.f ? A / L : 0.f;
+      } else {
+        float* out = part + (((size_t)cta + pair) * G + hh) * (D + 2);
+        out[d] = A;
+        if (d == 0) {
+          out[D] = M;
+          out[D + 1] = L;
+        }
+      }
+    }
+    if (!alone && done != nullptr) {
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) s_last = atomicAdd(done + pair, 1u) == (unsigned)(c1 - c0);
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
+          const int hh = i / D, d = i % D;
+          final_out[((size_t)pb * q_heads + ph * G + hh) * D + d] =
+              merge_slots<D>(part, (size_t)c0 + pair, c1 - c0 + 1, G, hh, d);
+        }
+        if (threadIdx.x == 0) done[pair] = 0u;
+      }
+    }
+    __syncthreads();   // s_m / s_acc / s_last free for the next segment
+    if (++ph == kvh) { ++pb; ph = 0; }
+  }
+  cp_wait_n<0>();
+  if (done == nullptr) return;   // paged_decode_combine_balanced writes every output
+  if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // pairs with no live block: zero output (no CTA range covers them)
+  for (int pair = cta; pair < B * kvh; pair += n_cta) {
+    const int b = pair / kvh;
+    if (s_pre[b + 1] != s_pre[b]) continue;
+    for (int i = threadIdx.x; i < G * D; i += blockDim.x) final_out[((size_t)b * q_heads + (pair % kvh) * G) * D + i] = 0.f;
+  }
+}
+
+// paged_decode_balanced's merge as a second kernel (launches without the
+// arrival counters, e.g. the first capture on a stream): grid (q_heads, B)
+template <int D>
+__global__ void paged_decode_combine_balanced(const int32_t* __restrict__ seq_start,
+                                              const int32_t* __restrict__ seq_tokens, const float* __restrict__ part,
+                                              float* __restrict__ out, int B, int q_heads, int kvh, int n_cta) {
+  const int qh = blockIdx.x, b = blockIdx.y, d = threadIdx.x;
+  const int g = q_heads / kvh, h = qh / g, hh = qh % g;
+  long long units = 0, before = 0;
+  int nbk = 0;
+  for (int i = 0; i < B; ++i) {
+    const int nb = max(0, min(seq_start[i + 1] - seq_start[i], (seq_tokens[i] + kBlockTok - 1) / kBlockTok));
+    if (i == b) { before = units; nbk = nb; }
+    units += (long long)nb * kvh;
+  }
+  float r = 0.f;
+  if (nbk > 0) {
+    const long long q0 = before + (long long)h * nbk;
+    const int c0 = cta_of(q0, units, n_cta), c1 = cta_of(q0 + nbk - 1, units, n_cta);
+    r = merge_slots<D>(part, (size_t)c0 + (size_t)b * kvh + h, c1 - c0 + 1, g, hh, d);
+  }
+  out[((size_t)b * q_heads + qh) * D + d] = r;
+}
+
 #ifndef HV_ATTN_MMA
 #define HV_ATTN_MMA 3
 #endif
@@ -597,6 +876,44 @@ unsigned* done_counters(int dev, size_t need, cudaStream_t s) {
 #define HV_ATTN_FUSED_COMBINE 1
 #endif
 
+constexpr uint32_t kBalancedMaxSeqs = 256;   // s_pre in shared memory beside the rings
+
+template <int D, int G>
+int launch_attn_balanced(const uint64_t* pages, const int32_t* seq_start, const int32_t* seq_tokens, const void* q,
+                         float* out, float* part, uint32_t B, uint32_t kvh, uint32_t n_cta, float scale,
+                         cudaStream_t s, unsigned flags) {
+  int dev = 0;
+  HV_CUDA(cudaGetDevice(&dev));
+  constexpr int kS = HV_ATTN_MMA ? HV_ATTN_MMA : 3;
+  const size_t smem = (size_t)kAttnWarps * kS * Ring<D>::kStage + (kBalancedMaxSeqs + 1) * sizeof(int);
+  int st = hv::kernel_attr<paged_decode_balanced<D, G, kS>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                            (int)smem);
+  if (st) return st;
+  unsigned* done = HV_ATTN_FUSED_COMBINE ? done_counters(dev, (size_t)B * kvh, s) : nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_cta);
+  cfg.blockDim = dim3(kAttnWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (flags & HV_ATTN_OVERLAP_PREVIOUS) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HV_CUDA(cudaLaunchKernelEx(&cfg, paged_decode_balanced<D, G, kS>, pages, seq_start, seq_tokens,
+                             reinterpret_cast<const __half*>(q), part, (int)B, (int)kvh, scale, out, done));
+  HV_CUDA(cudaGetLastError());
+  if (done) {
+    hv::note_launch(1);
+    return HV_OK;
+  }
+  paged_decode_combine_balanced<D><<<dim3(kvh * G, B), D, 0, s>>>(seq_start, seq_tokens, part, out, (int)B,
+                                                                  (int)(kvh * G), (int)kvh, (int)n_cta);
+  HV_CUDA(cudaGetLastError());
+  hv::note_launch(2);
+  return HV_OK;
+}
+
 template <int D, int G>
 int launch_attn(const uint64_t* pages, const int32_t* seq_start, const int32_t* seq_tokens, const void* q,
                 float* out, float* part, uint32_t B, uint32_t kvh, uint32_t splits, float scale, cudaStream_t s,
@@ -649,6 +966,15 @@ template <int D>
 int launch_attn_g(uint32_t g, const uint64_t* pages, const int32_t* seq_start, const int32_t* seq_tokens,
                   const void* q, float* out, float* part, uint32_t B, uint32_t kvh, uint32_t splits, float scale,
                   cudaStream_t s, unsigned flags) {
+  if (flags & HV_ATTN_BALANCED) {
+    switch (g) {
+      case 1: return launch_attn_balanced<D, 1>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s, flags);
+      case 2: return launch_attn_balanced<D, 2>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s, flags);
+      case 4: return launch_attn_balanced<D, 4>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s, flags);
+      case 8: return launch_attn_balanced<D, 8>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s, flags);
+      default: return HV_E_INVALID;
+    }
+  }
   switch (g) {
     case 1: return launch_attn<D, 1>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s, flags);
     case 2: return launch_attn<D, 2>(pages, seq_start, seq_tokens, q, out, part, B, kvh, splits, scale, s, flags);
@@ -675,7 +1001,8 @@ HV_EXPORT int hv_paged_decode_attention_ex(const uint64_t* d_page_ptrs, const in
   HV_CHECK_ARG(head_dim == 64 || head_dim == 128);
   HV_CHECK_ARG(block_tokens == (uint32_t)kBlockTok);
   HV_CHECK_ARG(splits >= 1 && splits <= 1024 && batch <= 65535u && kv_heads <= 65535u);
-  HV_CHECK_ARG((flags & ~(unsigned)HV_ATTN_OVERLAP_PREVIOUS) == 0);
+  HV_CHECK_ARG((flags & ~(unsigned)(HV_ATTN_OVERLAP_PREVIOUS | HV_ATTN_BALANCED)) == 0);
+  HV_CHECK_ARG(!(flags & HV_ATTN_BALANCED) || batch <= kBalancedMaxSeqs);
   int dev = 0;
   hv::DeviceGuard dg;
   int st = hv::bind_stream_device(stream, &dev, dg);

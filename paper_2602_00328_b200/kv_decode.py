@@ -49,6 +49,7 @@ class KVAttentionDecoder:
     timed_events = True     # timing-enabled stream events in eager steps
     overlap_layers = True   # K5 of layer l+1 starts as K5 of layer l drains (HV_ATTN_OVERLAP_PREVIOUS)
     overlap_gather = False  # the same in gather mode (measured slower, see _attend)
+    balanced = True         # K5 as balanced (stream-K) ranges, one CTA per SM (HV_ATTN_BALANCED)
 
     def __init__(self, kv, sequences, q_heads: int, tokens: int | None = None, seed: int = 0,
                  engine: str | None = None, max_ctas: int | None = None, trace: bool = False,
@@ -95,11 +96,20 @@ class KVAttentionDecoder:
         # pages, KV GB/s): 4 x 4k: 4 splits 3,988, 8: 3,313, 19: 2,339;
         # 1 x 128k: 18 splits 5,900, 37: 5,227, 74: 4,568 -- fewer, longer
         # splits amortize the partial write and merge
+        # Balanced form (the default for up to 256 sequences): the (sequence,
+        # KV head, block) units are cut into one equal range per SM, so the
+        # grid fills the machine whatever pairs x splits comes to (config 1:
+        # 32 pairs -> 4 splits = 128 CTAs on 148 SMs in the grid form).
         sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
-        self.splits = splits or max(1, min(self.nb, sms // (self.B * m.kv_heads)))
+        self.use_balanced = self.balanced and splits is None and self.B <= 256
+        if self.use_balanced:
+            self.splits = sms
+            slots = sms + self.B * m.kv_heads
+        else:
+            self.splits = splits or max(1, min(self.nb, sms // (self.B * m.kv_heads)))
+            slots = self.B * m.kv_heads * self.splits
         g_heads = q_heads // m.kv_heads
-        self.part = torch.empty(self.B * m.kv_heads * self.splits * g_heads * (m.head_dim + 2), dtype=torch.float32,
-                                device=self.dev)
+        self.part = torch.empty(slots * g_heads * (m.head_dim + 2), dtype=torch.float32, device=self.dev)
         self.scale = 1.0 / math.sqrt(m.head_dim)
         self.fetch_h = kv.stream
         self.fetch = torch.cuda.ExternalStream(kv.stream, device=self.dev)
@@ -161,6 +171,8 @@ class KVAttentionDecoder:
         # vs 108 -- priority orders dispatch, it cannot evict resident CTAs.
         flags = N.ATTN_OVERLAP_PREVIOUS if (self.overlap_layers and (self.fused or self.overlap_gather)
                                             and layer > 0) else 0
+        if self.use_balanced:
+            flags |= N.ATTN_BALANCED
         N.call("hv_paged_decode_attention_ex", pages.data_ptr(), self.seq_start.data_ptr(),
                self.seq_tokens.data_ptr(), self.q[layer].data_ptr(), out.data_ptr(), self.part.data_ptr(), self.B,
                self.Hq, m.kv_heads, m.head_dim, m.block_tokens, self.splits, self.scale, flags,

@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2602_00328_b200 import _native as N  # noqa: E402
 
 
-def run(B, ctx, splits_list, kvh=8, g=4, D=128, layers=4):
+def run(B, ctx, splits_list, kvh=8, g=4, D=128, layers=4, balanced=()):
     """``layers`` distinct page pools are attended in turn (a decode step
     walks every layer), so the working set exceeds the 126 MB L2 and no call
     reads the previous call's pages from L2."""
@@ -28,8 +28,11 @@ def run(B, ctx, splits_list, kvh=8, g=4, D=128, layers=4):
     q = torch.randn(B, kvh * g, D, device="cuda").to(torch.float16)
     out = torch.empty(B, kvh * g, D, device="cuda")
     res = {}
-    for sp in splits_list:
-        part = torch.empty(B * kvh * sp * g * (D + 2), device="cuda")
+    cases = [(f"splits{sp}", sp, 0) for sp in splits_list]
+    cases += [(f"balanced{c}", c, N.ATTN_BALANCED) for c in balanced]
+    cases += [(f"balanced{c}_pdl", c, N.ATTN_BALANCED | N.ATTN_OVERLAP_PREVIOUS) for c in balanced]
+    for name, sp, flags in cases:
+        part = torch.empty((B * kvh * sp + (sp + B * kvh)) * g * (D + 2), device="cuda")
         s = torch.cuda.current_stream().cuda_stream
 
         it = [0]
@@ -37,8 +40,8 @@ def run(B, ctx, splits_list, kvh=8, g=4, D=128, layers=4):
         def f():
             ptrs = ptr_sets[it[0] % layers]
             it[0] += 1
-            N.call("hv_paged_decode_attention", ptrs.data_ptr(), start.data_ptr(), tok.data_ptr(), q.data_ptr(),
-                   out.data_ptr(), part.data_ptr(), B, kvh * g, kvh, D, 16, sp, 1 / D ** 0.5, s)
+            N.call("hv_paged_decode_attention_ex", ptrs.data_ptr(), start.data_ptr(), tok.data_ptr(), q.data_ptr(),
+                   out.data_ptr(), part.data_ptr(), B, kvh * g, kvh, D, 16, sp, 1 / D ** 0.5, flags, s)
         for _ in range(3):
             f()
         torch.cuda.synchronize()
@@ -49,12 +52,15 @@ def run(B, ctx, splits_list, kvh=8, g=4, D=128, layers=4):
         e1.record()
         e1.synchronize()
         us = e0.elapsed_time(e1) / 20 * 1e3
-        res[f"splits{sp}"] = {"us": us, "GBps": n * page / (us * 1e-6) / 1e9}
+        res[name] = {"us": us, "GBps": n * page / (us * 1e-6) / 1e9}
     res["layers_rotated"] = layers
     return res
 
 
 if __name__ == "__main__":
-    out = {"config1_4x4k": run(4, 4096, [2, 3, 4, 5, 8, 9, 10, 19, 37]),
-           "config4_1x128k": run(1, 131072, [9, 18, 37, 74, 148])}
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    bal = (sms, 2 * sms)
+    out = {"config1_4x4k": run(4, 4096, [3, 4, 5, 8], balanced=bal),
+           "config4_1x128k": run(1, 131072, [18, 37], balanced=bal),
+           "batch32_x_2k": run(32, 2048, [1, 2], balanced=bal)}
     print(json.dumps(out, indent=1))

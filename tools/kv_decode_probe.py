@@ -64,7 +64,9 @@ if __name__ == "__main__":
         KVAttentionDecoder.overlap_layers = False
     if "--gather-pdl" in sys.argv:   # the same launch in gather mode
         KVAttentionDecoder.overlap_gather = True
-    print(json.dumps({"overlap_layers": KVAttentionDecoder.overlap_layers,
+    if "--grid" in sys.argv:         # A/B of the balanced (stream-K) K5 against the (split, head, seq) grid
+        KVAttentionDecoder.balanced = False
+    print(json.dumps({"overlap_layers": KVAttentionDecoder.overlap_layers, "balanced": KVAttentionDecoder.balanced,
                       "config1_4x4k": case(4, 4096), "context_128k": case(1, 131072),
                       "note": "self-donor VMM pool: the peer tier is this GPU's HBM; outputs of every mode "
                               "bit-identical to the all-local run"}, indent=1))
