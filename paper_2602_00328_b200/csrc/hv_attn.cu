@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_balanced(
   const int q_heads = kvh * G;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gr = lane >> 2, c = lane & 3;
-  const int n_cta = gridDim.x, cta = blockIdx.x;
+  const int cta = blockIdx.x;
   char* my_ring = ring_smem + (size_t)warp * S * Ring<D>::kStage;
 
   if (warp == 0) {   // live blocks x kv heads per sequence, exclusive prefix
@@ -637,7 +637,11 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_balanced(
   }
   __syncthreads();
   const long long units = s_pre[B];
-  const int u0 = (int)((long long)cta * units / n_cta), u1 = (int)((long long)(cta + 1) * units / n_cta);
+  // at most one CTA per unit, so every range is non-empty and the CTAs
+  // cta_of() names for a pair all arrive on its counter
+  const int n_cta = (int)min((long long)gridDim.x, units);
+  const int u0 = cta < n_cta ? (int)((long long)cta * units / n_cta) : 0;
+  const int u1 = cta < n_cta ? (int)((long long)(cta + 1) * units / n_cta) : 0;
 
   // the pair holding unit u0: sequence by binary search over the prefix
   int sb = 0, sh = 0;
@@ -790,7 +794,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) paged_decode_balanced(
   if (done == nullptr) return;   // paged_decode_combine_balanced writes every output
   if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
   // pairs with no live block: zero output (no CTA range covers them)
-  for (int pair = cta; pair < B * kvh; pair += n_cta) {
+  for (int pair = cta; pair < B * kvh; pair += gridDim.x) {
     const int b = pair / kvh;
     if (s_pre[b + 1] != s_pre[b]) continue;
     for (int i = threadIdx.x; i < G * D; i += blockDim.x) final_out[((size_t)b * q_heads + (pair % kvh) * G) * D + i] = 0.f;
@@ -814,6 +818,7 @@ __global__ void paged_decode_combine_balanced(const int32_t* __restrict__ seq_st
   }
   float r = 0.f;
   if (nbk > 0) {
+    n_cta = (int)min((long long)n_cta, units);   // as in paged_decode_balanced
     const long long q0 = before + (long long)h * nbk;
     const int c0 = cta_of(q0, units, n_cta), c1 = cta_of(q0 + nbk - 1, units, n_cta);
     r = merge_slots<D>(part, (size_t)c0 + (size_t)b * kvh + h, c1 - c0 + 1, g, hh, d);

@@ -49,7 +49,7 @@ class KVAttentionDecoder:
     timed_events = True     # timing-enabled stream events in eager steps
     overlap_layers = True   # K5 of layer l+1 starts as K5 of layer l drains (HV_ATTN_OVERLAP_PREVIOUS)
     overlap_gather = False  # the same in gather mode (measured slower, see _attend)
-    balanced = True         # K5 as balanced (stream-K) ranges, one CTA per SM (HV_ATTN_BALANCED)
+    balanced = False        # K5 as balanced (stream-K) ranges, one CTA per SM (HV_ATTN_BALANCED): measured slower
 
     def __init__(self, kv, sequences, q_heads: int, tokens: int | None = None, seed: int = 0,
                  engine: str | None = None, max_ctas: int | None = None, trace: bool = False,
@@ -96,10 +96,16 @@ class KVAttentionDecoder:
         # pages, KV GB/s): 4 x 4k: 4 splits 3,988, 8: 3,313, 19: 2,339;
         # 1 x 128k: 18 splits 5,900, 37: 5,227, 74: 4,568 -- fewer, longer
         # splits amortize the partial write and merge
-        # Balanced form (the default for up to 256 sequences): the (sequence,
-        # KV head, block) units are cut into one equal range per SM, so the
-        # grid fills the machine whatever pairs x splits comes to (config 1:
-        # 32 pairs -> 4 splits = 128 CTAs on 148 SMs in the grid form).
+        # Balanced form (opt-in, up to 256 sequences): the (sequence, KV head,
+        # block) units cut into one equal range per SM, so the grid fills the
+        # machine whatever pairs x splits comes to (config 1: 32 pairs -> 4
+        # splits = 128 CTAs on 148 SMs in the grid form).  Measured (r5d,
+        # tools/kv_decode_probe.py, in place, CUDA graph, PDL across layers):
+        # 4 x 4k 6,842 vs 10,277 tok/s for the grid, 128k 330 vs 407 -- with
+        # programmatic dependent launch the grid's idle SMs are where the next
+        # layer's CTAs start, and its CTAs finish staggered; the balanced
+        # CTAs all finish together.  Alone (tools/attn_probe.py) 26.3 vs 21.0 us
+        # at 4 x 4k and 98 vs 96 us at 128k.
         sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self.use_balanced = self.balanced and splits is None and self.B <= 256
         if self.use_balanced:
