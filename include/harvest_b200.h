@@ -320,6 +320,19 @@ int hv_expert_ffn_max_tokens(int* out);
  * started (they are its own inputs).  Measured on B200 it does not pay
  * (Qwen stage 201.5 vs 195.4 us); the decoder uses the plain launch. */
 #define HV_FFN_OVERLAP_PREVIOUS 1u
+/* HV_FFN_TILED: the expert's matrices are stored pre-tiled for the tensor
+ * cores -- matrix [R][K] bf16 as [R/128][K/64] contiguous 16 KiB tiles, tile
+ * row r holding columns 64*kt .. 64*kt+63 of row 128*rb + r with its 16-byte
+ * chunk c at chunk (c ^ (r & 7)) (UMMA's 128B-swizzled K-major layout), the
+ * matrices at the same offsets as the row-major form.  Each tile then reaches
+ * shared memory as one bulk copy on the TMA engine instead of 1,024 16-byte
+ * cp.async.  Requires R % 128 == 0 (the tcgen05 kernel); results are bitwise
+ * those of the row-major form on the same logical weights
+ * (fetch.tile_expert_matrix writes the layout). */
+#define HV_FFN_TILED 2u
+int hv_expert_ffn_gate_up_ex(const uint64_t* d_w_addr, const int32_t* d_counts, const int32_t* d_offs,
+                             const int32_t* d_tok, const void* d_x, void* d_act, uint32_t n_experts,
+                             uint32_t hidden, uint32_t intermediate, unsigned flags, void* stream);
 int hv_expert_ffn_down_ex(const uint64_t* d_w_addr, const int32_t* d_counts, const int32_t* d_offs,
                           const void* d_act, float* d_y, uint32_t n_experts, uint32_t hidden,
                           uint32_t intermediate, unsigned flags, void* stream);

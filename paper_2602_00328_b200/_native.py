@@ -35,6 +35,7 @@ POOL_IPC = 1
 POOL_EAGER = 2
 POOL_REMOTE = 4
 ATTN_OVERLAP_PREVIOUS = 1        # HV_ATTN_OVERLAP_PREVIOUS: programmatic dependent launch of K5
+FFN_TILED = 2                    # HV_FFN_TILED: K4 over experts stored as swizzled 128 x 64 tiles (bulk-copy stream)
 ATTN_BALANCED = 2                # HV_ATTN_BALANCED: K5 as balanced (stream-K) ranges over `splits` CTAs
 FFN_OVERLAP_PREVIOUS = 1         # HV_FFN_OVERLAP_PREVIOUS: K4 down behind gate/up
 GRAPH_NODE_PRIORITY = 1          # HV_GRAPH_NODE_PRIORITY
@@ -149,6 +150,7 @@ _SIGS = {
     "hv_expert_ffn_down": [u64, u64, u64, u64, u64, u32, u32, u32, vp],
     "hv_expert_ffn_max_tokens": [C.POINTER(i32)],
     "hv_expert_ffn_down_ex": [u64, u64, u64, u64, u64, u32, u32, u32, C.c_uint, vp],
+    "hv_expert_ffn_gate_up_ex": [u64, u64, u64, u64, u64, u64, u32, u32, u32, C.c_uint, vp],
     "hv_paged_decode_attention": [u64, u64, u64, u64, u64, u64, u32, u32, u32, u32, u32, u32, C.c_float, vp],
     "hv_paged_decode_attention_ex": [u64, u64, u64, u64, u64, u64, u32, u32, u32, u32, u32, u32, C.c_float,
                                      C.c_uint, vp],

@@ -103,6 +103,7 @@ struct FfnArgs {
   int rows, K;
   int pair;                 // down projection as a pair of row blocks (NMAT=2 kernel, fp32 out, no SiLU)
   int wait_x;               // launched with programmatic serialization: x comes from the previous kernel
+  int tiled;                // HV_FFN_TILED: matrices stored as swizzled 128 x 64 tiles (expert_ffn_umma only)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -1284,7 +1285,9 @@ __global__ void __launch_bounds__(kUThreads, 1) expert_ffn_umma(FfnArgs a, int n
   }
   if (tid == 0) {
     for (int s = 0; s < U::kS; ++s) {
-      u_mbar_init(smem_u32(&full_bar[s]), kUProd);   // one cp.async-completion arrival per producer thread
+      // one cp.async-completion arrival per producer thread, plus the tiled
+      // form's arrive.expect_tx of the weight tiles' bulk copies
+      u_mbar_init(smem_u32(&full_bar[s]), kUProd + (a.tiled ? 1 : 0));
       u_mbar_init(smem_u32(&empty_bar[s]), 1);       // tcgen05.commit of the stage's MMAs
     }
     for (int b = 0; b < 2; ++b) {
@@ -1329,14 +1332,32 @@ __global__ void __launch_bounds__(kUThreads, 1) expert_ffn_umma(FfnArgs a, int n
         if (round > 0) u_mbar_wait(smem_u32(&empty_bar[s]), (round - 1) & 1);
         char* base = smem + s * U::kStage;
         const size_t kb = (size_t)kt * kRowBytes;
+        if (a.tiled) {
+          // tile (row block, kt) of each matrix is 16 KiB contiguous and
+          // already in the swizzled order: one bulk copy (TMA engine) each,
+          // completing on the stage's full barrier
+          if (pt == 0) {
+            const uint32_t fb = smem_u32(&full_bar[s]);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(NMAT * U::kWm)
+                         : "memory");
 #pragma unroll
-        for (int m = 0; m < NMAT; ++m) {
-          const uint32_t ws = smem_u32(base + m * U::kWm);
-          const char* src = m == 0 ? c.w0 : c.w1;
+            for (int m = 0; m < NMAT; ++m)
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                      smem_u32(base + m * U::kWm)),
+                  "l"((m == 0 ? c.w0 : c.w1) + (size_t)kt * U::kWm), "r"(U::kWm), "r"(fb)
+                  : "memory");
+          }
+        } else {
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m) {
+            const uint32_t ws = smem_u32(base + m * U::kWm);
+            const char* src = m == 0 ? c.w0 : c.w1;
 #pragma unroll 4
-          for (int i = pt; i < kURows * kChunksPerRow; i += kUProd) {
-            const int r = i / kChunksPerRow, ch = i % kChunksPerRow;
-            cp_async16(ws + swz(r, ch), src + r * wstride + kb + ch * 16);
+            for (int i = pt; i < kURows * kChunksPerRow; i += kUProd) {
+              const int r = i / kChunksPerRow, ch = i % kChunksPerRow;
+              cp_async16(ws + swz(r, ch), src + r * wstride + kb + ch * 16);
+            }
           }
         }
         const uint32_t xs = smem_u32(base + NMAT * U::kWm);
@@ -1443,6 +1464,9 @@ int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
   HV_CHECK_ARG(a.w_addr && a.counts && a.offs && a.x && a.out);
   HV_CHECK_ARG(a.rows > 0 && a.K > 0 && a.rows % kRows == 0 && a.K % kKT == 0);
   HV_CHECK_ARG(n_experts <= 65535u);
+#if !HV_FFN_UMMA
+  HV_CHECK_ARG(!a.tiled);   // the swizzled-tile layout is read by the tcgen05 form only
+#endif
   int dev = 0;
   hv::DeviceGuard dg;
   int st = hv::bind_stream_device(stream, &dev, dg);
@@ -1450,6 +1474,7 @@ int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
   st = hv::kernel_attr<expert_ffn_kernel<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<NMAT>::kTotal);
   if (st) return st;
 #if HV_FFN_UMMA
+  HV_CHECK_ARG(!a.tiled || (!a.pair && !a.wait_x && a.rows % kURows == 0));
   if (!a.pair && !a.wait_x && a.rows % kURows == 0) {
     using U = USmem<NMAT>;
     st = hv::kernel_attr<expert_ffn_umma<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, U::kTotal);
@@ -1569,8 +1594,17 @@ int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
 HV_EXPORT int hv_expert_ffn_gate_up(const uint64_t* d_w_addr, const int32_t* d_counts, const int32_t* d_offs,
                                     const int32_t* d_tok, const void* d_x, void* d_act, uint32_t n_experts,
                                     uint32_t hidden, uint32_t intermediate, void* stream) {
+  return hv_expert_ffn_gate_up_ex(d_w_addr, d_counts, d_offs, d_tok, d_x, d_act, n_experts, hidden, intermediate, 0u,
+                                  stream);
+}
+
+HV_EXPORT int hv_expert_ffn_gate_up_ex(const uint64_t* d_w_addr, const int32_t* d_counts, const int32_t* d_offs,
+                                       const int32_t* d_tok, const void* d_x, void* d_act, uint32_t n_experts,
+                                       uint32_t hidden, uint32_t intermediate, unsigned flags, void* stream) {
   HV_CHECK_ARG(d_tok != nullptr || n_experts == 0);
+  HV_CHECK_ARG((flags & ~(unsigned)HV_FFN_TILED) == 0);
   FfnArgs a{};
+  a.tiled = (flags & HV_FFN_TILED) ? 1 : 0;
   a.w_addr = d_w_addr;
   a.counts = d_counts;
   a.offs = d_offs;
@@ -1593,8 +1627,9 @@ HV_EXPORT int hv_expert_ffn_down(const uint64_t* d_w_addr, const int32_t* d_coun
 HV_EXPORT int hv_expert_ffn_down_ex(const uint64_t* d_w_addr, const int32_t* d_counts, const int32_t* d_offs,
                                     const void* d_act, float* d_y, uint32_t n_experts, uint32_t hidden,
                                     uint32_t intermediate, unsigned flags, void* stream) {
-  HV_CHECK_ARG((flags & ~(unsigned)HV_FFN_OVERLAP_PREVIOUS) == 0);
+  HV_CHECK_ARG((flags & ~(unsigned)(HV_FFN_OVERLAP_PREVIOUS | HV_FFN_TILED)) == 0);
   FfnArgs a{};
+  a.tiled = (flags & HV_FFN_TILED) ? 1 : 0;
 #if HV_FFN_PERSISTENT
   a.wait_x = (flags & HV_FFN_OVERLAP_PREVIOUS) ? 1 : 0;
 #endif
@@ -1609,7 +1644,7 @@ HV_EXPORT int hv_expert_ffn_down_ex(const uint64_t* d_w_addr, const int32_t* d_c
   a.rows = (int)hidden;
   a.K = (int)intermediate;
 #if HV_FFN_DOWN_PAIR && HV_FFN_PERSISTENT
-  if (hidden % (2 * kRows) == 0) {
+  if (!a.tiled && hidden % (2 * kRows) == 0) {
     // two 64-row blocks per item through the two-matrix kernel: every
     // activation fragment (ldmatrix) and every barrier feeds two mma tiles, as
     // in gate/up

@@ -89,11 +89,18 @@ class MoEDecoder:
         self.host_plan = host_plan
         if host_plan and fused:
             raise ValueError("host_plan applies to the staged decoder")
+        # experts stored as HV_FFN_TILED tiles (ExpertStore.fill_host(layout=
+        # "tiled")): both decoders compute with K4, whose weight tiles then
+        # arrive as one bulk copy each -- fused in place, staged over its
+        # staging slots (the staged FFN's cuBLAS bmm reads row-major bytes)
+        self.tiled = getattr(fetcher.store, "layout", "row") == "tiled"
+        if fused or self.tiled:
             mt = N.c_int_out("hv_expert_ffn_max_tokens")
             if self.tmb > mt:
-                raise ValueError(f"fused decode: at most {mt} tokens per micro-batch")
+                raise ValueError(f"K4 decode: at most {mt} tokens per micro-batch")
             if self.I % 64 or self.H % 64:
-                raise ValueError("fused decode needs hidden and intermediate sizes that are multiples of 64")
+                raise ValueError("K4 decode needs hidden and intermediate sizes that are multiples of 64")
+        self.ffn_flags = N.FFN_TILED if self.tiled else 0
         # fused mode reads peer / local experts in place; only host-tier
         # experts are staged (one buffer: K2 and K4 run in order on one stream)
         self.staging = [torch.zeros(self.K, self.S, dtype=torch.uint8, device=self.dev)
@@ -195,7 +202,13 @@ class MoEDecoder:
         torch.add(rank.clamp_(min=0) * self.S, self.slot_base[slot], out=self.dst_ptrs[slot])
         torch.lt(self._kslots, active.sum(), out=self.valid[slot])
 
-    def _ffn(self, h: torch.Tensor, slot: int, buf: int) -> torch.Tensor:
+    def _ffn(self, h: torch.Tensor, slot: int, buf: int, layer: int) -> torch.Tensor:
+        if self.tiled:
+            # K4 over the staging slots: dst_ptrs[slot][e] is active expert e's
+            # slot (the routing is _route's, recomputed on the same inputs)
+            probs, counts, offs, tok, pos = self._route_pairs(h, layer, count=False)
+            return self._k4(h, self.dst_ptrs[slot], probs, counts, offs, tok, pos,
+                            torch.cuda.current_stream(self.dev).cuda_stream)
         K, I, H = self.K, self.I, self.H
         w = self.staging[buf].view(torch.bfloat16).view(K, 3 * I * H)
         gate = w[:, :I * H].view(K, I, H)
@@ -384,7 +397,7 @@ class MoEDecoder:
                 if self.trace:
                     cs = torch.cuda.Event(enable_timing=True)
                     cs.record(self.compute)
-                y = self._ffn(hs[mb], slot, buf)
+                y = self._ffn(hs[mb], slot, buf, layer)
                 if self.trace:
                     ce = torch.cuda.Event(enable_timing=True)
                     ce.record(self.compute)
@@ -407,14 +420,14 @@ class MoEDecoder:
         return torch.stack(hs).view(self.T, self.H)
 
     # ---------------------------------------------------------------- fused
-    def _route_pairs(self, h: torch.Tensor, layer: int):
+    def _route_pairs(self, h: torch.Tensor, layer: int, count: bool = True):
         """Router -> top-k -> routed pairs sorted by expert, all on the device:
         counts/offsets per expert, the token row of each sorted pair, and the
         sorted position of pair (t, j) for the combine."""
         k = self.m.top_k
         logits = (h @ self.router[layer].t()).float()
         topv, topi = logits.topk(k, dim=1)
-        if self._counts is not None:
+        if count and self._counts is not None:
             self._counts[layer].index_add_(0, topi.reshape(-1), torch.ones_like(topi.reshape(-1)))
         probs = torch.softmax(topv, dim=1)
         flat = topi.reshape(-1)
@@ -429,9 +442,6 @@ class MoEDecoder:
 
     def _ffn_fused(self, h: torch.Tensor, layer: int) -> torch.Tensor:
         probs, counts, offs, tok, pos = self._route_pairs(h, layer)
-        P, H, I = pos.numel(), self.H, self.I
-        act = torch.empty(P, I, dtype=torch.bfloat16, device=self.dev)
-        y = torch.empty(P, H, dtype=torch.float32, device=self.dev)
         stream = torch.cuda.current_stream(self.dev).cuda_stream
         addr = self.addr[layer]
         if self._capturing or self._any_host[layer]:
@@ -445,14 +455,22 @@ class MoEDecoder:
             N.call("hv_batch_copy", addr.data_ptr(), dst.data_ptr(), sizes.data_ptr(), self.E, self.engine_id,
                    self.max_ctas, stream)
             addr = torch.where(stage, dst, addr)
+        return self._k4(h, addr, probs, counts, offs, tok, pos, stream)
+
+    def _k4(self, h, addr, probs, counts, offs, tok, pos, stream) -> torch.Tensor:
+        """K4 (gate/up, then down) over the experts at `addr` and the top-k
+        combine."""
+        P, H, I = pos.numel(), self.H, self.I
+        act = torch.empty(P, I, dtype=torch.bfloat16, device=self.dev)
+        y = torch.empty(P, H, dtype=torch.float32, device=self.dev)
         w = addr.data_ptr()
-        N.call("hv_expert_ffn_gate_up", w, counts.data_ptr(), offs.data_ptr(), tok.data_ptr(), h.data_ptr(),
-               act.data_ptr(), self.E, H, I, stream)
+        N.call("hv_expert_ffn_gate_up_ex", w, counts.data_ptr(), offs.data_ptr(), tok.data_ptr(), h.data_ptr(),
+               act.data_ptr(), self.E, H, I, self.ffn_flags, stream)
         # (HV_FFN_OVERLAP_PREVIOUS, down as a programmatic dependent of gate/up,
         # measured slower: Qwen stage 201.5 vs 195.4 us, Phi-3.5 batch 1 123.8
         # vs 107.8 -- r3b; so the plain launch)
-        N.call("hv_expert_ffn_down", w, counts.data_ptr(), offs.data_ptr(), act.data_ptr(), y.data_ptr(), self.E,
-               H, I, stream)
+        N.call("hv_expert_ffn_down_ex", w, counts.data_ptr(), offs.data_ptr(), act.data_ptr(), y.data_ptr(), self.E,
+               H, I, self.ffn_flags, stream)
         # top-k combine in a fixed order (deterministic, no atomics)
         yt = y.index_select(0, pos).view(h.shape[0], self.m.top_k, H)
         return (yt * probs.unsqueeze(-1)).sum(1).to(h.dtype)

@@ -189,3 +189,24 @@ def layer_runs(src_b, src_s, dst_b, dst_s, page: int, n_layers: int, min_run_byt
     dst = (db[starts][None, :] + lay * ds[starts][None, :]).reshape(-1)
     nbytes = np.broadcast_to(lengths.astype(np.uint64) * pg, (n_layers, len(starts))).reshape(-1)
     return np.ascontiguousarray(src), np.ascontiguousarray(dst), np.ascontiguousarray(nbytes)
+
+
+def tile_expert_matrix(w: torch.Tensor, inverse: bool = False) -> torch.Tensor:
+    """The HV_FFN_TILED storage of one bf16 matrix [R][K] (R % 128 == 0,
+    K % 64 == 0): [R/128][K/64] tiles of 128 rows x 64 columns, 16 KiB each,
+    row r of a tile holding its 16-byte chunk c at chunk (c ^ (r & 7)) -- the
+    128B-swizzled K-major layout the tcgen05 K4 reads, so each tile is one
+    bulk copy.  Returns a new [R][K]-sized tensor of the same dtype holding
+    the tiled bytes; ``inverse=True`` turns tiled bytes back into the
+    row-major matrix.  Pure permutation: any device, no arithmetic."""
+    R, K = w.shape
+    if R % 128 or K % 64 or w.element_size() != 2:
+        raise ValueError("tiled expert matrices are 16-bit [R][K] with R % 128 == 0 and K % 64 == 0")
+    r = torch.arange(128, device=w.device)
+    c = torch.arange(8, device=w.device)
+    sw = c[None, :] ^ (r[:, None] & 7)          # [128, 8]: the XOR is its own inverse
+    if not inverse:
+        t = w.reshape(R // 128, 128, K // 64, 8, 8).permute(0, 2, 1, 3, 4)    # [rb, kt, r, c, 8 elems]
+        return t[:, :, r[:, None], sw].contiguous().view(R, K)
+    t = w.reshape(R // 128, K // 64, 128, 8, 8)[:, :, r[:, None], sw]        # [rb, kt, r, c, 8]
+    return t.permute(0, 2, 1, 3, 4).contiguous().view(R, K)

@@ -141,6 +141,10 @@ class ExpertStore:
         self.host_device_id = host_device_id
         self.host = host_tier
         self.base_offset = base_offset
+        # byte layout of every copy of an expert: "row" (gate [I][H], up [I][H],
+        # down [H][I], row-major) or "tiled" (the same matrices as HV_FFN_TILED
+        # swizzled 128 x 64 tiles, for the tcgen05 K4's bulk-copy weight stream)
+        self.layout = "row"
 
     def host_offset(self, layer: int, expert: int) -> int:
         return self.base_offset + (layer * self.model.num_experts + expert) * self.model.expert_size
@@ -148,11 +152,20 @@ class ExpertStore:
     def host_segment(self, layer: int, expert: int) -> Segment:
         return Segment(self.host_offset(layer, expert), self.model.expert_size)
 
-    def fill_host(self, device: int = 0, layers=None, weights: bool = False) -> None:
+    def fill_host(self, device: int = 0, layers=None, weights: bool = False, layout: str = "row") -> None:
         """Write every expert's synthetic content into the pinned host tier
         (the fill kernel writes through the mapped alias over PCIe).
-        ``weights=True`` writes the bf16-weights variant (finite values)."""
+        ``weights=True`` writes the bf16-weights variant (finite values).
+        ``layout="tiled"`` then stores each matrix of those logical weights as
+        HV_FFN_TILED tiles (fetch.tile_expert_matrix); every later copy of the
+        expert (peer, staging) carries the same bytes."""
         m = self.model
+        if layout not in ("row", "tiled"):
+            raise ValueError(f"unknown expert layout {layout!r}")
+        if layout == "tiled" and not weights:
+            raise ValueError("the tiled layout is a layout of bf16 weights (weights=True)")
+        if layout == "tiled" and (m.hidden % 128 or m.intermediate % 128):
+            raise ValueError("tiled experts need hidden and intermediate sizes that are multiples of 128")
         layers = range(m.num_layers) if layers is None else layers
         fill = F.fill_weights_bf16 if weights else F.fill_content
         for layer in layers:
@@ -160,6 +173,20 @@ class ExpertStore:
             fill(F.ptrs_tensor(ptrs, f"cuda:{device}"), F.ptrs_tensor([m.expert_size] * m.num_experts, f"cuda:{device}"),
                  [expert_content(m, layer, e) for e in range(m.num_experts)])
         torch.cuda.synchronize(device)
+        if layout == "tiled":
+            view = self.host.view()
+            H, I = m.hidden, m.intermediate
+            for layer in layers:
+                for e in range(m.num_experts):
+                    o = self.host_offset(layer, e)
+                    cpu = torch.from_numpy(view[o:o + m.expert_size])          # aliases the pinned host tier
+                    w = cpu.to(f"cuda:{device}").view(torch.bfloat16)
+                    t = torch.cat([F.tile_expert_matrix(w[:I * H].view(I, H)).reshape(-1),
+                                   F.tile_expert_matrix(w[I * H:2 * I * H].view(I, H)).reshape(-1),
+                                   F.tile_expert_matrix(w[2 * I * H:].view(H, I)).reshape(-1)])
+                    cpu.copy_(t.view(torch.uint8))
+            torch.cuda.synchronize(device)
+        self.layout = layout
 
     def host_digests(self, device: int = 0) -> np.ndarray:
         """Digest of every expert's authoritative host copy ([L, E] uint64,

@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 RS = 256.0  # residual scale: makes the tiny MoE delta visible in bf16 (power of two: exact)
 
 
-def _setup(model, peer_experts, microbatches=2, tokens=16, seed=0):
+def _setup(model, peer_experts, microbatches=2, tokens=16, seed=0, layout="row"):
     from paper_2602_00328_b200.decode import MoEDecoder
     from paper_2602_00328_b200.moe import ExpertFetcher, ExpertResidency, ExpertStore, rebalance
     from paper_2602_00328_b200.system import HarvestSystem
@@ -20,7 +20,7 @@ def _setup(model, peer_experts, microbatches=2, tokens=16, seed=0):
     sysm = HarvestSystem(0, donors=[0], donor_bytes=max(1, peer_experts) * S, host_bytes=L * E * S,
                          local_bytes=1 << 20)
     store = ExpertStore(model, sysm.host_id, sysm.host)
-    store.fill_host(0, weights=True)
+    store.fill_host(0, weights=True, layout=layout)
     res = ExpertResidency(model)
     counts = np.ones((L, E), dtype=np.int64)
     if peer_experts:
@@ -45,6 +45,7 @@ def _all_local(model, tokens, microbatches, seed, host_store):
         for e in range(E):
             res.set_tier(layer, e, Tier.LOCAL_HBM)
     store = ExpertStore(model, sysm.host_id, None)
+    store.layout = host_store.layout          # the resident copy holds the host tier's bytes
     local_addr = [[resident.data_ptr() + (layer * E + e) * S for e in range(E)] for layer in range(L)]
     fetcher = ExpertFetcher(sysm.runtime, model, res, store, local_addr=local_addr)
     dec = MoEDecoder(fetcher, tokens=tokens, microbatches=microbatches, seed=seed, residual_scale=RS)
@@ -215,6 +216,103 @@ def test_fused_ffn_kernels_match_fp32(H, I, counts):
             y_ref = down @ a_got                        # exact bf16 inputs the kernel saw
             assert (y[p].cpu() - y_ref).abs().max() <= 1e-3 * y_ref.abs().max() + 1e-6, (e, j)
     assert S == W[0].numel() * 2
+
+
+@pytest.mark.parametrize("H,I,counts", [(256, 128, [3, 0, 1, 8, 64, 17]), (2048, 1408, [2, 5, 0, 1, 9, 33]),
+                                        (4096, 6400, [1, 0, 2])])
+def test_fused_ffn_tiled_layout_equals_row_major(H, I, counts):
+    """HV_FFN_TILED: the same experts stored as swizzled 128 x 64 tiles
+    (fetch.tile_expert_matrix), each tile one bulk copy on the TMA engine.
+    The tiles land in shared memory byte for byte where the row-major form's
+    cp.async puts them, so act and y are bitwise those of the row-major form."""
+    from paper_2602_00328_b200 import _native as N
+    from paper_2602_00328_b200 import fetch as F
+    g = torch.Generator().manual_seed(7 + H + I)
+    E, T = len(counts), 64
+    W = (torch.randn(E, 3 * H * I, generator=g) * 0.03).to(torch.bfloat16).cuda()
+    Wt = torch.empty_like(W)
+    for e in range(E):
+        Wt[e, :I * H] = F.tile_expert_matrix(W[e, :I * H].view(I, H)).reshape(-1)
+        Wt[e, I * H:2 * I * H] = F.tile_expert_matrix(W[e, I * H:2 * I * H].view(I, H)).reshape(-1)
+        Wt[e, 2 * I * H:] = F.tile_expert_matrix(W[e, 2 * I * H:].view(H, I)).reshape(-1)
+    assert torch.equal(F.tile_expert_matrix(Wt[0, 2 * I * H:].view(H, I), inverse=True), W[0, 2 * I * H:].view(H, I))
+    x = (torch.randn(T, H, generator=g)).to(torch.bfloat16).cuda()
+    cnt = torch.tensor(counts, dtype=torch.int32)
+    offs = torch.cumsum(cnt, 0, dtype=torch.int32) - cnt
+    P = int(cnt.sum())
+    tok = torch.cat([torch.randperm(T, generator=g)[:c] for c in counts]).to(torch.int32).cuda()
+    cnt_d, offs_d = cnt.cuda(), offs.cuda()
+    s = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for weights, flags in ((W, 0), (Wt, N.FFN_TILED)):
+        addr = torch.tensor([weights[e].data_ptr() for e in range(E)], dtype=torch.int64).cuda()
+        act = torch.full((P, I), float("nan"), dtype=torch.bfloat16, device="cuda")
+        y = torch.full((P, H), float("nan"), dtype=torch.float32, device="cuda")
+        N.call("hv_expert_ffn_gate_up_ex", addr.data_ptr(), cnt_d.data_ptr(), offs_d.data_ptr(), tok.data_ptr(),
+               x.data_ptr(), act.data_ptr(), E, H, I, flags, s)
+        N.call("hv_expert_ffn_down_ex", addr.data_ptr(), cnt_d.data_ptr(), offs_d.data_ptr(), act.data_ptr(),
+               y.data_ptr(), E, H, I, flags, s)
+        outs.append((act, y))
+    torch.cuda.synchronize()
+    assert not torch.isnan(outs[0][1]).any()
+    assert torch.equal(outs[0][0].view(torch.int16), outs[1][0].view(torch.int16))
+    assert torch.equal(outs[0][1].view(torch.int32), outs[1][1].view(torch.int32))
+
+
+def test_fused_ffn_tiled_layout_rejects_unsupported_shapes():
+    """Rows not a multiple of 128 (the mma.sync form's shapes) cannot take the
+    tiled layout: refused, not silently read as row-major."""
+    from paper_2602_00328_b200 import _native as N
+    E, H, I = 1, 256, 192
+    W = torch.zeros(E, 3 * H * I, dtype=torch.bfloat16, device="cuda")
+    addr = torch.tensor([W[0].data_ptr()], dtype=torch.int64).cuda()
+    one = torch.ones(1, dtype=torch.int32).cuda()
+    zero = torch.zeros(1, dtype=torch.int32).cuda()
+    x = torch.zeros(1, H, dtype=torch.bfloat16, device="cuda")
+    act = torch.zeros(1, I, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(N.HarvestNativeError):
+        N.call("hv_expert_ffn_gate_up_ex", addr.data_ptr(), one.data_ptr(), zero.data_ptr(), zero.data_ptr(),
+               x.data_ptr(), act.data_ptr(), E, H, I, N.FFN_TILED, torch.cuda.current_stream().cuda_stream)
+
+
+@pytest.mark.parametrize("microbatches", [1, 2])
+def test_tiled_experts_decode_equals_row_major(microbatches):
+    """Experts stored as HV_FFN_TILED tiles (ExpertStore.fill_host(layout=
+    "tiled")), half on the donor and half in the host tier: the fused decoder
+    (K4 in place, one bulk copy per weight tile) and the staged decoder (K2
+    into the staging slots, then K4 over them) are both bit-identical to the
+    fused decoder over the same logical weights stored row-major, and to the
+    tiled all-local run.  The host copy's bytes are the row-major bytes
+    permuted (fetch.tile_expert_matrix, inverse checked)."""
+    from paper_2602_00328_b200 import fetch as F
+    from paper_2602_00328_b200.decode import MoEDecoder
+    model = _tiny()
+    L, E, S, H, I = model.num_layers, model.num_experts, model.expert_size, model.hidden, model.intermediate
+    half = L * E // 2
+    sysm, store, res, fetcher, dec = _setup(model, peer_experts=half, microbatches=microbatches)
+    ref = MoEDecoder(fetcher, tokens=16, microbatches=microbatches, seed=0, residual_scale=RS, fused=True).decode(3)
+    tsys, tstore, tres, tfetcher, tdec = _setup(model, peer_experts=half, microbatches=microbatches, layout="tiled")
+    assert tstore.layout == "tiled" and tdec.tiled
+    row = torch.from_numpy(store.host.view()[:S].copy()).view(torch.bfloat16)
+    til = torch.from_numpy(tstore.host.view()[:S].copy()).view(torch.bfloat16)
+    assert not torch.equal(row, til)
+    assert torch.equal(F.tile_expert_matrix(til[2 * I * H:].view(H, I), inverse=True), row[2 * I * H:].view(H, I))
+    fused = MoEDecoder(tfetcher, tokens=16, microbatches=microbatches, seed=0, residual_scale=RS, fused=True)
+    out_f = fused.decode(3)
+    out_s = tdec.decode(3)
+    torch.cuda.synchronize()
+    assert torch.equal(out_f.view(torch.int16), ref.view(torch.int16))
+    assert torch.equal(out_s.view(torch.int16), ref.view(torch.int16))
+    sys2, _d2, keep = _all_local(model, 16, microbatches, 0, tstore)
+    out_l = MoEDecoder(_d2.f, tokens=16, microbatches=microbatches, seed=0, residual_scale=RS, fused=True).decode(3)
+    torch.cuda.synchronize()
+    assert torch.equal(out_l.view(torch.int16), ref.view(torch.int16))
+    if microbatches == 1:   # host plan (copy engine for host-tier experts) over tiled experts: the same bits
+        hp = MoEDecoder(tfetcher, tokens=16, microbatches=1, seed=0, residual_scale=RS, host_plan=True)
+        assert torch.equal(hp.decode(3).view(torch.int16), ref.view(torch.int16))
+    for s_ in (sysm, tsys):
+        s_.loop.run()
+    sysm.close(); tsys.close(); sys2.close()
 
 
 @pytest.mark.parametrize("microbatches", [1, 2])

@@ -58,11 +58,15 @@ def case(name, E, T, k, H, I, source):
     wbytes = active * S
     s = torch.cuda.current_stream().cuda_stream
 
-    def gate_up():
-        N.call("hv_expert_ffn_gate_up", addr.data_ptr(), counts.data_ptr(), offs.data_ptr(), tok.data_ptr(),
-               h.data_ptr(), act.data_ptr(), E, H, I, s)
+    # --tiled: the experts read as HV_FFN_TILED (random bytes either way, so
+    # the timing needs no re-layout; tests/test_gpu_decode.py checks the bits)
+    tiled = N.FFN_TILED if "--tiled" in sys.argv else 0
 
-    pdl = N.FFN_OVERLAP_PREVIOUS if "--pdl" in sys.argv else 0
+    def gate_up():
+        N.call("hv_expert_ffn_gate_up_ex", addr.data_ptr(), counts.data_ptr(), offs.data_ptr(), tok.data_ptr(),
+               h.data_ptr(), act.data_ptr(), E, H, I, tiled, s)
+
+    pdl = (N.FFN_OVERLAP_PREVIOUS if "--pdl" in sys.argv else 0) | tiled
 
     def down():
         N.call("hv_expert_ffn_down_ex", addr.data_ptr(), counts.data_ptr(), offs.data_ptr(), act.data_ptr(),
