@@ -41,7 +41,8 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 from benchlib.common import (KV_SLAB_BLOCKS, KV_TOKENS, METRIC, SEED, emit, kv_slab_bytes, load_peaks, load_traffic, model, routing, workload_config)  # noqa: E402
-from benchlib.compare import (autotune, measure_pcie_h2d, probe_engines_on_peer, same_run_comparisons)  # noqa: E402
+from benchlib.compare import (autotune, measure_pcie_h2d, measure_peer_copy, probe_engines_on_peer,  # noqa: E402
+                             same_run_comparisons)
 from benchlib.cpu import (cpu_gather_sample, cpu_host_copy, cpu_model, reference_simulator, run_reference)  # noqa: E402
 from benchlib.phases import (churn_phase, host_offload_decode, kv_decode_config1, kv_long_context,  # noqa: E402
                              offload_sweep_phase, phi_phase, run_decode)
@@ -420,11 +421,15 @@ def run_b200(a):
                     "frac": achieved / peak if peak else None,
                     "peak_source": "measured in this run: pinned host->device cudaMemcpyAsync, 1 GiB, best of 5"}
         else:
-            peak = 770.0
+            donor_dev = device_of(layout.donors_of(rank)[0])
+            meas = measure_peer_copy(dev, donor_dev)
+            peak = meas or 770.0
             roof = {"bound": "nvlink", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak,
-                    "peak_source": "B200_PROFILING.md fallback: measured peer copy 770 GB/s per direction "
-                                   "(900 nominal)"}
+                    "peak_source": (f"measured in this run: cudaMemcpyPeerAsync GPU {donor_dev} -> GPU {dev}, "
+                                    "256 MiB, best of 5" if meas else
+                                    "B200_PROFILING.md fallback: measured peer copy 770 GB/s per direction "
+                                    "(900 nominal); the donor is this GPU (single-GPU stand-in)")}
         roof["engine"] = a.engine
         if a.engine in ("ce", "auto") and source == "host":
             # the copy engine moves the host-tier experts: a DMA engine, not a
@@ -579,7 +584,8 @@ def north_star_targets(line, world):
     roof = line.get("roofline") or {}
     if world > 1:
         out["peer_fetch_frac_of_nvlink"] = {"value": roof.get("frac"), "target": ">= 0.80",
-                                            "source": "roofline.achieved / 770 GB/s per direction"}
+                                            "source": "roofline.achieved / roofline.peak (" +
+                                                      str(roof.get("peak_source", "")) + ")"}
     else:
         out["peer_fetch_frac_of_nvlink"] = {"value": None, "note": "N=1 has no donor: host tier only"}
     lat = line.get("single_expert_latency_us") or {}

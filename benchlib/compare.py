@@ -32,6 +32,33 @@ def measure_pcie_h2d(dev):
     h.close()
     return best
 
+def measure_peer_copy(dev, src_dev, nbytes=256 << 20):
+    """Peer -> this GPU copy-engine rate (cudaMemcpyPeerAsync through torch's
+    cross-device copy), best of 5, GB/s; None when the donor is this GPU (a
+    single-GPU stand-in) or the copy fails."""
+    import torch
+    if src_dev == dev:
+        return None
+    try:
+        src = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{src_dev}")
+        d = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{dev}")
+        s = torch.cuda.Stream(dev)
+        best = 0.0
+        with torch.cuda.stream(s):
+            for i in range(6):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                d.copy_(src, non_blocking=True)
+                e1.record(s)
+                e1.synchronize()
+                if i:
+                    best = max(best, nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        del src, d
+        return best or None
+    except Exception:   # noqa: BLE001 -- the fallback peak is reported instead
+        return None
+
+
 PROBE_CHILD = r"""
 import json, sys
 sys.path.insert(0, {repo!r})
