@@ -474,12 +474,27 @@ struct DigestOp {
   unsigned long long* out;
   __device__ __forceinline__ void operator()(const ChunkRef& r, uint32_t lane) const {
     const uint64_t w0 = r.off >> 3;
-    const uint32_t nfull = r.len >> 3;
-    const uint64_t* s = reinterpret_cast<const uint64_t*>(r.src);
     uint64_t acc = 0;
-    for (uint32_t k = lane; k < nfull; k += 32) acc += digest_term(w0 + k, s[k]);
-    const uint32_t tail = r.len & 7;
-    if (tail && lane == 0) acc += digest_term(w0 + nfull, load_word_tail(r.src + nfull * 8, tail));
+    if ((reinterpret_cast<uintptr_t>(r.src) & 15) == 0 && r.len == (uint32_t)kLdgUnroll * 512u) {
+      // a whole chunk: every lane's 128-bit loads in flight before any
+      // digest arithmetic (the 8-byte loop below leaves one load per lane in
+      // flight and stalls on it -- ncu r5c: long-scoreboard stalls dominant)
+      uint4 v[kLdgUnroll];
+#pragma unroll
+      for (int j = 0; j < kLdgUnroll; ++j) v[j] = ld_stream(r.src + (j * 32 + lane) * 16);
+#pragma unroll
+      for (int j = 0; j < kLdgUnroll; ++j) {
+        const uint64_t i = w0 + (uint64_t)(j * 32 + lane) * 2;
+        acc += digest_term(i, (uint64_t)v[j].x | ((uint64_t)v[j].y << 32));
+        acc += digest_term(i + 1, (uint64_t)v[j].z | ((uint64_t)v[j].w << 32));
+      }
+    } else {
+      const uint32_t nfull = r.len >> 3;
+      const uint64_t* s = reinterpret_cast<const uint64_t*>(r.src);
+      for (uint32_t k = lane; k < nfull; k += 32) acc += digest_term(w0 + k, s[k]);
+      const uint32_t tail = r.len & 7;
+      if (tail && lane == 0) acc += digest_term(w0 + nfull, load_word_tail(r.src + nfull * 8, tail));
+    }
     if (r.off == 0 && lane == 0) acc += __ldg(bytes + r.obj);
     acc = warp_sum(acc);
     if (lane == 0) atomicAdd(out + r.obj, (unsigned long long)acc);
