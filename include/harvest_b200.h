@@ -337,6 +337,36 @@ int hv_expert_ffn_down_ex(const uint64_t* d_w_addr, const int32_t* d_counts, con
                           const void* d_act, float* d_y, uint32_t n_experts, uint32_t hidden,
                           uint32_t intermediate, unsigned flags, void* stream);
 
+/* ---- MoE decode glue around K4: router and top-k combine ------------------ */
+/* The fused decoder's per-stage router (moe.py:315-340 stage semantics; the
+ * reference models the compute as a constant): logits =
+ * h . router^T in fp32 (d_h bf16 [tokens][hidden], d_router bf16
+ * [n_experts][hidden], 16-byte aligned), per token the top_k experts (largest
+ * first, ties to the lower id), softmax over their logits -> d_probs
+ * [tokens][top_k] and d_topi (int64), the routed pairs (t, j) sorted by expert
+ * (stable): d_counts / d_offs [n_experts], d_tok [tokens*top_k] (token of each
+ * sorted pair), d_pos [tokens*top_k] (sorted position of pair t*top_k + j) --
+ * the inputs of hv_expert_ffn_*.  d_logits: [tokens][n_experts] fp32 scratch;
+ * d_ticket: one unsigned, zero before the first launch (the kernel re-arms it),
+ * not shared by concurrent launches.  tokens <= 256, n_experts <= 256,
+ * top_k <= 8.  One launch. */
+int hv_moe_route(const void* d_h, const void* d_router, uint32_t tokens, uint32_t hidden, uint32_t n_experts,
+                 uint32_t top_k, float* d_logits, float* d_probs, int64_t* d_topi, int32_t* d_counts,
+                 int32_t* d_offs, int32_t* d_tok, int64_t* d_pos, unsigned* d_ticket, void* stream);
+/* h[t] <- h[t] + rs * bf16(sum_j probs[t][j] * y[pos[t*top_k + j]]) in bf16,
+ * j in order (deterministic); d_y fp32 [tokens*top_k][hidden] (K4 down's
+ * output), d_h bf16 [tokens][hidden] updated in place. */
+/* The fused decoder's staging plan for one stage: expert e is staged iff
+ * d_counts[e] > 0 and d_host[e] (its copy is in the pinned host tier); staged
+ * experts take consecutive slots of slot_bytes from slot_base in expert order:
+ * d_dst[e] / d_sizes[e] (0 when not staged) describe its K2 fetch and
+ * d_addr_out[e] is where K4 then reads it (the slot, or d_addr[e] in place). */
+int hv_moe_stage_plan(const int32_t* d_counts, const uint64_t* d_addr, const uint8_t* d_host, uint64_t slot_base,
+                      uint64_t slot_bytes, uint32_t n_experts, uint64_t* d_dst, uint64_t* d_sizes,
+                      uint64_t* d_addr_out, void* stream);
+int hv_moe_combine(const float* d_y, const float* d_probs, const int64_t* d_pos, void* d_h, uint32_t tokens,
+                   uint32_t hidden, uint32_t top_k, float residual_scale, void* stream);
+
 /* ---- paged decode attention over KV pages in any tier -------------------- */
 /* One query token per sequence, grouped-query (q_heads = g * kv_heads,
  * g in {1, 2, 4, 8}), head_dim 64 or 128, 16-token blocks.  d_page_ptrs holds

@@ -16,7 +16,7 @@ REPO_DIR = os.path.dirname(PKG_DIR)
 CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_NAME = "libharvest_b200.so"
 LIB_PATH = os.path.join(PKG_DIR, LIB_NAME)
-SOURCES = ["hv_kernels.cu", "hv_ffn.cu", "hv_attn.cu", "hv_pool.cpp", "hv_segalloc.cpp", "hv_place.cpp"]
+SOURCES = ["hv_kernels.cu", "hv_ffn.cu", "hv_attn.cu", "hv_moe.cu", "hv_pool.cpp", "hv_segalloc.cpp", "hv_place.cpp"]
 GENCODE = "arch=compute_100a,code=sm_100a"
 
 

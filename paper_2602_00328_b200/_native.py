@@ -151,6 +151,9 @@ _SIGS = {
     "hv_expert_ffn_max_tokens": [C.POINTER(i32)],
     "hv_expert_ffn_down_ex": [u64, u64, u64, u64, u64, u32, u32, u32, C.c_uint, vp],
     "hv_expert_ffn_gate_up_ex": [u64, u64, u64, u64, u64, u64, u32, u32, u32, C.c_uint, vp],
+    "hv_moe_route": [u64, u64, u32, u32, u32, u32, u64, u64, u64, u64, u64, u64, u64, u64, vp],
+    "hv_moe_combine": [u64, u64, u64, u64, u32, u32, u32, C.c_float, vp],
+    "hv_moe_stage_plan": [u64, u64, u64, u64, u64, u32, u64, u64, u64, vp],
     "hv_paged_decode_attention": [u64, u64, u64, u64, u64, u64, u32, u32, u32, u32, u32, u32, C.c_float, vp],
     "hv_paged_decode_attention_ex": [u64, u64, u64, u64, u64, u64, u32, u32, u32, u32, u32, u32, C.c_float,
                                      C.c_uint, vp],

@@ -49,6 +49,10 @@ from .moe import ExpertFetcher
 
 
 class MoEDecoder:
+    # router / top-k / pair sort and the top-k combine + residual as library
+    # kernels (hv_moe_route, hv_moe_combine); False: the torch ops (A/B)
+    glue = True
+
     def __init__(self, fetcher: ExpertFetcher, tokens: int, microbatches: int = 1, seed: int = 0,
                  engine: str = "auto", max_ctas: int = 0, router_scale: float = 0.5,
                  residual_scale: float = 1.0, trace: bool = False, fused: bool = False,
@@ -101,6 +105,11 @@ class MoEDecoder:
             if self.I % 64 or self.H % 64:
                 raise ValueError("K4 decode needs hidden and intermediate sizes that are multiples of 64")
         self.ffn_flags = N.FFN_TILED if self.tiled else 0
+        # router logits scratch and the route kernel's arrival ticket (zeroed
+        # here; the kernel re-arms it); the routed pairs of each staging slot
+        self._logits = torch.empty(self.tmb * self.E, dtype=torch.float32, device=self.dev)
+        self._ticket = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self._pairs = [None, None]
         # fused mode reads peer / local experts in place; only host-tier
         # experts are staged (one buffer: K2 and K4 run in order on one stream)
         self.staging = [torch.zeros(self.K, self.S, dtype=torch.uint8, device=self.dev)
@@ -181,15 +190,22 @@ class MoEDecoder:
 
     # ---------------------------------------------------------------- pieces
     def _route(self, h: torch.Tensor, layer: int, slot: int) -> None:
-        logits = (h @ self.router[layer].t()).float()
-        topv, topi = logits.topk(self.m.top_k, dim=1)
-        if self._counts is not None:
-            self._counts[layer].index_add_(0, topi.reshape(-1), torch.ones_like(topi.reshape(-1)))
-        probs = torch.softmax(topv, dim=1)
         comb = self.comb[slot]
         comb.zero_()
-        comb.scatter_(1, topi, probs)
-        active = (comb > 0).any(dim=0)
+        if self.glue:
+            probs, topi, counts, offs, tok, pos = self._route_k(h, layer)
+            self._pairs[slot] = (probs, counts, offs, tok, pos)   # K4 over tiled staging slots reuses them
+            comb.scatter_(1, topi, probs)
+            active = counts > 0
+        else:
+            logits = (h @ self.router[layer].t()).float()
+            topv, topi = logits.topk(self.m.top_k, dim=1)
+            if self._counts is not None:
+                self._counts[layer].index_add_(0, topi.reshape(-1), torch.ones_like(topi.reshape(-1)))
+            probs = torch.softmax(topv, dim=1)
+            comb.scatter_(1, topi, probs)
+            active = (comb > 0).any(dim=0)
+            self._pairs[slot] = None
         torch.where(active, torch.full_like(self.sizes[slot], self.S), torch.zeros_like(self.sizes[slot]),
                     out=self.sizes[slot])
         # compact placement: rank among active experts -> staging slot; the
@@ -203,12 +219,13 @@ class MoEDecoder:
         torch.lt(self._kslots, active.sum(), out=self.valid[slot])
 
     def _ffn(self, h: torch.Tensor, slot: int, buf: int, layer: int) -> torch.Tensor:
+        """The stage's expert FFN over the staging slots; returns the new h
+        (h + residual_scale * moe(h))."""
         if self.tiled:
             # K4 over the staging slots: dst_ptrs[slot][e] is active expert e's
-            # slot (the routing is _route's, recomputed on the same inputs)
-            probs, counts, offs, tok, pos = self._route_pairs(h, layer, count=False)
-            return self._k4(h, self.dst_ptrs[slot], probs, counts, offs, tok, pos,
-                            torch.cuda.current_stream(self.dev).cuda_stream)
+            # slot; the routed pairs are _route's (or recomputed on the same inputs)
+            pr = self._pairs[slot] if self._pairs[slot] is not None else self._route_pairs(h, layer, count=False)
+            return self._k4(h, self.dst_ptrs[slot], *pr, torch.cuda.current_stream(self.dev).cuda_stream)
         K, I, H = self.K, self.I, self.H
         w = self.staging[buf].view(torch.bfloat16).view(K, 3 * I * H)
         gate = w[:, :I * H].view(K, I, H)
@@ -221,7 +238,10 @@ class MoEDecoder:
         # bytes) get weight exactly 0
         wk = self.comb[slot].index_select(1, self.idx[slot]) * self.valid[slot].to(torch.float32)
         wts = wk.t().unsqueeze(-1).to(y.dtype)                       # [K, T, 1]
-        return (y * wts).sum(0)
+        return self._residual(h, (y * wts).sum(0))
+
+    def _residual(self, h: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
+        return h + (y * self.residual_scale if self.residual_scale != 1.0 else y)
 
     def _issue_fetch(self, s: int, ready: torch.cuda.Event, buf_free: torch.cuda.Event | None) -> torch.cuda.Event:
         layer, _ = self.stages[s]
@@ -397,12 +417,11 @@ class MoEDecoder:
                 if self.trace:
                     cs = torch.cuda.Event(enable_timing=True)
                     cs.record(self.compute)
-                y = self._ffn(hs[mb], slot, buf, layer)
+                hs[mb] = self._ffn(hs[mb], slot, buf, layer)
                 if self.trace:
                     ce = torch.cuda.Event(enable_timing=True)
                     ce.record(self.compute)
                     self._tr.setdefault(s, {})["compute"] = (cs, ce)
-                hs[mb] = hs[mb] + (y * self.residual_scale if self.residual_scale != 1.0 else y)
                 done = torch.cuda.Event()
                 done.record(self.compute)
                 buf_free[buf] = done
@@ -420,10 +439,39 @@ class MoEDecoder:
         return torch.stack(hs).view(self.T, self.H)
 
     # ---------------------------------------------------------------- fused
+    def _route_k(self, h: torch.Tensor, layer: int):
+        """hv_moe_route: router logits (fp32), top-k, softmax and the routed
+        pairs sorted by expert in one launch."""
+        if not h.is_contiguous():
+            h = h.contiguous()
+        T, k, E = h.shape[0], self.m.top_k, self.E
+        probs = torch.empty(T, k, dtype=torch.float32, device=self.dev)
+        topi = torch.empty(T, k, dtype=torch.int64, device=self.dev)
+        counts = torch.empty(E, dtype=torch.int32, device=self.dev)
+        offs = torch.empty(E, dtype=torch.int32, device=self.dev)
+        tok = torch.empty(T * k, dtype=torch.int32, device=self.dev)
+        pos = torch.empty(T * k, dtype=torch.int64, device=self.dev)
+        N.call("hv_moe_route", h.data_ptr(), self.router[layer].data_ptr(), T, self.H, E, k,
+               self._logits.data_ptr(), probs.data_ptr(), topi.data_ptr(), counts.data_ptr(), offs.data_ptr(),
+               tok.data_ptr(), pos.data_ptr(), self._ticket.data_ptr(), torch.cuda.current_stream(self.dev).cuda_stream)
+        if self._counts is not None:
+            self._counts[layer].index_add_(0, topi.reshape(-1), torch.ones_like(topi.reshape(-1)))
+        return probs, topi, counts, offs, tok, pos
+
+    def _route_k_nocount(self, h: torch.Tensor, layer: int):
+        saved, self._counts = self._counts, None
+        try:
+            return self._route_k(h, layer)
+        finally:
+            self._counts = saved
+
     def _route_pairs(self, h: torch.Tensor, layer: int, count: bool = True):
         """Router -> top-k -> routed pairs sorted by expert, all on the device:
         counts/offsets per expert, the token row of each sorted pair, and the
         sorted position of pair (t, j) for the combine."""
+        if self.glue:
+            probs, _topi, counts, offs, tok, pos = self._route_k(h, layer) if count else self._route_k_nocount(h, layer)
+            return probs, counts, offs, tok, pos
         k = self.m.top_k
         logits = (h @ self.router[layer].t()).float()
         topv, topi = logits.topk(k, dim=1)
@@ -448,13 +496,21 @@ class MoEDecoder:
             # host-tier experts: K2 over PCIe into compact local slots first
             # (sequential reads, the PCIe-efficient path), then K4 reads those
             # slots and every peer / local expert in place
-            stage = (counts > 0) & self.hosttier[layer]
-            rank = torch.cumsum(stage.to(torch.int64), 0) - 1
-            dst = torch.where(stage, rank * self.S + self.slot_base[0], 0)
-            sizes = torch.where(stage, self.S, 0)
+            if self.glue:
+                dst = torch.empty(self.E, dtype=torch.int64, device=self.dev)
+                sizes = torch.empty_like(dst)
+                staged = torch.empty_like(dst)
+                N.call("hv_moe_stage_plan", counts.data_ptr(), addr.data_ptr(), self.hosttier[layer].data_ptr(),
+                       self.slot_base[0], self.S, self.E, dst.data_ptr(), sizes.data_ptr(), staged.data_ptr(), stream)
+            else:
+                stage = (counts > 0) & self.hosttier[layer]
+                rank = torch.cumsum(stage.to(torch.int64), 0) - 1
+                dst = torch.where(stage, rank * self.S + self.slot_base[0], 0)
+                sizes = torch.where(stage, self.S, 0)
+                staged = torch.where(stage, dst, addr)
             N.call("hv_batch_copy", addr.data_ptr(), dst.data_ptr(), sizes.data_ptr(), self.E, self.engine_id,
                    self.max_ctas, stream)
-            addr = torch.where(stage, dst, addr)
+            addr = staged
         return self._k4(h, addr, probs, counts, offs, tok, pos, stream)
 
     def _k4(self, h, addr, probs, counts, offs, tok, pos, stream) -> torch.Tensor:
@@ -471,9 +527,15 @@ class MoEDecoder:
         # vs 107.8 -- r3b; so the plain launch)
         N.call("hv_expert_ffn_down_ex", w, counts.data_ptr(), offs.data_ptr(), act.data_ptr(), y.data_ptr(), self.E,
                H, I, self.ffn_flags, stream)
-        # top-k combine in a fixed order (deterministic, no atomics)
+        # top-k combine in a fixed order (deterministic, no atomics), plus the residual
+        if self.glue:
+            if not h.is_contiguous():
+                h = h.contiguous()
+            N.call("hv_moe_combine", y.data_ptr(), probs.data_ptr(), pos.data_ptr(), h.data_ptr(), h.shape[0], H,
+                   self.m.top_k, float(self.residual_scale), stream)
+            return h
         yt = y.index_select(0, pos).view(h.shape[0], self.m.top_k, H)
-        return (yt * probs.unsqueeze(-1)).sum(1).to(h.dtype)
+        return self._residual(h, (yt * probs.unsqueeze(-1)).sum(1).to(h.dtype))
 
     def _step_fused(self, x: torch.Tensor) -> torch.Tensor:
         hs = list(x.view(self.nmb, self.tmb, self.H).clone().unbind(0))
@@ -486,12 +548,11 @@ class MoEDecoder:
                 if self.trace:
                     cs = torch.cuda.Event(enable_timing=True)
                     cs.record(self.compute)
-                y = self._ffn_fused(hs[mb], layer)
+                hs[mb] = self._ffn_fused(hs[mb], layer)
                 if self.trace:
                     ce = torch.cuda.Event(enable_timing=True)
                     ce.record(self.compute)
                     self._tr.setdefault(s, {})["fused"] = (cs, ce)
-                hs[mb] = hs[mb] + (y * self.residual_scale if self.residual_scale != 1.0 else y)
         cur.wait_stream(self.compute)
         done = torch.cuda.Event()
         done.record(cur)
