@@ -21,8 +21,15 @@
  *    that served it, the expected destination bytes of a batched
  *    fetch are the host-authoritative bytes of each object: a memcpy gather.
  *  - Digest.  A position-keyed 64-bit sum used for size-independent checks at
- *    full sizes: D = size + sum_i fmix64(w_i ^ ((i+1) * 0xD1B54A32D192ED03))
- *    over little-endian 8-byte words, the last one zero-padded.
+ *    full sizes: D = size + sum_i a_i * b_i (mod 2^64) over little-endian
+ *    8-byte words w_i (the last one zero-padded), with j = (i+1) mod 2^32 and
+ *    a_i = lo32(w_i) + j*0x9E3779B1, b_i = hi32(w_i) + j*0x85EBCA77 +
+ *    0xC2B2AE3D (32-bit wrapping), the product exact in 64 bits -- the NH
+ *    hash of UMAC (Black, Halevi, Krawczyk, Krovetz, Rogaway, CRYPTO 1999)
+ *    with fixed position keys.  Not a restatement of a reference function:
+ *    the reference compares one 64-bit content hash per object
+ *    (moe.py:315-319); this is the B200 build's byte-level counterpart, and
+ *    the device kernels (csrc/hv_kernels.cu digest_term) must equal it.
  */
 #include <pthread.h>
 #include <stdint.h>
@@ -30,7 +37,16 @@
 #include <string.h>
 
 #define HVO_GOLDEN 0x9E3779B97F4A7C15ull
-#define HVO_DKEY 0xD1B54A32D192ED03ull
+#define HVO_DKEY_A 0x9E3779B1u
+#define HVO_DKEY_B 0x85EBCA77u
+#define HVO_DKEY_C 0xC2B2AE3Du
+
+static inline uint64_t digest_term(uint64_t i, uint64_t w) {
+  const uint32_t j = (uint32_t)(i + 1);
+  const uint32_t a = (uint32_t)w + j * HVO_DKEY_A;
+  const uint32_t b = (uint32_t)(w >> 32) + j * HVO_DKEY_B + HVO_DKEY_C;
+  return (uint64_t)a * (uint64_t)b;
+}
 
 static inline uint64_t fmix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -74,13 +90,13 @@ uint64_t hvo_digest(const uint8_t* src, uint64_t bytes) {
   for (uint64_t i = 0; i < nfull; ++i) {
     uint64_t w;
     memcpy(&w, src + 8 * i, 8);
-    acc += fmix64(w ^ ((i + 1) * HVO_DKEY));
+    acc += digest_term(i, w);
   }
   const uint64_t tail = bytes & 7;
   if (tail) {
     uint64_t w = 0;
     for (uint64_t b = 0; b < tail; ++b) w |= (uint64_t)src[8 * nfull + b] << (8 * b);
-    acc += fmix64(w ^ ((nfull + 1) * HVO_DKEY));
+    acc += digest_term(nfull, w);
   }
   return acc;
 }
@@ -89,11 +105,11 @@ uint64_t hvo_digest(const uint8_t* src, uint64_t bytes) {
 uint64_t hvo_content_digest(uint64_t seed, uint64_t bytes) {
   uint64_t acc = bytes;
   const uint64_t nfull = bytes / 8;
-  for (uint64_t i = 0; i < nfull; ++i) acc += fmix64(hvo_content_word(seed, i) ^ ((i + 1) * HVO_DKEY));
+  for (uint64_t i = 0; i < nfull; ++i) acc += digest_term(i, hvo_content_word(seed, i));
   const uint64_t tail = bytes & 7;
   if (tail) {
     const uint64_t mask = (1ull << (8 * tail)) - 1;
-    acc += fmix64((hvo_content_word(seed, nfull) & mask) ^ ((nfull + 1) * HVO_DKEY));
+    acc += digest_term(nfull, hvo_content_word(seed, nfull) & mask);
   }
   return acc;
 }

@@ -98,7 +98,7 @@ constexpr uint32_t kPageBatchMax = 1u << 30;
 // splitmix64 (Steele, Lea, Flood 2014) — the synthetic content generator; the
 // seed is stable_hash64(tag) (runtime.py:38-44, moe.py:114-115).
 constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
-constexpr uint64_t kDigestKey = 0xD1B54A32D192ED03ull;
+constexpr uint32_t kDigestKeyA = 0x9E3779B1u, kDigestKeyB = 0x85EBCA77u, kDigestKeyC = 0xC2B2AE3Du;
 
 __host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -108,8 +108,18 @@ __host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
 __host__ __device__ __forceinline__ uint64_t content_word(uint64_t seed, uint64_t i) {
   return fmix64(seed + (i + 1) * kGolden);
 }
+// Content digest term of 8-byte word i (oracle hvo_digest): an NH-style
+// product (Black et al., UMAC, CRYPTO 1999) of the word's two 32-bit halves,
+// each offset by a position key, exact in 64 bits.  A changed word changes its
+// term unless the other half's keyed value is 0 (probability 2^-32); the
+// digest is size + the sum of the terms mod 2^64.  ~6 instructions per word
+// (two IMAD, one IMAD.WIDE.U32, a 64-bit add) where a 64-bit finalizer took
+// ~25 and left the content check ALU-bound (ncu r5n: ALU pipe 61% at 3.7 TB/s).
 __host__ __device__ __forceinline__ uint64_t digest_term(uint64_t i, uint64_t w) {
-  return fmix64(w ^ ((i + 1) * kDigestKey));
+  const uint32_t j = (uint32_t)(i + 1);
+  const uint32_t a = (uint32_t)w + j * kDigestKeyA;
+  const uint32_t b = (uint32_t)(w >> 32) + j * kDigestKeyB + kDigestKeyC;
+  return (uint64_t)a * (uint64_t)b;
 }
 
 // ---------------------------------------------------------------------------
@@ -687,6 +697,124 @@ __global__ void __launch_bounds__(kTmaThreads) desc_copy_tma(DescResolver res) {
 }
 
 constexpr size_t kTmaSmem = (size_t)kTmaStages * kTmaChunk;
+
+// Content check (DigestOp) on the TMA engine: lane 0 of a producer warp
+// streams the CTA's chunks into a ring of shared-memory stages with bulk
+// copies; each consumer warp digests whole chunks (chunk t of the CTA goes to
+// warp t mod W) from shared memory -- a lane's 16-byte units are contiguous
+// across the warp, conflict-free LDS.128, many independent units per lane --
+// and releases the stage.  The loads no longer wait behind the digest
+// arithmetic of the same warp (the LDG form's limit: ncu r5c, long-scoreboard
+// stalls, 3.4 TB/s).  Each warp keeps its running sum per object in a
+// register and adds it to the object's accumulator when the object changes.
+// Same digest as DigestOp, bit for bit.  Splitting every chunk over all
+// consumer warps (r5n-r5p) was slower: 8 / 12 / 16 warps 0.213 / 0.268 /
+// 0.306 ms per Qwen stage -- the per-chunk resolve, barrier and reduction
+// then dominate.
+#ifndef HV_DG_CONSUMERS
+#define HV_DG_CONSUMERS 6
+#endif
+#ifndef HV_DG_STAGES
+#define HV_DG_STAGES 6
+#endif
+#ifndef HV_DG_CHUNK
+#define HV_DG_CHUNK 16384
+#endif
+constexpr int kDgConsumers = HV_DG_CONSUMERS;
+constexpr int kDgThreads = (kDgConsumers + 1) * 32;
+constexpr int kDgStages = HV_DG_STAGES;
+constexpr uint32_t kDgChunk = HV_DG_CHUNK;
+constexpr size_t kDgSmem = (size_t)kDgStages * kDgChunk;
+// chunk t and chunk t + S share a stage; with S a multiple of W they also
+// share the consumer warp, which has therefore seen the stage's previous
+// phase complete before it waits on the next one (an mbarrier parity wait
+// cannot tell phase r from phase r - 2: measured as launch failures with
+// W = 4, S = 6 and W = 8, S = 12)
+static_assert(kDgStages % kDgConsumers == 0, "digest ring: stages must be a multiple of the consumer warps");
+
+__global__ void __launch_bounds__(kDgThreads) desc_digest_tma(DescResolver res, const uint64_t* __restrict__ bytes,
+                                                              unsigned long long* __restrict__ out) {
+  extern __shared__ __align__(128) char ring[];
+  __shared__ __align__(8) uint64_t full[kDgStages], empty[kDgStages];
+  __shared__ uint32_t s_start[kDescSmemWords];
+  const uint32_t total = res.setup(s_start);
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kDgStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t G = gridDim.x;
+  const uint32_t mine = blockIdx.x < total ? (total - blockIdx.x + G - 1) / G : 0;
+  if (warp == kDgConsumers) {   // producer
+    if (lane == 0) {
+      uint32_t hint = 0;
+      for (uint32_t t = 0; t < mine; ++t) {
+        const uint32_t st = t % kDgStages, round = t / kDgStages;
+        if (round > 0) mbar_wait(&empty[st], (round - 1) & 1);
+        const ChunkRef r = res.at(blockIdx.x + t * G, hint, s_start);
+        if (tma_ok(r)) {
+          mbar_expect_tx(&full[st], r.len);
+          bulk_g2s(ring + (size_t)st * kDgChunk, r.src, r.len, &full[st]);
+        } else {   // digested from global by its consumer; keep the phase sequence
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[st])) : "memory");
+        }
+      }
+    }
+    return;
+  }
+  uint32_t hint = 0, cur_obj = 0xFFFFFFFFu;
+  uint64_t run = 0;
+  for (uint32_t t = warp; t < mine; t += kDgConsumers) {
+    const uint32_t st = t % kDgStages;
+    const ChunkRef r = res.at(blockIdx.x + t * G, hint, s_start);
+    mbar_wait(&full[st], (t / kDgStages) & 1);
+    const uint64_t w0 = r.off >> 3;
+    uint64_t acc = 0;
+    if (tma_ok(r)) {
+      const char* sb = ring + (size_t)st * kDgChunk;
+#pragma unroll 8
+      for (uint32_t u = lane; u < r.len / 16; u += 32) {
+        const uint4 v = *reinterpret_cast<const uint4*>(sb + (size_t)u * 16);
+        const uint64_t i = w0 + (uint64_t)u * 2;
+        acc += digest_term(i, (uint64_t)v.x | ((uint64_t)v.y << 32));
+        acc += digest_term(i + 1, (uint64_t)v.z | ((uint64_t)v.w << 32));
+      }
+    } else {
+      const uint32_t nfull = r.len >> 3;
+      for (uint32_t k = lane; k < nfull; k += 32) {
+        uint64_t w = 0;
+        memcpy(&w, r.src + (size_t)k * 8, 8);
+        acc += digest_term(w0 + k, w);
+      }
+      const uint32_t tail = r.len & 7;
+      if (tail && lane == 0) acc += digest_term(w0 + nfull, load_word_tail(r.src + nfull * 8, tail));
+    }
+    if (r.off == 0 && lane == 0) acc += __ldg(bytes + r.obj);
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
+    if (r.obj != cur_obj) {
+      if (cur_obj != 0xFFFFFFFFu) {
+        const uint64_t tot = warp_sum(run);
+        if (lane == 0) atomicAdd(out + cur_obj, (unsigned long long)tot);
+      }
+      cur_obj = r.obj;
+      run = 0;
+    }
+    run += acc;
+  }
+  if (cur_obj != 0xFFFFFFFFu) {
+    const uint64_t tot = warp_sum(run);
+    if (lane == 0) atomicAdd(out + cur_obj, (unsigned long long)tot);
+  }
+}
+
+#ifndef HV_DIGEST_TMA
+#define HV_DIGEST_TMA 1
+#endif
 
 // ---------------------------------------------------------------------------
 // launch helpers
@@ -1325,10 +1453,29 @@ HV_EXPORT int hv_check_digests(const uint64_t* d_src, const uint64_t* d_bytes, c
   int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
   HV_CUDA(cudaMemsetAsync(d_scratch, 0, (size_t)n * 8, (cudaStream_t)stream));
+#if HV_DIGEST_TMA
+  if ((st = hv::kernel_attr<desc_digest_tma>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDgSmem)))
+    return st;
+  for (uint32_t base = 0; base < n; base += kMaxSmemDescs) {
+    const uint32_t m = (n - base) < kMaxSmemDescs ? (n - base) : kMaxSmemDescs;
+    DescResolver res;
+    res.src = d_src + base;
+    res.dst = d_src + base;
+    res.bytes = d_bytes + base;
+    res.n = m;
+    res.interleave = 0;
+    res.chunk = kDgChunk;
+    desc_digest_tma<<<2 * hv::sm_count(dev), kDgThreads, kDgSmem, (cudaStream_t)stream>>>(
+        res, d_bytes + base, reinterpret_cast<unsigned long long*>(d_scratch) + base);
+    HV_CUDA(cudaGetLastError());
+    hv::note_launch();
+  }
+#else
   DigestOpR op;
   op.bytes = d_bytes;
   op.out = reinterpret_cast<unsigned long long*>(d_scratch);
   if ((st = launch_descs(d_src, d_src, d_bytes, n, HV_ENGINE_LDG, 0, stream, op, false))) return st;
+#endif
   digest_compare_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
       d_scratch, d_expected, n, d_flags, reinterpret_cast<unsigned long long*>(d_errors));
   HV_CUDA(cudaGetLastError());

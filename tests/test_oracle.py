@@ -135,3 +135,32 @@ def test_resolve_fallback_spec_examples():
     e_star = a / (r - b / B)
     assert O.resolve_fallback(int(e_star) + 2, b, r, a, B, True) == "FetchFromHost"
     assert O.resolve_fallback(max(1, int(e_star) - 2), b, r, a, B, True) == "Recompute"
+
+
+def _nh_digest_py(buf: bytes) -> int:
+    """The digest's definition (oracle/hv_oracle.c header) in plain Python."""
+    M32, M64 = (1 << 32) - 1, (1 << 64) - 1
+    acc = len(buf)
+    for i in range(0, len(buf), 8):
+        w = int.from_bytes(buf[i:i + 8].ljust(8, b"\0"), "little")
+        j = (i // 8 + 1) & M32
+        a = ((w & M32) + j * 0x9E3779B1) & M32
+        b = ((w >> 32) + j * 0x85EBCA77 + 0xC2B2AE3D) & M32
+        acc = (acc + a * b) & M64
+    return acc
+
+
+@pytest.mark.parametrize("n", [0, 5, 8, 64, 1001])
+def test_digest_matches_its_definition(n):
+    """The C digest (and so the device kernels, which tests/test_gpu_fetch.py
+    compares with it) equals the NH definition written out in Python; a single
+    changed word, two swapped words, or a page moved by one word all change it."""
+    seed = O.expert_seed("nh", 1, n)
+    buf = O.content(seed, n)
+    assert O.digest(buf) == _nh_digest_py(buf.tobytes()) == O.content_digest(seed, n)
+    if n >= 16:
+        swapped = buf.copy()
+        swapped[0:8], swapped[8:16] = buf[8:16].copy(), buf[0:8].copy()
+        assert O.digest(swapped) != O.digest(buf)
+        shifted = np.concatenate([buf[8:], buf[:8]])
+        assert O.digest(shifted) != O.digest(buf)
