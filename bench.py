@@ -466,7 +466,7 @@ def run_b200(a):
             trc = None
         else:
             chk_gbps = bytes_per_launch / (statistics.mean(check_ms) * 1e-3) / 1e9
-            roof_check = {"kernel": "hv_check_digests (digest of every arrival + compare; desc_op_kernel<DigestOpR> + "
+            roof_check = {"kernel": "hv_check_digests (digest of every arrival + compare; desc_digest_tma + "
                                     "digest_compare_kernel), beside the copy engine on a side stream",
                           "bound": "hbm", "achieved": chk_gbps,
                           "peak": hbm_peak, "unit": "GB/s", "frac": chk_gbps / hbm_peak if hbm_peak else None,
