@@ -45,7 +45,7 @@ from benchlib.compare import (autotune, measure_pcie_h2d, measure_peer_copy, pro
                              same_run_comparisons)
 from benchlib.cpu import (cpu_gather_sample, cpu_host_copy, cpu_model, reference_simulator, run_reference)  # noqa: E402
 from benchlib.phases import (churn_phase, host_offload_decode, kv_decode_config1, kv_long_context,  # noqa: E402
-                             offload_sweep_phase, phi_phase, run_decode)
+                             offload_sweep_phase, phi_phase, run_decode, all_local_decode)
 
 
 def parse():
@@ -379,6 +379,10 @@ def run_b200(a):
                                              microbatches=1, host_plan=True)
         except Exception as e:
             decode["host_plan"] = {"error": repr(e)[:300]}
+        try:   # the same decoder with every expert in HBM: its compute ceiling (not an offload mode)
+            decode["all_local_ceiling"] = all_local_decode(sysm, store, m, dev)
+        except Exception as e:
+            decode["all_local_ceiling"] = {"error": repr(e)[:300]}
     # the faster of the measured decode modes (each one bit-identical to its all-local run)
     modes = {"staged": decode.get("tokens_per_s"), "staged_cuda_graph": (decode.get("cuda_graph") or {}).get("tokens_per_s"),
              "fused": decode["fused"].get("tokens_per_s"),

@@ -37,7 +37,7 @@ def run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, micro
                     "attention not modeled"}
     if fused:
         out["mode"] = ("fused: experts consumed in place (hv_expert_ffn_gate_up/down stream weight tiles from "
-                       "the resident copy into mma.sync; no K2 staging copy)")
+                       "the resident copy into tcgen05.mma; host-tier experts staged by K2 first)")
     if host_plan:
         out["mode"] = ("staged, host plan: each stage's plan read back once routed and fetched through the engine per "
                        "source (copy engine for host-tier experts); eager only")
@@ -69,6 +69,69 @@ def run_decode(fetcher, m, dev, world, max_over_ranks, barrier, a, source, micro
             out["cuda_graph"] = {"error": repr(e)[:300]}
     del dec
     return out
+
+def all_local_decode(sysm, store, m, dev, steps=5, warm=2):
+    """The decoder's compute ceiling: every expert resident in this GPU's HBM
+    (the host tier's bytes copied once), fused decode as one CUDA graph per
+    step, experts row-major and then stored as HV_FFN_TILED tiles (the same
+    logical weights: outputs must be bit-identical).  Not an offload number --
+    it bounds what any tier can deliver to this decoder."""
+    import torch
+    from paper_2602_00328_b200 import fetch as F
+    from paper_2602_00328_b200.decode import MoEDecoder
+    from paper_2602_00328_b200.memalloc import Tier
+    from paper_2602_00328_b200.moe import ExpertFetcher, ExpertResidency, ExpertStore
+    L, E, S, H, I = m.num_layers, m.num_experts, m.expert_size, m.hidden, m.intermediate
+    view = store.host.view()
+    resident = torch.empty(L * E * S, dtype=torch.uint8, device=f"cuda:{dev}")
+    step = E * S
+    for o in range(0, L * E * S, step):
+        resident[o:o + step].copy_(torch.from_numpy(view[store.base_offset + o:store.base_offset + o + step]))
+    res = ExpertResidency(m)
+    for layer in range(L):
+        for e in range(E):
+            res.set_tier(layer, e, Tier.LOCAL_HBM)
+    addr = [[resident.data_ptr() + (layer * E + e) * S for e in range(E)] for layer in range(L)]
+    out, ref = {"model": f"{m.name}: {L} layers x {E} experts, batch {TOKENS}, top-{m.top_k}",
+                "expert_source": "local HBM (all resident)", "mode": "fused, CUDA graph per step"}, None
+    for layout in ("row", "tiled"):
+        if layout == "tiled":
+            for o in range(0, L * E * S, S):
+                w = resident[o:o + S].view(torch.bfloat16)
+                t = torch.cat([F.tile_expert_matrix(w[:I * H].view(I, H)).reshape(-1),
+                               F.tile_expert_matrix(w[I * H:2 * I * H].view(I, H)).reshape(-1),
+                               F.tile_expert_matrix(w[2 * I * H:].view(H, I)).reshape(-1)])
+                w.copy_(t)
+        lstore = ExpertStore(m, store.host_device_id, None)
+        lstore.layout = layout
+        f = ExpertFetcher(sysm.runtime, m, res, lstore, local_addr=addr)
+        dec = MoEDecoder(f, tokens=TOKENS, microbatches=1, seed=7, fused=True)
+        h = dec.decode(warm)
+        dec.capture_graph()
+        h0 = h.clone()
+        for _ in range(warm):
+            h = dec.step(h)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cur = torch.cuda.current_stream()
+        e0.record(cur)
+        hg = h
+        for _ in range(steps):
+            hg = dec.step(hg)
+        e1.record(cur)
+        e1.synchronize()
+        dt = e0.elapsed_time(e1) * 1e-3
+        one = dec.step(h0).clone()
+        torch.cuda.synchronize()
+        if ref is None:
+            ref = one
+        out[layout] = {"tokens_per_s": TOKENS * steps / dt, "ms_per_decode_step": dt / steps * 1e3,
+                       "equals_row_major_bitwise": bool(torch.equal(one.view(torch.int16), ref.view(torch.int16)))}
+        del dec, f
+    del resident
+    torch.cuda.empty_cache()
+    return out
+
 
 def host_offload_decode(m, dev, a, microbatches=1, steps=3, warm=2):
     """The same decode with every expert served from pinned host DRAM (the
