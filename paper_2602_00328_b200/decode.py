@@ -107,6 +107,8 @@ class MoEDecoder:
         self.ffn_flags = N.FFN_TILED if self.tiled else 0
         # router logits scratch and the route kernel's arrival ticket (zeroed
         # here; the kernel re-arms it); the routed pairs of each staging slot
+        # (the route kernel's limits: up to 256 experts, top-8, 256 tokens per stage)
+        self.glue = type(self).glue and self.E <= 256 and m.top_k <= 8 and self.tmb <= 256 and self.H % 8 == 0
         self._logits = torch.empty(self.tmb * self.E, dtype=torch.float32, device=self.dev)
         self._ticket = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self._pairs = [None, None]
