@@ -742,7 +742,7 @@ __global__ void __launch_bounds__(kDgThreads) desc_digest_tma(DescResolver res, 
   if (threadIdx.x == 0) {
     for (int st = 0; st < kDgStages; ++st) {
       mbar_init(&full[st], 1);
-      mbar_init(&empty[st], 1);
+      mbar_init(&empty[st], 32);   // every lane of the consuming warp releases its own reads
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -754,7 +754,12 @@ __global__ void __launch_bounds__(kDgThreads) desc_digest_tma(DescResolver res, 
       uint32_t hint = 0;
       for (uint32_t t = 0; t < mine; ++t) {
         const uint32_t st = t % kDgStages, round = t / kDgStages;
-        if (round > 0) mbar_wait(&empty[st], (round - 1) & 1);
+        if (round > 0) {
+          mbar_wait(&empty[st], (round - 1) & 1);
+          // the consumer's generic-proxy reads of this stage, ordered before
+          // the bulk copy's async-proxy writes into it
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
         const ChunkRef r = res.at(blockIdx.x + t * G, hint, s_start);
         if (tma_ok(r)) {
           mbar_expect_tx(&full[st], r.len);
@@ -794,8 +799,12 @@ __global__ void __launch_bounds__(kDgThreads) desc_digest_tma(DescResolver res, 
       if (tail && lane == 0) acc += digest_term(w0 + nfull, load_word_tail(r.src + nfull * 8, tail));
     }
     if (r.off == 0 && lane == 0) acc += __ldg(bytes + r.obj);
-    __syncwarp();
-    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
+    // release: each lane's generic-proxy reads of the stage, ordered before the
+    // producer's next bulk (async-proxy) write into it.  Every lane arrives
+    // (a lane-0 arrive after __syncwarp is the same ordering, but racecheck
+    // reports it as a write-after-read hazard: build/rc repro, r5y)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
     if (r.obj != cur_obj) {
       if (cur_obj != 0xFFFFFFFFu) {
         const uint64_t tot = warp_sum(run);

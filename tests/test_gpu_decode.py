@@ -504,3 +504,31 @@ def test_fetch_stream_is_urgent_and_node_priority_graph_equals_eager():
     del dec
     sysm.close()
     sys2.close()
+
+
+def test_library_glue_agrees_with_torch_glue():
+    """MoEDecoder.glue: the router / pair sort / combine as library kernels
+    (default) or as torch ops.  Logits differ in rounding (fp32 dot vs a bf16
+    GEMM), so the two agree to tolerance, and each is bit-identical to its
+    own all-local run."""
+    from paper_2602_00328_b200.decode import MoEDecoder
+    model = _tiny()
+    L, E = model.num_layers, model.num_experts
+    sysm, store, res, fetcher, dec = _setup(model, peer_experts=L * E // 2, microbatches=1)
+    sys2, _d2, keep = _all_local(model, 16, 1, 0, store)
+    outs = {}
+    try:
+        for glue in (True, False):
+            MoEDecoder.glue = glue
+            a = MoEDecoder(fetcher, tokens=16, microbatches=1, seed=0, residual_scale=RS, fused=True).decode(3)
+            b = MoEDecoder(_d2.f, tokens=16, microbatches=1, seed=0, residual_scale=RS, fused=True).decode(3)
+            torch.cuda.synchronize()
+            assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+            outs[glue] = a
+    finally:
+        MoEDecoder.glue = True
+    x0 = dec.x0.float()
+    d_k, d_t = outs[True].float() - x0, outs[False].float() - x0
+    assert (d_k - d_t).abs().max() <= 5e-2 * d_t.abs().max()
+    sysm.loop.run()
+    sysm.close(); sys2.close()
