@@ -31,9 +31,54 @@ namespace {
 constexpr int kRouteWarps = 8;                 // tokens per route CTA (one warp each)
 constexpr int kRouteThreads = kRouteWarps * 32;
 constexpr uint32_t kMaxE = 256, kMaxK = 8, kMaxT = 256;
+constexpr int kStageFloats = 8192;             // 32 KiB of logits staged per chunk of tokens
 
 __device__ __forceinline__ float bf16lo(uint32_t x) { return __uint_as_float(x << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t x) { return __uint_as_float(x & 0xFFFF0000u); }
+
+// top-K of one token's logits (largest first, ties to the lower expert id,
+// NaN ranked last), the softmax over them, and the token's pairs
+template <int K>
+__device__ __forceinline__ void token_topk(const float* __restrict__ lg, int tt, int E, float* __restrict__ probs,
+                                           int64_t* __restrict__ topi, int* __restrict__ s_exp) {
+  float tv[K];
+  int ti[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    tv[j] = -INFINITY;
+    ti[j] = 0x7FFFFFFF;
+  }
+  for (int e = 0; e < E; ++e) {
+    float x = lg[e];   // the token's row, staged in shared memory
+    x = x != x ? -INFINITY : x;
+    if (x > tv[K - 1] || ti[K - 1] == 0x7FFFFFFF) {   // a free slot, or better than the k-th
+      tv[K - 1] = x;
+      ti[K - 1] = e;
+#pragma unroll
+      for (int j = K - 1; j > 0; --j) {
+        // bubble up past strictly smaller values (or free slots); an equal
+        // value stays behind the lower expert id scanned before it
+        if (tv[j] > tv[j - 1] || ti[j - 1] == 0x7FFFFFFF) {
+          const float fv = tv[j];
+          tv[j] = tv[j - 1];
+          tv[j - 1] = fv;
+          const int fi = ti[j];
+          ti[j] = ti[j - 1];
+          ti[j - 1] = fi;
+        }
+      }
+    }
+  }
+  float sum = 0.f;
+#pragma unroll
+  for (int j = 0; j < K; ++j) sum += expf(tv[j] - tv[0]);
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    probs[(size_t)tt * K + j] = expf(tv[j] - tv[0]) / sum;
+    topi[(size_t)tt * K + j] = ti[j];
+    s_exp[tt * K + j] = ti[j];
+  }
+}
 
 // grid (E, ceil(T / 8)): warp w of CTA (e, tb) computes logit[t = tb*8 + w][e]
 __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(
@@ -46,6 +91,7 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(
     const uint4* hr = reinterpret_cast<const uint4*>(h + (size_t)t * H);
     const uint4* rr = reinterpret_cast<const uint4*>(router + (size_t)e * H);
     float acc = 0.f;
+#pragma unroll 8
     for (int c = lane; c < H / 8; c += 32) {
       const uint4 a = __ldg(hr + c), b = __ldg(rr + c);
       acc = fmaf(bf16lo(a.x), bf16lo(b.x), acc);
@@ -73,49 +119,30 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(
   __shared__ int s_exp[kMaxT * kMaxK];
   for (int i = threadIdx.x; i < E; i += blockDim.x) s_cnt[i] = 0;
   __syncthreads();
-  for (int tt = warp; tt < T; tt += kRouteWarps) {
-    const float* lg = logits + (size_t)tt * E;
-    float v[kMaxE / 32];
-#pragma unroll
-    for (int i = 0; i < (int)(kMaxE / 32); ++i) {
-      const int ee = lane + 32 * i;
-      const float x = ee < E ? __ldcg(lg + ee) : -INFINITY;
-      v[i] = x != x ? -INFINITY : x;   // a NaN logit ranks last
-    }
-    unsigned taken = 0u;               // bit i: expert lane + 32 i already chosen
-    float top[kMaxK];
-    for (int j = 0; j < k; ++j) {
-      // lane's best remaining (largest value, then lowest expert id)
-      float bv = -INFINITY;
-      int be = 0x7FFFFFFF;
-#pragma unroll
-      for (int i = 0; i < (int)(kMaxE / 32); ++i) {
-        const int ee = lane + 32 * i;
-        if (ee < E && !(taken >> i & 1u) && (v[i] > bv || (v[i] == bv && ee < be))) {
-          bv = v[i];
-          be = ee;
-        }
+  // one thread per token: scan its E logits (L2, each row contiguous) keeping
+  // the top k in registers; strict '>' keeps the lower expert first on ties
+  // rows staged through shared memory in token chunks (coalesced loads; a
+  // per-element scan of L2 would pay its latency E times per token)
+  __shared__ float s_lg[kStageFloats];
+  const int chunk = kStageFloats / E;   // E <= 256: at least 32 tokens per chunk
+  for (int t0 = 0; t0 < T; t0 += chunk) {
+    const int nt = min(chunk, T - t0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nt * E; i += blockDim.x) s_lg[i] = __ldcg(logits + (size_t)t0 * E + i);
+    __syncthreads();
+    for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+      const float* row = s_lg + j * E;
+      const int tt = t0 + j;
+      switch (k) {
+        case 1: token_topk<1>(row, tt, E, probs, topi, s_exp); break;
+        case 2: token_topk<2>(row, tt, E, probs, topi, s_exp); break;
+        case 3: token_topk<3>(row, tt, E, probs, topi, s_exp); break;
+        case 4: token_topk<4>(row, tt, E, probs, topi, s_exp); break;
+        case 5: token_topk<5>(row, tt, E, probs, topi, s_exp); break;
+        case 6: token_topk<6>(row, tt, E, probs, topi, s_exp); break;
+        case 7: token_topk<7>(row, tt, E, probs, topi, s_exp); break;
+        default: token_topk<8>(row, tt, E, probs, topi, s_exp); break;
       }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oe = __shfl_xor_sync(0xffffffffu, be, o);
-        if (ov > bv || (ov == bv && oe < be)) {
-          bv = ov;
-          be = oe;
-        }
-      }
-      top[j] = bv;
-      if ((be & 31) == lane) taken |= 1u << (be >> 5);
-      if (lane == 0) {
-        topi[(size_t)tt * k + j] = be;
-        s_exp[tt * k + j] = be;
-      }
-    }
-    if (lane == 0) {
-      float sum = 0.f;
-      for (int j = 0; j < k; ++j) sum += expf(top[j] - top[0]);
-      for (int j = 0; j < k; ++j) probs[(size_t)tt * k + j] = expf(top[j] - top[0]) / sum;
     }
   }
   __syncthreads();
@@ -145,6 +172,7 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(
   for (int p = threadIdx.x; p < P; p += blockDim.x) {   // stable: rank among earlier pairs of the same expert
     const int ex = s_exp[p];
     int r = 0;
+#pragma unroll 8
     for (int q = 0; q < p; ++q) r += s_exp[q] == ex;
     const int sorted = s_off[ex] + r;
     pos[p] = sorted;
@@ -153,7 +181,7 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(
   if (threadIdx.x == 0) *ticket = 0u;   // re-armed for the next launch / graph replay
 }
 
-// grid (T), H/8 threads max 256 (loop): h[t][d] = bf16(h + bf16(bf16(sum) * rs))
+// grid (T, H / (4 * threads)): h[t][d] = bf16(h + bf16(bf16(sum) * rs))
 __global__ void __launch_bounds__(256) moe_combine_kernel(const float* __restrict__ y, const float* __restrict__ probs,
                                                           const int64_t* __restrict__ pos,
                                                           __nv_bfloat16* __restrict__ h, int H, int k, float rs,
@@ -168,7 +196,7 @@ __global__ void __launch_bounds__(256) moe_combine_kernel(const float* __restric
       rows[j] = y + (size_t)__ldg(pos + (size_t)t * k + j) * H;
     }
   }
-  for (int d = threadIdx.x * 4; d < H; d += blockDim.x * 4) {
+  for (int d = (blockIdx.y * blockDim.x + threadIdx.x) * 4; d < H; d += gridDim.y * blockDim.x * 4) {
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int j = 0; j < (int)kMaxK; ++j) {   // fixed order j = 0..k-1
@@ -270,7 +298,9 @@ HV_EXPORT int hv_moe_combine(const float* d_y, const float* d_probs, const int64
   int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
   const int threads = hidden / 4 < 256 ? (int)((hidden / 4 + 31) / 32 * 32) : 256;
-  moe_combine_kernel<<<tokens, threads, 0, (cudaStream_t)stream>>>(
+  // one 16-byte column group per thread: (tokens, hidden / (4 * threads)) CTAs
+  const dim3 grid(tokens, (hidden + 4 * threads - 1) / (4 * threads));
+  moe_combine_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(
       d_y, d_probs, d_pos, reinterpret_cast<__nv_bfloat16*>(d_h), (int)hidden, (int)top_k, residual_scale,
       residual_scale != 1.0f ? 1 : 0);
   HV_CUDA(cudaGetLastError());
