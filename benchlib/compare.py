@@ -265,6 +265,8 @@ def same_run_comparisons(dev, m, a, source, fetcher=None, n=53):
                                f"cuda:{dev}")
     dt_h = t(lambda: F.kv_gather(host_pages, page, dst=kdst, engine=keng, stream=s.cuda_stream))
     kv["host_us"], kv["host_GBps"] = dt_h * 1e6, npg * page / dt_h / 1e9
+    kv["distribution_us"] = {"host": pct(lambda: F.kv_gather(host_pages, page, dst=kdst, engine=keng,
+                                                              stream=s.cuda_stream))}
     if source == "peer":
         base = fetcher.src_addr[0, :n]   # peer memory of n experts viewed as page slots
         slots = [int(base[i]) + j * page for i in range(n) for j in range(S // page)]
@@ -272,6 +274,8 @@ def same_run_comparisons(dev, m, a, source, fetcher=None, n=53):
         dt_p = t(lambda: F.kv_gather(peer_pages, page, dst=kdst, engine=keng, stream=s.cuda_stream))
         kv["peer_us"], kv["peer_GBps"] = dt_p * 1e6, npg * page / dt_p / 1e9
         kv["peer_vs_host_speedup"] = dt_h / dt_p
+        kv["distribution_us"]["peer"] = pct(lambda: F.kv_gather(peer_pages, page, dst=kdst, engine=keng,
+                                                                 stream=s.cuda_stream))
     out["kv_config1_layer_gather"] = kv
     out.update(latency_curves(dev, a, s, t, h, fetcher if source == "peer" else None))
     try:
