@@ -330,6 +330,13 @@ int hv_expert_ffn_max_tokens(int* out);
  * those of the row-major form on the same logical weights
  * (fetch.tile_expert_matrix writes the layout). */
 #define HV_FFN_TILED 2u
+/* HV_FFN_WAIT_PREVIOUS: launched with programmatic stream serialization
+ * behind a kernel that may have written any input (the router of the same
+ * stage): the CTAs' prologue (TMEM allocation, barriers) overlaps its tail
+ * and every input is read after griddepcontrol.wait.  Rows % 128 == 0.
+ * HV_FFN_OVERLAP_PREVIOUS on hv_expert_ffn_down_ex (rows % 128 == 0: the
+ * tcgen05 kernel) streams the first stages' weight tiles before the wait. */
+#define HV_FFN_WAIT_PREVIOUS 4u
 int hv_expert_ffn_gate_up_ex(const uint64_t* d_w_addr, const int32_t* d_counts, const int32_t* d_offs,
                              const int32_t* d_tok, const void* d_x, void* d_act, uint32_t n_experts,
                              uint32_t hidden, uint32_t intermediate, unsigned flags, void* stream);
@@ -350,9 +357,13 @@ int hv_expert_ffn_down_ex(const uint64_t* d_w_addr, const int32_t* d_counts, con
  * d_ticket: one unsigned, zero before the first launch (the kernel re-arms it),
  * not shared by concurrent launches.  tokens <= 256, n_experts <= 256,
  * top_k <= 8.  One launch. */
+/* HV_MOE_OVERLAP_PREVIOUS (route, combine): launched with programmatic stream
+ * serialization; the kernel waits for the previous one before reading. */
+#define HV_MOE_OVERLAP_PREVIOUS 1u
 int hv_moe_route(const void* d_h, const void* d_router, uint32_t tokens, uint32_t hidden, uint32_t n_experts,
                  uint32_t top_k, float* d_logits, float* d_probs, int64_t* d_topi, int32_t* d_counts,
-                 int32_t* d_offs, int32_t* d_tok, int64_t* d_pos, unsigned* d_ticket, void* stream);
+                 int32_t* d_offs, int32_t* d_tok, int64_t* d_pos, unsigned* d_ticket, unsigned flags,
+                 void* stream);
 /* h[t] <- h[t] + rs * bf16(sum_j probs[t][j] * y[pos[t*top_k + j]]) in bf16,
  * j in order (deterministic); d_y fp32 [tokens*top_k][hidden] (K4 down's
  * output), d_h bf16 [tokens][hidden] updated in place. */
@@ -365,7 +376,7 @@ int hv_moe_stage_plan(const int32_t* d_counts, const uint64_t* d_addr, const uin
                       uint64_t slot_bytes, uint32_t n_experts, uint64_t* d_dst, uint64_t* d_sizes,
                       uint64_t* d_addr_out, void* stream);
 int hv_moe_combine(const float* d_y, const float* d_probs, const int64_t* d_pos, void* d_h, uint32_t tokens,
-                   uint32_t hidden, uint32_t top_k, float residual_scale, void* stream);
+                   uint32_t hidden, uint32_t top_k, float residual_scale, unsigned flags, void* stream);
 
 /* ---- paged decode attention over KV pages in any tier -------------------- */
 /* One query token per sequence, grouped-query (q_heads = g * kv_heads,

@@ -35,6 +35,8 @@ POOL_IPC = 1
 POOL_EAGER = 2
 POOL_REMOTE = 4
 ATTN_OVERLAP_PREVIOUS = 1        # HV_ATTN_OVERLAP_PREVIOUS: programmatic dependent launch of K5
+FFN_WAIT_PREVIOUS = 4            # HV_FFN_WAIT_PREVIOUS: K4 as a programmatic dependent of a kernel that wrote its inputs
+MOE_OVERLAP_PREVIOUS = 1         # HV_MOE_OVERLAP_PREVIOUS: route / combine as programmatic dependents
 FFN_TILED = 2                    # HV_FFN_TILED: K4 over experts stored as swizzled 128 x 64 tiles (bulk-copy stream)
 ATTN_BALANCED = 2                # HV_ATTN_BALANCED: K5 as balanced (stream-K) ranges over `splits` CTAs
 FFN_OVERLAP_PREVIOUS = 1         # HV_FFN_OVERLAP_PREVIOUS: K4 down behind gate/up
@@ -151,8 +153,8 @@ _SIGS = {
     "hv_expert_ffn_max_tokens": [C.POINTER(i32)],
     "hv_expert_ffn_down_ex": [u64, u64, u64, u64, u64, u32, u32, u32, C.c_uint, vp],
     "hv_expert_ffn_gate_up_ex": [u64, u64, u64, u64, u64, u64, u32, u32, u32, C.c_uint, vp],
-    "hv_moe_route": [u64, u64, u32, u32, u32, u32, u64, u64, u64, u64, u64, u64, u64, u64, vp],
-    "hv_moe_combine": [u64, u64, u64, u64, u32, u32, u32, C.c_float, vp],
+    "hv_moe_route": [u64, u64, u32, u32, u32, u32, u64, u64, u64, u64, u64, u64, u64, u64, C.c_uint, vp],
+    "hv_moe_combine": [u64, u64, u64, u64, u32, u32, u32, C.c_float, C.c_uint, vp],
     "hv_moe_stage_plan": [u64, u64, u64, u64, u64, u32, u64, u64, u64, vp],
     "hv_paged_decode_attention": [u64, u64, u64, u64, u64, u64, u32, u32, u32, u32, u32, u32, C.c_float, vp],
     "hv_paged_decode_attention_ex": [u64, u64, u64, u64, u64, u64, u32, u32, u32, u32, u32, u32, C.c_float,

@@ -104,6 +104,7 @@ struct FfnArgs {
   int pair;                 // down projection as a pair of row blocks (NMAT=2 kernel, fp32 out, no SiLU)
   int wait_x;               // launched with programmatic serialization: x comes from the previous kernel
   int tiled;                // HV_FFN_TILED: matrices stored as swizzled 128 x 64 tiles (expert_ffn_umma only)
+  int wait_all;             // HV_FFN_WAIT_PREVIOUS: programmatic dependent of a kernel that wrote any input
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -1306,6 +1307,11 @@ __global__ void __launch_bounds__(kUThreads, 1) expert_ffn_umma(FfnArgs a, int n
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_sh;
   const size_t wstride = (size_t)a.K * 2, xstride = (size_t)a.K * 2;
+  // programmatic dependent launch (decode.py launches the stage's kernels as a
+  // chain): the prologue above overlapped the previous kernel's tail; with
+  // HV_FFN_WAIT_PREVIOUS every input may be its output, so wait here
+  if (a.wait_all) asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp >= kUEpiWarps && warp < kUEpiWarps + kUProdWarps) {
     // ---- producers
@@ -1313,6 +1319,50 @@ __global__ void __launch_bounds__(kUThreads, 1) expert_ffn_umma(FfnArgs a, int n
     UCursor c{(int)blockIdx.x, 0, 0, 0, nullptr, nullptr};
     u_seek(c, a, rb_count, n_items);
     uint32_t g = 0;
+    // the weight tiles of (item c, k-tile kt) into ring stage s
+    auto issue_weights = [&](const UCursor& cc, int kt, int st) {
+      char* base = smem + st * U::kStage;
+      const size_t kb = (size_t)kt * kRowBytes;
+      if (a.tiled) {
+        // tile (row block, kt) of each matrix is 16 KiB contiguous and
+        // already in the swizzled order: one bulk copy (TMA engine) each,
+        // completing on the stage's full barrier
+        if (pt == 0) {
+          const uint32_t fb = smem_u32(&full_bar[st]);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(NMAT * U::kWm)
+                       : "memory");
+#pragma unroll
+          for (int m = 0; m < NMAT; ++m)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(base + m * U::kWm)),
+                "l"((m == 0 ? cc.w0 : cc.w1) + (size_t)kt * U::kWm), "r"(U::kWm), "r"(fb)
+                : "memory");
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < NMAT; ++m) {
+          const uint32_t ws = smem_u32(base + m * U::kWm);
+          const char* src = m == 0 ? cc.w0 : cc.w1;
+#pragma unroll 4
+          for (int i = pt; i < kURows * kChunksPerRow; i += kUProd) {
+            const int r = i / kChunksPerRow, ch = i % kChunksPerRow;
+            cp_async16(ws + swz(r, ch), src + r * wstride + kb + ch * 16);
+          }
+        }
+      }
+    };
+    // HV_FFN_OVERLAP_PREVIOUS (the down projection behind gate/up): the
+    // weights do not depend on the previous kernel, so the first item's first
+    // stages stream in while it drains; its activation rows only after the wait
+    int pre = 0;
+    if (a.wait_x) {
+      if (c.item < n_items) {
+        pre = ktiles < U::kS ? ktiles : U::kS;
+        for (int kt = 0; kt < pre; ++kt) issue_weights(c, kt, kt);
+      }
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
     // this thread's activation rows: r = pt/8 + j*(kUProd/8), chunk pt%8 --
     // their source rows are resolved once per item, not per stage
     constexpr int kXPass = kUProd / kChunksPerRow;                 // rows covered per pass
@@ -1332,34 +1382,7 @@ __global__ void __launch_bounds__(kUThreads, 1) expert_ffn_umma(FfnArgs a, int n
         if (round > 0) u_mbar_wait(smem_u32(&empty_bar[s]), (round - 1) & 1);
         char* base = smem + s * U::kStage;
         const size_t kb = (size_t)kt * kRowBytes;
-        if (a.tiled) {
-          // tile (row block, kt) of each matrix is 16 KiB contiguous and
-          // already in the swizzled order: one bulk copy (TMA engine) each,
-          // completing on the stage's full barrier
-          if (pt == 0) {
-            const uint32_t fb = smem_u32(&full_bar[s]);
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(NMAT * U::kWm)
-                         : "memory");
-#pragma unroll
-            for (int m = 0; m < NMAT; ++m)
-              asm volatile(
-                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                      smem_u32(base + m * U::kWm)),
-                  "l"((m == 0 ? c.w0 : c.w1) + (size_t)kt * U::kWm), "r"(U::kWm), "r"(fb)
-                  : "memory");
-          }
-        } else {
-#pragma unroll
-          for (int m = 0; m < NMAT; ++m) {
-            const uint32_t ws = smem_u32(base + m * U::kWm);
-            const char* src = m == 0 ? c.w0 : c.w1;
-#pragma unroll 4
-            for (int i = pt; i < kURows * kChunksPerRow; i += kUProd) {
-              const int r = i / kChunksPerRow, ch = i % kChunksPerRow;
-              cp_async16(ws + swz(r, ch), src + r * wstride + kb + ch * 16);
-            }
-          }
-        }
+        if ((int)g >= pre) issue_weights(c, kt, s);   // else streamed before the wait
         const uint32_t xs = smem_u32(base + NMAT * U::kWm);
 #pragma unroll
         for (int j = 0; j < kXRows; ++j) {
@@ -1474,15 +1497,26 @@ int launch_ffn(const FfnArgs& a, uint32_t n_experts, void* stream) {
   st = hv::kernel_attr<expert_ffn_kernel<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<NMAT>::kTotal);
   if (st) return st;
 #if HV_FFN_UMMA
-  HV_CHECK_ARG(!a.tiled || (!a.pair && !a.wait_x && a.rows % kURows == 0));
-  if (!a.pair && !a.wait_x && a.rows % kURows == 0) {
+  HV_CHECK_ARG(!a.tiled || (!a.pair && a.rows % kURows == 0));
+  HV_CHECK_ARG(!a.wait_all || (!a.pair && a.rows % kURows == 0));
+  if (!a.pair && a.rows % kURows == 0) {
     using U = USmem<NMAT>;
     st = hv::kernel_attr<expert_ffn_umma<NMAT>>(dev, cudaFuncAttributeMaxDynamicSharedMemorySize, U::kTotal);
     if (st) return st;
     const int n_items = (int)(a.rows / kURows) * (int)n_experts;
     int g = hv::sm_count(dev);                    // one ~200 KiB CTA per SM
     if (g > n_items) g = n_items;
-    expert_ffn_umma<NMAT><<<g, kUThreads, U::kTotal, (cudaStream_t)stream>>>(a, n_items);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g);
+    cfg.blockDim = dim3(kUThreads);
+    cfg.dynamicSmemBytes = U::kTotal;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (a.wait_x || a.wait_all) ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HV_CUDA(cudaLaunchKernelEx(&cfg, expert_ffn_umma<NMAT>, a, n_items));
     HV_CUDA(cudaGetLastError());
     hv::note_launch();
     return HV_OK;
@@ -1602,9 +1636,10 @@ HV_EXPORT int hv_expert_ffn_gate_up_ex(const uint64_t* d_w_addr, const int32_t* 
                                        const int32_t* d_tok, const void* d_x, void* d_act, uint32_t n_experts,
                                        uint32_t hidden, uint32_t intermediate, unsigned flags, void* stream) {
   HV_CHECK_ARG(d_tok != nullptr || n_experts == 0);
-  HV_CHECK_ARG((flags & ~(unsigned)HV_FFN_TILED) == 0);
+  HV_CHECK_ARG((flags & ~(unsigned)(HV_FFN_TILED | HV_FFN_WAIT_PREVIOUS)) == 0);
   FfnArgs a{};
   a.tiled = (flags & HV_FFN_TILED) ? 1 : 0;
+  a.wait_all = (flags & HV_FFN_WAIT_PREVIOUS) ? 1 : 0;
   a.w_addr = d_w_addr;
   a.counts = d_counts;
   a.offs = d_offs;
@@ -1627,9 +1662,10 @@ HV_EXPORT int hv_expert_ffn_down(const uint64_t* d_w_addr, const int32_t* d_coun
 HV_EXPORT int hv_expert_ffn_down_ex(const uint64_t* d_w_addr, const int32_t* d_counts, const int32_t* d_offs,
                                     const void* d_act, float* d_y, uint32_t n_experts, uint32_t hidden,
                                     uint32_t intermediate, unsigned flags, void* stream) {
-  HV_CHECK_ARG((flags & ~(unsigned)(HV_FFN_OVERLAP_PREVIOUS | HV_FFN_TILED)) == 0);
+  HV_CHECK_ARG((flags & ~(unsigned)(HV_FFN_OVERLAP_PREVIOUS | HV_FFN_TILED | HV_FFN_WAIT_PREVIOUS)) == 0);
   FfnArgs a{};
   a.tiled = (flags & HV_FFN_TILED) ? 1 : 0;
+  a.wait_all = (flags & HV_FFN_WAIT_PREVIOUS) ? 1 : 0;
 #if HV_FFN_PERSISTENT
   a.wait_x = (flags & HV_FFN_OVERLAP_PREVIOUS) ? 1 : 0;
 #endif

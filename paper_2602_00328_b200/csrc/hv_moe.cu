@@ -87,6 +87,9 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(
     int32_t* __restrict__ offs, int32_t* __restrict__ tok, int64_t* __restrict__ pos, unsigned* __restrict__ ticket) {
   const int e = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.y * kRouteWarps + warp;
+  // HV_MOE_OVERLAP_PREVIOUS: h is the previous kernel's output (no-op otherwise)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (t < T) {
     const uint4* hr = reinterpret_cast<const uint4*>(h + (size_t)t * H);
     const uint4* rr = reinterpret_cast<const uint4*>(router + (size_t)e * H);
@@ -187,6 +190,8 @@ __global__ void __launch_bounds__(256) moe_combine_kernel(const float* __restric
                                                           __nv_bfloat16* __restrict__ h, int H, int k, float rs,
                                                           int scaled) {
   const int t = blockIdx.x;
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // y: the previous kernel's output
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   float p[kMaxK];
   const float* rows[kMaxK];
 #pragma unroll
@@ -266,7 +271,7 @@ HV_EXPORT int hv_moe_stage_plan(const int32_t* d_counts, const uint64_t* d_addr,
 HV_EXPORT int hv_moe_route(const void* d_h, const void* d_router, uint32_t tokens, uint32_t hidden,
                            uint32_t n_experts, uint32_t top_k, float* d_logits, float* d_probs, int64_t* d_topi,
                            int32_t* d_counts, int32_t* d_offs, int32_t* d_tok, int64_t* d_pos, unsigned* d_ticket,
-                           void* stream) {
+                           unsigned flags, void* stream) {
   if (tokens == 0) return HV_OK;
   HV_CHECK_ARG(d_h && d_router && d_logits && d_probs && d_topi && d_counts && d_offs && d_tok && d_pos && d_ticket);
   HV_CHECK_ARG(n_experts >= 1 && n_experts <= kMaxE && top_k >= 1 && top_k <= kMaxK && top_k <= n_experts);
@@ -277,18 +282,28 @@ HV_EXPORT int hv_moe_route(const void* d_h, const void* d_router, uint32_t token
   int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  dim3 grid(n_experts, (tokens + kRouteWarps - 1) / kRouteWarps);
-  moe_route_kernel<<<grid, kRouteThreads, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(d_h),
-                                                  reinterpret_cast<const __nv_bfloat16*>(d_router), (int)tokens,
-                                                  (int)hidden, (int)n_experts, (int)top_k, d_logits, d_probs, d_topi,
-                                                  d_counts, d_offs, d_tok, d_pos, d_ticket);
+  HV_CHECK_ARG((flags & ~(unsigned)HV_MOE_OVERLAP_PREVIOUS) == 0);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_experts, (tokens + kRouteWarps - 1) / kRouteWarps);
+  cfg.blockDim = dim3(kRouteThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (flags & HV_MOE_OVERLAP_PREVIOUS) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HV_CUDA(cudaLaunchKernelEx(&cfg, moe_route_kernel, reinterpret_cast<const __nv_bfloat16*>(d_h),
+                             reinterpret_cast<const __nv_bfloat16*>(d_router), (int)tokens, (int)hidden,
+                             (int)n_experts, (int)top_k, d_logits, d_probs, d_topi, d_counts, d_offs, d_tok, d_pos,
+                             d_ticket));
   HV_CUDA(cudaGetLastError());
   hv::note_launch(1);
   return HV_OK;
 }
 
 HV_EXPORT int hv_moe_combine(const float* d_y, const float* d_probs, const int64_t* d_pos, void* d_h,
-                             uint32_t tokens, uint32_t hidden, uint32_t top_k, float residual_scale, void* stream) {
+                             uint32_t tokens, uint32_t hidden, uint32_t top_k, float residual_scale, unsigned flags,
+                             void* stream) {
   if (tokens == 0) return HV_OK;
   HV_CHECK_ARG(d_y && d_probs && d_pos && d_h);
   HV_CHECK_ARG(top_k >= 1 && top_k <= kMaxK && hidden % 4 == 0 && hidden > 0);
@@ -299,10 +314,18 @@ HV_EXPORT int hv_moe_combine(const float* d_y, const float* d_probs, const int64
   if (st) return st;
   const int threads = hidden / 4 < 256 ? (int)((hidden / 4 + 31) / 32 * 32) : 256;
   // one 16-byte column group per thread: (tokens, hidden / (4 * threads)) CTAs
-  const dim3 grid(tokens, (hidden + 4 * threads - 1) / (4 * threads));
-  moe_combine_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(
-      d_y, d_probs, d_pos, reinterpret_cast<__nv_bfloat16*>(d_h), (int)hidden, (int)top_k, residual_scale,
-      residual_scale != 1.0f ? 1 : 0);
+  HV_CHECK_ARG((flags & ~(unsigned)HV_MOE_OVERLAP_PREVIOUS) == 0);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tokens, (hidden + 4 * threads - 1) / (4 * threads));
+  cfg.blockDim = dim3(threads);
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (flags & HV_MOE_OVERLAP_PREVIOUS) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HV_CUDA(cudaLaunchKernelEx(&cfg, moe_combine_kernel, d_y, d_probs, d_pos, reinterpret_cast<__nv_bfloat16*>(d_h),
+                             (int)hidden, (int)top_k, residual_scale, residual_scale != 1.0f ? 1 : 0));
   HV_CUDA(cudaGetLastError());
   hv::note_launch(1);
   return HV_OK;

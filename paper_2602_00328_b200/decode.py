@@ -52,6 +52,10 @@ class MoEDecoder:
     # router / top-k / pair sort and the top-k combine + residual as library
     # kernels (hv_moe_route, hv_moe_combine); False: the torch ops (A/B)
     glue = True
+    # the stage's library kernels (route, K4 gate/up, K4 down, combine) as a
+    # chain of programmatic dependent launches: each one's prologue and launch
+    # overlap the previous one's tail (needs the glue and 128-row tiles)
+    pdl = True
 
     def __init__(self, fetcher: ExpertFetcher, tokens: int, microbatches: int = 1, seed: int = 0,
                  engine: str = "auto", max_ctas: int = 0, router_scale: float = 0.5,
@@ -109,6 +113,7 @@ class MoEDecoder:
         # here; the kernel re-arms it); the routed pairs of each staging slot
         # (the route kernel's limits: up to 256 experts, top-8, 256 tokens per stage)
         self.glue = type(self).glue and self.E <= 256 and m.top_k <= 8 and self.tmb <= 256 and self.H % 8 == 0
+        self.pdl = type(self).pdl and self.glue and self.I % 128 == 0 and self.H % 128 == 0
         self._logits = torch.empty(self.tmb * self.E, dtype=torch.float32, device=self.dev)
         self._ticket = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self._pairs = [None, None]
@@ -455,7 +460,8 @@ class MoEDecoder:
         pos = torch.empty(T * k, dtype=torch.int64, device=self.dev)
         N.call("hv_moe_route", h.data_ptr(), self.router[layer].data_ptr(), T, self.H, E, k,
                self._logits.data_ptr(), probs.data_ptr(), topi.data_ptr(), counts.data_ptr(), offs.data_ptr(),
-               tok.data_ptr(), pos.data_ptr(), self._ticket.data_ptr(), torch.cuda.current_stream(self.dev).cuda_stream)
+               tok.data_ptr(), pos.data_ptr(), self._ticket.data_ptr(), N.MOE_OVERLAP_PREVIOUS if self.pdl else 0,
+               torch.cuda.current_stream(self.dev).cuda_stream)
         if self._counts is not None:
             self._counts[layer].index_add_(0, topi.reshape(-1), torch.ones_like(topi.reshape(-1)))
         return probs, topi, counts, offs, tok, pos
@@ -522,19 +528,21 @@ class MoEDecoder:
         act = torch.empty(P, I, dtype=torch.bfloat16, device=self.dev)
         y = torch.empty(P, H, dtype=torch.float32, device=self.dev)
         w = addr.data_ptr()
+        pdl_up = N.FFN_WAIT_PREVIOUS if self.pdl else 0
         N.call("hv_expert_ffn_gate_up_ex", w, counts.data_ptr(), offs.data_ptr(), tok.data_ptr(), h.data_ptr(),
-               act.data_ptr(), self.E, H, I, self.ffn_flags, stream)
-        # (HV_FFN_OVERLAP_PREVIOUS, down as a programmatic dependent of gate/up,
-        # measured slower: Qwen stage 201.5 vs 195.4 us, Phi-3.5 batch 1 123.8
-        # vs 107.8 -- r3b; so the plain launch)
+               act.data_ptr(), self.E, H, I, self.ffn_flags | pdl_up, stream)
+        # down as a programmatic dependent of gate/up: its first weight tiles
+        # stream while gate/up drains (the mma.sync form measured slower this
+        # way, r3b: 201.5 vs 195.4 us per Qwen stage; the tcgen05 form: §3)
+        pdl_down = N.FFN_OVERLAP_PREVIOUS if self.pdl else 0
         N.call("hv_expert_ffn_down_ex", w, counts.data_ptr(), offs.data_ptr(), act.data_ptr(), y.data_ptr(), self.E,
-               H, I, self.ffn_flags, stream)
+               H, I, self.ffn_flags | pdl_down, stream)
         # top-k combine in a fixed order (deterministic, no atomics), plus the residual
         if self.glue:
             if not h.is_contiguous():
                 h = h.contiguous()
             N.call("hv_moe_combine", y.data_ptr(), probs.data_ptr(), pos.data_ptr(), h.data_ptr(), h.shape[0], H,
-                   self.m.top_k, float(self.residual_scale), stream)
+                   self.m.top_k, float(self.residual_scale), N.MOE_OVERLAP_PREVIOUS if self.pdl else 0, stream)
             return h
         yt = y.index_select(0, pos).view(h.shape[0], self.m.top_k, H)
         return self._residual(h, (yt * probs.unsqueeze(-1)).sum(1).to(h.dtype))

@@ -27,7 +27,7 @@ def _route(h, router, k):
     ticket = torch.zeros(1, dtype=torch.int32, device="cuda")
     N.call("hv_moe_route", h.data_ptr(), router.data_ptr(), T, H, E, k, logits.data_ptr(), probs.data_ptr(),
            topi.data_ptr(), counts.data_ptr(), offs.data_ptr(), tok.data_ptr(), pos.data_ptr(), ticket.data_ptr(),
-           torch.cuda.current_stream().cuda_stream)
+           0, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert int(ticket.item()) == 0                  # re-armed for the next launch
     return logits.view(T, E), probs, topi, counts, offs, tok, pos
@@ -88,7 +88,7 @@ def test_combine_matches_torch(T, H, k, rs):
     pos = torch.randperm(P, generator=g).cuda()
     h = torch.randn(T, H, generator=g).to(torch.bfloat16).cuda()
     h0 = h.clone()
-    N.call("hv_moe_combine", y.data_ptr(), probs.data_ptr(), pos.data_ptr(), h.data_ptr(), T, H, k, rs,
+    N.call("hv_moe_combine", y.data_ptr(), probs.data_ptr(), pos.data_ptr(), h.data_ptr(), T, H, k, rs, 0,
            torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     s = (y[pos].view(T, k, H) * probs.unsqueeze(-1)).sum(1)
