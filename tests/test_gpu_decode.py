@@ -532,3 +532,32 @@ def test_library_glue_agrees_with_torch_glue():
     assert (d_k - d_t).abs().max() <= 5e-2 * d_t.abs().max()
     sysm.loop.run()
     sysm.close(); sys2.close()
+
+
+@pytest.mark.parametrize("layout", ["row", "tiled"])
+def test_pdl_chain_changes_no_bits(layout):
+    """MoEDecoder.pdl: the stage's route / K4 gate_up / K4 down / combine as a
+    chain of programmatic dependent launches.  Only when kernels start
+    changes, so every output bit equals the plainly launched chain's, eager
+    and as a CUDA graph."""
+    from paper_2602_00328_b200.decode import MoEDecoder
+    model = _tiny()
+    L, E = model.num_layers, model.num_experts
+    sysm, store, res, fetcher, dec = _setup(model, peer_experts=L * E // 2, microbatches=1, layout=layout)
+    outs = {}
+    try:
+        for pdl in (False, True):
+            MoEDecoder.pdl = pdl
+            d = MoEDecoder(fetcher, tokens=16, microbatches=1, seed=0, residual_scale=RS, fused=True)
+            assert d.pdl == pdl
+            eager = d.decode(3)
+            d.capture_graph()
+            graph = d.decode(3)
+            torch.cuda.synchronize()
+            assert torch.equal(eager.view(torch.int16), graph.view(torch.int16))
+            outs[pdl] = eager
+    finally:
+        MoEDecoder.pdl = True
+    assert torch.equal(outs[True].view(torch.int16), outs[False].view(torch.int16))
+    sysm.loop.run()
+    sysm.close()
