@@ -133,11 +133,12 @@ def main():
         act = torch.empty(T * k, I, dtype=torch.bfloat16, device=dev)
         y = torch.empty(T * k, H, dtype=torch.float32, device=dev)
         s = torch.cuda.current_stream().cuda_stream
+        fl = N.FFN_TILED if eng == "tiled" else 0   # the engine argument "tiled": HV_FFN_TILED (random bytes either way)
         for _ in range(reps):
-            N.call("hv_expert_ffn_gate_up", addr.data_ptr(), counts.data_ptr(), offs.data_ptr(), tok.data_ptr(),
-                   h.data_ptr(), act.data_ptr(), E, H, I, s)
-            N.call("hv_expert_ffn_down", addr.data_ptr(), counts.data_ptr(), offs.data_ptr(), act.data_ptr(),
-                   y.data_ptr(), E, H, I, s)
+            N.call("hv_expert_ffn_gate_up_ex", addr.data_ptr(), counts.data_ptr(), offs.data_ptr(), tok.data_ptr(),
+                   h.data_ptr(), act.data_ptr(), E, H, I, fl, s)
+            N.call("hv_expert_ffn_down_ex", addr.data_ptr(), counts.data_ptr(), offs.data_ptr(), act.data_ptr(),
+                   y.data_ptr(), E, H, I, fl, s)
         print("active experts", int((counts > 0).sum()))
     else:  # KV config 1: 1024 pages x 64 KiB from 4096 HBM slots
         page, npg, nslots = 65536, 1024, 4096
