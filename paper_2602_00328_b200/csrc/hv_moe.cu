@@ -277,12 +277,12 @@ HV_EXPORT int hv_moe_route(const void* d_h, const void* d_router, uint32_t token
   HV_CHECK_ARG(n_experts >= 1 && n_experts <= kMaxE && top_k >= 1 && top_k <= kMaxK && top_k <= n_experts);
   HV_CHECK_ARG(tokens <= kMaxT && hidden % 8 == 0 && hidden > 0);
   HV_CHECK_ARG(((reinterpret_cast<uintptr_t>(d_h) | reinterpret_cast<uintptr_t>(d_router)) & 15) == 0);
+  HV_CHECK_ARG((flags & ~(unsigned)HV_MOE_OVERLAP_PREVIOUS) == 0);
   int dev = 0;
   hv::DeviceGuard dg;
   int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  HV_CHECK_ARG((flags & ~(unsigned)HV_MOE_OVERLAP_PREVIOUS) == 0);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_experts, (tokens + kRouteWarps - 1) / kRouteWarps);
   cfg.blockDim = dim3(kRouteThreads);
@@ -308,13 +308,13 @@ HV_EXPORT int hv_moe_combine(const float* d_y, const float* d_probs, const int64
   HV_CHECK_ARG(d_y && d_probs && d_pos && d_h);
   HV_CHECK_ARG(top_k >= 1 && top_k <= kMaxK && hidden % 4 == 0 && hidden > 0);
   HV_CHECK_ARG(((reinterpret_cast<uintptr_t>(d_y) | reinterpret_cast<uintptr_t>(d_h)) & 15) == 0);
+  HV_CHECK_ARG((flags & ~(unsigned)HV_MOE_OVERLAP_PREVIOUS) == 0);
   int dev = 0;
   hv::DeviceGuard dg;
   int st = hv::bind_stream_device(stream, &dev, dg);
   if (st) return st;
   const int threads = hidden / 4 < 256 ? (int)((hidden / 4 + 31) / 32 * 32) : 256;
   // one 16-byte column group per thread: (tokens, hidden / (4 * threads)) CTAs
-  HV_CHECK_ARG((flags & ~(unsigned)HV_MOE_OVERLAP_PREVIOUS) == 0);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tokens, (hidden + 4 * threads - 1) / (4 * threads));
   cfg.blockDim = dim3(threads);

@@ -141,6 +141,28 @@ def test_launch_entry_points_validate_arguments_without_a_gpu():
     assert attn(d=96) == INV                 # head_dim 64 or 128 only
     assert attn(bt=32) == INV                # 16-token blocks
     assert attn(splits=0) == INV
+    # K5 flags: balanced (stream-K) form needs batch <= 256; unknown flags are rejected
+    def attn_ex(batch=2, flags=N.ATTN_BALANCED):
+        return lib.hv_paged_decode_attention_ex(A, A, A, A, A, A, batch, 32, 8, 128, 16, 148, 0.1, flags, None)
+    assert attn_ex(batch=257) == INV
+    assert attn_ex(flags=8) == INV
+    # tiled K4: rows must be multiples of 128 (the tcgen05 kernel); unknown flags rejected
+    assert lib.hv_expert_ffn_gate_up_ex(A, A, A, A, A, A, 4, 2048, 1408, 16, None) == INV
+    assert lib.hv_expert_ffn_down_ex(A, A, A, A, A, 4, 2048, 1408, 16, None) == INV
+    # decode glue: empty batches are no-ops; limits of the route kernel are enforced
+    def route(T=32, H=2048, E=60, k=4, ptr=A, flags=0):
+        return lib.hv_moe_route(ptr, A, T, H, E, k, A, A, A, A, A, A, A, A, flags, None)
+    assert route(T=0) == N.HV_OK
+    assert route(ptr=0) == INV
+    assert route(E=257) == INV
+    assert route(k=9) == INV
+    assert route(T=257) == INV
+    assert route(H=2047) == INV
+    assert route(flags=2) == INV
+    assert lib.hv_moe_combine(A, A, A, A, 0, 2048, 4, 1.0, 0, None) == N.HV_OK
+    assert lib.hv_moe_combine(A, A, A, A, 4, 2048, 9, 1.0, 0, None) == INV
+    assert lib.hv_moe_stage_plan(A, A, A, 1 << 32, 0, 60, A, A, A, None) == INV      # zero slot size
+    assert lib.hv_moe_stage_plan(A, A, A, 1 << 32, 4096, 0, A, A, A, None) == N.HV_OK
     # the Python layer raises the matching exception type
     with pytest.raises(N.HarvestNativeError) as ei:
         N.call("hv_batch_copy", 0, 0x1000, 0x1000, 2, 0, 0, None)
