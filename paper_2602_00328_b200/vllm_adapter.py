@@ -195,6 +195,17 @@ class HarvestPeerHandler(OffloadingHandler):
         [num_blocks, page_bytes] tensors (vLLM's CanonicalKVCaches.tensors,
         one page of each per block)."""
         self.sys, self.rt, self.pool = system, system.runtime, pool
+        self.engine, self.max_ctas = N.ENGINES[engine], max_ctas
+        self.stream = system.engine.stream
+        self._jobs: dict[int, tuple] = {}
+        self._done: list = []
+        self.bind(gpu_cache)
+
+    def bind(self, gpu_cache) -> None:
+        """(Re)bind the GPU KV tensors the handler moves pages of.  A serving
+        engine that re-initializes its KV cache (vLLM 0.22 can register the
+        cache more than once) keeps this handler registered and rebinds it."""
+        pool = self.pool
         if isinstance(gpu_cache, torch.Tensor):
             tensors = [gpu_cache[i] for i in range(gpu_cache.shape[0])]
         else:
@@ -215,11 +226,7 @@ class HarvestPeerHandler(OffloadingHandler):
         self.block_form = (pool.uniform and (len(d) == 0 or (d == d[0]).all() and d[0] > 0)
                            and (self.rows == np.uint64(pool.page)).all())
         self.layer_stride = int(d[0]) if len(d) else 0
-        self.engine, self.max_ctas = N.ENGINES[engine], max_ctas
         self.dev = tensors[0].device
-        self.stream = system.engine.stream
-        self._jobs: dict[int, tuple] = {}
-        self._done: list = []
 
     def _gpu_pages(self, block_ids) -> np.ndarray:
         b = np.asarray(block_ids, dtype=np.uint64)
@@ -243,6 +250,7 @@ class HarvestPeerHandler(OffloadingHandler):
         elif sm == "PEER" and dm == "GPU":                                 # load (reload)
             gpu_ids, peer_ids = dst.block_ids, src.block_ids
             if any(not self.pool.is_resident(b) for b in peer_ids):
+                _STATS["failed_loads"] += 1
                 self._done.append(TransferResult(job_id, False, 0, 0.0, ("PEER", "GPU")))
                 return True  # completes as failed: Lossy -> recompute
             r = self.pool.page_ptrs(peer_ids, for_store=False)
@@ -255,6 +263,10 @@ class HarvestPeerHandler(OffloadingHandler):
         if len(gpu_ids) and int(np.max(gpu_ids)) >= self.nblocks:
             return False
         peer_pages, handles = r
+        key = "store" if kind[0] == "GPU" else "load"
+        _STATS[key + "_jobs"] += 1
+        _STATS[key + "_blocks"] += len(gpu_ids)
+        _STATS[key + "_bytes"] += len(gpu_ids) * self.pool.block_bytes
         gpu_pages = self._gpu_pages(gpu_ids)
         nb = len(gpu_ids)
         nbytes = nb * self.pool.block_bytes
@@ -496,10 +508,18 @@ class HarvestOffloadingSpec(OffloadingSpec):
         self._handler = HarvestPeerHandler(self.system, tensors, self._pool)
 
     def get_handlers(self, kv_caches):
-        if self._handler is None:
-            tensors = [t.tensor for t in kv_caches.tensors]
-            page_sizes = [t.page_size_bytes for t in kv_caches.tensors]
-            self._build_worker(tensors, page_sizes)
+        tensors = [t.tensor for t in kv_caches.tensors]
+        page_sizes = [t.page_size_bytes for t in kv_caches.tensors]
+        if self._handler is not None:
+            # a second registration of the engine's KV cache (vLLM 0.22
+            # re-initializes it): the worker already holds this handler for
+            # both directions, so rebind it to the new tensors and register
+            # nothing twice (the worker asserts on a repeated transfer type)
+            if list(page_sizes) != list(self._pool.page_sizes):
+                raise ValueError("re-registered KV cache with a different page layout")
+            self._handler.bind(tensors)
+            return
+        self._build_worker(tensors, page_sizes)
         gpu_spec = _gpu_spec_type()
         yield gpu_spec, PeerBlocks, self._handler
         yield PeerBlocks, gpu_spec, self._handler
@@ -510,6 +530,17 @@ def _gpu_spec_type():
         from vllm.v1.kv_offload.base import GPULoadStoreSpec  # type: ignore
         return GPULoadStoreSpec
     return GPUBlocks
+
+
+_STATS = {"store_jobs": 0, "store_blocks": 0, "store_bytes": 0, "load_jobs": 0, "load_blocks": 0, "load_bytes": 0,
+          "failed_loads": 0}
+
+
+def handler_stats() -> dict:
+    """Jobs, blocks and bytes every HarvestPeerHandler of this process has
+    launched (stores GPU -> PEER, loads PEER -> GPU) and loads failed because
+    a block was revoked."""
+    return dict(_STATS)
 
 
 def register_with_vllm() -> bool:
