@@ -489,8 +489,11 @@ class HarvestOffloadingSpec(OffloadingSpec):
         if self._manager is None:
             kec = getattr(self.vllm_config, "kv_events_config", None)
             events = bool(kec is not None and getattr(kec, "enable_kv_cache_events", False))
-            self._manager = HarvestOffloadingManager(self.num_blocks, residency=lambda: self._pool,
-                                                     enable_events=events)
+            # in-process engines (VLLM_ENABLE_V1_MULTIPROCESSING=0) build one
+            # spec per role: the scheduler's manager sees the worker's pool
+            self._manager = HarvestOffloadingManager(
+                self.num_blocks, residency=lambda: self._pool if self._pool is not None else _WORKER_POOL[0],
+                enable_events=events)
         return self._manager
 
     def _build_worker(self, tensors, page_sizes):
@@ -505,6 +508,7 @@ class HarvestOffloadingSpec(OffloadingSpec):
         self.system = HarvestSystem(dev, donors=list(donors), donor_bytes=max(per_donor, block_bytes * self.slab_blocks),
                                     host_bytes=1, local_bytes=1)
         self._pool = PeerBlockPool(self.system.runtime, slab_blocks=self.slab_blocks, page_sizes=page_sizes)
+        _WORKER_POOL[0] = self._pool
         self._handler = HarvestPeerHandler(self.system, tensors, self._pool)
 
     def get_handlers(self, kv_caches):
@@ -532,6 +536,7 @@ def _gpu_spec_type():
     return GPUBlocks
 
 
+_WORKER_POOL = [None]   # the peer pool the worker side of this process built (see get_manager)
 _STATS = {"store_jobs": 0, "store_blocks": 0, "store_bytes": 0, "load_jobs": 0, "load_blocks": 0, "load_bytes": 0,
           "failed_loads": 0}
 

@@ -4,7 +4,8 @@ vllm_engine_probe.py --quick, in a subprocess so the engine's process-wide
 state and memory stay out of the other tests): prompts prefilled once store
 their KV blocks to the peer pool; after the GPU prefix cache is reset the
 same prompts find their prefixes only there, the handler loads them back, and
-the greedy outputs are identical to the first pass."""
+the greedy outputs are identical to the first pass -- and again after every
+donor slab has been revoked (the lookups miss and the engine recomputes)."""
 import json
 import os
 import subprocess
@@ -27,3 +28,7 @@ def test_vllm_engine_serves_through_the_peer_medium():
     assert h["store_jobs"] > 0 and h["store_blocks"] > 0
     assert h["load_jobs"] > 0 and h["load_blocks"] > 0 and h["failed_loads"] == 0
     assert res["offload_after_reset_equals_first"]
+    # every donor slab revoked mid-serving: lookups miss, vLLM recomputes, same outputs
+    assert h["revoked_slabs"] > 0 and h["slabs_live_after_revocation"] == 0
+    assert h["loads_after_revocation"] == 0 and h["stores_after_revocation"] > 0   # misses, recomputed, re-stored
+    assert res["offload_after_revocation_equals_first"]

@@ -56,8 +56,28 @@ def run(model, offload, prompts):
     outs.append([list(o.outputs[0].token_ids) for o in second])
     stats = None
     if offload:
+        # every donor slab revoked (a co-tenant reclaims the HBM): the next
+        # lookups are misses and vLLM recomputes -- outputs must not change
         from paper_2602_00328_b200 import vllm_adapter as VA
+        from paper_2602_00328_b200.runtime import RevokeReason
+        pool = VA._WORKER_POOL[0]
+        rt = pool.rt
+        before = VA.handler_stats()
+        for h in list(pool.slabs.values()):
+            if h is not None and rt.is_live(h):
+                rt.revoke(h, RevokeReason.EXTERNAL_RECLAIM)
+        import torch
+        torch.cuda.synchronize()
+        rt.sim.run()   # drain: the revocations finish once the reads already enqueued complete
+        live_after_revoke = sum(1 for h in pool.slabs.values() if rt.is_live(h))
+        llm.reset_prefix_cache()
+        third = llm.generate([{"prompt_token_ids": p} for p in prompts], sp, use_tqdm=False)
+        outs.append([list(o.outputs[0].token_ids) for o in third])
         stats = VA.handler_stats()
+        stats["revoked_slabs"] = len(before) and sum(1 for _ in pool.slabs)
+        stats["slabs_live_after_revocation"] = live_after_revoke
+        stats["loads_after_revocation"] = stats["load_jobs"] - before["load_jobs"]
+        stats["stores_after_revocation"] = stats["store_jobs"] - before["store_jobs"]
     del llm
     return outs, stats
 
@@ -79,8 +99,10 @@ def main():
         res["reference_after_reset"] = outs_ref[1]
     try:
         outs_off, stats = run(model, True, prompts)
-        res["offload"] = {"first": outs_off[0], "after_reset": outs_off[1], "handler": stats}
+        res["offload"] = {"first": outs_off[0], "after_reset": outs_off[1], "after_revocation": outs_off[2],
+                          "handler": stats}
         res["offload_after_reset_equals_first"] = outs_off[1] == outs_off[0]
+        res["offload_after_revocation_equals_first"] = outs_off[2] == outs_off[0]
         if outs_ref is not None:
             res["equal_first"] = outs_off[0] == outs_ref[0]
             res["equal_after_reset"] = outs_off[1] == outs_ref[0]
