@@ -316,6 +316,8 @@ class HarvestPeerHandler(OffloadingHandler):
     def shutdown(self) -> None:
         self.sys.engine.synchronize()
         self.sys.loop.poll()
+        if _WORKER_POOL[0] is self.pool:   # no later manager of this process reads a finished engine's pool
+            _WORKER_POOL[0] = None
 
 
 @dataclass
